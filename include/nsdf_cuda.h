@@ -1,0 +1,217 @@
+/*
+ * nsdf_cuda.h — the C ABI of libnsdf_cuda.so, the B200 (sm_100a) engine behind the
+ * reference renderer's C++ API.
+ *
+ * This is the drop-in boundary: every entry point here replaces one C++ entry point
+ * of the reference library (paths relative to /root/reference/proj):
+ *
+ *   nsdf_cuda_upload_mlp      NeuralField ctor, f64 master -> f32 copy   src/fields/field.cpp:149-154
+ *                             NeuralTimeField ctor                      src/fields/field.cpp:256-261
+ *   nsdf_cuda_upload_analytic SphereField / TorusField / BoxField       include/nsdf/fields/field.hpp:42-80
+ *   nsdf_cuda_eval            mlp::forward_batch<float>                 src/mlp/mlp.cpp:171-177 (mlp.cpp:267-273)
+ *                             Field::eval_batch(Matrix<float>)          src/fields/field.cpp:167-169, 303-305
+ *   nsdf_cuda_grad            mlp::gradient_batch<float> /              src/mlp/mlp.cpp:275-295
+ *                             spatial_gradient_batch<float>
+ *                             Field::grad_batch(Matrix<float>)          src/fields/field.cpp:173-175, 309-311
+ *   nsdf_cuda_eval_grad       mlp::forward_and_gradient_batch<float>    src/mlp/mlp.cpp:297-306
+ *   nsdf_cuda_generate_rays   tracer::generate_rays                     src/tracer/camera.cpp:20-43
+ *   nsdf_cuda_trace_rays      tracer::multiscale_sphere_trace (batched) src/tracer/trace.cpp:86-132, 162-169
+ *                             tracer::sphere_trace (m = 1, offset)      src/tracer/trace.cpp:136-160
+ *   nsdf_cuda_trace_image     tracer::trace_image                       src/tracer/trace.cpp:171-186
+ *   nsdf_cuda_normal_map      shading::neural_normal_map                src/shading/shade.cpp:8-42
+ *   nsdf_cuda_shade           shading::shade                            src/shading/shade.cpp:44-93
+ *   nsdf_cuda_render          shading::render                           src/shading/render.cpp:12-82
+ *   nsdf_cuda_render_device   shading::render, device-resident framebuffer + tile sharding
+ *                             (the multi-GPU frame/tile scheduler's per-rank call)
+ *
+ * Conventions
+ *   - Plain C types only; no exceptions cross this boundary.  Every function returns an
+ *     nsdf_status; on failure nsdf_cuda_last_error() (thread-local) holds the message and
+ *     the host shim rethrows nsdf::Error with the matching ErrorKind (core.hpp:12-18).
+ *   - Point batches keep the reference layout: `rows x k` row-major float, one point per
+ *     column (matrix.hpp:32-33).  rows is the network input dim (3 or 4); a 3-row batch
+ *     fed to a 4-input net gets the constant `time` row appended (field.cpp:213-220).
+ *   - Functions without the _device suffix take HOST pointers and are synchronous.
+ *     _device variants take device pointers and run asynchronously on the context stream.
+ *   - A context is bound to one device and one stream; calls on one context are
+ *     serialised by an internal mutex, so concurrent callers are safe.
+ *   - No CPU fallback: if the device or the kernels are unavailable, calls fail loudly
+ *     with NSDF_ERR_DEVICE.
+ */
+#ifndef NSDF_CUDA_H_
+#define NSDF_CUDA_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NSDF_CUDA_ABI_VERSION 1
+#define NSDF_MAX_LEVELS 8 /* tracer::kMaxLevels, trace.hpp:32 */
+#define NSDF_MAX_LIGHTS 8
+
+typedef enum {
+  NSDF_OK = 0,
+  NSDF_ERR_CONTRACT = 1,   /* ErrorKind::contract   — shape / precondition violation   */
+  NSDF_ERR_CONFIG = 2,     /* ErrorKind::config     — bad configuration value          */
+  NSDF_ERR_VALIDATION = 3, /* ErrorKind::validation — inconsistent data                */
+  NSDF_ERR_PARSE = 4,      /* ErrorKind::parse                                         */
+  NSDF_ERR_DIVERGENCE = 5, /* ErrorKind::divergence                                    */
+  NSDF_ERR_DEVICE = 6      /* CUDA failure / no device; the host shim maps to validation */
+} nsdf_status;
+
+/* Arithmetic mode of the MLP evaluator.
+ *   FP32_ORACLE: FFMA kernels that restate the reference AVX2 arithmetic operation for
+ *                operation (k-sequential fma chains from the bias, Cephes sincos with
+ *                separately rounded mul/add) — bit-exact with the reference CPU path.
+ *   FP16_FAST:   tcgen05 tensor-core tiles, fp16 operands / fp32 TMEM accumulators, fp32
+ *                first layer, range-reduced MUFU sine; parity within the BASELINE
+ *                tolerances (mask >= 99.9%, |dt| <= 1e-3, normals <= 0.5 deg).        */
+typedef enum { NSDF_MODE_FP32_ORACLE = 0, NSDF_MODE_FP16_FAST = 1 } nsdf_mode;
+
+typedef enum { NSDF_ACT_SINE = 0, NSDF_ACT_IDENTITY = 1 } nsdf_activation; /* ops.hpp Activation */
+typedef enum { NSDF_FIELD_SPHERE = 1, NSDF_FIELD_TORUS = 2, NSDF_FIELD_BOX = 3 } nsdf_analytic_kind;
+typedef enum { NSDF_NORMALS_OWN = 0, NSDF_NORMALS_MAPPED = 1 } nsdf_normal_source; /* shading.hpp:113 */
+
+typedef struct nsdf_ctx nsdf_ctx;
+typedef int32_t nsdf_field; /* handle > 0 */
+
+/* tracer::Camera (trace.hpp:13-22) */
+typedef struct {
+  double position[3];
+  double look_at[3];
+  double up[3];
+  double vertical_fov_deg;
+  int32_t width;
+  int32_t height;
+} nsdf_camera;
+
+/* tracer::TraceConfig (trace.hpp:49-55); n_levels must equal the sequence size */
+typedef struct {
+  int32_t n_levels;
+  int32_t budgets[NSDF_MAX_LEVELS];
+  float eps_stop;
+  float t_max;
+} nsdf_trace_config;
+
+/* tracer::HitRecord (trace.hpp:34-47) */
+typedef struct {
+  int32_t hit;
+  float point[3];
+  float t;
+  int32_t level_reached;
+  uint16_t iterations_used[NSDF_MAX_LEVELS];
+  float final_distance;
+} nsdf_hit_record;
+
+/* shading::ShadeConfig / Material / DirectionalLight (shading.hpp:90-107) */
+typedef struct {
+  float albedo[3];
+  float ambient;
+  float diffuse;
+  float specular;
+  float shininess;
+  int32_t n_lights;
+  float light_direction[NSDF_MAX_LIGHTS][3];
+  float light_intensity[NSDF_MAX_LIGHTS];
+  float background[3];
+} nsdf_shade_config;
+
+/* One member of a nested sequence, coarse to fine (nesting.hpp:53-61).  `time` is the
+ * slice time for 4-input nets (AnimatedSequence::slice, nesting.cpp:71-78), ignored
+ * otherwise.  `delta` is the nesting threshold deltas[j]. */
+typedef struct {
+  nsdf_field field;
+  float time;
+  double delta;
+} nsdf_level;
+
+/* Per-frame accounting, filled by render/trace when non-NULL (the FLOP source of
+ * iterations_used summed per level, hits, normal evaluations). */
+typedef struct {
+  uint64_t evals[NSDF_MAX_LEVELS]; /* MLP forward evaluations per level           */
+  uint64_t hits;                   /* rays that converged at the final level       */
+  uint64_t normal_evals;           /* fwd+gradient evaluations for normals         */
+  uint64_t fallback_evals;         /* own-field normals computed for the fallback  */
+  uint64_t kernel_launches;        /* engine kernels launched for the frame        */
+} nsdf_frame_stats;
+
+/* ---- context ---------------------------------------------------------------------- */
+int nsdf_cuda_abi_version(void);
+const char* nsdf_cuda_last_error(void);
+int nsdf_cuda_create(int device, nsdf_ctx** out);
+int nsdf_cuda_destroy(nsdf_ctx* ctx);
+int nsdf_cuda_set_mode(nsdf_ctx* ctx, int mode);
+int nsdf_cuda_get_mode(nsdf_ctx* ctx, int* mode);
+/* Bind the context to an existing cudaStream_t (NULL restores the context's own). */
+int nsdf_cuda_set_stream(nsdf_ctx* ctx, void* stream);
+int nsdf_cuda_synchronize(nsdf_ctx* ctx);
+
+/* ---- fields -------------------------------------------------------------------------
+ * Packed weights: for each layer l, rows[l]*cols[l] row-major weights (out x in) then
+ * rows[l] biases, as doubles (the f64 master of NeuralField).  The engine keeps the f32
+ * cast (field.cpp:150) for the oracle mode and fp16 tiles for the fast mode.
+ * Validation follows MlpParams::validate (mlp.cpp:13-39). */
+int nsdf_cuda_upload_mlp(nsdf_ctx* ctx, int n_layers, const int32_t* rows, const int32_t* cols,
+                         const double* packed, int activation, double omega0, int input_dim,
+                         nsdf_field* out);
+/* sphere: {cx, cy, cz, r}; torus: {R, r}; box: {hx, hy, hz} (field.hpp:42-80) */
+int nsdf_cuda_upload_analytic(nsdf_ctx* ctx, int kind, const double* params, int n_params,
+                              nsdf_field* out);
+int nsdf_cuda_release(nsdf_ctx* ctx, nsdf_field field);
+int nsdf_cuda_field_info(nsdf_ctx* ctx, nsdf_field field, int* input_dim, int* n_layers,
+                         int* width);
+
+/* ---- batch evaluation (Field::eval_batch / grad_batch, mlp::*_batch) ------------------
+ * points: rows x k; out: 1 x k; grad: 3 x k.  Either output may be NULL in eval_grad. */
+int nsdf_cuda_eval(nsdf_ctx* ctx, nsdf_field field, const float* points, int rows, int k,
+                   float time, float* out);
+int nsdf_cuda_grad(nsdf_ctx* ctx, nsdf_field field, const float* points, int rows, int k,
+                   float time, float* grad);
+int nsdf_cuda_eval_grad(nsdf_ctx* ctx, nsdf_field field, const float* points, int rows, int k,
+                        float time, float* out, float* grad);
+int nsdf_cuda_eval_grad_device(nsdf_ctx* ctx, nsdf_field field, const float* d_points, int rows,
+                               int k, float time, float* d_out, float* d_grad);
+
+/* ---- tracing --------------------------------------------------------------------------
+ * rays: n x 6 floats {ox, oy, oz, dx, dy, dz} (tracer::Ray, trace.hpp:24-27). */
+int nsdf_cuda_generate_rays(nsdf_ctx* ctx, const nsdf_camera* camera, float* rays);
+int nsdf_cuda_trace_rays(nsdf_ctx* ctx, const nsdf_level* levels, int m,
+                         const nsdf_trace_config* config, const float* rays, int n,
+                         nsdf_hit_record* out);
+int nsdf_cuda_trace_image(nsdf_ctx* ctx, const nsdf_level* levels, int m,
+                          const nsdf_camera* camera, const nsdf_trace_config* config,
+                          nsdf_hit_record* out, nsdf_frame_stats* stats);
+
+/* ---- normals and shading -------------------------------------------------------------- */
+int nsdf_cuda_normal_map(nsdf_ctx* ctx, nsdf_field fine, float time, const float* points, int k,
+                         double delta, const float* fallback_normals, float* normals,
+                         uint64_t* outside_count, uint64_t* fallback_count);
+int nsdf_cuda_shade(nsdf_ctx* ctx, const float* points, const float* normals, int k,
+                    const nsdf_shade_config* config, const nsdf_camera* camera, float* rgb);
+
+/* ---- whole frame ------------------------------------------------------------------------
+ * rgb: 3*W*H, depth: W*H, mask: W*H (ImageBuffer, shading.hpp:22-34).  fine_index < 0
+ * selects the finest member (RenderConfig::mapped_fine_index). */
+int nsdf_cuda_render(nsdf_ctx* ctx, const nsdf_level* levels, int m, const nsdf_camera* camera,
+                     const nsdf_trace_config* trace, const nsdf_shade_config* shade,
+                     int normal_source, int fine_index, float* rgb, float* depth, uint8_t* mask,
+                     nsdf_frame_stats* stats);
+/* Device framebuffer variant used by the frame/tile scheduler: renders the pixels of the
+ * image tiles t with t % tile_world == tile_rank (tile_size x tile_size tiles, row-major
+ * tile order; tile_world = 1 renders everything) into full-frame device buffers.  Pixels
+ * of other tiles are left untouched.  Asynchronous on the context stream; `stats` (host,
+ * may be NULL) forces a synchronize. */
+int nsdf_cuda_render_device(nsdf_ctx* ctx, const nsdf_level* levels, int m,
+                            const nsdf_camera* camera, const nsdf_trace_config* trace,
+                            const nsdf_shade_config* shade, int normal_source, int fine_index,
+                            int tile_size, int tile_rank, int tile_world, float* d_rgb,
+                            float* d_depth, uint8_t* d_mask, nsdf_frame_stats* stats);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* NSDF_CUDA_H_ */

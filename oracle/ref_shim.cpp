@@ -1,0 +1,372 @@
+// TEST INFRASTRUCTURE ONLY — never linked into the product.
+//
+// A C shim over the UNMODIFIED reference library (compiled from /root/reference/proj/src by
+// oracle/Makefile) so the parity suite, the fixture generator and bench.py's reference arm
+// can drive the reference CPU path through ctypes.  Every call goes through the
+// reference's own public API (include/nsdf/*.hpp); nothing here re-implements arithmetic.
+// PODs are the ones of our C ABI (include/nsdf_cuda.h) so results compare field by field.
+
+#include <chrono>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "nsdf/core.hpp"
+#include "nsdf/fields/field.hpp"
+#include "nsdf/fields/nesting.hpp"
+#include "nsdf/mlp/mlp.hpp"
+#include "nsdf/shading/shading.hpp"
+#include "nsdf/tensor/kernels.hpp"
+#include "nsdf/tracer/trace.hpp"
+#include "nsdf_cuda.h"
+
+using namespace nsdf;
+
+namespace {
+
+thread_local std::string g_error;
+
+int fail(const std::exception& e) {
+  g_error = e.what();
+  if (auto* ne = dynamic_cast<const Error*>(&e)) return 1 + int(ne->kind());
+  return 3;
+}
+
+#define SHIM_TRY try {
+#define SHIM_CATCH                    \
+  }                                   \
+  catch (const std::exception& e) {   \
+    return fail(e);                   \
+  }                                   \
+  return 0;
+
+mlp::MlpParams<double> unpack(int n_layers, const int32_t* rows, const int32_t* cols,
+                              const double* packed, int activation, double omega0,
+                              int input_dim) {
+  mlp::MlpParams<double> p;
+  p.input_dim = input_dim;
+  p.activation = activation == NSDF_ACT_SINE ? tensor::ActivationSpec::sine(omega0)
+                                             : tensor::ActivationSpec::identity();
+  size_t off = 0;
+  for (int l = 0; l < n_layers; ++l) {
+    std::vector<double> w(packed + off, packed + off + size_t(rows[l]) * cols[l]);
+    off += size_t(rows[l]) * cols[l];
+    std::vector<double> b(packed + off, packed + off + rows[l]);
+    off += rows[l];
+    p.layers.push_back({tensor::Matrix<double>(rows[l], cols[l], std::move(w)),
+                        tensor::Matrix<double>(rows[l], 1, std::move(b))});
+  }
+  return p;
+}
+
+tracer::Camera to_camera(const nsdf_camera* c) {
+  tracer::Camera cam;
+  cam.position = {c->position[0], c->position[1], c->position[2]};
+  cam.look_at = {c->look_at[0], c->look_at[1], c->look_at[2]};
+  cam.up = {c->up[0], c->up[1], c->up[2]};
+  cam.vertical_fov_deg = c->vertical_fov_deg;
+  cam.width = c->width;
+  cam.height = c->height;
+  return cam;
+}
+
+tracer::TraceConfig to_trace(const nsdf_trace_config* t) {
+  tracer::TraceConfig cfg;
+  cfg.budgets.assign(t->budgets, t->budgets + t->n_levels);
+  cfg.eps_stop = t->eps_stop;
+  cfg.t_max = t->t_max;
+  return cfg;
+}
+
+shading::ShadeConfig to_shade(const nsdf_shade_config* s) {
+  shading::ShadeConfig cfg;
+  cfg.material.albedo = {s->albedo[0], s->albedo[1], s->albedo[2]};
+  cfg.material.ambient = s->ambient;
+  cfg.material.diffuse = s->diffuse;
+  cfg.material.specular = s->specular;
+  cfg.material.shininess = s->shininess;
+  cfg.lights.clear();
+  for (int i = 0; i < s->n_lights; ++i)
+    cfg.lights.push_back({{s->light_direction[i][0], s->light_direction[i][1],
+                           s->light_direction[i][2]},
+                          s->light_intensity[i]});
+  cfg.background = {s->background[0], s->background[1], s->background[2]};
+  return cfg;
+}
+
+void to_pod(const tracer::HitRecord& r, nsdf_hit_record* o) {
+  o->hit = r.hit ? 1 : 0;
+  o->point[0] = r.point.x;
+  o->point[1] = r.point.y;
+  o->point[2] = r.point.z;
+  o->t = r.t;
+  o->level_reached = r.level_reached;
+  for (int i = 0; i < NSDF_MAX_LEVELS; ++i) o->iterations_used[i] = r.iterations_used[i];
+  o->final_distance = r.final_distance;
+}
+
+fields::NestedSequence load_sequence(const char* manifest, double time) {
+  fields::SequenceManifest m = fields::load_manifest(manifest);
+  return m.time_dependent ? m.animated.slice(time) : m.sequence;
+}
+
+tensor::Matrix<float> points_matrix(const float* pts, int rows, int k) {
+  return tensor::Matrix<float>(rows, k, std::vector<float>(pts, pts + size_t(rows) * k));
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* nsdf_ref_last_error(void) { return g_error.c_str(); }
+
+int nsdf_ref_worker_threads(void) { return worker_thread_count(); }
+
+int nsdf_ref_set_backend(const char* name) {
+  SHIM_TRY
+  std::string n(name);
+  tensor::set_backend(n == "scalar" ? tensor::Backend::scalar
+                                    : n == "neon" ? tensor::Backend::neon : tensor::Backend::avx2);
+  SHIM_CATCH
+}
+
+const char* nsdf_ref_backend(void) { return tensor::backend_name(tensor::active_backend()); }
+
+// mlp::random_init (mlp.cpp:63-88) with Rng(seed); writes the packed layout.
+int nsdf_ref_random_init(int width, int hidden, int input_dim, double omega0, uint64_t seed,
+                         double* packed, int32_t* rows, int32_t* cols) {
+  SHIM_TRY
+  Rng rng(seed);
+  mlp::Architecture arch{width, hidden, input_dim};
+  auto p = mlp::random_init(arch, omega0, rng);
+  size_t off = 0;
+  for (size_t l = 0; l < p.layers.size(); ++l) {
+    const auto& L = p.layers[l];
+    rows[l] = L.weights.rows();
+    cols[l] = L.weights.cols();
+    std::memcpy(packed + off, L.weights.data(), L.weights.size() * sizeof(double));
+    off += L.weights.size();
+    std::memcpy(packed + off, L.bias.data(), L.bias.size() * sizeof(double));
+    off += L.bias.size();
+  }
+  SHIM_CATCH
+}
+
+// mode 0: forward_batch, 1: gradient_batch (spatial for 4-input nets), 2: fused.
+// f32 path exactly as NeuralField (params cast once, field.cpp:150).
+int nsdf_ref_mlp(int mode, int n_layers, const int32_t* rows, const int32_t* cols,
+                 const double* packed, int activation, double omega0, int input_dim,
+                 const float* pts, int k, float* dist, float* grad) {
+  SHIM_TRY
+  auto p64 = unpack(n_layers, rows, cols, packed, activation, omega0, input_dim);
+  auto p = p64.cast<float>();
+  auto P = points_matrix(pts, input_dim, k);
+  if (mode == 0) {
+    auto d = mlp::forward_batch(p, P);
+    std::memcpy(dist, d.data(), sizeof(float) * k);
+  } else if (mode == 1) {
+    auto g = input_dim == 4 ? mlp::spatial_gradient_batch(p, P) : mlp::gradient_batch(p, P);
+    std::memcpy(grad, g.data(), sizeof(float) * 3 * k);
+  } else {
+    auto [d, g] = mlp::forward_and_gradient_batch(p, P);
+    std::memcpy(dist, d.data(), sizeof(float) * k);
+    std::memcpy(grad, g.data(), sizeof(float) * 3 * k);
+  }
+  SHIM_CATCH
+}
+
+int nsdf_ref_mlp_f64(int mode, int n_layers, const int32_t* rows, const int32_t* cols,
+                     const double* packed, int activation, double omega0, int input_dim,
+                     const double* pts, int k, double* dist, double* grad) {
+  SHIM_TRY
+  auto p = unpack(n_layers, rows, cols, packed, activation, omega0, input_dim);
+  tensor::Matrix<double> P(input_dim, k, std::vector<double>(pts, pts + size_t(input_dim) * k));
+  if (mode == 0 || mode == 2) {
+    auto d = mlp::forward_batch(p, P);
+    std::memcpy(dist, d.data(), sizeof(double) * k);
+  }
+  if (mode == 1 || mode == 2) {
+    auto g = input_dim == 4 ? mlp::spatial_gradient_batch(p, P) : mlp::gradient_batch(p, P);
+    std::memcpy(grad, g.data(), sizeof(double) * 3 * k);
+  }
+  SHIM_CATCH
+}
+
+int nsdf_ref_save_params(int n_layers, const int32_t* rows, const int32_t* cols,
+                         const double* packed, int activation, double omega0, int input_dim,
+                         const char* path) {
+  SHIM_TRY
+  mlp::save_params(unpack(n_layers, rows, cols, packed, activation, omega0, input_dim), path);
+  SHIM_CATCH
+}
+
+int nsdf_ref_generate_rays(const nsdf_camera* camera, float* rays) {
+  SHIM_TRY
+  auto rs = tracer::generate_rays(to_camera(camera));
+  for (size_t i = 0; i < rs.size(); ++i) {
+    rays[6 * i + 0] = rs[i].origin.x;
+    rays[6 * i + 1] = rs[i].origin.y;
+    rays[6 * i + 2] = rs[i].origin.z;
+    rays[6 * i + 3] = rs[i].direction.x;
+    rays[6 * i + 4] = rs[i].direction.y;
+    rays[6 * i + 5] = rs[i].direction.z;
+  }
+  SHIM_CATCH
+}
+
+// Field batch evaluation of one member of a manifest (eval_batch / grad_batch, f32).
+int nsdf_ref_field_eval(const char* manifest, double time, int index, const float* pts, int k,
+                        float* dist, float* grad) {
+  SHIM_TRY
+  auto seq = load_sequence(manifest, time);
+  auto P = points_matrix(pts, 3, k);
+  if (dist) {
+    auto d = seq.field(index).eval_batch(P);
+    std::memcpy(dist, d.data(), sizeof(float) * k);
+  }
+  if (grad) {
+    auto g = seq.field(index).grad_batch(P);
+    std::memcpy(grad, g.data(), sizeof(float) * 3 * k);
+  }
+  SHIM_CATCH
+}
+
+int nsdf_ref_trace_image(const char* manifest, double time, const nsdf_camera* camera,
+                         const nsdf_trace_config* config, nsdf_hit_record* out) {
+  SHIM_TRY
+  auto seq = load_sequence(manifest, time);
+  auto recs = tracer::trace_image(seq, to_camera(camera), to_trace(config));
+  for (size_t i = 0; i < recs.size(); ++i) to_pod(recs[i], out + i);
+  SHIM_CATCH
+}
+
+// Per-ray multiscale_sphere_trace (trace.cpp:162-169).
+int nsdf_ref_trace_rays(const char* manifest, double time, const nsdf_trace_config* config,
+                        const float* rays, int n, nsdf_hit_record* out) {
+  SHIM_TRY
+  auto seq = load_sequence(manifest, time);
+  auto cfg = to_trace(config);
+  for (int i = 0; i < n; ++i) {
+    tracer::Ray r{{rays[6 * i], rays[6 * i + 1], rays[6 * i + 2]},
+                  {rays[6 * i + 3], rays[6 * i + 4], rays[6 * i + 5]}};
+    to_pod(tracer::multiscale_sphere_trace(seq, r, cfg), out + i);
+  }
+  SHIM_CATCH
+}
+
+// Classic sphere_trace of one member (trace.cpp:136-160).
+int nsdf_ref_sphere_trace(const char* manifest, double time, int index, float delta,
+                          float eps_stop, int max_iters, float t_max, const float* rays, int n,
+                          nsdf_hit_record* out) {
+  SHIM_TRY
+  auto seq = load_sequence(manifest, time);
+  for (int i = 0; i < n; ++i) {
+    tracer::Ray r{{rays[6 * i], rays[6 * i + 1], rays[6 * i + 2]},
+                  {rays[6 * i + 3], rays[6 * i + 4], rays[6 * i + 5]}};
+    to_pod(tracer::sphere_trace(seq.field(index), r, delta, eps_stop, max_iters, t_max), out + i);
+  }
+  SHIM_CATCH
+}
+
+int nsdf_ref_normal_map(const char* manifest, double time, int index, const float* pts, int k,
+                        double delta, const float* fallback, float* normals,
+                        uint64_t* outside, uint64_t* fallbacks) {
+  SHIM_TRY
+  auto seq = load_sequence(manifest, time);
+  auto P = points_matrix(pts, 3, k);
+  std::unique_ptr<tensor::Matrix<float>> fb;
+  if (fallback) fb = std::make_unique<tensor::Matrix<float>>(points_matrix(fallback, 3, k));
+  auto r = shading::neural_normal_map(seq.field(index), P, delta, fb.get());
+  std::memcpy(normals, r.normals.data(), sizeof(float) * 3 * k);
+  *outside = r.outside_count;
+  *fallbacks = r.fallback_count;
+  SHIM_CATCH
+}
+
+int nsdf_ref_shade(const float* pts, const float* normals, int k, const nsdf_shade_config* shade,
+                   const nsdf_camera* camera, float* rgb) {
+  SHIM_TRY
+  auto r = shading::shade(points_matrix(pts, 3, k), points_matrix(normals, 3, k),
+                          to_shade(shade), to_camera(camera));
+  std::memcpy(rgb, r.data(), sizeof(float) * 3 * k);
+  SHIM_CATCH
+}
+
+// shading::render of a manifest (sliced at `time` when time-dependent), timed with
+// steady_clock like `nsdf bench` (nsdf_main.cpp:466-470); `seconds` gets the wall time
+// of the render call alone (manifest loading excluded).
+int nsdf_ref_render(const char* manifest, double time, const nsdf_camera* camera,
+                    const nsdf_trace_config* trace, const nsdf_shade_config* shade,
+                    int normal_source, int fine_index, float* rgb, float* depth, uint8_t* mask,
+                    double* seconds) {
+  SHIM_TRY
+  auto seq = load_sequence(manifest, time);
+  shading::RenderConfig cfg;
+  cfg.trace = to_trace(trace);
+  cfg.shade = to_shade(shade);
+  cfg.normal_source =
+      normal_source == NSDF_NORMALS_MAPPED ? shading::NormalSource::mapped : shading::NormalSource::own;
+  cfg.mapped_fine_index = fine_index;
+  auto t0 = std::chrono::steady_clock::now();
+  auto img = shading::render(seq, to_camera(camera), cfg);
+  auto t1 = std::chrono::steady_clock::now();
+  if (seconds) *seconds = std::chrono::duration<double>(t1 - t0).count();
+  std::memcpy(rgb, img.rgb.data(), sizeof(float) * img.rgb.size());
+  std::memcpy(depth, img.depth.data(), sizeof(float) * img.depth.size());
+  std::memcpy(mask, img.mask.data(), img.mask.size());
+  SHIM_CATCH
+}
+
+// Fixture certification (fit.cpp:262-298 minus the fitting): eps_i = estimate_sup_diff
+// of each weight file against the analytic reference shape, Prop-2 thresholds, empirical
+// verify_nesting, save_manifest.  Returns eps/deltas and the violation count.
+int nsdf_ref_certify(const char* const* weight_paths, const char* const* labels, int m,
+                     const char* analytic_spec, uint64_t n_uniform, uint64_t n_surface,
+                     double margin, uint64_t sup_seed, uint64_t verify_samples,
+                     const char* out_manifest, double* eps_out, double* deltas_out,
+                     uint64_t* violations) {
+  SHIM_TRY
+  auto oracle = fields::make_analytic_field(fields::parse_field_spec(analytic_spec));
+  fields::NestedSequence seq;
+  std::vector<double> eps;
+  for (int i = 0; i < m; ++i) {
+    auto params = mlp::load_params(weight_paths[i]);
+    size_t count = params.parameter_count();
+    auto field = std::make_shared<fields::NeuralField>(std::move(params));
+    field->set_domain(oracle->domain());
+    fields::SupSamplerConfig sup;
+    sup.n_uniform = n_uniform;
+    sup.n_surface = n_surface;
+    sup.margin = margin;
+    sup.seed = sup_seed + 31 * i;
+    eps.push_back(fields::estimate_sup_diff(*field, *oracle, sup).eps);
+    fields::FieldSource src;
+    src.kind = fields::FieldSource::Kind::weights;
+    std::string wp(weight_paths[i]);
+    src.weights_path = wp.substr(wp.find_last_of('/') + 1);
+    seq.entries.push_back({field, src, labels[i], count});
+  }
+  seq.deltas = m == 1 ? std::vector<double>{eps[0] + margin} : fields::thresholds_prop2(eps);
+  seq.provenance.proposition = m == 1 ? 0 : 2;
+  seq.provenance.eps = eps;
+  seq.provenance.margin = margin;
+  seq.provenance.sampler_seed = sup_seed;
+  seq.provenance.n_uniform = n_uniform;
+  seq.provenance.n_surface = n_surface;
+  fields::VerifyConfig vc;
+  vc.samples = verify_samples;
+  auto report = fields::verify_nesting(seq, vc);
+  seq.provenance.verify_samples = verify_samples;
+  seq.provenance.verify_violations = report.violation_count;
+  if (!report.ok()) seq.provenance.note = "empirical nesting violations recorded";
+  fields::save_manifest(seq, out_manifest);
+  for (int i = 0; i < m; ++i) {
+    eps_out[i] = eps[i];
+    deltas_out[i] = seq.deltas[i];
+  }
+  *violations = report.violation_count;
+  SHIM_CATCH
+}
+
+}  // extern "C"

@@ -1,0 +1,101 @@
+"""Builds the in-tree native libraries (no JIT cache: the .so files travel with the repo).
+
+  libnsdf_cuda.so   CUDA engine + C ABI (include/nsdf_cuda.h), sm_100a only.
+  libnsdf_b200.so   C++ drop-in host library (include/nsdf/*.hpp) over the C ABI.
+
+Per-file flags: engine.cu (trace loop, rays, shading, FFMA oracle tiles) is compiled with
+-fmad=false so no multiply-add can be contracted behind the explicit _rn intrinsics;
+mlp_tc.cu (tcgen05 fast path) keeps contraction on.
+"""
+from __future__ import annotations
+
+import os
+import shutil
+import subprocess
+import sys
+from concurrent.futures import ThreadPoolExecutor
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(PKG)
+CSRC = os.path.join(PKG, "csrc")
+HOST = os.path.join(PKG, "host")
+OBJ = os.path.join(PKG, "_obj")
+INC = os.path.join(ROOT, "include")
+NVCC = os.environ.get("NVCC", shutil.which("nvcc") or "/usr/local/cuda/bin/nvcc")
+ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+JSON_DIR = "/opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty/nlohmann"
+
+CUDA_SOURCES = {
+    "engine.cu": ["-fmad=false"],
+    "capi.cu": ["-fmad=false"],
+    "mlp_tc.cu": [],
+}
+
+
+def _run(cmd):
+    r = subprocess.run(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)
+    if r.returncode != 0:
+        sys.stderr.write(" ".join(cmd) + "\n" + r.stdout)
+        raise RuntimeError(f"build failed: {os.path.basename(cmd[-1])}")
+    return r.stdout
+
+
+def _stale(target, deps):
+    if not os.path.exists(target):
+        return True
+    t = os.path.getmtime(target)
+    return any(os.path.getmtime(d) > t for d in deps)
+
+
+def _headers(d):
+    return [os.path.join(d, f) for f in os.listdir(d) if f.endswith((".cuh", ".h", ".hpp"))]
+
+
+def build_cuda(force=False, verbose=False):
+    os.makedirs(OBJ, exist_ok=True)
+    deps_common = _headers(CSRC) + [os.path.join(INC, "nsdf_cuda.h")]
+    jobs = []
+    objs = []
+    for src, extra in CUDA_SOURCES.items():
+        s = os.path.join(CSRC, src)
+        o = os.path.join(OBJ, src + ".o")
+        objs.append(o)
+        if force or _stale(o, [s] + deps_common):
+            cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-ffp-contract=off",
+                   "-Xptxas", "-v" if verbose else "-O3", "-I", INC, "-I", CSRC, *extra, "-c", s, "-o", o]
+            jobs.append(cmd)
+    with ThreadPoolExecutor(max_workers=4) as ex:
+        outs = list(ex.map(_run, jobs))
+    if verbose:
+        for o in outs:
+            print(o)
+    lib = os.path.join(PKG, "libnsdf_cuda.so")
+    if force or jobs or _stale(lib, objs):
+        _run([NVCC, *ARCH, "-shared", "-o", lib, *objs, "-lcudart"])
+    return lib
+
+
+def build_host(force=False):
+    """The drop-in C++ library: include/nsdf headers, host/*.cpp, links libnsdf_cuda.so."""
+    if not os.path.isdir(HOST):
+        return None
+    srcs = sorted(os.path.join(HOST, f) for f in os.listdir(HOST) if f.endswith(".cpp"))
+    if not srcs:
+        return None
+    lib = os.path.join(PKG, "libnsdf_b200.so")
+    hdrs = []
+    for dp, _, fs in os.walk(os.path.join(INC, "nsdf")):
+        hdrs += [os.path.join(dp, f) for f in fs]
+    if force or _stale(lib, srcs + hdrs + [os.path.join(PKG, "libnsdf_cuda.so")]):
+        _run(["g++", "-O2", "-std=c++20", "-fPIC", "-shared", "-ffp-contract=off", "-Wall", "-I", INC,
+              "-I", JSON_DIR, *srcs, "-o", lib, "-L", PKG, "-lnsdf_cuda", "-Wl,-rpath,$ORIGIN"])
+    return lib
+
+
+def build(force=False, verbose=False):
+    build_cuda(force, verbose)
+    build_host(force)
+
+
+if __name__ == "__main__":
+    build(force="--force" in sys.argv, verbose="-v" in sys.argv)

@@ -1,0 +1,718 @@
+// The C ABI of libnsdf_cuda.so (include/nsdf_cuda.h): contexts, weight upload, and the
+// batch / trace / render entry points.  Host-side validation mirrors the reference's
+// (MlpParams::validate mlp.cpp:13-39, TraceConfig::validate trace.cpp:10-23,
+// Camera::validate camera.cpp:7-18, NestedSequence::validate nesting.cpp:56-69,
+// render() render.cpp:12-25, shade() shade.cpp:47-65); no exception crosses the boundary.
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <algorithm>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "engine.cuh"
+#include "mlp_tc.cuh"
+
+using namespace nsdf_b200;
+
+namespace {
+
+thread_local std::string g_error;
+
+int fail(int status, const std::string& msg) {
+  g_error = msg;
+  return status;
+}
+
+#define NSDF_CUDA(call)                                                                          \
+  do {                                                                                           \
+    cudaError_t e_ = (call);                                                                     \
+    if (e_ != cudaSuccess) return fail(NSDF_ERR_DEVICE, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+struct FieldRec {
+  DevField dev{};
+  std::vector<void*> allocs;
+  int input_dim = 3;
+  int n_layers = 0;
+  int width = 0;
+  ~FieldRec() {
+    for (void* p : allocs) cudaFree(p);
+  }
+};
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+}  // namespace
+
+struct nsdf_ctx {
+  int device = 0;
+  cudaStream_t own = nullptr;
+  cudaStream_t stream = nullptr;
+  int mode = NSDF_MODE_FP32_ORACLE;
+  std::mutex mu;
+  std::map<int, std::unique_ptr<FieldRec>> fields;
+  int next_handle = 1;
+  Workspace frame;   // ray state, lists, counters
+  Workspace io;      // API staging: points, outputs, framebuffers, records
+};
+
+namespace {
+
+Mode mode_of(const nsdf_ctx* c) { return c->mode == NSDF_MODE_FP16_FAST ? Mode::Fp16Fast : Mode::Fp32Oracle; }
+
+int find_field(nsdf_ctx* c, nsdf_field h, FieldRec** out) {
+  auto it = c->fields.find(h);
+  if (it == c->fields.end()) return fail(NSDF_ERR_CONTRACT, "unknown field handle " + std::to_string(h));
+  *out = it->second.get();
+  return NSDF_OK;
+}
+
+struct V3 {
+  double x, y, z;
+};
+V3 sub(V3 a, V3 b) { return {a.x - b.x, a.y - b.y, a.z - b.z}; }
+double norm(V3 a) { return std::sqrt(a.x * a.x + a.y * a.y + a.z * a.z); }
+V3 normalized(V3 a) {
+  double n = norm(a);
+  return n > 0 ? V3{a.x / n, a.y / n, a.z / n} : V3{0, 0, 0};
+}
+V3 cross(V3 a, V3 o) { return {a.y * o.z - a.z * o.y, a.z * o.x - a.x * o.z, a.x * o.y - a.y * o.x}; }
+
+int camera_basis(const nsdf_camera* c, CamBasis* cb) {
+  if (!c) return fail(NSDF_ERR_CONTRACT, "camera is null");
+  if (c->width <= 0 || c->height <= 0)
+    return fail(NSDF_ERR_CONFIG, "image size must be positive, got " + std::to_string(c->width) + "x" +
+                                     std::to_string(c->height));
+  if (!(c->vertical_fov_deg > 0) || !(c->vertical_fov_deg < 180))
+    return fail(NSDF_ERR_CONFIG, "vertical fov must be in (0,180) degrees");
+  const V3 pos{c->position[0], c->position[1], c->position[2]};
+  const V3 at{c->look_at[0], c->look_at[1], c->look_at[2]};
+  const V3 up0{c->up[0], c->up[1], c->up[2]};
+  const V3 fwd = normalized(sub(at, pos));
+  if (norm(fwd) == 0) return fail(NSDF_ERR_CONFIG, "camera position and look_at coincide");
+  if (norm(cross(fwd, up0)) < 1e-9) return fail(NSDF_ERR_CONFIG, "up vector is parallel to the view direction");
+  const V3 right = normalized(cross(fwd, up0));
+  const V3 up = cross(right, fwd);
+  cb->fwd[0] = fwd.x, cb->fwd[1] = fwd.y, cb->fwd[2] = fwd.z;
+  cb->right[0] = right.x, cb->right[1] = right.y, cb->right[2] = right.z;
+  cb->up[0] = up.x, cb->up[1] = up.y, cb->up[2] = up.z;
+  cb->half_h = std::tan(c->vertical_fov_deg * M_PI / 360.0);
+  cb->half_w = cb->half_h * double(c->width) / double(c->height);
+  cb->origin[0] = float(pos.x), cb->origin[1] = float(pos.y), cb->origin[2] = float(pos.z);
+  cb->width = c->width;
+  cb->height = c->height;
+  return NSDF_OK;
+}
+
+int shade_params(const nsdf_shade_config* s, const nsdf_camera* cam, ShadeParams* sp) {
+  if (!s) return fail(NSDF_ERR_CONTRACT, "shade config is null");
+  if (s->n_lights < 1) return fail(NSDF_ERR_CONTRACT, "at least one directional light is required");
+  if (s->n_lights > NSDF_MAX_LIGHTS)
+    return fail(NSDF_ERR_CONFIG, "at most " + std::to_string(NSDF_MAX_LIGHTS) + " lights supported");
+  for (int c = 0; c < 3; ++c) sp->albedo[c] = s->albedo[c], sp->background[c] = s->background[c];
+  sp->ambient = s->ambient;
+  sp->diffuse = s->diffuse;
+  sp->specular = s->specular;
+  sp->shininess = s->shininess;
+  sp->n_lights = s->n_lights;
+  for (int i = 0; i < s->n_lights; ++i) {
+    const float* d = s->light_direction[i];
+    const float n = std::sqrt(d[0] * d[0] + d[1] * d[1] + d[2] * d[2]);
+    if (n == 0) return fail(NSDF_ERR_CONTRACT, "light direction must be nonzero");
+    sp->light[i][0] = d[0] / n;
+    sp->light[i][1] = d[1] / n;
+    sp->light[i][2] = d[2] / n;
+    sp->light[i][3] = s->light_intensity[i];
+  }
+  sp->cam[0] = float(cam->position[0]);
+  sp->cam[1] = float(cam->position[1]);
+  sp->cam[2] = float(cam->position[2]);
+  return NSDF_OK;
+}
+
+int validate_sequence(nsdf_ctx* c, const nsdf_level* levels, int m, const nsdf_trace_config* cfg) {
+  if (!levels || m < 1) return fail(NSDF_ERR_VALIDATION, "sequence has no fields");
+  for (int i = 0; i < m; ++i) {
+    if (!(levels[i].delta > 0))
+      return fail(NSDF_ERR_VALIDATION, "threshold " + std::to_string(i) + " is not positive");
+    FieldRec* f;
+    if (int st = find_field(c, levels[i].field, &f)) return st;
+    (void)f;
+  }
+  if (!cfg) return fail(NSDF_ERR_CONTRACT, "trace config is null");
+  if (cfg->n_levels != m)
+    return fail(NSDF_ERR_CONFIG, "got " + std::to_string(cfg->n_levels) + " budgets for " + std::to_string(m) +
+                                     " levels");
+  if (m > NSDF_MAX_LEVELS) return fail(NSDF_ERR_CONFIG, "at most 8 levels supported");
+  bool any = false;
+  for (int j = 0; j < m; ++j) {
+    if (cfg->budgets[j] < 0) return fail(NSDF_ERR_CONFIG, "iteration budgets must be non-negative");
+    if (cfg->budgets[j] > 0) any = true;
+    if (cfg->budgets[j] > 65535) return fail(NSDF_ERR_CONFIG, "iteration budget exceeds the uint16 counter");
+  }
+  if (!any) return fail(NSDF_ERR_CONFIG, "all iteration budgets are zero");
+  if (!(cfg->eps_stop > 0)) return fail(NSDF_ERR_CONFIG, "eps_stop must be positive");
+  return NSDF_OK;
+}
+
+// Traced levels (trace_rays, trace.cpp:89-117): zero budgets skipped, the last nonzero
+// one is final and traces the zero set.
+std::vector<LevelDesc> traced_levels(nsdf_ctx* c, const nsdf_level* levels, int m, const nsdf_trace_config* cfg,
+                                     int* n_counters) {
+  int eff = -1;
+  for (int j = 0; j < m; ++j)
+    if (cfg->budgets[j] > 0) eff = j;
+  std::vector<LevelDesc> out;
+  int nc = 1;
+  for (int j = 0; j <= eff; ++j) {
+    if (cfg->budgets[j] == 0) continue;
+    LevelDesc d;
+    d.field = c->fields[levels[j].field]->dev;
+    d.time = levels[j].time;
+    d.final_level = j == eff;
+    d.delta = d.final_level ? 0.0f : float(levels[j].delta);
+    d.budget = cfg->budgets[j];
+    d.level = j;
+    out.push_back(d);
+    nc += 1 + d.budget;
+  }
+  *n_counters = nc + 2;  // + fallback count + spare
+  return out;
+}
+
+void fill_stats(const std::vector<LevelDesc>& lv, const TraceResult& tr, const std::vector<int>& counters,
+                nsdf_frame_stats* stats) {
+  std::memset(stats, 0, sizeof(*stats));
+  int in = counters[0];
+  for (size_t i = 0; i < lv.size(); ++i) {
+    const int base = tr.counter_layout_base[i];
+    uint64_t ev = 0;
+    int cur = in;
+    for (int it = 0; it < lv[i].budget; ++it) {
+      ev += uint64_t(cur);
+      cur = counters[base + 1 + it];
+    }
+    stats->evals[lv[i].level] = ev;
+    in = counters[base];  // advanced count feeds the next level
+  }
+  stats->hits = uint64_t(in);
+}
+
+// Shared frame pipeline: rays -> trace -> (records | framebuffer).
+struct FrameOut {
+  nsdf_hit_record* d_records = nullptr;  // trace_image / trace_rays
+  float* d_rgb = nullptr;                // render
+  float* d_depth = nullptr;
+  uint8_t* d_mask = nullptr;
+};
+
+int run_frame(nsdf_ctx* c, const nsdf_level* levels, int m, const nsdf_trace_config* cfg, const CamBasis* cam,
+              const float* d_rays6, int n_rays, const ShadeParams* sp, int normal_source, int fine_index,
+              int tile_size, int tile_rank, int tile_world, const FrameOut& out, nsdf_frame_stats* stats) {
+  int n_counters = 0;
+  std::vector<LevelDesc> lv = traced_levels(c, levels, m, cfg, &n_counters);
+  const int n_max = cam ? cam->width * cam->height : n_rays;
+  NSDF_CUDA(c->frame.reserve(frame_workspace_bytes(n_max, n_counters)));
+  FrameBuffers fb = carve_frame(c->frame.base, n_max, n_counters);
+  cudaStream_t s = c->stream;
+  NSDF_CUDA(cudaMemsetAsync(fb.counters, 0, size_t(n_counters) * 4, s));
+  int* n_slots = fb.counters;
+  uint64_t launches = 0;
+  if (cam) {
+    if (tile_world <= 1) NSDF_CUDA(cudaMemcpyAsync(n_slots, &n_max, 4, cudaMemcpyHostToDevice, s));
+    launch_generate_rays(*cam, tile_size, tile_rank, tile_world, fb.st, n_slots, s);
+  } else {
+    NSDF_CUDA(cudaMemcpyAsync(n_slots, &n_rays, 4, cudaMemcpyHostToDevice, s));
+    launch_init_state_from_rays(d_rays6, n_rays, fb.st, s);
+  }
+  launches++;
+  launch_reset_state(fb.st, n_max, s);
+  TraceResult tr = run_trace(mode_of(c), lv, cfg->eps_stop, cfg->t_max, fb, n_max, n_slots, s);
+  launches += tr.launches;
+  if (out.d_records) {
+    launch_mark_hits(tr.hit_list, tr.hit_count, n_max, fb.st, s);
+    launch_write_records(fb.st, n_max, out.d_records, s);
+    launches += 2;
+  }
+  int* fb_count = fb.counters + n_counters - 2;
+  if (out.d_rgb) {
+    int eff = 0;
+    for (int j = 0; j < m; ++j)
+      if (cfg->budgets[j] > 0) eff = j;
+    const int fine = fine_index < 0 ? m - 1 : fine_index;
+    const bool mapped = normal_source == NSDF_NORMALS_MAPPED;
+    const int nidx = mapped ? fine : eff;
+    launch_fb_background(fb.st, n_slots, n_max, *sp, out.d_rgb, out.d_depth, out.d_mask, s);
+    const bool defer = mapped && fine != eff;
+    const DevField& nf = c->fields[levels[nidx].field]->dev;
+    launch_normals_shade(mode_of(c), nf, levels[nidx].time, tr.hit_list, tr.hit_count, n_max, fb.st, *sp, defer,
+                         fb.fallback_list, fb_count, out.d_rgb, out.d_depth, out.d_mask, s);
+    launches += 2;
+    if (defer) {  // own-field normals only where the fine gradient vanished (render.cpp:62-65)
+      const DevField& own = c->fields[levels[eff].field]->dev;
+      launch_normals_shade(mode_of(c), own, levels[eff].time, fb.fallback_list, fb_count, n_max, fb.st, *sp, false,
+                           nullptr, nullptr, out.d_rgb, out.d_depth, out.d_mask, s);
+      launches++;
+    }
+  }
+  NSDF_CUDA(cudaGetLastError());
+  if (stats) {
+    std::vector<int> counters(n_counters);
+    NSDF_CUDA(cudaMemcpyAsync(counters.data(), fb.counters, size_t(n_counters) * 4, cudaMemcpyDeviceToHost, s));
+    NSDF_CUDA(cudaStreamSynchronize(s));
+    fill_stats(lv, tr, counters, stats);
+    stats->normal_evals = out.d_rgb ? stats->hits : 0;
+    stats->fallback_evals = out.d_rgb ? uint64_t(counters[n_counters - 2]) : 0;
+    stats->kernel_launches = launches;
+  }
+  return NSDF_OK;
+}
+
+template <typename T>
+T* carve(void* base, size_t& off, size_t count) {
+  off = (off + 255) / 256 * 256;
+  T* p = reinterpret_cast<T*>(static_cast<char*>(base) + off);
+  off += count * sizeof(T);
+  return p;
+}
+
+int check_points(FieldRec* f, int rows, int k) {
+  if (k < 0) return fail(NSDF_ERR_CONTRACT, "matrix dimensions must be non-negative");
+  const bool ok = rows == f->input_dim || (rows == 3 && f->input_dim == 4);
+  if (!ok)
+    return fail(NSDF_ERR_CONTRACT, "point batch is " + std::to_string(rows) + "x" + std::to_string(k) + " but " +
+                                       std::to_string(f->input_dim) + " rows are required");
+  return NSDF_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int nsdf_cuda_abi_version(void) { return NSDF_CUDA_ABI_VERSION; }
+
+const char* nsdf_cuda_last_error(void) { return g_error.c_str(); }
+
+int nsdf_cuda_create(int device, nsdf_ctx** out) {
+  if (!out) return fail(NSDF_ERR_CONTRACT, "out is null");
+  int count = 0;
+  cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count == 0)
+    return fail(NSDF_ERR_DEVICE, std::string("no CUDA device available (") + cudaGetErrorString(e) +
+                                     "); the nsdf engine has no CPU fallback");
+  if (device < 0 || device >= count) return fail(NSDF_ERR_CONFIG, "device index out of range");
+  cudaDeviceProp prop;
+  cudaGetDeviceProperties(&prop, device);
+  if (prop.major < 10)
+    return fail(NSDF_ERR_DEVICE, std::string("device ") + prop.name + " is not sm_100 (B200); this build targets sm_100a");
+  DeviceGuard g(device);
+  auto* c = new nsdf_ctx;
+  c->device = device;
+  e = cudaStreamCreateWithFlags(&c->own, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    delete c;
+    return fail(NSDF_ERR_DEVICE, cudaGetErrorString(e));
+  }
+  c->stream = c->own;
+  *out = c;
+  return NSDF_OK;
+}
+
+int nsdf_cuda_destroy(nsdf_ctx* c) {
+  if (!c) return NSDF_OK;
+  {
+    DeviceGuard g(c->device);
+    cudaStreamSynchronize(c->stream);
+    c->fields.clear();
+    c->frame.~Workspace();
+    new (&c->frame) Workspace();
+    c->io.~Workspace();
+    new (&c->io) Workspace();
+    if (c->own) cudaStreamDestroy(c->own);
+  }
+  delete c;
+  return NSDF_OK;
+}
+
+int nsdf_cuda_set_mode(nsdf_ctx* c, int mode) {
+  if (!c) return fail(NSDF_ERR_CONTRACT, "context is null");
+  if (mode != NSDF_MODE_FP32_ORACLE && mode != NSDF_MODE_FP16_FAST) return fail(NSDF_ERR_CONFIG, "unknown mode");
+  std::lock_guard<std::mutex> lk(c->mu);
+  c->mode = mode;
+  return NSDF_OK;
+}
+
+int nsdf_cuda_get_mode(nsdf_ctx* c, int* mode) {
+  if (!c || !mode) return fail(NSDF_ERR_CONTRACT, "null argument");
+  *mode = c->mode;
+  return NSDF_OK;
+}
+
+int nsdf_cuda_set_stream(nsdf_ctx* c, void* stream) {
+  if (!c) return fail(NSDF_ERR_CONTRACT, "context is null");
+  std::lock_guard<std::mutex> lk(c->mu);
+  c->stream = stream ? static_cast<cudaStream_t>(stream) : c->own;
+  return NSDF_OK;
+}
+
+int nsdf_cuda_synchronize(nsdf_ctx* c) {
+  if (!c) return fail(NSDF_ERR_CONTRACT, "context is null");
+  DeviceGuard g(c->device);
+  NSDF_CUDA(cudaStreamSynchronize(c->stream));
+  return NSDF_OK;
+}
+
+int nsdf_cuda_upload_mlp(nsdf_ctx* c, int n_layers, const int32_t* rows, const int32_t* cols, const double* packed,
+                         int activation, double omega0, int input_dim, nsdf_field* out) {
+  if (!c || !out) return fail(NSDF_ERR_CONTRACT, "null argument");
+  // MlpParams::validate (mlp.cpp:13-39)
+  if (n_layers < 1) return fail(NSDF_ERR_VALIDATION, "network has no layers");
+  if (input_dim != 3 && input_dim != 4)
+    return fail(NSDF_ERR_VALIDATION, "input_dim must be 3 or 4, got " + std::to_string(input_dim));
+  if (cols[0] != input_dim)
+    return fail(NSDF_ERR_VALIDATION, "layer 0 expects input dim " + std::to_string(cols[0]) +
+                                         " but network input_dim is " + std::to_string(input_dim));
+  for (int i = 0; i + 1 < n_layers; ++i)
+    if (cols[i + 1] != rows[i])
+      return fail(NSDF_ERR_VALIDATION, "dimension chain broken between layers " + std::to_string(i) + "," +
+                                           std::to_string(i + 1));
+  if (rows[n_layers - 1] != 1)
+    return fail(NSDF_ERR_VALIDATION,
+                "output layer must have a single output, got " + std::to_string(rows[n_layers - 1]));
+  if (activation != NSDF_ACT_SINE && activation != NSDF_ACT_IDENTITY)
+    return fail(NSDF_ERR_CONFIG, "unknown activation kind");
+  if (n_layers > kMaxLayers)
+    return fail(NSDF_ERR_CONFIG, "the device engine supports at most " + std::to_string(kMaxLayers) + " layers");
+  int maxw = input_dim;
+  for (int i = 0; i < n_layers; ++i) {
+    if (rows[i] < 1 || cols[i] < 1) return fail(NSDF_ERR_VALIDATION, "layer dimensions must be positive");
+    maxw = std::max(maxw, int(rows[i]));
+  }
+  if (maxw > kMaxWidth)
+    return fail(NSDF_ERR_CONFIG, "the device engine supports widths up to " + std::to_string(kMaxWidth));
+  std::lock_guard<std::mutex> lk(c->mu);
+  DeviceGuard g(c->device);
+  auto rec = std::make_unique<FieldRec>();
+  DevNet& n = rec->dev.net;
+  rec->dev.kind = kFieldMlp;
+  n.n_layers = n_layers;
+  n.input_dim = input_dim;
+  n.activation = activation;
+  n.omega = float(omega0);
+  n.max_width = maxw;
+  size_t off = 0;
+  for (int l = 0; l < n_layers; ++l) {
+    const int R = rows[l], K = cols[l], Rp = (R + 3) / 4 * 4;
+    std::vector<float> w(size_t(R) * K), wt(size_t(K) * Rp, 0.0f), b(R);
+    for (size_t i = 0; i < w.size(); ++i) w[i] = float(packed[off + i]);  // field.cpp:150
+    off += w.size();
+    for (int i = 0; i < R; ++i) b[i] = float(packed[off + i]);
+    off += R;
+    for (int i = 0; i < R; ++i)
+      for (int k = 0; k < K; ++k) wt[size_t(k) * Rp + i] = w[size_t(i) * K + k];
+    float *dw, *dwt, *db;
+    NSDF_CUDA(cudaMalloc(&dw, w.size() * 4));
+    rec->allocs.push_back(dw);
+    NSDF_CUDA(cudaMalloc(&dwt, wt.size() * 4));
+    rec->allocs.push_back(dwt);
+    NSDF_CUDA(cudaMalloc(&db, b.size() * 4));
+    rec->allocs.push_back(db);
+    NSDF_CUDA(cudaMemcpy(dw, w.data(), w.size() * 4, cudaMemcpyHostToDevice));
+    NSDF_CUDA(cudaMemcpy(dwt, wt.data(), wt.size() * 4, cudaMemcpyHostToDevice));
+    NSDF_CUDA(cudaMemcpy(db, b.data(), b.size() * 4, cudaMemcpyHostToDevice));
+    n.rows[l] = R;
+    n.cols[l] = K;
+    n.rows_pad[l] = Rp;
+    n.w[l] = dw;
+    n.wt[l] = dwt;
+    n.b[l] = db;
+  }
+  rec->input_dim = input_dim;
+  rec->n_layers = n_layers;
+  rec->width = int(rows[0]);
+  const int h = c->next_handle++;
+  c->fields[h] = std::move(rec);
+  *out = h;
+  return NSDF_OK;
+}
+
+int nsdf_cuda_upload_analytic(nsdf_ctx* c, int kind, const double* params, int n_params, nsdf_field* out) {
+  if (!c || !out || !params) return fail(NSDF_ERR_CONTRACT, "null argument");
+  const int want = kind == NSDF_FIELD_SPHERE ? 4 : kind == NSDF_FIELD_TORUS ? 2 : kind == NSDF_FIELD_BOX ? 3 : -1;
+  if (want < 0) return fail(NSDF_ERR_CONFIG, "unknown analytic field (expected sphere, torus or box)");
+  if (n_params != want) return fail(NSDF_ERR_CONTRACT, "analytic field expects " + std::to_string(want) + " params");
+  std::lock_guard<std::mutex> lk(c->mu);
+  auto rec = std::make_unique<FieldRec>();
+  rec->dev.kind = kind;
+  for (int i = 0; i < n_params; ++i) rec->dev.analytic[i] = params[i];
+  rec->input_dim = 3;
+  const int h = c->next_handle++;
+  c->fields[h] = std::move(rec);
+  *out = h;
+  return NSDF_OK;
+}
+
+int nsdf_cuda_release(nsdf_ctx* c, nsdf_field f) {
+  if (!c) return fail(NSDF_ERR_CONTRACT, "context is null");
+  std::lock_guard<std::mutex> lk(c->mu);
+  DeviceGuard g(c->device);
+  cudaStreamSynchronize(c->stream);
+  c->fields.erase(f);
+  return NSDF_OK;
+}
+
+int nsdf_cuda_field_info(nsdf_ctx* c, nsdf_field h, int* input_dim, int* n_layers, int* width) {
+  if (!c) return fail(NSDF_ERR_CONTRACT, "context is null");
+  std::lock_guard<std::mutex> lk(c->mu);
+  FieldRec* f;
+  if (int st = find_field(c, h, &f)) return st;
+  if (input_dim) *input_dim = f->input_dim;
+  if (n_layers) *n_layers = f->n_layers;
+  if (width) *width = f->width;
+  return NSDF_OK;
+}
+
+int nsdf_cuda_eval_grad_device(nsdf_ctx* c, nsdf_field h, const float* d_points, int rows, int k, float time,
+                               float* d_out, float* d_grad) {
+  if (!c) return fail(NSDF_ERR_CONTRACT, "context is null");
+  std::lock_guard<std::mutex> lk(c->mu);
+  DeviceGuard g(c->device);
+  FieldRec* f;
+  if (int st = find_field(c, h, &f)) return st;
+  if (int st = check_points(f, rows, k)) return st;
+  launch_eval(mode_of(c), f->dev, d_points, rows, k, time, d_out, d_grad, c->stream);
+  NSDF_CUDA(cudaGetLastError());
+  return NSDF_OK;
+}
+
+int nsdf_cuda_eval_grad(nsdf_ctx* c, nsdf_field h, const float* points, int rows, int k, float time, float* out,
+                        float* grad) {
+  if (!c) return fail(NSDF_ERR_CONTRACT, "context is null");
+  std::lock_guard<std::mutex> lk(c->mu);
+  DeviceGuard g(c->device);
+  FieldRec* f;
+  if (int st = find_field(c, h, &f)) return st;
+  if (int st = check_points(f, rows, k)) return st;
+  if (k == 0) return NSDF_OK;
+  if (!points) return fail(NSDF_ERR_CONTRACT, "points is null");
+  size_t off = 0;
+  NSDF_CUDA(c->io.reserve(size_t(k) * (rows + 4) * 4 + 4096));
+  float* dp = carve<float>(c->io.base, off, size_t(rows) * k);
+  float* dout = carve<float>(c->io.base, off, size_t(k));
+  float* dgrad = carve<float>(c->io.base, off, size_t(3) * k);
+  cudaStream_t s = c->stream;
+  NSDF_CUDA(cudaMemcpyAsync(dp, points, size_t(rows) * k * 4, cudaMemcpyHostToDevice, s));
+  launch_eval(mode_of(c), f->dev, dp, rows, k, time, out ? dout : (grad ? nullptr : dout), grad ? dgrad : nullptr, s);
+  NSDF_CUDA(cudaGetLastError());
+  if (out) NSDF_CUDA(cudaMemcpyAsync(out, dout, size_t(k) * 4, cudaMemcpyDeviceToHost, s));
+  if (grad) NSDF_CUDA(cudaMemcpyAsync(grad, dgrad, size_t(3) * k * 4, cudaMemcpyDeviceToHost, s));
+  NSDF_CUDA(cudaStreamSynchronize(s));
+  return NSDF_OK;
+}
+
+int nsdf_cuda_eval(nsdf_ctx* c, nsdf_field h, const float* points, int rows, int k, float time, float* out) {
+  if (!out && k > 0) return fail(NSDF_ERR_CONTRACT, "out is null");
+  return nsdf_cuda_eval_grad(c, h, points, rows, k, time, out, nullptr);
+}
+
+int nsdf_cuda_grad(nsdf_ctx* c, nsdf_field h, const float* points, int rows, int k, float time, float* grad) {
+  if (!grad && k > 0) return fail(NSDF_ERR_CONTRACT, "grad is null");
+  return nsdf_cuda_eval_grad(c, h, points, rows, k, time, nullptr, grad);
+}
+
+int nsdf_cuda_generate_rays(nsdf_ctx* c, const nsdf_camera* camera, float* rays) {
+  if (!c || !rays) return fail(NSDF_ERR_CONTRACT, "null argument");
+  std::lock_guard<std::mutex> lk(c->mu);
+  DeviceGuard g(c->device);
+  CamBasis cb;
+  if (int st = camera_basis(camera, &cb)) return st;
+  const int n = cb.width * cb.height;
+  NSDF_CUDA(c->frame.reserve(frame_workspace_bytes(n, 4)));
+  FrameBuffers fb = carve_frame(c->frame.base, n, 4);
+  size_t off = 0;
+  NSDF_CUDA(c->io.reserve(size_t(n) * 24 + 4096));
+  float* d = carve<float>(c->io.base, off, size_t(6) * n);
+  launch_generate_rays(cb, 1, 0, 1, fb.st, fb.counters, c->stream);
+  launch_rays_to_host_layout(fb.st, n, d, c->stream);
+  NSDF_CUDA(cudaGetLastError());
+  NSDF_CUDA(cudaMemcpyAsync(rays, d, size_t(n) * 24, cudaMemcpyDeviceToHost, c->stream));
+  NSDF_CUDA(cudaStreamSynchronize(c->stream));
+  return NSDF_OK;
+}
+
+int nsdf_cuda_trace_rays(nsdf_ctx* c, const nsdf_level* levels, int m, const nsdf_trace_config* config,
+                         const float* rays, int n, nsdf_hit_record* out) {
+  if (!c) return fail(NSDF_ERR_CONTRACT, "context is null");
+  std::lock_guard<std::mutex> lk(c->mu);
+  DeviceGuard g(c->device);
+  if (int st = validate_sequence(c, levels, m, config)) return st;
+  if (n < 0) return fail(NSDF_ERR_CONTRACT, "ray count must be non-negative");
+  if (n == 0) return NSDF_OK;
+  size_t off = 0;
+  NSDF_CUDA(c->io.reserve(size_t(n) * (24 + sizeof(nsdf_hit_record)) + 4096));
+  float* dr = carve<float>(c->io.base, off, size_t(6) * n);
+  nsdf_hit_record* drec = carve<nsdf_hit_record>(c->io.base, off, size_t(n));
+  NSDF_CUDA(cudaMemcpyAsync(dr, rays, size_t(n) * 24, cudaMemcpyHostToDevice, c->stream));
+  FrameOut fo;
+  fo.d_records = drec;
+  if (int st = run_frame(c, levels, m, config, nullptr, dr, n, nullptr, 0, -1, 1, 0, 1, fo, nullptr)) return st;
+  NSDF_CUDA(cudaMemcpyAsync(out, drec, size_t(n) * sizeof(nsdf_hit_record), cudaMemcpyDeviceToHost, c->stream));
+  NSDF_CUDA(cudaStreamSynchronize(c->stream));
+  return NSDF_OK;
+}
+
+int nsdf_cuda_trace_image(nsdf_ctx* c, const nsdf_level* levels, int m, const nsdf_camera* camera,
+                          const nsdf_trace_config* config, nsdf_hit_record* out, nsdf_frame_stats* stats) {
+  if (!c) return fail(NSDF_ERR_CONTRACT, "context is null");
+  std::lock_guard<std::mutex> lk(c->mu);
+  DeviceGuard g(c->device);
+  if (int st = validate_sequence(c, levels, m, config)) return st;
+  CamBasis cb;
+  if (int st = camera_basis(camera, &cb)) return st;
+  const int n = cb.width * cb.height;
+  size_t off = 0;
+  NSDF_CUDA(c->io.reserve(size_t(n) * sizeof(nsdf_hit_record) + 4096));
+  nsdf_hit_record* drec = carve<nsdf_hit_record>(c->io.base, off, size_t(n));
+  FrameOut fo;
+  fo.d_records = drec;
+  if (int st = run_frame(c, levels, m, config, &cb, nullptr, 0, nullptr, 0, -1, 1, 0, 1, fo, stats)) return st;
+  NSDF_CUDA(cudaMemcpyAsync(out, drec, size_t(n) * sizeof(nsdf_hit_record), cudaMemcpyDeviceToHost, c->stream));
+  NSDF_CUDA(cudaStreamSynchronize(c->stream));
+  return NSDF_OK;
+}
+
+int nsdf_cuda_normal_map(nsdf_ctx* c, nsdf_field fine, float time, const float* points, int k, double delta,
+                         const float* fallback_normals, float* normals, uint64_t* outside_count,
+                         uint64_t* fallback_count) {
+  if (!c) return fail(NSDF_ERR_CONTRACT, "context is null");
+  std::lock_guard<std::mutex> lk(c->mu);
+  DeviceGuard g(c->device);
+  FieldRec* f;
+  if (int st = find_field(c, fine, &f)) return st;
+  if (k < 0) return fail(NSDF_ERR_CONTRACT, "points must be 3xk");
+  if (outside_count) *outside_count = 0;
+  if (fallback_count) *fallback_count = 0;
+  if (k == 0) return NSDF_OK;
+  size_t off = 0;
+  NSDF_CUDA(c->io.reserve(size_t(k) * 36 + 8192));
+  float* dp = carve<float>(c->io.base, off, size_t(3) * k);
+  float* dfb = carve<float>(c->io.base, off, size_t(3) * k);
+  float* dn = carve<float>(c->io.base, off, size_t(3) * k);
+  unsigned long long* dc = carve<unsigned long long>(c->io.base, off, 2);
+  cudaStream_t s = c->stream;
+  NSDF_CUDA(cudaMemcpyAsync(dp, points, size_t(k) * 12, cudaMemcpyHostToDevice, s));
+  if (fallback_normals) NSDF_CUDA(cudaMemcpyAsync(dfb, fallback_normals, size_t(k) * 12, cudaMemcpyHostToDevice, s));
+  NSDF_CUDA(cudaMemsetAsync(dc, 0, 16, s));
+  launch_normal_map(mode_of(c), f->dev, dp, k, time, delta, fallback_normals ? dfb : nullptr, dn, dc, s);
+  NSDF_CUDA(cudaGetLastError());
+  unsigned long long hc[2];
+  NSDF_CUDA(cudaMemcpyAsync(normals, dn, size_t(k) * 12, cudaMemcpyDeviceToHost, s));
+  NSDF_CUDA(cudaMemcpyAsync(hc, dc, 16, cudaMemcpyDeviceToHost, s));
+  NSDF_CUDA(cudaStreamSynchronize(s));
+  if (outside_count) *outside_count = hc[0];
+  if (fallback_count) *fallback_count = hc[1];
+  return NSDF_OK;
+}
+
+int nsdf_cuda_shade(nsdf_ctx* c, const float* points, const float* normals, int k, const nsdf_shade_config* config,
+                    const nsdf_camera* camera, float* rgb) {
+  if (!c || !camera) return fail(NSDF_ERR_CONTRACT, "null argument");
+  std::lock_guard<std::mutex> lk(c->mu);
+  DeviceGuard g(c->device);
+  ShadeParams sp;
+  if (int st = shade_params(config, camera, &sp)) return st;
+  if (k <= 0) return NSDF_OK;
+  size_t off = 0;
+  NSDF_CUDA(c->io.reserve(size_t(k) * 36 + 4096));
+  float* dp = carve<float>(c->io.base, off, size_t(3) * k);
+  float* dn = carve<float>(c->io.base, off, size_t(3) * k);
+  float* dc = carve<float>(c->io.base, off, size_t(3) * k);
+  cudaStream_t s = c->stream;
+  NSDF_CUDA(cudaMemcpyAsync(dp, points, size_t(k) * 12, cudaMemcpyHostToDevice, s));
+  NSDF_CUDA(cudaMemcpyAsync(dn, normals, size_t(k) * 12, cudaMemcpyHostToDevice, s));
+  launch_shade(dp, dn, k, sp, dc, s);
+  NSDF_CUDA(cudaGetLastError());
+  NSDF_CUDA(cudaMemcpyAsync(rgb, dc, size_t(k) * 12, cudaMemcpyDeviceToHost, s));
+  NSDF_CUDA(cudaStreamSynchronize(s));
+  return NSDF_OK;
+}
+
+static int render_checks(nsdf_ctx* c, const nsdf_level* levels, int m, const nsdf_camera* camera,
+                         const nsdf_trace_config* trace, const nsdf_shade_config* shade, int normal_source,
+                         int fine_index, CamBasis* cb, ShadeParams* sp) {
+  if (int st = validate_sequence(c, levels, m, trace)) return st;
+  if (int st = camera_basis(camera, cb)) return st;
+  if (int st = shade_params(shade, camera, sp)) return st;
+  if (normal_source != NSDF_NORMALS_OWN && normal_source != NSDF_NORMALS_MAPPED)
+    return fail(NSDF_ERR_CONFIG, "normal source must be own or mapped");
+  const int fine = fine_index < 0 ? m - 1 : fine_index;
+  if (normal_source == NSDF_NORMALS_MAPPED && fine >= m)
+    return fail(NSDF_ERR_CONFIG, "mapped-normal field index " + std::to_string(fine) + " is out of range");
+  return NSDF_OK;
+}
+
+int nsdf_cuda_render_device(nsdf_ctx* c, const nsdf_level* levels, int m, const nsdf_camera* camera,
+                            const nsdf_trace_config* trace, const nsdf_shade_config* shade, int normal_source,
+                            int fine_index, int tile_size, int tile_rank, int tile_world, float* d_rgb,
+                            float* d_depth, uint8_t* d_mask, nsdf_frame_stats* stats) {
+  if (!c || !d_rgb || !d_depth || !d_mask) return fail(NSDF_ERR_CONTRACT, "null argument");
+  std::lock_guard<std::mutex> lk(c->mu);
+  DeviceGuard g(c->device);
+  CamBasis cb;
+  ShadeParams sp;
+  if (int st = render_checks(c, levels, m, camera, trace, shade, normal_source, fine_index, &cb, &sp)) return st;
+  if (tile_world < 1 || tile_rank < 0 || tile_rank >= tile_world)
+    return fail(NSDF_ERR_CONFIG, "tile rank/world out of range");
+  if (tile_world > 1 && tile_size < 1) return fail(NSDF_ERR_CONFIG, "tile size must be positive");
+  FrameOut fo;
+  fo.d_rgb = d_rgb;
+  fo.d_depth = d_depth;
+  fo.d_mask = d_mask;
+  return run_frame(c, levels, m, trace, &cb, nullptr, 0, &sp, normal_source, fine_index, tile_size, tile_rank,
+                   tile_world, fo, stats);
+}
+
+int nsdf_cuda_render(nsdf_ctx* c, const nsdf_level* levels, int m, const nsdf_camera* camera,
+                     const nsdf_trace_config* trace, const nsdf_shade_config* shade, int normal_source,
+                     int fine_index, float* rgb, float* depth, uint8_t* mask, nsdf_frame_stats* stats) {
+  if (!c || !rgb || !depth || !mask) return fail(NSDF_ERR_CONTRACT, "null argument");
+  std::lock_guard<std::mutex> lk(c->mu);
+  DeviceGuard g(c->device);
+  CamBasis cb;
+  ShadeParams sp;
+  if (int st = render_checks(c, levels, m, camera, trace, shade, normal_source, fine_index, &cb, &sp)) return st;
+  const size_t n = size_t(cb.width) * cb.height;
+  size_t off = 0;
+  NSDF_CUDA(c->io.reserve(n * 17 + 8192));
+  float* drgb = carve<float>(c->io.base, off, 3 * n);
+  float* ddepth = carve<float>(c->io.base, off, n);
+  uint8_t* dmask = carve<uint8_t>(c->io.base, off, n);
+  FrameOut fo;
+  fo.d_rgb = drgb;
+  fo.d_depth = ddepth;
+  fo.d_mask = dmask;
+  if (int st = run_frame(c, levels, m, trace, &cb, nullptr, 0, &sp, normal_source, fine_index, 1, 0, 1, fo, stats))
+    return st;
+  cudaStream_t s = c->stream;
+  NSDF_CUDA(cudaMemcpyAsync(rgb, drgb, 3 * n * 4, cudaMemcpyDeviceToHost, s));
+  NSDF_CUDA(cudaMemcpyAsync(depth, ddepth, n * 4, cudaMemcpyDeviceToHost, s));
+  NSDF_CUDA(cudaMemcpyAsync(mask, dmask, n, cudaMemcpyDeviceToHost, s));
+  NSDF_CUDA(cudaStreamSynchronize(s));
+  return NSDF_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,116 @@
+// Host-side launch interface of the engine kernels (engine.cu).  Used by the C ABI
+// (capi.cu); everything here is device-pointer based and asynchronous on `stream`.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <vector>
+
+#include "common.cuh"
+
+namespace nsdf_b200 {
+
+// Camera basis computed on the host in double exactly as generate_rays does
+// (camera.cpp:21-26); per-pixel arithmetic runs on the device.
+struct CamBasis {
+  double fwd[3], right[3], up[3];
+  double half_h, half_w;
+  float origin[3];
+  int width, height;
+};
+
+// Lights normalized on the host exactly as shade() does (shade.cpp:59-65).
+struct ShadeParams {
+  float albedo[3];
+  float ambient, diffuse, specular, shininess;
+  int n_lights;
+  float light[NSDF_MAX_LIGHTS][4];  // x, y, z, intensity
+  float background[3];
+  float cam[3];                     // Vec3f::from(camera.position), shade.cpp:53
+};
+
+// One traced level as the kernels see it.
+struct LevelDesc {
+  DevField field;
+  float time;
+  float delta;    // float(seq.deltas[j]) or 0 at the final level (trace.cpp:111)
+  int budget;
+  int final_level;
+  int level;      // index j into iterations_used
+};
+
+// Resizable device workspace owned by a context.
+struct Workspace {
+  void* base = nullptr;
+  size_t bytes = 0;
+  void* host_pinned = nullptr;
+  size_t host_bytes = 0;
+  ~Workspace();
+  cudaError_t reserve(size_t need);
+  cudaError_t reserve_host(size_t need);
+};
+
+// Carves the ray-state arrays and lists out of a workspace.
+struct FrameBuffers {
+  RayState st;
+  int* list[3];
+  int* counters;   // per-iteration list sizes + adv counts + misc
+  int n_counters;
+  int* fallback_list;
+};
+size_t frame_workspace_bytes(int n_rays, int n_counters);
+FrameBuffers carve_frame(void* base, int n_rays, int n_counters);
+
+// Which kernel family runs the MLP tiles.
+enum class Mode : int { Fp32Oracle = 0, Fp16Fast = 1 };
+
+struct TraceResult {
+  int* hit_list;        // device: slots that converged at the final level
+  int* hit_count;       // device counter
+  std::vector<int> counter_layout_base;  // offsets of per-level iteration counters
+  int launches = 0;
+};
+
+// Ray generation for all pixels (world == 1, slot == pixel) or the owned image tiles.
+// Returns the number of slots on the device counter `n_slots` (host value written when
+// world == 1).
+void launch_generate_rays(const CamBasis& cb, int tile_size, int tile_rank, int tile_world,
+                          RayState st, int* n_slots_dev, cudaStream_t s);
+void launch_rays_to_host_layout(const RayState& st, int n, float* rays6, cudaStream_t s);
+void launch_init_state_from_rays(const float* rays6, int n, RayState st, cudaStream_t s);
+void launch_reset_state(RayState st, int n, cudaStream_t s);
+
+// Multiscale sphere tracing of `n_slots` rays (trace.cpp:86-132): level by level, one
+// compacting launch per iteration.  counters must be zeroed.  Returns the hit list.
+TraceResult run_trace(Mode mode, const std::vector<LevelDesc>& levels, float eps, float t_max,
+                      FrameBuffers& fb, int n_slots_host_max, const int* n_slots_dev,
+                      cudaStream_t s);
+
+void launch_write_records(const RayState& st, int n, nsdf_hit_record* out, cudaStream_t s);
+void launch_mark_hits(const int* list, const int* count, int n_max, RayState st, cudaStream_t s);
+
+// Framebuffer background for the slots' pixels (render.cpp:28-33).
+void launch_fb_background(const RayState& st, const int* n_slots_dev, int n_max,
+                          const ShadeParams& sp, float* rgb, float* depth, uint8_t* mask,
+                          cudaStream_t s);
+// Normals (fused fwd + 3 tangent chains) + normalize/fallback + shade + framebuffer write
+// for the hit list (render.cpp:48-80).  With `defer_fallback`, zero-gradient hits are
+// appended to fb_list instead of getting (0,1,0).
+int launch_normals_shade(Mode mode, const DevField& nf, float time, const int* list,
+                         const int* count, int n_max, const RayState& st, const ShadeParams& sp,
+                         bool defer_fallback, int* fb_list, int* fb_count, float* rgb,
+                         float* depth, uint8_t* mask, cudaStream_t s);
+
+// Batch evaluation of a field (API path).
+void launch_eval(Mode mode, const DevField& f, const float* pts, int rows, int k, float time,
+                 float* out, float* grad, cudaStream_t s);
+void launch_normal_map(Mode mode, const DevField& f, const float* pts, int k, float time,
+                       double delta, const float* fallback, float* normals,
+                       unsigned long long* counts, cudaStream_t s);
+void launch_shade(const float* pts, const float* normals, int k, const ShadeParams& sp, float* rgb,
+                  cudaStream_t s);
+
+// Tensor-core availability of a net for the fast mode (mlp_tc.cu).
+bool tc_supported(const DevNet& n);
+
+}  // namespace nsdf_b200

@@ -1,0 +1,200 @@
+"""Python-side mirror of the reference API over the C ABI (include/nsdf_cuda.h).
+
+Names follow the reference (proj/include/nsdf): eval_batch / grad_batch,
+forward_and_gradient_batch, generate_rays, multiscale_sphere_trace / trace_image,
+neural_normal_map, shade, render.  Everything runs in libnsdf_cuda.so on the GPU; a
+missing library or device raises NsdfError (there is no CPU fallback).
+"""
+from __future__ import annotations
+
+import ctypes
+from typing import Optional, Sequence as Seq
+
+import numpy as np
+
+from . import abi
+from .abi import Camera, FrameStats, HitRecord, Level, NsdfError, ShadeConfig, TraceConfig, check
+from .manifest import Analytic, Net, Sequence
+
+_F = ctypes.POINTER(ctypes.c_float)
+_I32 = ctypes.POINTER(ctypes.c_int32)
+_D = ctypes.POINTER(ctypes.c_double)
+_U8 = ctypes.POINTER(ctypes.c_uint8)
+
+
+def _fp(a):
+    return a.ctypes.data_as(_F)
+
+
+class Context:
+    """One nsdf_ctx: a device, a stream and the uploaded fields."""
+
+    def __init__(self, device: int = 0, mode: str = "fp32"):
+        self.lib = abi.load_library()
+        self._ctx = ctypes.c_void_p()
+        check(self.lib.nsdf_cuda_create(device, ctypes.byref(self._ctx)))
+        self.device = device
+        self.set_mode(mode)
+
+    def close(self):
+        if self._ctx:
+            self.lib.nsdf_cuda_destroy(self._ctx)
+            self._ctx = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def set_mode(self, mode: str):
+        m = {"fp32": abi.MODE_FP32_ORACLE, "oracle": abi.MODE_FP32_ORACLE, "fp16": abi.MODE_FP16_FAST,
+             "fast": abi.MODE_FP16_FAST}[mode]
+        check(self.lib.nsdf_cuda_set_mode(self._ctx, m))
+        self.mode = mode
+
+    def set_stream(self, stream_ptr: int):
+        check(self.lib.nsdf_cuda_set_stream(self._ctx, ctypes.c_void_p(stream_ptr)))
+
+    def synchronize(self):
+        check(self.lib.nsdf_cuda_synchronize(self._ctx))
+
+    # ---- fields -------------------------------------------------------------------------
+    def upload(self, member) -> int:
+        h = ctypes.c_int32()
+        if isinstance(member, Net):
+            rows = np.ascontiguousarray(member.rows, np.int32)
+            cols = np.ascontiguousarray(member.cols, np.int32)
+            packed = np.ascontiguousarray(member.packed, np.float64)
+            check(self.lib.nsdf_cuda_upload_mlp(self._ctx, len(rows), rows.ctypes.data_as(_I32),
+                                                cols.ctypes.data_as(_I32), packed.ctypes.data_as(_D),
+                                                member.activation, ctypes.c_double(member.omega0),
+                                                member.input_dim, ctypes.byref(h)))
+        elif isinstance(member, Analytic):
+            kind = {"sphere": abi.FIELD_SPHERE, "torus": abi.FIELD_TORUS, "box": abi.FIELD_BOX}.get(member.name)
+            if kind is None:
+                raise NsdfError(abi.ERR_CONFIG, f"analytic field '{member.name}' is not available on the device")
+            vals = np.asarray(member.values(), np.float64)
+            check(self.lib.nsdf_cuda_upload_analytic(self._ctx, kind, vals.ctypes.data_as(_D), len(vals),
+                                                     ctypes.byref(h)))
+        else:
+            raise NsdfError(abi.ERR_CONTRACT, f"cannot upload {type(member).__name__}")
+        return h.value
+
+    def release(self, handle: int):
+        check(self.lib.nsdf_cuda_release(self._ctx, handle))
+
+    def upload_sequence(self, seq: Sequence) -> "DeviceSequence":
+        return DeviceSequence(self, seq)
+
+    # ---- batch evaluation -----------------------------------------------------------------
+    def eval_grad(self, handle: int, points, time: float = 0.0, want_value=True, want_grad=True):
+        pts = np.ascontiguousarray(points, np.float32)
+        if pts.ndim != 2:
+            raise NsdfError(abi.ERR_CONTRACT, "points must be rows x k")
+        rows, k = pts.shape
+        out = np.zeros(k, np.float32) if want_value else None
+        grad = np.zeros((3, k), np.float32) if want_grad else None
+        check(self.lib.nsdf_cuda_eval_grad(self._ctx, handle, _fp(pts), rows, k, ctypes.c_float(time),
+                                           _fp(out) if out is not None else None,
+                                           _fp(grad) if grad is not None else None))
+        return out, grad
+
+    def eval(self, handle, points, time=0.0):
+        return self.eval_grad(handle, points, time, True, False)[0]
+
+    def grad(self, handle, points, time=0.0):
+        return self.eval_grad(handle, points, time, False, True)[1]
+
+    def eval_grad_device(self, handle, d_points, rows, k, time, d_out, d_grad):
+        check(self.lib.nsdf_cuda_eval_grad_device(self._ctx, handle, ctypes.c_void_p(d_points), rows, k,
+                                                  ctypes.c_float(time), ctypes.c_void_p(d_out),
+                                                  ctypes.c_void_p(d_grad)))
+
+    # ---- tracing --------------------------------------------------------------------------
+    def generate_rays(self, cam: Camera):
+        rays = np.zeros((cam.width * cam.height, 6), np.float32)
+        check(self.lib.nsdf_cuda_generate_rays(self._ctx, ctypes.byref(cam), _fp(rays)))
+        return rays
+
+    def trace_rays(self, levels, cfg: TraceConfig, rays):
+        r = np.ascontiguousarray(rays, np.float32).reshape(-1, 6)
+        out = (HitRecord * max(len(r), 1))()
+        lv, m = _levels(levels)
+        check(self.lib.nsdf_cuda_trace_rays(self._ctx, lv, m, ctypes.byref(cfg), _fp(r), len(r), out))
+        return out
+
+    def trace_image(self, levels, cam: Camera, cfg: TraceConfig):
+        out = (HitRecord * (cam.width * cam.height))()
+        st = FrameStats()
+        lv, m = _levels(levels)
+        check(self.lib.nsdf_cuda_trace_image(self._ctx, lv, m, ctypes.byref(cam), ctypes.byref(cfg), out,
+                                             ctypes.byref(st)))
+        return out, st
+
+    # ---- normals / shading / render ---------------------------------------------------------
+    def normal_map(self, handle, points, delta, fallback=None, time=0.0):
+        pts = np.ascontiguousarray(points, np.float32)
+        k = pts.shape[1]
+        nrm = np.zeros((3, k), np.float32)
+        fb = None if fallback is None else np.ascontiguousarray(fallback, np.float32)
+        o, f = ctypes.c_uint64(), ctypes.c_uint64()
+        check(self.lib.nsdf_cuda_normal_map(self._ctx, handle, ctypes.c_float(time), _fp(pts), k,
+                                            ctypes.c_double(delta), _fp(fb) if fb is not None else None,
+                                            _fp(nrm), ctypes.byref(o), ctypes.byref(f)))
+        return nrm, o.value, f.value
+
+    def shade(self, points, normals, cfg: ShadeConfig, cam: Camera):
+        pts = np.ascontiguousarray(points, np.float32)
+        nrm = np.ascontiguousarray(normals, np.float32)
+        k = pts.shape[1]
+        rgb = np.zeros((3, k), np.float32)
+        check(self.lib.nsdf_cuda_shade(self._ctx, _fp(pts), _fp(nrm), k, ctypes.byref(cfg), ctypes.byref(cam),
+                                       _fp(rgb)))
+        return rgb
+
+    def render(self, levels, cam: Camera, trace: TraceConfig, shade: ShadeConfig, normal_source=0, fine_index=-1):
+        n = cam.width * cam.height
+        rgb = np.zeros(3 * n, np.float32)
+        depth = np.zeros(n, np.float32)
+        mask = np.zeros(n, np.uint8)
+        st = FrameStats()
+        lv, m = _levels(levels)
+        check(self.lib.nsdf_cuda_render(self._ctx, lv, m, ctypes.byref(cam), ctypes.byref(trace),
+                                        ctypes.byref(shade), normal_source, fine_index, _fp(rgb), _fp(depth),
+                                        mask.ctypes.data_as(_U8), ctypes.byref(st)))
+        return rgb.reshape(cam.height, cam.width, 3), depth.reshape(cam.height, cam.width), \
+            mask.reshape(cam.height, cam.width), st
+
+    def render_device(self, levels, cam, trace, shade, d_rgb: int, d_depth: int, d_mask: int, normal_source=0,
+                      fine_index=-1, tile_size=64, tile_rank=0, tile_world=1, stats: bool = False):
+        """Device framebuffer (raw device pointers, e.g. torch tensor .data_ptr()); async."""
+        lv, m = _levels(levels)
+        st = FrameStats() if stats else None
+        check(self.lib.nsdf_cuda_render_device(self._ctx, lv, m, ctypes.byref(cam), ctypes.byref(trace),
+                                               ctypes.byref(shade), normal_source, fine_index, tile_size, tile_rank,
+                                               tile_world, ctypes.c_void_p(d_rgb), ctypes.c_void_p(d_depth),
+                                               ctypes.c_void_p(d_mask), ctypes.byref(st) if st else None))
+        return st
+
+
+def _levels(levels):
+    arr = (Level * len(levels))()
+    for i, lv in enumerate(levels):
+        arr[i] = lv
+    return arr, len(levels)
+
+
+class DeviceSequence:
+    """A NestedSequence / AnimatedSequence resident on the device (weights uploaded once)."""
+
+    def __init__(self, ctx: Context, seq: Sequence):
+        self.ctx = ctx
+        self.seq = seq
+        self.handles = [ctx.upload(m) for m in seq.members]
+
+    def levels(self, time: float = 0.0, indices: Optional[Seq[int]] = None):
+        """nsdf_level array; for animated sequences `time` is the slice (float(t),
+        field.cpp:303-305)."""
+        idx = range(len(self.handles)) if indices is None else indices
+        return [Level(self.handles[i], float(np.float32(time)), float(self.seq.deltas[i])) for i in idx]
