@@ -138,6 +138,18 @@ typedef struct {
   uint64_t kernel_launches;        /* engine kernels launched for the frame        */
 } nsdf_frame_stats;
 
+/* Per-kernel-family device time (CUDA events on the context stream), accumulated over
+ * frames while profiling is enabled — the "CUDA events per level and per frame" of
+ * SURVEY.md §5.  Reading it synchronizes the stream. */
+typedef struct {
+  double level_ms[NSDF_MAX_LEVELS]; /* trace-iteration kernels (MLP tiles) per level    */
+  double normals_ms;                /* fused normal + shade kernels                     */
+  double frame_ms;                  /* whole frames (rays .. framebuffer)              */
+  uint64_t frames;
+  uint64_t trace_launches;
+  uint64_t normal_launches;
+} nsdf_profile;
+
 /* ---- context ---------------------------------------------------------------------- */
 int nsdf_cuda_abi_version(void);
 const char* nsdf_cuda_last_error(void);
@@ -148,6 +160,9 @@ int nsdf_cuda_get_mode(nsdf_ctx* ctx, int* mode);
 /* Bind the context to an existing cudaStream_t (NULL restores the context's own). */
 int nsdf_cuda_set_stream(nsdf_ctx* ctx, void* stream);
 int nsdf_cuda_synchronize(nsdf_ctx* ctx);
+/* Enable / disable per-kernel-family CUDA-event timing (resets the accumulators). */
+int nsdf_cuda_set_profiling(nsdf_ctx* ctx, int enable);
+int nsdf_cuda_get_profile(nsdf_ctx* ctx, nsdf_profile* out);
 
 /* ---- fields -------------------------------------------------------------------------
  * Packed weights: for each layer l, rows[l]*cols[l] row-major weights (out x in) then

@@ -107,6 +107,12 @@ class FrameStats(ctypes.Structure):
                 ("kernel_launches", ctypes.c_uint64)]
 
 
+class Profile(ctypes.Structure):
+    _fields_ = [("level_ms", ctypes.c_double * MAX_LEVELS), ("normals_ms", ctypes.c_double),
+                ("frame_ms", ctypes.c_double), ("frames", ctypes.c_uint64), ("trace_launches", ctypes.c_uint64),
+                ("normal_launches", ctypes.c_uint64)]
+
+
 _LIB = None
 
 

@@ -12,6 +12,8 @@
 #include <string>
 #include <vector>
 
+#include <cuda_fp16.h>
+
 #include "engine.cuh"
 #include "mlp_tc.cuh"
 
@@ -68,6 +70,7 @@ struct nsdf_ctx {
   int next_handle = 1;
   Workspace frame;   // ray state, lists, counters
   Workspace io;      // API staging: points, outputs, framebuffers, records
+  Profiler prof;
 };
 
 namespace {
@@ -232,6 +235,8 @@ int run_frame(nsdf_ctx* c, const nsdf_level* levels, int m, const nsdf_trace_con
   NSDF_CUDA(cudaMemsetAsync(fb.counters, 0, size_t(n_counters) * 4, s));
   int* n_slots = fb.counters;
   uint64_t launches = 0;
+  Profiler* prof = c->prof.on ? &c->prof : nullptr;
+  cudaEvent_t ev_frame = prof ? prof->begin(s) : nullptr;
   if (cam) {
     if (tile_world <= 1) NSDF_CUDA(cudaMemcpyAsync(n_slots, &n_max, 4, cudaMemcpyHostToDevice, s));
     launch_generate_rays(*cam, tile_size, tile_rank, tile_world, fb.st, n_slots, s);
@@ -241,7 +246,7 @@ int run_frame(nsdf_ctx* c, const nsdf_level* levels, int m, const nsdf_trace_con
   }
   launches++;
   launch_reset_state(fb.st, n_max, s);
-  TraceResult tr = run_trace(mode_of(c), lv, cfg->eps_stop, cfg->t_max, fb, n_max, n_slots, s);
+  TraceResult tr = run_trace(mode_of(c), lv, cfg->eps_stop, cfg->t_max, fb, n_max, n_slots, s, prof);
   launches += tr.launches;
   if (out.d_records) {
     launch_mark_hits(tr.hit_list, tr.hit_count, n_max, fb.st, s);
@@ -259,6 +264,7 @@ int run_frame(nsdf_ctx* c, const nsdf_level* levels, int m, const nsdf_trace_con
     launch_fb_background(fb.st, n_slots, n_max, *sp, out.d_rgb, out.d_depth, out.d_mask, s);
     const bool defer = mapped && fine != eff;
     const DevField& nf = c->fields[levels[nidx].field]->dev;
+    cudaEvent_t ev_n = prof ? prof->begin(s) : nullptr;
     launch_normals_shade(mode_of(c), nf, levels[nidx].time, tr.hit_list, tr.hit_count, n_max, fb.st, *sp, defer,
                          fb.fallback_list, fb_count, out.d_rgb, out.d_depth, out.d_mask, s);
     launches += 2;
@@ -268,7 +274,12 @@ int run_frame(nsdf_ctx* c, const nsdf_level* levels, int m, const nsdf_trace_con
                            nullptr, nullptr, out.d_rgb, out.d_depth, out.d_mask, s);
       launches++;
     }
+    if (prof) {
+      prof->end(Profiler::kNormals, ev_n, s);
+      prof->acc.normal_launches += defer ? 2 : 1;
+    }
   }
+  if (prof) prof->end(Profiler::kFrame, ev_frame, s);
   NSDF_CUDA(cudaGetLastError());
   if (stats) {
     std::vector<int> counters(n_counters);
@@ -376,6 +387,24 @@ int nsdf_cuda_synchronize(nsdf_ctx* c) {
   return NSDF_OK;
 }
 
+int nsdf_cuda_set_profiling(nsdf_ctx* c, int enable) {
+  if (!c) return fail(NSDF_ERR_CONTRACT, "context is null");
+  std::lock_guard<std::mutex> lk(c->mu);
+  DeviceGuard g(c->device);
+  c->prof.reset();
+  c->prof.on = enable != 0;
+  return NSDF_OK;
+}
+
+int nsdf_cuda_get_profile(nsdf_ctx* c, nsdf_profile* out) {
+  if (!c || !out) return fail(NSDF_ERR_CONTRACT, "null argument");
+  std::lock_guard<std::mutex> lk(c->mu);
+  DeviceGuard g(c->device);
+  c->prof.collect();
+  *out = c->prof.acc;
+  return NSDF_OK;
+}
+
 int nsdf_cuda_upload_mlp(nsdf_ctx* c, int n_layers, const int32_t* rows, const int32_t* cols, const double* packed,
                          int activation, double omega0, int input_dim, nsdf_field* out) {
   if (!c || !out) return fail(NSDF_ERR_CONTRACT, "null argument");
@@ -440,6 +469,48 @@ int nsdf_cuda_upload_mlp(nsdf_ctx* c, int n_layers, const int32_t* rows, const i
     n.w[l] = dw;
     n.wt[l] = dwt;
     n.b[l] = db;
+  }
+  // Fast-mode copy (mlp_tc.cu): sine nets whose hidden layers are square W x W with
+  // W in {64, 128, 256}.  Hidden weights -> fp16 in the UMMA canonical K-major layout,
+  // element (n, k) at ((k/8)*(W/8) + n/8)*64 + (n%8)*8 + k%8, so every 32-wide K chunk is
+  // one contiguous bulk copy.
+  n.tc_ok = 0;
+  {
+    const int W = rows[0];
+    bool ok = activation == NSDF_ACT_SINE && n_layers >= 3 && (W == 64 || W == 128 || W == 256);
+    for (int l = 1; ok && l + 1 < n_layers; ++l) ok = rows[l] == W && cols[l] == W;
+    if (ok) {
+      const int H = n_layers - 2;
+      std::vector<__half> wq(size_t(H) * W * W);
+      std::vector<float> bias(size_t(n_layers - 1) * W);
+      size_t o = 0;
+      for (int l = 0; l < n_layers; ++l) {
+        const size_t nw = size_t(rows[l]) * cols[l];
+        if (l >= 1 && l + 1 < n_layers) {
+          __half* dst = wq.data() + size_t(l - 1) * W * W;
+          for (int r = 0; r < W; ++r)
+            for (int k = 0; k < W; ++k)
+              dst[size_t((k / 8) * (W / 8) + r / 8) * 64 + (r % 8) * 8 + k % 8] =
+                  __float2half_rn(float(packed[o + size_t(r) * W + k]));
+        }
+        o += nw;
+        if (l + 1 < n_layers)
+          for (int r = 0; r < rows[l]; ++r) bias[size_t(l) * W + r] = float(packed[o + r]);
+        else
+          n.bout = float(packed[o]);
+        o += rows[l];
+      }
+      void *dq, *db;
+      NSDF_CUDA(cudaMalloc(&dq, wq.size() * 2));
+      rec->allocs.push_back(dq);
+      NSDF_CUDA(cudaMalloc(&db, bias.size() * 4));
+      rec->allocs.push_back(db);
+      NSDF_CUDA(cudaMemcpy(dq, wq.data(), wq.size() * 2, cudaMemcpyHostToDevice));
+      NSDF_CUDA(cudaMemcpy(db, bias.data(), bias.size() * 4, cudaMemcpyHostToDevice));
+      n.wq = static_cast<const uint16_t*>(dq);
+      n.bias_cat = static_cast<const float*>(db);
+      n.tc_ok = 1;
+    }
   }
   rec->input_dim = input_dim;
   rec->n_layers = n_layers;

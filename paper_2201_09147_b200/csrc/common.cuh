@@ -32,6 +32,11 @@ struct DevNet {
   const float* w[kMaxLayers];
   const float* wt[kMaxLayers];
   const float* b[kMaxLayers];
+  // Fast-mode (tcgen05) copy, built at upload when tc-eligible (mlp_tc.cu):
+  int tc_ok;
+  const uint16_t* wq;      // hidden layers, fp16, UMMA canonical K-major chunked layout
+  const float* bias_cat;   // biases of layers 0 .. L-2, [L-1][width]
+  float bout;              // output bias
 };
 
 struct DevField {

@@ -43,6 +43,57 @@ cudaError_t Workspace::reserve_host(size_t need) {
   return e;
 }
 
+cudaEvent_t Profiler::begin(cudaStream_t s) {
+  if (!on) return nullptr;
+  cudaEvent_t e;
+  if (pool.empty()) {
+    cudaEventCreate(&e);
+  } else {
+    e = pool.back();
+    pool.pop_back();
+  }
+  cudaEventRecord(e, s);
+  return e;
+}
+
+void Profiler::end(int kind, cudaEvent_t a, cudaStream_t s) {
+  if (!on || !a) return;
+  cudaEvent_t b = begin(s);
+  pending.push_back({kind, a, b});
+}
+
+void Profiler::collect() {
+  for (const Span& sp : pending) {
+    cudaEventSynchronize(sp.b);
+    float ms = 0.0f;
+    cudaEventElapsedTime(&ms, sp.a, sp.b);
+    if (sp.kind < NSDF_MAX_LEVELS) {
+      acc.level_ms[sp.kind] += ms;
+    } else if (sp.kind == kNormals) {
+      acc.normals_ms += ms;
+    } else {
+      acc.frame_ms += ms;
+      acc.frames++;
+    }
+    pool.push_back(sp.a);
+    pool.push_back(sp.b);
+  }
+  pending.clear();
+}
+
+void Profiler::reset() {
+  collect();
+  acc = nsdf_profile{};
+}
+
+Profiler::~Profiler() {
+  for (const Span& sp : pending) {
+    cudaEventDestroy(sp.a);
+    cudaEventDestroy(sp.b);
+  }
+  for (cudaEvent_t e : pool) cudaEventDestroy(e);
+}
+
 static size_t align_up(size_t v, size_t a) { return (v + a - 1) / a * a; }
 
 size_t frame_workspace_bytes(int n_rays, int n_counters) {
@@ -284,7 +335,7 @@ __global__ void iota_kernel(int* list, const int* n) {
 }
 
 TraceResult run_trace(Mode mode, const std::vector<LevelDesc>& levels, float eps, float t_max,
-                      FrameBuffers& fb, int n_max, const int* n_slots_dev, cudaStream_t s) {
+                      FrameBuffers& fb, int n_max, const int* n_slots_dev, cudaStream_t s, Profiler* prof) {
   TraceResult res;
   int cur = 0, nxt = 1, adv = 2;
   iota_kernel<<<std::max(1, std::min((n_max + 255) / 256, num_sms() * 8)), 256, 0, s>>>(fb.list[cur], n_slots_dev);
@@ -306,6 +357,7 @@ TraceResult run_trace(Mode mode, const std::vector<LevelDesc>& levels, float eps
     const int* in_list = fb.list[cur];
     const int* in_count = level_in_count;
     int ping = cur, pong = nxt;
+    cudaEvent_t ev = prof ? prof->begin(s) : nullptr;
     for (int iter = 0; iter < lv.budget; ++iter) {
       a.iter = iter;
       a.in_list = in_list;
@@ -332,6 +384,10 @@ TraceResult run_trace(Mode mode, const std::vector<LevelDesc>& levels, float eps
       in_list = fb.list[pong];
       in_count = it_counts + iter;
       std::swap(ping, pong);
+    }
+    if (prof) {
+      prof->end(lv.level, ev, s);
+      prof->acc.trace_launches += lv.budget;
     }
     // The advanced list feeds the next level; the other two lists are free again.
     level_in_count = adv_count;

@@ -61,6 +61,25 @@ struct FrameBuffers {
 size_t frame_workspace_bytes(int n_rays, int n_counters);
 FrameBuffers carve_frame(void* base, int n_rays, int n_counters);
 
+// CUDA-event timing per kernel family (nsdf_cuda_set_profiling).  Events are recorded on
+// the launching stream around each family and folded into `acc` by collect().
+struct Profiler {
+  enum Kind { kLevel0 = 0, kNormals = NSDF_MAX_LEVELS, kFrame = NSDF_MAX_LEVELS + 1 };
+  bool on = false;
+  nsdf_profile acc{};
+  std::vector<cudaEvent_t> pool;
+  struct Span {
+    int kind;
+    cudaEvent_t a, b;
+  };
+  std::vector<Span> pending;
+  cudaEvent_t begin(cudaStream_t s);
+  void end(int kind, cudaEvent_t a, cudaStream_t s);
+  void collect();
+  void reset();
+  ~Profiler();
+};
+
 // Which kernel family runs the MLP tiles.
 enum class Mode : int { Fp32Oracle = 0, Fp16Fast = 1 };
 
@@ -84,7 +103,7 @@ void launch_reset_state(RayState st, int n, cudaStream_t s);
 // compacting launch per iteration.  counters must be zeroed.  Returns the hit list.
 TraceResult run_trace(Mode mode, const std::vector<LevelDesc>& levels, float eps, float t_max,
                       FrameBuffers& fb, int n_slots_host_max, const int* n_slots_dev,
-                      cudaStream_t s);
+                      cudaStream_t s, Profiler* prof = nullptr);
 
 void launch_write_records(const RayState& st, int n, nsdf_hit_record* out, cudaStream_t s);
 void launch_mark_hits(const int* list, const int* count, int n_max, RayState st, cudaStream_t s);

@@ -1,19 +1,587 @@
-// tcgen05 fast path (FP16 operands, FP32 TMEM accumulators).  Round-1 placeholder: the
-// fast mode is not enabled yet, so every launcher declines and the FFMA tiles run.
+// tcgen05 fast path of the SIREN evaluator (north_star subsystems 1 + 2).
+//
+// One persistent CTA evaluates tiles of 128 TMEM lanes: 128 rays (forward) or 32 rays x 4
+// chains (value + 3 input tangents: the "width x 4" analytic-normal tile).  Per tile:
+//
+//   layer 0 (K = 3/4)    FP32 FFMA in the epilogue warps, sin -> fp16 A operand in SMEM
+//   hidden layers        D[128 x W] (fp32, TMEM) = A[128 x W] (fp16, SMEM) . W_l^T
+//                        tcgen05.mma.cta_group::1.kind::f16, M=128 N=W K=16 per instruction,
+//                        issued by one thread; weight K-chunks streamed into a 2-stage SMEM
+//                        ring with cp.async.bulk (pre-arranged in the UMMA canonical layout at
+//                        upload, so a chunk is one contiguous 1-D bulk copy)
+//   epilogue             tcgen05.ld 32x32b -> + bias -> range-reduced MUFU sine (turns:
+//                        t = z*omega/2pi, r = t - rint(t)) -> fp16 -> next A operand;
+//                        tangent lanes multiply by omega*cos of their ray's value lane
+//                        (warp shuffle); the last hidden layer folds the 1 x W output layer
+//                        into an FP32 dot product
+//   consumer             trace update + warp-ballot compaction | normal/shade/framebuffer
+//                        | batch outputs
+//
+// Warp roles (192 threads): warp 0 = MMA issuer (+ TMEM allocator), warp 1 = weight
+// producer, warps 2-5 = epilogue (warp w reads TMEM lanes 32*(w%4) .. +31).  Two CTAs per SM
+// overlap one CTA's tensor work with the other's sine epilogue.
+//
+// SMEM operand layout (K-major, SWIZZLE_NONE canonical): element (row r, k) of an R-row
+// operand at ((k/8)*(R/8) + r/8)*64 + (r%8)*8 + k%8 halves, i.e. 8x16-byte core matrices;
+// descriptor SBO = 128 B (next 8 rows), LBO = R*16 B (next 8 k).
+#include <cuda_fp16.h>
+
+#include "device_ops.cuh"
 #include "mlp_tc.cuh"
 
 namespace nsdf_b200 {
 
-bool tc_supported(const DevNet&) { return false; }
+namespace {
 
-bool tc_trace_iter(const LevelDesc&, float, float, int, const int*, const int*, int*, int*, int*, int*,
-                   const RayState&, int, cudaStream_t) {
-  return false;
+constexpr int kTcThreads = 192;
+constexpr int kRows = 128;   // TMEM lanes per tile
+constexpr int kKC = 32;      // K elements per streamed weight chunk
+constexpr int kStages = 2;
+constexpr float kInv2Pi = 0.15915494309189535f;
+constexpr float k2Pi = 6.283185307179586f;
+
+// ---- PTX wrappers ---------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
-bool tc_normals_shade(const DevField&, float, const int*, const int*, int, const RayState&, const ShadeParams&, bool,
-                      int*, int*, float*, float*, uint8_t*, cudaStream_t) {
-  return false;
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count));
 }
-bool tc_eval(const DevField&, const float*, int, int, float, float*, float*, cudaStream_t) { return false; }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  const uint32_t a = smem_addr(bar);
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(a), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_addr(dst)),
+               "l"(src), "r"(bytes), "r"(smem_addr(bar))
+               : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_addr(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tc_mma(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
+                                       uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float v[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// UMMA shared-memory descriptor, K-major SWIZZLE_NONE (sm_100 version bit 46).
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return uint64_t((saddr >> 4) & 0x3FFFu) | (uint64_t((lbo >> 4) & 0x3FFFu) << 16) |
+         (uint64_t((sbo >> 4) & 0x3FFFu) << 32) | (uint64_t(1) << 46);
+}
+// Instruction descriptor kind::f16: D f32, A/B f16, both K-major, M=128, N.
+__host__ __device__ constexpr uint32_t umma_idesc(int n) {
+  return (1u << 4) | (uint32_t(n >> 3) << 17) | (uint32_t(kRows >> 4) << 24);
+}
+
+// Offset (in halves) of element (row, k) in a 128-row canonical operand.
+__device__ __forceinline__ int a_off(int row, int k) { return ((k >> 3) * (kRows / 8) + (row >> 3)) * 64 + (row & 7) * 8; }
+
+// sin(omega * z) from t = z * omega / 2pi (turns): explicit reduction to [-1/2, 1/2]
+// turns, then the MUFU sine.  |error| ~ 1e-6, far below the fp16 activation rounding.
+__device__ __forceinline__ float sin_turns(float t) {
+  const float r = t - rintf(t);
+  return __sinf(r * k2Pi);
+}
+__device__ __forceinline__ void sincos_turns(float t, float& s, float& c) {
+  const float r = t - rintf(t);
+  __sincosf(r * k2Pi, &s, &c);
+}
+
+__device__ __forceinline__ uint32_t pack_half2(float a, float b) {
+  __half2 h = __floats2half2_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
+// ---- kernel parameters -------------------------------------------------------------------
+enum TcOp : int { kOpTrace = 0, kOpNormals = 1, kOpEval = 2 };
+
+struct TcNet {
+  int n_layers, width, input_dim;
+  float turns;                      // omega / 2pi
+  float omega;
+  const __half* wq;                 // hidden-layer weights, canonical chunked layout
+  const float* w0;                  // layer 0, row-major W x input_dim (fp32)
+  const float* b;                   // biases, [n_layers-1][W] (fp32)
+  const float* wout;                // output row (fp32), W
+  float bout;
+};
+
+struct TcArgs {
+  TcNet net;
+  int op;
+  // trace
+  LevelDesc lv;
+  float eps, t_max;
+  int iter;
+  const int* in_list;
+  const int* in_count;
+  int* next_list;
+  int* next_count;
+  int* adv_list;
+  int* adv_count;
+  RayState st;
+  // normals
+  float time;
+  ShadeParams sp;
+  int defer_fallback;
+  int* fb_list;
+  int* fb_count;
+  float* rgb;
+  float* depth;
+  uint8_t* mask;
+  // eval
+  const float* pts;
+  int rows, k;
+  float* out;
+  float* grad;
+};
+
+// Dynamic shared-memory carve-up (sized for the net's layer count, so two 256-wide CTAs
+// fit one SM).
+struct TcSmem {
+  __half* a;            // [128 x W] A operand
+  __half* wst;          // [kStages][W * kKC] streamed weight chunks
+  float* w0t;           // [W x input_dim] layer-0 weights * omega/2pi
+  float* w0;            // [W x input_dim] layer-0 weights
+  float* bias;          // [(L-1) x W] biases * omega/2pi
+  float* wout;          // [W]
+  uint64_t* bars;       // full[kStages], empty[kStages], aready, dfull
+  uint32_t* tmem_base;
+};
+
+__host__ __device__ inline size_t tc_smem_bytes(int W, int L) {
+  size_t b = 0;
+  b += size_t(kRows) * W * 2;
+  b += size_t(kStages) * W * kKC * 2;
+  b += size_t(W) * 4 * 4 * 2;
+  b += size_t(L - 1) * W * 4;
+  b += size_t(W) * 4;
+  b += (2 * kStages + 2) * 8 + 16;
+  return b + 1024;  // alignment slack
+}
+
+__device__ inline TcSmem tc_carve(uint8_t* raw, int W, int L) {
+  uintptr_t p = (reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023);
+  TcSmem s;
+  s.a = reinterpret_cast<__half*>(p);
+  p += size_t(kRows) * W * 2;
+  s.wst = reinterpret_cast<__half*>(p);
+  p += size_t(kStages) * W * kKC * 2;
+  s.w0t = reinterpret_cast<float*>(p);
+  p += size_t(W) * 4 * 4;
+  s.w0 = reinterpret_cast<float*>(p);
+  p += size_t(W) * 4 * 4;
+  s.bias = reinterpret_cast<float*>(p);
+  p += size_t(L - 1) * W * 4;
+  s.wout = reinterpret_cast<float*>(p);
+  p += size_t(W) * 4;
+  s.bars = reinterpret_cast<uint64_t*>((p + 7) & ~uintptr_t(7));
+  s.tmem_base = reinterpret_cast<uint32_t*>(s.bars + 2 * kStages + 2);
+  return s;
+}
+
+template <int W, bool kGrad>
+__global__ void __launch_bounds__(kTcThreads, 2) tc_mlp_kernel(TcArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  const TcNet& net = a.net;
+  const int L = net.n_layers;
+  const TcSmem sm = tc_carve(smem_raw, W, L);
+  uint64_t* full = sm.bars;
+  uint64_t* empty = sm.bars + kStages;
+  uint64_t* aready = sm.bars + 2 * kStages;
+  uint64_t* dfull = sm.bars + 2 * kStages + 1;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int IN = net.input_dim;
+  const int n_hidden = L - 2;  // MMA layers
+  constexpr int kRaysPerTile = kGrad ? kRows / 4 : kRows;
+  constexpr int kChunks = W / kKC;
+  constexpr uint32_t kChunkBytes = uint32_t(W) * kKC * 2;
+
+  // total work: tiles over the list / batch
+  int n_items;
+  if (a.op == kOpEval) n_items = a.k;
+  else n_items = *a.in_count;
+  const int n_tiles = (n_items + kRaysPerTile - 1) / kRaysPerTile;
+  const int my_tiles = blockIdx.x < n_tiles ? (n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+  if (my_tiles == 0) return;
+
+  // ---- setup: constants to SMEM, barriers, TMEM ----
+  for (int i = threadIdx.x; i < W * IN; i += kTcThreads) {
+    sm.w0[i] = net.w0[i];
+    sm.w0t[i] = net.w0[i] * net.turns;
+  }
+  for (int i = threadIdx.x; i < (L - 1) * W; i += kTcThreads) sm.bias[i] = net.b[i] * net.turns;
+  for (int i = threadIdx.x; i < W; i += kTcThreads) sm.wout[i] = net.wout[i];
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(aready, 128);
+    mbar_init(dfull, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(sm.tmem_base)),
+                 "r"(uint32_t(W < 32 ? 32 : W)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *sm.tmem_base;
+
+  if (warp == 0) {
+    // ================= MMA issuer =================
+    if (lane == 0) {
+      const uint32_t idesc = umma_idesc(W);
+      const uint32_t a_base = smem_addr(sm.a);
+      uint32_t chunk_iter = 0, aready_phase = 0;
+      for (int t = 0; t < my_tiles; ++t) {
+        for (int h = 0; h < n_hidden; ++h) {
+          mbar_wait(aready, aready_phase);
+          aready_phase ^= 1;
+          tc_fence_after();
+          for (int c = 0; c < kChunks; ++c, ++chunk_iter) {
+            const int s = chunk_iter % kStages;
+            mbar_wait(&full[s], (chunk_iter / kStages) & 1);
+            tc_fence_after();
+            const uint32_t b_base = smem_addr(sm.wst + size_t(s) * W * kKC);
+#pragma unroll
+            for (int ks = 0; ks < kKC / 16; ++ks) {
+              const int kg = c * (kKC / 8) + ks * 2;  // first 8-element k group of this K=16 step
+              const uint64_t ad = umma_desc(a_base + uint32_t(kg) * (kRows / 8) * 128, kRows * 16, 128);
+              const uint64_t bd = umma_desc(b_base + uint32_t(ks * 2) * (W / 8) * 128, W * 16, 128);
+              tc_mma(tmem, ad, bd, idesc, (c | ks) != 0);
+            }
+            tc_commit(&empty[s]);  // frees the weight stage once these MMAs retire
+          }
+          tc_commit(dfull);       // accumulator complete
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ================= weight producer =================
+    if (lane == 0) {
+      uint32_t chunk_iter = 0;
+      for (int t = 0; t < my_tiles; ++t) {
+        for (int h = 0; h < n_hidden; ++h) {
+          const __half* lw = reinterpret_cast<const __half*>(net.wq) + size_t(h) * W * W;
+          for (int c = 0; c < kChunks; ++c, ++chunk_iter) {
+            const int s = chunk_iter % kStages;
+            mbar_wait(&empty[s], ((chunk_iter / kStages) & 1) ^ 1);
+            mbar_expect_tx(&full[s], kChunkBytes);
+            bulk_g2s(sm.wst + size_t(s) * W * kKC, lw + size_t(c) * (W * kKC), kChunkBytes, &full[s]);
+          }
+        }
+      }
+    }
+  } else {
+    // ================= epilogue warps =================
+    const int q = warp & 3;
+    const int row = q * 32 + lane;                       // TMEM lane = A row
+    const uint32_t taddr = tmem + (uint32_t(q * 32) << 16);
+    const int ray = kGrad ? row >> 2 : row;             // ray within the tile
+    const int chain = kGrad ? row & 3 : 0;               // 0 = value, 1..3 = d/dx, d/dy, d/dz
+    const unsigned group_mask = 0xFu << (lane & ~3);
+    uint32_t dfull_phase = 0;
+    for (int t = 0; t < my_tiles; ++t) {
+      const int tile = blockIdx.x + t * gridDim.x;
+      const int item = tile * kRaysPerTile + ray;
+      const bool valid = item < n_items;
+      // ---- gather the point ----
+      int slot = -1;
+      float p[4] = {0.f, 0.f, 0.f, 0.f};
+      if (a.op == kOpEval) {
+        if (valid) {
+          for (int r = 0; r < 4; ++r) p[r] = r < a.rows ? a.pts[size_t(r) * a.k + item] : a.time;
+        }
+      } else {
+        if (valid) {
+          slot = a.in_list[item];
+          p[0] = a.st.px[slot];
+          p[1] = a.st.py[slot];
+          p[2] = a.st.pz[slot];
+        }
+        p[3] = a.time;
+      }
+      // ---- layer 0: FP32 FFMA, sin -> fp16 A ----
+      for (int n0 = 0; n0 < W; n0 += 8) {
+        uint32_t pk[4];
+#pragma unroll
+        for (int j = 0; j < 8; j += 2) {
+          float o[2];
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const int n = n0 + j + u;
+            float z = sm.bias[n];  // pre-scaled: turns
+#pragma unroll
+            for (int kk = 0; kk < 4; ++kk)
+              if (kk < IN) z = fmaf(sm.w0t[n * IN + kk], p[kk], z);
+            if (kGrad) {
+              float s, cs;
+              sincos_turns(z, s, cs);
+              const float dphi = __shfl_sync(group_mask, net.omega * cs, lane & ~3, 32);
+              o[u] = chain == 0 ? s : sm.w0[n * IN + chain - 1] * dphi;
+            } else {
+              o[u] = sin_turns(z);
+            }
+          }
+          pk[j / 2] = pack_half2(o[0], o[1]);
+        }
+        *reinterpret_cast<uint4*>(&sm.a[a_off(row, n0)]) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+      }
+      fence_proxy_async();
+      tc_fence_before();
+      mbar_arrive(aready);
+      // ---- hidden layers ----
+      float acc_out = 0.0f;
+      for (int h = 0; h < n_hidden; ++h) {
+        const bool last = h == n_hidden - 1;
+        mbar_wait(dfull, dfull_phase);
+        dfull_phase ^= 1;
+        tc_fence_after();
+        const float* bias = sm.bias + size_t(h + 1) * W;
+#pragma unroll 1
+        for (int c0 = 0; c0 < W; c0 += 32) {
+          float v[32];
+          tmem_ld32(taddr + uint32_t(c0), v);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            if (kGrad) {
+              const float z = fmaf(v[j], net.turns, bias[c0 + j]);
+              float s, cs;
+              sincos_turns(z, s, cs);  // only the value lane's result is used
+              const float dphi = __shfl_sync(group_mask, net.omega * cs, lane & ~3, 32);
+              v[j] = chain == 0 ? s : v[j] * dphi;
+            } else {
+              v[j] = sin_turns(fmaf(v[j], net.turns, bias[c0 + j]));
+            }
+          }
+          if (!last) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 8) {
+              *reinterpret_cast<uint4*>(&sm.a[a_off(row, c0 + j)]) =
+                  make_uint4(pack_half2(v[j], v[j + 1]), pack_half2(v[j + 2], v[j + 3]),
+                             pack_half2(v[j + 4], v[j + 5]), pack_half2(v[j + 6], v[j + 7]));
+            }
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) acc_out = fmaf(sm.wout[c0 + j], v[j], acc_out);
+          }
+        }
+        tc_fence_before();
+        if (!last) {
+          fence_proxy_async();
+          mbar_arrive(aready);
+        }
+      }
+      // ---- consumer ----
+      const float fval = (!kGrad || chain == 0) ? acc_out + net.bout : acc_out;
+      if (a.op == kOpTrace) {
+        // forward tiles: one ray per lane
+        bool conv = false, cont = false;
+        if (valid) {
+          IterArgs ia;
+          ia.lv = a.lv;
+          ia.eps = a.eps;
+          ia.t_max = a.t_max;
+          ia.iter = a.iter;
+          ia.st = a.st;
+          trace_update(ia, slot, fval, conv, cont);
+        }
+        warp_append(conv, slot, a.adv_list, a.adv_count);
+        warp_append(cont, slot, a.next_list, a.next_count);
+      } else if (kGrad) {
+        const int base = lane & ~3;
+        const float gx = __shfl_sync(0xffffffffu, fval, base + 1);
+        const float gy = __shfl_sync(0xffffffffu, fval, base + 2);
+        const float gz = __shfl_sync(0xffffffffu, fval, base + 3);
+        const float f = __shfl_sync(0xffffffffu, fval, base);
+        bool defer = false;
+        const bool lead = chain == 0 && valid;
+        if (a.op == kOpNormals) {
+          if (lead) {
+            float nrm[3];
+            if (!normalize_normal(gx, gy, gz, nrm)) {
+              nrm[0] = 0.0f;
+              nrm[1] = 1.0f;
+              nrm[2] = 0.0f;
+              defer = a.defer_fallback != 0;
+            }
+            if (!defer) shade_and_write(a.sp, a.st, slot, nrm, a.rgb, a.depth, a.mask);
+          }
+          warp_append(defer, slot, a.fb_list, a.fb_count);
+        } else if (lead) {
+          if (a.out) a.out[item] = f;
+          if (a.grad) {
+            a.grad[item] = gx;
+            a.grad[size_t(a.k) + item] = gy;
+            a.grad[size_t(2) * a.k + item] = gz;
+          }
+        }
+      } else if (valid) {
+        a.out[item] = fval;
+      }
+    }
+  }
+  // ---- teardown ----
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    __syncwarp();
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(uint32_t(W < 32 ? 32 : W)));
+  }
+}
+
+template <int W, bool kGrad>
+bool launch_w(TcArgs& a, int n_max_items, cudaStream_t s) {
+  const size_t smem = tc_smem_bytes(W, a.net.n_layers);
+  static int configured_smem = 0;
+  static int per_sm = 0;
+  if (configured_smem != int(smem)) {
+    if (cudaFuncSetAttribute(tc_mlp_kernel<W, kGrad>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) !=
+        cudaSuccess)
+      return false;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tc_mlp_kernel<W, kGrad>, kTcThreads, smem);
+    configured_smem = int(smem);
+  }
+  const int tmem_limit = 512 / (W < 32 ? 32 : W);
+  int sms = 0, dev = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int per = std::max(1, std::min(per_sm, tmem_limit));
+  constexpr int kRaysPerTile = kGrad ? kRows / 4 : kRows;
+  const int tiles = (n_max_items + kRaysPerTile - 1) / kRaysPerTile;
+  const int grid = std::max(1, std::min(tiles, sms * per));
+  tc_mlp_kernel<W, kGrad><<<grid, kTcThreads, smem, s>>>(a);
+  return cudaGetLastError() == cudaSuccess;
+}
+
+template <bool kGrad>
+bool launch_any(TcArgs& a, int n_max_items, cudaStream_t s) {
+  switch (a.net.width) {
+    case 64: return launch_w<64, kGrad>(a, n_max_items, s);
+    case 128: return launch_w<128, kGrad>(a, n_max_items, s);
+    case 256: return launch_w<256, kGrad>(a, n_max_items, s);
+    default: return false;
+  }
+}
+
+TcNet tc_net(const DevNet& n) {
+  TcNet t;
+  t.n_layers = n.n_layers;
+  t.width = n.rows[0];
+  t.input_dim = n.input_dim;
+  t.omega = n.omega;
+  t.turns = n.omega * kInv2Pi;
+  t.wq = reinterpret_cast<const __half*>(n.wq);
+  t.w0 = n.w[0];
+  t.b = n.bias_cat;
+  t.wout = n.w[n.n_layers - 1];
+  t.bout = n.bout;
+  return t;
+}
+
+}  // namespace
+
+bool tc_supported(const DevNet& n) { return n.tc_ok != 0; }
+
+bool tc_trace_iter(const LevelDesc& lv, float eps, float t_max, int iter, const int* in_list, const int* in_count,
+                   int* next_list, int* next_count, int* adv_list, int* adv_count, const RayState& st, int n_max,
+                   cudaStream_t s) {
+  TcArgs a{};
+  a.net = tc_net(lv.field.net);
+  a.op = kOpTrace;
+  a.lv = lv;
+  a.eps = eps;
+  a.t_max = t_max;
+  a.iter = iter;
+  a.in_list = in_list;
+  a.in_count = in_count;
+  a.next_list = next_list;
+  a.next_count = next_count;
+  a.adv_list = adv_list;
+  a.adv_count = adv_count;
+  a.st = st;
+  a.time = lv.time;
+  return launch_any<false>(a, n_max, s);
+}
+
+bool tc_normals_shade(const DevField& nf, float time, const int* list, const int* count, int n_max,
+                      const RayState& st, const ShadeParams& sp, bool defer_fallback, int* fb_list, int* fb_count,
+                      float* rgb, float* depth, uint8_t* mask, cudaStream_t s) {
+  TcArgs a{};
+  a.net = tc_net(nf.net);
+  a.op = kOpNormals;
+  a.in_list = list;
+  a.in_count = count;
+  a.st = st;
+  a.time = time;
+  a.sp = sp;
+  a.defer_fallback = defer_fallback ? 1 : 0;
+  a.fb_list = fb_list;
+  a.fb_count = fb_count;
+  a.rgb = rgb;
+  a.depth = depth;
+  a.mask = mask;
+  return launch_any<true>(a, n_max, s);
+}
+
+bool tc_eval(const DevField& f, const float* pts, int rows, int k, float time, float* out, float* grad,
+             cudaStream_t s) {
+  TcArgs a{};
+  a.net = tc_net(f.net);
+  a.op = kOpEval;
+  a.pts = pts;
+  a.rows = rows;
+  a.k = k;
+  a.time = time;
+  a.out = out;
+  a.grad = grad;
+  if (grad) return launch_any<true>(a, k, s);
+  return launch_any<false>(a, k, s);
+}
 
 }  // namespace nsdf_b200

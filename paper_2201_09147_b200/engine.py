@@ -59,6 +59,14 @@ class Context:
     def synchronize(self):
         check(self.lib.nsdf_cuda_synchronize(self._ctx))
 
+    def set_profiling(self, on: bool):
+        check(self.lib.nsdf_cuda_set_profiling(self._ctx, int(bool(on))))
+
+    def get_profile(self) -> "abi.Profile":
+        p = abi.Profile()
+        check(self.lib.nsdf_cuda_get_profile(self._ctx, ctypes.byref(p)))
+        return p
+
     # ---- fields -------------------------------------------------------------------------
     def upload(self, member) -> int:
         h = ctypes.c_int32()

@@ -74,7 +74,7 @@ def sample(n, g, sdf_fn, surface_fn, t=None):
 
 
 class Siren(torch.nn.Module):
-    def __init__(self, width, hidden, input_dim, omega0, seed):
+    def __init__(self, width, hidden, input_dim, omega0, seed, first_scale=1.0):
         super().__init__()
         g = torch.Generator().manual_seed(seed)
         dims = [input_dim] + [width] * (hidden + 1) + [1]
@@ -83,7 +83,9 @@ class Siren(torch.nn.Module):
         for i in range(len(dims) - 1):
             lin = torch.nn.Linear(dims[i], dims[i + 1])
             fan_in = dims[i]
-            bound = 1.0 / fan_in if i == 0 else math.sqrt(6.0 / fan_in) / omega0  # mlp.cpp:71-74
+            # mlp.cpp:71-74; coarse nets start the first layer at a lower frequency
+            # (first_scale < 1) so a 64-wide sine net can fit a smooth SDF at omega0 = 30.
+            bound = first_scale / fan_in if i == 0 else math.sqrt(6.0 / fan_in) / omega0
             with torch.no_grad():
                 lin.weight.uniform_(-bound, bound, generator=g)
                 bb = 1.0 / math.sqrt(fan_in)
@@ -105,9 +107,9 @@ class Siren(torch.nn.Module):
         return np.array(rows, np.int32), np.array(cols, np.int32), np.concatenate(chunks)
 
 
-def fit(width, hidden, input_dim, omega0, steps, batch, seed, sdf_fn, surface_fn, lr=1e-4):
+def fit(width, hidden, input_dim, omega0, steps, batch, seed, sdf_fn, surface_fn, lr=1e-4, first_scale=1.0):
     torch.manual_seed(seed)
-    net = Siren(width, hidden, input_dim, omega0, seed)
+    net = Siren(width, hidden, input_dim, omega0, seed, first_scale)
     opt = torch.optim.Adam(net.parameters(), lr=lr)
     sched = torch.optim.lr_scheduler.CosineAnnealingLR(opt, steps, eta_min=lr * 0.05)
     g = torch.Generator().manual_seed(seed + 1)
@@ -144,9 +146,9 @@ def main():
 
     if args.only in ("", "torus"):
         names = []
-        for i, (w, k) in enumerate([(64, 1), (128, 2), (256, 3)]):
-            steps = args.steps if w < 256 else int(args.steps * 1.3)
-            net = fit(w, k, 3, 30.0, steps, args.batch, 31 + 1000 * i, torus_sdf, torus_surface)
+        for i, (w, k, fs, sm) in enumerate([(64, 1, 0.7, 1.3), (128, 2, 0.5, 1.0), (256, 3, 1.0, 1.3)]):
+            steps = int(args.steps * sm)
+            net = fit(w, k, 3, 30.0, steps, args.batch, 31 + 1000 * i, torus_sdf, torus_surface, first_scale=fs)
             rows, cols, packed = net.packed()
             path = os.path.join(out, f"torus_w30_{w}x{k}.sdfnet")
             refshim.save_params(ref, rows, cols, packed, 0, 30.0, 3, path)
@@ -159,7 +161,7 @@ def main():
     if args.only in ("", "blend"):
         names = []
         for i, (w, k) in enumerate([(64, 1), (128, 2)]):
-            net = fit(w, k, 4, 30.0, args.steps, args.batch, 51 + 1000 * i, None, None)
+            net = fit(w, k, 4, 30.0, args.steps, args.batch, 51 + 1000 * i, None, None, first_scale=0.5)
             rows, cols, packed = net.packed()
             path = os.path.join(out, f"blend4d_w30_{w}x{k}.sdfnet")
             refshim.save_params(ref, rows, cols, packed, 0, 30.0, 4, path)
