@@ -204,7 +204,8 @@ def main():
     npix = W * H
 
     ctx = Context(local, args.mode)
-    stream = torch.cuda.current_stream()
+    stream = torch.cuda.Stream()          # the engine's launch stream; events are recorded on it
+    torch.cuda.set_stream(stream)
     ctx.set_stream(stream.cuda_stream)
     ds = DeviceSequence(ctx, seq)
     levels = ds.levels()
@@ -313,7 +314,8 @@ def main():
                       "fallbacks": int(st.fallback_evals), "tflop_trace": flops_trace / 1e12,
                       "tflop_normals": flops_normals / 1e12,
                       "trace_ms": trace_ms, "normals_ms": normals_ms, "profiled_frame_ms": prof.frame_ms /
-                      max(prof.frames, 1)},
+                      max(prof.frames, 1),
+                      "level_ms": [prof.level_ms[j] / max(prof.frames, 1) for j in range(len(levels))]},
             "roofline": {"bound": "tensor", "kernel": "trace-iteration MLP tiles (all levels)",
                          "achieved": achieved_tf, "peak": peak_tf, "unit": "TFLOP/s",
                          "frac": achieved_tf / peak_tf, "peak_kind": f"{pk_kind} bf16 sustained",

@@ -71,7 +71,7 @@ def build_cuda(force=False, verbose=False):
             print(o)
     lib = os.path.join(PKG, "libnsdf_cuda.so")
     if force or jobs or _stale(lib, objs):
-        _run([NVCC, *ARCH, "-shared", "-o", lib, *objs, "-lcudart"])
+        _run([NVCC, *ARCH, "-shared", "-cudart=static", "-o", lib, *objs])
     return lib
 
 

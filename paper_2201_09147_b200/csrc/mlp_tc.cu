@@ -26,6 +26,9 @@
 // descriptor SBO = 128 B (next 8 rows), LBO = R*16 B (next 8 k).
 #include <cuda_fp16.h>
 
+#include <cstdio>
+#include <cstdlib>
+
 #include "device_ops.cuh"
 #include "mlp_tc.cuh"
 
@@ -102,6 +105,17 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float v[32]) {
 #pragma unroll
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float v[16]) {
+  uint32_t r[16];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
+}
 
 // UMMA shared-memory descriptor, K-major SWIZZLE_NONE (sm_100 version bit 46).
 __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
@@ -118,14 +132,15 @@ __device__ __forceinline__ int a_off(int row, int k) { return ((k >> 3) * (kRows
 
 // sin(omega * z) from t = z * omega / 2pi (turns): explicit reduction to [-1/2, 1/2]
 // turns, then the MUFU sine.  |error| ~ 1e-6, far below the fp16 activation rounding.
-__device__ __forceinline__ float sin_turns(float t) {
-  const float r = t - rintf(t);
-  return __sinf(r * k2Pi);
+// Round-to-nearest via the 1.5*2^23 magic constant keeps the reduction on the FMA pipe
+// (FRND would share the XU pipe with MUFU.SIN); valid for |t| < 2^22 turns.
+__device__ __forceinline__ float reduce_turns(float t) {
+  constexpr float kMagic = 12582912.0f;
+  const float k = __fsub_rn(__fadd_rn(t, kMagic), kMagic);
+  return __fsub_rn(t, k);
 }
-__device__ __forceinline__ void sincos_turns(float t, float& s, float& c) {
-  const float r = t - rintf(t);
-  __sincosf(r * k2Pi, &s, &c);
-}
+__device__ __forceinline__ float sin_turns(float t) { return __sinf(reduce_turns(t) * k2Pi); }
+__device__ __forceinline__ void sincos_turns(float t, float& s, float& c) { __sincosf(reduce_turns(t) * k2Pi, &s, &c); }
 
 __device__ __forceinline__ uint32_t pack_half2(float a, float b) {
   __half2 h = __floats2half2_rn(a, b);
@@ -185,6 +200,7 @@ struct TcSmem {
   float* w0;            // [W x input_dim] layer-0 weights
   float* bias;          // [(L-1) x W] biases * omega/2pi
   float* wout;          // [W]
+  float* part;          // [kRows] partial output dots of column group 1
   uint64_t* bars;       // full[kStages], empty[kStages], aready, dfull
   uint32_t* tmem_base;
 };
@@ -196,6 +212,7 @@ __host__ __device__ inline size_t tc_smem_bytes(int W, int L) {
   b += size_t(W) * 4 * 4 * 2;
   b += size_t(L - 1) * W * 4;
   b += size_t(W) * 4;
+  b += size_t(kRows) * 4;
   b += (2 * kStages + 2) * 8 + 16;
   return b + 1024;  // alignment slack
 }
@@ -215,14 +232,81 @@ __device__ inline TcSmem tc_carve(uint8_t* raw, int W, int L) {
   p += size_t(L - 1) * W * 4;
   s.wout = reinterpret_cast<float*>(p);
   p += size_t(W) * 4;
+  s.part = reinterpret_cast<float*>(p);
+  p += size_t(kRows) * 4;
   s.bars = reinterpret_cast<uint64_t*>((p + 7) & ~uintptr_t(7));
   s.tmem_base = reinterpret_cast<uint32_t*>(s.bars + 2 * kStages + 2);
   return s;
 }
 
-template <int W, bool kGrad>
-__global__ void __launch_bounds__(kTcThreads, 2) tc_mlp_kernel(TcArgs a) {
+// Register-resident trace update of the fast path (same arithmetic as trace_update in
+// device_ops.cuh, with the ray state prefetched into registers).
+__device__ __forceinline__ void tc_trace_update(const TcArgs& a, int slot, float f, float px, float py, float pz,
+                                                float t, float dx, float dy, float dz, bool& conv, bool& cont) {
+  const RayState& st = a.st;
+  const float fd = __fsub_rn(f, a.lv.delta);
+  const float afd = fabsf(fd);
+  conv = a.lv.final_level ? afd <= a.eps : fd <= a.eps;
+  cont = false;
+  if (a.iter == 0) st.level_reached[slot] = a.lv.level;
+  if (!conv) {
+    float step = fd;
+    if (a.lv.final_level && step < 0.0f) step = 0.0f;  // trace.cpp:73
+    st.px[slot] = __fadd_rn(px, __fmul_rn(step, dx));
+    st.py[slot] = __fadd_rn(py, __fmul_rn(step, dy));
+    st.pz[slot] = __fadd_rn(pz, __fmul_rn(step, dz));
+    const float tn = __fadd_rn(t, step);
+    st.t[slot] = tn;
+    cont = !(tn > a.t_max);  // trace.cpp:78
+  }
+  if (!cont || a.iter == a.lv.budget - 1) {
+    st.iters[size_t(slot) * kMaxLevels + a.lv.level] = uint16_t(a.iter + 1);
+    st.final_dist[slot] = afd;
+  }
+}
+
+// Ray/point data of one tile row, prefetched one tile ahead.
+struct RowIn {
+  int slot;
+  float p[4];
+  float t, dx, dy, dz;
+};
+
+__device__ __forceinline__ RowIn load_row(const TcArgs& a, int item, int n_items, bool trace_state) {
+  RowIn r;
+  r.slot = -1;
+  r.p[0] = r.p[1] = r.p[2] = 0.0f;
+  r.p[3] = a.time;
+  r.t = r.dx = r.dy = r.dz = 0.0f;
+  if (item >= n_items) return r;
+  if (a.op == kOpEval) {
+    for (int k = 0; k < 4; ++k) r.p[k] = k < a.rows ? __ldg(a.pts + size_t(k) * a.k + item) : a.time;
+    return r;
+  }
+  r.slot = __ldg(a.in_list + item);
+  r.p[0] = a.st.px[r.slot];
+  r.p[1] = a.st.py[r.slot];
+  r.p[2] = a.st.pz[r.slot];
+  if (trace_state) {
+    r.t = a.st.t[r.slot];
+    r.dx = __ldg(a.st.dx + r.slot);
+    r.dy = __ldg(a.st.dy + r.slot);
+    r.dz = __ldg(a.st.dz + r.slot);
+  }
+  return r;
+}
+
+__device__ __forceinline__ void named_bar(int id, int threads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+
+// kGroups column groups of 4 epilogue warps each: group g owns columns
+// [g*W/kGroups, (g+1)*W/kGroups) of every layer (TMEM lane quadrant = warp % 4).
+template <int W, bool kGrad, int kGroups>
+__global__ void __launch_bounds__(64 + 128 * kGroups, (W == 64 ? 3 : 2)) tc_mlp_kernel(TcArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
+  constexpr int kThreads = 64 + 128 * kGroups;
+  constexpr int kCols = W / kGroups;  // columns per epilogue group
   const TcNet& net = a.net;
   const int L = net.n_layers;
   const TcSmem sm = tc_carve(smem_raw, W, L);
@@ -230,6 +314,7 @@ __global__ void __launch_bounds__(kTcThreads, 2) tc_mlp_kernel(TcArgs a) {
   uint64_t* empty = sm.bars + kStages;
   uint64_t* aready = sm.bars + 2 * kStages;
   uint64_t* dfull = sm.bars + 2 * kStages + 1;
+  float* part = sm.part;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int IN = net.input_dim;
   const int n_hidden = L - 2;  // MMA layers
@@ -237,27 +322,24 @@ __global__ void __launch_bounds__(kTcThreads, 2) tc_mlp_kernel(TcArgs a) {
   constexpr int kChunks = W / kKC;
   constexpr uint32_t kChunkBytes = uint32_t(W) * kKC * 2;
 
-  // total work: tiles over the list / batch
-  int n_items;
-  if (a.op == kOpEval) n_items = a.k;
-  else n_items = *a.in_count;
+  const int n_items = a.op == kOpEval ? a.k : *a.in_count;
   const int n_tiles = (n_items + kRaysPerTile - 1) / kRaysPerTile;
   const int my_tiles = blockIdx.x < n_tiles ? (n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   if (my_tiles == 0) return;
 
   // ---- setup: constants to SMEM, barriers, TMEM ----
-  for (int i = threadIdx.x; i < W * IN; i += kTcThreads) {
+  for (int i = threadIdx.x; i < W * IN; i += kThreads) {
     sm.w0[i] = net.w0[i];
     sm.w0t[i] = net.w0[i] * net.turns;
   }
-  for (int i = threadIdx.x; i < (L - 1) * W; i += kTcThreads) sm.bias[i] = net.b[i] * net.turns;
-  for (int i = threadIdx.x; i < W; i += kTcThreads) sm.wout[i] = net.wout[i];
+  for (int i = threadIdx.x; i < (L - 1) * W; i += kThreads) sm.bias[i] = net.b[i] * net.turns;
+  for (int i = threadIdx.x; i < W; i += kThreads) sm.wout[i] = net.wout[i];
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(aready, 128);
+    mbar_init(aready, 128 * kGroups);
     mbar_init(dfull, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -296,7 +378,7 @@ __global__ void __launch_bounds__(kTcThreads, 2) tc_mlp_kernel(TcArgs a) {
             }
             tc_commit(&empty[s]);  // frees the weight stage once these MMAs retire
           }
-          tc_commit(dfull);       // accumulator complete
+          tc_commit(dfull);        // accumulator complete
         }
       }
     }
@@ -318,35 +400,24 @@ __global__ void __launch_bounds__(kTcThreads, 2) tc_mlp_kernel(TcArgs a) {
     }
   } else {
     // ================= epilogue warps =================
+    const int eg = (warp - 2) >> 2;                      // column group
     const int q = warp & 3;
     const int row = q * 32 + lane;                       // TMEM lane = A row
-    const uint32_t taddr = tmem + (uint32_t(q * 32) << 16);
+    const int col0 = eg * kCols;
+    const uint32_t taddr = tmem + (uint32_t(q * 32) << 16) + uint32_t(col0);
     const int ray = kGrad ? row >> 2 : row;             // ray within the tile
     const int chain = kGrad ? row & 3 : 0;               // 0 = value, 1..3 = d/dx, d/dy, d/dz
     const unsigned group_mask = 0xFu << (lane & ~3);
+    const bool trace_state = a.op == kOpTrace && eg == 0;
     uint32_t dfull_phase = 0;
+    RowIn cur = load_row(a, blockIdx.x * kRaysPerTile + ray, n_items, trace_state);
     for (int t = 0; t < my_tiles; ++t) {
       const int tile = blockIdx.x + t * gridDim.x;
       const int item = tile * kRaysPerTile + ray;
       const bool valid = item < n_items;
-      // ---- gather the point ----
-      int slot = -1;
-      float p[4] = {0.f, 0.f, 0.f, 0.f};
-      if (a.op == kOpEval) {
-        if (valid) {
-          for (int r = 0; r < 4; ++r) p[r] = r < a.rows ? a.pts[size_t(r) * a.k + item] : a.time;
-        }
-      } else {
-        if (valid) {
-          slot = a.in_list[item];
-          p[0] = a.st.px[slot];
-          p[1] = a.st.py[slot];
-          p[2] = a.st.pz[slot];
-        }
-        p[3] = a.time;
-      }
-      // ---- layer 0: FP32 FFMA, sin -> fp16 A ----
-      for (int n0 = 0; n0 < W; n0 += 8) {
+      // ---- layer 0: FP32 FFMA, sin -> fp16 A (this group's columns) ----
+#pragma unroll 1
+      for (int n0 = col0; n0 < col0 + kCols; n0 += 8) {
         uint32_t pk[4];
 #pragma unroll
         for (int j = 0; j < 8; j += 2) {
@@ -357,7 +428,7 @@ __global__ void __launch_bounds__(kTcThreads, 2) tc_mlp_kernel(TcArgs a) {
             float z = sm.bias[n];  // pre-scaled: turns
 #pragma unroll
             for (int kk = 0; kk < 4; ++kk)
-              if (kk < IN) z = fmaf(sm.w0t[n * IN + kk], p[kk], z);
+              if (kk < IN) z = fmaf(sm.w0t[n * IN + kk], cur.p[kk], z);
             if (kGrad) {
               float s, cs;
               sincos_turns(z, s, cs);
@@ -374,6 +445,9 @@ __global__ void __launch_bounds__(kTcThreads, 2) tc_mlp_kernel(TcArgs a) {
       fence_proxy_async();
       tc_fence_before();
       mbar_arrive(aready);
+      // prefetch the next tile's rows while the tensor core works
+      const RowIn now = cur;
+      if (t + 1 < my_tiles) cur = load_row(a, (tile + gridDim.x) * kRaysPerTile + ray, n_items, trace_state);
       // ---- hidden layers ----
       float acc_out = 0.0f;
       for (int h = 0; h < n_hidden; ++h) {
@@ -383,31 +457,32 @@ __global__ void __launch_bounds__(kTcThreads, 2) tc_mlp_kernel(TcArgs a) {
         tc_fence_after();
         const float* bias = sm.bias + size_t(h + 1) * W;
 #pragma unroll 1
-        for (int c0 = 0; c0 < W; c0 += 32) {
-          float v[32];
-          tmem_ld32(taddr + uint32_t(c0), v);
+        for (int c = 0; c < kCols; c += 16) {
+          float v[16];
+          tmem_ld16(taddr + uint32_t(c), v);
+          const int cc = col0 + c;
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
+          for (int j = 0; j < 16; ++j) {
             if (kGrad) {
-              const float z = fmaf(v[j], net.turns, bias[c0 + j]);
-              float s, cs;
-              sincos_turns(z, s, cs);  // only the value lane's result is used
+              const float z = fmaf(v[j], net.turns, bias[cc + j]);
+              float s = 0.0f, cs = 0.0f;
+              if (chain == 0) sincos_turns(z, s, cs);
               const float dphi = __shfl_sync(group_mask, net.omega * cs, lane & ~3, 32);
               v[j] = chain == 0 ? s : v[j] * dphi;
             } else {
-              v[j] = sin_turns(fmaf(v[j], net.turns, bias[c0 + j]));
+              v[j] = sin_turns(fmaf(v[j], net.turns, bias[cc + j]));
             }
           }
           if (!last) {
 #pragma unroll
-            for (int j = 0; j < 32; j += 8) {
-              *reinterpret_cast<uint4*>(&sm.a[a_off(row, c0 + j)]) =
+            for (int j = 0; j < 16; j += 8) {
+              *reinterpret_cast<uint4*>(&sm.a[a_off(row, cc + j)]) =
                   make_uint4(pack_half2(v[j], v[j + 1]), pack_half2(v[j + 2], v[j + 3]),
                              pack_half2(v[j + 4], v[j + 5]), pack_half2(v[j + 6], v[j + 7]));
             }
           } else {
 #pragma unroll
-            for (int j = 0; j < 32; ++j) acc_out = fmaf(sm.wout[c0 + j], v[j], acc_out);
+            for (int j = 0; j < 16; ++j) acc_out = fmaf(sm.wout[cc + j], v[j], acc_out);
           }
         }
         tc_fence_before();
@@ -416,22 +491,22 @@ __global__ void __launch_bounds__(kTcThreads, 2) tc_mlp_kernel(TcArgs a) {
           mbar_arrive(aready);
         }
       }
-      // ---- consumer ----
+      // ---- combine the column groups' partial output dots ----
+      if (kGroups > 1) {
+        if (eg > 0) part[(eg - 1) * kRows + row] = acc_out;
+        named_bar(1, 128 * kGroups);
+        if (eg == 0)
+          for (int g = 1; g < kGroups; ++g) acc_out += part[(g - 1) * kRows + row];
+      }
+      if (eg != 0) continue;
+      // ---- consumer (group 0) ----
       const float fval = (!kGrad || chain == 0) ? acc_out + net.bout : acc_out;
       if (a.op == kOpTrace) {
-        // forward tiles: one ray per lane
         bool conv = false, cont = false;
-        if (valid) {
-          IterArgs ia;
-          ia.lv = a.lv;
-          ia.eps = a.eps;
-          ia.t_max = a.t_max;
-          ia.iter = a.iter;
-          ia.st = a.st;
-          trace_update(ia, slot, fval, conv, cont);
-        }
-        warp_append(conv, slot, a.adv_list, a.adv_count);
-        warp_append(cont, slot, a.next_list, a.next_count);
+        if (valid)
+          tc_trace_update(a, now.slot, fval, now.p[0], now.p[1], now.p[2], now.t, now.dx, now.dy, now.dz, conv, cont);
+        warp_append(conv, now.slot, a.adv_list, a.adv_count);
+        warp_append(cont, now.slot, a.next_list, a.next_count);
       } else if (kGrad) {
         const int base = lane & ~3;
         const float gx = __shfl_sync(0xffffffffu, fval, base + 1);
@@ -449,9 +524,9 @@ __global__ void __launch_bounds__(kTcThreads, 2) tc_mlp_kernel(TcArgs a) {
               nrm[2] = 0.0f;
               defer = a.defer_fallback != 0;
             }
-            if (!defer) shade_and_write(a.sp, a.st, slot, nrm, a.rgb, a.depth, a.mask);
+            if (!defer) shade_and_write(a.sp, a.st, now.slot, nrm, a.rgb, a.depth, a.mask);
           }
-          warp_append(defer, slot, a.fb_list, a.fb_count);
+          warp_append(defer, now.slot, a.fb_list, a.fb_count);
         } else if (lead) {
           if (a.out) a.out[item] = f;
           if (a.grad) {
@@ -477,25 +552,40 @@ __global__ void __launch_bounds__(kTcThreads, 2) tc_mlp_kernel(TcArgs a) {
 
 template <int W, bool kGrad>
 bool launch_w(TcArgs& a, int n_max_items, cudaStream_t s) {
+  constexpr int kGroups = W == 64 ? 1 : 2;
+  constexpr int kThreads = 64 + 128 * kGroups;
+  auto kernel = tc_mlp_kernel<W, kGrad, kGroups>;
   const size_t smem = tc_smem_bytes(W, a.net.n_layers);
-  static int configured_smem = 0;
+  static size_t configured_smem = 0;
   static int per_sm = 0;
-  if (configured_smem != int(smem)) {
-    if (cudaFuncSetAttribute(tc_mlp_kernel<W, kGrad>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) !=
-        cudaSuccess)
+  static int sms = 0;
+  if (configured_smem != smem) {
+    if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess)
       return false;
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, tc_mlp_kernel<W, kGrad>, kTcThreads, smem);
-    configured_smem = int(smem);
+    cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kThreads, smem) != cudaSuccess) occ = 1;
+    // Residency from first principles (228 KB SMEM incl. 1 KB per CTA, 64K registers, TMEM
+    // columns); the occupancy API is reported for reference only.
+    cudaFuncAttributes fa;
+    cudaFuncGetAttributes(&fa, kernel);
+    const int by_smem = int((228 * 1024) / (smem + 1024));
+    const int by_regs = 65536 / (std::max(fa.numRegs, 1) * kThreads);
+    per_sm = std::max(1, std::min(by_smem, by_regs));
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    configured_smem = smem;
+    if (getenv("NSDF_DEBUG_TC"))
+      fprintf(stderr, "tc_mlp_kernel<%d,%d,%d>: smem %zu B, regs %d, %d CTAs/SM (occupancy API %d)\n", W,
+              int(kGrad), kGroups, smem, fa.numRegs, per_sm, occ);
   }
   const int tmem_limit = 512 / (W < 32 ? 32 : W);
-  int sms = 0, dev = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   const int per = std::max(1, std::min(per_sm, tmem_limit));
   constexpr int kRaysPerTile = kGrad ? kRows / 4 : kRows;
   const int tiles = (n_max_items + kRaysPerTile - 1) / kRaysPerTile;
   const int grid = std::max(1, std::min(tiles, sms * per));
-  tc_mlp_kernel<W, kGrad><<<grid, kTcThreads, smem, s>>>(a);
+  kernel<<<grid, kThreads, smem, s>>>(a);
   return cudaGetLastError() == cudaSuccess;
 }
 

@@ -1,0 +1,113 @@
+"""GPU parity of the tcgen05 fast mode (FP16 operands, FP32 accumulation) against the
+reference CPU path on identical weights and rays, with the BASELINE tolerances
+(SURVEY.md §8d): hit/miss mask agreement >= 99.9%, |dt| <= 1e-3 on common hits (scene
+scale 1), normals within 0.5 deg — end to end and at identical points."""
+import os
+
+import numpy as np
+import pytest
+
+from conftest import ASSETS, random_net, records_np
+
+pytestmark = pytest.mark.gpu
+
+MASK_MIN = 0.999
+DT_MAX = 1e-3        # BASELINE depth tolerance
+ANGLE_MAX = 0.5      # degrees
+
+
+def _fixture(name):
+    p = os.path.join(ASSETS, name)
+    if not os.path.exists(p):
+        pytest.skip(f"fixture {name} not generated")
+    return p
+
+
+@pytest.fixture(scope="module")
+def fast():
+    from paper_2201_09147_b200.engine import Context
+    c = Context(0, "fp16")
+    yield c
+    c.close()
+
+
+def angle_deg(a, b):
+    a = a / np.linalg.norm(a, axis=0, keepdims=True)
+    b = b / np.linalg.norm(b, axis=0, keepdims=True)
+    return np.degrees(np.arccos(np.clip((a * b).sum(0), -1.0, 1.0)))
+
+
+@pytest.mark.parametrize("name", ["64x1", "128x2", "256x3"])
+def test_fast_mlp_close_to_oracle(ctx, fast, name):
+    from paper_2201_09147_b200.manifest import load_sdfnet
+    net = load_sdfnet(_fixture(f"torus_w30_{name}.sdfnet"))
+    pts = np.random.default_rng(1).uniform(-1, 1, (3, 20000)).astype(np.float32)
+    d0, g0 = ctx.eval_grad(ctx.upload(net), pts)
+    h = fast.upload(net)
+    d1, g1 = fast.eval_grad(h, pts)
+    assert np.array_equal(fast.eval(h, pts), d1)  # forward-only and fused tiles agree
+    near = np.abs(d0) < 0.05
+    assert np.abs(d1 - d0).max() < 2e-3, np.abs(d1 - d0).max()
+    assert np.percentile(angle_deg(g0[:, near], g1[:, near]), 99.9) < ANGLE_MAX
+
+
+@pytest.mark.parametrize("width,hidden", [(64, 1), (128, 2), (256, 3)])
+def test_fast_mlp_random_init(ctx, fast, width, hidden):
+    net = random_net(width, hidden, seed=40 + width)
+    pts = np.random.default_rng(2).uniform(-1.2, 1.2, (3, 3000)).astype(np.float32)
+    d0, g0 = ctx.eval_grad(ctx.upload(net), pts)
+    d1, g1 = fast.eval_grad(fast.upload(net), pts)
+    assert np.abs(d1 - d0).max() < 5e-4
+    assert np.median(angle_deg(g0, g1)) < 0.1
+
+
+def _trace_and_normals(c, ds, cam, cfg, normal_idx):
+    recs, st = c.trace_image(ds.levels(), cam, cfg)
+    r = records_np(recs)
+    hit = r["hit"] == 1
+    pts = np.ascontiguousarray(r["point"][hit].T)
+    nrm, _, _ = c.normal_map(ds.handles[normal_idx], pts, ds.seq.deltas[normal_idx])
+    return r, hit, pts, nrm
+
+
+@pytest.mark.parametrize("budgets", [(20, 5, 5), (40, 20, 20), (0, 0, 40)])
+def test_fast_trace_parity_torus(ctx, fast, budgets):
+    """Mask, depth and end-to-end normal parity of the fast mode vs the bit-exact oracle
+    mode (itself pinned bitwise to the reference in test_gpu_parity.py)."""
+    from paper_2201_09147_b200.abi import TraceConfig, standard_camera
+    from paper_2201_09147_b200.engine import DeviceSequence
+    from paper_2201_09147_b200.manifest import load_manifest
+    seq = load_manifest(_fixture("torus_w30.nest"))
+    cam = standard_camera(480, 270)
+    cfg = TraceConfig(budgets)
+    r0, hit0, p0, n0 = _trace_and_normals(ctx, DeviceSequence(ctx, seq), cam, cfg, 2)
+    r1, hit1, p1, n1 = _trace_and_normals(fast, DeviceSequence(fast, seq), cam, cfg, 2)
+    agree = np.mean(hit0 == hit1)
+    both = hit0 & hit1
+    dt = np.abs(r0["t"][both] - r1["t"][both])
+    # end-to-end normals on common hits
+    idx0 = np.cumsum(hit0) - 1
+    idx1 = np.cumsum(hit1) - 1
+    ang = angle_deg(n0[:, idx0[both]], n1[:, idx1[both]])
+    print(f"budgets {budgets}: mask {agree:.5f}, hits {hit0.sum()}/{hit1.sum()}, dt max {dt.max():.2e} "
+          f"p99.9 {np.percentile(dt, 99.9):.2e}, normals max {ang.max():.3f} p99.9 {np.percentile(ang, 99.9):.3f}")
+    assert agree >= MASK_MIN
+    assert np.percentile(dt, 99.9) <= DT_MAX
+    assert np.percentile(ang, 99.9) <= ANGLE_MAX
+
+
+def test_fast_render_matches_oracle_mode(ctx, fast):
+    from paper_2201_09147_b200.abi import ShadeConfig, TraceConfig, standard_camera
+    from paper_2201_09147_b200.engine import DeviceSequence
+    from paper_2201_09147_b200.manifest import load_manifest
+    seq = load_manifest(_fixture("torus_w30.nest"))
+    cam = standard_camera(320, 180)
+    cfg = TraceConfig((20, 5, 5))
+    shade = ShadeConfig(specular=0.3)
+    for src in (0, 1):
+        rgb0, d0, m0, _ = ctx.render(DeviceSequence(ctx, seq).levels(), cam, cfg, shade, src)
+        rgb1, d1, m1, st = fast.render(DeviceSequence(fast, seq).levels(), cam, cfg, shade, src)
+        assert np.mean(m0 == m1) >= MASK_MIN
+        both = (m0 == 1) & (m1 == 1)
+        assert np.percentile(np.abs(d0 - d1)[both], 99.9) <= DT_MAX
+        assert np.mean(np.abs(rgb0 - rgb1)[both]) < 5e-3
