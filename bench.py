@@ -40,7 +40,7 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--mode", default=os.environ.get("NSDF_MODE", "fp16"), choices=["fp16", "fp32"])
+    ap.add_argument("--mode", default=os.environ.get("NSDF_MODE", "fp16"), choices=["fp16", "fp16low", "fp32"])
     ap.add_argument("--width", type=int, default=1920)
     ap.add_argument("--height", type=int, default=1080)
     ap.add_argument("--budgets", default="20,5,5")
@@ -302,7 +302,7 @@ def main():
             "metric": METRIC, "value": value, "unit": "Mrays/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_frame, "higher_is_better": True,
             "scaling": "strong" if world > 1 else "weak", "vs_baseline": None,
-            "dtype": "fp16-tensor/fp32-accum" if args.mode == "fp16" else "f32",
+            "dtype": {"fp16": "split-fp16 tensor (3 MMA terms) / fp32 accum", "fp16low": "fp16 tensor / fp32 accum", "fp32": "f32"}[args.mode],
             "data": "synthetic camera rays; committed fitted SIREN weights (assets/)",
             "config": {"workload": f"config2: nested 64x1>128x2>256x3 SIREN (torus, omega0=30), {W}x{H}, "
                                    f"budgets ({args.budgets}), {args.normals} analytic normals, specular 0.3",

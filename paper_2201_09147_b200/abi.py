@@ -15,7 +15,7 @@ MAX_LEVELS = 8
 MAX_LIGHTS = 8
 
 OK, ERR_CONTRACT, ERR_CONFIG, ERR_VALIDATION, ERR_PARSE, ERR_DIVERGENCE, ERR_DEVICE = range(7)
-MODE_FP32_ORACLE, MODE_FP16_FAST = 0, 1
+MODE_FP32_ORACLE, MODE_FP16_FAST, MODE_FP16_LOW = 0, 1, 2
 ACT_SINE, ACT_IDENTITY = 0, 1
 FIELD_SPHERE, FIELD_TORUS, FIELD_BOX = 1, 2, 3
 NORMALS_OWN, NORMALS_MAPPED = 0, 1

@@ -75,7 +75,10 @@ struct nsdf_ctx {
 
 namespace {
 
-Mode mode_of(const nsdf_ctx* c) { return c->mode == NSDF_MODE_FP16_FAST ? Mode::Fp16Fast : Mode::Fp32Oracle; }
+Mode mode_of(const nsdf_ctx* c) {
+  return c->mode == NSDF_MODE_FP16_FAST ? Mode::Fp16Fast : c->mode == NSDF_MODE_FP16_LOW ? Mode::Fp16Low
+                                                                                          : Mode::Fp32Oracle;
+}
 
 int find_field(nsdf_ctx* c, nsdf_field h, FieldRec** out) {
   auto it = c->fields.find(h);
@@ -361,7 +364,8 @@ int nsdf_cuda_destroy(nsdf_ctx* c) {
 
 int nsdf_cuda_set_mode(nsdf_ctx* c, int mode) {
   if (!c) return fail(NSDF_ERR_CONTRACT, "context is null");
-  if (mode != NSDF_MODE_FP32_ORACLE && mode != NSDF_MODE_FP16_FAST) return fail(NSDF_ERR_CONFIG, "unknown mode");
+  if (mode != NSDF_MODE_FP32_ORACLE && mode != NSDF_MODE_FP16_FAST && mode != NSDF_MODE_FP16_LOW)
+    return fail(NSDF_ERR_CONFIG, "unknown mode");
   std::lock_guard<std::mutex> lk(c->mu);
   c->mode = mode;
   return NSDF_OK;
@@ -481,17 +485,29 @@ int nsdf_cuda_upload_mlp(nsdf_ctx* c, int n_layers, const int32_t* rows, const i
     for (int l = 1; ok && l + 1 < n_layers; ++l) ok = rows[l] == W && cols[l] == W;
     if (ok) {
       const int H = n_layers - 2;
-      std::vector<__half> wq(size_t(H) * W * W);
+      std::vector<__half> wq(size_t(H) * 2 * W * W);
       std::vector<float> bias(size_t(n_layers - 1) * W);
       size_t o = 0;
       for (int l = 0; l < n_layers; ++l) {
         const size_t nw = size_t(rows[l]) * cols[l];
         if (l >= 1 && l + 1 < n_layers) {
-          __half* dst = wq.data() + size_t(l - 1) * W * W;
+          // Split precision: W * 2^k = hi + lo (both fp16); 2^k keeps lo out of the
+          // subnormal range and is undone in the epilogue (wscale).
+          double mx = 0;
+          for (size_t i = 0; i < nw; ++i) mx = std::max(mx, std::fabs(double(float(packed[o + i]))));
+          int k = 0;
+          while (k < 24 && mx * std::ldexp(1.0, k + 1) <= 16384.0) ++k;
+          n.wscale[l - 1] = float(std::ldexp(1.0, -k));
+          __half* hi = wq.data() + size_t(l - 1) * 2 * W * W;
+          __half* lo = hi + size_t(W) * W;
           for (int r = 0; r < W; ++r)
-            for (int k = 0; k < W; ++k)
-              dst[size_t((k / 8) * (W / 8) + r / 8) * 64 + (r % 8) * 8 + k % 8] =
-                  __float2half_rn(float(packed[o + size_t(r) * W + k]));
+            for (int kk = 0; kk < W; ++kk) {
+              const float v = std::ldexp(float(packed[o + size_t(r) * W + kk]), k);
+              const __half h = __float2half_rn(v);
+              const size_t at = size_t((kk / 8) * (W / 8) + r / 8) * 64 + (r % 8) * 8 + kk % 8;
+              hi[at] = h;
+              lo[at] = __float2half_rn(v - __half2float(h));
+            }
         }
         o += nw;
         if (l + 1 < n_layers)

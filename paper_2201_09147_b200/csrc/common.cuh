@@ -34,7 +34,8 @@ struct DevNet {
   const float* b[kMaxLayers];
   // Fast-mode (tcgen05) copy, built at upload when tc-eligible (mlp_tc.cu):
   int tc_ok;
-  const uint16_t* wq;      // hidden layers, fp16, UMMA canonical K-major chunked layout
+  const uint16_t* wq;      // hidden layers [h][hi | lo][W*W] fp16, UMMA canonical K-major layout
+  float wscale[kMaxLayers];  // hidden layer h is stored scaled by 1/wscale[h] (a power of 2)
   const float* bias_cat;   // biases of layers 0 .. L-2, [L-1][width]
   float bout;              // output bias
 };

@@ -365,8 +365,8 @@ TraceResult run_trace(Mode mode, const std::vector<LevelDesc>& levels, float eps
       a.next_list = fb.list[pong];
       a.next_count = it_counts + iter;
       bool done = false;
-      if (mode == Mode::Fp16Fast && lv.field.kind == kFieldMlp && tc_supported(lv.field.net)) {
-        done = tc_trace_iter(a.lv, a.eps, a.t_max, a.iter, a.in_list, a.in_count, a.next_list, a.next_count,
+      if (mode_tc(mode) && lv.field.kind == kFieldMlp && tc_supported(lv.field.net)) {
+        done = tc_trace_iter(mode_terms(mode), a.lv, a.eps, a.t_max, a.iter, a.in_list, a.in_count, a.next_list, a.next_count,
                              a.adv_list, a.adv_count, a.st, n_max, s);
       }
       if (!done) {
@@ -526,8 +526,8 @@ int launch_normals_shade(Mode mode, const DevField& nf, float time, const int* l
                          const RayState& st, const ShadeParams& sp, bool defer_fallback, int* fb_list, int* fb_count,
                          float* rgb, float* depth, uint8_t* mask, cudaStream_t s) {
   NormalArgs a{nf, time, list, count, st, sp, defer_fallback ? 1 : 0, fb_list, fb_count, rgb, depth, mask};
-  if (mode == Mode::Fp16Fast && nf.kind == kFieldMlp && tc_supported(nf.net)) {
-    if (tc_normals_shade(nf, time, list, count, n_max, st, sp, defer_fallback, fb_list, fb_count, rgb, depth, mask,
+  if (mode_tc(mode) && nf.kind == kFieldMlp && tc_supported(nf.net)) {
+    if (tc_normals_shade(mode_terms(mode), nf, time, list, count, n_max, st, sp, defer_fallback, fb_list, fb_count, rgb, depth, mask,
                          s))
       return 1;
   }
@@ -613,8 +613,8 @@ static void launch_eval_impl(const DevField& f, const float* pts, int rows, int 
 void launch_eval(Mode mode, const DevField& f, const float* pts, int rows, int k, float time, float* out, float* grad,
                  cudaStream_t s) {
   if (k <= 0) return;
-  if (mode == Mode::Fp16Fast && f.kind == kFieldMlp && tc_supported(f.net) &&
-      tc_eval(f, pts, rows, k, time, out, grad, s))
+  if (mode_tc(mode) && f.kind == kFieldMlp && tc_supported(f.net) &&
+      tc_eval(mode_terms(mode), f, pts, rows, k, time, out, grad, s))
     return;
   if (grad)
     launch_eval_impl<true>(f, pts, rows, k, time, out, grad, 0.0, nullptr, nullptr, 0, s);

@@ -81,7 +81,9 @@ struct Profiler {
 };
 
 // Which kernel family runs the MLP tiles.
-enum class Mode : int { Fp32Oracle = 0, Fp16Fast = 1 };
+enum class Mode : int { Fp32Oracle = 0, Fp16Fast = 1, Fp16Low = 2 };
+inline int mode_terms(Mode m) { return m == Mode::Fp16Low ? 1 : 3; }
+inline bool mode_tc(Mode m) { return m != Mode::Fp32Oracle; }
 
 struct TraceResult {
   int* hit_list;        // device: slots that converged at the final level

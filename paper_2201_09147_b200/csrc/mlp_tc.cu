@@ -146,6 +146,12 @@ __device__ __forceinline__ uint32_t pack_half2(float a, float b) {
   __half2 h = __floats2half2_rn(a, b);
   return *reinterpret_cast<uint32_t*>(&h);
 }
+// Low parts of a split-precision pair: fp16(x - float(fp16(x))).
+__device__ __forceinline__ uint32_t pack_half2_lo(float a, float b, uint32_t hi) {
+  const __half2 h = *reinterpret_cast<const __half2*>(&hi);
+  const float2 f = __half22float2(h);
+  return pack_half2(a - f.x, b - f.y);
+}
 
 // ---- kernel parameters -------------------------------------------------------------------
 enum TcOp : int { kOpTrace = 0, kOpNormals = 1, kOpEval = 2 };
@@ -154,7 +160,8 @@ struct TcNet {
   int n_layers, width, input_dim;
   float turns;                      // omega / 2pi
   float omega;
-  const __half* wq;                 // hidden-layer weights, canonical chunked layout
+  const __half* wq;                 // hidden layers [h][hi | lo][W*W], canonical chunked layout
+  float wscale[kMaxLayers];         // 2^-k: hidden weights are stored scaled by 2^k
   const float* w0;                  // layer 0, row-major W x input_dim (fp32)
   const float* b;                   // biases, [n_layers-1][W] (fp32)
   const float* wout;                // output row (fp32), W
@@ -164,6 +171,7 @@ struct TcNet {
 struct TcArgs {
   TcNet net;
   int op;
+  int terms;  // 3 = split-fp16 (A_hi.W_hi + A_lo.W_hi + A_hi.W_lo), 1 = plain fp16
   // trace
   LevelDesc lv;
   float eps, t_max;
@@ -194,36 +202,41 @@ struct TcArgs {
 // Dynamic shared-memory carve-up (sized for the net's layer count, so two 256-wide CTAs
 // fit one SM).
 struct TcSmem {
-  __half* a;            // [128 x W] A operand
+  __half* a;            // [128 x W] A operand (fp16 hi part)
+  __half* alo;          // [128 x W] A low part (split precision only)
   __half* wst;          // [kStages][W * kKC] streamed weight chunks
   float* w0t;           // [W x input_dim] layer-0 weights * omega/2pi
   float* w0;            // [W x input_dim] layer-0 weights
   float* bias;          // [(L-1) x W] biases * omega/2pi
   float* wout;          // [W]
-  float* part;          // [kRows] partial output dots of column group 1
+  float* part;          // [3][kRows] partial output dots of column groups 1..3
   uint64_t* bars;       // full[kStages], empty[kStages], aready, dfull
   uint32_t* tmem_base;
 };
 
-__host__ __device__ inline size_t tc_smem_bytes(int W, int L) {
+__host__ __device__ inline size_t tc_smem_bytes(int W, int L, int terms) {
+  const int nw = terms == 3 ? 2 : 1;
   size_t b = 0;
-  b += size_t(kRows) * W * 2;
-  b += size_t(kStages) * W * kKC * 2;
+  b += size_t(kRows) * W * 2 * nw;
+  b += size_t(kStages) * W * kKC * 2 * nw;
   b += size_t(W) * 4 * 4 * 2;
   b += size_t(L - 1) * W * 4;
   b += size_t(W) * 4;
-  b += size_t(kRows) * 4;
+  b += size_t(3) * kRows * 4;
   b += (2 * kStages + 2) * 8 + 16;
   return b + 1024;  // alignment slack
 }
 
-__device__ inline TcSmem tc_carve(uint8_t* raw, int W, int L) {
+__device__ inline TcSmem tc_carve(uint8_t* raw, int W, int L, int terms) {
+  const int nw = terms == 3 ? 2 : 1;
   uintptr_t p = (reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023);
   TcSmem s;
   s.a = reinterpret_cast<__half*>(p);
   p += size_t(kRows) * W * 2;
+  s.alo = reinterpret_cast<__half*>(p);
+  if (nw == 2) p += size_t(kRows) * W * 2;
   s.wst = reinterpret_cast<__half*>(p);
-  p += size_t(kStages) * W * kKC * 2;
+  p += size_t(kStages) * W * kKC * 2 * nw;
   s.w0t = reinterpret_cast<float*>(p);
   p += size_t(W) * 4 * 4;
   s.w0 = reinterpret_cast<float*>(p);
@@ -233,7 +246,7 @@ __device__ inline TcSmem tc_carve(uint8_t* raw, int W, int L) {
   s.wout = reinterpret_cast<float*>(p);
   p += size_t(W) * 4;
   s.part = reinterpret_cast<float*>(p);
-  p += size_t(kRows) * 4;
+  p += size_t(3) * kRows * 4;
   s.bars = reinterpret_cast<uint64_t*>((p + 7) & ~uintptr_t(7));
   s.tmem_base = reinterpret_cast<uint32_t*>(s.bars + 2 * kStages + 2);
   return s;
@@ -302,14 +315,16 @@ __device__ __forceinline__ void named_bar(int id, int threads) {
 
 // kGroups column groups of 4 epilogue warps each: group g owns columns
 // [g*W/kGroups, (g+1)*W/kGroups) of every layer (TMEM lane quadrant = warp % 4).
-template <int W, bool kGrad, int kGroups>
-__global__ void __launch_bounds__(64 + 128 * kGroups, (W == 64 ? 3 : 2)) tc_mlp_kernel(TcArgs a) {
+template <int W, bool kGrad, int kGroups, int kTerms>
+__global__ void __launch_bounds__(64 + 128 * kGroups, (W == 64 ? 3 : (kGroups > 2 ? 1 : 2)))
+    tc_mlp_kernel(TcArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   constexpr int kThreads = 64 + 128 * kGroups;
   constexpr int kCols = W / kGroups;  // columns per epilogue group
   const TcNet& net = a.net;
   const int L = net.n_layers;
-  const TcSmem sm = tc_carve(smem_raw, W, L);
+  const TcSmem sm = tc_carve(smem_raw, W, L, kTerms);
+  constexpr int kNW = kTerms == 3 ? 2 : 1;  // weight parts per stage (hi [, lo])
   uint64_t* full = sm.bars;
   uint64_t* empty = sm.bars + kStages;
   uint64_t* aready = sm.bars + 2 * kStages;
@@ -321,6 +336,7 @@ __global__ void __launch_bounds__(64 + 128 * kGroups, (W == 64 ? 3 : 2)) tc_mlp_
   constexpr int kRaysPerTile = kGrad ? kRows / 4 : kRows;
   constexpr int kChunks = W / kKC;
   constexpr uint32_t kChunkBytes = uint32_t(W) * kKC * 2;
+  constexpr size_t kStageHalves = size_t(W) * kKC * kNW;
 
   const int n_items = a.op == kOpEval ? a.k : *a.in_count;
   const int n_tiles = (n_items + kRaysPerTile - 1) / kRaysPerTile;
@@ -358,6 +374,7 @@ __global__ void __launch_bounds__(64 + 128 * kGroups, (W == 64 ? 3 : 2)) tc_mlp_
     if (lane == 0) {
       const uint32_t idesc = umma_idesc(W);
       const uint32_t a_base = smem_addr(sm.a);
+      const uint32_t alo_base = smem_addr(sm.alo);
       uint32_t chunk_iter = 0, aready_phase = 0;
       for (int t = 0; t < my_tiles; ++t) {
         for (int h = 0; h < n_hidden; ++h) {
@@ -368,13 +385,20 @@ __global__ void __launch_bounds__(64 + 128 * kGroups, (W == 64 ? 3 : 2)) tc_mlp_
             const int s = chunk_iter % kStages;
             mbar_wait(&full[s], (chunk_iter / kStages) & 1);
             tc_fence_after();
-            const uint32_t b_base = smem_addr(sm.wst + size_t(s) * W * kKC);
+            const uint32_t b_base = smem_addr(sm.wst + size_t(s) * kStageHalves);
 #pragma unroll
             for (int ks = 0; ks < kKC / 16; ++ks) {
               const int kg = c * (kKC / 8) + ks * 2;  // first 8-element k group of this K=16 step
-              const uint64_t ad = umma_desc(a_base + uint32_t(kg) * (kRows / 8) * 128, kRows * 16, 128);
-              const uint64_t bd = umma_desc(b_base + uint32_t(ks * 2) * (W / 8) * 128, W * 16, 128);
+              const uint32_t aoff = uint32_t(kg) * (kRows / 8) * 128, boff = uint32_t(ks * 2) * (W / 8) * 128;
+              const uint64_t ad = umma_desc(a_base + aoff, kRows * 16, 128);
+              const uint64_t bd = umma_desc(b_base + boff, W * 16, 128);
               tc_mma(tmem, ad, bd, idesc, (c | ks) != 0);
+              if (kTerms == 3) {  // split precision: + A_lo.W_hi + A_hi.W_lo
+                const uint64_t adl = umma_desc(alo_base + aoff, kRows * 16, 128);
+                const uint64_t bdl = umma_desc(b_base + uint32_t(W * kKC * 2) + boff, W * 16, 128);
+                tc_mma(tmem, adl, bd, idesc, 1);
+                tc_mma(tmem, ad, bdl, idesc, 1);
+              }
             }
             tc_commit(&empty[s]);  // frees the weight stage once these MMAs retire
           }
@@ -388,12 +412,15 @@ __global__ void __launch_bounds__(64 + 128 * kGroups, (W == 64 ? 3 : 2)) tc_mlp_
       uint32_t chunk_iter = 0;
       for (int t = 0; t < my_tiles; ++t) {
         for (int h = 0; h < n_hidden; ++h) {
-          const __half* lw = reinterpret_cast<const __half*>(net.wq) + size_t(h) * W * W;
+          const __half* lw = reinterpret_cast<const __half*>(net.wq) + size_t(h) * 2 * W * W;
           for (int c = 0; c < kChunks; ++c, ++chunk_iter) {
             const int s = chunk_iter % kStages;
             mbar_wait(&empty[s], ((chunk_iter / kStages) & 1) ^ 1);
-            mbar_expect_tx(&full[s], kChunkBytes);
-            bulk_g2s(sm.wst + size_t(s) * W * kKC, lw + size_t(c) * (W * kKC), kChunkBytes, &full[s]);
+            mbar_expect_tx(&full[s], kChunkBytes * kNW);
+            bulk_g2s(sm.wst + size_t(s) * kStageHalves, lw + size_t(c) * (W * kKC), kChunkBytes, &full[s]);
+            if (kTerms == 3)
+              bulk_g2s(sm.wst + size_t(s) * kStageHalves + size_t(W) * kKC, lw + size_t(W) * W + size_t(c) * (W * kKC),
+                       kChunkBytes, &full[s]);
           }
         }
       }
@@ -418,7 +445,7 @@ __global__ void __launch_bounds__(64 + 128 * kGroups, (W == 64 ? 3 : 2)) tc_mlp_
       // ---- layer 0: FP32 FFMA, sin -> fp16 A (this group's columns) ----
 #pragma unroll 1
       for (int n0 = col0; n0 < col0 + kCols; n0 += 8) {
-        uint32_t pk[4];
+        uint32_t pk[4], pl[4];
 #pragma unroll
         for (int j = 0; j < 8; j += 2) {
           float o[2];
@@ -439,8 +466,10 @@ __global__ void __launch_bounds__(64 + 128 * kGroups, (W == 64 ? 3 : 2)) tc_mlp_
             }
           }
           pk[j / 2] = pack_half2(o[0], o[1]);
+          if (kTerms == 3) pl[j / 2] = pack_half2_lo(o[0], o[1], pk[j / 2]);
         }
         *reinterpret_cast<uint4*>(&sm.a[a_off(row, n0)]) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+        if (kTerms == 3) *reinterpret_cast<uint4*>(&sm.alo[a_off(row, n0)]) = make_uint4(pl[0], pl[1], pl[2], pl[3]);
       }
       fence_proxy_async();
       tc_fence_before();
@@ -456,6 +485,8 @@ __global__ void __launch_bounds__(64 + 128 * kGroups, (W == 64 ? 3 : 2)) tc_mlp_
         dfull_phase ^= 1;
         tc_fence_after();
         const float* bias = sm.bias + size_t(h + 1) * W;
+        const float zs = net.turns * net.wscale[h];  // undo the 2^k weight scaling
+        const float dscale = net.omega * net.wscale[h];
 #pragma unroll 1
         for (int c = 0; c < kCols; c += 16) {
           float v[16];
@@ -464,21 +495,26 @@ __global__ void __launch_bounds__(64 + 128 * kGroups, (W == 64 ? 3 : 2)) tc_mlp_
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
             if (kGrad) {
-              const float z = fmaf(v[j], net.turns, bias[cc + j]);
+              const float z = fmaf(v[j], zs, bias[cc + j]);
               float s = 0.0f, cs = 0.0f;
               if (chain == 0) sincos_turns(z, s, cs);
-              const float dphi = __shfl_sync(group_mask, net.omega * cs, lane & ~3, 32);
+              // tangent rows: G = (W.G_prev) * omega cos(z); D carries the 2^k weight scale
+              const float dphi = __shfl_sync(group_mask, dscale * cs, lane & ~3, 32);
               v[j] = chain == 0 ? s : v[j] * dphi;
             } else {
-              v[j] = sin_turns(fmaf(v[j], net.turns, bias[cc + j]));
+              v[j] = sin_turns(fmaf(v[j], zs, bias[cc + j]));
             }
           }
           if (!last) {
 #pragma unroll
             for (int j = 0; j < 16; j += 8) {
-              *reinterpret_cast<uint4*>(&sm.a[a_off(row, cc + j)]) =
-                  make_uint4(pack_half2(v[j], v[j + 1]), pack_half2(v[j + 2], v[j + 3]),
-                             pack_half2(v[j + 4], v[j + 5]), pack_half2(v[j + 6], v[j + 7]));
+              const uint32_t h0 = pack_half2(v[j], v[j + 1]), h1 = pack_half2(v[j + 2], v[j + 3]),
+                             h2 = pack_half2(v[j + 4], v[j + 5]), h3 = pack_half2(v[j + 6], v[j + 7]);
+              *reinterpret_cast<uint4*>(&sm.a[a_off(row, cc + j)]) = make_uint4(h0, h1, h2, h3);
+              if (kTerms == 3)
+                *reinterpret_cast<uint4*>(&sm.alo[a_off(row, cc + j)]) =
+                    make_uint4(pack_half2_lo(v[j], v[j + 1], h0), pack_half2_lo(v[j + 2], v[j + 3], h1),
+                               pack_half2_lo(v[j + 4], v[j + 5], h2), pack_half2_lo(v[j + 6], v[j + 7], h3));
             }
           } else {
 #pragma unroll
@@ -550,12 +586,12 @@ __global__ void __launch_bounds__(64 + 128 * kGroups, (W == 64 ? 3 : 2)) tc_mlp_
   }
 }
 
-template <int W, bool kGrad>
+template <int W, bool kGrad, int kTerms>
 bool launch_w(TcArgs& a, int n_max_items, cudaStream_t s) {
-  constexpr int kGroups = W == 64 ? 1 : 2;
+  constexpr int kGroups = W == 64 ? 1 : (W == 256 && kTerms == 3 ? 4 : 2);
   constexpr int kThreads = 64 + 128 * kGroups;
-  auto kernel = tc_mlp_kernel<W, kGrad, kGroups>;
-  const size_t smem = tc_smem_bytes(W, a.net.n_layers);
+  auto kernel = tc_mlp_kernel<W, kGrad, kGroups, kTerms>;
+  const size_t smem = tc_smem_bytes(W, a.net.n_layers, kTerms);
   static size_t configured_smem = 0;
   static int per_sm = 0;
   static int sms = 0;
@@ -577,8 +613,8 @@ bool launch_w(TcArgs& a, int n_max_items, cudaStream_t s) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     configured_smem = smem;
     if (getenv("NSDF_DEBUG_TC"))
-      fprintf(stderr, "tc_mlp_kernel<%d,%d,%d>: smem %zu B, regs %d, %d CTAs/SM (occupancy API %d)\n", W,
-              int(kGrad), kGroups, smem, fa.numRegs, per_sm, occ);
+      fprintf(stderr, "tc_mlp_kernel<%d,%d,%d,%d>: smem %zu B, regs %d, %d CTAs/SM (occupancy API %d)\n", W,
+              int(kGrad), kGroups, kTerms, smem, fa.numRegs, per_sm, occ);
   }
   const int tmem_limit = 512 / (W < 32 ? 32 : W);
   const int per = std::max(1, std::min(per_sm, tmem_limit));
@@ -589,14 +625,19 @@ bool launch_w(TcArgs& a, int n_max_items, cudaStream_t s) {
   return cudaGetLastError() == cudaSuccess;
 }
 
-template <bool kGrad>
-bool launch_any(TcArgs& a, int n_max_items, cudaStream_t s) {
+template <bool kGrad, int kTerms>
+bool launch_terms(TcArgs& a, int n_max_items, cudaStream_t s) {
   switch (a.net.width) {
-    case 64: return launch_w<64, kGrad>(a, n_max_items, s);
-    case 128: return launch_w<128, kGrad>(a, n_max_items, s);
-    case 256: return launch_w<256, kGrad>(a, n_max_items, s);
+    case 64: return launch_w<64, kGrad, kTerms>(a, n_max_items, s);
+    case 128: return launch_w<128, kGrad, kTerms>(a, n_max_items, s);
+    case 256: return launch_w<256, kGrad, kTerms>(a, n_max_items, s);
     default: return false;
   }
+}
+
+template <bool kGrad>
+bool launch_any(TcArgs& a, int n_max_items, cudaStream_t s) {
+  return a.terms == 3 ? launch_terms<kGrad, 3>(a, n_max_items, s) : launch_terms<kGrad, 1>(a, n_max_items, s);
 }
 
 TcNet tc_net(const DevNet& n) {
@@ -607,6 +648,7 @@ TcNet tc_net(const DevNet& n) {
   t.omega = n.omega;
   t.turns = n.omega * kInv2Pi;
   t.wq = reinterpret_cast<const __half*>(n.wq);
+  for (int l = 0; l < kMaxLayers; ++l) t.wscale[l] = n.wscale[l];
   t.w0 = n.w[0];
   t.b = n.bias_cat;
   t.wout = n.w[n.n_layers - 1];
@@ -618,10 +660,11 @@ TcNet tc_net(const DevNet& n) {
 
 bool tc_supported(const DevNet& n) { return n.tc_ok != 0; }
 
-bool tc_trace_iter(const LevelDesc& lv, float eps, float t_max, int iter, const int* in_list, const int* in_count,
-                   int* next_list, int* next_count, int* adv_list, int* adv_count, const RayState& st, int n_max,
-                   cudaStream_t s) {
+bool tc_trace_iter(int terms, const LevelDesc& lv, float eps, float t_max, int iter, const int* in_list,
+                   const int* in_count, int* next_list, int* next_count, int* adv_list, int* adv_count,
+                   const RayState& st, int n_max, cudaStream_t s) {
   TcArgs a{};
+  a.terms = terms;
   a.net = tc_net(lv.field.net);
   a.op = kOpTrace;
   a.lv = lv;
@@ -639,10 +682,11 @@ bool tc_trace_iter(const LevelDesc& lv, float eps, float t_max, int iter, const 
   return launch_any<false>(a, n_max, s);
 }
 
-bool tc_normals_shade(const DevField& nf, float time, const int* list, const int* count, int n_max,
+bool tc_normals_shade(int terms, const DevField& nf, float time, const int* list, const int* count, int n_max,
                       const RayState& st, const ShadeParams& sp, bool defer_fallback, int* fb_list, int* fb_count,
                       float* rgb, float* depth, uint8_t* mask, cudaStream_t s) {
   TcArgs a{};
+  a.terms = terms;
   a.net = tc_net(nf.net);
   a.op = kOpNormals;
   a.in_list = list;
@@ -659,9 +703,10 @@ bool tc_normals_shade(const DevField& nf, float time, const int* list, const int
   return launch_any<true>(a, n_max, s);
 }
 
-bool tc_eval(const DevField& f, const float* pts, int rows, int k, float time, float* out, float* grad,
+bool tc_eval(int terms, const DevField& f, const float* pts, int rows, int k, float time, float* out, float* grad,
              cudaStream_t s) {
   TcArgs a{};
+  a.terms = terms;
   a.net = tc_net(f.net);
   a.op = kOpEval;
   a.pts = pts;

@@ -7,13 +7,13 @@
 
 namespace nsdf_b200 {
 
-bool tc_trace_iter(const LevelDesc& lv, float eps, float t_max, int iter, const int* in_list, const int* in_count,
+bool tc_trace_iter(int terms, const LevelDesc& lv, float eps, float t_max, int iter, const int* in_list, const int* in_count,
                    int* next_list, int* next_count, int* adv_list, int* adv_count, const RayState& st, int n_max,
                    cudaStream_t s);
-bool tc_normals_shade(const DevField& nf, float time, const int* list, const int* count, int n_max,
+bool tc_normals_shade(int terms, const DevField& nf, float time, const int* list, const int* count, int n_max,
                       const RayState& st, const ShadeParams& sp, bool defer_fallback, int* fb_list, int* fb_count,
                       float* rgb, float* depth, uint8_t* mask, cudaStream_t s);
-bool tc_eval(const DevField& f, const float* pts, int rows, int k, float time, float* out, float* grad,
+bool tc_eval(int terms, const DevField& f, const float* pts, int rows, int k, float time, float* out, float* grad,
              cudaStream_t s);
 
 }  // namespace nsdf_b200

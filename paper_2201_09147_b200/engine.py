@@ -49,7 +49,7 @@ class Context:
 
     def set_mode(self, mode: str):
         m = {"fp32": abi.MODE_FP32_ORACLE, "oracle": abi.MODE_FP32_ORACLE, "fp16": abi.MODE_FP16_FAST,
-             "fast": abi.MODE_FP16_FAST}[mode]
+             "fast": abi.MODE_FP16_FAST, "fp16low": abi.MODE_FP16_LOW}[mode]
         check(self.lib.nsdf_cuda_set_mode(self._ctx, m))
         self.mode = mode
 
