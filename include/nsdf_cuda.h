@@ -16,7 +16,7 @@
  *   nsdf_cuda_eval_grad       mlp::forward_and_gradient_batch<float>    src/mlp/mlp.cpp:297-306
  *   nsdf_cuda_generate_rays   tracer::generate_rays                     src/tracer/camera.cpp:20-43
  *   nsdf_cuda_trace_rays      tracer::multiscale_sphere_trace (batched) src/tracer/trace.cpp:86-132, 162-169
- *                             tracer::sphere_trace (m = 1, offset)      src/tracer/trace.cpp:136-160
+ *   nsdf_cuda_sphere_trace    tracer::sphere_trace                      src/tracer/trace.cpp:136-160
  *   nsdf_cuda_trace_image     tracer::trace_image                       src/tracer/trace.cpp:171-186
  *   nsdf_cuda_normal_map      shading::neural_normal_map                src/shading/shade.cpp:8-42
  *   nsdf_cuda_shade           shading::shade                            src/shading/shade.cpp:44-93
@@ -199,6 +199,10 @@ int nsdf_cuda_generate_rays(nsdf_ctx* ctx, const nsdf_camera* camera, float* ray
 int nsdf_cuda_trace_rays(nsdf_ctx* ctx, const nsdf_level* levels, int m,
                          const nsdf_trace_config* config, const float* rays, int n,
                          nsdf_hit_record* out);
+/* Classic sphere tracing of one field's delta-offset level set (tracer::sphere_trace,
+ * trace.cpp:136-160): a single final level with fd = f - delta, two-sided convergence. */
+int nsdf_cuda_sphere_trace(nsdf_ctx* ctx, nsdf_field field, float time, float delta, float eps_stop,
+                           int max_iters, float t_max, const float* rays, int n, nsdf_hit_record* out);
 int nsdf_cuda_trace_image(nsdf_ctx* ctx, const nsdf_level* levels, int m,
                           const nsdf_camera* camera, const nsdf_trace_config* config,
                           nsdf_hit_record* out, nsdf_frame_stats* stats);

@@ -75,6 +75,9 @@ def build_cuda(force=False, verbose=False):
     return lib
 
 
+HOST_FLAGS = ["-O2", "-std=c++20", "-fPIC", "-ffp-contract=off", "-Wall"]
+
+
 def build_host(force=False):
     """The drop-in C++ library: include/nsdf headers, host/*.cpp, links libnsdf_cuda.so."""
     if not os.path.isdir(HOST):
@@ -83,18 +86,53 @@ def build_host(force=False):
     if not srcs:
         return None
     lib = os.path.join(PKG, "libnsdf_b200.so")
-    hdrs = []
+    hdrs = _headers(HOST) + [os.path.join(INC, "nsdf_cuda.h"), os.path.join(INC, "nsdf_host.h")]
     for dp, _, fs in os.walk(os.path.join(INC, "nsdf")):
         hdrs += [os.path.join(dp, f) for f in fs]
-    if force or _stale(lib, srcs + hdrs + [os.path.join(PKG, "libnsdf_cuda.so")]):
-        _run(["g++", "-O2", "-std=c++20", "-fPIC", "-shared", "-ffp-contract=off", "-Wall", "-I", INC,
-              "-I", JSON_DIR, *srcs, "-o", lib, "-L", PKG, "-lnsdf_cuda", "-Wl,-rpath,$ORIGIN"])
+    os.makedirs(OBJ, exist_ok=True)
+    jobs, objs = [], []
+    for s in srcs:
+        o = os.path.join(OBJ, "host_" + os.path.basename(s) + ".o")
+        objs.append(o)
+        if force or _stale(o, [s] + hdrs):
+            jobs.append(["g++", *HOST_FLAGS, "-I", INC, "-I", JSON_DIR, "-I", HOST, "-c", s, "-o", o])
+    with ThreadPoolExecutor(max_workers=8) as ex:
+        list(ex.map(_run, jobs))
+    if force or jobs or _stale(lib, objs + [os.path.join(PKG, "libnsdf_cuda.so")]):
+        _run(["g++", "-shared", *objs, "-o", lib, "-L", PKG, "-lnsdf_cuda", "-lz", "-Wl,-rpath,$ORIGIN"])
     return lib
+
+
+def build_cpp_tests(force=False):
+    """tests/cpp/*.cpp -> tests/cpp/bin/*: reference-style checks of the drop-in C++ API."""
+    tdir = os.path.join(ROOT, "tests", "cpp")
+    if not os.path.isdir(tdir):
+        return []
+    out = os.path.join(tdir, "bin")
+    os.makedirs(out, exist_ok=True)
+    lib = os.path.join(PKG, "libnsdf_b200.so")
+    hdrs = [os.path.join(tdir, f) for f in os.listdir(tdir) if f.endswith(".hpp")]
+    for dp, _, fs in os.walk(os.path.join(INC, "nsdf")):
+        hdrs += [os.path.join(dp, f) for f in fs]
+    jobs, bins = [], []
+    for f in sorted(os.listdir(tdir)):
+        if not f.endswith(".cpp"):
+            continue
+        src = os.path.join(tdir, f)
+        exe = os.path.join(out, f[:-4])
+        bins.append(exe)
+        if force or _stale(exe, [src, lib] + hdrs):
+            jobs.append(["g++", *HOST_FLAGS, "-I", INC, src, "-o", exe, "-L", PKG, "-lnsdf_b200", "-lnsdf_cuda",
+                         "-Wl,-rpath," + PKG])
+    with ThreadPoolExecutor(max_workers=4) as ex:
+        list(ex.map(_run, jobs))
+    return bins
 
 
 def build(force=False, verbose=False):
     build_cuda(force, verbose)
     build_host(force)
+    build_cpp_tests(force)
 
 
 if __name__ == "__main__":

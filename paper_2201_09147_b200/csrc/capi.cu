@@ -178,7 +178,7 @@ int validate_sequence(nsdf_ctx* c, const nsdf_level* levels, int m, const nsdf_t
 // Traced levels (trace_rays, trace.cpp:89-117): zero budgets skipped, the last nonzero
 // one is final and traces the zero set.
 std::vector<LevelDesc> traced_levels(nsdf_ctx* c, const nsdf_level* levels, int m, const nsdf_trace_config* cfg,
-                                     int* n_counters) {
+                                     int* n_counters, float final_delta = 0.0f) {
   int eff = -1;
   for (int j = 0; j < m; ++j)
     if (cfg->budgets[j] > 0) eff = j;
@@ -190,7 +190,7 @@ std::vector<LevelDesc> traced_levels(nsdf_ctx* c, const nsdf_level* levels, int 
     d.field = c->fields[levels[j].field]->dev;
     d.time = levels[j].time;
     d.final_level = j == eff;
-    d.delta = d.final_level ? 0.0f : float(levels[j].delta);
+    d.delta = d.final_level ? final_delta : float(levels[j].delta);
     d.budget = cfg->budgets[j];
     d.level = j;
     out.push_back(d);
@@ -228,9 +228,10 @@ struct FrameOut {
 
 int run_frame(nsdf_ctx* c, const nsdf_level* levels, int m, const nsdf_trace_config* cfg, const CamBasis* cam,
               const float* d_rays6, int n_rays, const ShadeParams* sp, int normal_source, int fine_index,
-              int tile_size, int tile_rank, int tile_world, const FrameOut& out, nsdf_frame_stats* stats) {
+              int tile_size, int tile_rank, int tile_world, const FrameOut& out, nsdf_frame_stats* stats,
+              float final_delta = 0.0f) {
   int n_counters = 0;
-  std::vector<LevelDesc> lv = traced_levels(c, levels, m, cfg, &n_counters);
+  std::vector<LevelDesc> lv = traced_levels(c, levels, m, cfg, &n_counters, final_delta);
   const int n_max = cam ? cam->width * cam->height : n_rays;
   NSDF_CUDA(c->frame.reserve(frame_workspace_bytes(n_max, n_counters)));
   FrameBuffers fb = carve_frame(c->frame.base, n_max, n_counters);
@@ -657,6 +658,47 @@ int nsdf_cuda_trace_rays(nsdf_ctx* c, const nsdf_level* levels, int m, const nsd
   FrameOut fo;
   fo.d_records = drec;
   if (int st = run_frame(c, levels, m, config, nullptr, dr, n, nullptr, 0, -1, 1, 0, 1, fo, nullptr)) return st;
+  NSDF_CUDA(cudaMemcpyAsync(out, drec, size_t(n) * sizeof(nsdf_hit_record), cudaMemcpyDeviceToHost, c->stream));
+  NSDF_CUDA(cudaStreamSynchronize(c->stream));
+  return NSDF_OK;
+}
+
+int nsdf_cuda_sphere_trace(nsdf_ctx* c, nsdf_field field, float time, float delta, float eps_stop, int max_iters,
+                           float t_max, const float* rays, int n, nsdf_hit_record* out) {
+  if (!c) return fail(NSDF_ERR_CONTRACT, "context is null");
+  if (!(eps_stop > 0)) return fail(NSDF_ERR_CONFIG, "eps_stop must be positive");
+  if (delta < 0) return fail(NSDF_ERR_CONFIG, "offset must be non-negative");
+  std::lock_guard<std::mutex> lk(c->mu);
+  DeviceGuard g(c->device);
+  FieldRec* f;
+  if (int st = find_field(c, field, &f)) return st;
+  if (n < 0) return fail(NSDF_ERR_CONTRACT, "ray count must be non-negative");
+  if (n == 0) return NSDF_OK;
+  if (max_iters > 65535) return fail(NSDF_ERR_CONFIG, "iteration budget exceeds the uint16 counter");
+  nsdf_level lvl{field, time, 1.0};
+  nsdf_trace_config cfg{};
+  cfg.n_levels = 1;
+  cfg.budgets[0] = std::max(max_iters, 0);
+  cfg.eps_stop = eps_stop;
+  cfg.t_max = t_max;
+  size_t off = 0;
+  NSDF_CUDA(c->io.reserve(size_t(n) * (24 + sizeof(nsdf_hit_record)) + 4096));
+  float* dr = carve<float>(c->io.base, off, size_t(6) * n);
+  nsdf_hit_record* drec = carve<nsdf_hit_record>(c->io.base, off, size_t(n));
+  NSDF_CUDA(cudaMemcpyAsync(dr, rays, size_t(n) * 24, cudaMemcpyHostToDevice, c->stream));
+  FrameOut fo;
+  fo.d_records = drec;
+  if (max_iters <= 0) {  // no evaluation: every ray stays at its origin, a miss
+    std::vector<nsdf_hit_record> recs(n);
+    for (int i = 0; i < n; ++i) {
+      recs[i] = nsdf_hit_record{};
+      recs[i].level_reached = -1;
+      for (int k = 0; k < 3; ++k) recs[i].point[k] = rays[6 * i + k];
+    }
+    std::memcpy(out, recs.data(), sizeof(nsdf_hit_record) * n);
+    return NSDF_OK;
+  }
+  if (int st = run_frame(c, &lvl, 1, &cfg, nullptr, dr, n, nullptr, 0, -1, 1, 0, 1, fo, nullptr, delta)) return st;
   NSDF_CUDA(cudaMemcpyAsync(out, drec, size_t(n) * sizeof(nsdf_hit_record), cudaMemcpyDeviceToHost, c->stream));
   NSDF_CUDA(cudaStreamSynchronize(c->stream));
   return NSDF_OK;

@@ -1,0 +1,120 @@
+// extern "C" entry points into the drop-in C++ API, so tests and bench.py can drive the
+// reference-shaped call chain (load_manifest -> shading::render / tracer::trace_image ->
+// C ABI -> B200) in-process through ctypes.  Declared in include/nsdf_host.h.
+#include <cstring>
+#include <string>
+
+#include "device_seq.hpp"
+#include "nsdf_host.h"
+
+using namespace nsdf;
+
+namespace {
+thread_local std::string g_err;
+
+int fail_from(const std::exception& e) {
+  g_err = e.what();
+  if (auto* ne = dynamic_cast<const Error*>(&e)) return 1 + int(ne->kind());
+  return NSDF_ERR_VALIDATION;
+}
+
+fields::NestedSequence sequence_of(const char* manifest, double time) {
+  auto m = fields::load_manifest(manifest);
+  return m.time_dependent ? m.animated.slice(time) : m.sequence;
+}
+
+tracer::Camera camera_of(const nsdf_camera* c) {
+  tracer::Camera cam;
+  cam.position = {c->position[0], c->position[1], c->position[2]};
+  cam.look_at = {c->look_at[0], c->look_at[1], c->look_at[2]};
+  cam.up = {c->up[0], c->up[1], c->up[2]};
+  cam.vertical_fov_deg = c->vertical_fov_deg;
+  cam.width = c->width;
+  cam.height = c->height;
+  return cam;
+}
+
+tracer::TraceConfig trace_of(const nsdf_trace_config* t) {
+  tracer::TraceConfig cfg;
+  cfg.budgets.assign(t->budgets, t->budgets + t->n_levels);
+  cfg.eps_stop = t->eps_stop;
+  cfg.t_max = t->t_max;
+  return cfg;
+}
+
+shading::ShadeConfig shade_of(const nsdf_shade_config* s) {
+  shading::ShadeConfig cfg;
+  cfg.material.albedo = {s->albedo[0], s->albedo[1], s->albedo[2]};
+  cfg.material.ambient = s->ambient;
+  cfg.material.diffuse = s->diffuse;
+  cfg.material.specular = s->specular;
+  cfg.material.shininess = s->shininess;
+  cfg.lights.clear();
+  for (int i = 0; i < s->n_lights; ++i)
+    cfg.lights.push_back({{s->light_direction[i][0], s->light_direction[i][1], s->light_direction[i][2]},
+                          s->light_intensity[i]});
+  cfg.background = {s->background[0], s->background[1], s->background[2]};
+  return cfg;
+}
+}  // namespace
+
+extern "C" {
+
+const char* nsdf_host_last_error(void) { return g_err.c_str(); }
+
+int nsdf_host_render_manifest(const char* manifest, double time, const nsdf_camera* camera,
+                              const nsdf_trace_config* trace, const nsdf_shade_config* shade, int normal_source,
+                              int fine_index, float* rgb, float* depth, uint8_t* mask) {
+  try {
+    const auto seq = sequence_of(manifest, time);
+    shading::RenderConfig cfg;
+    cfg.trace = trace_of(trace);
+    cfg.shade = shade_of(shade);
+    cfg.normal_source = normal_source == NSDF_NORMALS_MAPPED ? shading::NormalSource::mapped : shading::NormalSource::own;
+    cfg.mapped_fine_index = fine_index;
+    const auto img = shading::render(seq, camera_of(camera), cfg);
+    std::memcpy(rgb, img.rgb.data(), img.rgb.size() * sizeof(float));
+    std::memcpy(depth, img.depth.data(), img.depth.size() * sizeof(float));
+    std::memcpy(mask, img.mask.data(), img.mask.size());
+    return NSDF_OK;
+  } catch (const std::exception& e) {
+    return fail_from(e);
+  }
+}
+
+int nsdf_host_trace_image_manifest(const char* manifest, double time, const nsdf_camera* camera,
+                                   const nsdf_trace_config* trace, nsdf_hit_record* out) {
+  try {
+    const auto recs = tracer::trace_image(sequence_of(manifest, time), camera_of(camera), trace_of(trace));
+    for (size_t i = 0; i < recs.size(); ++i) {
+      const auto& r = recs[i];
+      nsdf_hit_record& o = out[i];
+      o.hit = r.hit ? 1 : 0;
+      o.point[0] = r.point.x;
+      o.point[1] = r.point.y;
+      o.point[2] = r.point.z;
+      o.t = r.t;
+      o.level_reached = r.level_reached;
+      for (int j = 0; j < NSDF_MAX_LEVELS; ++j) o.iterations_used[j] = r.iterations_used[j];
+      o.final_distance = r.final_distance;
+    }
+    return NSDF_OK;
+  } catch (const std::exception& e) {
+    return fail_from(e);
+  }
+}
+
+int nsdf_host_forward_and_gradient(const char* sdfnet, const float* points, int k, float* dist, float* grad) {
+  try {
+    const auto p = mlp::load_params(sdfnet).cast<float>();
+    tensor::Matrix<float> pts(3, k, std::vector<float>(points, points + size_t(3) * k));
+    auto [d, g] = mlp::forward_and_gradient_batch(p, pts);
+    std::memcpy(dist, d.data(), sizeof(float) * size_t(k));
+    std::memcpy(grad, g.data(), sizeof(float) * size_t(3) * k);
+    return NSDF_OK;
+  } catch (const std::exception& e) {
+    return fail_from(e);
+  }
+}
+
+}  // extern "C"

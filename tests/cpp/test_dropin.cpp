@@ -1,0 +1,264 @@
+// Reference-style checks of the drop-in C++ API (include/nsdf/*.hpp) running on the B200.
+// Cases follow the reference's own suites (proj/tests/test_mlp.cpp, test_tracer.cpp,
+// test_shading.cpp); file:line of the originals is given per case.  Run with
+// NSDF_MODE=oracle for the bit-exact assertions.
+#include <cstdlib>
+#include <filesystem>
+
+#include "check.hpp"
+#include "nsdf/shading/shading.hpp"
+
+using namespace nsdf;
+using fields::NestedSequence;
+using fields::SphereField;
+using tensor::Matrix;
+using namespace nsdf::tracer;
+
+namespace {
+
+mlp::MlpParams<double> linear(std::vector<double> w, double b) {
+  mlp::MlpParams<double> p;
+  p.input_dim = int(w.size());
+  p.activation = tensor::ActivationSpec::identity();
+  p.layers.push_back({Matrix<double>(1, int(w.size()), w), Matrix<double>(1, 1, {b})});
+  return p;
+}
+
+Ray axis_ray(Vec3 origin, Vec3 toward) { return {Vec3f::from(origin), Vec3f::from((toward - origin).normalized())}; }
+
+NestedSequence spheres(std::vector<double> radii, std::vector<double> deltas) {
+  NestedSequence s;
+  for (double r : radii) s.entries.push_back({std::make_shared<SphereField>(Vec3{0, 0, 0}, r), {}, "s", 0});
+  s.deltas = std::move(deltas);
+  return s;
+}
+
+Matrix<float> random_points(int k, uint64_t seed) {
+  Rng rng(seed);
+  Matrix<float> m(3, k);
+  for (auto& v : m.storage()) v = float(rng.uniform(-1, 1));
+  return m;
+}
+
+}  // namespace
+
+TEST_CASE("forward: single affine layer picks out a coordinate (test_mlp.cpp:64-68)") {
+  auto p = linear({1, 0, 0}, 0.0).cast<float>();
+  CHECK(mlp::forward_batch(p, Matrix<float>(3, 1, {2, 0, 0}))(0, 0) == 2.0f);
+}
+
+TEST_CASE("gradient of a linear network is its weight row (test_mlp.cpp:82-91)") {
+  auto p = linear({0.5, -2.0, 3.25}, 1.0).cast<float>();
+  auto g = mlp::gradient_batch(p, random_points(7, 8));
+  for (int j = 0; j < 7; ++j) CHECK(g(0, j) == 0.5f && g(1, j) == -2.0f && g(2, j) == 3.25f);
+}
+
+TEST_CASE("hand-sized sine network gradient at the origin (test_mlp.cpp:93-111)") {
+  mlp::MlpParams<double> p;
+  p.activation = tensor::ActivationSpec::sine(2.0);
+  p.layers.push_back({Matrix<double>{{1, 2, 3}, {4, 5, 6}}, Matrix<double>{{0.1}, {-0.2}}});
+  p.layers.push_back({Matrix<double>{{0.5, -1.5}}, Matrix<double>{{0.3}}});
+  auto g = mlp::gradient_batch(p.cast<float>(), Matrix<float>(3, 1));
+  for (int c = 0; c < 3; ++c) {
+    const double want = 0.5 * 2 * std::cos(0.2) * p.layers[0].weights(0, c) +
+                        (-1.5) * 2 * std::cos(-0.4) * p.layers[0].weights(1, c);
+    CHECK_NEAR(g(c, 0), want, 2e-5 * std::abs(want) + 1e-6);
+  }
+}
+
+TEST_CASE("fused evaluation is bitwise equal to the separate calls (test_mlp.cpp:128-137)") {
+  for (int it = 0; it < 12; ++it) {
+    Rng rng(300 + it);
+    auto net = mlp::random_init({4 + (it % 3) * 4, 1 + it % 2, 3}, 30.0, rng).cast<float>();
+    auto pts = random_points(1 + it % 5, 400 + it);
+    auto [d, g] = mlp::forward_and_gradient_batch(net, pts);
+    CHECK(d == mlp::forward_batch(net, pts));
+    CHECK(g == mlp::gradient_batch(net, pts));
+  }
+}
+
+TEST_CASE("batch width invariance and single point == batch (test_tensor.cpp:283-309, test_mlp.cpp:182-202)") {
+  Rng rng(9);
+  auto net = mlp::random_init({128, 2, 3}, 30.0, rng).cast<float>();
+  auto pts = random_points(300, 10);
+  auto all = mlp::forward_batch(net, pts);
+  for (int j = 0; j < 300; j += 37) {
+    Matrix<float> one(3, 1, {pts(0, j), pts(1, j), pts(2, j)});
+    CHECK(mlp::forward_batch(net, one)(0, 0) == all(0, j));
+  }
+}
+
+TEST_CASE("validation and contract errors") {
+  mlp::MlpParams<float> empty;
+  CHECK_THROWS(mlp::forward_batch(empty, Matrix<float>(3, 1)));
+  auto p = linear({1, 0, 0}, 0).cast<float>();
+  CHECK_THROWS(mlp::forward_batch(p, Matrix<float>(2, 1)));
+  CHECK_THROWS(mlp::parse_architecture("64"));
+  CHECK(mlp::parse_architecture("256x3").parameter_count() == 198657u);
+  CHECK_THROWS(mlp::forward_batch(linear({1, 0, 0}, 0), Matrix<double>(3, 1)));  // f64: not the render path
+}
+
+TEST_CASE("classic sphere tracing hits the surface and the offset surface (test_tracer.cpp:74-87)") {
+  SphereField sphere({0, 0, 0}, 1.0);
+  const Ray ray = axis_ray({3, 0, 0}, {-1, 0, 0});
+  HitRecord hit = sphere_trace(sphere, ray, 0.0f, 1e-3f, 100);
+  CHECK(hit.hit);
+  CHECK_NEAR(hit.point.x, 1.0, 2e-3);
+  CHECK_NEAR(hit.t, 2.0, 4e-3);
+  CHECK(hit.final_distance <= 1e-3f);
+  HitRecord off = sphere_trace(sphere, ray, 0.1f, 1e-3f, 100);
+  CHECK(off.hit);
+  CHECK_NEAR(off.point.x, 1.1, 2.2e-3);
+}
+
+TEST_CASE("multiscale trace on certified concentric spheres (test_tracer.cpp:104-121)") {
+  auto seq = spheres({1.0, 0.95}, {0.1, 0.05});
+  TraceConfig cfg;
+  cfg.budgets = {50, 50};
+  HitRecord hit = multiscale_sphere_trace(seq, axis_ray({3, 0, 0}, {0, 0, 0}), cfg);
+  CHECK(hit.hit);
+  CHECK(hit.level_reached == 1);
+  CHECK_NEAR(hit.point.x, 0.95, 2e-3);
+  CHECK(hit.iterations_used[0] > 0 && hit.iterations_used[1] > 0);
+}
+
+TEST_CASE("a single-level sequence is classic sphere tracing bit for bit (test_tracer.cpp:123-141)") {
+  auto seq = spheres({0.8}, {0.05});
+  TraceConfig cfg;
+  cfg.budgets = {60};
+  Rng rng(5);
+  for (int i = 0; i < 20; ++i) {
+    const Vec3 o{rng.uniform(2, 3), rng.uniform(-0.5, 0.5), rng.uniform(-0.5, 0.5)};
+    const Vec3 to{rng.uniform(-0.2, 0.2), rng.uniform(-0.2, 0.2), rng.uniform(-0.2, 0.2)};
+    const Ray ray = axis_ray(o, to);
+    HitRecord a = multiscale_sphere_trace(seq, ray, cfg);
+    HitRecord b = sphere_trace(seq.field(0), ray, 0.0f, cfg.eps_stop, 60);
+    CHECK(a.hit == b.hit && a.point.x == b.point.x && a.point.y == b.point.y && a.point.z == b.point.z);
+    CHECK(a.t == b.t && a.final_distance == b.final_distance);
+  }
+}
+
+TEST_CASE("budget exhaustion, trailing zero budget, origin inside the shell (test_tracer.cpp:185-192, 281-307)") {
+  auto one = spheres({1.0}, {0.05});
+  TraceConfig b1;
+  b1.budgets = {1};
+  HitRecord miss = multiscale_sphere_trace(one, axis_ray({4, 0.3, 0}, {0, 0.3, 0}), b1);
+  CHECK(!miss.hit && miss.iterations_used[0] == 1 && miss.t > 0);
+  auto con = spheres({1.0, 0.95}, {0.1, 0.05});
+  TraceConfig trailing;
+  trailing.budgets = {50, 0};
+  HitRecord h = multiscale_sphere_trace(con, axis_ray({3, 0, 0}, {0, 0, 0}), trailing);
+  CHECK(h.hit && h.iterations_used[1] == 0);
+  CHECK_NEAR(h.point.x, 1.0, 2e-3);
+  TraceConfig zero;
+  zero.budgets = {0, 0};
+  CHECK_THROWS(multiscale_sphere_trace(con, axis_ray({3, 0, 0}, {0, 0, 0}), zero));
+  TraceConfig c30;
+  c30.budgets = {30, 30};
+  HitRecord in = multiscale_sphere_trace(con, axis_ray({1.05, 0, 0}, {-1, 0, 0}), c30);
+  CHECK(in.hit && in.iterations_used[0] == 1);
+  CHECK_NEAR(in.point.x, 0.95, 2e-3);
+}
+
+TEST_CASE("trace_image: empty view, filled disc, per-ray equivalence (test_tracer.cpp:194-244)") {
+  auto seq = spheres({0.7}, {0.05});
+  TraceConfig cfg;
+  cfg.budgets = {60};
+  Camera away;
+  away.position = {0, 0, 3};
+  away.look_at = {0, 0, 6};
+  away.width = away.height = 32;
+  for (const auto& r : trace_image(seq, away, cfg)) CHECK(!r.hit);
+  Camera cam;
+  cam.position = {0, 0, 3};
+  cam.width = cam.height = 129;
+  cam.vertical_fov_deg = 40;
+  auto recs = trace_image(seq, cam, cfg);
+  const double screen = std::tan(std::asin(0.7 / 3.0)) / std::tan(cam.vertical_fov_deg * M_PI / 360.0);
+  int first = -1, last = -1;
+  for (int x = 0; x < cam.width; ++x)
+    if (recs[size_t(64) * cam.width + x].hit) {
+      if (first < 0) first = x;
+      last = x;
+    }
+  CHECK(first >= 0);
+  CHECK(std::abs((last - first + 1) / 2.0 - screen * cam.height / 2.0) <= 1.0);
+  auto rays = generate_rays(cam);
+  for (size_t i = 0; i < recs.size(); i += 37) {
+    HitRecord one = multiscale_sphere_trace(seq, rays[i], cfg);
+    CHECK(one.hit == recs[i].hit);
+    if (one.hit) CHECK(one.point.x == recs[i].point.x && one.t == recs[i].t);
+  }
+}
+
+TEST_CASE("ray generation geometry (test_tracer.cpp:38-72)") {
+  Camera cam;
+  cam.width = cam.height = 101;
+  auto rays = generate_rays(cam);
+  CHECK(rays.size() == 101u * 101u);
+  const auto& c = rays[50 * 101 + 50].direction;
+  CHECK(std::abs(c.x) < 1e-6 && std::abs(c.y) < 1e-6 && std::abs(c.z + 1) < 1e-6);
+  Camera bad = cam;
+  bad.width = 0;
+  CHECK_THROWS(generate_rays(bad));
+}
+
+TEST_CASE("analytic-sphere render: unit normals, parallel level sets (test_shading.cpp:142-165, 197-213)") {
+  auto seq = spheres({0.7}, {0.05});
+  Camera cam;
+  cam.width = cam.height = 64;
+  shading::RenderConfig cfg;
+  cfg.trace.budgets = {80};
+  auto img = shading::render(seq, cam, cfg);
+  size_t hits = 0;
+  for (auto m : img.mask) hits += m;
+  CHECK(hits > 300);
+  Matrix<float> pts(3, 4, {0.7f, 0, 0, -0.8f, 0, 0.7f, 0, 0, 0, 0, 0.7f, 0});
+  auto r = shading::neural_normal_map(seq.field(0), pts, 0.05);
+  for (int j = 0; j < 4; ++j) {
+    const double n = std::sqrt(double(r.normals(0, j)) * r.normals(0, j) + double(r.normals(1, j)) * r.normals(1, j) +
+                               double(r.normals(2, j)) * r.normals(2, j));
+    CHECK_NEAR(n, 1.0, 1e-6);
+  }
+  CHECK(r.normals(0, 0) > 0.999f);
+  CHECK(r.outside_count == 1);  // (-0.8, 0, 0): |f| = 0.1 > delta
+}
+
+TEST_CASE("self-mapped normals reproduce the own-normal render exactly (test_shading.cpp:332-349)") {
+  auto seq = spheres({0.7}, {0.05});
+  Camera cam;
+  cam.width = cam.height = 48;
+  shading::RenderConfig own;
+  own.trace.budgets = {60};
+  shading::RenderConfig mapped = own;
+  mapped.normal_source = shading::NormalSource::mapped;
+  CHECK(shading::image_mse(shading::render(seq, cam, own), shading::render(seq, cam, mapped)) == 0.0);
+}
+
+TEST_CASE("manifest + sdfnet round trip and image / mesh I/O") {
+  const auto dir = std::filesystem::temp_directory_path() / "nsdf_dropin_test";
+  std::filesystem::create_directories(dir);
+  Rng rng(3);
+  auto p = mlp::random_init({16, 1, 3}, 30.0, rng);
+  mlp::save_params(p, dir / "n.sdfnet");
+  auto q = mlp::load_params(dir / "n.sdfnet");
+  CHECK(q.layers[1].weights == p.layers[1].weights);
+  NestedSequence seq;
+  fields::FieldSource src;
+  src.kind = fields::FieldSource::Kind::weights;
+  src.weights_path = "n.sdfnet";
+  seq.entries.push_back({std::make_shared<fields::NeuralField>(p), src, "16x1", p.parameter_count()});
+  seq.deltas = {0.1};
+  fields::save_manifest(seq, dir / "s.nest");
+  auto m = fields::load_manifest(dir / "s.nest");
+  CHECK(!m.time_dependent && m.sequence.size() == 1 && m.sequence.deltas[0] == 0.1);
+  shading::ImageBuffer img(4, 3);
+  for (size_t i = 0; i < img.rgb.size(); ++i) img.rgb[i] = float(i % 256) / 255.0f;
+  shading::write_ppm(img, dir / "a.ppm");
+  CHECK(shading::image_mse(img, shading::read_ppm(dir / "a.ppm")) < 1e-10);
+  shading::write_png(img, dir / "a.png");
+  CHECK(std::filesystem::file_size(dir / "a.png") > 40);
+  CHECK(fields::thresholds_prop2({0.3, 0.1, 0.05})[2] == 0.1 + 0.05);
+}
+
+int main() { return chk::run_all(); }
