@@ -9,8 +9,8 @@
 //                        issued by one thread; weight K-chunks streamed into a 2-stage SMEM
 //                        ring with cp.async.bulk (pre-arranged in the UMMA canonical layout at
 //                        upload, so a chunk is one contiguous 1-D bulk copy)
-//   epilogue             tcgen05.ld 32x32b -> + bias -> range-reduced MUFU sine (turns:
-//                        t = z*omega/2pi, r = t - rint(t)) -> fp16 -> next A operand;
+//   epilogue             tcgen05.ld 32x32b -> one FFMA forms omega*(z + b) in radians ->
+//                        MUFU sine (hardware reduction in revolutions) -> fp16 -> next A;
 //                        tangent lanes multiply by omega*cos of their ray's value lane
 //                        (warp shuffle); the last hidden layer folds the 1 x W output layer
 //                        into an FP32 dot product
@@ -57,10 +57,44 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
                : "memory");
 }
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+// mbarrier wait.  With a suspend-time hint (ns) the waiting warp may sleep in hardware
+// until the phase completes instead of spinning through SYNCS/YIELD/BRA; 0 = plain
+// try_wait loop.  Selected at launch (NSDF_TC_SUSPEND_NS, default below).
+constexpr uint32_t kBackoffNs = 0;
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity, uint32_t suspend_ns) {
   uint32_t done = 0;
   const uint32_t a = smem_addr(bar);
-  do {
+  if (suspend_ns) {
+    do {
+      asm volatile(
+          "{\n\t.reg .pred p;\n\t"
+          "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+          "selp.u32 %0, 1, 0, p;\n\t}"
+          : "=r"(done)
+          : "r"(a), "r"(parity), "r"(suspend_ns)
+          : "memory");
+    } while (!done);
+  } else {
+    for (;;) {
+      asm volatile(
+          "{\n\t.reg .pred p;\n\t"
+          "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+          "selp.u32 %0, 1, 0, p;\n\t}"
+          : "=r"(done)
+          : "r"(a), "r"(parity)
+          : "memory");
+      if (done) break;
+      if (kBackoffNs) __nanosleep(kBackoffNs);
+    }
+  }
+}
+// Spin-wait with nanosleep back-off: the single-lane MMA / producer warps would otherwise
+// take issue slots from the epilogue warps while they wait.
+template <uint32_t kBackoff>
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_addr(bar);
+  for (;;) {
+    uint32_t done;
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
         "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
@@ -68,7 +102,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "=r"(done)
         : "r"(a), "r"(parity)
         : "memory");
-  } while (!done);
+    if (done) return;
+    __nanosleep(kBackoff);
+  }
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -130,17 +166,14 @@ __host__ __device__ constexpr uint32_t umma_idesc(int n) {
 // Offset (in halves) of element (row, k) in a 128-row canonical operand.
 __device__ __forceinline__ int a_off(int row, int k) { return ((k >> 3) * (kRows / 8) + (row >> 3)) * 64 + (row & 7) * 8; }
 
-// sin(omega * z) from t = z * omega / 2pi (turns): explicit reduction to [-1/2, 1/2]
-// turns, then the MUFU sine.  |error| ~ 1e-6, far below the fp16 activation rounding.
-// Round-to-nearest via the 1.5*2^23 magic constant keeps the reduction on the FMA pipe
-// (FRND would share the XU pipe with MUFU.SIN); valid for |t| < 2^22 turns.
-__device__ __forceinline__ float reduce_turns(float t) {
-  constexpr float kMagic = 12582912.0f;
-  const float k = __fsub_rn(__fadd_rn(t, kMagic), kMagic);
-  return __fsub_rn(t, k);
-}
-__device__ __forceinline__ float sin_turns(float t) { return __sinf(reduce_turns(t) * k2Pi); }
-__device__ __forceinline__ void sincos_turns(float t, float& s, float& c) { __sincosf(reduce_turns(t) * k2Pi, &s, &c); }
+// sin(omega * z) on the MUFU pipe: the argument is formed in radians by one FFMA
+// (omega folded into the scale and the bias) and fed to sin.approx, which ptxas lowers to
+// FMUL.RZ(x, 1/2pi) + MUFU.SIN: the hardware reduces the revolutions exactly, so the only
+// error beyond the fp32 rounding of x itself (ulp(x) ~1e-5 rad at |x| ~ 150, shared by any
+// fp32 reduction including the reference's Cody-Waite) is one RZ rounding of x/2pi.
+// 3 issue slots per activation instead of 7 for an explicit turns reduction.
+__device__ __forceinline__ float fast_sin(float x) { return __sinf(x); }
+__device__ __forceinline__ void fast_sincos(float x, float& s, float& c) { __sincosf(x, &s, &c); }
 
 __device__ __forceinline__ uint32_t pack_half2(float a, float b) {
   __half2 h = __floats2half2_rn(a, b);
@@ -158,7 +191,6 @@ enum TcOp : int { kOpTrace = 0, kOpNormals = 1, kOpEval = 2 };
 
 struct TcNet {
   int n_layers, width, input_dim;
-  float turns;                      // omega / 2pi
   float omega;
   const __half* wq;                 // hidden layers [h][hi | lo][W*W], canonical chunked layout
   float wscale[kMaxLayers];         // 2^-k: hidden weights are stored scaled by 2^k
@@ -172,6 +204,7 @@ struct TcArgs {
   TcNet net;
   int op;
   int terms;  // 3 = split-fp16 (A_hi.W_hi + A_lo.W_hi + A_hi.W_lo), 1 = plain fp16
+  uint32_t suspend_ns;
   // trace
   LevelDesc lv;
   float eps, t_max;
@@ -205,50 +238,59 @@ struct TcSmem {
   __half* a;            // [128 x W] A operand (fp16 hi part)
   __half* alo;          // [128 x W] A low part (split precision only)
   __half* wst;          // [kStages][W * kKC] streamed weight chunks
-  float* w0t;           // [W x input_dim] layer-0 weights * omega/2pi
-  float* w0;            // [W x input_dim] layer-0 weights
+  float4* w0r;          // [W] {omega*w0x, omega*w0y, omega*w0z, omega*(b0 + w0t*time)}
   float* bias;          // [(L-1) x W] biases * omega/2pi
   float* wout;          // [W]
   float* part;          // [3][kRows] partial output dots of column groups 1..3
+  int* stage_buf;       // [2][kStageCap] staged compaction appends (next, adv)
+  int* stage_count;     // [2]
+  int* stage_base;      // flush base broadcast
   uint64_t* bars;       // full[kStages], empty[kStages], aready, dfull
   uint32_t* tmem_base;
 };
 
-__host__ __device__ inline size_t tc_smem_bytes(int W, int L, int terms) {
+__host__ __device__ inline size_t tc_weight_bytes(int W, int L, int terms, bool resident) {
+  const int nw = terms == 3 ? 2 : 1;
+  // resident: every hidden layer's [hi | lo] pair, as laid out in global memory
+  return resident ? size_t(L - 2) * W * W * 2 * 2 : size_t(kStages) * W * kKC * 2 * nw;
+}
+
+__host__ __device__ inline size_t tc_smem_bytes(int W, int L, int terms, bool resident) {
   const int nw = terms == 3 ? 2 : 1;
   size_t b = 0;
   b += size_t(kRows) * W * 2 * nw;
-  b += size_t(kStages) * W * kKC * 2 * nw;
-  b += size_t(W) * 4 * 4 * 2;
+  b += tc_weight_bytes(W, L, terms, resident);
+  b += size_t(W) * 4 * 4;
   b += size_t(L - 1) * W * 4;
   b += size_t(W) * 4;
   b += size_t(3) * kRows * 4;
+  b += size_t(2) * 1024 * 4 + 64;   // compaction staging (kStageCap per list) + counters
   b += (2 * kStages + 2) * 8 + 16;
   return b + 1024;  // alignment slack
 }
 
-__device__ inline TcSmem tc_carve(uint8_t* raw, int W, int L, int terms) {
+__device__ inline TcSmem tc_carve(uint8_t* raw, int W, int L, int terms, bool resident) {
   const int nw = terms == 3 ? 2 : 1;
-  uintptr_t p = (reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023);
+  size_t off = 0;
+  auto take = [&](size_t bytes, size_t align) {
+    off = (off + align - 1) / align * align;
+    uint8_t* p = raw + off;
+    off += bytes;
+    return p;
+  };
   TcSmem s;
-  s.a = reinterpret_cast<__half*>(p);
-  p += size_t(kRows) * W * 2;
-  s.alo = reinterpret_cast<__half*>(p);
-  if (nw == 2) p += size_t(kRows) * W * 2;
-  s.wst = reinterpret_cast<__half*>(p);
-  p += size_t(kStages) * W * kKC * 2 * nw;
-  s.w0t = reinterpret_cast<float*>(p);
-  p += size_t(W) * 4 * 4;
-  s.w0 = reinterpret_cast<float*>(p);
-  p += size_t(W) * 4 * 4;
-  s.bias = reinterpret_cast<float*>(p);
-  p += size_t(L - 1) * W * 4;
-  s.wout = reinterpret_cast<float*>(p);
-  p += size_t(W) * 4;
-  s.part = reinterpret_cast<float*>(p);
-  p += size_t(3) * kRows * 4;
-  s.bars = reinterpret_cast<uint64_t*>((p + 7) & ~uintptr_t(7));
-  s.tmem_base = reinterpret_cast<uint32_t*>(s.bars + 2 * kStages + 2);
+  s.a = reinterpret_cast<__half*>(take(size_t(kRows) * W * 2, 1024));
+  s.alo = reinterpret_cast<__half*>(take(nw == 2 ? size_t(kRows) * W * 2 : 0, 1024));
+  s.wst = reinterpret_cast<__half*>(take(tc_weight_bytes(W, L, terms, resident), 1024));
+  s.w0r = reinterpret_cast<float4*>(take(size_t(W) * 4 * 4, 16));
+  s.bias = reinterpret_cast<float*>(take(size_t(L - 1) * W * 4, 16));
+  s.wout = reinterpret_cast<float*>(take(size_t(W) * 4, 16));
+  s.part = reinterpret_cast<float*>(take(size_t(3) * kRows * 4, 16));
+  s.stage_buf = reinterpret_cast<int*>(take(size_t(2) * 1024 * 4, 16));
+  s.stage_count = reinterpret_cast<int*>(take(16, 16));
+  s.stage_base = s.stage_count + 2;
+  s.bars = reinterpret_cast<uint64_t*>(take((2 * kStages + 2) * 8, 8));
+  s.tmem_base = reinterpret_cast<uint32_t*>(take(16, 16));
   return s;
 }
 
@@ -278,33 +320,39 @@ __device__ __forceinline__ void tc_trace_update(const TcArgs& a, int slot, float
   }
 }
 
-// Ray/point data of one tile row, prefetched one tile ahead.
+// Per-row inputs of a tile, software-pipelined two tiles ahead: the list slot of tile t+2
+// is loaded while tile t runs, its ray state while tile t+1 runs, so no dependent load
+// sits on the critical path.
 struct RowIn {
   int slot;
   float p[4];
   float t, dx, dy, dz;
 };
 
-__device__ __forceinline__ RowIn load_row(const TcArgs& a, int item, int n_items, bool trace_state) {
+__device__ __forceinline__ int load_slot(const TcArgs& a, int item, int n_items) {
+  if (item >= n_items || a.op == kOpEval) return item < n_items ? item : -1;
+  return __ldg(a.in_list + item);
+}
+
+__device__ __forceinline__ RowIn load_row(const TcArgs& a, int slot, bool trace_state) {
   RowIn r;
-  r.slot = -1;
+  r.slot = slot;
   r.p[0] = r.p[1] = r.p[2] = 0.0f;
   r.p[3] = a.time;
   r.t = r.dx = r.dy = r.dz = 0.0f;
-  if (item >= n_items) return r;
+  if (slot < 0) return r;
   if (a.op == kOpEval) {
-    for (int k = 0; k < 4; ++k) r.p[k] = k < a.rows ? __ldg(a.pts + size_t(k) * a.k + item) : a.time;
+    for (int k = 0; k < 4; ++k) r.p[k] = k < a.rows ? __ldg(a.pts + size_t(k) * a.k + slot) : a.time;
     return r;
   }
-  r.slot = __ldg(a.in_list + item);
-  r.p[0] = a.st.px[r.slot];
-  r.p[1] = a.st.py[r.slot];
-  r.p[2] = a.st.pz[r.slot];
+  r.p[0] = a.st.px[slot];
+  r.p[1] = a.st.py[slot];
+  r.p[2] = a.st.pz[slot];
   if (trace_state) {
-    r.t = a.st.t[r.slot];
-    r.dx = __ldg(a.st.dx + r.slot);
-    r.dy = __ldg(a.st.dy + r.slot);
-    r.dz = __ldg(a.st.dz + r.slot);
+    r.t = a.st.t[slot];
+    r.dx = __ldg(a.st.dx + slot);
+    r.dy = __ldg(a.st.dy + slot);
+    r.dz = __ldg(a.st.dz + slot);
   }
   return r;
 }
@@ -313,18 +361,54 @@ __device__ __forceinline__ void named_bar(int id, int threads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
 }
 
+// CTA-local staging of compaction appends: warps append with shared atomics; the staged
+// slots are flushed to the global list with one global atomic per flush (every few tiles)
+// instead of one per warp per tile.
+struct StageList {
+  int* buf;
+  int* count;
+};
+constexpr int kStageCap = 1024;
+
+__device__ __forceinline__ void stage_append(bool pred, int value, StageList s) {
+  const unsigned mask = __ballot_sync(0xffffffffu, pred);
+  if (!mask) return;
+  const int lane = threadIdx.x & 31;
+  const int leader = __ffs(mask) - 1;
+  int base = 0;
+  if (lane == leader) base = atomicAdd(s.count, __popc(mask));
+  base = __shfl_sync(0xffffffffu, base, leader);
+  if (pred) s.buf[base + __popc(mask & ((1u << lane) - 1u))] = value;
+}
+
+// Called by the 128 consumer threads (named barrier 2) after a tile's appends.
+__device__ __forceinline__ void stage_flush(StageList s, int* list, int* gcount, int* gbase, int ctid, bool force) {
+  named_bar(2, 128);
+  const int n = *s.count;
+  if (n == 0 || (!force && n <= kStageCap - kRows)) return;  // uniform decision
+  if (ctid == 0) *gbase = atomicAdd(gcount, n);
+  named_bar(2, 128);
+  const int base = *gbase;
+  for (int i = ctid; i < n; i += 128) list[base + i] = s.buf[i];
+  named_bar(2, 128);
+  if (ctid == 0) *s.count = 0;
+}
+
 // kGroups column groups of 4 epilogue warps each: group g owns columns
 // [g*W/kGroups, (g+1)*W/kGroups) of every layer (TMEM lane quadrant = warp % 4).
-template <int W, bool kGrad, int kGroups, int kTerms>
-__global__ void __launch_bounds__(64 + 128 * kGroups, (W == 64 ? 3 : (kGroups > 2 ? 1 : 2)))
-    tc_mlp_kernel(TcArgs a) {
+// kResident: all hidden-layer weights stay in SMEM for the whole launch (64-wide nets);
+// otherwise a producer warp streams 32-wide K chunks through a 2-stage ring.
+template <int W, bool kGrad, int kGroups, int kTerms, bool kResident>
+__global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
+                                  (W == 64 ? 4 : (kGroups > 2 ? 1 : 2))) tc_mlp_kernel(TcArgs a) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  constexpr int kThreads = 64 + 128 * kGroups;
-  constexpr int kCols = W / kGroups;  // columns per epilogue group
+  constexpr int kCtl = kResident ? 1 : 2;  // control warps: MMA issuer [+ weight producer]
+  constexpr int kThreads = 32 * kCtl + 128 * kGroups;
+  constexpr int kCols = W / kGroups;       // columns per epilogue group
   const TcNet& net = a.net;
   const int L = net.n_layers;
-  const TcSmem sm = tc_carve(smem_raw, W, L, kTerms);
-  constexpr int kNW = kTerms == 3 ? 2 : 1;  // weight parts per stage (hi [, lo])
+  const TcSmem sm = tc_carve(smem_raw, W, L, kTerms, kResident);
+  constexpr int kNW = kTerms == 3 ? 2 : 1;  // weight parts (hi [, lo])
   uint64_t* full = sm.bars;
   uint64_t* empty = sm.bars + kStages;
   uint64_t* aready = sm.bars + 2 * kStages;
@@ -344,11 +428,15 @@ __global__ void __launch_bounds__(64 + 128 * kGroups, (W == 64 ? 3 : (kGroups > 
   if (my_tiles == 0) return;
 
   // ---- setup: constants to SMEM, barriers, TMEM ----
-  for (int i = threadIdx.x; i < W * IN; i += kThreads) {
-    sm.w0[i] = net.w0[i];
-    sm.w0t[i] = net.w0[i] * net.turns;
+  // layer 0 folded into one float4 per neuron; a 4-input net's time column joins the bias
+  // (time is fixed per launch: the slice time, field.cpp:213-220)
+  for (int n = threadIdx.x; n < W; n += kThreads) {
+    const float* w = net.w0 + n * IN;
+    float b0 = net.b[n];
+    if (IN == 4) b0 = fmaf(w[3], a.time, b0);
+    sm.w0r[n] = make_float4(net.omega * w[0], net.omega * w[1], net.omega * w[2], net.omega * b0);
   }
-  for (int i = threadIdx.x; i < (L - 1) * W; i += kThreads) sm.bias[i] = net.b[i] * net.turns;
+  for (int i = threadIdx.x; i < (L - 1) * W; i += kThreads) sm.bias[i] = net.b[i] * net.omega;
   for (int i = threadIdx.x; i < W; i += kThreads) sm.wout[i] = net.wout[i];
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -357,6 +445,7 @@ __global__ void __launch_bounds__(64 + 128 * kGroups, (W == 64 ? 3 : (kGroups > 
     }
     mbar_init(aready, 128 * kGroups);
     mbar_init(dfull, 1);
+    sm.stage_count[0] = sm.stage_count[1] = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
@@ -370,22 +459,36 @@ __global__ void __launch_bounds__(64 + 128 * kGroups, (W == 64 ? 3 : (kGroups > 
   const uint32_t tmem = *sm.tmem_base;
 
   if (warp == 0) {
-    // ================= MMA issuer =================
+    // ================= MMA issuer (resident mode: also loads the weights once) =================
     if (lane == 0) {
       const uint32_t idesc = umma_idesc(W);
       const uint32_t a_base = smem_addr(sm.a);
       const uint32_t alo_base = smem_addr(sm.alo);
+      if (kResident) {
+        const uint32_t bytes = uint32_t(n_hidden) * W * W * 2 * 2;
+        mbar_expect_tx(&full[0], bytes);
+        bulk_g2s(sm.wst, net.wq, bytes, &full[0]);
+        mbar_wait(&full[0], 0, 0);
+      }
       uint32_t chunk_iter = 0, aready_phase = 0;
       for (int t = 0; t < my_tiles; ++t) {
         for (int h = 0; h < n_hidden; ++h) {
-          mbar_wait(aready, aready_phase);
+          mbar_wait(aready, aready_phase, a.suspend_ns);
           aready_phase ^= 1;
           tc_fence_after();
           for (int c = 0; c < kChunks; ++c, ++chunk_iter) {
             const int s = chunk_iter % kStages;
-            mbar_wait(&full[s], (chunk_iter / kStages) & 1);
-            tc_fence_after();
-            const uint32_t b_base = smem_addr(sm.wst + size_t(s) * kStageHalves);
+            uint32_t b_base, lo_off;
+            if (kResident) {
+              // resident layout per layer: [hi W*W][lo W*W], chunk c contiguous inside each
+              b_base = smem_addr(sm.wst + size_t(h) * 2 * W * W + size_t(c) * W * kKC);
+              lo_off = uint32_t(W) * W * 2;
+            } else {
+              mbar_wait(&full[s], (chunk_iter / kStages) & 1, a.suspend_ns);
+              tc_fence_after();
+              b_base = smem_addr(sm.wst + size_t(s) * kStageHalves);
+              lo_off = uint32_t(W) * kKC * 2;
+            }
 #pragma unroll
             for (int ks = 0; ks < kKC / 16; ++ks) {
               const int kg = c * (kKC / 8) + ks * 2;  // first 8-element k group of this K=16 step
@@ -395,18 +498,18 @@ __global__ void __launch_bounds__(64 + 128 * kGroups, (W == 64 ? 3 : (kGroups > 
               tc_mma(tmem, ad, bd, idesc, (c | ks) != 0);
               if (kTerms == 3) {  // split precision: + A_lo.W_hi + A_hi.W_lo
                 const uint64_t adl = umma_desc(alo_base + aoff, kRows * 16, 128);
-                const uint64_t bdl = umma_desc(b_base + uint32_t(W * kKC * 2) + boff, W * 16, 128);
+                const uint64_t bdl = umma_desc(b_base + lo_off + boff, W * 16, 128);
                 tc_mma(tmem, adl, bd, idesc, 1);
                 tc_mma(tmem, ad, bdl, idesc, 1);
               }
             }
-            tc_commit(&empty[s]);  // frees the weight stage once these MMAs retire
+            if (!kResident) tc_commit(&empty[s]);  // frees the weight stage once these MMAs retire
           }
-          tc_commit(dfull);        // accumulator complete
+          tc_commit(dfull);  // accumulator complete
         }
       }
     }
-  } else if (warp == 1) {
+  } else if (!kResident && warp == 1) {
     // ================= weight producer =================
     if (lane == 0) {
       uint32_t chunk_iter = 0;
@@ -415,7 +518,7 @@ __global__ void __launch_bounds__(64 + 128 * kGroups, (W == 64 ? 3 : (kGroups > 
           const __half* lw = reinterpret_cast<const __half*>(net.wq) + size_t(h) * 2 * W * W;
           for (int c = 0; c < kChunks; ++c, ++chunk_iter) {
             const int s = chunk_iter % kStages;
-            mbar_wait(&empty[s], ((chunk_iter / kStages) & 1) ^ 1);
+            mbar_wait(&empty[s], ((chunk_iter / kStages) & 1) ^ 1, a.suspend_ns);
             mbar_expect_tx(&full[s], kChunkBytes * kNW);
             bulk_g2s(sm.wst + size_t(s) * kStageHalves, lw + size_t(c) * (W * kKC), kChunkBytes, &full[s]);
             if (kTerms == 3)
@@ -427,21 +530,29 @@ __global__ void __launch_bounds__(64 + 128 * kGroups, (W == 64 ? 3 : (kGroups > 
     }
   } else {
     // ================= epilogue warps =================
-    const int eg = (warp - 2) >> 2;                      // column group
-    const int q = warp & 3;
+    const int ew = warp - kCtl;                          // epilogue warp index
+    const int eg = ew >> 2;                              // column group
+    const int q = warp & 3;                              // TMEM lane quadrant of this warp
     const int row = q * 32 + lane;                       // TMEM lane = A row
+    const int ctid = (ew & 3) * 32 + lane;               // consumer thread id within group 0
     const int col0 = eg * kCols;
     const uint32_t taddr = tmem + (uint32_t(q * 32) << 16) + uint32_t(col0);
     const int ray = kGrad ? row >> 2 : row;             // ray within the tile
     const int chain = kGrad ? row & 3 : 0;               // 0 = value, 1..3 = d/dx, d/dy, d/dz
     const unsigned group_mask = 0xFu << (lane & ~3);
     const bool trace_state = a.op == kOpTrace && eg == 0;
+    const StageList st_next{sm.stage_buf, sm.stage_count};
+    const StageList st_adv{sm.stage_buf + kStageCap, sm.stage_count + 1};
     uint32_t dfull_phase = 0;
-    RowIn cur = load_row(a, blockIdx.x * kRaysPerTile + ray, n_items, trace_state);
+    auto item_of = [&](int t) { return (blockIdx.x + t * gridDim.x) * kRaysPerTile + ray; };
+    RowIn now = load_row(a, load_slot(a, item_of(0), n_items), trace_state);
+    int slot_next = my_tiles > 1 ? load_slot(a, item_of(1), n_items) : -1;
     for (int t = 0; t < my_tiles; ++t) {
-      const int tile = blockIdx.x + t * gridDim.x;
-      const int item = tile * kRaysPerTile + ray;
+      const int item = item_of(t);
       const bool valid = item < n_items;
+      // prefetch: ray state of tile t+1 (slot known), list slot of tile t+2
+      const RowIn next = t + 1 < my_tiles ? load_row(a, slot_next, trace_state) : RowIn{-1};
+      slot_next = t + 2 < my_tiles ? load_slot(a, item_of(t + 2), n_items) : -1;
       // ---- layer 0: FP32 FFMA, sin -> fp16 A (this group's columns) ----
 #pragma unroll 1
       for (int n0 = col0; n0 < col0 + kCols; n0 += 8) {
@@ -451,18 +562,16 @@ __global__ void __launch_bounds__(64 + 128 * kGroups, (W == 64 ? 3 : (kGroups > 
           float o[2];
 #pragma unroll
           for (int u = 0; u < 2; ++u) {
-            const int n = n0 + j + u;
-            float z = sm.bias[n];  // pre-scaled: turns
-#pragma unroll
-            for (int kk = 0; kk < 4; ++kk)
-              if (kk < IN) z = fmaf(sm.w0t[n * IN + kk], cur.p[kk], z);
+            const float4 w = sm.w0r[n0 + j + u];  // radians: omega*(W0 p + b0)
+            const float z = fmaf(w.z, now.p[2], fmaf(w.y, now.p[1], fmaf(w.x, now.p[0], w.w)));
             if (kGrad) {
               float s, cs;
-              sincos_turns(z, s, cs);
-              const float dphi = __shfl_sync(group_mask, net.omega * cs, lane & ~3, 32);
-              o[u] = chain == 0 ? s : sm.w0[n * IN + chain - 1] * dphi;
+              fast_sincos(z, s, cs);
+              const float c = __shfl_sync(group_mask, cs, lane & ~3, 32);
+              // tangent c: W0[n, c] * omega cos(z) = (omega W0[n, c]) * cos(z)
+              o[u] = chain == 0 ? s : (chain == 1 ? w.x : (chain == 2 ? w.y : w.z)) * c;
             } else {
-              o[u] = sin_turns(z);
+              o[u] = fast_sin(z);
             }
           }
           pk[j / 2] = pack_half2(o[0], o[1]);
@@ -474,18 +583,15 @@ __global__ void __launch_bounds__(64 + 128 * kGroups, (W == 64 ? 3 : (kGroups > 
       fence_proxy_async();
       tc_fence_before();
       mbar_arrive(aready);
-      // prefetch the next tile's rows while the tensor core works
-      const RowIn now = cur;
-      if (t + 1 < my_tiles) cur = load_row(a, (tile + gridDim.x) * kRaysPerTile + ray, n_items, trace_state);
       // ---- hidden layers ----
       float acc_out = 0.0f;
       for (int h = 0; h < n_hidden; ++h) {
         const bool last = h == n_hidden - 1;
-        mbar_wait(dfull, dfull_phase);
+        mbar_wait(dfull, dfull_phase, a.suspend_ns);
         dfull_phase ^= 1;
         tc_fence_after();
         const float* bias = sm.bias + size_t(h + 1) * W;
-        const float zs = net.turns * net.wscale[h];  // undo the 2^k weight scaling
+        const float zs = net.omega * net.wscale[h];  // radians; undoes the 2^k weight scaling
         const float dscale = net.omega * net.wscale[h];
 #pragma unroll 1
         for (int c = 0; c < kCols; c += 16) {
@@ -497,12 +603,12 @@ __global__ void __launch_bounds__(64 + 128 * kGroups, (W == 64 ? 3 : (kGroups > 
             if (kGrad) {
               const float z = fmaf(v[j], zs, bias[cc + j]);
               float s = 0.0f, cs = 0.0f;
-              if (chain == 0) sincos_turns(z, s, cs);
+              if (chain == 0) fast_sincos(z, s, cs);
               // tangent rows: G = (W.G_prev) * omega cos(z); D carries the 2^k weight scale
               const float dphi = __shfl_sync(group_mask, dscale * cs, lane & ~3, 32);
               v[j] = chain == 0 ? s : v[j] * dphi;
             } else {
-              v[j] = sin_turns(fmaf(v[j], zs, bias[cc + j]));
+              v[j] = fast_sin(fmaf(v[j], zs, bias[cc + j]));
             }
           }
           if (!last) {
@@ -534,46 +640,52 @@ __global__ void __launch_bounds__(64 + 128 * kGroups, (W == 64 ? 3 : (kGroups > 
         if (eg == 0)
           for (int g = 1; g < kGroups; ++g) acc_out += part[(g - 1) * kRows + row];
       }
-      if (eg != 0) continue;
-      // ---- consumer (group 0) ----
-      const float fval = (!kGrad || chain == 0) ? acc_out + net.bout : acc_out;
-      if (a.op == kOpTrace) {
-        bool conv = false, cont = false;
-        if (valid)
-          tc_trace_update(a, now.slot, fval, now.p[0], now.p[1], now.p[2], now.t, now.dx, now.dy, now.dz, conv, cont);
-        warp_append(conv, now.slot, a.adv_list, a.adv_count);
-        warp_append(cont, now.slot, a.next_list, a.next_count);
-      } else if (kGrad) {
-        const int base = lane & ~3;
-        const float gx = __shfl_sync(0xffffffffu, fval, base + 1);
-        const float gy = __shfl_sync(0xffffffffu, fval, base + 2);
-        const float gz = __shfl_sync(0xffffffffu, fval, base + 3);
-        const float f = __shfl_sync(0xffffffffu, fval, base);
-        bool defer = false;
-        const bool lead = chain == 0 && valid;
-        if (a.op == kOpNormals) {
-          if (lead) {
-            float nrm[3];
-            if (!normalize_normal(gx, gy, gz, nrm)) {
-              nrm[0] = 0.0f;
-              nrm[1] = 1.0f;
-              nrm[2] = 0.0f;
-              defer = a.defer_fallback != 0;
+      if (eg == 0) {
+        // ---- consumer (group 0) ----
+        const float fval = (!kGrad || chain == 0) ? acc_out + net.bout : acc_out;
+        if (a.op == kOpTrace) {
+          bool conv = false, cont = false;
+          if (valid)
+            tc_trace_update(a, now.slot, fval, now.p[0], now.p[1], now.p[2], now.t, now.dx, now.dy, now.dz, conv,
+                            cont);
+          stage_append(conv, now.slot, st_adv);
+          stage_append(cont, now.slot, st_next);
+          const bool last_tile = t + 1 == my_tiles;
+          stage_flush(st_adv, a.adv_list, a.adv_count, sm.stage_base, ctid, last_tile);
+          stage_flush(st_next, a.next_list, a.next_count, sm.stage_base, ctid, last_tile);
+        } else if (kGrad) {
+          const int base = lane & ~3;
+          const float gx = __shfl_sync(0xffffffffu, fval, base + 1);
+          const float gy = __shfl_sync(0xffffffffu, fval, base + 2);
+          const float gz = __shfl_sync(0xffffffffu, fval, base + 3);
+          const float f = __shfl_sync(0xffffffffu, fval, base);
+          bool defer = false;
+          const bool lead = chain == 0 && valid;
+          if (a.op == kOpNormals) {
+            if (lead) {
+              float nrm[3];
+              if (!normalize_normal(gx, gy, gz, nrm)) {
+                nrm[0] = 0.0f;
+                nrm[1] = 1.0f;
+                nrm[2] = 0.0f;
+                defer = a.defer_fallback != 0;
+              }
+              if (!defer) shade_and_write(a.sp, a.st, now.slot, nrm, a.rgb, a.depth, a.mask);
             }
-            if (!defer) shade_and_write(a.sp, a.st, now.slot, nrm, a.rgb, a.depth, a.mask);
+            warp_append(defer, now.slot, a.fb_list, a.fb_count);
+          } else if (lead) {
+            if (a.out) a.out[item] = f;
+            if (a.grad) {
+              a.grad[item] = gx;
+              a.grad[size_t(a.k) + item] = gy;
+              a.grad[size_t(2) * a.k + item] = gz;
+            }
           }
-          warp_append(defer, now.slot, a.fb_list, a.fb_count);
-        } else if (lead) {
-          if (a.out) a.out[item] = f;
-          if (a.grad) {
-            a.grad[item] = gx;
-            a.grad[size_t(a.k) + item] = gy;
-            a.grad[size_t(2) * a.k + item] = gz;
-          }
+        } else if (valid) {
+          a.out[item] = fval;
         }
-      } else if (valid) {
-        a.out[item] = fval;
       }
+      now = next;
     }
   }
   // ---- teardown ----
@@ -586,12 +698,12 @@ __global__ void __launch_bounds__(64 + 128 * kGroups, (W == 64 ? 3 : (kGroups > 
   }
 }
 
-template <int W, bool kGrad, int kTerms>
+template <int W, bool kGrad, int kTerms, bool kResident>
 bool launch_w(TcArgs& a, int n_max_items, cudaStream_t s) {
   constexpr int kGroups = W == 64 ? 1 : (W == 256 && kTerms == 3 ? 4 : 2);
-  constexpr int kThreads = 64 + 128 * kGroups;
-  auto kernel = tc_mlp_kernel<W, kGrad, kGroups, kTerms>;
-  const size_t smem = tc_smem_bytes(W, a.net.n_layers, kTerms);
+  constexpr int kThreads = 32 * (kResident ? 1 : 2) + 128 * kGroups;
+  auto kernel = tc_mlp_kernel<W, kGrad, kGroups, kTerms, kResident>;
+  const size_t smem = tc_smem_bytes(W, a.net.n_layers, kTerms, kResident);
   static size_t configured_smem = 0;
   static int per_sm = 0;
   static int sms = 0;
@@ -613,8 +725,8 @@ bool launch_w(TcArgs& a, int n_max_items, cudaStream_t s) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     configured_smem = smem;
     if (getenv("NSDF_DEBUG_TC"))
-      fprintf(stderr, "tc_mlp_kernel<%d,%d,%d,%d>: smem %zu B, regs %d, %d CTAs/SM (occupancy API %d)\n", W,
-              int(kGrad), kGroups, kTerms, smem, fa.numRegs, per_sm, occ);
+      fprintf(stderr, "tc_mlp_kernel<%d,%d,%d,%d,%d>: smem %zu B, regs %d, %d CTAs/SM (occupancy API %d)\n", W,
+              int(kGrad), kGroups, kTerms, int(kResident), smem, fa.numRegs, per_sm, occ);
   }
   const int tmem_limit = 512 / (W < 32 ? 32 : W);
   const int per = std::max(1, std::min(per_sm, tmem_limit));
@@ -627,16 +739,29 @@ bool launch_w(TcArgs& a, int n_max_items, cudaStream_t s) {
 
 template <bool kGrad, int kTerms>
 bool launch_terms(TcArgs& a, int n_max_items, cudaStream_t s) {
+  // 64-wide nets keep every hidden layer resident in SMEM when it fits (<= 4 layers).
+  const bool resident = a.net.width == 64 && a.net.n_layers - 2 <= 4;
   switch (a.net.width) {
-    case 64: return launch_w<64, kGrad, kTerms>(a, n_max_items, s);
-    case 128: return launch_w<128, kGrad, kTerms>(a, n_max_items, s);
-    case 256: return launch_w<256, kGrad, kTerms>(a, n_max_items, s);
+    case 64:
+      return resident ? launch_w<64, kGrad, kTerms, true>(a, n_max_items, s)
+                      : launch_w<64, kGrad, kTerms, false>(a, n_max_items, s);
+    case 128: return launch_w<128, kGrad, kTerms, false>(a, n_max_items, s);
+    case 256: return launch_w<256, kGrad, kTerms, false>(a, n_max_items, s);
     default: return false;
   }
 }
 
+uint32_t suspend_hint() {
+  static const uint32_t v = [] {
+    const char* e = getenv("NSDF_TC_SUSPEND_NS");
+    return e ? uint32_t(strtoul(e, nullptr, 0)) : 0u;
+  }();
+  return v;
+}
+
 template <bool kGrad>
 bool launch_any(TcArgs& a, int n_max_items, cudaStream_t s) {
+  a.suspend_ns = suspend_hint();
   return a.terms == 3 ? launch_terms<kGrad, 3>(a, n_max_items, s) : launch_terms<kGrad, 1>(a, n_max_items, s);
 }
 
@@ -646,7 +771,6 @@ TcNet tc_net(const DevNet& n) {
   t.width = n.rows[0];
   t.input_dim = n.input_dim;
   t.omega = n.omega;
-  t.turns = n.omega * kInv2Pi;
   t.wq = reinterpret_cast<const __half*>(n.wq);
   for (int l = 0; l < kMaxLayers; ++l) t.wscale[l] = n.wscale[l];
   t.w0 = n.w[0];
@@ -715,6 +839,9 @@ bool tc_eval(int terms, const DevField& f, const float* pts, int rows, int k, fl
   a.time = time;
   a.out = out;
   a.grad = grad;
+  // a 4-row batch carries a per-column time; the tiles fold a single slice time into the
+  // layer-0 bias, so such batches take the FFMA tiles
+  if (rows == 4) return false;
   if (grad) return launch_any<true>(a, k, s);
   return launch_any<false>(a, k, s);
 }
