@@ -37,7 +37,7 @@ PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustain
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--mode", default=os.environ.get("NSDF_MODE", "fp16"), choices=["fp16", "fp16low", "fp32"])
@@ -69,12 +69,12 @@ class ClockSampler:
         self.proc = None
 
     def __enter__(self):
-        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+        q = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
              "clocks_event_reasons.sw_power_cap")
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                          "--format=csv,noheader,nounits", "-lms", "20"],
                                          stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
@@ -84,7 +84,10 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.samples.append([x.strip() for x in line.split(",")])
+            self.samples.append((time.time(), [x.strip() for x in line.split(",")][1:]))
+
+    def mark(self, which):
+        setattr(self, which, time.time())
 
     def __exit__(self, *exc):
         if self.proc:
@@ -95,15 +98,24 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
-        if not self.samples:
+        """Samples taken inside the timed window [t0, t1] (widened to the nearest samples
+        when the window is shorter than the 20 ms sampling period)."""
+        t0, t1 = getattr(self, "t0", 0.0), getattr(self, "t1", time.time())
+        inside = [s for ts, s in self.samples if t0 <= ts <= t1]
+        window = "timed region"
+        if not inside and self.samples:
+            near = sorted(self.samples, key=lambda x: min(abs(x[0] - t0), abs(x[0] - t1)))[:3]
+            inside = [s for _, s in near]
+            window = "nearest samples (timed region shorter than the sampling period)"
+        if not inside:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
-        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        sm = [float(s[0]) for s in inside if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in inside if s[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for s in self.samples for i in range(4) if len(s) > 3 + i and
+        reasons = sorted({names[i] for s in inside for i in range(4) if len(s) > 3 + i and
                           s[3 + i].lower().startswith("active")})
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.samples)}
+                "reasons": reasons, "samples": len(inside), "window": window}
 
 
 def frame_flops(seq, stats):
@@ -224,23 +236,25 @@ def main():
     st = ctx.render_device(levels, cam, cfg, shade, rgb.data_ptr(), depth.data_ptr(), mask.data_ptr(), src, -1,
                            args.tile, rank, world, stats=True)
     flops_trace, flops_normals = frame_flops(seq, st)
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    ctx.set_profiling(True)
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clocks:
+        for _ in range(args.warmup):
+            step()
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
+        ctx.set_profiling(True)
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        clocks.mark("t0")
         e0.record(stream)
         for _ in range(args.steps):
             step()
         e1.record(stream)
         torch.cuda.synchronize()
+        clocks.mark("t1")
     prof = ctx.get_profile()
     ctx.set_profiling(False)
     ms_total = e0.elapsed_time(e1)
@@ -261,8 +275,11 @@ def main():
     # e2e through the C ABI with host buffers (nsdf_cuda_render: D2H of the framebuffer inside)
     e2e = None
     if not args.no_e2e:
-        h_rgb = np.zeros(npix * 3, np.float32)
-        ctx.render(levels, cam, cfg, shade, src)  # warm
+        # caller-owned pinned host framebuffer: the D2H of every frame is inside the timing
+        h_rgb = torch.empty(npix * 3, dtype=torch.float32, pin_memory=True)
+        h_depth = torch.empty(npix, dtype=torch.float32, pin_memory=True)
+        h_mask = torch.empty(npix, dtype=torch.uint8, pin_memory=True)
+        ctx.render_into(levels, cam, cfg, shade, h_rgb.data_ptr(), h_depth.data_ptr(), h_mask.data_ptr(), src)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
@@ -276,7 +293,8 @@ def main():
                 if rank == 0:
                     gather.to_host()
             else:
-                ctx.render(levels, cam, cfg, shade, src)
+                ctx.render_into(levels, cam, cfg, shade, h_rgb.data_ptr(), h_depth.data_ptr(), h_mask.data_ptr(),
+                                src)
         f1.record(stream)
         torch.cuda.synchronize()
         wall = (time.perf_counter() - w0) * 1e3
@@ -285,11 +303,11 @@ def main():
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e_ms = float(te.item())
-        del h_rgb
+        del h_rgb, h_depth, h_mask
         level_bytes = 16 * len(levels) + 4 * 8 + 128 + 272  # camera + configs + level table
         e2e = {"value": npix * args.steps / (e_ms / 1e3) / 1e6, "unit": "Mrays/s", "ms_per_frame": e_ms / args.steps,
                "h2d_bytes_per_step": level_bytes, "d2h_bytes_per_step": npix * (12 + 4 + 1),
-               "path": "nsdf_cuda_render (C ABI, host framebuffer)" if world == 1 else
+               "path": "nsdf_cuda_render (C ABI) into a pinned host framebuffer" if world == 1 else
                        "nsdf_cuda_render_device per rank + NCCL tile gather + D2H on rank 0"}
 
     cpu = None

@@ -174,6 +174,14 @@ class Context:
         return rgb.reshape(cam.height, cam.width, 3), depth.reshape(cam.height, cam.width), \
             mask.reshape(cam.height, cam.width), st
 
+    def render_into(self, levels, cam: Camera, trace: TraceConfig, shade: ShadeConfig, h_rgb: int, h_depth: int,
+                    h_mask: int, normal_source=0, fine_index=-1):
+        """nsdf_cuda_render into caller-owned HOST buffers (raw pointers, e.g. pinned memory)."""
+        lv, m = _levels(levels)
+        check(self.lib.nsdf_cuda_render(self._ctx, lv, m, ctypes.byref(cam), ctypes.byref(trace), ctypes.byref(shade),
+                                        normal_source, fine_index, ctypes.c_void_p(h_rgb), ctypes.c_void_p(h_depth),
+                                        ctypes.c_void_p(h_mask), None))
+
     def render_device(self, levels, cam, trace, shade, d_rgb: int, d_depth: int, d_mask: int, normal_source=0,
                       fine_index=-1, tile_size=64, tile_rank=0, tile_world=1, stats: bool = False):
         """Device framebuffer (raw device pointers, e.g. torch tensor .data_ptr()); async."""
