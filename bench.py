@@ -1,18 +1,25 @@
 #!/usr/bin/env python3
 """Benchmark: Mrays/s & ms/frame at 1080p, multiscale sphere tracing + analytic normals.
 
-Workload (BASELINE.json configs[1]): the nested 3-level SIREN
+Default workload (BASELINE.json configs[1]): the nested 3-level SIREN
 sequence 64x1 > 128x2 > 256x3 (omega0 = 30, Prop-2 certified, assets/torus_w30.nest) traced
 at 1920x1080 from the standard camera with budgets (20,5,5), own analytic normals from the
 256x3 net, Lambert + Blinn-Phong (specular 0.3, the `nsdf bench` shading,
 nsdf_main.cpp:446).  One step = one whole frame: rays -> multiscale trace -> normals ->
 shade -> framebuffer.  Weights are resident (uploaded once; broadcast over NCCL for N>1);
-the per-frame ray state (~200 MB at 1080p) exceeds the 126 MB L2, so no flush is needed.
+the per-frame working set (ray state + lists + framebuffer, ~160 MB at 1080p) exceeds the
+126 MB L2, so no flush is needed between steps.
+
+--config 1|3|4|5 selects the other BASELINE workloads (1: single 256x3 at 512^2; 3: neural
+normal mapping 64x1 (40,0) + 256x3 normals at 1080p; 4: torus-mesh G-buffer -> 256x3 normals
+at 2560x1440; 5: animated 4-D 64x1 > 128x2 blend, 120 frames at 3840x2160, frames sharded
+across ranks).
 
 N > 1 (torchrun): image tiles are interleaved across ranks (tile t -> rank t % N, the
 frame/tile scheduler of SURVEY.md §8e) and rank 0 gathers the packed tiles over NCCL:
-strong scaling of one frame.  --impl reference times the reference's own CPU renderer
-(oracle/_ref/libnsdf_ref.so, all host threads) on the same config.
+strong scaling of one frame (config 5: whole frames per rank, no gather).
+--impl reference times the reference's own CPU renderer (oracle/_ref/libnsdf_ref.so, all
+host threads) on the same config.
 """
 from __future__ import annotations
 
@@ -21,6 +28,7 @@ import json
 import os
 import subprocess
 import sys
+import tempfile
 import threading
 import time
 
@@ -29,9 +37,28 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-MANIFEST = os.path.join(ROOT, "assets", "torus_w30.nest")
-METRIC = "Mrays/s & ms/frame at 1080p (multiscale ST + analytic normals)"
+TORUS = os.path.join(ROOT, "assets", "torus_w30.nest")
+BLEND = os.path.join(ROOT, "assets", "blend4d_w30.nest")
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+CONFIGS = {
+    1: dict(manifest=TORUS, members=[2], budgets="40", normals="own", res=(512, 512),
+            metric="Mrays/s & ms/frame at 512x512 (single 256x3 SIREN ST + analytic normals)",
+            desc="config1: single 256x3 SIREN (torus, omega0=30), 512x512, budgets ({b}), own analytic normals"),
+    2: dict(manifest=TORUS, members=[0, 1, 2], budgets="20,5,5", normals="own", res=(1920, 1080),
+            metric="Mrays/s & ms/frame at 1080p (multiscale ST + analytic normals)",
+            desc="config2: nested 64x1>128x2>256x3 SIREN (torus, omega0=30), 1920x1080, budgets ({b}), "
+                 "own analytic normals, specular 0.3"),
+    3: dict(manifest=TORUS, members=[0, 2], budgets="40,0", normals="mapped", res=(1920, 1080),
+            metric="Mrays/s & ms/frame at 1080p (neural normal mapping: 64x1 traced, 256x3 normals)",
+            desc="config3: 64x1 traced with budgets ({b}), normals mapped from 256x3, 1920x1080"),
+    4: dict(manifest=TORUS, members=[2], kind="gbuffer", res=(2560, 1440),
+            metric="Mnormals/s & ms/frame at 2560x1440 (mesh G-buffer -> neural normals)",
+            desc="config4: torus mesh (96x48 quads) G-buffer at 2560x1440 -> 256x3 neural normal map"),
+    5: dict(manifest=BLEND, members=[0, 1], budgets="20,10", normals="own", res=(3840, 2160), frames=120,
+            metric="Mrays/s & ms/frame at 3840x2160 (animated 4-D SIREN, 120 frames)",
+            desc="config5: animated 4-D 64x1>128x2 blend, 120 frames t=i/119 at 3840x2160, budgets ({b})"),
+}
 
 
 def parse():
@@ -40,16 +67,22 @@ def parse():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=2, choices=sorted(CONFIGS))
     ap.add_argument("--mode", default=os.environ.get("NSDF_MODE", "fp16"), choices=["fp16", "fp16low", "fp32"])
-    ap.add_argument("--width", type=int, default=1920)
-    ap.add_argument("--height", type=int, default=1080)
-    ap.add_argument("--budgets", default="20,5,5")
-    ap.add_argument("--normals", default="own", choices=["own", "mapped"])
+    ap.add_argument("--width", type=int, default=0)
+    ap.add_argument("--height", type=int, default=0)
+    ap.add_argument("--budgets", default="")
     ap.add_argument("--tile", type=int, default=64)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--cpu-frames", type=int, default=1)
-    return ap.parse_args()
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    args.width = args.width or cfg["res"][0]
+    args.height = args.height or cfg["res"][1]
+    args.budgets = args.budgets or cfg.get("budgets", "")
+    args.normals = cfg.get("normals", "own")
+    args.cfg = cfg
+    return args
 
 
 def peaks():
@@ -118,71 +151,159 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(inside), "window": window}
 
 
-def frame_flops(seq, stats):
+def sub_manifest(args):
+    """A .nest listing the selected members (absolute weight paths) for the reference."""
+    with open(args.cfg["manifest"]) as f:
+        j = json.load(f)
+    base = os.path.dirname(args.cfg["manifest"])
+    members = args.cfg["members"]
+    j["fields"] = [dict(j["fields"][i], weights=os.path.join(base, j["fields"][i]["weights"])) for i in members]
+    j["deltas"] = [j["deltas"][i] for i in members]
+    fd, path = tempfile.mkstemp(suffix=".nest")
+    with os.fdopen(fd, "w") as f:
+        json.dump(j, f)
+    return path
+
+
+def workload_text(args):
+    return args.cfg["desc"].format(b=args.budgets)
+
+
+def frame_flops(seq, stats, normal_idx):
     """Algorithmic FLOPs of one frame: 2 x MACs, no credit for bias/sine."""
     trace = sum(int(stats.evals[j]) * 2 * seq.members[j].macs_forward() for j in range(len(seq.members)))
-    normal_net = seq.members[-1]  # own normals from the effective final level (finest here)
-    normals = int(stats.normal_evals) * 2 * normal_net.macs_normal()
+    normals = int(stats.normal_evals) * 2 * seq.members[normal_idx].macs_normal()
+    normals += int(stats.fallback_evals) * 2 * seq.members[-1].macs_normal()
     return trace, normals
 
 
-def run_reference(args):
-    """--impl reference: the reference CPU renderer (oracle/_ref, all host threads)."""
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
-        return
+def gbuffer_points(ctx, args):
+    """Device G-buffer of the torus mesh: hit positions (3 x k, device tensor)."""
+    import torch
+    from paper_2201_09147_b200.abi import standard_camera
+    from paper_2201_09147_b200.meshes import torus_mesh
+    cam = standard_camera(args.width, args.height)
+    n = args.width * args.height
+    pos = torch.zeros(3 * n, dtype=torch.float32, device="cuda")
+    mask = torch.zeros(n, dtype=torch.uint8, device="cuda")
+    v, t = torus_mesh()
+    ctx.raycast_mesh(cam, v, t, pos.data_ptr(), mask.data_ptr())
+    return pos.view(3, n)[:, mask.bool()].contiguous()
+
+
+def reference_time(args, gbuffer_pts=None):
+    """One bounded sample of the workload on the reference CPU path (oracle/_ref, all host
+    threads); returns (seconds, units, sample text, cores)."""
     from oracle import refshim
     from paper_2201_09147_b200.abi import ShadeConfig, TraceConfig, standard_camera
-    budgets = tuple(int(b) for b in args.budgets.split(","))
-    cam = standard_camera(args.width, args.height)
-    cfg = TraceConfig(budgets)
-    shade = ShadeConfig(specular=0.3)
-    src = 1 if args.normals == "mapped" else 0
+    from paper_2201_09147_b200.manifest import load_manifest
     refshim.set_backend("avx2")
-    times = []
-    # each step is one full frame; warm-up capped at one frame to keep the run bounded
-    for i in range(min(args.warmup, 1) + args.steps):
-        _, _, mask, sec = refshim.render(MANIFEST, cam, cfg, shade, src)
-        if i >= min(args.warmup, 1):
-            times.append(sec)
-    ms = 1000.0 * float(np.mean(times))
-    mrays = args.width * args.height / (ms / 1000.0) / 1e6
     cores = refshim.worker_threads()
-    line = {"impl": "reference", "metric": METRIC, "value": mrays, "unit": "Mrays/s", "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": min(args.warmup, 1), "ms_per_step": ms, "higher_is_better": True,
+    man = sub_manifest(args)
+    try:
+        if args.cfg.get("kind") == "gbuffer":
+            if gbuffer_pts is None:
+                raise RuntimeError("the config-4 sample needs the device G-buffer positions")
+            pts = gbuffer_pts[:, :60000]
+            delta = load_manifest(args.cfg["manifest"]).deltas[args.cfg["members"][0]]
+            t0 = time.perf_counter()
+            refshim.normal_map(man, 0, pts, delta)
+            sec = time.perf_counter() - t0
+            return sec, pts.shape[1], (f"neural_normal_map on {pts.shape[1]} of the 2560x1440 G-buffer hits, "
+                                       f"reference library, {cores} threads"), cores
+        cam = standard_camera(args.width, args.height)
+        budgets = tuple(int(b) for b in args.budgets.split(","))
+        src = 1 if args.normals == "mapped" else 0
+        tm = 0.5 if args.config == 5 else 0.0
+        _, _, _, sec = refshim.render(man, cam, TraceConfig(budgets), ShadeConfig(specular=0.3), src, -1, time=tm)
+        text = f"one full {args.width}x{args.height} frame"
+        if args.config == 5:
+            text += " (t=0.5; the 120-frame sequence scales linearly)"
+        return sec, args.width * args.height, text + f", reference shading::render (oracle/_ref, AVX2, {cores} threads)", cores
+    finally:
+        os.unlink(man)
+
+
+def run_reference(args):
+    """--impl reference: the reference CPU path (oracle/_ref, all host threads)."""
+    if int(os.environ.get("RANK", "0")) != 0:
+        return
+    pts = None
+    if args.cfg.get("kind") == "gbuffer":
+        from paper_2201_09147_b200.engine import Context
+        ctx = Context(0, "fp32")
+        pts = gbuffer_points(ctx, args).cpu().numpy()
+        ctx.close()
+    warm = min(args.warmup, 1)
+    times = []
+    for i in range(warm + min(args.steps, 10)):
+        sec, units, sample, cores = reference_time(args, pts)
+        if i >= warm:
+            times.append(sec)
+    sec = float(np.mean(times))
+    value = units / sec / 1e6
+    unit = "Mnormals/s" if args.cfg.get("kind") == "gbuffer" else "Mrays/s"
+    line = {"impl": "reference", "metric": args.cfg["metric"], "value": value, "unit": unit, "n_gpus": args.gpus,
+            "steps": len(times), "warmup": warm, "ms_per_step": sec * 1e3, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": f"config2 nested 64x1>128x2>256x3 torus w30, {args.width}x{args.height}, "
-                                   f"budgets {args.budgets}, normals {args.normals}",
-                       "budgets": args.budgets, "resolution": f"{args.width}x{args.height}"},
-            "cpu_baseline": {"value": mrays, "unit": "Mrays/s", "cores": cores, "kind": "reference",
-                             "sample": f"full {args.width}x{args.height} frame per step, shading::render of the "
-                                       f"reference library (AVX2 backend, {cores} threads)"},
-            "e2e": {"value": mrays, "unit": "Mrays/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-            "hit_pixels": int(mask.sum())}
+            "config": {"workload": workload_text(args), "config": args.config,
+                       "resolution": f"{args.width}x{args.height}", "budgets": args.budgets},
+            "cpu_baseline": {"value": value, "unit": unit, "cores": cores, "kind": "reference", "sample": sample},
+            "e2e": {"value": value, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
-def cpu_baseline(args, budgets, src):
-    """Reference CPU renderer on this host, bounded: one full frame (~10-30 s)."""
-    try:
-        from oracle import refshim
-        from paper_2201_09147_b200.abi import ShadeConfig, TraceConfig, standard_camera
-        if not refshim.available():
-            raise OSError("oracle/_ref/libnsdf_ref.so missing")
-        refshim.set_backend("avx2")
-        cam = standard_camera(args.width, args.height)
-        secs = []
-        for _ in range(args.cpu_frames):
-            _, _, _, sec = refshim.render(MANIFEST, cam, TraceConfig(budgets), ShadeConfig(specular=0.3), src)
-            secs.append(sec)
-        sec = float(np.mean(secs))
-        cores = refshim.worker_threads()
-        return {"value": args.width * args.height / sec / 1e6, "unit": "Mrays/s", "cores": cores,
-                "kind": "reference", "ms_per_frame": sec * 1e3,
-                "sample": f"{args.cpu_frames} full {args.width}x{args.height} frame(s), reference shading::render "
-                          f"(oracle/_ref, AVX2, {cores} threads)"}
-    except Exception as e:  # reported, never silently replaced
-        return {"value": None, "unit": "Mrays/s", "cores": 0, "kind": "reference", "sample": f"unavailable: {e}"}
+def run_e2e(args, ctx, ds, seq, stream, world, rank, W):
+    """Same metric through the C ABI with HOST buffers: pinned host framebuffer (render) or
+    host point/normal arrays (normal map); every step's D2H is inside the timing."""
+    import torch
+    import torch.distributed as dist
+    npix = args.width * args.height
+    steps = args.steps
+    if W["gbuffer"]:
+        pts = W["pts"].cpu().numpy()
+        k = pts.shape[1]
+        delta = float(seq.deltas[0])
+        ctx.normal_map(ds.handles[0], pts, delta)
+        w0 = time.perf_counter()
+        for _ in range(steps):
+            ctx.normal_map(ds.handles[0], pts, delta)
+        e_ms = (time.perf_counter() - w0) * 1e3
+        return {"value": k * steps / (e_ms / 1e3) / 1e6, "unit": "Mnormals/s", "ms_per_frame": e_ms / steps,
+                "h2d_bytes_per_step": 12 * k, "d2h_bytes_per_step": 12 * k + 16,
+                "path": "nsdf_cuda_normal_map (C ABI, host points -> host normals)"}
+    cam, cfg, shade, src, levels = W["cam"], W["cfg"], W["shade"], W["src"], W["levels"]
+    h_rgb = torch.empty(npix * 3, dtype=torch.float32, pin_memory=True)
+    h_depth = torch.empty(npix, dtype=torch.float32, pin_memory=True)
+    h_mask = torch.empty(npix, dtype=torch.uint8, pin_memory=True)
+    ctx.render_into(levels, cam, cfg, shade, h_rgb.data_ptr(), h_depth.data_ptr(), h_mask.data_ptr(), src)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    f0 = torch.cuda.Event(enable_timing=True)
+    f1 = torch.cuda.Event(enable_timing=True)
+    f0.record(stream)
+    w0 = time.perf_counter()
+    for i in range(steps):
+        if world > 1:
+            W["step"](i)
+            if rank == 0:
+                W["gather"].to_host()
+        else:
+            ctx.render_into(levels, cam, cfg, shade, h_rgb.data_ptr(), h_depth.data_ptr(), h_mask.data_ptr(), src)
+    f1.record(stream)
+    torch.cuda.synchronize()
+    wall = (time.perf_counter() - w0) * 1e3
+    e_ms = max(f0.elapsed_time(f1), wall)
+    te = torch.tensor([e_ms], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+    e_ms = float(te.item())
+    level_bytes = 16 * len(levels) + 4 * 8 + 128 + 272  # camera + configs + level table
+    return {"value": npix * steps / (e_ms / 1e3) / 1e6, "unit": "Mrays/s", "ms_per_frame": e_ms / steps,
+            "h2d_bytes_per_step": level_bytes, "d2h_bytes_per_step": npix * (12 + 4 + 1),
+            "path": "nsdf_cuda_render (C ABI) into a pinned host framebuffer" if world == 1 else
+                    "nsdf_cuda_render_device per rank + NCCL tile gather + D2H on rank 0"}
 
 
 def main():
@@ -201,46 +322,75 @@ def main():
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
-    from paper_2201_09147_b200.abi import FrameStats, ShadeConfig, TraceConfig, standard_camera
+    from paper_2201_09147_b200.abi import ShadeConfig, TraceConfig, standard_camera
     from paper_2201_09147_b200.engine import Context, DeviceSequence
-    from paper_2201_09147_b200.manifest import load_manifest
     from paper_2201_09147_b200 import scheduler
 
-    budgets = tuple(int(b) for b in args.budgets.split(","))
-    src = 1 if args.normals == "mapped" else 0
-    seq = scheduler.broadcast_sequence(MANIFEST if rank == 0 else None, world, rank)
-    cam = standard_camera(args.width, args.height)
-    cfg = TraceConfig(budgets)
-    shade = ShadeConfig(specular=0.3)
-    W, H = args.width, args.height
-    npix = W * H
+    cfgw = args.cfg
+    seq = scheduler.broadcast_sequence(cfgw["manifest"] if rank == 0 else None, world, rank)
+    seq = seq.subsequence(cfgw["members"])
+    Wd, Hd = args.width, args.height
+    npix = Wd * Hd
+    W = {"cam": standard_camera(Wd, Hd), "shade": ShadeConfig(specular=0.3),
+         "src": 1 if args.normals == "mapped" else 0, "gbuffer": cfgw.get("kind") == "gbuffer"}
+    animated = "frames" in cfgw
 
     ctx = Context(local, args.mode)
     stream = torch.cuda.Stream()          # the engine's launch stream; events are recorded on it
     torch.cuda.set_stream(stream)
     ctx.set_stream(stream.cuda_stream)
     ds = DeviceSequence(ctx, seq)
-    levels = ds.levels()
-    rgb = torch.zeros(npix * 3, dtype=torch.float32, device="cuda")
-    depth = torch.zeros(npix, dtype=torch.float32, device="cuda")
-    mask = torch.zeros(npix, dtype=torch.uint8, device="cuda")
-    gather = scheduler.TileGather(W, H, args.tile, rank, world) if world > 1 else None
+    steps = args.steps
+    stats = None
 
-    def step():
-        ctx.render_device(levels, cam, cfg, shade, rgb.data_ptr(), depth.data_ptr(), mask.data_ptr(), src, -1,
-                          args.tile, rank, world)
-        if gather is not None:
-            gather(rgb, depth, mask)
+    if W["gbuffer"]:
+        pts = gbuffer_points(ctx, args)
+        W["pts"] = pts
+        k = pts.shape[1]
+        units_per_step = k
+        normals = torch.zeros_like(pts)
+        counts = torch.zeros(2, dtype=torch.int64, device="cuda")
+        delta = float(seq.deltas[0])
 
-    # accounting frame (not timed): per-level evaluation counts -> algorithmic FLOPs
-    st = ctx.render_device(levels, cam, cfg, shade, rgb.data_ptr(), depth.data_ptr(), mask.data_ptr(), src, -1,
-                           args.tile, rank, world, stats=True)
-    flops_trace, flops_normals = frame_flops(seq, st)
+        def step(i=0):
+            ctx.normal_map_device(ds.handles[0], pts.data_ptr(), k, delta, normals.data_ptr(), counts.data_ptr())
+    else:
+        units_per_step = npix
+        budgets = tuple(int(b) for b in args.budgets.split(","))
+        W["cfg"] = cfg = TraceConfig(budgets)
+        rgb = torch.zeros(npix * 3, dtype=torch.float32, device="cuda")
+        depth = torch.zeros(npix, dtype=torch.float32, device="cuda")
+        mask = torch.zeros(npix, dtype=torch.uint8, device="cuda")
+        if animated:
+            # frames t_i = i/(n-1) (nsdf_main.cpp:308-324); frame i renders on rank i % world
+            n_frames = cfgw["frames"]
+            my_frames = [i for i in range(n_frames) if i % world == rank]
+            steps = len(my_frames)
+            frame_levels = [ds.levels(time=i / (n_frames - 1)) for i in my_frames]
+            W["levels"] = frame_levels[0]
+        else:
+            W["levels"] = ds.levels()
+        gather = scheduler.TileGather(Wd, Hd, args.tile, rank, world) if world > 1 and not animated else None
+        W["gather"] = gather
+        tile_world, tile_rank = (1, 0) if animated else (world, rank)
+
+        def step(i=0):
+            lv = frame_levels[i % len(frame_levels)] if animated else W["levels"]
+            ctx.render_device(lv, W["cam"], cfg, W["shade"], rgb.data_ptr(), depth.data_ptr(), mask.data_ptr(),
+                              W["src"], -1, args.tile, tile_rank, tile_world)
+            if gather is not None:
+                gather(rgb, depth, mask)
+
+        # accounting frame (not timed): per-level evaluation counts -> algorithmic FLOPs
+        stats = ctx.render_device(W["levels"], W["cam"], cfg, W["shade"], rgb.data_ptr(), depth.data_ptr(),
+                                  mask.data_ptr(), W["src"], -1, args.tile, tile_rank, tile_world, stats=True)
+    W["step"] = step
+
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clocks:
-        for _ in range(args.warmup):
-            step()
+        for i in range(args.warmup):
+            step(i)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
@@ -250,8 +400,8 @@ def main():
             dist.barrier()
         clocks.mark("t0")
         e0.record(stream)
-        for _ in range(args.steps):
-            step()
+        for i in range(steps):
+            step(i)
         e1.record(stream)
         torch.cuda.synchronize()
         clocks.mark("t1")
@@ -262,82 +412,68 @@ def main():
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_total = float(t.item())
-    ms_per_frame = ms_total / args.steps
-    value = npix * args.steps / (ms_total / 1e3) / 1e6
+    if animated:
+        total_units = units_per_step * cfgw["frames"]              # all frames, all ranks
+    elif W["gbuffer"]:
+        total_units = units_per_step * steps * world               # every rank maps its own G-buffer
+    else:
+        total_units = units_per_step * steps                       # tiles of the same frames
+    ms_per_frame = ms_total / steps
+    value = total_units / (ms_total / 1e3) / 1e6
+    unit = "Mnormals/s" if W["gbuffer"] else "Mrays/s"
 
-    # roofline of the dominant kernel family: the trace-iteration MLP tiles
-    trace_ms = sum(prof.level_ms) / max(prof.frames, 1)
-    normals_ms = prof.normals_ms / max(prof.frames, 1)
     pk, pk_kind = peaks()
     peak_tf = pk.get("bf16_tflops_sustained", pk["bf16_tflops"])
-    achieved_tf = flops_trace / (trace_ms / 1e3) / 1e12 if trace_ms > 0 else 0.0
+    if W["gbuffer"]:
+        flops_trace, flops_normals = 0, units_per_step * 2 * seq.members[0].macs_normal()
+        achieved_tf = flops_normals / (ms_per_frame / 1e3) / 1e12
+        kernel = "fused fwd+3-tangent normal tiles (256x3)"
+        frame = {"points": units_per_step}
+    else:
+        normal_idx = len(seq.members) - 1 if W["src"] == 1 else max(j for j, b in enumerate(budgets) if b > 0)
+        flops_trace, flops_normals = frame_flops(seq, stats, normal_idx)
+        trace_ms = sum(prof.level_ms) / max(prof.frames, 1)
+        normals_ms = prof.normals_ms / max(prof.frames, 1)
+        achieved_tf = flops_trace / (trace_ms / 1e3) / 1e12 if trace_ms > 0 else 0.0
+        kernel = "trace-iteration MLP tiles (all levels)"
+        frame = {"evals_per_level": [int(x) for x in list(stats.evals)[:len(seq.members)]], "hits": int(stats.hits),
+                 "fallbacks": int(stats.fallback_evals), "tflop_trace": flops_trace / 1e12,
+                 "tflop_normals": flops_normals / 1e12, "trace_ms": trace_ms, "normals_ms": normals_ms,
+                 "profiled_frame_ms": prof.frame_ms / max(prof.frames, 1),
+                 "level_ms": [prof.level_ms[j] / max(prof.frames, 1) for j in range(len(seq.members))]}
 
-    # e2e through the C ABI with host buffers (nsdf_cuda_render: D2H of the framebuffer inside)
     e2e = None
-    if not args.no_e2e:
-        # caller-owned pinned host framebuffer: the D2H of every frame is inside the timing
-        h_rgb = torch.empty(npix * 3, dtype=torch.float32, pin_memory=True)
-        h_depth = torch.empty(npix, dtype=torch.float32, pin_memory=True)
-        h_mask = torch.empty(npix, dtype=torch.uint8, pin_memory=True)
-        ctx.render_into(levels, cam, cfg, shade, h_rgb.data_ptr(), h_depth.data_ptr(), h_mask.data_ptr(), src)
-        torch.cuda.synchronize()
-        if world > 1:
-            dist.barrier()
-        f0 = torch.cuda.Event(enable_timing=True)
-        f1 = torch.cuda.Event(enable_timing=True)
-        f0.record(stream)
-        w0 = time.perf_counter()
-        for _ in range(args.steps):
-            if world > 1:
-                step()
-                if rank == 0:
-                    gather.to_host()
-            else:
-                ctx.render_into(levels, cam, cfg, shade, h_rgb.data_ptr(), h_depth.data_ptr(), h_mask.data_ptr(),
-                                src)
-        f1.record(stream)
-        torch.cuda.synchronize()
-        wall = (time.perf_counter() - w0) * 1e3
-        e_ms = max(f0.elapsed_time(f1), wall)
-        te = torch.tensor([e_ms], dtype=torch.float64, device="cuda")
-        if world > 1:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        e_ms = float(te.item())
-        del h_rgb, h_depth, h_mask
-        level_bytes = 16 * len(levels) + 4 * 8 + 128 + 272  # camera + configs + level table
-        e2e = {"value": npix * args.steps / (e_ms / 1e3) / 1e6, "unit": "Mrays/s", "ms_per_frame": e_ms / args.steps,
-               "h2d_bytes_per_step": level_bytes, "d2h_bytes_per_step": npix * (12 + 4 + 1),
-               "path": "nsdf_cuda_render (C ABI) into a pinned host framebuffer" if world == 1 else
-                       "nsdf_cuda_render_device per rank + NCCL tile gather + D2H on rank 0"}
+    if not args.no_e2e and not animated:
+        e2e = run_e2e(args, ctx, ds, seq, stream, world, rank, W)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        cpu = cpu_baseline(args, budgets, src)
+        try:
+            gp = W["pts"].cpu().numpy() if W["gbuffer"] else None
+            sec, units, sample, cores = reference_time(args, gp)
+            cpu = {"value": units / sec / 1e6, "unit": unit, "cores": cores, "kind": "reference",
+                   "ms_per_frame": None if W["gbuffer"] else sec * 1e3, "sample": sample}
+        except Exception as e:  # reported, never silently replaced
+            cpu = {"value": None, "unit": unit, "cores": 0, "kind": "reference", "sample": f"unavailable: {e}"}
 
     if rank == 0:
-        launches = int(st.kernel_launches) * args.steps
+        launches = (int(stats.kernel_launches) if stats is not None else 1) * steps
         line = {
-            "metric": METRIC, "value": value, "unit": "Mrays/s", "n_gpus": world, "steps": args.steps,
+            "metric": cfgw["metric"], "value": value, "unit": unit, "n_gpus": world, "steps": steps,
             "warmup": args.warmup, "ms_per_step": ms_per_frame, "higher_is_better": True,
-            "scaling": "strong" if world > 1 else "weak", "vs_baseline": None,
-            "dtype": {"fp16": "split-fp16 tensor (3 MMA terms) / fp32 accum", "fp16low": "fp16 tensor / fp32 accum", "fp32": "f32"}[args.mode],
+            "scaling": "strong" if world > 1 and not W["gbuffer"] else "weak", "vs_baseline": None,
+            "dtype": {"fp16": "split-fp16 tensor (3 MMA terms) / fp32 accum", "fp16low": "fp16 tensor / fp32 accum",
+                      "fp32": "f32"}[args.mode],
             "data": "synthetic camera rays; committed fitted SIREN weights (assets/)",
-            "config": {"workload": f"config2: nested 64x1>128x2>256x3 SIREN (torus, omega0=30), {W}x{H}, "
-                                   f"budgets ({args.budgets}), {args.normals} analytic normals, specular 0.3",
-                       "resolution": f"{W}x{H}", "budgets": args.budgets, "mode": args.mode,
-                       "tile": args.tile, "parallelism": f"tiles{world}" if world > 1 else "single",
-                       "l2": "per-frame ray state ~200 MB > 126 MB L2; weights L2-resident by design"},
+            "config": {"workload": workload_text(args), "config": args.config, "resolution": f"{Wd}x{Hd}",
+                       "budgets": args.budgets, "mode": args.mode, "tile": args.tile,
+                       "parallelism": (f"frames{world}" if animated else f"tiles{world}") if world > 1 else "single",
+                       "l2": "per-frame working set (ray state, lists, framebuffer) > 126 MB L2; weights L2-resident"},
             "fps": 1000.0 / ms_per_frame,
-            "frame": {"evals_per_level": [int(x) for x in list(st.evals)[:len(levels)]], "hits": int(st.hits),
-                      "fallbacks": int(st.fallback_evals), "tflop_trace": flops_trace / 1e12,
-                      "tflop_normals": flops_normals / 1e12,
-                      "trace_ms": trace_ms, "normals_ms": normals_ms, "profiled_frame_ms": prof.frame_ms /
-                      max(prof.frames, 1),
-                      "level_ms": [prof.level_ms[j] / max(prof.frames, 1) for j in range(len(levels))]},
-            "roofline": {"bound": "tensor", "kernel": "trace-iteration MLP tiles (all levels)",
-                         "achieved": achieved_tf, "peak": peak_tf, "unit": "TFLOP/s",
-                         "frac": achieved_tf / peak_tf, "peak_kind": f"{pk_kind} bf16 sustained",
-                         "traffic": None,
+            "frame": frame,
+            "roofline": {"bound": "tensor", "kernel": kernel, "achieved": achieved_tf, "peak": peak_tf,
+                         "unit": "TFLOP/s", "frac": achieved_tf / peak_tf,
+                         "peak_kind": f"{pk_kind} bf16 sustained (MEASURED_PEAKS.json)", "traffic": None,
                          "whole_frame_tflops": (flops_trace + flops_normals) / (ms_per_frame / 1e3) / 1e12},
             "cpu_baseline": cpu,
             "e2e": e2e,

@@ -211,6 +211,17 @@ int nsdf_cuda_trace_image(nsdf_ctx* ctx, const nsdf_level* levels, int m,
 int nsdf_cuda_normal_map(nsdf_ctx* ctx, nsdf_field fine, float time, const float* points, int k,
                          double delta, const float* fallback_normals, float* normals,
                          uint64_t* outside_count, uint64_t* fallback_count);
+/* Device-pointer variant (async): points/normals/fallback 3 x k, counts = 2 x u64
+ * {outside, fallback} accumulated (zero them first).  Used for mesh G-buffers. */
+int nsdf_cuda_normal_map_device(nsdf_ctx* ctx, nsdf_field fine, float time, const float* d_points,
+                                int k, double delta, const float* d_fallback_normals,
+                                float* d_normals, uint64_t* d_counts);
+/* G-buffer of a triangle mesh (BASELINE config 4; the reference has no rasterizer): the
+ * nearest hit of every camera ray (generate_rays pixel centres) against the triangles,
+ * written as positions 3 x (W*H) (device) and a 0/1 mask (device).  Deterministic. */
+int nsdf_cuda_raycast_mesh(nsdf_ctx* ctx, const nsdf_camera* camera, const float* vertices,
+                           int n_vertices, const int32_t* triangles, int n_triangles,
+                           float* d_positions, uint8_t* d_mask);
 int nsdf_cuda_shade(nsdf_ctx* ctx, const float* points, const float* normals, int k,
                     const nsdf_shade_config* config, const nsdf_camera* camera, float* rgb);
 

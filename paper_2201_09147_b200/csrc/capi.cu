@@ -757,6 +757,45 @@ int nsdf_cuda_normal_map(nsdf_ctx* c, nsdf_field fine, float time, const float* 
   return NSDF_OK;
 }
 
+int nsdf_cuda_normal_map_device(nsdf_ctx* c, nsdf_field fine, float time, const float* d_points, int k,
+                                double delta, const float* d_fallback, float* d_normals, uint64_t* d_counts) {
+  if (!c || !d_points || !d_normals || !d_counts) return fail(NSDF_ERR_CONTRACT, "null argument");
+  std::lock_guard<std::mutex> lk(c->mu);
+  DeviceGuard g(c->device);
+  FieldRec* f;
+  if (int st = find_field(c, fine, &f)) return st;
+  if (k < 0) return fail(NSDF_ERR_CONTRACT, "points must be 3xk");
+  launch_normal_map(mode_of(c), f->dev, d_points, k, time, delta, d_fallback, d_normals,
+                    reinterpret_cast<unsigned long long*>(d_counts), c->stream);
+  NSDF_CUDA(cudaGetLastError());
+  return NSDF_OK;
+}
+
+int nsdf_cuda_raycast_mesh(nsdf_ctx* c, const nsdf_camera* camera, const float* vertices, int n_vertices,
+                           const int32_t* triangles, int n_triangles, float* d_positions, uint8_t* d_mask) {
+  if (!c || !vertices || !triangles || !d_positions || !d_mask) return fail(NSDF_ERR_CONTRACT, "null argument");
+  std::lock_guard<std::mutex> lk(c->mu);
+  DeviceGuard g(c->device);
+  CamBasis cb;
+  if (int st = camera_basis(camera, &cb)) return st;
+  if (n_triangles < 0 || n_vertices < 0) return fail(NSDF_ERR_CONTRACT, "negative mesh size");
+  std::vector<float> tv(size_t(n_triangles) * 9);
+  for (int t = 0; t < n_triangles; ++t)
+    for (int v = 0; v < 3; ++v) {
+      const int idx = triangles[3 * t + v];
+      if (idx < 0 || idx >= n_vertices) return fail(NSDF_ERR_CONTRACT, "triangle index out of range");
+      for (int a = 0; a < 3; ++a) tv[size_t(t) * 9 + v * 3 + a] = vertices[3 * idx + a];
+    }
+  size_t off = 0;
+  NSDF_CUDA(c->io.reserve(tv.size() * 4 + 4096));
+  float* dtv = carve<float>(c->io.base, off, tv.size());
+  NSDF_CUDA(cudaMemcpyAsync(dtv, tv.data(), tv.size() * 4, cudaMemcpyHostToDevice, c->stream));
+  launch_raycast_mesh(cb, dtv, n_triangles, d_positions, d_mask, c->stream);
+  NSDF_CUDA(cudaGetLastError());
+  NSDF_CUDA(cudaStreamSynchronize(c->stream));
+  return NSDF_OK;
+}
+
 int nsdf_cuda_shade(nsdf_ctx* c, const float* points, const float* normals, int k, const nsdf_shade_config* config,
                     const nsdf_camera* camera, float* rgb) {
   if (!c || !camera) return fail(NSDF_ERR_CONTRACT, "null argument");

@@ -625,7 +625,9 @@ void launch_eval(Mode mode, const DevField& f, const float* pts, int rows, int k
 void launch_normal_map(Mode mode, const DevField& f, const float* pts, int k, float time, double delta,
                        const float* fallback, float* normals, unsigned long long* counts, cudaStream_t s) {
   if (k <= 0) return;
-  (void)mode;
+  if (mode_tc(mode) && f.kind == kFieldMlp && tc_supported(f.net) &&
+      tc_normal_map(mode_terms(mode), f, pts, k, time, delta, fallback, normals, counts, s))
+    return;
   launch_eval_impl<true>(f, pts, 3, k, time, nullptr, normals, delta, fallback, counts, 1, s);
 }
 
@@ -641,6 +643,55 @@ __global__ void shade_kernel(const float* pts, const float* nrm, int k, ShadePar
 void launch_shade(const float* pts, const float* normals, int k, const ShadeParams& sp, float* rgb, cudaStream_t s) {
   if (k <= 0) return;
   shade_kernel<<<std::min((k + 255) / 256, num_sms() * 8), 256, 0, s>>>(pts, normals, k, sp, rgb);
+}
+
+// ---------------------------------------------------------------------------------------
+// Mesh G-buffer (config 4).  Triangles are staged through shared memory in blocks of 256;
+// each thread keeps its pixel's nearest positive hit.
+// ---------------------------------------------------------------------------------------
+__global__ void raycast_mesh_kernel(CamBasis c, const float* __restrict__ tv, int n_tri, float* pos, uint8_t* mask) {
+  __shared__ float tri[256 * 9];
+  const int npix = c.width * c.height;
+  const int pix = blockIdx.x * blockDim.x + threadIdx.x;
+  float d[3] = {0, 0, 1};
+  if (pix < npix) pixel_ray(c, pix % c.width, pix / c.width, d);
+  const float ox = c.origin[0], oy = c.origin[1], oz = c.origin[2];
+  float best = 3.0e38f;
+  for (int base = 0; base < n_tri; base += 256) {
+    const int cnt = min(256, n_tri - base);
+    __syncthreads();
+    for (int i = threadIdx.x; i < cnt * 9; i += blockDim.x) tri[i] = tv[size_t(base) * 9 + i];
+    __syncthreads();
+    for (int k = 0; k < cnt; ++k) {
+      const float* t = tri + k * 9;
+      const float e1x = t[3] - t[0], e1y = t[4] - t[1], e1z = t[5] - t[2];
+      const float e2x = t[6] - t[0], e2y = t[7] - t[1], e2z = t[8] - t[2];
+      const float px = d[1] * e2z - d[2] * e2y, py = d[2] * e2x - d[0] * e2z, pz = d[0] * e2y - d[1] * e2x;
+      const float det = e1x * px + e1y * py + e1z * pz;
+      if (fabsf(det) < 1e-12f) continue;
+      const float inv = 1.0f / det;
+      const float sx = ox - t[0], sy = oy - t[1], sz = oz - t[2];
+      const float u = (sx * px + sy * py + sz * pz) * inv;
+      if (u < 0.0f || u > 1.0f) continue;
+      const float qx = sy * e1z - sz * e1y, qy = sz * e1x - sx * e1z, qz = sx * e1y - sy * e1x;
+      const float v = (d[0] * qx + d[1] * qy + d[2] * qz) * inv;
+      if (v < 0.0f || u + v > 1.0f) continue;
+      const float tt = (e2x * qx + e2y * qy + e2z * qz) * inv;
+      if (tt > 1e-6f && tt < best) best = tt;
+    }
+  }
+  if (pix >= npix) return;
+  const bool hit = best < 3.0e38f;
+  mask[pix] = hit ? 1 : 0;
+  pos[pix] = hit ? ox + best * d[0] : 0.0f;
+  pos[size_t(npix) + pix] = hit ? oy + best * d[1] : 0.0f;
+  pos[size_t(2) * npix + pix] = hit ? oz + best * d[2] : 0.0f;
+}
+
+void launch_raycast_mesh(const CamBasis& cb, const float* tri_verts, int n_tri, float* positions, uint8_t* mask,
+                         cudaStream_t s) {
+  const int npix = cb.width * cb.height;
+  raycast_mesh_kernel<<<(npix + 255) / 256, 256, 0, s>>>(cb, tri_verts, n_tri, positions, mask);
 }
 
 }  // namespace nsdf_b200

@@ -131,6 +131,10 @@ void launch_normal_map(Mode mode, const DevField& f, const float* pts, int k, fl
 void launch_shade(const float* pts, const float* normals, int k, const ShadeParams& sp, float* rgb,
                   cudaStream_t s);
 
+// Mesh G-buffer: nearest ray-triangle hit per pixel (Moller-Trumbore, fp32).
+void launch_raycast_mesh(const CamBasis& cb, const float* tri_verts /* n_tri x 9 */, int n_tri, float* positions,
+                         uint8_t* mask, cudaStream_t s);
+
 // Tensor-core availability of a net for the fast mode (mlp_tc.cu).
 bool tc_supported(const DevNet& n);
 

@@ -187,7 +187,7 @@ __device__ __forceinline__ uint32_t pack_half2_lo(float a, float b, uint32_t hi)
 }
 
 // ---- kernel parameters -------------------------------------------------------------------
-enum TcOp : int { kOpTrace = 0, kOpNormals = 1, kOpEval = 2 };
+enum TcOp : int { kOpTrace = 0, kOpNormals = 1, kOpEval = 2, kOpNormalMap = 3 };
 
 struct TcNet {
   int n_layers, width, input_dim;
@@ -230,6 +230,10 @@ struct TcArgs {
   int rows, k;
   float* out;
   float* grad;
+  // normal map (neural_normal_map semantics, shade.cpp:8-42)
+  double delta;
+  const float* fallback;
+  unsigned long long* counts;
 };
 
 // Dynamic shared-memory carve-up (sized for the net's layer count, so two 256-wide CTAs
@@ -330,7 +334,7 @@ struct RowIn {
 };
 
 __device__ __forceinline__ int load_slot(const TcArgs& a, int item, int n_items) {
-  if (item >= n_items || a.op == kOpEval) return item < n_items ? item : -1;
+  if (item >= n_items || a.op == kOpEval || a.op == kOpNormalMap) return item < n_items ? item : -1;
   return __ldg(a.in_list + item);
 }
 
@@ -341,7 +345,7 @@ __device__ __forceinline__ RowIn load_row(const TcArgs& a, int slot, bool trace_
   r.p[3] = a.time;
   r.t = r.dx = r.dy = r.dz = 0.0f;
   if (slot < 0) return r;
-  if (a.op == kOpEval) {
+  if (a.op == kOpEval || a.op == kOpNormalMap) {
     for (int k = 0; k < 4; ++k) r.p[k] = k < a.rows ? __ldg(a.pts + size_t(k) * a.k + slot) : a.time;
     return r;
   }
@@ -422,7 +426,7 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
   constexpr uint32_t kChunkBytes = uint32_t(W) * kKC * 2;
   constexpr size_t kStageHalves = size_t(W) * kKC * kNW;
 
-  const int n_items = a.op == kOpEval ? a.k : *a.in_count;
+  const int n_items = (a.op == kOpEval || a.op == kOpNormalMap) ? a.k : *a.in_count;
   const int n_tiles = (n_items + kRaysPerTile - 1) / kRaysPerTile;
   const int my_tiles = blockIdx.x < n_tiles ? (n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
   if (my_tiles == 0) return;
@@ -673,6 +677,23 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
               if (!defer) shade_and_write(a.sp, a.st, now.slot, nrm, a.rgb, a.depth, a.mask);
             }
             warp_append(defer, now.slot, a.fb_list, a.fb_count);
+          } else if (a.op == kOpNormalMap) {
+            bool outside = false, fell_back = false;
+            if (lead) {
+              outside = fabs(double(f)) > a.delta;
+              float nrm[3];
+              if (!normalize_normal(gx, gy, gz, nrm)) {
+                fell_back = true;
+                for (int c = 0; c < 3; ++c)
+                  nrm[c] = a.fallback ? a.fallback[size_t(c) * a.k + item] : (c == 1 ? 1.0f : 0.0f);
+              }
+              for (int c = 0; c < 3; ++c) a.grad[size_t(c) * a.k + item] = nrm[c];
+            }
+            const unsigned mo = __ballot_sync(0xffffffffu, outside), mf = __ballot_sync(0xffffffffu, fell_back);
+            if (lane == 0 && (mo | mf)) {
+              atomicAdd(a.counts + 0, (unsigned long long)__popc(mo));
+              atomicAdd(a.counts + 1, (unsigned long long)__popc(mf));
+            }
           } else if (lead) {
             if (a.out) a.out[item] = f;
             if (a.grad) {
@@ -844,6 +865,23 @@ bool tc_eval(int terms, const DevField& f, const float* pts, int rows, int k, fl
   if (rows == 4) return false;
   if (grad) return launch_any<true>(a, k, s);
   return launch_any<false>(a, k, s);
+}
+
+bool tc_normal_map(int terms, const DevField& f, const float* pts, int k, float time, double delta,
+                   const float* fallback, float* normals, unsigned long long* counts, cudaStream_t s) {
+  TcArgs a{};
+  a.terms = terms;
+  a.net = tc_net(f.net);
+  a.op = kOpNormalMap;
+  a.pts = pts;
+  a.rows = 3;
+  a.k = k;
+  a.time = time;
+  a.grad = normals;
+  a.delta = delta;
+  a.fallback = fallback;
+  a.counts = counts;
+  return launch_any<true>(a, k, s);
 }
 
 }  // namespace nsdf_b200

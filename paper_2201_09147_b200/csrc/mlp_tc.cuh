@@ -16,4 +16,7 @@ bool tc_normals_shade(int terms, const DevField& nf, float time, const int* list
 bool tc_eval(int terms, const DevField& f, const float* pts, int rows, int k, float time, float* out, float* grad,
              cudaStream_t s);
 
+bool tc_normal_map(int terms, const DevField& f, const float* pts, int k, float time, double delta,
+                   const float* fallback, float* normals, unsigned long long* counts, cudaStream_t s);
+
 }  // namespace nsdf_b200

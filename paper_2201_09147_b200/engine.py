@@ -152,6 +152,19 @@ class Context:
                                             _fp(nrm), ctypes.byref(o), ctypes.byref(f)))
         return nrm, o.value, f.value
 
+    def normal_map_device(self, handle, d_points: int, k: int, delta: float, d_normals: int, d_counts: int,
+                          d_fallback: int = 0, time: float = 0.0):
+        check(self.lib.nsdf_cuda_normal_map_device(self._ctx, handle, ctypes.c_float(time), ctypes.c_void_p(d_points),
+                                                   k, ctypes.c_double(delta), ctypes.c_void_p(d_fallback or None),
+                                                   ctypes.c_void_p(d_normals), ctypes.c_void_p(d_counts)))
+
+    def raycast_mesh(self, cam: Camera, vertices, triangles, d_positions: int, d_mask: int):
+        v = np.ascontiguousarray(vertices, np.float32)
+        t = np.ascontiguousarray(triangles, np.int32)
+        check(self.lib.nsdf_cuda_raycast_mesh(self._ctx, ctypes.byref(cam), _fp(v), len(v),
+                                              t.ctypes.data_as(_I32), len(t), ctypes.c_void_p(d_positions),
+                                              ctypes.c_void_p(d_mask)))
+
     def shade(self, points, normals, cfg: ShadeConfig, cam: Camera):
         pts = np.ascontiguousarray(points, np.float32)
         nrm = np.ascontiguousarray(normals, np.float32)

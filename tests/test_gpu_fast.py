@@ -111,3 +111,100 @@ def test_fast_render_matches_oracle_mode(ctx, fast):
         both = (m0 == 1) & (m1 == 1)
         assert np.percentile(np.abs(d0 - d1)[both], 99.9) <= DT_MAX
         assert np.mean(np.abs(rgb0 - rgb1)[both]) < 5e-3
+
+
+def _render_pair(ctx, fast, seq, cam, cfg, shade, src, time=0.0):
+    from paper_2201_09147_b200.engine import DeviceSequence
+    a = ctx.render(DeviceSequence(ctx, seq).levels(time=time), cam, cfg, shade, src)
+    b = fast.render(DeviceSequence(fast, seq).levels(time=time), cam, cfg, shade, src)
+    return a, b
+
+
+def _assert_render_parity(a, b):
+    rgb0, d0, m0, _ = a
+    rgb1, d1, m1, _ = b
+    assert np.mean(m0 == m1) >= MASK_MIN
+    both = (m0 == 1) & (m1 == 1)
+    if both.any():
+        assert np.percentile(np.abs(d0 - d1)[both], 99.9) <= DT_MAX
+        assert np.mean(np.abs(rgb0 - rgb1)[both]) < 5e-3
+
+
+def test_config1_single_256x3(ctx, fast, oracle_built):
+    """BASELINE config 1 (single 256x3, budgets {40}) at 128^2: oracle mode bit-exact vs the
+    reference, fast mode within tolerance."""
+    from oracle import refshim
+    from paper_2201_09147_b200.abi import ShadeConfig, TraceConfig, standard_camera
+    from paper_2201_09147_b200.engine import DeviceSequence
+    from paper_2201_09147_b200.manifest import load_manifest, write_manifest
+    full = load_manifest(_fixture("torus_w30.nest"))
+    seq = full.subsequence([2])
+    cam = standard_camera(128, 128)
+    cfg = TraceConfig((40,))
+    shade = ShadeConfig(specular=0.3)
+    a, b = _render_pair(ctx, fast, seq, cam, cfg, shade, 0)
+    _assert_render_parity(a, b)
+    import json, tempfile
+    j = json.load(open(_fixture("torus_w30.nest")))
+    j["fields"] = [dict(j["fields"][2], weights=os.path.join(ASSETS, j["fields"][2]["weights"]))]
+    j["deltas"] = [j["deltas"][2]]
+    with tempfile.NamedTemporaryFile("w", suffix=".nest", delete=False) as f:
+        json.dump(j, f)
+    r = refshim.render(f.name, cam, cfg, shade, 0)
+    os.unlink(f.name)
+    assert np.array_equal(a[2], r[2]) and np.array_equal(a[1].view(np.uint32), r[1].view(np.uint32))
+
+
+def test_config4_mesh_gbuffer_normals(ctx, fast, oracle_built):
+    """BASELINE config 4: torus-mesh G-buffer positions -> 256x3 neural normals; oracle mode
+    bit-exact vs the reference's neural_normal_map on the identical positions, fast mode
+    within 0.5 deg."""
+    import torch
+    from oracle import refshim
+    from paper_2201_09147_b200.abi import standard_camera
+    from paper_2201_09147_b200.manifest import load_manifest
+    from paper_2201_09147_b200.meshes import torus_mesh
+    full = load_manifest(_fixture("torus_w30.nest"))
+    net, delta = full.members[2], full.deltas[2]
+    cam = standard_camera(256, 144)
+    n = cam.width * cam.height
+    pos = torch.zeros(3 * n, dtype=torch.float32, device="cuda")
+    mask = torch.zeros(n, dtype=torch.uint8, device="cuda")
+    v, t = torus_mesh()
+    ctx.raycast_mesh(cam, v, t, pos.data_ptr(), mask.data_ptr())
+    pts = pos.view(3, n)[:, mask.bool()].cpu().numpy()
+    assert pts.shape[1] > 1000
+    # hits lie on the mesh, i.e. near the torus surface
+    s = np.hypot(pts[0], pts[2])
+    assert np.abs(np.hypot(s - 0.6, pts[1]) - 0.3).max() < 0.01
+    n0, o0, f0 = ctx.normal_map(ctx.upload(net), pts, delta)
+    n1, o1, f1 = fast.normal_map(fast.upload(net), pts, delta)
+    import json, tempfile
+    j = json.load(open(_fixture("torus_w30.nest")))
+    j["fields"] = [dict(j["fields"][2], weights=os.path.join(ASSETS, j["fields"][2]["weights"]))]
+    j["deltas"] = [j["deltas"][2]]
+    with tempfile.NamedTemporaryFile("w", suffix=".nest", delete=False) as f:
+        json.dump(j, f)
+    nr, orr, fr = refshim.normal_map(f.name, 0, pts, delta)
+    os.unlink(f.name)
+    assert np.array_equal(n0.view(np.uint32), nr.view(np.uint32)) and (o0, f0) == (orr, fr)
+    assert np.percentile(angle_deg(n0, n1), 99.9) <= ANGLE_MAX
+
+
+@pytest.mark.parametrize("t", [0.0, 0.37, 1.0])
+def test_config5_animated_slices(ctx, fast, oracle_built, t):
+    """BASELINE config 5 (4-D 64x1 > 128x2 blend) time slices: oracle mode bit-exact vs the
+    reference's AnimatedSequence::slice render, fast mode within tolerance."""
+    from oracle import refshim
+    from paper_2201_09147_b200.abi import ShadeConfig, TraceConfig, standard_camera
+    from paper_2201_09147_b200.manifest import load_manifest
+    path = _fixture("blend4d_w30.nest")
+    seq = load_manifest(path)
+    cam = standard_camera(96, 64)
+    cfg = TraceConfig((20, 10))
+    shade = ShadeConfig(specular=0.3)
+    a, b = _render_pair(ctx, fast, seq, cam, cfg, shade, 0, time=t)
+    _assert_render_parity(a, b)
+    r = refshim.render(path, cam, cfg, shade, 0, time=t)
+    assert np.array_equal(a[2], r[2]) and np.array_equal(a[1].view(np.uint32), r[1].view(np.uint32))
+    assert np.max(np.abs(a[0] - r[0])) <= 1e-6
