@@ -42,6 +42,7 @@ constexpr int kKC = 32;      // K elements per streamed weight chunk
 constexpr int kStages = 2;
 constexpr float kInv2Pi = 0.15915494309189535f;
 constexpr float k2Pi = 6.283185307179586f;
+constexpr float kHalfPi = 1.5707963267948966f;
 
 // ---- PTX wrappers ---------------------------------------------------------------------
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
@@ -267,8 +268,8 @@ __host__ __device__ inline size_t tc_smem_bytes(int W, int L, int terms, bool re
   b += size_t(W) * 4 * 4;
   b += size_t(L - 1) * W * 4;
   b += size_t(W) * 4;
-  b += size_t(3) * kRows * 4;
-  b += size_t(2) * 1024 * 4 + 64;   // compaction staging (kStageCap per list) + counters
+  b += (W == 64 ? 0 : size_t(3) * kRows * 4);
+  b += size_t(2) * 512 * 4 + 64;    // compaction staging (kStageCap per list) + counters
   b += (2 * kStages + 2) * 8 + 16;
   return b + 1024;  // alignment slack
 }
@@ -289,8 +290,8 @@ __device__ inline TcSmem tc_carve(uint8_t* raw, int W, int L, int terms, bool re
   s.w0r = reinterpret_cast<float4*>(take(size_t(W) * 4 * 4, 16));
   s.bias = reinterpret_cast<float*>(take(size_t(L - 1) * W * 4, 16));
   s.wout = reinterpret_cast<float*>(take(size_t(W) * 4, 16));
-  s.part = reinterpret_cast<float*>(take(size_t(3) * kRows * 4, 16));
-  s.stage_buf = reinterpret_cast<int*>(take(size_t(2) * 1024 * 4, 16));
+  s.part = reinterpret_cast<float*>(take(W == 64 ? 0 : size_t(3) * kRows * 4, 16));
+  s.stage_buf = reinterpret_cast<int*>(take(size_t(2) * 512 * 4, 16));
   s.stage_count = reinterpret_cast<int*>(take(16, 16));
   s.stage_base = s.stage_count + 2;
   s.bars = reinterpret_cast<uint64_t*>(take((2 * kStages + 2) * 8, 8));
@@ -372,7 +373,7 @@ struct StageList {
   int* buf;
   int* count;
 };
-constexpr int kStageCap = 1024;
+constexpr int kStageCap = 512;
 
 __device__ __forceinline__ void stage_append(bool pred, int value, StageList s) {
   const unsigned mask = __ballot_sync(0xffffffffu, pred);
@@ -569,11 +570,10 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
             const float4 w = sm.w0r[n0 + j + u];  // radians: omega*(W0 p + b0)
             const float z = fmaf(w.z, now.p[2], fmaf(w.y, now.p[1], fmaf(w.x, now.p[0], w.w)));
             if (kGrad) {
-              float s, cs;
-              fast_sincos(z, s, cs);
-              const float c = __shfl_sync(group_mask, cs, lane & ~3, 32);
+              // all 4 rows of a ray see the same point: one sine per lane, cos = sin(z + pi/2);
               // tangent c: W0[n, c] * omega cos(z) = (omega W0[n, c]) * cos(z)
-              o[u] = chain == 0 ? s : (chain == 1 ? w.x : (chain == 2 ? w.y : w.z)) * c;
+              const float r = fast_sin(chain == 0 ? z : z + kHalfPi);
+              o[u] = chain == 0 ? r : (chain == 1 ? w.x : (chain == 2 ? w.y : w.z)) * r;
             } else {
               o[u] = fast_sin(z);
             }
@@ -605,12 +605,12 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
             if (kGrad) {
-              const float z = fmaf(v[j], zs, bias[cc + j]);
-              float s = 0.0f, cs = 0.0f;
-              if (chain == 0) fast_sincos(z, s, cs);
+              // the value row's pre-activation, broadcast to its 3 tangent rows; every lane
+              // issues ONE sine: sin(z) on the value row, cos(z) = sin(z + pi/2) on tangents
+              const float z = __shfl_sync(group_mask, fmaf(v[j], zs, bias[cc + j]), lane & ~3, 32);
+              const float r = fast_sin(chain == 0 ? z : z + kHalfPi);
               // tangent rows: G = (W.G_prev) * omega cos(z); D carries the 2^k weight scale
-              const float dphi = __shfl_sync(group_mask, dscale * cs, lane & ~3, 32);
-              v[j] = chain == 0 ? s : v[j] * dphi;
+              v[j] = chain == 0 ? r : v[j] * (dscale * r);
             } else {
               v[j] = fast_sin(fmaf(v[j], zs, bias[cc + j]));
             }
