@@ -1,0 +1,135 @@
+"""GPU: engine behaviour beyond arithmetic parity — the frame/tile scheduler's per-rank path
+(tile-sharded renders reassemble the single-GPU frame bit for bit), determinism, stats
+accounting, and the reference's error conventions through the C ABI."""
+import os
+
+import numpy as np
+import pytest
+
+from conftest import ASSETS, random_net
+
+pytestmark = pytest.mark.gpu
+
+
+def _seq():
+    from paper_2201_09147_b200.manifest import load_manifest
+    p = os.path.join(ASSETS, "torus_w30.nest")
+    if not os.path.exists(p):
+        pytest.skip("fixture missing")
+    return load_manifest(p)
+
+
+@pytest.mark.parametrize("mode", ["fp32", "fp16"])
+@pytest.mark.parametrize("world,tile", [(2, 64), (3, 32), (8, 16)])
+def test_tile_sharded_ranks_reassemble_the_frame(mode, world, tile):
+    """Each simulated rank renders only its tiles (t % world == rank) into its own device
+    framebuffer, exactly as bench.py's ranks do; the packed-tile gather (scheduler.py) is
+    emulated by the same index sets.  The union must equal the single-GPU frame bitwise."""
+    import torch
+    from paper_2201_09147_b200.abi import ShadeConfig, TraceConfig, standard_camera
+    from paper_2201_09147_b200.engine import Context, DeviceSequence
+    from paper_2201_09147_b200.scheduler import owned_pixels
+    ctx = Context(0, mode)
+    ds = DeviceSequence(ctx, _seq())
+    W, H = 200, 120
+    cam = standard_camera(W, H)
+    cfg = TraceConfig((20, 5, 5))
+    shade = ShadeConfig(specular=0.3)
+    n = W * H
+
+    def bufs():
+        return (torch.full((3 * n,), -1.0, device="cuda"), torch.full((n,), -1.0, device="cuda"),
+                torch.full((n,), 7, dtype=torch.uint8, device="cuda"))
+
+    full = bufs()
+    ctx.render_device(ds.levels(), cam, cfg, shade, *(b.data_ptr() for b in full))
+    torch.cuda.synchronize()
+    out = bufs()
+    for rank in range(world):
+        mine = bufs()
+        ctx.render_device(ds.levels(), cam, cfg, shade, *(b.data_ptr() for b in mine), tile_size=tile,
+                          tile_rank=rank, tile_world=world)
+        torch.cuda.synchronize()
+        idx = torch.from_numpy(owned_pixels(W, H, tile, rank, world)).cuda()
+        # untouched pixels keep the sentinel, owned pixels are written
+        others = torch.ones(n, dtype=torch.bool, device="cuda")
+        others[idx] = False
+        assert bool((mine[2][others] == 7).all())
+        out[0].view(-1, 3)[idx] = mine[0].view(-1, 3)[idx]
+        out[1][idx] = mine[1][idx]
+        out[2][idx] = mine[2][idx]
+    for a, b in zip(out, full):
+        assert torch.equal(a.view(torch.uint8) if a.dtype != torch.uint8 else a,
+                           b.view(torch.uint8) if b.dtype != torch.uint8 else b)
+    ctx.close()
+
+
+def test_fast_mode_is_deterministic():
+    from paper_2201_09147_b200.abi import ShadeConfig, TraceConfig, standard_camera
+    from paper_2201_09147_b200.engine import Context, DeviceSequence
+    ctx = Context(0, "fp16")
+    ds = DeviceSequence(ctx, _seq())
+    cam = standard_camera(256, 160)
+    a = ctx.render(ds.levels(), cam, TraceConfig((20, 5, 5)), ShadeConfig(specular=0.3))
+    b = ctx.render(ds.levels(), cam, TraceConfig((20, 5, 5)), ShadeConfig(specular=0.3))
+    for x, y in zip(a[:3], b[:3]):
+        assert np.array_equal(x, y)
+    ctx.close()
+
+
+def test_stats_match_records(ctx):
+    """Per-level evaluation counts (the FLOP source) equal the HitRecords' iterations_used."""
+    from conftest import records_np
+    from paper_2201_09147_b200.abi import TraceConfig, standard_camera
+    from paper_2201_09147_b200.engine import DeviceSequence
+    ds = DeviceSequence(ctx, _seq())
+    recs, st = ctx.trace_image(ds.levels(), standard_camera(160, 90), TraceConfig((20, 5, 5)))
+    r = records_np(recs)
+    for j in range(3):
+        assert st.evals[j] == int(r["iters"][:, j].astype(np.int64).sum())
+    assert st.hits == int(r["hit"].sum())
+
+
+def test_error_conventions(ctx):
+    """ErrorKinds and messages of the reference's validation (trace.cpp:10-23,
+    camera.cpp:7-18, mlp.cpp:13-39, nesting.cpp:56-69, shade.cpp:47-65)."""
+    from paper_2201_09147_b200.abi import Camera, Level, NsdfError, ShadeConfig, TraceConfig, standard_camera
+    from paper_2201_09147_b200.engine import DeviceSequence
+    from paper_2201_09147_b200.manifest import Analytic, Net, Sequence
+    ds = DeviceSequence(ctx, Sequence([Analytic("sphere", {"r": 1.0}), Analytic("sphere", {"r": 0.9})],
+                                      [0.1, 0.05], ["a", "b"]))
+    cam = standard_camera(16, 16)
+    cases = [
+        (lambda: ctx.trace_image(ds.levels(), cam, TraceConfig((0, 0))), "config", "all iteration budgets are zero"),
+        (lambda: ctx.trace_image(ds.levels(), cam, TraceConfig((5,))), "config", "got 1 budgets for 2 levels"),
+        (lambda: ctx.trace_image(ds.levels(), cam, TraceConfig((5, -1))), "config", "non-negative"),
+        (lambda: ctx.trace_image(ds.levels(), cam, TraceConfig((5, 5), eps_stop=0.0)), "config", "eps_stop"),
+        (lambda: ctx.trace_image(ds.levels(), Camera(width=0), TraceConfig((5, 5))), "config", "image size"),
+        (lambda: ctx.trace_image(ds.levels(), Camera((0, 0, 3), (0, 0, 3)), TraceConfig((5, 5))), "config",
+         "coincide"),
+        (lambda: ctx.trace_image(ds.levels(), Camera((0, 3, 0), (0, 0, 0)), TraceConfig((5, 5))), "config",
+         "parallel"),
+        (lambda: ctx.trace_image([Level(ds.handles[0], 0.0, 0.1), Level(ds.handles[1], 0.0, -1.0)], cam,
+                                 TraceConfig((5, 5))), "validation", "not positive"),
+        (lambda: ctx.render(ds.levels(), cam, TraceConfig((5, 5)), ShadeConfig(lights=())), "contract",
+         "at least one directional light"),
+        (lambda: ctx.render(ds.levels(), cam, TraceConfig((5, 5)), ShadeConfig(), 1, 7), "config", "out of range"),
+        (lambda: ctx.upload(Net.from_layers([(np.zeros((4, 3)), np.zeros(4)), (np.zeros((2, 4)), np.zeros(2))])),
+         "validation", "single output"),
+        (lambda: ctx.eval(ds.handles[0], np.zeros((2, 5), np.float32)), "contract", "rows are required"),
+    ]
+    for fn, kind, text in cases:
+        with pytest.raises(NsdfError) as e:
+            fn()
+        assert e.value.kind == kind and text in str(e.value), (kind, text, str(e.value))
+
+
+def test_empty_and_ragged_batches(ctx):
+    net = random_net(64, 1, seed=4)
+    h = ctx.upload(net)
+    d, g = ctx.eval_grad(h, np.zeros((3, 0), np.float32))
+    assert d.shape == (0,) and g.shape == (3, 0)
+    for k in (1, 127, 128, 129, 4097):
+        pts = np.random.default_rng(k).uniform(-1, 1, (3, k)).astype(np.float32)
+        d1, g1 = ctx.eval_grad(h, pts)
+        assert d1.shape == (k,) and np.isfinite(d1).all() and np.isfinite(g1).all()
