@@ -142,6 +142,22 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, float v[32]) {
 #pragma unroll
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
+// Asynchronous 32x32b.x16 load: the registers are only valid after tmem_wait16 (which
+// names them as outputs, so the compiler cannot read them earlier).
+__device__ __forceinline__ void tmem_issue16(uint32_t taddr, uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait16(uint32_t (&r)[16]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                 "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]), "+r"(r[15])
+               :
+               : "memory");
+}
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, float v[16]) {
   uint32_t r[16];
   asm volatile(
@@ -597,10 +613,17 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
         const float* bias = sm.bias + size_t(h + 1) * W;
         const float zs = net.omega * net.wscale[h];  // radians; undoes the 2^k weight scaling
         const float dscale = net.omega * net.wscale[h];
-#pragma unroll 1
+        // TMEM loads software-pipelined one 16-column chunk ahead of the math
+        uint32_t raw[2][16];
+        tmem_issue16(taddr, raw[0]);
+#pragma unroll
         for (int c = 0; c < kCols; c += 16) {
+          const int buf = (c / 16) & 1;
+          tmem_wait16(raw[buf]);
+          if (c + 16 < kCols) tmem_issue16(taddr + uint32_t(c + 16), raw[buf ^ 1]);
           float v[16];
-          tmem_ld16(taddr + uint32_t(c), v);
+#pragma unroll
+          for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(raw[buf][j]);
           const int cc = col0 + c;
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
