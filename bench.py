@@ -288,6 +288,7 @@ def run_e2e(args, ctx, ds, seq, stream, world, rank, W):
         if world > 1:
             W["step"](i)
             if rank == 0:
+                torch.cuda.current_stream().wait_stream(W["gstream"])
                 W["gather"].to_host()
         else:
             ctx.render_into(levels, cam, cfg, shade, h_rgb.data_ptr(), h_depth.data_ptr(), h_mask.data_ptr(), src)
@@ -373,13 +374,31 @@ def main():
         gather = scheduler.TileGather(Wd, Hd, args.tile, rank, world) if world > 1 and not animated else None
         W["gather"] = gather
         tile_world, tile_rank = (1, 0) if animated else (world, rank)
+        # N > 1: double-buffered framebuffers; frame i's NCCL tile gather runs on its own
+        # stream while frame i+1 renders (frames pipeline; each frame is still complete)
+        fbs = [(rgb, depth, mask)]
+        if gather is not None:
+            fbs.append((torch.zeros_like(rgb), torch.zeros_like(depth), torch.zeros_like(mask)))
+        gstream = torch.cuda.Stream() if gather is not None else None
+        free_ev = [None, None]
+        W["gstream"] = gstream
 
         def step(i=0):
             lv = frame_levels[i % len(frame_levels)] if animated else W["levels"]
-            ctx.render_device(lv, W["cam"], cfg, W["shade"], rgb.data_ptr(), depth.data_ptr(), mask.data_ptr(),
+            b = i % len(fbs)
+            if free_ev[b] is not None:
+                stream.wait_event(free_ev[b])
+            fr, fd, fm = fbs[b]
+            ctx.render_device(lv, W["cam"], cfg, W["shade"], fr.data_ptr(), fd.data_ptr(), fm.data_ptr(),
                               W["src"], -1, args.tile, tile_rank, tile_world)
             if gather is not None:
-                gather(rgb, depth, mask)
+                done = torch.cuda.Event()
+                done.record(stream)
+                with torch.cuda.stream(gstream):
+                    gstream.wait_event(done)
+                    gather(fr, fd, fm)
+                    free_ev[b] = torch.cuda.Event()
+                    free_ev[b].record(gstream)
 
         # accounting frame (not timed): per-level evaluation counts -> algorithmic FLOPs
         stats = ctx.render_device(W["levels"], W["cam"], cfg, W["shade"], rgb.data_ptr(), depth.data_ptr(),
@@ -402,6 +421,8 @@ def main():
         e0.record(stream)
         for i in range(steps):
             step(i)
+        if W.get("gstream") is not None:
+            stream.wait_stream(W["gstream"])   # the last frame's gather is inside the timing
         e1.record(stream)
         torch.cuda.synchronize()
         clocks.mark("t1")

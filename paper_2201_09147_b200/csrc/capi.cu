@@ -232,7 +232,17 @@ int run_frame(nsdf_ctx* c, const nsdf_level* levels, int m, const nsdf_trace_con
               float final_delta = 0.0f) {
   int n_counters = 0;
   std::vector<LevelDesc> lv = traced_levels(c, levels, m, cfg, &n_counters, final_delta);
-  const int n_max = cam ? cam->width * cam->height : n_rays;
+  // slots needed: every pixel, or only the pixels of the owned tiles (tile % world == rank)
+  int n_max = cam ? cam->width * cam->height : n_rays;
+  if (cam && tile_world > 1) {
+    const int tx = (cam->width + tile_size - 1) / tile_size, ty = (cam->height + tile_size - 1) / tile_size;
+    long owned = 0;
+    for (int t = tile_rank; t < tx * ty; t += tile_world) {
+      const int x0 = (t % tx) * tile_size, y0 = (t / tx) * tile_size;
+      owned += long(std::min(tile_size, cam->width - x0)) * std::min(tile_size, cam->height - y0);
+    }
+    n_max = int(std::max(owned, 1L));
+  }
   NSDF_CUDA(c->frame.reserve(frame_workspace_bytes(n_max, n_counters)));
   FrameBuffers fb = carve_frame(c->frame.base, n_max, n_counters);
   cudaStream_t s = c->stream;
