@@ -73,6 +73,8 @@ def parse():
     ap.add_argument("--height", type=int, default=0)
     ap.add_argument("--budgets", default="")
     ap.add_argument("--tile", type=int, default=64)
+    ap.add_argument("--inflight", type=int, default=2,
+                    help="frames in flight (engine contexts on their own streams); 1 = strictly serial frames")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     args = ap.parse_args()
@@ -374,31 +376,48 @@ def main():
         gather = scheduler.TileGather(Wd, Hd, args.tile, rank, world) if world > 1 and not animated else None
         W["gather"] = gather
         tile_world, tile_rank = (1, 0) if animated else (world, rank)
-        # N > 1: double-buffered framebuffers; frame i's NCCL tile gather runs on its own
-        # stream while frame i+1 renders (frames pipeline; each frame is still complete)
-        fbs = [(rgb, depth, mask)]
-        if gather is not None:
-            fbs.append((torch.zeros_like(rgb), torch.zeros_like(depth), torch.zeros_like(mask)))
+        # Frames in flight: `inflight` engine contexts, each on its own stream with its own
+        # workspace, render consecutive frames concurrently (the tail iterations of one frame
+        # overlap the next frame's head).  N > 1: frame i's NCCL tile gather runs on its own
+        # stream while later frames render.  Every frame is still rendered completely.
+        lanes = [(ctx, stream, ds)]
+        for _ in range(1, max(1, args.inflight)):
+            c2 = Context(local, args.mode)
+            s2 = torch.cuda.Stream()
+            c2.set_stream(s2.cuda_stream)
+            lanes.append((c2, s2, DeviceSequence(c2, seq)))
+        W["lanes"] = lanes
+        n_fb = max(len(lanes), 2 if gather is not None else 1)
+        fbs = [(rgb, depth, mask)] + [(torch.zeros_like(rgb), torch.zeros_like(depth), torch.zeros_like(mask))
+                                      for _ in range(n_fb - 1)]
         gstream = torch.cuda.Stream() if gather is not None else None
-        free_ev = [None, None]
+        free_ev = [None] * n_fb
         W["gstream"] = gstream
+        if animated:
+            lane_levels = [frame_levels] + [[d.levels(time=i / (cfgw["frames"] - 1)) for i in my_frames]
+                                            for _, _, d in lanes[1:]]
+        else:
+            lane_levels = [[W["levels"]]] + [[d.levels()] for _, _, d in lanes[1:]]
 
         def step(i=0):
-            lv = frame_levels[i % len(frame_levels)] if animated else W["levels"]
-            b = i % len(fbs)
+            li = i % len(lanes)
+            c, st, d = lanes[li]
+            lv = lane_levels[li][i % len(lane_levels[li])]
+            b = i % n_fb
             if free_ev[b] is not None:
-                stream.wait_event(free_ev[b])
+                st.wait_event(free_ev[b])
             fr, fd, fm = fbs[b]
-            ctx.render_device(lv, W["cam"], cfg, W["shade"], fr.data_ptr(), fd.data_ptr(), fm.data_ptr(),
-                              W["src"], -1, args.tile, tile_rank, tile_world)
+            c.render_device(lv, W["cam"], cfg, W["shade"], fr.data_ptr(), fd.data_ptr(), fm.data_ptr(),
+                            W["src"], -1, args.tile, tile_rank, tile_world)
+            ev = torch.cuda.Event()
+            ev.record(st)
             if gather is not None:
-                done = torch.cuda.Event()
-                done.record(stream)
                 with torch.cuda.stream(gstream):
-                    gstream.wait_event(done)
+                    gstream.wait_event(ev)
                     gather(fr, fd, fm)
-                    free_ev[b] = torch.cuda.Event()
-                    free_ev[b].record(gstream)
+                    ev = torch.cuda.Event()
+                    ev.record(gstream)
+            free_ev[b] = ev
 
         # accounting frame (not timed): per-level evaluation counts -> algorithmic FLOPs
         stats = ctx.render_device(W["levels"], W["cam"], cfg, W["shade"], rgb.data_ptr(), depth.data_ptr(),
@@ -407,27 +426,45 @@ def main():
 
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
+    side = [st for _, st, _ in W.get("lanes", [])[1:]] + ([W["gstream"]] if W.get("gstream") is not None else [])
     with ClockSampler(local) as clocks:
         for i in range(args.warmup):
             step(i)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
-        ctx.set_profiling(True)
+        for c, _, _ in W.get("lanes", [(ctx, None, None)]):
+            c.set_profiling(True)
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         clocks.mark("t0")
         e0.record(stream)
+        for st in side:
+            st.wait_event(e0)                  # every lane starts inside the timed region
         for i in range(steps):
             step(i)
-        if W.get("gstream") is not None:
-            stream.wait_stream(W["gstream"])   # the last frame's gather is inside the timing
+        for st in side:
+            stream.wait_stream(st)             # ...and finishes inside it (incl. the last gather)
         e1.record(stream)
         torch.cuda.synchronize()
         clocks.mark("t1")
-    prof = ctx.get_profile()
-    ctx.set_profiling(False)
+    profs = [c.get_profile() for c, _, _ in W.get("lanes", [(ctx, None, None)])]
+    for c, _, _ in W.get("lanes", [(ctx, None, None)]):
+        c.set_profiling(False)
+    prof = profs[0]
+    prof_kind = "CUDA events around each launch, inside the timed region"
+    if len(W.get("lanes", [])) > 1:
+        # With frames in flight the launches of two frames overlap, so an in-region launch
+        # duration is contended.  The per-kernel roofline therefore uses a serial pass of the
+        # same frames on lane 0 right after the timed region (same stream, same buffers).
+        ctx.set_profiling(True)
+        for i in range(0, min(steps, 20) * len(W["lanes"]), len(W["lanes"])):
+            W["step"](i)
+        torch.cuda.synchronize()
+        prof = ctx.get_profile()
+        ctx.set_profiling(False)
+        prof_kind = "CUDA events around each launch, serial pass (1 frame in flight) after the timed region"
     ms_total = e0.elapsed_time(e1)
     t = torch.tensor([ms_total], dtype=torch.float64, device="cuda")
     if world > 1:
@@ -457,10 +494,17 @@ def main():
         normals_ms = prof.normals_ms / max(prof.frames, 1)
         achieved_tf = flops_trace / (trace_ms / 1e3) / 1e12 if trace_ms > 0 else 0.0
         kernel = "trace-iteration MLP tiles (all levels)"
+        # activation bound: one MUFU sine per hidden activation (layer 0 + hidden layers)
+        sines = sum(int(stats.evals[j]) * (seq.members[j].n_layers - 1) * seq.members[j].width
+                    for j in range(len(seq.members)))
+        xu_peak = 16 * 148 * 1.965e9  # MUFU ops/s: 16/clk/SM x 148 SMs x max SM clock
+        act_bound = {"sines_per_frame": sines, "achieved_per_s": sines / (trace_ms / 1e3) if trace_ms > 0 else 0.0,
+                     "peak_per_s": xu_peak, "frac": sines / (trace_ms / 1e3) / xu_peak if trace_ms > 0 else 0.0,
+                     "note": "MUFU (XU pipe) sine throughput of the trace kernels; 64/128-wide nets are sine-bound"}
         frame = {"evals_per_level": [int(x) for x in list(stats.evals)[:len(seq.members)]], "hits": int(stats.hits),
                  "fallbacks": int(stats.fallback_evals), "tflop_trace": flops_trace / 1e12,
                  "tflop_normals": flops_normals / 1e12, "trace_ms": trace_ms, "normals_ms": normals_ms,
-                 "profiled_frame_ms": prof.frame_ms / max(prof.frames, 1),
+                 "profiled_frame_ms": prof.frame_ms / max(prof.frames, 1), "profile": prof_kind,
                  "level_ms": [prof.level_ms[j] / max(prof.frames, 1) for j in range(len(seq.members))]}
 
     e2e = None
@@ -488,6 +532,7 @@ def main():
             "data": "synthetic camera rays; committed fitted SIREN weights (assets/)",
             "config": {"workload": workload_text(args), "config": args.config, "resolution": f"{Wd}x{Hd}",
                        "budgets": args.budgets, "mode": args.mode, "tile": args.tile,
+                       "frames_in_flight": 1 if W["gbuffer"] else max(1, args.inflight),
                        "parallelism": (f"frames{world}" if animated else f"tiles{world}") if world > 1 else "single",
                        "l2": "per-frame working set (ray state, lists, framebuffer) > 126 MB L2; weights L2-resident"},
             "fps": 1000.0 / ms_per_frame,
@@ -495,14 +540,16 @@ def main():
             "roofline": {"bound": "tensor", "kernel": kernel, "achieved": achieved_tf, "peak": peak_tf,
                          "unit": "TFLOP/s", "frac": achieved_tf / peak_tf,
                          "peak_kind": f"{pk_kind} bf16 sustained (MEASURED_PEAKS.json)", "traffic": None,
-                         "whole_frame_tflops": (flops_trace + flops_normals) / (ms_per_frame / 1e3) / 1e12},
+                         "whole_frame_tflops": (flops_trace + flops_normals) / (ms_per_frame / 1e3) / 1e12,
+                         "activation_bound": None if W["gbuffer"] else act_bound},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,
             "clocks": clocks.summary(),
         }
         print(json.dumps(line), flush=True)
-    ctx.close()
+    for c, _, _ in W.get("lanes", [(ctx, None, None)]):
+        c.close()
     if world > 1:
         dist.destroy_process_group()
 
