@@ -194,7 +194,7 @@ std::vector<LevelDesc> traced_levels(nsdf_ctx* c, const nsdf_level* levels, int 
     d.budget = cfg->budgets[j];
     d.level = j;
     out.push_back(d);
-    nc += 1 + d.budget;
+    nc += 3 + d.budget;  // adv count, claim cursor, evaluations, iteration list sizes
   }
   *n_counters = nc + 2;  // + fallback count + spare
   return out;
@@ -208,9 +208,13 @@ void fill_stats(const std::vector<LevelDesc>& lv, const TraceResult& tr, const s
     const int base = tr.counter_layout_base[i];
     uint64_t ev = 0;
     int cur = in;
-    for (int it = 0; it < lv[i].budget; ++it) {
-      ev += uint64_t(cur);
-      cur = counters[base + 1 + it];
+    if (tr.persistent[i]) {
+      ev = uint64_t(counters[base + 2]);
+    } else {
+      for (int it = 0; it < lv[i].budget; ++it) {
+        ev += uint64_t(cur);
+        cur = counters[base + 3 + it];
+      }
     }
     stats->evals[lv[i].level] = ev;
     in = counters[base];  // advanced count feeds the next level

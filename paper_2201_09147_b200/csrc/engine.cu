@@ -343,10 +343,13 @@ TraceResult run_trace(Mode mode, const std::vector<LevelDesc>& levels, float eps
   const int* level_in_count = n_slots_dev;
   int coff = 1;  // counters[0] holds the slot count
   for (const LevelDesc& lv : levels) {
+    // per level: [adv count, claim cursor, evaluations, iteration list sizes...]
     int* adv_count = fb.counters + coff;
-    int* it_counts = fb.counters + coff + 1;
+    int* cursor = fb.counters + coff + 1;
+    int* evals = fb.counters + coff + 2;
+    int* it_counts = fb.counters + coff + 3;
     res.counter_layout_base.push_back(coff);
-    coff += 1 + lv.budget;
+    coff += 3 + lv.budget;
     IterArgs a;
     a.lv = lv;
     a.eps = eps;
@@ -358,18 +361,19 @@ TraceResult run_trace(Mode mode, const std::vector<LevelDesc>& levels, float eps
     const int* in_count = level_in_count;
     int ping = cur, pong = nxt;
     cudaEvent_t ev = prof ? prof->begin(s) : nullptr;
-    for (int iter = 0; iter < lv.budget; ++iter) {
+    // fast mode: ONE persistent launch per level (rows refilled from the input list)
+    const bool persistent = mode_tc(mode) && lv.field.kind == kFieldMlp && tc_supported(lv.field.net) &&
+                            tc_trace_level(mode_terms(mode), lv, eps, t_max, in_list, in_count, cursor, evals,
+                                           fb.list[adv], adv_count, fb.st, n_max, s);
+    res.persistent.push_back(persistent ? 1 : 0);
+    if (persistent) res.launches++;
+    for (int iter = 0; !persistent && iter < lv.budget; ++iter) {
       a.iter = iter;
       a.in_list = in_list;
       a.in_count = in_count;
       a.next_list = fb.list[pong];
       a.next_count = it_counts + iter;
-      bool done = false;
-      if (mode_tc(mode) && lv.field.kind == kFieldMlp && tc_supported(lv.field.net)) {
-        done = tc_trace_iter(mode_terms(mode), a.lv, a.eps, a.t_max, a.iter, a.in_list, a.in_count, a.next_list, a.next_count,
-                             a.adv_list, a.adv_count, a.st, n_max, s);
-      }
-      if (!done) {
+      {
         const size_t smem = field_smem(lv.field) + kTileCols * sizeof(int);
         static int grid_cache_w = -1, grid_cache = 0;
         const int w = lv.field.kind == kFieldMlp ? lv.field.net.max_width : 4;
@@ -387,7 +391,7 @@ TraceResult run_trace(Mode mode, const std::vector<LevelDesc>& levels, float eps
     }
     if (prof) {
       prof->end(lv.level, ev, s);
-      prof->acc.trace_launches += lv.budget;
+      prof->acc.trace_launches += persistent ? 1 : lv.budget;
     }
     // The advanced list feeds the next level; the other two lists are free again.
     level_in_count = adv_count;

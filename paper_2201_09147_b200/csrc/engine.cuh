@@ -89,6 +89,7 @@ struct TraceResult {
   int* hit_list;        // device: slots that converged at the final level
   int* hit_count;       // device counter
   std::vector<int> counter_layout_base;  // offsets of per-level iteration counters
+  std::vector<char> persistent;          // level traced by one persistent launch
   int launches = 0;
 };
 
@@ -101,8 +102,9 @@ void launch_rays_to_host_layout(const RayState& st, int n, float* rays6, cudaStr
 void launch_init_state_from_rays(const float* rays6, int n, RayState st, cudaStream_t s);
 void launch_reset_state(RayState st, int n, cudaStream_t s);
 
-// Multiscale sphere tracing of `n_slots` rays (trace.cpp:86-132): level by level, one
-// compacting launch per iteration.  counters must be zeroed.  Returns the hit list.
+// Multiscale sphere tracing of `n_slots` rays (trace.cpp:86-132): level by level — one
+// persistent launch per level (tensor-core modes) or one compacting launch per iteration
+// (FFMA oracle tiles).  counters must be zeroed.  Returns the hit list.
 TraceResult run_trace(Mode mode, const std::vector<LevelDesc>& levels, float eps, float t_max,
                       FrameBuffers& fb, int n_slots_host_max, const int* n_slots_dev,
                       cudaStream_t s, Profiler* prof = nullptr);

@@ -40,6 +40,8 @@ constexpr int kTcThreads = 192;
 constexpr int kRows = 128;   // TMEM lanes per tile
 constexpr int kKC = 32;      // K elements per streamed weight chunk
 constexpr int kStages = 2;
+constexpr int kBlk = 16;     // columns per epilogue block = K per MMA step
+constexpr int kMaxSub = 8;   // max blocks per column group per layer (kready barriers)
 constexpr float kInv2Pi = 0.15915494309189535f;
 constexpr float k2Pi = 6.283185307179586f;
 constexpr float kHalfPi = 1.5707963267948966f;
@@ -222,16 +224,15 @@ struct TcArgs {
   int op;
   int terms;  // 3 = split-fp16 (A_hi.W_hi + A_lo.W_hi + A_hi.W_lo), 1 = plain fp16
   uint32_t suspend_ns;
-  // trace
+  // trace (persistent level)
   LevelDesc lv;
   float eps, t_max;
-  int iter;
   const int* in_list;
   const int* in_count;
-  int* next_list;
-  int* next_count;
   int* adv_list;
   int* adv_count;
+  int* cursor;   // claim cursor into in_list
+  int* evals;    // evaluation counter
   RayState st;
   // normals
   float time;
@@ -251,24 +252,35 @@ struct TcArgs {
   double delta;
   const float* fallback;
   unsigned long long* counts;
+  long long* dbg;  // debug timeline (NSDF_TC_TIMELINE): CTA 0, epilogue thread 0
 };
 
-// Dynamic shared-memory carve-up (sized for the net's layer count, so two 256-wide CTAs
-// fit one SM).
+// Layer 0 runs on the tensor cores as a K = 32 MMA: each row's A0 holds its point split
+// into three fp16 parts plus ones for the bias, B0 the matching fp16 hi/lo parts of
+// omega*W0 and a three-part omega*b0 (time folded in), so D0 = omega*(W0 p + b0) to ~2^-22.
+//   k 0-2: p_hi  3-5: p_mid  6-8: p_lo  9: 1      (x W_hi, W_hi, W_hi, b_hi)
+//   k 10-12: p_hi  13-15: p_mid  16: 1  17: 1     (x W_lo, W_lo, b_mid, b_lo)
+// A tangent row c (normal tiles) holds ones at k = c and 10 + c, so its D0 = omega*W0[:, c].
+constexpr int kK0 = 32;
+
+// Dynamic shared-memory carve-up.  SWIZZLE_NONE operands need 16-byte alignment only.
 struct TcSmem {
-  __half* a;            // [128 x W] A operand (fp16 hi part)
+  __half* a;            // [128 x W] A operand, hi part (A0 of layer 0 aliases K 0..31)
   __half* alo;          // [128 x W] A low part (split precision only)
-  __half* wst;          // [kStages][W * kKC] streamed weight chunks
-  float4* w0r;          // [W] {omega*w0x, omega*w0y, omega*w0z, omega*(b0 + w0t*time)}
-  float* bias;          // [(L-1) x W] biases * omega/2pi
+  __half* wst;          // resident hidden weights, or [kStages] streamed weight chunks
+  __half* b0;           // [W x 32] layer-0 B operand
+  float* bias;          // [(L-1) x W] omega*bias of the MMA layers' outputs (row 0 = 0)
   float* wout;          // [W]
   float* part;          // [3][kRows] partial output dots of column groups 1..3
-  int* stage_buf;       // [2][kStageCap] staged compaction appends (next, adv)
-  int* stage_count;     // [2]
+  int* stage_buf;       // [kStageCap] staged compaction appends (persistent trace)
+  int* stage_count;
   int* stage_base;      // flush base broadcast
-  uint64_t* bars;       // full[kStages], empty[kStages], aready, dfull
+  uint64_t* bars;       // full[kStages], empty[kStages], kready[kMaxSub], a0ready, dfull, tstart
   uint32_t* tmem_base;
+  int* done;            // persistent level: no more tiles
 };
+constexpr int kStageCap = 512;
+constexpr int kNumBars = 2 * kStages + kMaxSub + 3;
 
 __host__ __device__ inline size_t tc_weight_bytes(int W, int L, int terms, bool resident) {
   const int nw = terms == 3 ? 2 : 1;
@@ -276,21 +288,21 @@ __host__ __device__ inline size_t tc_weight_bytes(int W, int L, int terms, bool 
   return resident ? size_t(L - 2) * W * W * 2 * 2 : size_t(kStages) * W * kKC * 2 * nw;
 }
 
-__host__ __device__ inline size_t tc_smem_bytes(int W, int L, int terms, bool resident) {
+__host__ __device__ inline size_t tc_smem_bytes(int W, int L, int terms, bool resident, bool persist) {
   const int nw = terms == 3 ? 2 : 1;
   size_t b = 0;
   b += size_t(kRows) * W * 2 * nw;
   b += tc_weight_bytes(W, L, terms, resident);
-  b += size_t(W) * 4 * 4;
+  b += size_t(W) * kK0 * 2;
   b += size_t(L - 1) * W * 4;
   b += size_t(W) * 4;
   b += (W == 64 ? 0 : size_t(3) * kRows * 4);
-  b += size_t(2) * 512 * 4 + 64;    // compaction staging (kStageCap per list) + counters
-  b += (2 * kStages + 2) * 8 + 16;
-  return b + 1024;  // alignment slack
+  b += persist ? size_t(kStageCap) * 4 + 16 : 16;
+  b += kNumBars * 8 + 32;
+  return b + 128;  // alignment slack
 }
 
-__device__ inline TcSmem tc_carve(uint8_t* raw, int W, int L, int terms, bool resident) {
+__device__ inline TcSmem tc_carve(uint8_t* raw, int W, int L, int terms, bool resident, bool persist) {
   const int nw = terms == 3 ? 2 : 1;
   size_t off = 0;
   auto take = [&](size_t bytes, size_t align) {
@@ -300,86 +312,90 @@ __device__ inline TcSmem tc_carve(uint8_t* raw, int W, int L, int terms, bool re
     return p;
   };
   TcSmem s;
-  s.a = reinterpret_cast<__half*>(take(size_t(kRows) * W * 2, 1024));
-  s.alo = reinterpret_cast<__half*>(take(nw == 2 ? size_t(kRows) * W * 2 : 0, 1024));
-  s.wst = reinterpret_cast<__half*>(take(tc_weight_bytes(W, L, terms, resident), 1024));
-  s.w0r = reinterpret_cast<float4*>(take(size_t(W) * 4 * 4, 16));
+  s.a = reinterpret_cast<__half*>(take(size_t(kRows) * W * 2, 128));
+  s.alo = reinterpret_cast<__half*>(take(nw == 2 ? size_t(kRows) * W * 2 : 0, 128));
+  s.wst = reinterpret_cast<__half*>(take(tc_weight_bytes(W, L, terms, resident), 128));
+  s.b0 = reinterpret_cast<__half*>(take(size_t(W) * kK0 * 2, 128));
   s.bias = reinterpret_cast<float*>(take(size_t(L - 1) * W * 4, 16));
   s.wout = reinterpret_cast<float*>(take(size_t(W) * 4, 16));
   s.part = reinterpret_cast<float*>(take(W == 64 ? 0 : size_t(3) * kRows * 4, 16));
-  s.stage_buf = reinterpret_cast<int*>(take(size_t(2) * 512 * 4, 16));
+  s.stage_buf = reinterpret_cast<int*>(take(persist ? size_t(kStageCap) * 4 : 0, 16));
   s.stage_count = reinterpret_cast<int*>(take(16, 16));
-  s.stage_base = s.stage_count + 2;
-  s.bars = reinterpret_cast<uint64_t*>(take((2 * kStages + 2) * 8, 8));
+  s.stage_base = s.stage_count + 1;
+  s.done = s.stage_count + 2;
+  s.bars = reinterpret_cast<uint64_t*>(take(kNumBars * 8, 8));
   s.tmem_base = reinterpret_cast<uint32_t*>(take(16, 16));
   return s;
 }
 
-// Register-resident trace update of the fast path (same arithmetic as trace_update in
-// device_ops.cuh, with the ray state prefetched into registers).
-__device__ __forceinline__ void tc_trace_update(const TcArgs& a, int slot, float f, float px, float py, float pz,
-                                                float t, float dx, float dy, float dz, bool& conv, bool& cont) {
-  const RayState& st = a.st;
-  const float fd = __fsub_rn(f, a.lv.delta);
-  const float afd = fabsf(fd);
-  conv = a.lv.final_level ? afd <= a.eps : fd <= a.eps;
-  cont = false;
-  if (a.iter == 0) st.level_reached[slot] = a.lv.level;
-  if (!conv) {
-    float step = fd;
-    if (a.lv.final_level && step < 0.0f) step = 0.0f;  // trace.cpp:73
-    st.px[slot] = __fadd_rn(px, __fmul_rn(step, dx));
-    st.py[slot] = __fadd_rn(py, __fmul_rn(step, dy));
-    st.pz[slot] = __fadd_rn(pz, __fmul_rn(step, dz));
-    const float tn = __fadd_rn(t, step);
-    st.t[slot] = tn;
-    cont = !(tn > a.t_max);  // trace.cpp:78
-  }
-  if (!cont || a.iter == a.lv.budget - 1) {
-    st.iters[size_t(slot) * kMaxLevels + a.lv.level] = uint16_t(a.iter + 1);
-    st.final_dist[slot] = afd;
-  }
+// Offset (in halves) of element (n, k) of a [W x 32] K-major canonical operand.
+__device__ __forceinline__ int b0_off(int W, int n, int k) { return ((k >> 3) * (W >> 3) + (n >> 3)) * 64 + (n & 7) * 8 + (k & 7); }
+
+// fp32 -> three fp16 parts (hi + mid + lo = x to ~2^-33 relative, subnormals aside).
+__device__ __forceinline__ void split3(float x, __half& hi, __half& mid, __half& lo) {
+  hi = __float2half_rn(x);
+  const float r = x - __half2float(hi);
+  mid = __float2half_rn(r);
+  lo = __float2half_rn(r - __half2float(mid));
 }
 
-// Per-row inputs of a tile, software-pipelined two tiles ahead: the list slot of tile t+2
-// is loaded while tile t runs, its ray state while tile t+1 runs, so no dependent load
-// sits on the critical path.
+// Per-row inputs of a non-trace tile, software-pipelined two tiles ahead: the list slot of
+// tile t+2 is loaded while tile t runs, its point while tile t+1 runs.
 struct RowIn {
   int slot;
-  float p[4];
-  float t, dx, dy, dz;
+  float p[3];
 };
 
 __device__ __forceinline__ int load_slot(const TcArgs& a, int item, int n_items) {
-  if (item >= n_items || a.op == kOpEval || a.op == kOpNormalMap) return item < n_items ? item : -1;
+  if (item >= n_items) return -1;
+  if (a.op == kOpEval || a.op == kOpNormalMap) return item;
   return __ldg(a.in_list + item);
 }
 
-__device__ __forceinline__ RowIn load_row(const TcArgs& a, int slot, bool trace_state) {
+__device__ __forceinline__ RowIn load_row(const TcArgs& a, int slot) {
   RowIn r;
   r.slot = slot;
   r.p[0] = r.p[1] = r.p[2] = 0.0f;
-  r.p[3] = a.time;
-  r.t = r.dx = r.dy = r.dz = 0.0f;
   if (slot < 0) return r;
   if (a.op == kOpEval || a.op == kOpNormalMap) {
-    for (int k = 0; k < 4; ++k) r.p[k] = k < a.rows ? __ldg(a.pts + size_t(k) * a.k + slot) : a.time;
+    for (int k = 0; k < 3; ++k) r.p[k] = __ldg(a.pts + size_t(k) * a.k + slot);
     return r;
   }
   r.p[0] = a.st.px[slot];
   r.p[1] = a.st.py[slot];
   r.p[2] = a.st.pz[slot];
-  if (trace_state) {
-    r.t = a.st.t[slot];
-    r.dx = __ldg(a.st.dx + slot);
-    r.dy = __ldg(a.st.dy + slot);
-    r.dz = __ldg(a.st.dz + slot);
-  }
   return r;
 }
 
 __device__ __forceinline__ void named_bar(int id, int threads) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(threads) : "memory");
+}
+// Named barrier with an OR vote over the participating threads.
+__device__ __forceinline__ bool bar_vote_any(int id, int threads, bool pred) {
+  uint32_t r;
+  asm volatile(
+      "{\n\t.reg .pred p, q;\n\t"
+      "setp.ne.u32 p, %1, 0;\n\t"
+      "bar.red.or.pred q, %2, %3, p;\n\t"
+      "selp.u32 %0, 1, 0, q;\n\t}"
+      : "=r"(r)
+      : "r"(uint32_t(pred)), "r"(id), "r"(threads)
+      : "memory");
+  return r != 0;
+}
+// Position of the n-th (0-based) set bit of m (n < popc(m)).
+__device__ __forceinline__ int nth_set_bit(uint32_t m, int n) {
+  int pos = 0;
+#pragma unroll
+  for (int w = 16; w > 0; w >>= 1) {
+    const int c = __popc(m & ((1u << w) - 1u));
+    if (n >= c) {
+      n -= c;
+      m >>= w;
+      pos += w;
+    }
+  }
+  return pos;
 }
 
 // CTA-local staging of compaction appends: warps append with shared atomics; the staged
@@ -389,7 +405,6 @@ struct StageList {
   int* buf;
   int* count;
 };
-constexpr int kStageCap = 512;
 
 __device__ __forceinline__ void stage_append(bool pred, int value, StageList s) {
   const unsigned mask = __ballot_sync(0xffffffffu, pred);
@@ -415,69 +430,122 @@ __device__ __forceinline__ void stage_flush(StageList s, int* list, int* gcount,
   if (ctid == 0) *s.count = 0;
 }
 
-// kGroups column groups of 4 epilogue warps each: group g owns columns
-// [g*W/kGroups, (g+1)*W/kGroups) of every layer (TMEM lane quadrant = warp % 4).
-// kResident: all hidden-layer weights stay in SMEM for the whole launch (64-wide nets);
-// otherwise a producer warp streams 32-wide K chunks through a 2-stage ring.
-template <int W, bool kGrad, int kGroups, int kTerms, bool kResident>
+// Ray-slot pipeline of the persistent trace (kPersist): every epilogue row of group 0 owns
+// one ray; when a ray leaves the level its row takes a prefetched ray from the warp's pool
+// (one prefetch register set per lane).  A lane's prefetch runs NEED -> LISTED (claimed
+// list item, slot load in flight) -> READY (ray state loads in flight), one stage per
+// tile, so no load sits on the critical path of a tile.
+enum PfStage : int { kPfNeed = 0, kPfListed = 1, kPfReady = 2 };
+
+// The fused SIREN tile kernel.
+//  kGroups   column groups of 4 epilogue warps; 16-column block b of every layer belongs
+//            to group b % kGroups (TMEM lane quadrant = warp % 4)
+//  kResident all hidden-layer weights stay in SMEM (64-wide nets); otherwise a producer
+//            warp streams 32-wide K chunks through a 2-stage ring
+//  kPersist  one launch traces a whole level: rows are refilled from the level's input
+//            list until it drains (sphere_trace_level, trace.cpp:61-84)
+// MMA layer m = 0 is layer 0 (K = 32, B0 resident), m = 1..L-2 the hidden layers; the
+// last hidden layer's epilogue folds in the 1 x W output layer.
+template <int W, bool kGrad, int kGroups, int kTerms, bool kResident, bool kPersist>
 __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
                                   (W == 64 ? 4 : (kGroups > 2 ? 1 : 2))) tc_mlp_kernel(TcArgs a) {
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  extern __shared__ __align__(128) uint8_t smem_raw[];
   constexpr int kCtl = kResident ? 1 : 2;  // control warps: MMA issuer [+ weight producer]
   constexpr int kThreads = 32 * kCtl + 128 * kGroups;
-  constexpr int kCols = W / kGroups;       // columns per epilogue group
   const TcNet& net = a.net;
   const int L = net.n_layers;
-  const TcSmem sm = tc_carve(smem_raw, W, L, kTerms, kResident);
+  const TcSmem sm = tc_carve(smem_raw, W, L, kTerms, kResident, kPersist);
   constexpr int kNW = kTerms == 3 ? 2 : 1;  // weight parts (hi [, lo])
   uint64_t* full = sm.bars;
   uint64_t* empty = sm.bars + kStages;
-  uint64_t* aready = sm.bars + 2 * kStages;
-  uint64_t* dfull = sm.bars + 2 * kStages + 1;
+  uint64_t* kready = sm.bars + 2 * kStages;  // [kSub]: A block row i written by every group
+  uint64_t* a0ready = sm.bars + 2 * kStages + kMaxSub;
+  uint64_t* dfull = sm.bars + 2 * kStages + kMaxSub + 1;
+  uint64_t* tstart = sm.bars + 2 * kStages + kMaxSub + 2;
   float* part = sm.part;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int IN = net.input_dim;
-  const int n_hidden = L - 2;  // MMA layers
+  const int n_hidden = L - 2;  // hidden (W x W) MMA layers
   constexpr int kRaysPerTile = kGrad ? kRows / 4 : kRows;
   constexpr int kChunks = W / kKC;
   constexpr uint32_t kChunkBytes = uint32_t(W) * kKC * 2;
   constexpr size_t kStageHalves = size_t(W) * kKC * kNW;
+  // K streaming: block b of a layer's output belongs to group b % kGroups, so the groups
+  // together produce the next layer's A operand in natural K order, block row i = blocks
+  // [i*kGroups, (i+1)*kGroups), and the MMA of layer m+1 starts on block row 0 while the
+  // epilogue still works on layer m.  Accumulators alternate between two TMEM regions
+  // (layer m in columns (m & 1) * W).
+  constexpr int kSub = W / kBlk / kGroups;
+  static_assert(kSub <= kMaxSub, "kready barriers");
+  constexpr uint32_t kTmemCols = 2 * W;
 
   const int n_items = (a.op == kOpEval || a.op == kOpNormalMap) ? a.k : *a.in_count;
-  const int n_tiles = (n_items + kRaysPerTile - 1) / kRaysPerTile;
-  const int my_tiles = blockIdx.x < n_tiles ? (n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
-  if (my_tiles == 0) return;
-
-  // ---- setup: constants to SMEM, barriers, TMEM ----
-  // layer 0 folded into one float4 per neuron; a 4-input net's time column joins the bias
-  // (time is fixed per launch: the slice time, field.cpp:213-220)
-  for (int n = threadIdx.x; n < W; n += kThreads) {
-    const float* w = net.w0 + n * IN;
-    float b0 = net.b[n];
-    if (IN == 4) b0 = fmaf(w[3], a.time, b0);
-    sm.w0r[n] = make_float4(net.omega * w[0], net.omega * w[1], net.omega * w[2], net.omega * b0);
+  int my_tiles, claim = 1;
+  if (kPersist) {
+    // claim granularity: up to 32 list items per warp claim, fewer for short lists so the
+    // items spread over the CTAs
+    claim = max(1, min(32, (n_items + gridDim.x * 16 - 1) / (gridDim.x * 16)));
+    if (n_items == 0 || int(blockIdx.x) * 4 * claim >= n_items) return;
+    my_tiles = 0x7fffffff;
+  } else {
+    const int n_tiles = (n_items + kRaysPerTile - 1) / kRaysPerTile;
+    my_tiles = blockIdx.x < n_tiles ? (n_tiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    if (my_tiles == 0) return;
   }
-  for (int i = threadIdx.x; i < (L - 1) * W; i += kThreads) sm.bias[i] = net.b[i] * net.omega;
+
+  // ---- setup: B0, biases, barriers, TMEM ----
+  for (int i = threadIdx.x; i < W * kK0; i += kThreads) {
+    const int n = i / kK0, k = i % kK0;
+    const float* w = net.w0 + n * net.input_dim;
+    __half v = __float2half_rn(0.0f);
+    if (k < 9 || (k >= 10 && k < 16)) {
+      const float x = net.omega * w[(k < 9 ? k : k - 10) % 3];  // radians
+      const __half hi = __float2half_rn(x);
+      v = k < 9 ? hi : __float2half_rn(x - __half2float(hi));
+    } else if (k == 9 || k == 16 || k == 17) {
+      // a 4-input net's time column joins the bias (the slice time, field.cpp:213-220)
+      float b0 = net.b[n];
+      if (net.input_dim == 4) b0 = fmaf(w[3], a.time, b0);
+      __half hi, mid, lo;
+      split3(net.omega * b0, hi, mid, lo);
+      v = k == 9 ? hi : (k == 16 ? mid : lo);
+    }
+    sm.b0[b0_off(W, n, k)] = v;
+  }
+  for (int i = threadIdx.x; i < (L - 1) * W; i += kThreads) sm.bias[i] = i < W ? 0.0f : net.b[i] * net.omega;
   for (int i = threadIdx.x; i < W; i += kThreads) sm.wout[i] = net.wout[i];
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    mbar_init(aready, 128 * kGroups);
+    for (int i = 0; i < kSub; ++i) mbar_init(&kready[i], 128 * kGroups);
+    mbar_init(a0ready, 128 * kGroups);
     mbar_init(dfull, 1);
-    sm.stage_count[0] = sm.stage_count[1] = 0;
+    mbar_init(tstart, 1);
+    *sm.stage_count = 0;
+    *sm.done = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_addr(sm.tmem_base)),
-                 "r"(uint32_t(W < 32 ? 32 : W)));
+                 "r"(kTmemCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
+  fence_proxy_async();  // B0 (generic-proxy writes) -> tensor core
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *sm.tmem_base;
+
+  // Control warps' tile loop: a fixed tile count, or (persistent) one tstart phase per tile
+  // published by the epilogue, with the done flag ending the loop.
+  uint32_t ts_phase = 0;
+  auto more_tiles = [&](int t) -> bool {
+    if (!kPersist) return t < my_tiles;
+    mbar_wait(tstart, ts_phase, a.suspend_ns);
+    ts_phase ^= 1;
+    return *reinterpret_cast<volatile int*>(sm.done) == 0;
+  };
 
   if (warp == 0) {
     // ================= MMA issuer (resident mode: also loads the weights once) =================
@@ -485,47 +553,67 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
       const uint32_t idesc = umma_idesc(W);
       const uint32_t a_base = smem_addr(sm.a);
       const uint32_t alo_base = smem_addr(sm.alo);
+      const uint32_t b0_base = smem_addr(sm.b0);
       if (kResident) {
         const uint32_t bytes = uint32_t(n_hidden) * W * W * 2 * 2;
         mbar_expect_tx(&full[0], bytes);
         bulk_g2s(sm.wst, net.wq, bytes, &full[0]);
         mbar_wait(&full[0], 0, 0);
       }
-      uint32_t chunk_iter = 0, aready_phase = 0;
-      for (int t = 0; t < my_tiles; ++t) {
-        for (int h = 0; h < n_hidden; ++h) {
-          mbar_wait(aready, aready_phase, a.suspend_ns);
-          aready_phase ^= 1;
-          tc_fence_after();
-          for (int c = 0; c < kChunks; ++c, ++chunk_iter) {
-            const int s = chunk_iter % kStages;
-            uint32_t b_base, lo_off;
-            if (kResident) {
-              // resident layout per layer: [hi W*W][lo W*W], chunk c contiguous inside each
-              b_base = smem_addr(sm.wst + size_t(h) * 2 * W * W + size_t(c) * W * kKC);
-              lo_off = uint32_t(W) * W * 2;
-            } else {
-              mbar_wait(&full[s], (chunk_iter / kStages) & 1, a.suspend_ns);
-              tc_fence_after();
-              b_base = smem_addr(sm.wst + size_t(s) * kStageHalves);
-              lo_off = uint32_t(W) * kKC * 2;
-            }
+      uint32_t chunk_iter = 0, kr_phase = 0, a0_phase = 0;
+      for (int t = 0; more_tiles(t); ++t) {
+        // ---- layer 0: D0 = A0 . B0^T, K = 32 (the split lives in K: one term) ----
+        mbar_wait(a0ready, a0_phase, a.suspend_ns);
+        a0_phase ^= 1;
+        tc_fence_after();
 #pragma unroll
-            for (int ks = 0; ks < kKC / 16; ++ks) {
-              const int kg = c * (kKC / 8) + ks * 2;  // first 8-element k group of this K=16 step
-              const uint32_t aoff = uint32_t(kg) * (kRows / 8) * 128, boff = uint32_t(ks * 2) * (W / 8) * 128;
-              const uint64_t ad = umma_desc(a_base + aoff, kRows * 16, 128);
-              const uint64_t bd = umma_desc(b_base + boff, W * 16, 128);
-              tc_mma(tmem, ad, bd, idesc, (c | ks) != 0);
-              if (kTerms == 3) {  // split precision: + A_lo.W_hi + A_hi.W_lo
-                const uint64_t adl = umma_desc(alo_base + aoff, kRows * 16, 128);
-                const uint64_t bdl = umma_desc(b_base + lo_off + boff, W * 16, 128);
-                tc_mma(tmem, adl, bd, idesc, 1);
-                tc_mma(tmem, ad, bdl, idesc, 1);
+        for (int ks = 0; ks < kK0 / 16; ++ks) {
+          const uint64_t ad = umma_desc(a_base + uint32_t(ks * 2) * (kRows / 8) * 128, kRows * 16, 128);
+          const uint64_t bd = umma_desc(b0_base + uint32_t(ks * 2) * (W / 8) * 128, W * 16, 128);
+          tc_mma(tmem, ad, bd, idesc, ks != 0);
+        }
+        tc_commit(dfull);
+        // ---- hidden layers, K-streamed behind the epilogue ----
+        for (int h = 0; h < n_hidden; ++h) {
+          const uint32_t d_tmem = tmem + uint32_t((h + 1) & 1) * W;
+          uint32_t b_base = 0, lo_off = 0;
+          int s = 0;
+#pragma unroll 1
+          for (int blk = 0; blk < W / kBlk; ++blk) {
+            if (blk % kGroups == 0) {  // block row of the A operand written by every group
+              mbar_wait(&kready[blk / kGroups], kr_phase, a.suspend_ns);
+              tc_fence_after();
+            }
+            const int c = blk >> 1, ks = blk & 1;  // 32-K weight chunk, K=16 step inside it
+            if (ks == 0) {
+              s = chunk_iter % kStages;
+              if (kResident) {
+                // resident layout per layer: [hi W*W][lo W*W], chunk c contiguous inside each
+                b_base = smem_addr(sm.wst + size_t(h) * 2 * W * W + size_t(c) * W * kKC);
+                lo_off = uint32_t(W) * W * 2;
+              } else {
+                mbar_wait(&full[s], (chunk_iter / kStages) & 1, a.suspend_ns);
+                tc_fence_after();
+                b_base = smem_addr(sm.wst + size_t(s) * kStageHalves);
+                lo_off = uint32_t(W) * kKC * 2;
               }
             }
-            if (!kResident) tc_commit(&empty[s]);  // frees the weight stage once these MMAs retire
+            const uint32_t aoff = uint32_t(blk * 2) * (kRows / 8) * 128, boff = uint32_t(ks * 2) * (W / 8) * 128;
+            const uint64_t ad = umma_desc(a_base + aoff, kRows * 16, 128);
+            const uint64_t bd = umma_desc(b_base + boff, W * 16, 128);
+            tc_mma(d_tmem, ad, bd, idesc, blk != 0);
+            if (kTerms == 3) {  // split precision: + A_lo.W_hi + A_hi.W_lo
+              const uint64_t adl = umma_desc(alo_base + aoff, kRows * 16, 128);
+              const uint64_t bdl = umma_desc(b_base + lo_off + boff, W * 16, 128);
+              tc_mma(d_tmem, adl, bd, idesc, 1);
+              tc_mma(d_tmem, ad, bdl, idesc, 1);
+            }
+            if (ks == 1) {
+              if (!kResident) tc_commit(&empty[s]);  // frees the weight stage once these MMAs retire
+              ++chunk_iter;
+            }
           }
+          kr_phase ^= 1;
           tc_commit(dfull);  // accumulator complete
         }
       }
@@ -534,7 +622,7 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
     // ================= weight producer =================
     if (lane == 0) {
       uint32_t chunk_iter = 0;
-      for (int t = 0; t < my_tiles; ++t) {
+      for (int t = 0; more_tiles(t); ++t) {
         for (int h = 0; h < n_hidden; ++h) {
           const __half* lw = reinterpret_cast<const __half*>(net.wq) + size_t(h) * 2 * W * W;
           for (int c = 0; c < kChunks; ++c, ++chunk_iter) {
@@ -556,75 +644,82 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
     const int q = warp & 3;                              // TMEM lane quadrant of this warp
     const int row = q * 32 + lane;                       // TMEM lane = A row
     const int ctid = (ew & 3) * 32 + lane;               // consumer thread id within group 0
-    const int col0 = eg * kCols;
-    const uint32_t taddr = tmem + (uint32_t(q * 32) << 16) + uint32_t(col0);
+    const uint32_t taddr = tmem + (uint32_t(q * 32) << 16);
     const int ray = kGrad ? row >> 2 : row;             // ray within the tile
     const int chain = kGrad ? row & 3 : 0;               // 0 = value, 1..3 = d/dx, d/dy, d/dz
     const unsigned group_mask = 0xFu << (lane & ~3);
-    const bool trace_state = a.op == kOpTrace && eg == 0;
-    const StageList st_next{sm.stage_buf, sm.stage_count};
-    const StageList st_adv{sm.stage_buf + kStageCap, sm.stage_count + 1};
     uint32_t dfull_phase = 0;
-    auto item_of = [&](int t) { return (blockIdx.x + t * gridDim.x) * kRaysPerTile + ray; };
-    RowIn now = load_row(a, load_slot(a, item_of(0), n_items), trace_state);
-    int slot_next = my_tiles > 1 ? load_slot(a, item_of(1), n_items) : -1;
-    for (int t = 0; t < my_tiles; ++t) {
-      const int item = item_of(t);
-      const bool valid = item < n_items;
-      // prefetch: ray state of tile t+1 (slot known), list slot of tile t+2
-      const RowIn next = t + 1 < my_tiles ? load_row(a, slot_next, trace_state) : RowIn{-1};
-      slot_next = t + 2 < my_tiles ? load_slot(a, item_of(t + 2), n_items) : -1;
-      // ---- layer 0: FP32 FFMA, sin -> fp16 A (this group's columns) ----
-#pragma unroll 1
-      for (int n0 = col0; n0 < col0 + kCols; n0 += 8) {
-        uint32_t pk[4], pl[4];
-#pragma unroll
-        for (int j = 0; j < 8; j += 2) {
-          float o[2];
-#pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            const float4 w = sm.w0r[n0 + j + u];  // radians: omega*(W0 p + b0)
-            const float z = fmaf(w.z, now.p[2], fmaf(w.y, now.p[1], fmaf(w.x, now.p[0], w.w)));
-            if (kGrad) {
-              // all 4 rows of a ray see the same point: one sine per lane, cos = sin(z + pi/2);
-              // tangent c: W0[n, c] * omega cos(z) = (omega W0[n, c]) * cos(z)
-              const float r = fast_sin(chain == 0 ? z : z + kHalfPi);
-              o[u] = chain == 0 ? r : (chain == 1 ? w.x : (chain == 2 ? w.y : w.z)) * r;
-            } else {
-              o[u] = fast_sin(z);
-            }
+
+    // One tile through the net from each row's point p (group 0 rows; `live` = the row
+    // carries a point): A0 -> layer 0 and the hidden layers on the tensor cores, sine
+    // epilogues here -> output dot.  Returns the output pre-bias in group 0 (the other
+    // groups' partials are combined through SMEM).
+    int dbg_t = 0;
+    auto mark = [&](int k) {
+      if (a.dbg && blockIdx.x == 0 && ew == 0 && lane == 0 && dbg_t < 64) a.dbg[dbg_t * 8 + k] = clock64();
+    };
+    auto eval_tile = [&](const float* p, bool live) -> float {
+      mark(0);
+      if (eg == 0) {
+        // ---- A0: the point in three fp16 parts (value rows) or a unit tangent ----
+        // 32-bit words = K pairs (k, k+1); layout in the kK0 comment above
+        auto pk2 = [](__half lo16, __half hi16) {
+          return uint32_t(__half_as_ushort(lo16)) | (uint32_t(__half_as_ushort(hi16)) << 16);
+        };
+        const __half one = __float2half_rn(1.0f), zero = __float2half_rn(0.0f);
+        uint32_t w0 = 0, w1 = 0, w2 = 0, w3 = 0, w4 = 0, w8 = 0;
+        if (live) {
+          if (!kGrad || chain == 0) {
+            __half h0, m0, l0, h1, m1, l1, h2, m2, l2;
+            split3(p[0], h0, m0, l0);
+            split3(p[1], h1, m1, l1);
+            split3(p[2], h2, m2, l2);
+            w0 = pk2(h0, h1);
+            w1 = pk2(h2, m0);
+            w2 = pk2(m1, m2);
+            w3 = pk2(l0, l1);
+            w4 = pk2(l2, one);
+            w8 = pk2(one, one);
+          } else {
+            w0 = chain == 1 ? pk2(one, zero) : (chain == 2 ? pk2(zero, one) : 0u);
+            w1 = chain == 3 ? pk2(one, zero) : 0u;
           }
-          pk[j / 2] = pack_half2(o[0], o[1]);
-          if (kTerms == 3) pl[j / 2] = pack_half2_lo(o[0], o[1], pk[j / 2]);
         }
-        *reinterpret_cast<uint4*>(&sm.a[a_off(row, n0)]) = make_uint4(pk[0], pk[1], pk[2], pk[3]);
-        if (kTerms == 3) *reinterpret_cast<uint4*>(&sm.alo[a_off(row, n0)]) = make_uint4(pl[0], pl[1], pl[2], pl[3]);
+        *reinterpret_cast<uint4*>(&sm.a[a_off(row, 0)]) = make_uint4(w0, w1, w2, w3);
+        *reinterpret_cast<uint4*>(&sm.a[a_off(row, 8)]) = make_uint4(w4, w0, w1, w2);
+        *reinterpret_cast<uint4*>(&sm.a[a_off(row, 16)]) = make_uint4(w8, 0u, 0u, 0u);
+        *reinterpret_cast<uint4*>(&sm.a[a_off(row, 24)]) = make_uint4(0u, 0u, 0u, 0u);
+        mark(6);
+        fence_proxy_async();
       }
-      fence_proxy_async();
+      // every epilogue thread: done with the previous tile's TMEM (region 0 is reused)
       tc_fence_before();
-      mbar_arrive(aready);
-      // ---- hidden layers ----
+      mbar_arrive(a0ready);
+      mark(1);
       float acc_out = 0.0f;
-      for (int h = 0; h < n_hidden; ++h) {
-        const bool last = h == n_hidden - 1;
+      for (int m = 0; m <= n_hidden; ++m) {
+        const bool last = m == n_hidden;
         mbar_wait(dfull, dfull_phase, a.suspend_ns);
+        mark(2 + 2 * min(m, 2));
         dfull_phase ^= 1;
         tc_fence_after();
-        const float* bias = sm.bias + size_t(h + 1) * W;
-        const float zs = net.omega * net.wscale[h];  // radians; undoes the 2^k weight scaling
-        const float dscale = net.omega * net.wscale[h];
-        // TMEM loads software-pipelined one 16-column chunk ahead of the math
+        const float* bias = sm.bias + size_t(m) * W;  // row 0: layer 0's bias is inside D0
+        // radians; undoes the 2^k weight scaling of the hidden layers
+        const float zs = m == 0 ? 1.0f : net.omega * net.wscale[m - 1];
+        const float dscale = zs;
+        const uint32_t treg = taddr + uint32_t(m & 1) * W;
+        // TMEM loads software-pipelined one block ahead of the math
         uint32_t raw[2][16];
-        tmem_issue16(taddr, raw[0]);
+        tmem_issue16(treg + uint32_t(eg * kBlk), raw[0]);
 #pragma unroll
-        for (int c = 0; c < kCols; c += 16) {
-          const int buf = (c / 16) & 1;
+        for (int i = 0; i < kSub; ++i) {
+          const int buf = i & 1;
+          const int cc = (i * kGroups + eg) * kBlk;
           tmem_wait16(raw[buf]);
-          if (c + 16 < kCols) tmem_issue16(taddr + uint32_t(c + 16), raw[buf ^ 1]);
+          if (i + 1 < kSub) tmem_issue16(treg + uint32_t(cc + kGroups * kBlk), raw[buf ^ 1]);
           float v[16];
 #pragma unroll
           for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(raw[buf][j]);
-          const int cc = col0 + c;
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
             if (kGrad) {
@@ -649,17 +744,19 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
                     make_uint4(pack_half2_lo(v[j], v[j + 1], h0), pack_half2_lo(v[j + 2], v[j + 3], h1),
                                pack_half2_lo(v[j + 4], v[j + 5], h2), pack_half2_lo(v[j + 6], v[j + 7], h3));
             }
+            // block row i of the next layer's A is complete in this group: the MMA may
+            // start on it while this thread continues with block i + 1
+            fence_proxy_async();
+            tc_fence_before();
+            mbar_arrive(&kready[i]);
           } else {
 #pragma unroll
             for (int j = 0; j < 16; ++j) acc_out = fmaf(sm.wout[cc + j], v[j], acc_out);
           }
         }
-        tc_fence_before();
-        if (!last) {
-          fence_proxy_async();
-          mbar_arrive(aready);
-        }
+        mark(3 + 2 * min(m, 2));
       }
+      ++dbg_t;
       // ---- combine the column groups' partial output dots ----
       if (kGroups > 1) {
         if (eg > 0) part[(eg - 1) * kRows + row] = acc_out;
@@ -667,69 +764,201 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
         if (eg == 0)
           for (int g = 1; g < kGroups; ++g) acc_out += part[(g - 1) * kRows + row];
       }
-      if (eg == 0) {
-        // ---- consumer (group 0) ----
-        const float fval = (!kGrad || chain == 0) ? acc_out + net.bout : acc_out;
-        if (a.op == kOpTrace) {
-          bool conv = false, cont = false;
-          if (valid)
-            tc_trace_update(a, now.slot, fval, now.p[0], now.p[1], now.p[2], now.t, now.dx, now.dy, now.dz, conv,
-                            cont);
-          stage_append(conv, now.slot, st_adv);
-          stage_append(cont, now.slot, st_next);
-          const bool last_tile = t + 1 == my_tiles;
-          stage_flush(st_adv, a.adv_list, a.adv_count, sm.stage_base, ctid, last_tile);
-          stage_flush(st_next, a.next_list, a.next_count, sm.stage_base, ctid, last_tile);
-        } else if (kGrad) {
-          const int base = lane & ~3;
-          const float gx = __shfl_sync(0xffffffffu, fval, base + 1);
-          const float gy = __shfl_sync(0xffffffffu, fval, base + 2);
-          const float gz = __shfl_sync(0xffffffffu, fval, base + 3);
-          const float f = __shfl_sync(0xffffffffu, fval, base);
-          bool defer = false;
-          const bool lead = chain == 0 && valid;
-          if (a.op == kOpNormals) {
-            if (lead) {
-              float nrm[3];
-              if (!normalize_normal(gx, gy, gz, nrm)) {
-                nrm[0] = 0.0f;
-                nrm[1] = 1.0f;
-                nrm[2] = 0.0f;
-                defer = a.defer_fallback != 0;
-              }
-              if (!defer) shade_and_write(a.sp, a.st, now.slot, nrm, a.rgb, a.depth, a.mask);
+      return acc_out;
+    };
+
+    if constexpr (kPersist) {
+      // ============ persistent level trace (sphere_trace_level, trace.cpp:61-84) ============
+      const bool g0 = eg == 0;
+      const RayState& st = a.st;
+      const StageList st_adv{sm.stage_buf, sm.stage_count};
+      const uint32_t lt = (1u << lane) - 1u;
+      int slot = -1, it = 0, evals = 0;
+      float px = 0.f, py = 0.f, pz = 0.f, t = 0.f, dx = 0.f, dy = 0.f, dz = 0.f;
+      int pf_slot = -1, pf_stage = kPfNeed;
+      float fpx = 0.f, fpy = 0.f, fpz = 0.f, fpt = 0.f, fdx = 0.f, fdy = 0.f, fdz = 0.f;
+      int res_base = 0, res_end = 0, nres = 0;  // claimed list range; next claim (lane 0)
+      bool exhausted = false;
+      if (g0 && lane == 0) nres = atomicAdd(a.cursor, claim);
+      // advance this warp's ray pipeline by one stage (group 0 only)
+      auto refill = [&]() {
+        // READY prefetches -> empty rows (the k-th empty row takes the k-th ready lane)
+        const uint32_t emp = __ballot_sync(0xffffffffu, slot < 0);
+        const uint32_t rdy = __ballot_sync(0xffffffffu, pf_stage == kPfReady);
+        if (emp && rdy) {
+          const int k = min(__popc(emp), __popc(rdy));
+          const int r = __popc(emp & lt);
+          const bool take = slot < 0 && r < k;
+          const int src = take ? nth_set_bit(rdy, r) : lane;
+          const int s_slot = __shfl_sync(0xffffffffu, pf_slot, src);
+          const float s_px = __shfl_sync(0xffffffffu, fpx, src), s_py = __shfl_sync(0xffffffffu, fpy, src),
+                      s_pz = __shfl_sync(0xffffffffu, fpz, src), s_t = __shfl_sync(0xffffffffu, fpt, src),
+                      s_dx = __shfl_sync(0xffffffffu, fdx, src), s_dy = __shfl_sync(0xffffffffu, fdy, src),
+                      s_dz = __shfl_sync(0xffffffffu, fdz, src);
+          if (take) {
+            slot = s_slot;
+            it = 0;
+            px = s_px, py = s_py, pz = s_pz, t = s_t, dx = s_dx, dy = s_dy, dz = s_dz;
+            st.level_reached[slot] = a.lv.level;
+          }
+          if (pf_stage == kPfReady && __popc(rdy & lt) < k) pf_stage = kPfNeed;
+        }
+        // LISTED -> READY: the slot arrived last tile; issue the ray-state loads
+        if (pf_stage == kPfListed) {
+          fpx = __ldg(st.px + pf_slot);
+          fpy = __ldg(st.py + pf_slot);
+          fpz = __ldg(st.pz + pf_slot);
+          fpt = __ldg(st.t + pf_slot);
+          fdx = __ldg(st.dx + pf_slot);
+          fdy = __ldg(st.dy + pf_slot);
+          fdz = __ldg(st.dz + pf_slot);
+          pf_stage = kPfReady;
+        }
+        // NEED -> LISTED: claim list items (warp claims of `claim` items, one claim ahead)
+        uint32_t need = __ballot_sync(0xffffffffu, pf_stage == kPfNeed);
+        while (need && !exhausted) {
+          if (res_base == res_end) {
+            res_base = __shfl_sync(0xffffffffu, nres, 0);
+            if (res_base >= n_items) {
+              exhausted = true;
+              break;
             }
-            warp_append(defer, now.slot, a.fb_list, a.fb_count);
-          } else if (a.op == kOpNormalMap) {
-            bool outside = false, fell_back = false;
-            if (lead) {
-              outside = fabs(double(f)) > a.delta;
-              float nrm[3];
-              if (!normalize_normal(gx, gy, gz, nrm)) {
-                fell_back = true;
-                for (int c = 0; c < 3; ++c)
-                  nrm[c] = a.fallback ? a.fallback[size_t(c) * a.k + item] : (c == 1 ? 1.0f : 0.0f);
-              }
-              for (int c = 0; c < 3; ++c) a.grad[size_t(c) * a.k + item] = nrm[c];
+            res_end = min(res_base + claim, n_items);
+            if (lane == 0) nres = atomicAdd(a.cursor, claim);
+          }
+          const int k = min(__popc(need), res_end - res_base);
+          const int r = __popc(need & lt);
+          if (((need >> lane) & 1u) && r < k) {
+            pf_slot = __ldg(a.in_list + res_base + r);
+            pf_stage = kPfListed;
+          }
+          res_base += k;
+          need = __ballot_sync(0xffffffffu, pf_stage == kPfNeed);
+        }
+      };
+      if (g0)
+        for (int i = 0; i < 3; ++i) refill();  // prime: rows filled, prefetches claimed
+      for (bool first = true;; first = false) {
+        if (g0 && !first) refill();
+        if (!bar_vote_any(3, 128 * kGroups, g0 && slot >= 0)) {
+          // no live row: either prefetches are still in flight (refill again) or done
+          if (bar_vote_any(3, 128 * kGroups, g0 && pf_stage != kPfNeed)) continue;
+          break;
+        }
+        if (ew == 0 && lane == 0) mbar_arrive(tstart);  // control warps: one more tile
+        const float p[3] = {px, py, pz};
+        const float acc = eval_tile(p, slot >= 0);
+        if (g0) {
+          const int s0 = slot;
+          bool conv = false;
+          if (slot >= 0) {
+            // trace update (trace.cpp:61-84; same arithmetic as trace_update, device_ops.cuh)
+            ++evals;
+            const float f = acc + net.bout;
+            const float fd = __fsub_rn(f, a.lv.delta);
+            const float afd = fabsf(fd);
+            conv = a.lv.final_level ? afd <= a.eps : fd <= a.eps;
+            bool cont = false;
+            if (!conv) {
+              float step = fd;
+              if (a.lv.final_level && step < 0.0f) step = 0.0f;  // trace.cpp:73
+              px = __fadd_rn(px, __fmul_rn(step, dx));
+              py = __fadd_rn(py, __fmul_rn(step, dy));
+              pz = __fadd_rn(pz, __fmul_rn(step, dz));
+              t = __fadd_rn(t, step);
+              cont = !(t > a.t_max);  // trace.cpp:78
             }
-            const unsigned mo = __ballot_sync(0xffffffffu, outside), mf = __ballot_sync(0xffffffffu, fell_back);
-            if (lane == 0 && (mo | mf)) {
-              atomicAdd(a.counts + 0, (unsigned long long)__popc(mo));
-              atomicAdd(a.counts + 1, (unsigned long long)__popc(mf));
-            }
-          } else if (lead) {
-            if (a.out) a.out[item] = f;
-            if (a.grad) {
-              a.grad[item] = gx;
-              a.grad[size_t(a.k) + item] = gy;
-              a.grad[size_t(2) * a.k + item] = gz;
+            ++it;
+            if (!cont || it == a.lv.budget) {  // the ray leaves the level: write its state once
+              st.px[slot] = px;
+              st.py[slot] = py;
+              st.pz[slot] = pz;
+              st.t[slot] = t;
+              st.iters[size_t(slot) * kMaxLevels + a.lv.level] = uint16_t(it);
+              st.final_dist[slot] = afd;
+              slot = -1;
             }
           }
-        } else if (valid) {
-          a.out[item] = fval;
+          stage_append(conv, s0, st_adv);
+          stage_flush(st_adv, a.adv_list, a.adv_count, sm.stage_base, ctid, false);
         }
       }
-      now = next;
+      if (ew == 0 && lane == 0) {
+        *reinterpret_cast<volatile int*>(sm.done) = 1;
+        mbar_arrive(tstart);
+      }
+      if (g0) {
+        stage_flush(st_adv, a.adv_list, a.adv_count, sm.stage_base, ctid, true);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) evals += __shfl_xor_sync(0xffffffffu, evals, o);
+        if (lane == 0 && evals) atomicAdd(a.evals, evals);
+      }
+    } else {
+      // ============ fixed tiles: normals / batch eval / normal map ============
+      auto item_of = [&](int t) { return (blockIdx.x + t * gridDim.x) * kRaysPerTile + ray; };
+      RowIn now = eg == 0 ? load_row(a, load_slot(a, item_of(0), n_items)) : RowIn{-1};
+      int slot_next = my_tiles > 1 && eg == 0 ? load_slot(a, item_of(1), n_items) : -1;
+      for (int t = 0; t < my_tiles; ++t) {
+        const int item = item_of(t);
+        const bool valid = item < n_items;
+        // prefetch: point of tile t+1 (slot known), list slot of tile t+2
+        const RowIn next = t + 1 < my_tiles && eg == 0 ? load_row(a, slot_next) : RowIn{-1};
+        slot_next = t + 2 < my_tiles && eg == 0 ? load_slot(a, item_of(t + 2), n_items) : -1;
+        const float acc_out = eval_tile(now.p, valid);
+        if (eg == 0) {
+          // ---- consumer (group 0) ----
+          const float fval = (!kGrad || chain == 0) ? acc_out + net.bout : acc_out;
+          if (kGrad) {
+            const int base = lane & ~3;
+            const float gx = __shfl_sync(0xffffffffu, fval, base + 1);
+            const float gy = __shfl_sync(0xffffffffu, fval, base + 2);
+            const float gz = __shfl_sync(0xffffffffu, fval, base + 3);
+            const float f = __shfl_sync(0xffffffffu, fval, base);
+            bool defer = false;
+            const bool lead = chain == 0 && valid;
+            if (a.op == kOpNormals) {
+              if (lead) {
+                float nrm[3];
+                if (!normalize_normal(gx, gy, gz, nrm)) {
+                  nrm[0] = 0.0f;
+                  nrm[1] = 1.0f;
+                  nrm[2] = 0.0f;
+                  defer = a.defer_fallback != 0;
+                }
+                if (!defer) shade_and_write(a.sp, a.st, now.slot, nrm, a.rgb, a.depth, a.mask);
+              }
+              warp_append(defer, now.slot, a.fb_list, a.fb_count);
+            } else if (a.op == kOpNormalMap) {
+              bool outside = false, fell_back = false;
+              if (lead) {
+                outside = fabs(double(f)) > a.delta;
+                float nrm[3];
+                if (!normalize_normal(gx, gy, gz, nrm)) {
+                  fell_back = true;
+                  for (int c = 0; c < 3; ++c)
+                    nrm[c] = a.fallback ? a.fallback[size_t(c) * a.k + item] : (c == 1 ? 1.0f : 0.0f);
+                }
+                for (int c = 0; c < 3; ++c) a.grad[size_t(c) * a.k + item] = nrm[c];
+              }
+              const unsigned mo = __ballot_sync(0xffffffffu, outside), mf = __ballot_sync(0xffffffffu, fell_back);
+              if (lane == 0 && (mo | mf)) {
+                atomicAdd(a.counts + 0, (unsigned long long)__popc(mo));
+                atomicAdd(a.counts + 1, (unsigned long long)__popc(mf));
+              }
+            } else if (lead) {
+              if (a.out) a.out[item] = f;
+              if (a.grad) {
+                a.grad[item] = gx;
+                a.grad[size_t(a.k) + item] = gy;
+                a.grad[size_t(2) * a.k + item] = gz;
+              }
+            }
+          } else if (valid) {
+            a.out[item] = fval;
+          }
+        }
+        now = next;
+      }
     }
   }
   // ---- teardown ----
@@ -738,16 +967,16 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
   if (warp == 0) {
     __syncwarp();
     tc_fence_after();
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(uint32_t(W < 32 ? 32 : W)));
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols));
   }
 }
 
-template <int W, bool kGrad, int kTerms, bool kResident>
+template <int W, bool kGrad, int kTerms, bool kResident, bool kPersist>
 bool launch_w(TcArgs& a, int n_max_items, cudaStream_t s) {
   constexpr int kGroups = W == 64 ? 1 : (W == 256 && kTerms == 3 ? 4 : 2);
   constexpr int kThreads = 32 * (kResident ? 1 : 2) + 128 * kGroups;
-  auto kernel = tc_mlp_kernel<W, kGrad, kGroups, kTerms, kResident>;
-  const size_t smem = tc_smem_bytes(W, a.net.n_layers, kTerms, kResident);
+  auto kernel = tc_mlp_kernel<W, kGrad, kGroups, kTerms, kResident, kPersist>;
+  const size_t smem = tc_smem_bytes(W, a.net.n_layers, kTerms, kResident, kPersist);
   static size_t configured_smem = 0;
   static int per_sm = 0;
   static int sms = 0;
@@ -769,10 +998,10 @@ bool launch_w(TcArgs& a, int n_max_items, cudaStream_t s) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     configured_smem = smem;
     if (getenv("NSDF_DEBUG_TC"))
-      fprintf(stderr, "tc_mlp_kernel<%d,%d,%d,%d,%d>: smem %zu B, regs %d, %d CTAs/SM (occupancy API %d)\n", W,
-              int(kGrad), kGroups, kTerms, int(kResident), smem, fa.numRegs, per_sm, occ);
+      fprintf(stderr, "tc_mlp_kernel<%d,%d,%d,%d,%d,%d>: smem %zu B, regs %d, %d CTAs/SM (occupancy API %d)\n", W,
+              int(kGrad), kGroups, kTerms, int(kResident), int(kPersist), smem, fa.numRegs, per_sm, occ);
   }
-  const int tmem_limit = 512 / (W < 32 ? 32 : W);
+  const int tmem_limit = 512 / (2 * W);  // two accumulator regions per CTA
   const int per = std::max(1, std::min(per_sm, tmem_limit));
   constexpr int kRaysPerTile = kGrad ? kRows / 4 : kRows;
   const int tiles = (n_max_items + kRaysPerTile - 1) / kRaysPerTile;
@@ -781,18 +1010,37 @@ bool launch_w(TcArgs& a, int n_max_items, cudaStream_t s) {
   return cudaGetLastError() == cudaSuccess;
 }
 
-template <bool kGrad, int kTerms>
+template <bool kGrad, int kTerms, bool kPersist>
 bool launch_terms(TcArgs& a, int n_max_items, cudaStream_t s) {
   // 64-wide nets keep every hidden layer resident in SMEM when it fits (<= 4 layers).
   const bool resident = a.net.width == 64 && a.net.n_layers - 2 <= 4;
   switch (a.net.width) {
     case 64:
-      return resident ? launch_w<64, kGrad, kTerms, true>(a, n_max_items, s)
-                      : launch_w<64, kGrad, kTerms, false>(a, n_max_items, s);
-    case 128: return launch_w<128, kGrad, kTerms, false>(a, n_max_items, s);
-    case 256: return launch_w<256, kGrad, kTerms, false>(a, n_max_items, s);
+      return resident ? launch_w<64, kGrad, kTerms, true, kPersist>(a, n_max_items, s)
+                      : launch_w<64, kGrad, kTerms, false, kPersist>(a, n_max_items, s);
+    case 128: return launch_w<128, kGrad, kTerms, false, kPersist>(a, n_max_items, s);
+    case 256: return launch_w<256, kGrad, kTerms, false, kPersist>(a, n_max_items, s);
     default: return false;
   }
+}
+
+long long* timeline_buffer() {
+  static long long* buf = nullptr;
+  if (!getenv("NSDF_TC_TIMELINE")) return nullptr;
+  if (!buf) cudaMallocManaged(&buf, 64 * 8 * sizeof(long long));
+  return buf;
+}
+void timeline_dump(long long* buf, const char* what) {
+  if (!buf) return;
+  cudaDeviceSynchronize();
+  fprintf(stderr, "timeline %s (cycles from tile start: a0 | dfull0 ep0 | dfull1 ep1 | a0-before-fence | -- | next)\n", what);
+  for (int t = 0; t < 12; ++t) {
+    const long long* r = buf + t * 8;
+    fprintf(stderr, "  tile %2d:", t);
+    for (int k = 1; k < 8; ++k) fprintf(stderr, " %7lld", r[k] ? r[k] - r[0] : -1);
+    fprintf(stderr, " %7lld\n", t < 11 ? buf[(t + 1) * 8] - r[0] : 0);
+  }
+  cudaMemset(buf, 0, 64 * 8 * sizeof(long long));
 }
 
 uint32_t suspend_hint() {
@@ -803,10 +1051,20 @@ uint32_t suspend_hint() {
   return v;
 }
 
-template <bool kGrad>
+template <bool kGrad, bool kPersist = false>
 bool launch_any(TcArgs& a, int n_max_items, cudaStream_t s) {
   a.suspend_ns = suspend_hint();
-  return a.terms == 3 ? launch_terms<kGrad, 3>(a, n_max_items, s) : launch_terms<kGrad, 1>(a, n_max_items, s);
+  a.dbg = timeline_buffer();
+  if (a.dbg) {
+    const bool ok = a.terms == 3 ? launch_terms<kGrad, 3, kPersist>(a, n_max_items, s)
+                                 : launch_terms<kGrad, 1, kPersist>(a, n_max_items, s);
+    char what[64];
+    snprintf(what, sizeof what, "W=%d grad=%d persist=%d", a.net.width, int(kGrad), int(kPersist));
+    timeline_dump(a.dbg, what);
+    return ok;
+  }
+  return a.terms == 3 ? launch_terms<kGrad, 3, kPersist>(a, n_max_items, s)
+                      : launch_terms<kGrad, 1, kPersist>(a, n_max_items, s);
 }
 
 TcNet tc_net(const DevNet& n) {
@@ -828,9 +1086,9 @@ TcNet tc_net(const DevNet& n) {
 
 bool tc_supported(const DevNet& n) { return n.tc_ok != 0; }
 
-bool tc_trace_iter(int terms, const LevelDesc& lv, float eps, float t_max, int iter, const int* in_list,
-                   const int* in_count, int* next_list, int* next_count, int* adv_list, int* adv_count,
-                   const RayState& st, int n_max, cudaStream_t s) {
+bool tc_trace_level(int terms, const LevelDesc& lv, float eps, float t_max, const int* in_list, const int* in_count,
+                    int* cursor, int* evals, int* adv_list, int* adv_count, const RayState& st, int n_max,
+                    cudaStream_t s) {
   TcArgs a{};
   a.terms = terms;
   a.net = tc_net(lv.field.net);
@@ -838,16 +1096,15 @@ bool tc_trace_iter(int terms, const LevelDesc& lv, float eps, float t_max, int i
   a.lv = lv;
   a.eps = eps;
   a.t_max = t_max;
-  a.iter = iter;
   a.in_list = in_list;
   a.in_count = in_count;
-  a.next_list = next_list;
-  a.next_count = next_count;
+  a.cursor = cursor;
+  a.evals = evals;
   a.adv_list = adv_list;
   a.adv_count = adv_count;
   a.st = st;
   a.time = lv.time;
-  return launch_any<false>(a, n_max, s);
+  return launch_any<false, true>(a, n_max, s);
 }
 
 bool tc_normals_shade(int terms, const DevField& nf, float time, const int* list, const int* count, int n_max,

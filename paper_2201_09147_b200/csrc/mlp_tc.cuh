@@ -7,9 +7,12 @@
 
 namespace nsdf_b200 {
 
-bool tc_trace_iter(int terms, const LevelDesc& lv, float eps, float t_max, int iter, const int* in_list, const int* in_count,
-                   int* next_list, int* next_count, int* adv_list, int* adv_count, const RayState& st, int n_max,
-                   cudaStream_t s);
+// Persistent level trace: one launch runs every iteration of a level; rows are refilled
+// from in_list (claimed through *cursor) until it drains.  Converged slots -> adv_list,
+// evaluations -> *evals.  cursor / evals / adv_count must be zeroed.
+bool tc_trace_level(int terms, const LevelDesc& lv, float eps, float t_max, const int* in_list, const int* in_count,
+                    int* cursor, int* evals, int* adv_list, int* adv_count, const RayState& st, int n_max,
+                    cudaStream_t s);
 bool tc_normals_shade(int terms, const DevField& nf, float time, const int* list, const int* count, int n_max,
                       const RayState& st, const ShadeParams& sp, bool defer_fallback, int* fb_list, int* fb_count,
                       float* rgb, float* depth, uint8_t* mask, cudaStream_t s);
