@@ -656,7 +656,7 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
     // groups' partials are combined through SMEM).
     int dbg_t = 0;
     auto mark = [&](int k) {
-      if (a.dbg && blockIdx.x == 0 && ew == 0 && lane == 0 && dbg_t < 64) a.dbg[dbg_t * 8 + k] = clock64();
+      if (a.dbg && blockIdx.x == 0 && ew == 0 && lane == 0 && dbg_t < 64) a.dbg[dbg_t * 16 + k] = clock64();
     };
     auto eval_tile = [&](const float* p, bool live) -> float {
       mark(0);
@@ -689,7 +689,7 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
         *reinterpret_cast<uint4*>(&sm.a[a_off(row, 8)]) = make_uint4(w4, w0, w1, w2);
         *reinterpret_cast<uint4*>(&sm.a[a_off(row, 16)]) = make_uint4(w8, 0u, 0u, 0u);
         *reinterpret_cast<uint4*>(&sm.a[a_off(row, 24)]) = make_uint4(0u, 0u, 0u, 0u);
-        mark(6);
+        mark(10);
         fence_proxy_async();
       }
       // every epilogue thread: done with the previous tile's TMEM (region 0 is reused)
@@ -700,7 +700,7 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
       for (int m = 0; m <= n_hidden; ++m) {
         const bool last = m == n_hidden;
         mbar_wait(dfull, dfull_phase, a.suspend_ns);
-        mark(2 + 2 * min(m, 2));
+        mark(2 + 2 * min(m, 3));
         dfull_phase ^= 1;
         tc_fence_after();
         const float* bias = sm.bias + size_t(m) * W;  // row 0: layer 0's bias is inside D0
@@ -754,7 +754,7 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
             for (int j = 0; j < 16; ++j) acc_out = fmaf(sm.wout[cc + j], v[j], acc_out);
           }
         }
-        mark(3 + 2 * min(m, 2));
+        mark(3 + 2 * min(m, 3));
       }
       ++dbg_t;
       // ---- combine the column groups' partial output dots ----
@@ -840,14 +840,17 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
         for (int i = 0; i < 3; ++i) refill();  // prime: rows filled, prefetches claimed
       for (bool first = true;; first = false) {
         if (g0 && !first) refill();
+        mark(14);
         if (!bar_vote_any(3, 128 * kGroups, g0 && slot >= 0)) {
           // no live row: either prefetches are still in flight (refill again) or done
           if (bar_vote_any(3, 128 * kGroups, g0 && pf_stage != kPfNeed)) continue;
           break;
         }
+        mark(15);
         if (ew == 0 && lane == 0) mbar_arrive(tstart);  // control warps: one more tile
         const float p[3] = {px, py, pz};
         const float acc = eval_tile(p, slot >= 0);
+        mark(11);
         if (g0) {
           const int s0 = slot;
           bool conv = false;
@@ -879,8 +882,10 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
               slot = -1;
             }
           }
+          mark(12);
           stage_append(conv, s0, st_adv);
           stage_flush(st_adv, a.adv_list, a.adv_count, sm.stage_base, ctid, false);
+          mark(13);
         }
       }
       if (ew == 0 && lane == 0) {
@@ -1027,20 +1032,26 @@ bool launch_terms(TcArgs& a, int n_max_items, cudaStream_t s) {
 long long* timeline_buffer() {
   static long long* buf = nullptr;
   if (!getenv("NSDF_TC_TIMELINE")) return nullptr;
-  if (!buf) cudaMallocManaged(&buf, 64 * 8 * sizeof(long long));
+  if (!buf) cudaMallocManaged(&buf, 65 * 16 * sizeof(long long));
   return buf;
 }
 void timeline_dump(long long* buf, const char* what) {
   if (!buf) return;
   cudaDeviceSynchronize();
-  fprintf(stderr, "timeline %s (cycles from tile start: a0 | dfull0 ep0 | dfull1 ep1 | a0-before-fence | -- | next)\n", what);
+  fprintf(stderr,
+          "timeline %s (SM cycles from the tile's start)\n  tile: a0fence  a0arr | dfull, epilogue end per MMA layer | "
+          "ret  upd  flush || refill vote next\n",
+          what);
   for (int t = 0; t < 12; ++t) {
-    const long long* r = buf + t * 8;
-    fprintf(stderr, "  tile %2d:", t);
-    for (int k = 1; k < 8; ++k) fprintf(stderr, " %7lld", r[k] ? r[k] - r[0] : -1);
-    fprintf(stderr, " %7lld\n", t < 11 ? buf[(t + 1) * 8] - r[0] : 0);
+    const long long* r = buf + t * 16;
+    const long long* nx = buf + (t + 1) * 16;  // marks taken after the tile counter advanced
+    auto d = [&](const long long* q, int k) { return q[k] ? q[k] - r[0] : -1; };
+    fprintf(stderr, "  %2d: %6lld %6lld |", t, d(r, 10), d(r, 1));
+    for (int k = 2; k < 10; ++k) fprintf(stderr, " %6lld", d(r, k));
+    fprintf(stderr, " | %6lld %6lld %6lld || %6lld %6lld %6lld\n", d(nx, 11), d(nx, 12), d(nx, 13), d(nx, 14),
+            d(nx, 15), nx[0] ? nx[0] - r[0] : -1);
   }
-  cudaMemset(buf, 0, 64 * 8 * sizeof(long long));
+  cudaMemset(buf, 0, 65 * 16 * sizeof(long long));
 }
 
 uint32_t suspend_hint() {

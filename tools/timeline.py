@@ -1,0 +1,28 @@
+"""Per-tile timeline of CTA 0 of every tcgen05 launch of one config-2 frame (NSDF_TC_TIMELINE).
+
+    NSDF_TC_TIMELINE=1 python tools/timeline.py [width height]
+Columns (SM cycles from the tile's start): A0 arrive | dfull0 | ep0 end | dfull1 | ep1 end |
+A0 before fence | (trace) vote done (before the tile's start mark of the NEXT tile) | next tile.
+"""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+os.environ.setdefault("NSDF_TC_TIMELINE", "1")
+import torch  # noqa: E402
+
+from paper_2201_09147_b200.abi import ShadeConfig, TraceConfig, standard_camera  # noqa: E402
+from paper_2201_09147_b200.engine import Context, DeviceSequence  # noqa: E402
+from paper_2201_09147_b200.manifest import load_manifest  # noqa: E402
+
+w, h = (int(sys.argv[1]), int(sys.argv[2])) if len(sys.argv) > 2 else (1920, 1080)
+seq = load_manifest(os.path.join(ROOT, "assets", "torus_w30.nest"))
+ctx = Context(0, "fp16")
+ds = DeviceSequence(ctx, seq)
+n = w * h
+rgb, depth, mask = torch.zeros(3 * n, device="cuda"), torch.zeros(n, device="cuda"), torch.zeros(n, dtype=torch.uint8, device="cuda")
+ctx.render_device(ds.levels(), standard_camera(w, h), TraceConfig((20, 5, 5)), ShadeConfig(specular=0.3),
+                  rgb.data_ptr(), depth.data_ptr(), mask.data_ptr(), 0)
+torch.cuda.synchronize()
+ctx.close()
