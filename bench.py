@@ -95,6 +95,23 @@ def peaks():
         return PEAKS_FALLBACK, "fallback"
 
 
+def ncu_traffic(gbuffer: bool):
+    """DRAM bytes per launch of the roofline kernel(s) from the committed `ncu --set full`
+    capture (profiles/*_traffic.json, tools/summarize_profile.py): the three persistent
+    trace-level kernels of one frame (config 2), or None when no capture matches."""
+    import glob
+    import re
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_traffic.json")))
+    if not files or gbuffer:
+        return None, None
+    d = json.load(open(files[-1]))
+    sel = {k: v for k, v in d["dram_bytes_per_launch"].items() if re.match(r"tc_mlp_kernel<\d+, 0, \d, \d, \d, 1>", k)}
+    if not sel:
+        return None, None
+    return sum(sel.values()), f"DRAM read+write bytes of the {len(sel)} trace-level launches of one frame, " \
+                             f"ncu --set full ({d['source']})"
+
+
 class ClockSampler:
     """nvidia-smi clocks + throttle reasons sampled during the timed region."""
 
@@ -481,6 +498,7 @@ def main():
     unit = "Mnormals/s" if W["gbuffer"] else "Mrays/s"
 
     pk, pk_kind = peaks()
+    traffic, traffic_note = ncu_traffic(W["gbuffer"]) if args.config == 2 else (None, None)
     peak_tf = pk.get("bf16_tflops_sustained", pk["bf16_tflops"])
     if W["gbuffer"]:
         flops_trace, flops_normals = 0, units_per_step * 2 * seq.members[0].macs_normal()
@@ -539,7 +557,8 @@ def main():
             "frame": frame,
             "roofline": {"bound": "tensor", "kernel": kernel, "achieved": achieved_tf, "peak": peak_tf,
                          "unit": "TFLOP/s", "frac": achieved_tf / peak_tf,
-                         "peak_kind": f"{pk_kind} bf16 sustained (MEASURED_PEAKS.json)", "traffic": None,
+                         "peak_kind": f"{pk_kind} bf16 sustained (MEASURED_PEAKS.json)", "traffic": traffic,
+                         "traffic_note": traffic_note,
                          "whole_frame_tflops": (flops_trace + flops_normals) / (ms_per_frame / 1e3) / 1e12,
                          "activation_bound": None if W["gbuffer"] else act_bound},
             "cpu_baseline": cpu,
