@@ -72,8 +72,8 @@ def parse():
     ap.add_argument("--width", type=int, default=0)
     ap.add_argument("--height", type=int, default=0)
     ap.add_argument("--budgets", default="")
-    ap.add_argument("--tile", type=int, default=64)
-    ap.add_argument("--inflight", type=int, default=2,
+    ap.add_argument("--tile", type=int, default=32, help="image tile edge of the N>1 tile interleave")
+    ap.add_argument("--inflight", type=int, default=3,
                     help="frames in flight (engine contexts on their own streams); 1 = strictly serial frames")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")

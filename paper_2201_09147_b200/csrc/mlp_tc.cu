@@ -224,6 +224,7 @@ struct TcArgs {
   int op;
   int terms;  // 3 = split-fp16 (A_hi.W_hi + A_lo.W_hi + A_hi.W_lo), 1 = plain fp16
   uint32_t suspend_ns;
+  int claim_div;  // persistent trace: claim granularity = n / (grid * claim_div), clamped to [1, 32]
   // trace (persistent level)
   LevelDesc lv;
   float eps, t_max;
@@ -483,7 +484,8 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
   if (kPersist) {
     // claim granularity: up to 32 list items per warp claim, fewer for short lists so the
     // items spread over the CTAs
-    claim = max(1, min(32, (n_items + gridDim.x * 16 - 1) / (gridDim.x * 16)));
+    const int div = int(gridDim.x) * a.claim_div;
+    claim = max(1, min(32, (n_items + div - 1) / div));
     if (n_items == 0 || int(blockIdx.x) * 4 * claim >= n_items) return;
     my_tiles = 0x7fffffff;
   } else {
@@ -1065,6 +1067,11 @@ uint32_t suspend_hint() {
 template <bool kGrad, bool kPersist = false>
 bool launch_any(TcArgs& a, int n_max_items, cudaStream_t s) {
   a.suspend_ns = suspend_hint();
+  static const int claim_div = [] {
+    const char* e = getenv("NSDF_TC_CLAIM_DIV");
+    return e ? std::max(1, atoi(e)) : 4;
+  }();
+  a.claim_div = claim_div;
   a.dbg = timeline_buffer();
   if (a.dbg) {
     const bool ok = a.terms == 3 ? launch_terms<kGrad, 3, kPersist>(a, n_max_items, s)
