@@ -14,6 +14,10 @@
  *                             spatial_gradient_batch<float>
  *                             Field::grad_batch(Matrix<float>)          src/fields/field.cpp:173-175, 309-311
  *   nsdf_cuda_eval_grad       mlp::forward_and_gradient_batch<float>    src/mlp/mlp.cpp:297-306
+ *   nsdf_cuda_eval_f64        mlp::forward_batch / forward_and_gradient_batch / (spatial_)
+ *                             gradient_batch<double>                    src/mlp/mlp.cpp:104-210
+ *                             NeuralField / NeuralTimeField f64 batches src/fields/field.cpp:167-178, 301-311
+ *                             (the certification path: nesting.cpp:131-361)
  *   nsdf_cuda_generate_rays   tracer::generate_rays                     src/tracer/camera.cpp:20-43
  *   nsdf_cuda_trace_rays      tracer::multiscale_sphere_trace (batched) src/tracer/trace.cpp:86-132, 162-169
  *   nsdf_cuda_sphere_trace    tracer::sphere_trace                      src/tracer/trace.cpp:136-160
@@ -192,6 +196,13 @@ int nsdf_cuda_eval_grad(nsdf_ctx* ctx, nsdf_field field, const float* points, in
                         float time, float* out, float* grad);
 int nsdf_cuda_eval_grad_device(nsdf_ctx* ctx, nsdf_field field, const float* d_points, int rows,
                                int k, float time, float* d_out, float* d_grad);
+/* FP64 evaluation of a neural field, bit-exact with the reference's double AVX2 path
+ * (certification: estimate_sup_diff / verify_nesting / sample_near_surface).  points:
+ * rows x k doubles (HOST); out: k or NULL; grad: 3 x k or NULL (not both NULL).  A 3-row
+ * batch for a 4-input net gets the constant `time` row (double, field.cpp:213-220).
+ * Analytic fields return NSDF_ERR_CONFIG (they evaluate on the host). */
+int nsdf_cuda_eval_f64(nsdf_ctx* ctx, nsdf_field field, const double* points, int rows, int k,
+                       double time, double* out, double* grad);
 
 /* ---- tracing --------------------------------------------------------------------------
  * rays: n x 6 floats {ox, oy, oz, dx, dy, dz} (tracer::Ray, trace.hpp:24-27). */

@@ -24,6 +24,21 @@ int nsdf_host_trace_image_manifest(const char* manifest, double time, const nsdf
 int nsdf_host_forward_and_gradient(const char* sdfnet, const float* points, int k, float* dist,
                                    float* grad);
 
+/* Certification (fields::sample_near_surface / estimate_sup_diff / verify_nesting,
+ * nesting.cpp:131-361) through the drop-in library; neural fields evaluate on the device
+ * FP64 path.  A field source is "weights:<file.sdfnet>" or an analytic spec
+ * ("torus:R=0.6,r=0.3").
+ *   sample_near_surface: out = count x 3 doubles; gaussian != 0 selects gaussian noise.
+ *   sup_diff: f's domain is set to g's; out = {eps, raw_max, argmax x, y, z, samples}.
+ *   verify_nesting: counts = {samples_total, checked, violation_count, n_recorded};
+ *                   recorded = n_recorded x {x, y, z, pair, f_coarse, f_fine}. */
+int nsdf_host_sample_near_surface(const char* field, uint64_t count, int gaussian, double amount,
+                                  uint64_t seed, double* out);
+int nsdf_host_sup_diff(const char* f_src, const char* g_src, uint64_t n_uniform, uint64_t n_surface,
+                       double margin, double noise_halfwidth, uint64_t seed, double* out);
+int nsdf_host_verify_nesting(const char* manifest, double time, uint64_t samples, uint64_t seed,
+                             uint64_t max_recorded, uint64_t* counts, double* recorded);
+
 #ifdef __cplusplus
 }
 #endif

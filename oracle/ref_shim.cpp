@@ -369,4 +369,78 @@ int nsdf_ref_certify(const char* const* weight_paths, const char* const* labels,
   SHIM_CATCH
 }
 
+// ---- certification (nesting.cpp:131-361), same signatures as nsdf_host.h ----
+static fields::FieldPtr ref_field(const char* src, const Aabb* domain = nullptr) {
+  const std::string s(src);
+  if (s.rfind("weights:", 0) == 0) {
+    auto f = std::make_shared<fields::NeuralField>(mlp::load_params(s.substr(8)));
+    if (domain) f->set_domain(*domain);
+    return f;
+  }
+  return fields::make_analytic_field(fields::parse_field_spec(s));
+}
+
+int nsdf_ref_sample_near_surface(const char* field, uint64_t count, int gaussian, double amount, uint64_t seed,
+                                 double* out) {
+  SHIM_TRY
+  auto f = ref_field(field);
+  Rng rng(seed);
+  fields::SurfaceNoise noise;
+  noise.kind = gaussian ? fields::SurfaceNoise::Kind::gaussian : fields::SurfaceNoise::Kind::uniform;
+  noise.amount = amount;
+  auto pts = fields::sample_near_surface(*f, size_t(count), noise, rng);
+  for (size_t i = 0; i < pts.size(); ++i) {
+    out[3 * i] = pts[i].x;
+    out[3 * i + 1] = pts[i].y;
+    out[3 * i + 2] = pts[i].z;
+  }
+  SHIM_CATCH
+}
+
+int nsdf_ref_sup_diff(const char* f_src, const char* g_src, uint64_t n_uniform, uint64_t n_surface, double margin,
+                      double noise_halfwidth, uint64_t seed, double* out) {
+  SHIM_TRY
+  auto g = ref_field(g_src);
+  auto f = ref_field(f_src, &g->domain());
+  fields::SupSamplerConfig cfg;
+  cfg.n_uniform = size_t(n_uniform);
+  cfg.n_surface = size_t(n_surface);
+  cfg.margin = margin;
+  cfg.noise_halfwidth = noise_halfwidth;
+  cfg.seed = seed;
+  auto r = fields::estimate_sup_diff(*f, *g, cfg);
+  out[0] = r.eps;
+  out[1] = r.raw_max;
+  out[2] = r.argmax.x;
+  out[3] = r.argmax.y;
+  out[4] = r.argmax.z;
+  out[5] = double(r.samples);
+  SHIM_CATCH
+}
+
+int nsdf_ref_verify_nesting(const char* manifest, double time, uint64_t samples, uint64_t seed, uint64_t max_recorded,
+                            uint64_t* counts, double* recorded) {
+  SHIM_TRY
+  auto seq = load_sequence(manifest, time);
+  fields::VerifyConfig cfg;
+  cfg.samples = size_t(samples);
+  cfg.seed = seed;
+  cfg.max_recorded_violations = size_t(max_recorded);
+  auto r = fields::verify_nesting(seq, cfg);
+  counts[0] = r.samples_total;
+  counts[1] = r.checked;
+  counts[2] = r.violation_count;
+  counts[3] = r.violations.size();
+  for (size_t i = 0; i < r.violations.size(); ++i) {
+    double* o = recorded + 6 * i;
+    o[0] = r.violations[i].point.x;
+    o[1] = r.violations[i].point.y;
+    o[2] = r.violations[i].point.z;
+    o[3] = double(r.violations[i].pair_index);
+    o[4] = r.violations[i].f_coarse;
+    o[5] = r.violations[i].f_fine;
+  }
+  SHIM_CATCH
+}
+
 }  // extern "C"

@@ -231,3 +231,32 @@ def render(manifest, cam: Camera, trace: TraceConfig, shade_cfg: ShadeConfig, no
                                     _p(depth, F), _p(mask, U8), ctypes.byref(sec)))
     return (rgb.reshape(cam.height, cam.width, 3), depth.reshape(cam.height, cam.width),
             mask.reshape(cam.height, cam.width), sec.value)
+
+
+# ---- certification (nesting.cpp:131-361) -------------------------------------------------
+def sample_near_surface(field_src, count, gaussian=False, amount=0.1, seed=1):
+    lib = load()
+    out = np.zeros((count, 3), np.float64)
+    _check(lib, lib.nsdf_ref_sample_near_surface(field_src.encode(), U64(count), int(gaussian), D(amount),
+                                                 U64(seed), _p(out, D)))
+    return out
+
+
+def sup_diff(f_src, g_src, n_uniform=20000, n_surface=20000, margin=1e-3, noise=0.1, seed=1):
+    """{eps, raw_max, argmax (3,), samples} of fields::estimate_sup_diff."""
+    lib = load()
+    out = np.zeros(6, np.float64)
+    _check(lib, lib.nsdf_ref_sup_diff(f_src.encode(), g_src.encode(), U64(n_uniform), U64(n_surface), D(margin),
+                                      D(noise), U64(seed), _p(out, D)))
+    return {"eps": out[0], "raw_max": out[1], "argmax": out[2:5].copy(), "samples": int(out[5])}
+
+
+def verify_nesting(manifest, samples=100000, seed=7, max_recorded=1000, time=0.0):
+    """{samples_total, checked, violation_count, violations (n, 6)} of fields::verify_nesting."""
+    lib = load()
+    counts = np.zeros(4, np.uint64)
+    rec = np.zeros((max_recorded, 6), np.float64)
+    _check(lib, lib.nsdf_ref_verify_nesting(manifest.encode(), D(time), U64(samples), U64(seed), U64(max_recorded),
+                                            _p(counts, U64), _p(rec, D)))
+    return {"samples_total": int(counts[0]), "checked": int(counts[1]), "violation_count": int(counts[2]),
+            "violations": rec[:int(counts[3])].copy()}

@@ -29,6 +29,7 @@ CUDA_SOURCES = {
     "engine.cu": ["-fmad=false"],
     "capi.cu": ["-fmad=false"],
     "mlp_tc.cu": [],
+    "mlp_f64.cu": ["-fmad=false"],
 }
 
 

@@ -461,17 +461,36 @@ int nsdf_cuda_upload_mlp(nsdf_ctx* c, int n_layers, const int32_t* rows, const i
   n.input_dim = input_dim;
   n.activation = activation;
   n.omega = float(omega0);
+  n.omega_d = omega0;
   n.max_width = maxw;
   size_t off = 0;
   for (int l = 0; l < n_layers; ++l) {
     const int R = rows[l], K = cols[l], Rp = (R + 3) / 4 * 4;
     std::vector<float> w(size_t(R) * K), wt(size_t(K) * Rp, 0.0f), b(R);
+    std::vector<double> w64(packed + off, packed + off + w.size()), wt64(size_t(K) * Rp, 0.0),
+        b64(packed + off + w.size(), packed + off + w.size() + R);
     for (size_t i = 0; i < w.size(); ++i) w[i] = float(packed[off + i]);  // field.cpp:150
     off += w.size();
     for (int i = 0; i < R; ++i) b[i] = float(packed[off + i]);
     off += R;
     for (int i = 0; i < R; ++i)
-      for (int k = 0; k < K; ++k) wt[size_t(k) * Rp + i] = w[size_t(i) * K + k];
+      for (int k = 0; k < K; ++k) {
+        wt[size_t(k) * Rp + i] = w[size_t(i) * K + k];
+        wt64[size_t(k) * Rp + i] = w64[size_t(i) * K + k];
+      }
+    double *dw64, *dwt64, *db64;
+    NSDF_CUDA(cudaMalloc(&dw64, w64.size() * 8));
+    rec->allocs.push_back(dw64);
+    NSDF_CUDA(cudaMalloc(&dwt64, wt64.size() * 8));
+    rec->allocs.push_back(dwt64);
+    NSDF_CUDA(cudaMalloc(&db64, b64.size() * 8));
+    rec->allocs.push_back(db64);
+    NSDF_CUDA(cudaMemcpy(dw64, w64.data(), w64.size() * 8, cudaMemcpyHostToDevice));
+    NSDF_CUDA(cudaMemcpy(dwt64, wt64.data(), wt64.size() * 8, cudaMemcpyHostToDevice));
+    NSDF_CUDA(cudaMemcpy(db64, b64.data(), b64.size() * 8, cudaMemcpyHostToDevice));
+    n.w64[l] = dw64;
+    n.wt64[l] = dwt64;
+    n.b64[l] = db64;
     float *dw, *dwt, *db;
     NSDF_CUDA(cudaMalloc(&dw, w.size() * 4));
     rec->allocs.push_back(dw);
@@ -634,6 +653,34 @@ int nsdf_cuda_eval(nsdf_ctx* c, nsdf_field h, const float* points, int rows, int
 int nsdf_cuda_grad(nsdf_ctx* c, nsdf_field h, const float* points, int rows, int k, float time, float* grad) {
   if (!grad && k > 0) return fail(NSDF_ERR_CONTRACT, "grad is null");
   return nsdf_cuda_eval_grad(c, h, points, rows, k, time, nullptr, grad);
+}
+
+int nsdf_cuda_eval_f64(nsdf_ctx* c, nsdf_field h, const double* points, int rows, int k, double time, double* out,
+                       double* grad) {
+  if (!c) return fail(NSDF_ERR_CONTRACT, "context is null");
+  std::lock_guard<std::mutex> lk(c->mu);
+  DeviceGuard g(c->device);
+  FieldRec* f;
+  if (int st = find_field(c, h, &f)) return st;
+  if (f->dev.kind != kFieldMlp)
+    return fail(NSDF_ERR_CONFIG, "f64 device evaluation covers neural fields; analytic fields evaluate on the host");
+  if (int st = check_points(f, rows, k)) return st;
+  if (k == 0) return NSDF_OK;
+  if (!points) return fail(NSDF_ERR_CONTRACT, "points is null");
+  if (!out && !grad) return fail(NSDF_ERR_CONTRACT, "out and grad are both null");
+  size_t off = 0;
+  NSDF_CUDA(c->io.reserve(size_t(k) * (rows + 4) * 8 + 4096));
+  double* dp = carve<double>(c->io.base, off, size_t(rows) * k);
+  double* dout = carve<double>(c->io.base, off, size_t(k));
+  double* dgrad = carve<double>(c->io.base, off, size_t(3) * k);
+  cudaStream_t s = c->stream;
+  NSDF_CUDA(cudaMemcpyAsync(dp, points, size_t(rows) * k * 8, cudaMemcpyHostToDevice, s));
+  launch_eval_f64(f->dev.net, dp, rows, k, time, out ? dout : nullptr, grad ? dgrad : nullptr, s);
+  NSDF_CUDA(cudaGetLastError());
+  if (out) NSDF_CUDA(cudaMemcpyAsync(out, dout, size_t(k) * 8, cudaMemcpyDeviceToHost, s));
+  if (grad) NSDF_CUDA(cudaMemcpyAsync(grad, dgrad, size_t(3) * k * 8, cudaMemcpyDeviceToHost, s));
+  NSDF_CUDA(cudaStreamSynchronize(s));
+  return NSDF_OK;
 }
 
 int nsdf_cuda_generate_rays(nsdf_ctx* c, const nsdf_camera* camera, float* rays) {

@@ -38,6 +38,11 @@ struct DevNet {
   float wscale[kMaxLayers];  // hidden layer h is stored scaled by 1/wscale[h] (a power of 2)
   const float* bias_cat;   // biases of layers 0 .. L-2, [L-1][width]
   float bout;              // output bias
+  // FP64 master copy (the certification path, mlp_f64.cu): same layouts as w / wt / b.
+  double omega_d;
+  const double* w64[kMaxLayers];
+  const double* wt64[kMaxLayers];
+  const double* b64[kMaxLayers];
 };
 
 struct DevField {

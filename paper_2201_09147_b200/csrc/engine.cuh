@@ -137,6 +137,11 @@ void launch_shade(const float* pts, const float* normals, int k, const ShadePara
 void launch_raycast_mesh(const CamBasis& cb, const float* tri_verts /* n_tri x 9 */, int n_tri, float* positions,
                          uint8_t* mask, cudaStream_t s);
 
+// FP64 batch evaluation (mlp_f64.cu): forward_batch<double> / gradient_batch<double>
+// bit-exact with the reference's AVX2 double path.  pts rows x k (device), out k, grad 3 x k.
+void launch_eval_f64(const DevNet& n, const double* pts, int rows, int k, double time, double* out, double* grad,
+                     cudaStream_t s);
+
 // Tensor-core availability of a net for the fast mode (mlp_tc.cu).
 bool tc_supported(const DevNet& n);
 

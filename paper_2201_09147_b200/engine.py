@@ -114,6 +114,21 @@ class Context:
     def grad(self, handle, points, time=0.0):
         return self.eval_grad(handle, points, time, False, True)[1]
 
+    def eval_f64(self, handle: int, points, time: float = 0.0, want_value=True, want_grad=True):
+        """FP64 batch (forward_batch / gradient_batch<double>, the certification path),
+        bit-exact with the reference's double kernels."""
+        pts = np.ascontiguousarray(points, np.float64)
+        if pts.ndim != 2:
+            raise NsdfError(abi.ERR_CONTRACT, "points must be rows x k")
+        rows, k = pts.shape
+        out = np.zeros(k, np.float64) if want_value else None
+        grad = np.zeros((3, k), np.float64) if want_grad else None
+        dp = ctypes.POINTER(ctypes.c_double)
+        check(self.lib.nsdf_cuda_eval_f64(self._ctx, handle, pts.ctypes.data_as(dp), rows, k, ctypes.c_double(time),
+                                          out.ctypes.data_as(dp) if out is not None else None,
+                                          grad.ctypes.data_as(dp) if grad is not None else None))
+        return out, grad
+
     def eval_grad_device(self, handle, d_points, rows, k, time, d_out, d_grad):
         check(self.lib.nsdf_cuda_eval_grad_device(self._ctx, handle, ctypes.c_void_p(d_points), rows, k,
                                                   ctypes.c_float(time), ctypes.c_void_p(d_out),

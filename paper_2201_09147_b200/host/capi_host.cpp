@@ -42,6 +42,24 @@ tracer::TraceConfig trace_of(const nsdf_trace_config* t) {
   return cfg;
 }
 
+// "weights:<file.sdfnet>" -> NeuralField; anything else is an analytic spec ("torus:R=0.6,r=0.3").
+// A neural field takes `domain` when given (as the reference's certify flow does, fit.cpp).
+fields::FieldPtr field_of(const char* src, const Aabb* domain = nullptr) {
+  const std::string s(src);
+  if (s.rfind("weights:", 0) == 0) {
+    auto f = std::make_shared<fields::NeuralField>(mlp::load_params(s.substr(8)));
+    if (domain) f->set_domain(*domain);
+    return f;
+  }
+  return fields::make_analytic_field(fields::parse_field_spec(s));
+}
+
+void put_vec(const Vec3& v, double* out) {
+  out[0] = v.x;
+  out[1] = v.y;
+  out[2] = v.z;
+}
+
 shading::ShadeConfig shade_of(const nsdf_shade_config* s) {
   shading::ShadeConfig cfg;
   cfg.material.albedo = {s->albedo[0], s->albedo[1], s->albedo[2]};
@@ -111,6 +129,74 @@ int nsdf_host_forward_and_gradient(const char* sdfnet, const float* points, int 
     auto [d, g] = mlp::forward_and_gradient_batch(p, pts);
     std::memcpy(dist, d.data(), sizeof(float) * size_t(k));
     std::memcpy(grad, g.data(), sizeof(float) * size_t(3) * k);
+    return NSDF_OK;
+  } catch (const std::exception& e) {
+    return fail_from(e);
+  }
+}
+
+}  // extern "C"
+
+extern "C" {
+
+int nsdf_host_sample_near_surface(const char* field, uint64_t count, int gaussian, double amount, uint64_t seed,
+                                  double* out) {
+  try {
+    auto f = field_of(field);
+    Rng rng(seed);
+    fields::SurfaceNoise noise;
+    noise.kind = gaussian ? fields::SurfaceNoise::Kind::gaussian : fields::SurfaceNoise::Kind::uniform;
+    noise.amount = amount;
+    const auto pts = fields::sample_near_surface(*f, size_t(count), noise, rng);
+    for (size_t i = 0; i < pts.size(); ++i) put_vec(pts[i], out + 3 * i);
+    return NSDF_OK;
+  } catch (const std::exception& e) {
+    return fail_from(e);
+  }
+}
+
+int nsdf_host_sup_diff(const char* f_src, const char* g_src, uint64_t n_uniform, uint64_t n_surface, double margin,
+                       double noise_halfwidth, uint64_t seed, double* out) {
+  try {
+    auto g = field_of(g_src);
+    auto f = field_of(f_src, &g->domain());
+    fields::SupSamplerConfig cfg;
+    cfg.n_uniform = size_t(n_uniform);
+    cfg.n_surface = size_t(n_surface);
+    cfg.margin = margin;
+    cfg.noise_halfwidth = noise_halfwidth;
+    cfg.seed = seed;
+    const auto r = fields::estimate_sup_diff(*f, *g, cfg);
+    out[0] = r.eps;
+    out[1] = r.raw_max;
+    put_vec(r.argmax, out + 2);
+    out[5] = double(r.samples);
+    return NSDF_OK;
+  } catch (const std::exception& e) {
+    return fail_from(e);
+  }
+}
+
+int nsdf_host_verify_nesting(const char* manifest, double time, uint64_t samples, uint64_t seed,
+                             uint64_t max_recorded, uint64_t* counts, double* recorded) {
+  try {
+    const auto seq = sequence_of(manifest, time);
+    fields::VerifyConfig cfg;
+    cfg.samples = size_t(samples);
+    cfg.seed = seed;
+    cfg.max_recorded_violations = size_t(max_recorded);
+    const auto r = fields::verify_nesting(seq, cfg);
+    counts[0] = r.samples_total;
+    counts[1] = r.checked;
+    counts[2] = r.violation_count;
+    counts[3] = r.violations.size();
+    for (size_t i = 0; i < r.violations.size(); ++i) {
+      double* o = recorded + 6 * i;
+      put_vec(r.violations[i].point, o);
+      o[3] = double(r.violations[i].pair_index);
+      o[4] = r.violations[i].f_coarse;
+      o[5] = r.violations[i].f_fine;
+    }
     return NSDF_OK;
   } catch (const std::exception& e) {
     return fail_from(e);

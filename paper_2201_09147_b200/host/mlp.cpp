@@ -222,23 +222,61 @@ std::pair<Matrix<float>, Matrix<float>> forward_and_gradient_batch(const MlpPara
   return {std::move(d), std::move(g)};
 }
 
-// f64 evaluation serves certification and training in the reference — not the render path.
+// f64 evaluation (certification: nesting.cpp:131-361) runs on the device FP64 path
+// (mlp_f64.cu), bit-exact with the reference's double AVX2 kernels.
+namespace {
+
+void check_points_d(const Matrix<double>& pts, int rows) {
+  if (pts.rows() != rows)
+    throw Error(ErrorKind::contract,
+                "point batch is " + pts.shape_str() + " but " + std::to_string(rows) + " rows are required");
+}
+
+void eval_device_d(const MlpParams<double>& p, const Matrix<double>& pts, Matrix<double>* dist, Matrix<double>* grad) {
+  const int h = device_handle(p);
+  const int k = pts.cols();
+  if (dist) *dist = Matrix<double>(1, k);
+  if (grad) *grad = Matrix<double>(3, k);
+  engine::check(nsdf_cuda_eval_f64(engine::context(), h, pts.data(), pts.rows(), k, 0.0,
+                                   dist ? dist->data() : nullptr, grad ? grad->data() : nullptr));
+}
+
+}  // namespace
+
 template <>
-Matrix<double> forward_batch(const MlpParams<double>&, const Matrix<double>&) {
-  engine::unsupported("mlp::forward_batch<double>");
+Matrix<double> forward_batch(const MlpParams<double>& p, const Matrix<double>& points) {
+  if (p.layers.empty()) throw Error(ErrorKind::contract, "network has no layers");
+  check_points_d(points, p.input_dim);
+  Matrix<double> d;
+  eval_device_d(p, points, &d, nullptr);
+  return d;
 }
 template <>
-Matrix<double> gradient_batch(const MlpParams<double>&, const Matrix<double>&) {
-  engine::unsupported("mlp::gradient_batch<double>");
+Matrix<double> gradient_batch(const MlpParams<double>& p, const Matrix<double>& points) {
+  if (p.input_dim != 3)
+    throw Error(ErrorKind::contract,
+                "gradient_batch expects a 3-input network; use spatial_gradient_batch for time-extended networks");
+  check_points_d(points, 3);
+  Matrix<double> g;
+  eval_device_d(p, points, nullptr, &g);
+  return g;
 }
 template <>
-Matrix<double> spatial_gradient_batch(const MlpParams<double>&, const Matrix<double>&) {
-  engine::unsupported("mlp::spatial_gradient_batch<double>");
+Matrix<double> spatial_gradient_batch(const MlpParams<double>& p, const Matrix<double>& points) {
+  if (p.input_dim != 4) throw Error(ErrorKind::contract, "spatial_gradient_batch expects a 4-input network");
+  check_points_d(points, 4);
+  Matrix<double> g;
+  eval_device_d(p, points, nullptr, &g);
+  return g;
 }
 template <>
-std::pair<Matrix<double>, Matrix<double>> forward_and_gradient_batch(const MlpParams<double>&,
-                                                                      const Matrix<double>&) {
-  engine::unsupported("mlp::forward_and_gradient_batch<double>");
+std::pair<Matrix<double>, Matrix<double>> forward_and_gradient_batch(const MlpParams<double>& p,
+                                                                      const Matrix<double>& points) {
+  if (p.input_dim != 3) throw Error(ErrorKind::contract, "forward_and_gradient_batch expects a 3-input network");
+  check_points_d(points, 3);
+  Matrix<double> d, g;
+  eval_device_d(p, points, &d, &g);
+  return {std::move(d), std::move(g)};
 }
 
 // ---- .sdfnet: {activation, omega0, input_dim, layers[{rows, cols, weights_flat, bias}]} ----
