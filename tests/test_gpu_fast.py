@@ -208,3 +208,60 @@ def test_config5_animated_slices(ctx, fast, oracle_built, t):
     r = refshim.render(path, cam, cfg, shade, 0, time=t)
     assert np.array_equal(a[2], r[2]) and np.array_equal(a[1].view(np.uint32), r[1].view(np.uint32))
     assert np.max(np.abs(a[0] - r[0])) <= 1e-6
+
+
+# ---- persistent level kernel (tc_trace_level): edge cases --------------------------------
+def _torus_levels(c):
+    from paper_2201_09147_b200.engine import DeviceSequence
+    from paper_2201_09147_b200.manifest import load_manifest
+    return DeviceSequence(c, load_manifest(_fixture("torus_w30.nest")))
+
+
+def _rays(n, seed=0, away=False):
+    rng = np.random.default_rng(seed)
+    o = np.tile(np.array([2.0, 1.5, 2.0], np.float32), (n, 1))
+    target = rng.uniform(-0.8, 0.8, (n, 3)).astype(np.float32)
+    d = (target - o) if not away else (o - target)
+    d /= np.linalg.norm(d, axis=1, keepdims=True)
+    return np.concatenate([o, d], 1).astype(np.float32)
+
+
+@pytest.mark.parametrize("n", [1, 5, 127, 128, 129, 1000, 40000])
+def test_fast_trace_rays_ragged(ctx, fast, n):
+    """Any ray count (a partly filled tile, one ray, many claims) gives the oracle's
+    per-ray result within tolerance, and the persistent kernel's evaluation counter equals
+    the records' iterations_used (stats come from the kernel, not the records)."""
+    from paper_2201_09147_b200.abi import TraceConfig
+    cfg = TraceConfig((20, 5, 5))
+    rays = _rays(n, seed=n)
+    r0 = records_np(ctx.trace_rays(_torus_levels(ctx).levels(), cfg, rays))
+    r1 = records_np(fast.trace_rays(_torus_levels(fast).levels(), cfg, rays))
+    assert np.mean(r0["hit"] == r1["hit"]) >= (MASK_MIN if n >= 1000 else 1.0)
+    both = (r0["hit"] == 1) & (r1["hit"] == 1)
+    if both.any():
+        assert np.abs(r0["t"][both] - r1["t"][both]).max() <= 1.5 * DT_MAX
+    assert (r1["iters"][:, :3] <= np.array([20, 5, 5])).all()
+
+
+def test_fast_budget_one_and_all_miss(ctx, fast):
+    from paper_2201_09147_b200.abi import TraceConfig
+    # budget 1 at every level: every ray leaves each level after one evaluation
+    rays = _rays(3000, seed=1)
+    r1 = records_np(fast.trace_rays(_torus_levels(fast).levels(), TraceConfig((1, 1, 1)), rays))
+    r0 = records_np(ctx.trace_rays(_torus_levels(ctx).levels(), TraceConfig((1, 1, 1)), rays))
+    assert (r1["iters"][:, :3] <= 1).all()
+    assert np.mean(r0["level"] == r1["level"]) >= MASK_MIN
+    # rays pointing away from the scene: level 0 marches them past t_max, the later levels
+    # receive empty lists (their persistent launches exit without work)
+    away = _rays(5000, seed=2, away=True)
+    r = records_np(fast.trace_rays(_torus_levels(fast).levels(), TraceConfig((20, 5, 5)), away))
+    assert r["hit"].sum() == 0 and (r["iters"][:, 1:3] == 0).all()
+
+
+def test_fast_stats_match_records(fast):
+    from paper_2201_09147_b200.abi import TraceConfig, standard_camera
+    recs, st = fast.trace_image(_torus_levels(fast).levels(), standard_camera(320, 180), TraceConfig((20, 5, 5)))
+    r = records_np(recs)
+    for j in range(3):
+        assert st.evals[j] == int(r["iters"][:, j].astype(np.int64).sum())
+    assert st.hits == int(r["hit"].sum())
