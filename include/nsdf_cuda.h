@@ -27,6 +27,9 @@
  *   nsdf_cuda_render          shading::render                           src/shading/render.cpp:12-82
  *   nsdf_cuda_render_device   shading::render, device-resident framebuffer + tile sharding
  *                             (the multi-GPU frame/tile scheduler's per-rank call)
+ *   nsdf_cuda_render_multi    shading::render over N contexts (N GPUs) from one process:
+ *                             interleaved tiles per context, gathered into a host framebuffer
+ *                             (SURVEY.md §8b "nsdf_cuda_render_multi(ctxs[], n, ...)")
  *
  * Conventions
  *   - Plain C types only; no exceptions cross this boundary.  Every function returns an
@@ -248,6 +251,17 @@ int nsdf_cuda_render(nsdf_ctx* ctx, const nsdf_level* levels, int m, const nsdf_
  * tile order; tile_world = 1 renders everything) into full-frame device buffers.  Pixels
  * of other tiles are left untouched.  Asynchronous on the context stream; `stats` (host,
  * may be NULL) forces a synchronize. */
+/* Single-process multi-GPU render: context i (its own device and stream) renders the image
+ * tiles t % n == i (tile_size x tile_size, row-major tile order) with its own field handles
+ * levels[i][0..m); the owned pixels are packed on each device, copied to the host and
+ * scattered into the caller's HOST framebuffer (synchronous).  The contexts render
+ * concurrently; the image equals nsdf_cuda_render's for any n (per-ray work does not depend
+ * on the partition).  stats (optional) sums the contexts' counters. */
+int nsdf_cuda_render_multi(nsdf_ctx* const* ctxs, int n, const nsdf_level* const* levels, int m,
+                           const nsdf_camera* camera, const nsdf_trace_config* trace,
+                           const nsdf_shade_config* shade, int normal_source, int fine_index,
+                           int tile_size, float* rgb, float* depth, uint8_t* mask,
+                           nsdf_frame_stats* stats);
 int nsdf_cuda_render_device(nsdf_ctx* ctx, const nsdf_level* levels, int m,
                             const nsdf_camera* camera, const nsdf_trace_config* trace,
                             const nsdf_shade_config* shade, int normal_source, int fine_index,

@@ -228,6 +228,12 @@ struct FrameOut {
   float* d_rgb = nullptr;                // render
   float* d_depth = nullptr;
   uint8_t* d_mask = nullptr;
+  // render_multi: the slots' pixels packed in slot order (+ pixel index, + slot count)
+  float* d_pack_rgb = nullptr;
+  float* d_pack_depth = nullptr;
+  uint8_t* d_pack_mask = nullptr;
+  int* d_pack_pixel = nullptr;
+  int* d_pack_count = nullptr;
 };
 
 int run_frame(nsdf_ctx* c, const nsdf_level* levels, int m, const nsdf_trace_config* cfg, const CamBasis* cam,
@@ -296,6 +302,12 @@ int run_frame(nsdf_ctx* c, const nsdf_level* levels, int m, const nsdf_trace_con
       prof->end(Profiler::kNormals, ev_n, s);
       prof->acc.normal_launches += defer ? 2 : 1;
     }
+  }
+  if (out.d_pack_rgb) {
+    launch_pack_owned(fb.st, n_slots, n_max, out.d_rgb, out.d_depth, out.d_mask, out.d_pack_rgb, out.d_pack_depth,
+                      out.d_pack_mask, out.d_pack_pixel, s);
+    NSDF_CUDA(cudaMemcpyAsync(out.d_pack_count, n_slots, 4, cudaMemcpyDeviceToDevice, s));
+    launches++;
   }
   if (prof) prof->end(Profiler::kFrame, ev_frame, s);
   NSDF_CUDA(cudaGetLastError());
@@ -913,6 +925,103 @@ int nsdf_cuda_render_device(nsdf_ctx* c, const nsdf_level* levels, int m, const 
   fo.d_mask = d_mask;
   return run_frame(c, levels, m, trace, &cb, nullptr, 0, &sp, normal_source, fine_index, tile_size, tile_rank,
                    tile_world, fo, stats);
+}
+
+int nsdf_cuda_render_multi(nsdf_ctx* const* ctxs, int n, const nsdf_level* const* levels, int m,
+                           const nsdf_camera* camera, const nsdf_trace_config* trace, const nsdf_shade_config* shade,
+                           int normal_source, int fine_index, int tile_size, float* rgb, float* depth, uint8_t* mask,
+                           nsdf_frame_stats* stats) {
+  if (!ctxs || !levels || n < 1 || !rgb || !depth || !mask) return fail(NSDF_ERR_CONTRACT, "null argument");
+  if (tile_size < 1) return fail(NSDF_ERR_CONFIG, "tile size must be positive");
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < i; ++j)
+      if (!ctxs[i] || ctxs[i] == ctxs[j]) return fail(NSDF_ERR_CONTRACT, "render_multi needs n distinct contexts");
+  // lock in pointer order (deadlock-free against concurrent multi-context callers)
+  std::vector<nsdf_ctx*> order(ctxs, ctxs + n);
+  std::sort(order.begin(), order.end());
+  std::vector<std::unique_lock<std::mutex>> locks;
+  for (nsdf_ctx* c : order) locks.emplace_back(c->mu);
+  if (stats) std::memset(stats, 0, sizeof(*stats));
+  struct Part {
+    size_t n_max;
+    int* count;     // host pinned
+    float* h_rgb;   // host pinned staging, slot order
+    float* h_depth;
+    uint8_t* h_mask;
+    int* h_pixel;
+  };
+  std::vector<Part> parts(n);
+  // 1) every context renders its tiles (t % n == i) on its own device and stream, packs
+  //    the owned pixels and starts their D2H: the devices run concurrently
+  for (int i = 0; i < n; ++i) {
+    nsdf_ctx* c = ctxs[i];
+    DeviceGuard g(c->device);
+    CamBasis cb;
+    ShadeParams sp;
+    if (int st = render_checks(c, levels[i], m, camera, trace, shade, normal_source, fine_index, &cb, &sp)) return st;
+    const size_t np = size_t(cb.width) * cb.height;
+    const int tx = (cb.width + tile_size - 1) / tile_size, ty = (cb.height + tile_size - 1) / tile_size;
+    size_t owned = 0;
+    for (int t = i; t < tx * ty; t += n) {
+      const int x0 = (t % tx) * tile_size, y0 = (t / tx) * tile_size;
+      owned += size_t(std::min(tile_size, cb.width - x0)) * size_t(std::min(tile_size, cb.height - y0));
+    }
+    owned = std::max<size_t>(owned, 1);
+    size_t off = 0;
+    NSDF_CUDA(c->io.reserve(np * 17 + owned * 21 + 16384));
+    FrameOut fo;
+    fo.d_rgb = carve<float>(c->io.base, off, 3 * np);
+    fo.d_depth = carve<float>(c->io.base, off, np);
+    fo.d_mask = carve<uint8_t>(c->io.base, off, np);
+    fo.d_pack_rgb = carve<float>(c->io.base, off, 3 * owned);
+    fo.d_pack_depth = carve<float>(c->io.base, off, owned);
+    fo.d_pack_pixel = carve<int>(c->io.base, off, owned);
+    fo.d_pack_count = carve<int>(c->io.base, off, 1);
+    fo.d_pack_mask = carve<uint8_t>(c->io.base, off, owned);
+    nsdf_frame_stats fs;
+    if (int st = run_frame(c, levels[i], m, trace, &cb, nullptr, 0, &sp, normal_source, fine_index, tile_size, i, n,
+                           fo, stats ? &fs : nullptr))
+      return st;
+    if (stats) {
+      for (int l = 0; l < NSDF_MAX_LEVELS; ++l) stats->evals[l] += fs.evals[l];
+      stats->hits += fs.hits;
+      stats->normal_evals += fs.normal_evals;
+      stats->fallback_evals += fs.fallback_evals;
+      stats->kernel_launches += fs.kernel_launches;
+    }
+    NSDF_CUDA(c->frame.reserve_host(owned * 21 + 64));
+    uint8_t* h = static_cast<uint8_t*>(c->frame.host_pinned);
+    Part& p = parts[i];
+    p.n_max = owned;
+    p.count = reinterpret_cast<int*>(h);
+    p.h_rgb = reinterpret_cast<float*>(h + 16);
+    p.h_depth = p.h_rgb + 3 * owned;
+    p.h_pixel = reinterpret_cast<int*>(p.h_depth + owned);
+    p.h_mask = reinterpret_cast<uint8_t*>(p.h_pixel + owned);
+    cudaStream_t s = c->stream;
+    NSDF_CUDA(cudaMemcpyAsync(p.count, fo.d_pack_count, 4, cudaMemcpyDeviceToHost, s));
+    NSDF_CUDA(cudaMemcpyAsync(p.h_rgb, fo.d_pack_rgb, 3 * owned * 4, cudaMemcpyDeviceToHost, s));
+    NSDF_CUDA(cudaMemcpyAsync(p.h_depth, fo.d_pack_depth, owned * 4, cudaMemcpyDeviceToHost, s));
+    NSDF_CUDA(cudaMemcpyAsync(p.h_pixel, fo.d_pack_pixel, owned * 4, cudaMemcpyDeviceToHost, s));
+    NSDF_CUDA(cudaMemcpyAsync(p.h_mask, fo.d_pack_mask, owned, cudaMemcpyDeviceToHost, s));
+  }
+  // 2) gather: scatter every context's packed pixels into the caller's framebuffer
+  for (int i = 0; i < n; ++i) {
+    nsdf_ctx* c = ctxs[i];
+    DeviceGuard g(c->device);
+    NSDF_CUDA(cudaStreamSynchronize(c->stream));
+    const Part& p = parts[i];
+    const int cnt = std::min<int>(*p.count, int(p.n_max));
+    for (int k = 0; k < cnt; ++k) {
+      const size_t px = size_t(p.h_pixel[k]);
+      rgb[3 * px + 0] = p.h_rgb[3 * size_t(k) + 0];
+      rgb[3 * px + 1] = p.h_rgb[3 * size_t(k) + 1];
+      rgb[3 * px + 2] = p.h_rgb[3 * size_t(k) + 2];
+      depth[px] = p.h_depth[k];
+      mask[px] = p.h_mask[k];
+    }
+  }
+  return NSDF_OK;
 }
 
 int nsdf_cuda_render(nsdf_ctx* c, const nsdf_level* levels, int m, const nsdf_camera* camera,

@@ -451,6 +451,27 @@ __global__ void fb_background_kernel(RayState st, const int* n_slots, ShadeParam
   }
 }
 
+__global__ void pack_owned_kernel(RayState st, const int* n_slots, const float* rgb, const float* depth,
+                                  const uint8_t* mask, float* p_rgb, float* p_depth, uint8_t* p_mask, int* p_pixel) {
+  const int n = *n_slots;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const int p = st.pixel[i];
+    p_rgb[size_t(3) * i + 0] = rgb[size_t(3) * p + 0];
+    p_rgb[size_t(3) * i + 1] = rgb[size_t(3) * p + 1];
+    p_rgb[size_t(3) * i + 2] = rgb[size_t(3) * p + 2];
+    p_depth[i] = depth[p];
+    p_mask[i] = mask[p];
+    p_pixel[i] = p;
+  }
+}
+
+void launch_pack_owned(const RayState& st, const int* n_slots_dev, int n_max, const float* rgb, const float* depth,
+                       const uint8_t* mask, float* p_rgb, float* p_depth, uint8_t* p_mask, int* p_pixel,
+                       cudaStream_t s) {
+  pack_owned_kernel<<<std::max(1, std::min((n_max + 255) / 256, num_sms() * 8)), 256, 0, s>>>(
+      st, n_slots_dev, rgb, depth, mask, p_rgb, p_depth, p_mask, p_pixel);
+}
+
 void launch_fb_background(const RayState& st, const int* n_slots_dev, int n_max, const ShadeParams& sp, float* rgb,
                           float* depth, uint8_t* mask, cudaStream_t s) {
   fb_background_kernel<<<std::max(1, std::min((n_max + 255) / 256, num_sms() * 8)), 256, 0, s>>>(st, n_slots_dev, sp,

@@ -113,6 +113,12 @@ void launch_write_records(const RayState& st, int n, nsdf_hit_record* out, cudaS
 void launch_mark_hits(const int* list, const int* count, int n_max, RayState st, cudaStream_t s);
 
 // Framebuffer background for the slots' pixels (render.cpp:28-33).
+// Pack the framebuffer pixels of the frame's slots (the owned tiles of a sharded frame) into
+// slot order: rgb 3 x n, depth, mask and the pixel index of every slot.
+void launch_pack_owned(const RayState& st, const int* n_slots_dev, int n_max, const float* rgb, const float* depth,
+                       const uint8_t* mask, float* p_rgb, float* p_depth, uint8_t* p_mask, int* p_pixel,
+                       cudaStream_t s);
+
 void launch_fb_background(const RayState& st, const int* n_slots_dev, int n_max,
                           const ShadeParams& sp, float* rgb, float* depth, uint8_t* mask,
                           cudaStream_t s);

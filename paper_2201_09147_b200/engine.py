@@ -222,6 +222,31 @@ class Context:
         return st
 
 
+def render_multi(contexts, level_lists, cam: Camera, trace: TraceConfig, shade: ShadeConfig, normal_source=0,
+                 fine_index=-1, tile_size=32, stats: bool = False):
+    """nsdf_cuda_render_multi: one frame over N contexts (N GPUs) from one process —
+    context i renders the tiles t % N == i with its own field handles (level_lists[i]);
+    returns the gathered host framebuffer (rgb, depth, mask[, FrameStats])."""
+    n_ctx = len(contexts)
+    if n_ctx < 1 or len(level_lists) != n_ctx:
+        raise NsdfError(abi.ERR_CONTRACT, "one level list per context is required")
+    lib = contexts[0].lib
+    n = cam.width * cam.height
+    rgb = np.zeros(3 * n, np.float32)
+    depth = np.zeros(n, np.float32)
+    mask = np.zeros(n, np.uint8)
+    arrays = [_levels(lv) for lv in level_lists]
+    m = arrays[0][1]
+    ctxs = (ctypes.c_void_p * n_ctx)(*[c._ctx.value for c in contexts])
+    lvp = (ctypes.POINTER(Level) * n_ctx)(*[ctypes.cast(a, ctypes.POINTER(Level)) for a, _ in arrays])
+    st = FrameStats() if stats else None
+    check(lib.nsdf_cuda_render_multi(ctxs, n_ctx, lvp, m, ctypes.byref(cam), ctypes.byref(trace), ctypes.byref(shade),
+                                     normal_source, fine_index, tile_size, _fp(rgb), _fp(depth),
+                                     mask.ctypes.data_as(_U8), ctypes.byref(st) if st else None))
+    out = rgb.reshape(cam.height, cam.width, 3), depth.reshape(cam.height, cam.width), mask.reshape(cam.height, cam.width)
+    return (*out, st) if stats else out
+
+
 def _levels(levels):
     arr = (Level * len(levels))()
     for i, lv in enumerate(levels):

@@ -8,6 +8,11 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 if ROOT not in sys.path:
     sys.path.insert(0, ROOT)
 
+# The drop-in library (libnsdf_b200.so) creates ONE process-wide engine context on first
+# use, with the arithmetic mode from NSDF_MODE; the bit-exact drop-in tests need the oracle
+# mode whichever test loads the library first.
+os.environ.setdefault("NSDF_MODE", "oracle")
+
 ASSETS = os.path.join(ROOT, "assets")
 GOLDEN = os.path.join(ROOT, "tests", "golden")
 

@@ -95,7 +95,9 @@ TEST_CASE("validation and contract errors") {
   CHECK_THROWS(mlp::forward_batch(p, Matrix<float>(2, 1)));
   CHECK_THROWS(mlp::parse_architecture("64"));
   CHECK(mlp::parse_architecture("256x3").parameter_count() == 198657u);
-  CHECK_THROWS(mlp::forward_batch(linear({1, 0, 0}, 0), Matrix<double>(3, 1)));  // f64: not the render path
+  // f64 batches run on the device FP64 path (certification): a linear net is exact
+  CHECK(mlp::forward_batch(linear({1, 0, 0}, 0), Matrix<double>(3, 1, {2.0, 0.0, 0.0}))(0, 0) == 2.0);
+  CHECK_THROWS(mlp::forward_batch(linear({1, 0, 0}, 0), Matrix<double>(2, 1)));
 }
 
 TEST_CASE("classic sphere tracing hits the surface and the offset surface (test_tracer.cpp:74-87)") {
