@@ -563,9 +563,18 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
         mbar_wait(&full[0], 0, 0);
       }
       uint32_t chunk_iter = 0, kr_phase = 0, a0_phase = 0;
+      // debug timeline (NSDF_TC_TIMELINE): cycles the issuer waits for A0, A blocks, weights
+      const bool mdbg = a.dbg && blockIdx.x == 0;
+      long long w_a0 = 0, w_k = 0, w_full = 0, t_loop = 0;
+      auto timed_wait = [&](uint64_t* bar, uint32_t ph, long long& acc) {
+        const long long c0 = mdbg ? clock64() : 0;
+        mbar_wait(bar, ph, a.suspend_ns);
+        if (mdbg) acc += clock64() - c0;
+      };
       for (int t = 0; more_tiles(t); ++t) {
+        const long long tl0 = mdbg ? clock64() : 0;
         // ---- layer 0: D0 = A0 . B0^T, K = 32 (the split lives in K: one term) ----
-        mbar_wait(a0ready, a0_phase, a.suspend_ns);
+        timed_wait(a0ready, a0_phase, w_a0);
         a0_phase ^= 1;
         tc_fence_after();
 #pragma unroll
@@ -583,7 +592,7 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
 #pragma unroll 1
           for (int blk = 0; blk < W / kBlk; ++blk) {
             if (blk % kGroups == 0) {  // block row of the A operand written by every group
-              mbar_wait(&kready[blk / kGroups], kr_phase, a.suspend_ns);
+              timed_wait(&kready[blk / kGroups], kr_phase, w_k);
               tc_fence_after();
             }
             const int c = blk >> 1, ks = blk & 1;  // 32-K weight chunk, K=16 step inside it
@@ -594,7 +603,7 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
                 b_base = smem_addr(sm.wst + size_t(h) * 2 * W * W + size_t(c) * W * kKC);
                 lo_off = uint32_t(W) * W * 2;
               } else {
-                mbar_wait(&full[s], (chunk_iter / kStages) & 1, a.suspend_ns);
+                timed_wait(&full[s], (chunk_iter / kStages) & 1, w_full);
                 tc_fence_after();
                 b_base = smem_addr(sm.wst + size_t(s) * kStageHalves);
                 lo_off = uint32_t(W) * kKC * 2;
@@ -617,6 +626,14 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
           }
           kr_phase ^= 1;
           tc_commit(dfull);  // accumulator complete
+        }
+        if (mdbg && t < 64) {
+          t_loop = clock64() - tl0;
+          a.dbg[65 * 16 + t * 4 + 0] = w_a0;
+          a.dbg[65 * 16 + t * 4 + 1] = w_k;
+          a.dbg[65 * 16 + t * 4 + 2] = w_full;
+          a.dbg[65 * 16 + t * 4 + 3] = t_loop;
+          w_a0 = w_k = w_full = 0;
         }
       }
     }
@@ -1034,7 +1051,7 @@ bool launch_terms(TcArgs& a, int n_max_items, cudaStream_t s) {
 long long* timeline_buffer() {
   static long long* buf = nullptr;
   if (!getenv("NSDF_TC_TIMELINE")) return nullptr;
-  if (!buf) cudaMallocManaged(&buf, 65 * 16 * sizeof(long long));
+  if (!buf) cudaMallocManaged(&buf, (65 * 16 + 64 * 4) * sizeof(long long));
   return buf;
 }
 void timeline_dump(long long* buf, const char* what) {
@@ -1053,7 +1070,12 @@ void timeline_dump(long long* buf, const char* what) {
     fprintf(stderr, " | %6lld %6lld %6lld || %6lld %6lld %6lld\n", d(nx, 11), d(nx, 12), d(nx, 13), d(nx, 14),
             d(nx, 15), nx[0] ? nx[0] - r[0] : -1);
   }
-  cudaMemset(buf, 0, 65 * 16 * sizeof(long long));
+  for (int t = 0; t < 12; ++t) {
+    const long long* q = buf + 65 * 16 + t * 4;
+    fprintf(stderr, "  MMA issuer tile %2d: waits A0 %6lld, A blocks %6lld, weights %6lld of %6lld cycles\n", t, q[0],
+            q[1], q[2], q[3]);
+  }
+  cudaMemset(buf, 0, (65 * 16 + 64 * 4) * sizeof(long long));
 }
 
 uint32_t suspend_hint() {

@@ -1,8 +1,10 @@
 """Per-tile timeline of CTA 0 of every tcgen05 launch of one config-2 frame (NSDF_TC_TIMELINE).
 
     NSDF_TC_TIMELINE=1 python tools/timeline.py [width height]
-Columns (SM cycles from the tile's start): A0 arrive | dfull0 | ep0 end | dfull1 | ep1 end |
-A0 before fence | (trace) vote done (before the tile's start mark of the NEXT tile) | next tile.
+Columns (SM cycles from the tile's start): A0 before its fence, A0 arrive | per MMA layer: the
+accumulator-complete wait returning, the epilogue's end | (trace) return, update, flush ||
+refill done, vote done, next tile's start.  Then, per tile, the MMA issuer's waits for A0,
+for A block rows (kready) and for streamed weights, and its whole tile loop.
 """
 import os
 import sys
