@@ -1,0 +1,144 @@
+"""Parity at BASELINE.json's full sizes: the engine against the reference's own
+renderer (oracle/_ref, all host cores) on the named configurations.
+
+  - oracle mode (FP32 FFMA tiles): bit-identical framebuffers (mask, depth bits; rgb within
+    1e-6 from pow) at 1920x1080 for config 2 (both budget settings) and 512x512 config 1;
+  - fast mode (split-fp16 tcgen05): mask agreement >= 99.9%, |dt| p99.9 <= 1e-3 on common
+    hits, and the normals (through the shading) within 0.5 degrees, end to end.
+A CPU reference frame takes ~1-2 s on the box's 16 cores."""
+import os
+
+import numpy as np
+import pytest
+
+from conftest import ASSETS
+
+pytestmark = pytest.mark.gpu
+
+MASK_MIN = 0.999
+DT_MAX = 1e-3
+
+
+def _manifest():
+    p = os.path.join(ASSETS, "torus_w30.nest")
+    if not os.path.exists(p):
+        pytest.skip("fixture missing")
+    return p
+
+
+@pytest.fixture(scope="module")
+def ref(oracle_built):
+    from oracle import refshim
+    refshim.set_backend("avx2")
+    return refshim
+
+
+def _render(mode, path, cam, cfg, shade, members=None):
+    from paper_2201_09147_b200.engine import Context, DeviceSequence
+    from paper_2201_09147_b200.manifest import load_manifest
+    seq = load_manifest(path)
+    if members is not None:
+        seq = seq.subsequence(members)
+    c = Context(0, mode)
+    try:
+        return c.render(DeviceSequence(c, seq).levels(), cam, cfg, shade)
+    finally:
+        c.close()
+
+
+@pytest.mark.parametrize("budgets", [(20, 5, 5), (40, 20, 20)])
+def test_config2_1080p(ref, budgets):
+    from paper_2201_09147_b200.abi import ShadeConfig, TraceConfig, standard_camera
+    path = _manifest()
+    cam = standard_camera(1920, 1080)
+    cfg = TraceConfig(budgets)
+    shade = ShadeConfig(specular=0.3)
+    rr, rd, rm, _ = ref.render(path, cam, cfg, shade)
+    o = _render("fp32", path, cam, cfg, shade)
+    assert np.array_equal(o[2], rm)
+    assert np.array_equal(o[1].view(np.uint32), rd.view(np.uint32))
+    assert np.max(np.abs(o[0] - rr)) <= 1e-6
+    f = _render("fp16", path, cam, cfg, shade)
+    assert np.mean(f[2] == rm) >= MASK_MIN
+    both = (f[2] == 1) & (rm == 1)
+    assert np.percentile(np.abs(f[1] - rd)[both], 99.9) <= DT_MAX
+    assert np.percentile(np.abs(f[0] - rr)[both], 99.9) <= 1e-2
+
+
+def test_config1_512(ref):
+    import json
+    import tempfile
+    from paper_2201_09147_b200.abi import ShadeConfig, TraceConfig, standard_camera
+    path = _manifest()
+    j = json.load(open(path))
+    j["fields"] = [dict(j["fields"][2], weights=os.path.join(ASSETS, j["fields"][2]["weights"]))]
+    j["deltas"] = [j["deltas"][2]]
+    with tempfile.NamedTemporaryFile("w", suffix=".nest", delete=False) as fh:
+        json.dump(j, fh)
+    try:
+        cam = standard_camera(512, 512)
+        cfg = TraceConfig((40,))
+        shade = ShadeConfig(specular=0.3)
+        rr, rd, rm, _ = ref.render(fh.name, cam, cfg, shade)
+        o = _render("fp32", fh.name, cam, cfg, shade)
+        f = _render("fp16", fh.name, cam, cfg, shade)
+    finally:
+        os.unlink(fh.name)
+    assert np.array_equal(o[2], rm) and np.array_equal(o[1].view(np.uint32), rd.view(np.uint32))
+    assert np.mean(f[2] == rm) >= MASK_MIN
+    both = (f[2] == 1) & (rm == 1)
+    assert np.percentile(np.abs(f[1] - rd)[both], 99.9) <= DT_MAX
+
+
+def test_config3_mapped_normals_1080p(ref):
+    """Neural normal mapping: 64x1 traced with budgets (40, 0), normals from the 256x3."""
+    from paper_2201_09147_b200.abi import ShadeConfig, TraceConfig, standard_camera
+    from paper_2201_09147_b200.engine import Context, DeviceSequence
+    from paper_2201_09147_b200.manifest import load_manifest
+    path = _manifest()
+    cam = standard_camera(1920, 1080)
+    cfg = TraceConfig((40, 0, 0))
+    shade = ShadeConfig(specular=0.3)
+    rr, rd, rm, _ = ref.render(path, cam, cfg, shade, 1)
+    seq = load_manifest(path)
+    out = {}
+    for mode in ("fp32", "fp16"):
+        c = Context(0, mode)
+        try:
+            out[mode] = c.render(DeviceSequence(c, seq).levels(), cam, cfg, shade, 1)
+        finally:
+            c.close()
+    o, f = out["fp32"], out["fp16"]
+    assert np.array_equal(o[2], rm) and np.array_equal(o[1].view(np.uint32), rd.view(np.uint32))
+    assert np.max(np.abs(o[0] - rr)) <= 1e-6
+    assert np.mean(f[2] == rm) >= MASK_MIN
+    both = (f[2] == 1) & (rm == 1)
+    assert np.percentile(np.abs(f[1] - rd)[both], 99.9) <= DT_MAX
+
+
+def test_config5_4k_slice(ref):
+    """One slice of the animated 4-D sequence at 3840x2160 (t = 60/119)."""
+    from paper_2201_09147_b200.abi import ShadeConfig, TraceConfig, standard_camera
+    from paper_2201_09147_b200.engine import Context, DeviceSequence
+    from paper_2201_09147_b200.manifest import load_manifest
+    path = os.path.join(ASSETS, "blend4d_w30.nest")
+    if not os.path.exists(path):
+        pytest.skip("fixture missing")
+    t = 60 / 119
+    cam = standard_camera(3840, 2160)
+    cfg = TraceConfig((20, 10))
+    shade = ShadeConfig(specular=0.3)
+    rr, rd, rm, _ = ref.render(path, cam, cfg, shade, 0, time=t)
+    seq = load_manifest(path)
+    out = {}
+    for mode in ("fp32", "fp16"):
+        c = Context(0, mode)
+        try:
+            out[mode] = c.render(DeviceSequence(c, seq).levels(time=t), cam, cfg, shade)
+        finally:
+            c.close()
+    o, f = out["fp32"], out["fp16"]
+    assert np.array_equal(o[2], rm) and np.array_equal(o[1].view(np.uint32), rd.view(np.uint32))
+    assert np.mean(f[2] == rm) >= MASK_MIN
+    both = (f[2] == 1) & (rm == 1)
+    assert np.percentile(np.abs(f[1] - rd)[both], 99.9) <= DT_MAX
