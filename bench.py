@@ -77,6 +77,7 @@ def parse():
                     help="frames in flight (engine contexts on their own streams); 1 = strictly serial frames")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-alt", action="store_true", help="skip the (40,20,20) parity-setting line of config 2")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     args.width = args.width or cfg["res"][0]
@@ -431,6 +432,7 @@ def main():
         n_fb = max(len(lanes), 2 if gather is not None else 1)
         fbs = [(rgb, depth, mask)] + [(torch.zeros_like(rgb), torch.zeros_like(depth), torch.zeros_like(mask))
                                       for _ in range(n_fb - 1)]
+        W["fbs"] = fbs
         gstream = torch.cuda.Stream() if gather is not None else None
         free_ev = [None] * n_fb
         W["gstream"] = gstream
@@ -549,6 +551,38 @@ def main():
                  "profiled_frame_ms": prof.frame_ms / max(prof.frames, 1), "profile": prof_kind,
                  "level_ms": [prof.level_ms[j] / max(prof.frames, 1) for j in range(len(seq.members))]}
 
+    # config 2 is reported at the speed setting (20,5,5) — the headline — and
+    # at the generous parity setting (40,20,20), same frames-in-flight harness, device buffers.
+    alt = None
+    if args.config == 2 and world == 1 and args.budgets == "20,5,5" and not args.no_alt:
+        cfg_alt = TraceConfig((40, 20, 20))
+        lanes = W.get("lanes") or [(ctx, stream, ds)]
+        lv_alt = [d.levels() for _, _, d in lanes]
+        n_alt = max(6, min(steps, 30))
+
+        def alt_frame(i):
+            c, st_, _ = lanes[i % len(lanes)]
+            fr, fd, fm = W["fbs"][i % len(W["fbs"])]
+            c.render_device(lv_alt[i % len(lanes)], W["cam"], cfg_alt, W["shade"], fr.data_ptr(), fd.data_ptr(),
+                            fm.data_ptr(), W["src"], -1, args.tile, 0, 1)
+
+        for i in range(len(lanes)):
+            alt_frame(i)
+        torch.cuda.synchronize()
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record(stream)
+        for _, st_, _ in lanes[1:]:
+            st_.wait_event(a0)
+        for i in range(n_alt):
+            alt_frame(i)
+        for _, st_, _ in lanes[1:]:
+            stream.wait_stream(st_)
+        a1.record(stream)
+        torch.cuda.synchronize()
+        alt_ms = a0.elapsed_time(a1) / n_alt
+        alt = {"budgets": "40,20,20", "frames": n_alt, "ms_per_frame": alt_ms,
+               "value": units_per_step / (alt_ms / 1e3) / 1e6, "unit": "Mrays/s"}
+
     e2e = None
     if not args.no_e2e and not animated:
         e2e = run_e2e(args, ctx, ds, seq, stream, world, rank, W)
@@ -579,6 +613,7 @@ def main():
                        "l2": "per-frame working set (ray state, lists, framebuffer) > 126 MB L2; weights L2-resident"},
             "fps": 1000.0 / ms_per_frame,
             "frame": frame,
+            "parity_setting": alt,
             "roofline": {"bound": "tensor", "kernel": kernel, "achieved": achieved_tf, "peak": peak_tf,
                          "unit": "TFLOP/s", "frac": achieved_tf / peak_tf,
                          "peak_kind": f"{pk_kind} bf16 sustained (MEASURED_PEAKS.json)", "traffic": traffic,
