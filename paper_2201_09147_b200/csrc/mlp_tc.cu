@@ -418,6 +418,17 @@ __device__ __forceinline__ void stage_append(bool pred, int value, StageList s) 
   if (pred) s.buf[base + __popc(mask & ((1u << lane) - 1u))] = value;
 }
 
+// Flush body for callers that already synchronised the appends (the count is uniform).
+__device__ __forceinline__ void stage_flush_now(StageList s, int* list, int* gcount, int* gbase, int ctid) {
+  const int n = *s.count;
+  if (ctid == 0) *gbase = atomicAdd(gcount, n);
+  named_bar(2, 128);
+  const int base = *gbase;
+  for (int i = ctid; i < n; i += 128) list[base + i] = s.buf[i];
+  named_bar(2, 128);
+  if (ctid == 0) *s.count = 0;
+}
+
 // Called by the 128 consumer threads (named barrier 2) after a tile's appends.
 __device__ __forceinline__ void stage_flush(StageList s, int* list, int* gcount, int* gbase, int ctid, bool force) {
   named_bar(2, 128);
@@ -860,7 +871,11 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
       for (bool first = true;; first = false) {
         if (g0 && !first) refill();
         mark(14);
-        if (!bar_vote_any(3, 128 * kGroups, g0 && slot >= 0)) {
+        // one barrier per tile: the live-row vote also orders every warp's staged appends of
+        // the previous tile before the flush decision below
+        const bool live = bar_vote_any(3, 128 * kGroups, g0 && slot >= 0);
+        if (g0 && *sm.stage_count > kStageCap - kRows) stage_flush_now(st_adv, a.adv_list, a.adv_count, sm.stage_base, ctid);
+        if (!live) {
           // no live row: either prefetches are still in flight (refill again) or done
           if (bar_vote_any(3, 128 * kGroups, g0 && pf_stage != kPfNeed)) continue;
           break;
@@ -903,7 +918,6 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
           }
           mark(12);
           stage_append(conv, s0, st_adv);
-          stage_flush(st_adv, a.adv_list, a.adv_count, sm.stage_base, ctid, false);
           mark(13);
         }
       }
