@@ -18,6 +18,8 @@
  *                             gradient_batch<double>                    src/mlp/mlp.cpp:104-210
  *                             NeuralField / NeuralTimeField f64 batches src/fields/field.cpp:167-178, 301-311
  *                             (the certification path: nesting.cpp:131-361)
+ *   nsdf_cuda_backprop_f64    trainer::backprop_sine_mlp                src/trainer/backprop.cpp:66-78
+ *   nsdf_cuda_fit_mlp         trainer::fit_mlp (device-resident loop)   src/trainer/fit.cpp:87-196
  *   nsdf_cuda_generate_rays   tracer::generate_rays                     src/tracer/camera.cpp:20-43
  *   nsdf_cuda_trace_rays      tracer::multiscale_sphere_trace (batched) src/tracer/trace.cpp:86-132, 162-169
  *   nsdf_cuda_sphere_trace    tracer::sphere_trace                      src/tracer/trace.cpp:136-160
@@ -160,6 +162,29 @@ typedef struct {
   uint64_t normal_launches;
 } nsdf_profile;
 
+/* SIREN training (trainer::TrainConfig minus the architecture / omega0 / seed, which the
+ * caller applies through random_init, trainer.hpp:50-70) and its report (TrainReport). */
+typedef struct {
+  int epochs;
+  int batch_size;           /* 0 = full batch */
+  double learning_rate;     /* peak rate after warmup */
+  double momentum;
+  int warmup_epochs;
+  int plateau_patience;
+  double plateau_threshold;
+  double min_learning_rate;
+} nsdf_train_config;
+
+typedef struct {
+  double final_loss;
+  double validation_mse;
+  double validation_max_error;
+  double final_learning_rate;
+  int diverged;
+  int halvings;
+  int epochs_recorded;      /* entries written to epoch_loss */
+} nsdf_train_report;
+
 /* ---- context ---------------------------------------------------------------------- */
 int nsdf_cuda_abi_version(void);
 const char* nsdf_cuda_last_error(void);
@@ -206,6 +231,23 @@ int nsdf_cuda_eval_grad_device(nsdf_ctx* ctx, nsdf_field field, const float* d_p
  * Analytic fields return NSDF_ERR_CONFIG (they evaluate on the host). */
 int nsdf_cuda_eval_f64(nsdf_ctx* ctx, nsdf_field field, const double* points, int rows, int k,
                        double time, double* out, double* grad);
+
+/* ---- training (FP64, bit-exact with the reference trainer) ----------------------------
+ * Packed parameters as in nsdf_cuda_upload_mlp.  backprop: trainer::backprop_sine_mlp
+ * (backprop.cpp:66-78) — grads packed like the parameters, loss = mean squared error.
+ * fit: trainer::fit_mlp (fit.cpp:87-196) from caller-initialised parameters (random_init)
+ * and the caller's Rng state after it (xoshiro256++ s[4], core.hpp:75-118; advanced by the
+ * epoch shuffles); params returns the checkpoint; epoch_loss holds cfg->epochs entries. */
+int nsdf_cuda_backprop_f64(nsdf_ctx* ctx, int n_layers, const int32_t* rows, const int32_t* cols,
+                           const double* packed, int activation, double omega0, int input_dim,
+                           const double* points, const double* targets, int k, double* grads,
+                           double* loss);
+int nsdf_cuda_fit_mlp(nsdf_ctx* ctx, int n_layers, const int32_t* rows, const int32_t* cols,
+                      double* packed, int activation, double omega0, int input_dim,
+                      uint64_t* rng_state, const double* points, const double* targets, int n,
+                      const double* val_points, const double* val_targets, int n_val,
+                      const nsdf_train_config* config, double* epoch_loss,
+                      nsdf_train_report* report);
 
 /* ---- tracing --------------------------------------------------------------------------
  * rays: n x 6 floats {ox, oy, oz, dx, dy, dz} (tracer::Ray, trace.hpp:24-27). */

@@ -39,6 +39,24 @@ int nsdf_host_sup_diff(const char* f_src, const char* g_src, uint64_t n_uniform,
 int nsdf_host_verify_nesting(const char* manifest, double time, uint64_t samples, uint64_t seed,
                              uint64_t max_recorded, uint64_t* counts, double* recorded);
 
+/* Training (trainer::sample_training_set / fit_mlp / backprop_sine_mlp) through the drop-in
+ * library: sampling on the host, backprop and the fit loop on the device in FP64.
+ *   sample: oracle source as above; points_out 3 x (n_uniform + n_surface), targets_out,
+ *           val_points_out 3 x n_validation, val_targets_out.
+ *   fit: arch "WxK" (parse_architecture); params_out has parameter_count() entries (packed
+ *        per layer W then b); epoch_loss has cfg->epochs entries; report as nsdf_train_report.
+ *   backprop: grads_out packed like params; *loss = mean squared error. */
+int nsdf_host_sample_training_set(const char* oracle, uint64_t n_uniform, uint64_t n_surface, double sigma,
+                                  uint64_t n_validation, uint64_t seed, double* points_out,
+                                  double* targets_out, double* val_points_out, double* val_targets_out);
+int nsdf_host_fit_mlp(const char* arch, int input_dim, double omega0, uint64_t seed,
+                      const nsdf_train_config* cfg, const double* points, const double* targets, int n,
+                      const double* val_points, const double* val_targets, int n_val, double* params_out,
+                      double* epoch_loss, nsdf_train_report* report);
+int nsdf_host_backprop(const char* arch, int input_dim, double omega0, uint64_t seed,
+                       const double* points, const double* targets, int k, double* params_out,
+                       double* grads_out, double* loss);
+
 #ifdef __cplusplus
 }
 #endif

@@ -20,6 +20,7 @@
 #include "nsdf/tensor/kernels.hpp"
 #include "nsdf/tracer/trace.hpp"
 #include "nsdf_cuda.h"
+#include "nsdf/trainer/trainer.hpp"
 
 using namespace nsdf;
 
@@ -439,6 +440,93 @@ int nsdf_ref_verify_nesting(const char* manifest, double time, uint64_t samples,
     o[3] = double(r.violations[i].pair_index);
     o[4] = r.violations[i].f_coarse;
     o[5] = r.violations[i].f_fine;
+  }
+  SHIM_CATCH
+}
+
+// ---- training (trainer::sample_training_set / fit_mlp / backprop_sine_mlp) ----
+int nsdf_ref_sample_training_set(const char* oracle, uint64_t n_uniform, uint64_t n_surface, double sigma,
+                                 uint64_t n_validation, uint64_t seed, double* points_out, double* targets_out,
+                                 double* val_points_out, double* val_targets_out) {
+  SHIM_TRY
+  auto f = ref_field(oracle);
+  trainer::SampleConfig sc;
+  sc.n_uniform = size_t(n_uniform);
+  sc.n_surface = size_t(n_surface);
+  sc.sigma = sigma;
+  sc.n_validation = size_t(n_validation);
+  sc.seed = seed;
+  auto set = trainer::sample_training_set(*f, sc);
+  std::memcpy(points_out, set.points.data(), sizeof(double) * set.points.size());
+  std::memcpy(targets_out, set.targets.data(), sizeof(double) * set.targets.size());
+  std::memcpy(val_points_out, set.val_points.data(), sizeof(double) * set.val_points.size());
+  std::memcpy(val_targets_out, set.val_targets.data(), sizeof(double) * set.val_targets.size());
+  SHIM_CATCH
+}
+
+static void ref_put_params(const mlp::MlpParams<double>& p, double* out) {
+  size_t o = 0;
+  for (const auto& l : p.layers) {
+    std::memcpy(out + o, l.weights.data(), sizeof(double) * l.weights.size());
+    o += l.weights.size();
+    std::memcpy(out + o, l.bias.data(), sizeof(double) * l.bias.size());
+    o += l.bias.size();
+  }
+}
+
+int nsdf_ref_fit_mlp(const char* arch, int input_dim, double omega0, uint64_t seed, const nsdf_train_config* cfg,
+                     const double* points, const double* targets, int n, const double* val_points,
+                     const double* val_targets, int n_val, double* params_out, double* epoch_loss,
+                     nsdf_train_report* report) {
+  SHIM_TRY
+  trainer::TrainConfig tc;
+  tc.arch = mlp::parse_architecture(arch, input_dim);
+  tc.epochs = cfg->epochs;
+  tc.batch_size = cfg->batch_size;
+  tc.learning_rate = cfg->learning_rate;
+  tc.momentum = cfg->momentum;
+  tc.omega0 = omega0;
+  tc.seed = seed;
+  tc.warmup_epochs = cfg->warmup_epochs;
+  tc.plateau_patience = cfg->plateau_patience;
+  tc.plateau_threshold = cfg->plateau_threshold;
+  tc.min_learning_rate = cfg->min_learning_rate;
+  trainer::TrainingSet set;
+  set.input_dim = input_dim;
+  set.points = tensor::Matrix<double>(input_dim, n, std::vector<double>(points, points + size_t(input_dim) * n));
+  set.targets = tensor::Matrix<double>(1, n, std::vector<double>(targets, targets + n));
+  set.val_points = tensor::Matrix<double>(input_dim, n_val,
+                                          std::vector<double>(val_points, val_points + size_t(input_dim) * n_val));
+  set.val_targets = tensor::Matrix<double>(1, n_val, std::vector<double>(val_targets, val_targets + n_val));
+  auto fit = trainer::fit_mlp(tc, set);
+  ref_put_params(fit.params, params_out);
+  std::memset(report, 0, sizeof(*report));
+  for (size_t i = 0; i < fit.report.epoch_loss.size(); ++i) epoch_loss[i] = fit.report.epoch_loss[i];
+  report->epochs_recorded = int(fit.report.epoch_loss.size());
+  report->final_loss = fit.report.final_loss;
+  report->validation_mse = fit.report.validation_mse;
+  report->validation_max_error = fit.report.validation_max_error;
+  report->final_learning_rate = fit.report.final_learning_rate;
+  report->diverged = fit.report.diverged ? 1 : 0;
+  report->halvings = fit.report.halvings;
+  SHIM_CATCH
+}
+
+int nsdf_ref_backprop(const char* arch, int input_dim, double omega0, uint64_t seed, const double* points,
+                      const double* targets, int k, double* params_out, double* grads_out, double* loss) {
+  SHIM_TRY
+  Rng rng(seed);
+  auto params = mlp::random_init(mlp::parse_architecture(arch, input_dim), omega0, rng);
+  ref_put_params(params, params_out);
+  auto g = trainer::backprop_sine_mlp(
+      params, tensor::Matrix<double>(input_dim, k, std::vector<double>(points, points + size_t(input_dim) * k)),
+      tensor::Matrix<double>(1, k, std::vector<double>(targets, targets + k)), loss);
+  size_t o = 0;
+  for (const auto& l : g.layers) {
+    std::memcpy(grads_out + o, l.weights.data(), sizeof(double) * l.weights.size());
+    o += l.weights.size();
+    std::memcpy(grads_out + o, l.bias.data(), sizeof(double) * l.bias.size());
+    o += l.bias.size();
   }
   SHIM_CATCH
 }

@@ -260,3 +260,44 @@ def verify_nesting(manifest, samples=100000, seed=7, max_recorded=1000, time=0.0
                                             _p(counts, U64), _p(rec, D)))
     return {"samples_total": int(counts[0]), "checked": int(counts[1]), "violation_count": int(counts[2]),
             "violations": rec[:int(counts[3])].copy()}
+
+
+# ---- training (trainer::sample_training_set / fit_mlp / backprop_sine_mlp) -------------------
+def sample_training_set(oracle, n_uniform=100000, n_surface=100000, sigma=0.01, n_validation=10000, seed=1):
+    lib = load()
+    n = n_uniform + n_surface
+    pts, tg = np.zeros((3, n)), np.zeros(n)
+    vp, vt = np.zeros((3, n_validation)), np.zeros(n_validation)
+    _check(lib, lib.nsdf_ref_sample_training_set(oracle.encode(), U64(n_uniform), U64(n_surface), D(sigma),
+                                                 U64(n_validation), U64(seed), _p(pts, D), _p(tg, D), _p(vp, D),
+                                                 _p(vt, D)))
+    return pts, tg, vp, vt
+
+
+def fit_mlp(arch, points, targets, val_points, val_targets, config, omega0=30.0, seed=7):
+    from paper_2201_09147_b200.abi import TrainReportC
+    from paper_2201_09147_b200.train import arch_params
+    lib = load()
+    input_dim = points.shape[0]
+    params = np.zeros(arch_params(arch, input_dim))
+    loss = np.zeros(config.epochs)
+    rep = TrainReportC()
+    pts, tg = np.ascontiguousarray(points, np.float64), np.ascontiguousarray(targets, np.float64)
+    vp, vt = np.ascontiguousarray(val_points, np.float64), np.ascontiguousarray(val_targets, np.float64)
+    _check(lib, lib.nsdf_ref_fit_mlp(arch.encode(), input_dim, D(omega0), U64(seed), ctypes.byref(config),
+                                     _p(pts, D), _p(tg, D), pts.shape[1], _p(vp, D), _p(vt, D), vp.shape[1],
+                                     _p(params, D), _p(loss, D), ctypes.byref(rep)))
+    return params, loss[:rep.epochs_recorded].copy(), rep
+
+
+def backprop(arch, points, targets, omega0=30.0, seed=7):
+    from paper_2201_09147_b200.train import arch_params
+    lib = load()
+    input_dim = points.shape[0]
+    params = np.zeros(arch_params(arch, input_dim))
+    grads = np.zeros_like(params)
+    loss = D(0)
+    pts, tg = np.ascontiguousarray(points, np.float64), np.ascontiguousarray(targets, np.float64)
+    _check(lib, lib.nsdf_ref_backprop(arch.encode(), input_dim, D(omega0), U64(seed), _p(pts, D), _p(tg, D),
+                                      pts.shape[1], _p(params, D), _p(grads, D), ctypes.byref(loss)))
+    return params, grads, loss.value

@@ -133,3 +133,21 @@ def check(status: int) -> None:
     if status != OK:
         msg = load_library().nsdf_cuda_last_error().decode(errors="replace")
         raise NsdfError(status, msg)
+
+
+class TrainConfigC(ctypes.Structure):
+    """nsdf_train_config (trainer::TrainConfig minus arch / omega0 / seed)."""
+    _fields_ = [("epochs", ctypes.c_int), ("batch_size", ctypes.c_int), ("learning_rate", ctypes.c_double),
+                ("momentum", ctypes.c_double), ("warmup_epochs", ctypes.c_int), ("plateau_patience", ctypes.c_int),
+                ("plateau_threshold", ctypes.c_double), ("min_learning_rate", ctypes.c_double)]
+
+    def __init__(self, epochs=800, batch_size=8192, learning_rate=0.3, momentum=0.9, warmup_epochs=100,
+                 plateau_patience=60, plateau_threshold=0.05, min_learning_rate=1e-10):
+        super().__init__(epochs, batch_size, learning_rate, momentum, warmup_epochs, plateau_patience,
+                         plateau_threshold, min_learning_rate)
+
+
+class TrainReportC(ctypes.Structure):
+    _fields_ = [("final_loss", ctypes.c_double), ("validation_mse", ctypes.c_double),
+                ("validation_max_error", ctypes.c_double), ("final_learning_rate", ctypes.c_double),
+                ("diverged", ctypes.c_int), ("halvings", ctypes.c_int), ("epochs_recorded", ctypes.c_int)]

@@ -30,6 +30,7 @@ CUDA_SOURCES = {
     "capi.cu": ["-fmad=false"],
     "mlp_tc.cu": [],
     "mlp_f64.cu": ["-fmad=false"],
+    "train_f64.cu": ["-fmad=false"],
 }
 
 

@@ -695,6 +695,61 @@ int nsdf_cuda_eval_f64(nsdf_ctx* c, nsdf_field h, const double* points, int rows
   return NSDF_OK;
 }
 
+namespace {
+// MlpParams::validate (mlp.cpp:13-39) for the training entry points
+int check_arch(int n_layers, const int32_t* rows, const int32_t* cols, int activation, int input_dim) {
+  if (!rows || !cols) return fail(NSDF_ERR_CONTRACT, "null argument");
+  if (n_layers < 1) return fail(NSDF_ERR_VALIDATION, "network has no layers");
+  if (input_dim != 3 && input_dim != 4)
+    return fail(NSDF_ERR_VALIDATION, "input_dim must be 3 or 4, got " + std::to_string(input_dim));
+  if (cols[0] != input_dim)
+    return fail(NSDF_ERR_VALIDATION, "layer 0 expects input dim " + std::to_string(cols[0]) +
+                                         " but network input_dim is " + std::to_string(input_dim));
+  for (int i = 0; i + 1 < n_layers; ++i)
+    if (cols[i + 1] != rows[i])
+      return fail(NSDF_ERR_VALIDATION, "dimension chain broken between layers " + std::to_string(i) + "," +
+                                           std::to_string(i + 1));
+  if (rows[n_layers - 1] != 1)
+    return fail(NSDF_ERR_VALIDATION,
+                "output layer must have a single output, got " + std::to_string(rows[n_layers - 1]));
+  if (activation != NSDF_ACT_SINE && activation != NSDF_ACT_IDENTITY)
+    return fail(NSDF_ERR_CONFIG, "unknown activation kind");
+  return NSDF_OK;
+}
+}  // namespace
+
+int nsdf_cuda_backprop_f64(nsdf_ctx* c, int n_layers, const int32_t* rows, const int32_t* cols, const double* packed,
+                           int activation, double omega0, int input_dim, const double* points, const double* targets,
+                           int k, double* grads, double* loss) {
+  if (!c || !packed || !points || !targets || !grads) return fail(NSDF_ERR_CONTRACT, "null argument");
+  if (int st = check_arch(n_layers, rows, cols, activation, input_dim)) return st;
+  if (k < 1) return fail(NSDF_ERR_CONTRACT, "targets must be 1x" + std::to_string(k));
+  std::lock_guard<std::mutex> lk(c->mu);
+  DeviceGuard g(c->device);
+  NSDF_CUDA(train_backprop(n_layers, rows, cols, packed, activation, omega0, input_dim, points, targets, k, grads,
+                           loss, c->stream));
+  return NSDF_OK;
+}
+
+int nsdf_cuda_fit_mlp(nsdf_ctx* c, int n_layers, const int32_t* rows, const int32_t* cols, double* packed,
+                      int activation, double omega0, int input_dim, uint64_t* rng_state, const double* points,
+                      const double* targets, int n, const double* val_points, const double* val_targets, int n_val,
+                      const nsdf_train_config* cfg, double* epoch_loss, nsdf_train_report* report) {
+  if (!c || !packed || !rng_state || !points || !targets || !cfg || !epoch_loss || !report)
+    return fail(NSDF_ERR_CONTRACT, "null argument");
+  if (int st = check_arch(n_layers, rows, cols, activation, input_dim)) return st;
+  // fit.cpp:88-94
+  if (cfg->epochs <= 0 || !(cfg->learning_rate > 0))
+    return fail(NSDF_ERR_CONFIG, "epochs and learning rate must be positive");
+  if (n < 1) return fail(NSDF_ERR_CONTRACT, "the training set is empty");
+  if (n_val > 0 && (!val_points || !val_targets)) return fail(NSDF_ERR_CONTRACT, "null validation set");
+  std::lock_guard<std::mutex> lk(c->mu);
+  DeviceGuard g(c->device);
+  NSDF_CUDA(train_fit(n_layers, rows, cols, packed, activation, omega0, input_dim, rng_state, points, targets, n,
+                      val_points, val_targets, std::max(n_val, 0), cfg, epoch_loss, report, c->stream));
+  return NSDF_OK;
+}
+
 int nsdf_cuda_generate_rays(nsdf_ctx* c, const nsdf_camera* camera, float* rays) {
   if (!c || !rays) return fail(NSDF_ERR_CONTRACT, "null argument");
   std::lock_guard<std::mutex> lk(c->mu);

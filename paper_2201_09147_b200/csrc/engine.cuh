@@ -148,6 +148,15 @@ void launch_raycast_mesh(const CamBasis& cb, const float* tri_verts /* n_tri x 9
 void launch_eval_f64(const DevNet& n, const double* pts, int rows, int k, double time, double* out, double* grad,
                      cudaStream_t s);
 
+// FP64 SIREN training (train_f64.cu), host buffers in/out.
+cudaError_t train_backprop(int n_layers, const int32_t* rows, const int32_t* cols, const double* params_h,
+                           int activation, double omega0, int input_dim, const double* points_h,
+                           const double* targets_h, int k, double* grads_h, double* loss, cudaStream_t s);
+cudaError_t train_fit(int n_layers, const int32_t* rows, const int32_t* cols, double* params_h, int activation,
+                      double omega0, int input_dim, uint64_t* rng, const double* points_h, const double* targets_h,
+                      int n, const double* val_points_h, const double* val_targets_h, int n_val,
+                      const nsdf_train_config* cfg, double* epoch_loss, nsdf_train_report* rep, cudaStream_t s);
+
 // Tensor-core availability of a net for the fast mode (mlp_tc.cu).
 bool tc_supported(const DevNet& n);
 
