@@ -5,10 +5,10 @@
 set -e
 tag=${1:-r1}
 python bench.py > gpurun_out/${tag}_bench.json 2> gpurun_out/${tag}_bench.err
-python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e > /dev/null
+python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e --no-alt > /dev/null
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${tag}_launches.csv \
-    python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e > /dev/null 2>&1
-python bench.py --steps 1 --warmup 1 --inflight 1 --no-cpu-baseline --no-e2e > /dev/null
+    python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e --no-alt > /dev/null 2>&1
+python bench.py --steps 1 --warmup 1 --inflight 1 --no-cpu-baseline --no-e2e --no-alt > /dev/null
 ncu --set full --clock-control none --import-source on -k regex:tc_mlp --launch-skip 4 --launch-count 4 \
-    -o gpurun_out/${tag}_full -f python bench.py --steps 1 --warmup 1 --inflight 1 --no-cpu-baseline --no-e2e \
+    -o gpurun_out/${tag}_full -f python bench.py --steps 1 --warmup 1 --inflight 1 --no-cpu-baseline --no-e2e --no-alt \
     > gpurun_out/${tag}_ncu.log 2>&1
