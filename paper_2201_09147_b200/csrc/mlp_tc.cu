@@ -1,25 +1,30 @@
-// tcgen05 fast path of the SIREN evaluator (north_star subsystems 1 + 2).
+// tcgen05 fast path of the SIREN evaluator (north_star subsystems 1-3).
 //
-// One persistent CTA evaluates tiles of 128 TMEM lanes: 128 rays (forward) or 32 rays x 4
-// chains (value + 3 input tangents: the "width x 4" analytic-normal tile).  Per tile:
+// A CTA evaluates tiles of 128 TMEM lanes: 128 rays (forward) or 32 rays x 4 chains (value +
+// 3 input tangents: the "width x 4" analytic-normal tile).  Per tile:
 //
-//   layer 0 (K = 3/4)    FP32 FFMA in the epilogue warps, sin -> fp16 A operand in SMEM
-//   hidden layers        D[128 x W] (fp32, TMEM) = A[128 x W] (fp16, SMEM) . W_l^T
-//                        tcgen05.mma.cta_group::1.kind::f16, M=128 N=W K=16 per instruction,
-//                        issued by one thread; weight K-chunks streamed into a 2-stage SMEM
-//                        ring with cp.async.bulk (pre-arranged in the UMMA canonical layout at
-//                        upload, so a chunk is one contiguous 1-D bulk copy)
-//   epilogue             tcgen05.ld 32x32b -> one FFMA forms omega*(z + b) in radians ->
-//                        MUFU sine (hardware reduction in revolutions) -> fp16 -> next A;
-//                        tangent lanes multiply by omega*cos of their ray's value lane
-//                        (warp shuffle); the last hidden layer folds the 1 x W output layer
-//                        into an FP32 dot product
-//   consumer             trace update + warp-ballot compaction | normal/shade/framebuffer
-//                        | batch outputs
+//   layer 0              a K = 32 MMA: A0 = the point split into three fp16 parts (+ ones for
+//                        the bias), B0 = fp16 hi/lo parts of omega*W0 and omega*b0 (built per
+//                        CTA at launch) -> D0 = omega*(W0 p + b0) in TMEM
+//   hidden layers        D[128 x W] (fp32, TMEM) = A[128 x W] (fp16 hi/lo, SMEM) . W_l^T (fp16
+//                        hi/lo): tcgen05.mma.cta_group::1.kind::f16, M=128 N=W K=16, three
+//                        terms per K step (split precision), issued by one thread; weights
+//                        SMEM-resident (64-wide) or streamed in 32-K chunks through a 2-stage
+//                        cp.async.bulk ring by a producer warp (pre-arranged in the UMMA
+//                        canonical layout at upload, so a chunk is one contiguous bulk copy)
+//   K streaming          16-column block b belongs to column group b % groups; the MMA of
+//                        layer m+1 consumes block rows as the epilogue of layer m writes them
+//                        (kready mbarriers); accumulators alternate between two TMEM regions
+//   epilogue             tcgen05.ld 32x32b.x16 (one block ahead) -> one FFMA forms
+//                        omega*(z + b) in radians -> MUFU sine -> fp16 hi/lo -> next A;
+//                        tangent lanes multiply by omega*cos of their ray's value lane (warp
+//                        shuffle); the last hidden layer folds in the 1 x W output layer
+//   consumer             persistent trace (a whole level per launch, rows refilled from the
+//                        level's list) | normal + shade + framebuffer | batch outputs
 //
-// Warp roles (192 threads): warp 0 = MMA issuer (+ TMEM allocator), warp 1 = weight
-// producer, warps 2-5 = epilogue (warp w reads TMEM lanes 32*(w%4) .. +31).  Two CTAs per SM
-// overlap one CTA's tensor work with the other's sine epilogue.
+// Warp roles: warp 0 = MMA issuer (+ TMEM allocator), warp 1 = weight producer (streamed
+// nets), then 4 epilogue warps per column group (warp w reads TMEM lanes 32*(w%4) .. +31).
+// 64-wide nets run 4 CTAs per SM, 128-wide 2, 256-wide 1 (SMEM / TMEM / register bound).
 //
 // SMEM operand layout (K-major, SWIZZLE_NONE canonical): element (row r, k) of an R-row
 // operand at ((k/8)*(R/8) + r/8)*64 + (r%8)*8 + k%8 halves, i.e. 8x16-byte core matrices;
@@ -36,14 +41,11 @@ namespace nsdf_b200 {
 
 namespace {
 
-constexpr int kTcThreads = 192;
 constexpr int kRows = 128;   // TMEM lanes per tile
 constexpr int kKC = 32;      // K elements per streamed weight chunk
 constexpr int kStages = 2;
 constexpr int kBlk = 16;     // columns per epilogue block = K per MMA step
 constexpr int kMaxSub = 8;   // max blocks per column group per layer (kready barriers)
-constexpr float kInv2Pi = 0.15915494309189535f;
-constexpr float k2Pi = 6.283185307179586f;
 constexpr float kHalfPi = 1.5707963267948966f;
 
 // ---- PTX wrappers ---------------------------------------------------------------------
@@ -91,24 +93,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity, uint32
     }
   }
 }
-// Spin-wait with nanosleep back-off: the single-lane MMA / producer warps would otherwise
-// take issue slots from the epilogue warps while they wait.
-template <uint32_t kBackoff>
-__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity) {
-  const uint32_t a = smem_addr(bar);
-  for (;;) {
-    uint32_t done;
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(done)
-        : "r"(a), "r"(parity)
-        : "memory");
-    if (done) return;
-    __nanosleep(kBackoff);
-  }
-}
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                    smem_addr(dst)),
@@ -130,20 +114,6 @@ __device__ __forceinline__ void tc_mma(uint32_t d_tmem, uint64_t a_desc, uint64_
       "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
       "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
 }
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float v[32]) {
-  uint32_t r[32];
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
-        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
-        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
-        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-      : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-}
 // Asynchronous 32x32b.x16 load: the registers are only valid after tmem_wait16 (which
 // names them as outputs, so the compiler cannot read them earlier).
 __device__ __forceinline__ void tmem_issue16(uint32_t taddr, uint32_t (&r)[16]) {
@@ -160,18 +130,6 @@ __device__ __forceinline__ void tmem_wait16(uint32_t (&r)[16]) {
                :
                : "memory");
 }
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, float v[16]) {
-  uint32_t r[16];
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
-        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-      : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-  for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
-}
-
 // UMMA shared-memory descriptor, K-major SWIZZLE_NONE (sm_100 version bit 46).
 __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
   return uint64_t((saddr >> 4) & 0x3FFFu) | (uint64_t((lbo >> 4) & 0x3FFFu) << 16) |
@@ -192,7 +150,6 @@ __device__ __forceinline__ int a_off(int row, int k) { return ((k >> 3) * (kRows
 // fp32 reduction including the reference's Cody-Waite) is one RZ rounding of x/2pi.
 // 3 issue slots per activation instead of 7 for an explicit turns reduction.
 __device__ __forceinline__ float fast_sin(float x) { return __sinf(x); }
-__device__ __forceinline__ void fast_sincos(float x, float& s, float& c) { __sincosf(x, &s, &c); }
 
 __device__ __forceinline__ uint32_t pack_half2(float a, float b) {
   __half2 h = __floats2half2_rn(a, b);
