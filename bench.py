@@ -537,7 +537,7 @@ def main():
         trace_ms = sum(prof.level_ms) / max(prof.frames, 1)
         normals_ms = prof.normals_ms / max(prof.frames, 1)
         achieved_tf = flops_trace / (trace_ms / 1e3) / 1e12 if trace_ms > 0 else 0.0
-        kernel = "trace-iteration MLP tiles (all levels)"
+        kernel = "persistent trace-level MLP tiles (all levels)"
         # activation bound: one MUFU sine per hidden activation (layer 0 + hidden layers)
         sines = sum(int(stats.evals[j]) * (seq.members[j].n_layers - 1) * seq.members[j].width
                     for j in range(len(seq.members)))

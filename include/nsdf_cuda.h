@@ -154,7 +154,7 @@ typedef struct {
  * frames while profiling is enabled — the "CUDA events per level and per frame" of
  * SURVEY.md §5.  Reading it synchronizes the stream. */
 typedef struct {
-  double level_ms[NSDF_MAX_LEVELS]; /* trace-iteration kernels (MLP tiles) per level    */
+  double level_ms[NSDF_MAX_LEVELS]; /* trace kernels (MLP tiles) per level             */
   double normals_ms;                /* fused normal + shade kernels                     */
   double frame_ms;                  /* whole frames (rays .. framebuffer)              */
   uint64_t frames;
