@@ -72,7 +72,12 @@ def broadcast_sequence(manifest_path: Optional[str], world: int, rank: int, devi
 
 
 class TileGather:
-    """Packs this rank's tile pixels (rgb, depth, mask) and gathers them on rank 0."""
+    """Packs this rank's tile pixels (rgb, depth, mask) and gathers them on rank 0.
+
+    Per frame: one packing gather on every rank (a precomputed [n, 5] index into the flat
+    rgb|depth|mask view), one NCCL gather, and on rank 0 one scatter per buffer for all
+    remote ranks together (precomputed combined indices) — a handful of kernels, so rank 0's
+    extra work does not grow with the world size."""
 
     def __init__(self, width: int, height: int, tile: int, rank: int, world: int, device=None):
         import torch
@@ -81,29 +86,35 @@ class TileGather:
         if device is None:
             device = torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available() else "cpu"
         self.device = device
-        self.idx = [torch.from_numpy(owned_pixels(width, height, tile, r, world)).to(device) for r in range(world)]
-        self.n_max = max(int(i.numel()) for i in self.idx)
+        idx = [torch.from_numpy(owned_pixels(width, height, tile, r, world)) for r in range(world)]
+        self.n = [int(i.numel()) for i in idx]
+        self.n_max = max(self.n)
+        self.idx = idx[rank].to(device)
         self.send = torch.zeros((self.n_max, 5), dtype=torch.float32, device=device)
-        self.recv = [torch.zeros_like(self.send) for _ in range(world)] if rank == 0 else None
+        self.recv = None
+        if rank == 0:
+            self.recv_all = torch.zeros((world, self.n_max, 5), dtype=torch.float32, device=device)
+            self.recv = list(self.recv_all.unbind(0))
+            # rows of recv_all (flattened) holding remote pixels, and their pixel indices
+            rows = [torch.arange(self.n[r]) + r * self.n_max for r in range(1, world)]
+            self.remote_rows = torch.cat(rows).to(device) if rows else torch.zeros(0, dtype=torch.long, device=device)
+            self.remote_pix = torch.cat(idx[1:]).to(device) if world > 1 else self.remote_rows
         self.host = None
 
     def __call__(self, rgb, depth, mask):
+        import torch
         import torch.distributed as dist
 
-        idx = self.idx[self.rank]
+        idx = self.idx
         n = idx.numel()
-        self.send[:n, 0:3] = rgb.view(-1, 3)[idx]
-        self.send[:n, 3] = depth[idx]
-        self.send[:n, 4] = mask[idx].float()
+        self.send[:n] = torch.cat([rgb.view(-1, 3)[idx], depth[idx].unsqueeze(1), mask[idx].unsqueeze(1).float()], 1)
         dist.gather(self.send, self.recv if self.rank == 0 else None, dst=0)
         if self.rank == 0:
             self.rgb, self.depth, self.mask = rgb, depth, mask
-            for r in range(1, self.world):
-                ir = self.idx[r]
-                m = ir.numel()
-                rgb.view(-1, 3)[ir] = self.recv[r][:m, 0:3]
-                depth[ir] = self.recv[r][:m, 3]
-                mask[ir] = self.recv[r][:m, 4].to(mask.dtype)
+            got = self.recv_all.view(-1, 5)[self.remote_rows]
+            rgb.view(-1, 3)[self.remote_pix] = got[:, 0:3]
+            depth[self.remote_pix] = got[:, 3]
+            mask[self.remote_pix] = got[:, 4].to(mask.dtype)
 
     def to_host(self):
         """D2H of the assembled frame on rank 0 (the e2e read-back)."""
