@@ -265,3 +265,25 @@ def test_fast_stats_match_records(fast):
     for j in range(3):
         assert st.evals[j] == int(r["iters"][:, j].astype(np.int64).sum())
     assert st.hits == int(r["hit"].sum())
+
+
+def test_fast_mixed_analytic_and_neural_levels(ctx, fast, tmp_path):
+    """An analytic coarse level (FFMA iterations) feeding the persistent tcgen05 levels."""
+    import json
+    from paper_2201_09147_b200.abi import ShadeConfig, TraceConfig, standard_camera
+    from paper_2201_09147_b200.engine import DeviceSequence
+    from paper_2201_09147_b200.manifest import load_manifest
+    _fixture("torus_w30_256x3.sdfnet")
+    man = tmp_path / "mixed.nest"
+    man.write_text(json.dumps({"deltas": [0.45, 0.107, 0.05], "fields": [
+        {"analytic": "sphere", "params": {"r": 1.05}},
+        {"weights": os.path.join(ASSETS, "torus_w30_64x1.sdfnet")},
+        {"weights": os.path.join(ASSETS, "torus_w30_256x3.sdfnet")}]}))
+    seq = load_manifest(str(man))
+    cam = standard_camera(320, 200)
+    cfg = TraceConfig((10, 20, 8))
+    shade = ShadeConfig(specular=0.3)
+    a = ctx.render(DeviceSequence(ctx, seq).levels(), cam, cfg, shade)
+    b = fast.render(DeviceSequence(fast, seq).levels(), cam, cfg, shade)
+    _assert_render_parity(a, b)
+    assert a[2].sum() > 1000
