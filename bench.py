@@ -583,6 +583,23 @@ def main():
         alt = {"budgets": "40,20,20", "frames": n_alt, "ms_per_frame": alt_ms,
                "value": units_per_step / (alt_ms / 1e3) / 1e6, "unit": "Mrays/s"}
 
+    # HBM side of the roofline (north_star: "achieved HBM GB/s for compaction and normal
+    # mapping"): the trace kernels' measured DRAM bytes per frame (ncu capture, config 2) over
+    # their time; the normal map's algorithmic bytes (point in, normal out) over its time.
+    hbm_peak = pk.get("hbm_gbs", PEAKS_FALLBACK["hbm_gbs"])
+    if W["gbuffer"]:
+        nbytes = units_per_step * 24
+        gbs = nbytes / (ms_per_frame / 1e3) / 1e9
+        hbm = {"kernel": "normal map (12 B point in, 12 B normal out per point)", "bytes": nbytes,
+               "achieved_gbs": gbs, "peak_gbs": hbm_peak, "frac": gbs / hbm_peak, "bytes_kind": "algorithmic"}
+    elif traffic is not None:
+        tms = frame["trace_ms"]
+        gbs = traffic / (tms / 1e3) / 1e9 if tms > 0 else 0.0
+        hbm = {"kernel": "persistent trace levels incl. compaction", "bytes": traffic, "achieved_gbs": gbs,
+               "peak_gbs": hbm_peak, "frac": gbs / hbm_peak, "bytes_kind": "ncu dram read+write per frame"}
+    else:
+        hbm = None
+
     e2e = None
     if not args.no_e2e and not animated:
         e2e = run_e2e(args, ctx, ds, seq, stream, world, rank, W)
@@ -619,7 +636,8 @@ def main():
                          "peak_kind": f"{pk_kind} bf16 sustained (MEASURED_PEAKS.json)", "traffic": traffic,
                          "traffic_note": traffic_note,
                          "whole_frame_tflops": (flops_trace + flops_normals) / (ms_per_frame / 1e3) / 1e12,
-                         "activation_bound": None if W["gbuffer"] else act_bound},
+                         "activation_bound": None if W["gbuffer"] else act_bound,
+                         "hbm": hbm},
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,

@@ -7,6 +7,8 @@
 #include <cstring>
 #include <map>
 #include <memory>
+
+#include <nvtx3/nvToolsExt.h>
 #include <algorithm>
 #include <mutex>
 #include <string>
@@ -236,10 +238,27 @@ struct FrameOut {
   int* d_pack_count = nullptr;
 };
 
+int run_frame_impl(nsdf_ctx* c, const nsdf_level* levels, int m, const nsdf_trace_config* cfg, const CamBasis* cam,
+                   const float* d_rays6, int n_rays, const ShadeParams* sp, int normal_source, int fine_index,
+                   int tile_size, int tile_rank, int tile_world, const FrameOut& out, nsdf_frame_stats* stats,
+                   float final_delta);
+
+// NVTX range per frame (host-side launch sequence; visible in Nsight timelines, free otherwise)
 int run_frame(nsdf_ctx* c, const nsdf_level* levels, int m, const nsdf_trace_config* cfg, const CamBasis* cam,
               const float* d_rays6, int n_rays, const ShadeParams* sp, int normal_source, int fine_index,
               int tile_size, int tile_rank, int tile_world, const FrameOut& out, nsdf_frame_stats* stats,
               float final_delta = 0.0f) {
+  nvtxRangePushA(out.d_rgb ? "nsdf render frame" : "nsdf trace frame");
+  const int st = run_frame_impl(c, levels, m, cfg, cam, d_rays6, n_rays, sp, normal_source, fine_index, tile_size,
+                                tile_rank, tile_world, out, stats, final_delta);
+  nvtxRangePop();
+  return st;
+}
+
+int run_frame_impl(nsdf_ctx* c, const nsdf_level* levels, int m, const nsdf_trace_config* cfg, const CamBasis* cam,
+                   const float* d_rays6, int n_rays, const ShadeParams* sp, int normal_source, int fine_index,
+                   int tile_size, int tile_rank, int tile_world, const FrameOut& out, nsdf_frame_stats* stats,
+                   float final_delta) {
   int n_counters = 0;
   std::vector<LevelDesc> lv = traced_levels(c, levels, m, cfg, &n_counters, final_delta);
   // slots needed: every pixel, or only the pixels of the owned tiles (tile % world == rank)

@@ -7,6 +7,8 @@
 #include <algorithm>
 #include <cstdio>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "engine.cuh"
 #include "mlp_simt.cuh"
 #include "mlp_tc.cuh"
@@ -361,6 +363,9 @@ TraceResult run_trace(Mode mode, const std::vector<LevelDesc>& levels, float eps
     const int* in_count = level_in_count;
     int ping = cur, pong = nxt;
     cudaEvent_t ev = prof ? prof->begin(s) : nullptr;
+    char range[32];
+    snprintf(range, sizeof range, "nsdf level %d", lv.level);
+    nvtxRangePushA(range);
     // fast mode: ONE persistent launch per level (rows refilled from the input list)
     const bool persistent = mode_tc(mode) && lv.field.kind == kFieldMlp && tc_supported(lv.field.net) &&
                             tc_trace_level(mode_terms(mode), lv, eps, t_max, in_list, in_count, cursor, evals,
@@ -389,6 +394,7 @@ TraceResult run_trace(Mode mode, const std::vector<LevelDesc>& levels, float eps
       in_count = it_counts + iter;
       std::swap(ping, pong);
     }
+    nvtxRangePop();
     if (prof) {
       prof->end(lv.level, ev, s);
       prof->acc.trace_launches += persistent ? 1 : lv.budget;

@@ -24,6 +24,7 @@ METRICS = [
     ("launch__shared_mem_per_block_dynamic", "dyn smem/CTA"),
     ("sm__warps_active.avg.pct_of_peak_sustained_active", "warps active %"),
     ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue active %"),
+    ("smsp__thread_inst_executed_per_inst_executed.ratio", "active threads per warp instr (of 32)"),
     ("sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active", "tensor pipe active %"),
     ("sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active", "XU (MUFU) pipe %"),
     ("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active", "FMA pipe %"),
