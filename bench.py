@@ -73,6 +73,8 @@ def parse():
     ap.add_argument("--height", type=int, default=0)
     ap.add_argument("--budgets", default="")
     ap.add_argument("--tile", type=int, default=32, help="image tile edge of the N>1 tile interleave")
+    ap.add_argument("--gather", default="peer", choices=["peer", "nccl"],
+                    help="N>1 frame assembly: peer stores into rank 0's framebuffer, or an NCCL tile gather")
     ap.add_argument("--inflight", type=int, default=3,
                     help="frames in flight (engine contexts on their own streams); 1 = strictly serial frames")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -332,16 +334,26 @@ def run_e2e(args, ctx, ds, seq, stream, world, rank, W):
         f1 = torch.cuda.Event(enable_timing=True)
         f0.record(stream)
         w0 = time.perf_counter()
+        peer = W.get("peer")
+        if peer is not None and rank == 0:
+            hb = (torch.empty(npix * 3, dtype=torch.float32, pin_memory=True),
+                  torch.empty(npix, dtype=torch.float32, pin_memory=True),
+                  torch.empty(npix, dtype=torch.uint8, pin_memory=True))
         for i in range(steps):
             W["step"](i)
             if rank == 0:
-                torch.cuda.current_stream().wait_stream(W["gstream"])
-                W["gather"].to_host()
+                if peer is not None:
+                    W["lanes"][i % len(W["lanes"])][1].synchronize()
+                    peer.to_host(i % (2 * len(W["lanes"])), *(t.data_ptr() for t in hb))
+                else:
+                    torch.cuda.current_stream().wait_stream(W["gstream"])
+                    W["gather"].to_host()
         f1.record(stream)
         torch.cuda.synchronize()
         wall = (time.perf_counter() - w0) * 1e3
         e_ms = max(f0.elapsed_time(f1), wall)
-        path = "nsdf_cuda_render_device per rank + NCCL tile gather + D2H on rank 0"
+        path = ("nsdf_cuda_render_device per rank, tiles stored into rank 0's framebuffer over NVLink, D2H on rank 0"
+                if W.get("peer") is not None else "nsdf_cuda_render_device per rank + NCCL tile gather + D2H on rank 0")
     te = torch.tensor([e_ms], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
@@ -415,8 +427,6 @@ def main():
             W["levels"] = frame_levels[0]
         else:
             W["levels"] = ds.levels()
-        gather = scheduler.TileGather(Wd, Hd, args.tile, rank, world) if world > 1 and not animated else None
-        W["gather"] = gather
         tile_world, tile_rank = (1, 0) if animated else (world, rank)
         # Frames in flight: `inflight` engine contexts, each on its own stream with its own
         # workspace, render consecutive frames concurrently (the tail iterations of one frame
@@ -429,6 +439,22 @@ def main():
             c2.set_stream(s2.cuda_stream)
             lanes.append((c2, s2, DeviceSequence(c2, seq)))
         W["lanes"] = lanes
+        # N > 1 (tiles of one frame): the ranks' shading kernels store their tiles straight
+        # into rank 0's framebuffer ring over NVLink (PeerFramebuffer); NCCL tile gather only
+        # if peer mapping is unavailable.
+        peer, gather = None, None
+        if world > 1 and not animated:
+            if args.gather == "peer":
+                peer = scheduler.PeerFramebuffer(ctx, Wd, Hd, 2 * len(lanes), rank, world)
+                if not peer.ok:
+                    if rank == 0:
+                        print(f"peer framebuffer unavailable ({peer.reason}); NCCL tile gather", file=sys.stderr)
+                    peer.close()
+                    peer = None
+            if peer is None:
+                gather = scheduler.TileGather(Wd, Hd, args.tile, rank, world)
+        W["gather"], W["peer"] = gather, peer
+        tok = [torch.zeros(1, dtype=torch.int32, device="cuda") for _ in lanes]
         n_fb = max(len(lanes), 2 if gather is not None else 1)
         fbs = [(rgb, depth, mask)] + [(torch.zeros_like(rgb), torch.zeros_like(depth), torch.zeros_like(mask))
                                       for _ in range(n_fb - 1)]
@@ -446,6 +472,15 @@ def main():
             li = i % len(lanes)
             c, st, d = lanes[li]
             lv = lane_levels[li][i % len(lane_levels[li])]
+            if peer is not None:
+                # this rank's tiles of frame i land in rank 0's ring slot; the 4-byte all-reduce
+                # on the lane stream completes once every rank's kernels of frame i are done
+                fr, fd, fm = peer.ptrs(i % (2 * len(lanes)))
+                c.render_device(lv, W["cam"], cfg, W["shade"], fr, fd, fm, W["src"], -1, args.tile, tile_rank,
+                                tile_world)
+                with torch.cuda.stream(st):
+                    dist.all_reduce(tok[li])
+                return
             b = i % n_fb
             if free_ev[b] is not None:
                 st.wait_event(free_ev[b])
@@ -463,8 +498,11 @@ def main():
             free_ev[b] = ev
 
         # accounting frame (not timed): per-level evaluation counts -> algorithmic FLOPs
-        stats = ctx.render_device(W["levels"], W["cam"], cfg, W["shade"], rgb.data_ptr(), depth.data_ptr(),
-                                  mask.data_ptr(), W["src"], -1, args.tile, tile_rank, tile_world, stats=True)
+        fb0 = peer.ptrs(0) if peer is not None else (rgb.data_ptr(), depth.data_ptr(), mask.data_ptr())
+        stats = ctx.render_device(W["levels"], W["cam"], cfg, W["shade"], *fb0, W["src"], -1, args.tile, tile_rank,
+                                  tile_world, stats=True)
+        if peer is not None:
+            dist.barrier()
     W["step"] = step
 
     e0 = torch.cuda.Event(enable_timing=True)
@@ -627,6 +665,9 @@ def main():
                        "budgets": args.budgets, "mode": args.mode, "tile": args.tile,
                        "frames_in_flight": 1 if W["gbuffer"] else max(1, args.inflight),
                        "parallelism": (f"frames{world}" if animated else f"tiles{world}") if world > 1 else "single",
+                       "frame_assembly": None if world == 1 or animated else
+                       ("peer stores into rank 0's framebuffer (NVLink)" if W.get("peer") is not None
+                        else "NCCL tile gather"),
                        "l2": "per-frame working set (ray state, lists, framebuffer) > 126 MB L2; weights L2-resident"},
             "fps": 1000.0 / ms_per_frame,
             "frame": frame,

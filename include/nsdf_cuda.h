@@ -195,6 +195,18 @@ int nsdf_cuda_get_mode(nsdf_ctx* ctx, int* mode);
 /* Bind the context to an existing cudaStream_t (NULL restores the context's own). */
 int nsdf_cuda_set_stream(nsdf_ctx* ctx, void* stream);
 int nsdf_cuda_synchronize(nsdf_ctx* ctx);
+/* Device memory shared between the processes of one node (the multi-GPU scheduler's peer
+ * framebuffer: every rank's shading kernels store their tile pixels straight into rank 0's
+ * framebuffer over NVLink).  alloc/free: cudaMalloc on the context's device; ipc_export:
+ * a 64-byte cudaIpcMemHandle of an nsdf_cuda_alloc pointer; ipc_open: map it in this process
+ * (peer access enabled lazily); memcpy: any direction (cudaMemcpyDefault), synchronous on
+ * the context stream. */
+int nsdf_cuda_alloc(nsdf_ctx* ctx, size_t bytes, void** out);
+int nsdf_cuda_free(nsdf_ctx* ctx, void* ptr);
+int nsdf_cuda_ipc_export(nsdf_ctx* ctx, void* ptr, uint8_t* handle64);
+int nsdf_cuda_ipc_open(nsdf_ctx* ctx, const uint8_t* handle64, void** out);
+int nsdf_cuda_ipc_close(nsdf_ctx* ctx, void* ptr);
+int nsdf_cuda_memcpy(nsdf_ctx* ctx, void* dst, const void* src, size_t bytes);
 /* Enable / disable per-kernel-family CUDA-event timing (resets the accumulators). */
 int nsdf_cuda_set_profiling(nsdf_ctx* ctx, int enable);
 int nsdf_cuda_get_profile(nsdf_ctx* ctx, nsdf_profile* out);

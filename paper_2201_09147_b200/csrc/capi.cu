@@ -437,6 +437,56 @@ int nsdf_cuda_synchronize(nsdf_ctx* c) {
   return NSDF_OK;
 }
 
+// ---- device memory shared across the ranks of a node (peer framebuffers) ----
+int nsdf_cuda_alloc(nsdf_ctx* c, size_t bytes, void** out) {
+  if (!c || !out) return fail(NSDF_ERR_CONTRACT, "null argument");
+  DeviceGuard g(c->device);
+  *out = nullptr;
+  NSDF_CUDA(cudaMalloc(out, bytes ? bytes : 1));
+  return NSDF_OK;
+}
+
+int nsdf_cuda_free(nsdf_ctx* c, void* p) {
+  if (!c) return fail(NSDF_ERR_CONTRACT, "context is null");
+  DeviceGuard g(c->device);
+  if (p) NSDF_CUDA(cudaFree(p));
+  return NSDF_OK;
+}
+
+int nsdf_cuda_ipc_export(nsdf_ctx* c, void* p, uint8_t* handle) {
+  if (!c || !p || !handle) return fail(NSDF_ERR_CONTRACT, "null argument");
+  DeviceGuard g(c->device);
+  cudaIpcMemHandle_t h;
+  NSDF_CUDA(cudaIpcGetMemHandle(&h, p));
+  std::memcpy(handle, &h, sizeof(h));
+  return NSDF_OK;
+}
+
+int nsdf_cuda_ipc_open(nsdf_ctx* c, const uint8_t* handle, void** out) {
+  if (!c || !handle || !out) return fail(NSDF_ERR_CONTRACT, "null argument");
+  DeviceGuard g(c->device);
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle, sizeof(h));
+  *out = nullptr;
+  NSDF_CUDA(cudaIpcOpenMemHandle(out, h, cudaIpcMemLazyEnablePeerAccess));
+  return NSDF_OK;
+}
+
+int nsdf_cuda_ipc_close(nsdf_ctx* c, void* p) {
+  if (!c) return fail(NSDF_ERR_CONTRACT, "context is null");
+  DeviceGuard g(c->device);
+  if (p) NSDF_CUDA(cudaIpcCloseMemHandle(p));
+  return NSDF_OK;
+}
+
+int nsdf_cuda_memcpy(nsdf_ctx* c, void* dst, const void* src, size_t bytes) {
+  if (!c || (!dst && bytes) || (!src && bytes)) return fail(NSDF_ERR_CONTRACT, "null argument");
+  DeviceGuard g(c->device);
+  NSDF_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, c->stream));
+  NSDF_CUDA(cudaStreamSynchronize(c->stream));
+  return NSDF_OK;
+}
+
 int nsdf_cuda_set_profiling(nsdf_ctx* c, int enable) {
   if (!c) return fail(NSDF_ERR_CONTRACT, "context is null");
   std::lock_guard<std::mutex> lk(c->mu);

@@ -62,6 +62,33 @@ class Context:
     def set_profiling(self, on: bool):
         check(self.lib.nsdf_cuda_set_profiling(self._ctx, int(bool(on))))
 
+    # ---- device memory shared across processes (peer framebuffers) ------------------------
+    def alloc(self, nbytes: int) -> int:
+        p = ctypes.c_void_p()
+        check(self.lib.nsdf_cuda_alloc(self._ctx, ctypes.c_size_t(nbytes), ctypes.byref(p)))
+        return int(p.value)
+
+    def free(self, ptr: int):
+        check(self.lib.nsdf_cuda_free(self._ctx, ctypes.c_void_p(ptr)))
+
+    def ipc_export(self, ptr: int) -> bytes:
+        h = (ctypes.c_uint8 * 64)()
+        check(self.lib.nsdf_cuda_ipc_export(self._ctx, ctypes.c_void_p(ptr), h))
+        return bytes(h)
+
+    def ipc_open(self, handle: bytes) -> int:
+        h = (ctypes.c_uint8 * 64).from_buffer_copy(handle)
+        p = ctypes.c_void_p()
+        check(self.lib.nsdf_cuda_ipc_open(self._ctx, h, ctypes.byref(p)))
+        return int(p.value)
+
+    def ipc_close(self, ptr: int):
+        check(self.lib.nsdf_cuda_ipc_close(self._ctx, ctypes.c_void_p(ptr)))
+
+    def memcpy(self, dst: int, src: int, nbytes: int):
+        check(self.lib.nsdf_cuda_memcpy(self._ctx, ctypes.c_void_p(dst), ctypes.c_void_p(src),
+                                        ctypes.c_size_t(nbytes)))
+
     def get_profile(self) -> "abi.Profile":
         p = abi.Profile()
         check(self.lib.nsdf_cuda_get_profile(self._ctx, ctypes.byref(p)))

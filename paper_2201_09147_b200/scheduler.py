@@ -4,8 +4,13 @@ One process per GPU (torchrun), torch.distributed for the plumbing.  The only co
 are the ones the north star names:
   * broadcast_sequence: rank 0 reads the .nest/.sdfnet files and broadcasts the packed
     weights once (one NCCL broadcast of a float64 buffer + the small metadata);
-  * TileGather: every rank renders the image tiles t with t % world == rank
-    (nsdf_cuda_render_device) and rank 0 gathers the packed tile pixels (one NCCL gather).
+  * PeerFramebuffer (default): rank 0 owns a ring of framebuffers mapped into every rank
+    (CUDA IPC); every rank renders the image tiles t with t % world == rank
+    (nsdf_cuda_render_device) and its shading kernels store those pixels straight into rank
+    0's framebuffer over NVLink — the gather is fused into the producing kernels; one 4-byte
+    NCCL all-reduce per frame orders the frame's completion across the ranks;
+  * TileGather (fallback when peer mapping is unavailable): rank 0 gathers the packed tile
+    pixels with one NCCL gather.
 Per-ray work is independent and partition-invariant (trace.hpp:69-70), so the
 gathered frame is identical to a single-GPU render.  The host logic here is covered on
 the CPU with gloo (tests/test_scheduler.py).
@@ -119,3 +124,74 @@ class TileGather:
     def to_host(self):
         """D2H of the assembled frame on rank 0 (the e2e read-back)."""
         return self.rgb.cpu(), self.depth.cpu(), self.mask.cpu()
+
+
+class PeerFramebuffer:
+    """A ring of framebuffers owned by rank 0 and mapped into every rank (CUDA IPC), so each
+    rank's render kernels write their tiles' pixels directly into rank 0's memory (NVLink peer
+    stores).  `ptrs(b)` = (rgb, depth, mask) device pointers of ring slot b in this process.
+    `ok` is False (and the caller falls back to TileGather) unless every rank mapped the
+    ring and a probe written by every rank reached rank 0."""
+
+    def __init__(self, ctx, width: int, height: int, n_buffers: int, rank: int, world: int):
+        import torch
+        import torch.distributed as dist
+
+        self.ctx, self.rank, self.world = ctx, rank, world
+        n = width * height
+        al = lambda b: (b + 255) // 256 * 256  # noqa: E731
+        self.off = (0, al(12 * n), al(12 * n) + al(4 * n))
+        self.size = self.off[2] + al(n)
+        self.n = n
+        self.bases, self.local = [], rank == 0
+        handles = [None]
+        err = ""
+        try:
+            if rank == 0:
+                self.bases = [ctx.alloc(self.size) for _ in range(n_buffers)]
+                handles = [[ctx.ipc_export(b) for b in self.bases]]
+        except Exception as e:  # reported through the probe verdict
+            err = f"rank 0: {e}"
+        dist.broadcast_object_list(handles, src=0)
+        try:
+            if rank != 0 and handles[0] is not None:
+                self.bases = [ctx.ipc_open(h) for h in handles[0]]
+        except Exception as e:
+            err = f"rank {rank}: {e}"
+        # probe: every rank writes its rank id into its own 16 bytes of slot 0's mask plane
+        dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend() == "nccl" else "cpu"
+        ok = torch.tensor([0 if err or not self.bases else 1], dtype=torch.int32, device=dev)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        self.ok = bool(ok.item())
+        if self.ok:
+            marker = (np.full(16, rank + 1, np.uint8))
+            self.ctx.memcpy(self.bases[0] + self.off[2] + 16 * rank, marker.ctypes.data, 16)
+            dist.barrier()
+            good = 1
+            if rank == 0:
+                got = np.zeros(16 * world, np.uint8)
+                self.ctx.memcpy(got.ctypes.data, self.bases[0] + self.off[2], 16 * world)
+                good = int(all((got[16 * r:16 * r + 16] == r + 1).all() for r in range(world)))
+            ok = torch.tensor([good], dtype=torch.int32, device=ok.device)
+            dist.broadcast(ok, src=0)
+            self.ok = bool(ok.item())
+        self.reason = err or ("" if self.ok else "peer probe failed")
+
+    def ptrs(self, b: int):
+        base = self.bases[b % len(self.bases)]
+        return base + self.off[0], base + self.off[1], base + self.off[2]
+
+    def to_host(self, b: int, rgb_h: int, depth_h: int, mask_h: int):
+        """Rank 0: copy ring slot b into host buffers (raw pointers)."""
+        r, d, m = self.ptrs(b)
+        self.ctx.memcpy(rgb_h, r, 12 * self.n)
+        self.ctx.memcpy(depth_h, d, 4 * self.n)
+        self.ctx.memcpy(mask_h, m, self.n)
+
+    def close(self):
+        for b in self.bases:
+            try:
+                (self.ctx.free if self.local else self.ctx.ipc_close)(b)
+            except Exception:
+                pass
+        self.bases = []

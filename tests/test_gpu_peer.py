@@ -1,0 +1,84 @@
+"""GPU: the N>1 frame assembly through peer stores (scheduler.PeerFramebuffer, bench.py's
+default for tile-sharded frames).  Two processes on one GPU, host sync over gloo: rank 0
+owns the framebuffer ring and exports it (CUDA IPC), rank 1 maps it and renders its tiles
+straight into rank 0's memory, rank 0 renders its own tiles into the same slot.  The kernels
+of the two ranks never wait on each other (each rank synchronizes its own stream, then a
+host barrier).  The assembled slot must equal the single-process frame bit for bit."""
+import os
+import tempfile
+
+import numpy as np
+import pytest
+
+from conftest import ASSETS, ROOT
+
+pytestmark = pytest.mark.gpu
+
+NEST = os.path.join(ASSETS, "torus_w30.nest")
+W, H = 200, 120
+
+
+def _render_args():
+    from paper_2201_09147_b200.abi import ShadeConfig, TraceConfig, standard_camera
+    return standard_camera(W, H), TraceConfig((20, 5, 5)), ShadeConfig(specular=0.3)
+
+
+def _worker(rank, world, port, mode, tile, out_path):
+    import sys
+    sys.path.insert(0, ROOT)
+    import torch
+    import torch.distributed as dist
+    from paper_2201_09147_b200.engine import Context, DeviceSequence
+    from paper_2201_09147_b200.manifest import load_manifest
+    from paper_2201_09147_b200.scheduler import PeerFramebuffer
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    ctx = Context(0, mode)
+    ds = DeviceSequence(ctx, load_manifest(NEST))
+    cam, cfg, shade = _render_args()
+    pf = PeerFramebuffer(ctx, W, H, 2, rank, world)
+    assert pf.ok, pf.reason
+    for slot in range(2):  # two frames through the ring
+        ctx.render_device(ds.levels(), cam, cfg, shade, *pf.ptrs(slot), tile_size=tile, tile_rank=rank,
+                          tile_world=world)
+        ctx.synchronize()
+    dist.barrier()
+    if rank == 0:
+        n = W * H
+        res = []
+        for slot in range(2):
+            rgb = np.empty(3 * n, np.float32)
+            depth = np.empty(n, np.float32)
+            mask = np.empty(n, np.uint8)
+            pf.to_host(slot, rgb.ctypes.data, depth.ctypes.data, mask.ctypes.data)
+            res += [rgb, depth, mask]
+        np.savez(out_path, *res)
+    dist.barrier()
+    pf.close()
+    dist.barrier()
+    ctx.close()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("mode", ["fp32", "fp16"])
+@pytest.mark.parametrize("tile", [32, 16])
+def test_peer_framebuffer_assembles_the_frame(mode, tile):
+    import torch.multiprocessing as mp
+    from paper_2201_09147_b200.engine import Context, DeviceSequence
+    from paper_2201_09147_b200.manifest import load_manifest
+    if not os.path.exists(NEST):
+        pytest.skip("fixture missing")
+    out = tempfile.mktemp(suffix=".npz")
+    port = 29500 + (os.getpid() % 2000)
+    mp.start_processes(_worker, args=(2, port, mode, tile, out), nprocs=2, join=True, start_method="spawn")
+    got = np.load(out)
+    os.unlink(out)
+    ctx = Context(0, mode)
+    ref = ctx.render(DeviceSequence(ctx, load_manifest(NEST)).levels(), *_render_args())
+    ctx.close()
+    for slot in range(2):
+        rgb, depth, mask = (got[f"arr_{3 * slot + i}"] for i in range(3))
+        assert np.array_equal(mask, np.asarray(ref[2]).reshape(-1).astype(np.uint8))
+        assert np.array_equal(depth.view(np.uint32), np.asarray(ref[1], np.float32).reshape(-1).view(np.uint32))
+        assert np.array_equal(rgb.view(np.uint32), np.asarray(ref[0], np.float32).reshape(-1).view(np.uint32))

@@ -74,3 +74,100 @@ def test_gloo_world2_broadcast_and_gather():
     assert ok
     assert sums == [float(m.packed.sum()) for m in seq.members]
     assert deltas == list(seq.deltas)
+
+
+class _ShmCtx:
+    """Stand-in for engine.Context's shared-memory entry points on CPU: `alloc` is a POSIX
+    shared-memory block, the 'IPC handle' its name, `ipc_open` attaches it in the peer
+    process — so PeerFramebuffer's handle exchange, probe and verdict run unchanged."""
+
+    def __init__(self, fail_open=False):
+        from multiprocessing import shared_memory
+        self._sm, self.fail_open, self.blocks = shared_memory, fail_open, {}
+
+    def _addr(self, s):
+        import ctypes
+        a = ctypes.addressof(ctypes.c_char.from_buffer(s.buf))
+        self.blocks[a] = s
+        return a
+
+    def alloc(self, n):
+        return self._addr(self._sm.SharedMemory(create=True, size=n))
+
+    def ipc_export(self, p):
+        return self.blocks[p].name.encode().ljust(64, b"\0")
+
+    def ipc_open(self, h):
+        if self.fail_open:
+            raise RuntimeError("peer mapping refused")
+        return self._addr(self._sm.SharedMemory(name=h.rstrip(b"\0").decode()))
+
+    def memcpy(self, dst, src, n):
+        import ctypes
+        ctypes.memmove(dst, src, n)
+
+    def free(self, p):
+        self.blocks.pop(p).unlink()
+
+    def ipc_close(self, p):
+        self.blocks.pop(p)
+
+
+def _peer_worker(rank, world, port, fail, out):
+    import ctypes
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import sys
+    sys.path.insert(0, ROOT)
+    from paper_2201_09147_b200.scheduler import PeerFramebuffer, owned_pixels
+    W, H, T = 50, 30, 8
+    n = W * H
+    pf = PeerFramebuffer(_ShmCtx(fail_open=fail and rank == 1), W, H, 2, rank, world)
+    res = {"ok": pf.ok, "reason": pf.reason}
+    if pf.ok:
+        # each rank "renders" its tiles straight into rank 0's slot 1
+        r, d, m = pf.ptrs(1)
+        rgb = np.ctypeslib.as_array((ctypes.c_float * (3 * n)).from_address(r))
+        depth = np.ctypeslib.as_array((ctypes.c_float * n).from_address(d))
+        mask = np.ctypeslib.as_array((ctypes.c_uint8 * n).from_address(m))
+        idx = owned_pixels(W, H, T, rank, world)
+        rgb.reshape(-1, 3)[idx] = np.stack([idx, 2 * idx, 3 * idx], 1)
+        depth[idx] = idx * 0.5
+        mask[idx] = rank + 1
+        dist.barrier()
+        if rank == 0:
+            hr, hd, hm = np.empty(3 * n, np.float32), np.empty(n, np.float32), np.empty(n, np.uint8)
+            pf.to_host(1, hr.ctypes.data, hd.ctypes.data, hm.ctypes.data)
+            a = np.arange(n)
+            owner = np.empty(n, np.uint8)
+            for q in range(world):
+                owner[owned_pixels(W, H, T, q, world)] = q + 1
+            res["frame"] = bool(np.array_equal(hr.reshape(-1, 3)[:, 2], 3.0 * a) and
+                                np.array_equal(hd, a * 0.5) and np.array_equal(hm, owner))
+        del rgb, depth, mask
+        dist.barrier()
+    if rank == 0:
+        out.put(res)
+    dist.barrier()
+    pf.bases = []  # the shared blocks are released with the process
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("fail", [False, True])
+def test_gloo_world2_peer_framebuffer(fail):
+    """PeerFramebuffer over gloo: handles broadcast, probe verdict agreed by every rank, and
+    (when mapping works) both ranks' tiles assembled in rank 0's slot; a rank that cannot map
+    the ring makes every rank fall back (ok False with the reason)."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_peer_worker, args=(r, 2, port, fail, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    res = q.get(timeout=120)
+    for p in procs:
+        p.join(timeout=60)
+    if fail:
+        assert not res["ok"] and res["reason"]
+    else:
+        assert res["ok"] and res["frame"], res
