@@ -6,7 +6,8 @@
 //   layer 0              a K = 32 MMA: A0 = the point split into three fp16 parts (+ ones for
 //                        the bias), B0 = fp16 hi/lo parts of omega*W0 and omega*b0 (built per
 //                        CTA at launch) -> D0 = omega*(W0 p + b0) in TMEM
-//   hidden layers        D[128 x W] (fp32, TMEM) = A[128 x W] (fp16 hi/lo, SMEM) . W_l^T (fp16
+//   hidden layers        D[128 x W] (fp32, TMEM) = A[128 x W] (fp16 hi/lo, TMEM: written in
+//                        place over the previous layer's accumulator) . W_l^T (fp16
 //                        hi/lo): tcgen05.mma.cta_group::1.kind::f16, M=128 N=W K=16, three
 //                        terms per K step (split precision), issued by one thread; weights
 //                        SMEM-resident (64-wide) or streamed in 32-K chunks through a 2-stage
@@ -16,7 +17,8 @@
 //                        layer m+1 consumes block rows as the epilogue of layer m writes them
 //                        (kready mbarriers); accumulators alternate between two TMEM regions
 //   epilogue             tcgen05.ld 32x32b.x16 (one block ahead) -> one FFMA forms
-//                        omega*(z + b) in radians -> MUFU sine -> fp16 hi/lo -> next A;
+//                        omega*(z + b) in radians -> MUFU sine -> fp16 hi/lo -> tcgen05.st
+//                        into the block's own columns = the next layer's A;
 //                        tangent lanes multiply by omega*cos of their ray's value lane (warp
 //                        shuffle); the last hidden layer folds in the 1 x W output layer
 //   consumer             persistent trace (a whole level per launch, rows refilled from the
@@ -130,6 +132,24 @@ __device__ __forceinline__ void tmem_wait16(uint32_t (&r)[16]) {
                :
                : "memory");
 }
+// D[tmem] (+)= A[tmem] . B[smem]: the A operand read from tensor memory (128 lanes = rows,
+// K packed two fp16 per 32-bit column, 8 columns per K = 16 step).
+__device__ __forceinline__ void tc_mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                          uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate));
+}
+// Each lane writes 8 consecutive 32-bit columns of its own TMEM lane.
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, uint32_t w0, uint32_t w1, uint32_t w2, uint32_t w3,
+                                         uint32_t w4, uint32_t w5, uint32_t w6, uint32_t w7) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(w0),
+               "r"(w1), "r"(w2), "r"(w3), "r"(w4), "r"(w5), "r"(w6), "r"(w7)
+               : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 // UMMA shared-memory descriptor, K-major SWIZZLE_NONE (sm_100 version bit 46).
 __device__ __forceinline__ uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
   return uint64_t((saddr >> 4) & 0x3FFFu) | (uint64_t((lbo >> 4) & 0x3FFFu) << 16) |
@@ -246,10 +266,10 @@ __host__ __device__ inline size_t tc_weight_bytes(int W, int L, int terms, bool 
   return resident ? size_t(L - 2) * W * W * 2 * 2 : size_t(kStages) * W * kKC * 2 * nw;
 }
 
-__host__ __device__ inline size_t tc_smem_bytes(int W, int L, int terms, bool resident, bool persist) {
+__host__ __device__ inline size_t tc_smem_bytes(int W, int L, int terms, bool resident, bool persist, bool ta) {
   const int nw = terms == 3 ? 2 : 1;
   size_t b = 0;
-  b += size_t(kRows) * W * 2 * nw;
+  b += ta ? size_t(kRows) * kK0 * 2 : size_t(kRows) * W * 2 * nw;
   b += tc_weight_bytes(W, L, terms, resident);
   b += size_t(W) * kK0 * 2;
   b += size_t(L - 1) * W * 4;
@@ -260,7 +280,7 @@ __host__ __device__ inline size_t tc_smem_bytes(int W, int L, int terms, bool re
   return b + 128;  // alignment slack
 }
 
-__device__ inline TcSmem tc_carve(uint8_t* raw, int W, int L, int terms, bool resident, bool persist) {
+__device__ inline TcSmem tc_carve(uint8_t* raw, int W, int L, int terms, bool resident, bool persist, bool ta) {
   const int nw = terms == 3 ? 2 : 1;
   size_t off = 0;
   auto take = [&](size_t bytes, size_t align) {
@@ -270,8 +290,8 @@ __device__ inline TcSmem tc_carve(uint8_t* raw, int W, int L, int terms, bool re
     return p;
   };
   TcSmem s;
-  s.a = reinterpret_cast<__half*>(take(size_t(kRows) * W * 2, 128));
-  s.alo = reinterpret_cast<__half*>(take(nw == 2 ? size_t(kRows) * W * 2 : 0, 128));
+  s.a = reinterpret_cast<__half*>(take(size_t(kRows) * (ta ? kK0 : W) * 2, 128));
+  s.alo = reinterpret_cast<__half*>(take(nw == 2 && !ta ? size_t(kRows) * W * 2 : 0, 128));
   s.wst = reinterpret_cast<__half*>(take(tc_weight_bytes(W, L, terms, resident), 128));
   s.b0 = reinterpret_cast<__half*>(take(size_t(W) * kK0 * 2, 128));
   s.bias = reinterpret_cast<float*>(take(size_t(L - 1) * W * 4, 16));
@@ -415,7 +435,7 @@ enum PfStage : int { kPfNeed = 0, kPfListed = 1, kPfReady = 2 };
 //            list until it drains (sphere_trace_level, trace.cpp:61-84)
 // MMA layer m = 0 is layer 0 (K = 32, B0 resident), m = 1..L-2 the hidden layers; the
 // last hidden layer's epilogue folds in the 1 x W output layer.
-template <int W, bool kGrad, int kGroups, int kTerms, bool kResident, bool kPersist>
+template <int W, bool kGrad, int kGroups, int kTerms, bool kResident, bool kPersist, bool kTA>
 __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
                                   (W == 64 ? 4 : (kGroups > 2 ? 1 : 2))) tc_mlp_kernel(TcArgs a) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
@@ -423,7 +443,7 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
   constexpr int kThreads = 32 * kCtl + 128 * kGroups;
   const TcNet& net = a.net;
   const int L = net.n_layers;
-  const TcSmem sm = tc_carve(smem_raw, W, L, kTerms, kResident, kPersist);
+  const TcSmem sm = tc_carve(smem_raw, W, L, kTerms, kResident, kPersist, kTA);
   constexpr int kNW = kTerms == 3 ? 2 : 1;  // weight parts (hi [, lo])
   uint64_t* full = sm.bars;
   uint64_t* empty = sm.bars + kStages;
@@ -446,6 +466,12 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
   constexpr int kSub = W / kBlk / kGroups;
   static_assert(kSub <= kMaxSub, "kready barriers");
   constexpr uint32_t kTmemCols = 2 * W;
+  // kTA: the hidden layers' A operand lives in TMEM, written IN PLACE over the accumulator
+  // it is computed from: the epilogue reads D block b (16 fp32 columns of its lane), and
+  // stores the block's activations back into the same 16 columns as 8 columns of packed
+  // fp16 hi parts + 8 of lo parts, which is exactly K-block b of the next layer's A.  The
+  // next layer accumulates into the other region, so K streaming is unchanged and no SMEM
+  // holds A (no STS, no SMEM operand reads for A).
 
   const int n_items = (a.op == kOpEval || a.op == kOpNormalMap) ? a.k : *a.in_count;
   int my_tiles, claim = 1;
@@ -555,6 +581,7 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
         // ---- hidden layers, K-streamed behind the epilogue ----
         for (int h = 0; h < n_hidden; ++h) {
           const uint32_t d_tmem = tmem + uint32_t((h + 1) & 1) * W;
+          const uint32_t a_tmem = tmem + uint32_t(h & 1) * W;  // kTA: A in place of layer h's D
           uint32_t b_base = 0, lo_off = 0;
           int s = 0;
 #pragma unroll 1
@@ -578,14 +605,24 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
               }
             }
             const uint32_t aoff = uint32_t(blk * 2) * (kRows / 8) * 128, boff = uint32_t(ks * 2) * (W / 8) * 128;
-            const uint64_t ad = umma_desc(a_base + aoff, kRows * 16, 128);
             const uint64_t bd = umma_desc(b_base + boff, W * 16, 128);
-            tc_mma(d_tmem, ad, bd, idesc, blk != 0);
-            if (kTerms == 3) {  // split precision: + A_lo.W_hi + A_hi.W_lo
-              const uint64_t adl = umma_desc(alo_base + aoff, kRows * 16, 128);
-              const uint64_t bdl = umma_desc(b_base + lo_off + boff, W * 16, 128);
-              tc_mma(d_tmem, adl, bd, idesc, 1);
-              tc_mma(d_tmem, ad, bdl, idesc, 1);
+            if (kTA) {
+              const uint32_t at = a_tmem + uint32_t(blk * kBlk);
+              tc_mma_ts(d_tmem, at, bd, idesc, blk != 0);
+              if (kTerms == 3) {  // split precision: + A_lo.W_hi + A_hi.W_lo
+                const uint64_t bdl = umma_desc(b_base + lo_off + boff, W * 16, 128);
+                tc_mma_ts(d_tmem, at + 8, bd, idesc, 1);
+                tc_mma_ts(d_tmem, at, bdl, idesc, 1);
+              }
+            } else {
+              const uint64_t ad = umma_desc(a_base + aoff, kRows * 16, 128);
+              tc_mma(d_tmem, ad, bd, idesc, blk != 0);
+              if (kTerms == 3) {  // split precision: + A_lo.W_hi + A_hi.W_lo
+                const uint64_t adl = umma_desc(alo_base + aoff, kRows * 16, 128);
+                const uint64_t bdl = umma_desc(b_base + lo_off + boff, W * 16, 128);
+                tc_mma(d_tmem, adl, bd, idesc, 1);
+                tc_mma(d_tmem, ad, bdl, idesc, 1);
+              }
             }
             if (ks == 1) {
               if (!kResident) tc_commit(&empty[s]);  // frees the weight stage once these MMAs retire
@@ -695,6 +732,24 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
         const float zs = m == 0 ? 1.0f : net.omega * net.wscale[m - 1];
         const float dscale = zs;
         const uint32_t treg = taddr + uint32_t(m & 1) * W;
+        // sine epilogue of one 16-column block (value rows; tangent rows scale by omega cos)
+        auto activate = [&](const uint32_t (&r)[16], int cc, float (&v)[16]) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]);
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            if (kGrad) {
+              // the value row's pre-activation, broadcast to its 3 tangent rows; every lane
+              // issues ONE sine: sin(z) on the value row, cos(z) = sin(z + pi/2) on tangents
+              const float z = __shfl_sync(group_mask, fmaf(v[j], zs, bias[cc + j]), lane & ~3, 32);
+              const float r1 = fast_sin(chain == 0 ? z : z + kHalfPi);
+              // tangent rows: G = (W.G_prev) * omega cos(z); D carries the 2^k weight scale
+              v[j] = chain == 0 ? r1 : v[j] * (dscale * r1);
+            } else {
+              v[j] = fast_sin(fmaf(v[j], zs, bias[cc + j]));
+            }
+          }
+        };
         // TMEM loads software-pipelined one block ahead of the math
         uint32_t raw[2][16];
         tmem_issue16(treg + uint32_t(eg * kBlk), raw[0]);
@@ -705,22 +760,23 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
           tmem_wait16(raw[buf]);
           if (i + 1 < kSub) tmem_issue16(treg + uint32_t(cc + kGroups * kBlk), raw[buf ^ 1]);
           float v[16];
+          activate(raw[buf], cc, v);
+          if (kTA && !last) {
+            // in place: A block i of the next layer over the D columns just read
+            uint32_t hw[8];
 #pragma unroll
-          for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(raw[buf][j]);
+            for (int j = 0; j < 8; ++j) hw[j] = pack_half2(v[2 * j], v[2 * j + 1]);
+            tmem_st8(treg + uint32_t(cc), hw[0], hw[1], hw[2], hw[3], hw[4], hw[5], hw[6], hw[7]);
+            if (kTerms == 3) {
+              uint32_t lw[8];
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            if (kGrad) {
-              // the value row's pre-activation, broadcast to its 3 tangent rows; every lane
-              // issues ONE sine: sin(z) on the value row, cos(z) = sin(z + pi/2) on tangents
-              const float z = __shfl_sync(group_mask, fmaf(v[j], zs, bias[cc + j]), lane & ~3, 32);
-              const float r = fast_sin(chain == 0 ? z : z + kHalfPi);
-              // tangent rows: G = (W.G_prev) * omega cos(z); D carries the 2^k weight scale
-              v[j] = chain == 0 ? r : v[j] * (dscale * r);
-            } else {
-              v[j] = fast_sin(fmaf(v[j], zs, bias[cc + j]));
+              for (int j = 0; j < 8; ++j) lw[j] = pack_half2_lo(v[2 * j], v[2 * j + 1], hw[j]);
+              tmem_st8(treg + uint32_t(cc + 8), lw[0], lw[1], lw[2], lw[3], lw[4], lw[5], lw[6], lw[7]);
             }
-          }
-          if (!last) {
+            tmem_wait_st();
+            tc_fence_before();
+            mbar_arrive(&kready[i]);
+          } else if (!last) {
 #pragma unroll
             for (int j = 0; j < 16; j += 8) {
               const uint32_t h0 = pack_half2(v[j], v[j + 1]), h1 = pack_half2(v[j + 2], v[j + 3]),
@@ -838,7 +894,10 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
           break;
         }
         mark(15);
-        if (ew == 0 && lane == 0) mbar_arrive(tstart);  // control warps: one more tile
+        if (ew == 0 && lane == 0) {
+          mbar_arrive(tstart);  // control warps: one more tile
+          if (a.dbg) atomicAdd(reinterpret_cast<unsigned long long*>(a.dbg + 65 * 16 + 64 * 4), 1ull);
+        }
         const float p[3] = {px, py, pz};
         const float acc = eval_tile(p, slot >= 0);
         mark(11);
@@ -966,12 +1025,12 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
   }
 }
 
-template <int W, bool kGrad, int kTerms, bool kResident, bool kPersist>
+template <int W, bool kGrad, int kTerms, bool kResident, bool kPersist, bool kTA>
 bool launch_w(TcArgs& a, int n_max_items, cudaStream_t s) {
   constexpr int kGroups = W == 64 ? 1 : (W == 256 && kTerms == 3 ? 4 : 2);
   constexpr int kThreads = 32 * (kResident ? 1 : 2) + 128 * kGroups;
-  auto kernel = tc_mlp_kernel<W, kGrad, kGroups, kTerms, kResident, kPersist>;
-  const size_t smem = tc_smem_bytes(W, a.net.n_layers, kTerms, kResident, kPersist);
+  auto kernel = tc_mlp_kernel<W, kGrad, kGroups, kTerms, kResident, kPersist, kTA>;
+  const size_t smem = tc_smem_bytes(W, a.net.n_layers, kTerms, kResident, kPersist, kTA);
   static size_t configured_smem = 0;
   static int per_sm = 0;
   static int sms = 0;
@@ -993,8 +1052,8 @@ bool launch_w(TcArgs& a, int n_max_items, cudaStream_t s) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     configured_smem = smem;
     if (getenv("NSDF_DEBUG_TC"))
-      fprintf(stderr, "tc_mlp_kernel<%d,%d,%d,%d,%d,%d>: smem %zu B, regs %d, %d CTAs/SM (occupancy API %d)\n", W,
-              int(kGrad), kGroups, kTerms, int(kResident), int(kPersist), smem, fa.numRegs, per_sm, occ);
+      fprintf(stderr, "tc_mlp_kernel<%d,%d,%d,%d,%d,%d,%d>: smem %zu B, regs %d, %d CTAs/SM (occupancy API %d)\n", W,
+              int(kGrad), kGroups, kTerms, int(kResident), int(kPersist), int(kTA), smem, fa.numRegs, per_sm, occ);
   }
   const int tmem_limit = 512 / (2 * W);  // two accumulator regions per CTA
   const int per = std::max(1, std::min(per_sm, tmem_limit));
@@ -1005,16 +1064,33 @@ bool launch_w(TcArgs& a, int n_max_items, cudaStream_t s) {
   return cudaGetLastError() == cudaSuccess;
 }
 
+// NSDF_TC_TMEM_A: bit w/64 selects the TMEM-resident A operand for width w (1 = 64,
+// 2 = 128, 4 = 256); default all (0 = the SMEM A operand everywhere, for comparison).
+int tmem_a_mask() {
+  static const int v = [] {
+    const char* e = getenv("NSDF_TC_TMEM_A");
+    return e ? atoi(e) : 7;
+  }();
+  return v;
+}
+
 template <bool kGrad, int kTerms, bool kPersist>
 bool launch_terms(TcArgs& a, int n_max_items, cudaStream_t s) {
   // 64-wide nets keep every hidden layer resident in SMEM when it fits (<= 4 layers).
   const bool resident = a.net.width == 64 && a.net.n_layers - 2 <= 4;
+  const bool ta = (tmem_a_mask() & (a.net.width / 64)) != 0;
   switch (a.net.width) {
     case 64:
-      return resident ? launch_w<64, kGrad, kTerms, true, kPersist>(a, n_max_items, s)
-                      : launch_w<64, kGrad, kTerms, false, kPersist>(a, n_max_items, s);
-    case 128: return launch_w<128, kGrad, kTerms, false, kPersist>(a, n_max_items, s);
-    case 256: return launch_w<256, kGrad, kTerms, false, kPersist>(a, n_max_items, s);
+      if (resident)
+        return ta ? launch_w<64, kGrad, kTerms, true, kPersist, true>(a, n_max_items, s)
+                  : launch_w<64, kGrad, kTerms, true, kPersist, false>(a, n_max_items, s);
+      return launch_w<64, kGrad, kTerms, false, kPersist, false>(a, n_max_items, s);
+    case 128:
+      return ta ? launch_w<128, kGrad, kTerms, false, kPersist, true>(a, n_max_items, s)
+                : launch_w<128, kGrad, kTerms, false, kPersist, false>(a, n_max_items, s);
+    case 256:
+      return ta ? launch_w<256, kGrad, kTerms, false, kPersist, true>(a, n_max_items, s)
+                : launch_w<256, kGrad, kTerms, false, kPersist, false>(a, n_max_items, s);
     default: return false;
   }
 }
@@ -1022,7 +1098,10 @@ bool launch_terms(TcArgs& a, int n_max_items, cudaStream_t s) {
 long long* timeline_buffer() {
   static long long* buf = nullptr;
   if (!getenv("NSDF_TC_TIMELINE")) return nullptr;
-  if (!buf) cudaMallocManaged(&buf, (65 * 16 + 64 * 4) * sizeof(long long));
+  if (!buf) {
+    cudaMallocManaged(&buf, (65 * 16 + 64 * 4 + 1) * sizeof(long long));
+    cudaMemset(buf, 0, (65 * 16 + 64 * 4 + 1) * sizeof(long long));
+  }
   return buf;
 }
 void timeline_dump(long long* buf, const char* what) {
@@ -1046,7 +1125,8 @@ void timeline_dump(long long* buf, const char* what) {
     fprintf(stderr, "  MMA issuer tile %2d: waits A0 %6lld, A blocks %6lld, weights %6lld of %6lld cycles\n", t, q[0],
             q[1], q[2], q[3]);
   }
-  cudaMemset(buf, 0, (65 * 16 + 64 * 4) * sizeof(long long));
+  fprintf(stderr, "  tiles (all CTAs): %lld\n", buf[65 * 16 + 64 * 4]);
+  cudaMemset(buf, 0, (65 * 16 + 64 * 4 + 1) * sizeof(long long));
 }
 
 uint32_t suspend_hint() {
