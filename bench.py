@@ -377,16 +377,25 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    # NSDF_BENCH_ONE_GPU=1: plumbing check of the N > 1 path on a one-GPU box — every rank on
+    # cuda:0, host sync over gloo (no rank's kernels wait on another's).  Not a measurement.
+    one_gpu = world > 1 and os.environ.get("NSDF_BENCH_ONE_GPU") == "1"
+    if one_gpu:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if one_gpu:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     from paper_2201_09147_b200.abi import ShadeConfig, TraceConfig, standard_camera
     from paper_2201_09147_b200.engine import Context, DeviceSequence
     from paper_2201_09147_b200 import scheduler
 
     cfgw = args.cfg
-    seq = scheduler.broadcast_sequence(cfgw["manifest"] if rank == 0 else None, world, rank)
+    seq = scheduler.broadcast_sequence(cfgw["manifest"] if rank == 0 else None, world, rank,
+                                       device="cpu" if one_gpu else None)
     seq = seq.subsequence(cfgw["members"])
     Wd, Hd = args.width, args.height
     npix = Wd * Hd

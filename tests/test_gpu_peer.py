@@ -82,3 +82,29 @@ def test_peer_framebuffer_assembles_the_frame(mode, tile):
         assert np.array_equal(mask, np.asarray(ref[2]).reshape(-1).astype(np.uint8))
         assert np.array_equal(depth.view(np.uint32), np.asarray(ref[1], np.float32).reshape(-1).view(np.uint32))
         assert np.array_equal(rgb.view(np.uint32), np.asarray(ref[0], np.float32).reshape(-1).view(np.uint32))
+
+
+def test_bench_two_ranks_plumbing():
+    """bench.py's N > 1 path end to end (torchrun, 2 ranks, peer framebuffer, e2e to host)
+    with both ranks on this one GPU over gloo (NSDF_BENCH_ONE_GPU=1): the JSON line carries
+    the contract keys and reports the peer assembly.  Plumbing only — not a measurement."""
+    import json
+    import socket
+    import subprocess
+    import sys
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    env = dict(os.environ, NSDF_BENCH_ONE_GPU="1")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                        "--master-addr", "127.0.0.1", "--master-port", str(port), "bench.py", "--gpus", "2",
+                        "--steps", "4", "--warmup", "3", "--no-cpu-baseline", "--no-alt"],
+                       cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "e2e", "roofline", "clocks"):
+        assert k in line
+    assert line["n_gpus"] == 2 and line["value"] > 0 and line["e2e"]["value"] > 0
+    assert line["config"]["parallelism"] == "tiles2"
+    assert line["config"]["frame_assembly"].startswith("peer")
