@@ -33,8 +33,10 @@
 // descriptor SBO = 128 B (next 8 rows), LBO = R*16 B (next 8 k).
 #include <cuda_fp16.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <vector>
 
 #include "device_ops.cuh"
 #include "mlp_tc.cuh"
@@ -49,6 +51,19 @@ constexpr int kStages = 2;
 constexpr int kBlk = 16;     // columns per epilogue block = K per MMA step
 constexpr int kMaxSub = 8;   // max blocks per column group per layer (kready barriers)
 constexpr float kHalfPi = 1.5707963267948966f;
+// debug timeline buffer (NSDF_TC_TIMELINE): tile marks of CTA 0, MMA issuer waits, tile
+// count, then per CTA: globaltimer at start and end, tiles run
+constexpr int kDbgTiles = 65 * 16 + 64 * 4;
+constexpr int kDbgCta = kDbgTiles + 8;
+constexpr int kDbgMaxCta = 2048;
+constexpr int kDbgTileT = kDbgCta + 5 * kDbgMaxCta;  // CTA 0: clock64 at each tile's start
+constexpr int kDbgMaxTiles = 2048;
+constexpr int kDbgSize = kDbgTileT + kDbgMaxTiles;
+__device__ __forceinline__ long long global_ns() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 // ---- PTX wrappers ---------------------------------------------------------------------
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
@@ -532,6 +547,10 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *sm.tmem_base;
+  if (a.dbg && threadIdx.x == 0 && blockIdx.x < kDbgMaxCta) {
+    a.dbg[kDbgCta + 5 * blockIdx.x] = global_ns();
+    a.dbg[kDbgCta + 5 * blockIdx.x + 3] = clock64();
+  }
 
   // Control warps' tile loop: a fixed tile count, or (persistent) one tstart phase per tile
   // published by the epilogue, with the done flag ending the loop.
@@ -680,6 +699,8 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
     // groups' partials are combined through SMEM).
     int dbg_t = 0;
     auto mark = [&](int k) {
+      if (a.dbg && blockIdx.x == 0 && ew == 0 && lane == 0 && k == 0 && dbg_t < kDbgMaxTiles)
+        a.dbg[kDbgTileT + dbg_t] = clock64();
       if (a.dbg && blockIdx.x == 0 && ew == 0 && lane == 0 && dbg_t < 64) a.dbg[dbg_t * 16 + k] = clock64();
     };
     auto eval_tile = [&](const float* p, bool live) -> float {
@@ -896,7 +917,10 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
         mark(15);
         if (ew == 0 && lane == 0) {
           mbar_arrive(tstart);  // control warps: one more tile
-          if (a.dbg) atomicAdd(reinterpret_cast<unsigned long long*>(a.dbg + 65 * 16 + 64 * 4), 1ull);
+          if (a.dbg) {
+            atomicAdd(reinterpret_cast<unsigned long long*>(a.dbg + kDbgTiles), 1ull);
+            if (blockIdx.x < kDbgMaxCta) ++a.dbg[kDbgCta + 5 * blockIdx.x + 2];
+          }
         }
         const float p[3] = {px, py, pz};
         const float acc = eval_tile(p, slot >= 0);
@@ -1016,6 +1040,10 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
     }
   }
   // ---- teardown ----
+  if (a.dbg && threadIdx.x == 0 && blockIdx.x < kDbgMaxCta) {
+    a.dbg[kDbgCta + 5 * blockIdx.x + 1] = global_ns();
+    a.dbg[kDbgCta + 5 * blockIdx.x + 4] = clock64();
+  }
   tc_fence_before();
   __syncthreads();
   if (warp == 0) {
@@ -1099,8 +1127,8 @@ long long* timeline_buffer() {
   static long long* buf = nullptr;
   if (!getenv("NSDF_TC_TIMELINE")) return nullptr;
   if (!buf) {
-    cudaMallocManaged(&buf, (65 * 16 + 64 * 4 + 1) * sizeof(long long));
-    cudaMemset(buf, 0, (65 * 16 + 64 * 4 + 1) * sizeof(long long));
+    cudaMallocManaged(&buf, kDbgSize * sizeof(long long));
+    cudaMemset(buf, 0, kDbgSize * sizeof(long long));
   }
   return buf;
 }
@@ -1125,8 +1153,45 @@ void timeline_dump(long long* buf, const char* what) {
     fprintf(stderr, "  MMA issuer tile %2d: waits A0 %6lld, A blocks %6lld, weights %6lld of %6lld cycles\n", t, q[0],
             q[1], q[2], q[3]);
   }
-  fprintf(stderr, "  tiles (all CTAs): %lld\n", buf[65 * 16 + 64 * 4]);
-  cudaMemset(buf, 0, (65 * 16 + 64 * 4 + 1) * sizeof(long long));
+  fprintf(stderr, "  tiles (all CTAs): %lld\n", buf[kDbgTiles]);
+  // per-CTA spans (globaltimer): how long the level's tail keeps part of the GPU busy
+  long long t0 = 0, t1 = 0;
+  int n = 0;
+  std::vector<long long> ends;
+  std::vector<long long> tiles;
+  double cyc = 0, nsec = 0;
+  for (int c = 0; c < kDbgMaxCta; ++c) {
+    const long long* q = buf + kDbgCta + 5 * c;
+    if (!q[0]) continue;
+    if (!n || q[0] < t0) t0 = q[0];
+    t1 = std::max(t1, q[1]);
+    ends.push_back(q[1]);
+    tiles.push_back(q[2]);
+    cyc += double(q[4] - q[3]);
+    nsec += double(q[1] - q[0]);
+    ++n;
+  }
+  if (n) {
+    std::sort(ends.begin(), ends.end());
+    std::sort(tiles.begin(), tiles.end());
+    auto pe = [&](double f) { return (ends[std::min(n - 1, int(f * n))] - t0) / 1000.0; };
+    fprintf(stderr, "  CTAs %d: span %.1f us; CTA end p10 %.1f p50 %.1f p90 %.1f max %.1f us; tiles/CTA min %lld "
+            "p50 %lld max %lld; SM clock over the CTAs' lifetimes %.0f MHz\n", n, (t1 - t0) / 1000.0, pe(0.1), pe(0.5),
+            pe(0.9), pe(1.0), tiles[0], tiles[n / 2], tiles[n - 1], nsec > 0 ? cyc / nsec * 1000.0 : 0.0);
+  }
+  {  // CTA 0's tile durations over the whole launch, in eighths of its tile sequence
+    int nt = 0;
+    while (nt < kDbgMaxTiles && buf[kDbgTileT + nt]) ++nt;
+    if (nt > 16) {
+      fprintf(stderr, "  CTA 0: %d tiles, mean cycles per tile by eighth of the launch:", nt);
+      for (int e = 0; e < 8; ++e) {
+        const int a0 = e * (nt - 1) / 8, a1 = (e + 1) * (nt - 1) / 8;
+        fprintf(stderr, " %lld", a1 > a0 ? (buf[kDbgTileT + a1] - buf[kDbgTileT + a0]) / (a1 - a0) : 0ll);
+      }
+      fprintf(stderr, "\n");
+    }
+  }
+  cudaMemset(buf, 0, kDbgSize * sizeof(long long));
 }
 
 uint32_t suspend_hint() {

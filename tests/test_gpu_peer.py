@@ -97,6 +97,7 @@ def test_bench_two_ranks_plumbing():
     port = s.getsockname()[1]
     s.close()
     env = dict(os.environ, NSDF_BENCH_ONE_GPU="1")
+    env.pop("NSDF_MODE", None)  # conftest's oracle-mode default is not a bench --mode
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
                         "--master-addr", "127.0.0.1", "--master-port", str(port), "bench.py", "--gpus", "2",
                         "--steps", "4", "--warmup", "3", "--no-cpu-baseline", "--no-alt"],
