@@ -58,7 +58,10 @@ def build_cuda(force=False, verbose=False):
     deps_common = _headers(CSRC) + [os.path.join(INC, "nsdf_cuda.h")]
     jobs = []
     objs = []
+    timeline = os.environ.get("NSDF_TC_TIMELINE_BUILD") == "1"  # tools/timeline.py instrumentation
     for src, extra in CUDA_SOURCES.items():
+        if timeline and src == "mlp_tc.cu":
+            extra = extra + ["-DNSDF_TC_TIMELINE_BUILD=1"]
         s = os.path.join(CSRC, src)
         o = os.path.join(OBJ, src + ".o")
         objs.append(o)

@@ -53,6 +53,12 @@ constexpr int kMaxSub = 8;   // max blocks per column group per layer (kready ba
 constexpr float kHalfPi = 1.5707963267948966f;
 // debug timeline buffer (NSDF_TC_TIMELINE): tile marks of CTA 0, MMA issuer waits, tile
 // count, then per CTA: globaltimer at start and end, tiles run
+// Compiled in only with -DNSDF_TC_TIMELINE_BUILD=1 (build.py: env NSDF_TC_TIMELINE_BUILD=1):
+// even never-taken instrumentation branches cost ~3% in the tile loops.
+#ifndef NSDF_TC_TIMELINE_BUILD
+#define NSDF_TC_TIMELINE_BUILD 0
+#endif
+constexpr bool kTimeline = NSDF_TC_TIMELINE_BUILD != 0;
 constexpr int kDbgTiles = 65 * 16 + 64 * 4;
 constexpr int kDbgCta = kDbgTiles + 8;
 constexpr int kDbgMaxCta = 2048;
@@ -246,6 +252,7 @@ struct TcArgs {
   const float* fallback;
   unsigned long long* counts;
   long long* dbg;  // debug timeline (NSDF_TC_TIMELINE): CTA 0, epilogue thread 0
+  int dbg_skip;    // first tile recorded (NSDF_TC_TIMELINE_SKIP)
 };
 
 // Layer 0 runs on the tensor cores as a K = 32 MMA: each row's A0 holds its point split
@@ -375,6 +382,15 @@ __device__ __forceinline__ bool bar_vote_any(int id, int threads, bool pred) {
       : "r"(uint32_t(pred)), "r"(id), "r"(threads)
       : "memory");
   return r != 0;
+}
+// Claim ticket (the cursor counts claims): atom.inc, which the compiler cannot turn into a
+// warp-aggregated atomic.  An aggregated fetch-add broadcasts the old value with a shuffle
+// right after the atomic, putting the contended atomic's round trip on the critical path;
+// here the result is only waited for where it is used (claims run one reservation ahead).
+__device__ __forceinline__ int fetch_ticket(int* p) {
+  unsigned old;
+  asm volatile("atom.global.inc.u32 %0, [%1], %2;" : "=r"(old) : "l"(p), "r"(0x7fffffffu) : "memory");
+  return int(old);
 }
 // Position of the n-th (0-based) set bit of m (n < popc(m)).
 __device__ __forceinline__ int nth_set_bit(uint32_t m, int n) {
@@ -547,7 +563,7 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *sm.tmem_base;
-  if (a.dbg && threadIdx.x == 0 && blockIdx.x < kDbgMaxCta) {
+  if (kTimeline && a.dbg && threadIdx.x == 0 && blockIdx.x < kDbgMaxCta) {
     a.dbg[kDbgCta + 5 * blockIdx.x] = global_ns();
     a.dbg[kDbgCta + 5 * blockIdx.x + 3] = clock64();
   }
@@ -577,7 +593,7 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
       }
       uint32_t chunk_iter = 0, kr_phase = 0, a0_phase = 0;
       // debug timeline (NSDF_TC_TIMELINE): cycles the issuer waits for A0, A blocks, weights
-      const bool mdbg = a.dbg && blockIdx.x == 0;
+      const bool mdbg = kTimeline && a.dbg && blockIdx.x == 0;
       long long w_a0 = 0, w_k = 0, w_full = 0, t_loop = 0;
       auto timed_wait = [&](uint64_t* bar, uint32_t ph, long long& acc) {
         const long long c0 = mdbg ? clock64() : 0;
@@ -651,12 +667,12 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
           kr_phase ^= 1;
           tc_commit(dfull);  // accumulator complete
         }
-        if (mdbg && t < 64) {
+        if (mdbg && t >= a.dbg_skip && t - a.dbg_skip < 64) {
           t_loop = clock64() - tl0;
-          a.dbg[65 * 16 + t * 4 + 0] = w_a0;
-          a.dbg[65 * 16 + t * 4 + 1] = w_k;
-          a.dbg[65 * 16 + t * 4 + 2] = w_full;
-          a.dbg[65 * 16 + t * 4 + 3] = t_loop;
+          a.dbg[65 * 16 + (t - a.dbg_skip) * 4 + 0] = w_a0;
+          a.dbg[65 * 16 + (t - a.dbg_skip) * 4 + 1] = w_k;
+          a.dbg[65 * 16 + (t - a.dbg_skip) * 4 + 2] = w_full;
+          a.dbg[65 * 16 + (t - a.dbg_skip) * 4 + 3] = t_loop;
           w_a0 = w_k = w_full = 0;
         }
       }
@@ -699,9 +715,11 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
     // groups' partials are combined through SMEM).
     int dbg_t = 0;
     auto mark = [&](int k) {
-      if (a.dbg && blockIdx.x == 0 && ew == 0 && lane == 0 && k == 0 && dbg_t < kDbgMaxTiles)
+      if (kTimeline && a.dbg && blockIdx.x == 0 && ew == 0 && lane == 0 && k == 0 && dbg_t < kDbgMaxTiles)
         a.dbg[kDbgTileT + dbg_t] = clock64();
-      if (a.dbg && blockIdx.x == 0 && ew == 0 && lane == 0 && dbg_t < 64) a.dbg[dbg_t * 16 + k] = clock64();
+      if (kTimeline && a.dbg && blockIdx.x == 0 && ew == 0 && lane == 0 && dbg_t >= a.dbg_skip &&
+          dbg_t - a.dbg_skip < 64)
+        a.dbg[(dbg_t - a.dbg_skip) * 16 + k] = clock64();
     };
     auto eval_tile = [&](const float* p, bool live) -> float {
       mark(0);
@@ -837,13 +855,13 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
       const RayState& st = a.st;
       const StageList st_adv{sm.stage_buf, sm.stage_count};
       const uint32_t lt = (1u << lane) - 1u;
-      int slot = -1, it = 0, evals = 0;
+      int slot = -1, it = 0, evals = 0, n_tiles = 0;
       float px = 0.f, py = 0.f, pz = 0.f, t = 0.f, dx = 0.f, dy = 0.f, dz = 0.f;
       int pf_slot = -1, pf_stage = kPfNeed;
       float fpx = 0.f, fpy = 0.f, fpz = 0.f, fpt = 0.f, fdx = 0.f, fdy = 0.f, fdz = 0.f;
-      int res_base = 0, res_end = 0, nres = 0;  // claimed list range; next claim (lane 0)
+      int res_base = 0, res_end = 0, nres = 0;  // claimed list range; next claim ticket (lane 0)
       bool exhausted = false;
-      if (g0 && lane == 0) nres = atomicAdd(a.cursor, claim);
+      if (g0 && lane == 0) nres = fetch_ticket(a.cursor);
       // advance this warp's ray pipeline by one stage (group 0 only)
       auto refill = [&]() {
         // READY prefetches -> empty rows (the k-th empty row takes the k-th ready lane)
@@ -867,6 +885,7 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
           }
           if (pf_stage == kPfReady && __popc(rdy & lt) < k) pf_stage = kPfNeed;
         }
+        if (W == 64) mark(8);  // (64-wide: layer marks 6-9 are free) refill sub-steps
         // LISTED -> READY: the slot arrived last tile; issue the ray-state loads
         if (pf_stage == kPfListed) {
           fpx = __ldg(st.px + pf_slot);
@@ -878,17 +897,18 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
           fdz = __ldg(st.dz + pf_slot);
           pf_stage = kPfReady;
         }
+        if (W == 64) mark(9);
         // NEED -> LISTED: claim list items (warp claims of `claim` items, one claim ahead)
         uint32_t need = __ballot_sync(0xffffffffu, pf_stage == kPfNeed);
         while (need && !exhausted) {
           if (res_base == res_end) {
-            res_base = __shfl_sync(0xffffffffu, nres, 0);
+            res_base = __shfl_sync(0xffffffffu, nres, 0) * claim;
             if (res_base >= n_items) {
               exhausted = true;
               break;
             }
             res_end = min(res_base + claim, n_items);
-            if (lane == 0) nres = atomicAdd(a.cursor, claim);
+            if (lane == 0) nres = fetch_ticket(a.cursor);
           }
           const int k = min(__popc(need), res_end - res_base);
           const int r = __popc(need & lt);
@@ -917,10 +937,7 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
         mark(15);
         if (ew == 0 && lane == 0) {
           mbar_arrive(tstart);  // control warps: one more tile
-          if (a.dbg) {
-            atomicAdd(reinterpret_cast<unsigned long long*>(a.dbg + kDbgTiles), 1ull);
-            if (blockIdx.x < kDbgMaxCta) ++a.dbg[kDbgCta + 5 * blockIdx.x + 2];
-          }
+          ++n_tiles;
         }
         const float p[3] = {px, py, pz};
         const float acc = eval_tile(p, slot >= 0);
@@ -964,6 +981,10 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
       if (ew == 0 && lane == 0) {
         *reinterpret_cast<volatile int*>(sm.done) = 1;
         mbar_arrive(tstart);
+        if (kTimeline && a.dbg) {
+          atomicAdd(reinterpret_cast<unsigned long long*>(a.dbg + kDbgTiles), (unsigned long long)n_tiles);
+          if (blockIdx.x < kDbgMaxCta) a.dbg[kDbgCta + 5 * blockIdx.x + 2] = n_tiles;
+        }
       }
       if (g0) {
         stage_flush(st_adv, a.adv_list, a.adv_count, sm.stage_base, ctid, true);
@@ -1040,7 +1061,7 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
     }
   }
   // ---- teardown ----
-  if (a.dbg && threadIdx.x == 0 && blockIdx.x < kDbgMaxCta) {
+  if (kTimeline && a.dbg && threadIdx.x == 0 && blockIdx.x < kDbgMaxCta) {
     a.dbg[kDbgCta + 5 * blockIdx.x + 1] = global_ns();
     a.dbg[kDbgCta + 5 * blockIdx.x + 4] = clock64();
   }
@@ -1126,6 +1147,12 @@ bool launch_terms(TcArgs& a, int n_max_items, cudaStream_t s) {
 long long* timeline_buffer() {
   static long long* buf = nullptr;
   if (!getenv("NSDF_TC_TIMELINE")) return nullptr;
+  if (!kTimeline) {
+    static bool warned = false;
+    if (!warned) fprintf(stderr, "NSDF_TC_TIMELINE: rebuild with NSDF_TC_TIMELINE_BUILD=1 (instrumentation not compiled in)\n");
+    warned = true;
+    return nullptr;
+  }
   if (!buf) {
     cudaMallocManaged(&buf, kDbgSize * sizeof(long long));
     cudaMemset(buf, 0, kDbgSize * sizeof(long long));
@@ -1145,8 +1172,9 @@ void timeline_dump(long long* buf, const char* what) {
     auto d = [&](const long long* q, int k) { return q[k] ? q[k] - r[0] : -1; };
     fprintf(stderr, "  %2d: %6lld %6lld |", t, d(r, 10), d(r, 1));
     for (int k = 2; k < 10; ++k) fprintf(stderr, " %6lld", d(r, k));
-    fprintf(stderr, " | %6lld %6lld %6lld || %6lld %6lld %6lld\n", d(nx, 11), d(nx, 12), d(nx, 13), d(nx, 14),
-            d(nx, 15), nx[0] ? nx[0] - r[0] : -1);
+    fprintf(stderr, " | %6lld %6lld %6lld || %6lld %6lld %6lld [refill steps %lld %lld]\n", d(nx, 11), d(nx, 12),
+            d(nx, 13), d(nx, 14), d(nx, 15), nx[0] ? nx[0] - r[0] : -1, nx[8] ? nx[8] - r[0] : -1,
+            nx[9] ? nx[9] - r[0] : -1);
   }
   for (int t = 0; t < 12; ++t) {
     const long long* q = buf + 65 * 16 + t * 4;
@@ -1211,6 +1239,7 @@ bool launch_any(TcArgs& a, int n_max_items, cudaStream_t s) {
   }();
   a.claim_div = claim_div;
   a.dbg = timeline_buffer();
+  a.dbg_skip = getenv("NSDF_TC_TIMELINE_SKIP") ? std::max(0, atoi(getenv("NSDF_TC_TIMELINE_SKIP"))) : 0;
   if (a.dbg) {
     const bool ok = a.terms == 3 ? launch_terms<kGrad, 3, kPersist>(a, n_max_items, s)
                                  : launch_terms<kGrad, 1, kPersist>(a, n_max_items, s);

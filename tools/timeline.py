@@ -1,6 +1,8 @@
 """Per-tile timeline of CTA 0 of every tcgen05 launch of one config-2 frame (NSDF_TC_TIMELINE).
 
-    NSDF_TC_TIMELINE=1 python tools/timeline.py [width height]
+    NSDF_TC_TIMELINE_BUILD=1 python -c "from paper_2201_09147_b200 import build; build.build_cuda(force=True)"
+    NSDF_TC_TIMELINE=1 [NSDF_TC_TIMELINE_SKIP=first_tile] python tools/timeline.py [width height]
+(the instrumentation is compiled out of the normal build: rebuild without the variable after)
 Columns (SM cycles from the tile's start): A0 before its fence, A0 arrive | per MMA layer: the
 accumulator-complete wait returning, the epilogue's end | (trace) return, update, flush ||
 refill done, vote done, next tile's start.  Then, per tile, the MMA issuer's waits for A0,
