@@ -34,6 +34,7 @@
 #include <cuda_fp16.h>
 
 #include <algorithm>
+#include <type_traits>
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
@@ -85,36 +86,20 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(bar)), "r"(bytes)
                : "memory");
 }
-// mbarrier wait.  With a suspend-time hint (ns) the waiting warp may sleep in hardware
-// until the phase completes instead of spinning through SYNCS/YIELD/BRA; 0 = plain
-// try_wait loop.  Selected at launch (NSDF_TC_SUSPEND_NS, default below).
-constexpr uint32_t kBackoffNs = 0;
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity, uint32_t suspend_ns) {
+// mbarrier wait: a plain try_wait loop (a runtime-selectable suspend-time hint variant
+// cost 2.8% per frame: two loop bodies behind a branch at every wait).
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   uint32_t done = 0;
   const uint32_t a = smem_addr(bar);
-  if (suspend_ns) {
-    do {
-      asm volatile(
-          "{\n\t.reg .pred p;\n\t"
-          "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
-          "selp.u32 %0, 1, 0, p;\n\t}"
-          : "=r"(done)
-          : "r"(a), "r"(parity), "r"(suspend_ns)
-          : "memory");
-    } while (!done);
-  } else {
-    for (;;) {
-      asm volatile(
-          "{\n\t.reg .pred p;\n\t"
-          "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-          "selp.u32 %0, 1, 0, p;\n\t}"
-          : "=r"(done)
-          : "r"(a), "r"(parity)
-          : "memory");
-      if (done) break;
-      if (kBackoffNs) __nanosleep(kBackoffNs);
-    }
-  }
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(a), "r"(parity)
+        : "memory");
+  } while (!done);
 }
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -221,7 +206,6 @@ struct TcArgs {
   TcNet net;
   int op;
   int terms;  // 3 = split-fp16 (A_hi.W_hi + A_lo.W_hi + A_hi.W_lo), 1 = plain fp16
-  uint32_t suspend_ns;
   int claim_div;  // persistent trace: claim granularity = n / (grid * claim_div), clamped to [1, 32]
   // trace (persistent level)
   LevelDesc lv;
@@ -466,7 +450,7 @@ enum PfStage : int { kPfNeed = 0, kPfListed = 1, kPfReady = 2 };
 //            list until it drains (sphere_trace_level, trace.cpp:61-84)
 // MMA layer m = 0 is layer 0 (K = 32, B0 resident), m = 1..L-2 the hidden layers; the
 // last hidden layer's epilogue folds in the 1 x W output layer.
-template <int W, bool kGrad, int kGroups, int kTerms, bool kResident, bool kPersist, bool kTA>
+template <int W, bool kGrad, int kGroups, int kTerms, bool kResident, bool kPersist, bool kTA, int kHid>
 __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
                                   (W == 64 ? 4 : (kGroups > 2 ? 1 : 2))) tc_mlp_kernel(TcArgs a) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
@@ -484,7 +468,9 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
   uint64_t* tstart = sm.bars + 2 * kStages + kMaxSub + 2;
   float* part = sm.part;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n_hidden = L - 2;  // hidden (W x W) MMA layers
+  // hidden (W x W) MMA layers: compile-time for the standard architectures (kHid > 0), so
+  // the layer loops unroll and every per-layer constant folds
+  const int n_hidden = kHid > 0 ? kHid : L - 2;
   constexpr int kRaysPerTile = kGrad ? kRows / 4 : kRows;
   constexpr int kChunks = W / kKC;
   constexpr uint32_t kChunkBytes = uint32_t(W) * kKC * 2;
@@ -573,7 +559,7 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
   uint32_t ts_phase = 0;
   auto more_tiles = [&](int t) -> bool {
     if (!kPersist) return t < my_tiles;
-    mbar_wait(tstart, ts_phase, a.suspend_ns);
+    mbar_wait(tstart, ts_phase);
     ts_phase ^= 1;
     return *reinterpret_cast<volatile int*>(sm.done) == 0;
   };
@@ -589,7 +575,7 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
         const uint32_t bytes = uint32_t(n_hidden) * W * W * 2 * 2;
         mbar_expect_tx(&full[0], bytes);
         bulk_g2s(sm.wst, net.wq, bytes, &full[0]);
-        mbar_wait(&full[0], 0, 0);
+        mbar_wait(&full[0], 0);
       }
       uint32_t chunk_iter = 0, kr_phase = 0, a0_phase = 0;
       // debug timeline (NSDF_TC_TIMELINE): cycles the issuer waits for A0, A blocks, weights
@@ -597,7 +583,7 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
       long long w_a0 = 0, w_k = 0, w_full = 0, t_loop = 0;
       auto timed_wait = [&](uint64_t* bar, uint32_t ph, long long& acc) {
         const long long c0 = mdbg ? clock64() : 0;
-        mbar_wait(bar, ph, a.suspend_ns);
+        mbar_wait(bar, ph);
         if (mdbg) acc += clock64() - c0;
       };
       for (int t = 0; more_tiles(t); ++t) {
@@ -686,7 +672,7 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
           const __half* lw = reinterpret_cast<const __half*>(net.wq) + size_t(h) * 2 * W * W;
           for (int c = 0; c < kChunks; ++c, ++chunk_iter) {
             const int s = chunk_iter % kStages;
-            mbar_wait(&empty[s], ((chunk_iter / kStages) & 1) ^ 1, a.suspend_ns);
+            mbar_wait(&empty[s], ((chunk_iter / kStages) & 1) ^ 1);
             mbar_expect_tx(&full[s], kChunkBytes * kNW);
             bulk_g2s(sm.wst + size_t(s) * kStageHalves, lw + size_t(c) * (W * kKC), kChunkBytes, &full[s]);
             if (kTerms == 3)
@@ -760,9 +746,10 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
       mbar_arrive(a0ready);
       mark(1);
       float acc_out = 0.0f;
-      for (int m = 0; m <= n_hidden; ++m) {
-        const bool last = m == n_hidden;
-        mbar_wait(dfull, dfull_phase, a.suspend_ns);
+      // one MMA layer's epilogue; the last one (compile-time) folds in the output dot
+      auto layer = [&](int m, auto last_tag) {
+        constexpr bool last = decltype(last_tag)::value;
+        mbar_wait(dfull, dfull_phase);
         mark(2 + 2 * min(m, 3));
         dfull_phase ^= 1;
         tc_fence_after();
@@ -800,7 +787,7 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
           if (i + 1 < kSub) tmem_issue16(treg + uint32_t(cc + kGroups * kBlk), raw[buf ^ 1]);
           float v[16];
           activate(raw[buf], cc, v);
-          if (kTA && !last) {
+          if constexpr (kTA && !last) {
             // in place: A block i of the next layer over the D columns just read
             uint32_t hw[8];
 #pragma unroll
@@ -815,7 +802,7 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
             tmem_wait_st();
             tc_fence_before();
             mbar_arrive(&kready[i]);
-          } else if (!last) {
+          } else if constexpr (!last) {
 #pragma unroll
             for (int j = 0; j < 16; j += 8) {
               const uint32_t h0 = pack_half2(v[j], v[j + 1]), h1 = pack_half2(v[j + 2], v[j + 3]),
@@ -837,7 +824,10 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
           }
         }
         mark(3 + 2 * min(m, 3));
-      }
+      };
+#pragma unroll
+      for (int m = 0; m < n_hidden; ++m) layer(m, std::false_type{});
+      layer(n_hidden, std::true_type{});
       ++dbg_t;
       // ---- combine the column groups' partial output dots ----
       if (kGroups > 1) {
@@ -1074,11 +1064,11 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
   }
 }
 
-template <int W, bool kGrad, int kTerms, bool kResident, bool kPersist, bool kTA>
+template <int W, bool kGrad, int kTerms, bool kResident, bool kPersist, bool kTA, int kHid>
 bool launch_w(TcArgs& a, int n_max_items, cudaStream_t s) {
   constexpr int kGroups = W == 64 ? 1 : (W == 256 && kTerms == 3 ? 4 : 2);
   constexpr int kThreads = 32 * (kResident ? 1 : 2) + 128 * kGroups;
-  auto kernel = tc_mlp_kernel<W, kGrad, kGroups, kTerms, kResident, kPersist, kTA>;
+  auto kernel = tc_mlp_kernel<W, kGrad, kGroups, kTerms, kResident, kPersist, kTA, kHid>;
   const size_t smem = tc_smem_bytes(W, a.net.n_layers, kTerms, kResident, kPersist, kTA);
   static size_t configured_smem = 0;
   static int per_sm = 0;
@@ -1101,8 +1091,9 @@ bool launch_w(TcArgs& a, int n_max_items, cudaStream_t s) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     configured_smem = smem;
     if (getenv("NSDF_DEBUG_TC"))
-      fprintf(stderr, "tc_mlp_kernel<%d,%d,%d,%d,%d,%d,%d>: smem %zu B, regs %d, %d CTAs/SM (occupancy API %d)\n", W,
-              int(kGrad), kGroups, kTerms, int(kResident), int(kPersist), int(kTA), smem, fa.numRegs, per_sm, occ);
+      fprintf(stderr, "tc_mlp_kernel<%d,%d,%d,%d,%d,%d,%d,%d>: smem %zu B, regs %d, %d CTAs/SM (occupancy API %d)\n",
+              W, int(kGrad), kGroups, kTerms, int(kResident), int(kPersist), int(kTA), kHid, smem, fa.numRegs, per_sm,
+              occ);
   }
   const int tmem_limit = 512 / (2 * W);  // two accumulator regions per CTA
   const int per = std::max(1, std::min(per_sm, tmem_limit));
@@ -1113,33 +1104,25 @@ bool launch_w(TcArgs& a, int n_max_items, cudaStream_t s) {
   return cudaGetLastError() == cudaSuccess;
 }
 
-// NSDF_TC_TMEM_A: bit w/64 selects the TMEM-resident A operand for width w (1 = 64,
-// 2 = 128, 4 = 256); default all (0 = the SMEM A operand everywhere, for comparison).
-int tmem_a_mask() {
-  static const int v = [] {
-    const char* e = getenv("NSDF_TC_TMEM_A");
-    return e ? atoi(e) : 7;
-  }();
-  return v;
+// The hidden-layer count is compiled in for the standard architectures (64x1, 128x2, 256x3:
+// the nets of every BASELINE config); other depths take the runtime-count kernels.
+template <int W, bool kGrad, int kTerms, bool kResident, bool kPersist>
+bool launch_h(TcArgs& a, int n_max_items, cudaStream_t s) {
+  constexpr int kStd = W == 64 ? 1 : (W == 128 ? 2 : 3);
+  return a.net.n_layers - 2 == kStd ? launch_w<W, kGrad, kTerms, kResident, kPersist, true, kStd>(a, n_max_items, s)
+                                    : launch_w<W, kGrad, kTerms, kResident, kPersist, true, 0>(a, n_max_items, s);
 }
 
 template <bool kGrad, int kTerms, bool kPersist>
 bool launch_terms(TcArgs& a, int n_max_items, cudaStream_t s) {
   // 64-wide nets keep every hidden layer resident in SMEM when it fits (<= 4 layers).
   const bool resident = a.net.width == 64 && a.net.n_layers - 2 <= 4;
-  const bool ta = (tmem_a_mask() & (a.net.width / 64)) != 0;
   switch (a.net.width) {
     case 64:
-      if (resident)
-        return ta ? launch_w<64, kGrad, kTerms, true, kPersist, true>(a, n_max_items, s)
-                  : launch_w<64, kGrad, kTerms, true, kPersist, false>(a, n_max_items, s);
-      return launch_w<64, kGrad, kTerms, false, kPersist, false>(a, n_max_items, s);
-    case 128:
-      return ta ? launch_w<128, kGrad, kTerms, false, kPersist, true>(a, n_max_items, s)
-                : launch_w<128, kGrad, kTerms, false, kPersist, false>(a, n_max_items, s);
-    case 256:
-      return ta ? launch_w<256, kGrad, kTerms, false, kPersist, true>(a, n_max_items, s)
-                : launch_w<256, kGrad, kTerms, false, kPersist, false>(a, n_max_items, s);
+      return resident ? launch_h<64, kGrad, kTerms, true, kPersist>(a, n_max_items, s)
+                      : launch_h<64, kGrad, kTerms, false, kPersist>(a, n_max_items, s);
+    case 128: return launch_h<128, kGrad, kTerms, false, kPersist>(a, n_max_items, s);
+    case 256: return launch_h<256, kGrad, kTerms, false, kPersist>(a, n_max_items, s);
     default: return false;
   }
 }
@@ -1222,17 +1205,8 @@ void timeline_dump(long long* buf, const char* what) {
   cudaMemset(buf, 0, kDbgSize * sizeof(long long));
 }
 
-uint32_t suspend_hint() {
-  static const uint32_t v = [] {
-    const char* e = getenv("NSDF_TC_SUSPEND_NS");
-    return e ? uint32_t(strtoul(e, nullptr, 0)) : 0u;
-  }();
-  return v;
-}
-
 template <bool kGrad, bool kPersist = false>
 bool launch_any(TcArgs& a, int n_max_items, cudaStream_t s) {
-  a.suspend_ns = suspend_hint();
   static const int claim_div = [] {
     const char* e = getenv("NSDF_TC_CLAIM_DIV");
     return e ? std::max(1, atoi(e)) : 4;
