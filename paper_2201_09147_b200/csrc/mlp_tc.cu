@@ -60,6 +60,7 @@ constexpr float kHalfPi = 1.5707963267948966f;
 #define NSDF_TC_TIMELINE_BUILD 0
 #endif
 constexpr bool kTimeline = NSDF_TC_TIMELINE_BUILD != 0;
+
 constexpr int kDbgTiles = 65 * 16 + 64 * 4;
 constexpr int kDbgCta = kDbgTiles + 8;
 constexpr int kDbgMaxCta = 2048;
@@ -249,8 +250,7 @@ constexpr int kK0 = 32;
 
 // Dynamic shared-memory carve-up.  SWIZZLE_NONE operands need 16-byte alignment only.
 struct TcSmem {
-  __half* a;            // [128 x W] A operand, hi part (A0 of layer 0 aliases K 0..31)
-  __half* alo;          // [128 x W] A low part (split precision only)
+  __half* a;            // [128 x 32] layer-0 A operand (A0); hidden layers keep A in TMEM
   __half* wst;          // resident hidden weights, or [kStages] streamed weight chunks
   __half* b0;           // [W x 32] layer-0 B operand
   float* bias;          // [(L-1) x W] omega*bias of the MMA layers' outputs (row 0 = 0)
@@ -272,10 +272,9 @@ __host__ __device__ inline size_t tc_weight_bytes(int W, int L, int terms, bool 
   return resident ? size_t(L - 2) * W * W * 2 * 2 : size_t(kStages) * W * kKC * 2 * nw;
 }
 
-__host__ __device__ inline size_t tc_smem_bytes(int W, int L, int terms, bool resident, bool persist, bool ta) {
-  const int nw = terms == 3 ? 2 : 1;
+__host__ __device__ inline size_t tc_smem_bytes(int W, int L, int terms, bool resident, bool persist) {
   size_t b = 0;
-  b += ta ? size_t(kRows) * kK0 * 2 : size_t(kRows) * W * 2 * nw;
+  b += size_t(kRows) * kK0 * 2;  // A0 (the hidden layers' A lives in TMEM)
   b += tc_weight_bytes(W, L, terms, resident);
   b += size_t(W) * kK0 * 2;
   b += size_t(L - 1) * W * 4;
@@ -286,8 +285,7 @@ __host__ __device__ inline size_t tc_smem_bytes(int W, int L, int terms, bool re
   return b + 128;  // alignment slack
 }
 
-__device__ inline TcSmem tc_carve(uint8_t* raw, int W, int L, int terms, bool resident, bool persist, bool ta) {
-  const int nw = terms == 3 ? 2 : 1;
+__device__ inline TcSmem tc_carve(uint8_t* raw, int W, int L, int terms, bool resident, bool persist) {
   size_t off = 0;
   auto take = [&](size_t bytes, size_t align) {
     off = (off + align - 1) / align * align;
@@ -296,8 +294,7 @@ __device__ inline TcSmem tc_carve(uint8_t* raw, int W, int L, int terms, bool re
     return p;
   };
   TcSmem s;
-  s.a = reinterpret_cast<__half*>(take(size_t(kRows) * (ta ? kK0 : W) * 2, 128));
-  s.alo = reinterpret_cast<__half*>(take(nw == 2 && !ta ? size_t(kRows) * W * 2 : 0, 128));
+  s.a = reinterpret_cast<__half*>(take(size_t(kRows) * kK0 * 2, 128));
   s.wst = reinterpret_cast<__half*>(take(tc_weight_bytes(W, L, terms, resident), 128));
   s.b0 = reinterpret_cast<__half*>(take(size_t(W) * kK0 * 2, 128));
   s.bias = reinterpret_cast<float*>(take(size_t(L - 1) * W * 4, 16));
@@ -450,7 +447,7 @@ enum PfStage : int { kPfNeed = 0, kPfListed = 1, kPfReady = 2 };
 //            list until it drains (sphere_trace_level, trace.cpp:61-84)
 // MMA layer m = 0 is layer 0 (K = 32, B0 resident), m = 1..L-2 the hidden layers; the
 // last hidden layer's epilogue folds in the 1 x W output layer.
-template <int W, bool kGrad, int kGroups, int kTerms, bool kResident, bool kPersist, bool kTA, int kHid>
+template <int W, bool kGrad, int kGroups, int kTerms, bool kResident, bool kPersist, int kHid>
 __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
                                   (W == 64 ? 4 : (kGroups > 2 ? 1 : 2))) tc_mlp_kernel(TcArgs a) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
@@ -458,7 +455,7 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
   constexpr int kThreads = 32 * kCtl + 128 * kGroups;
   const TcNet& net = a.net;
   const int L = net.n_layers;
-  const TcSmem sm = tc_carve(smem_raw, W, L, kTerms, kResident, kPersist, kTA);
+  const TcSmem sm = tc_carve(smem_raw, W, L, kTerms, kResident, kPersist);
   constexpr int kNW = kTerms == 3 ? 2 : 1;  // weight parts (hi [, lo])
   uint64_t* full = sm.bars;
   uint64_t* empty = sm.bars + kStages;
@@ -483,7 +480,7 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
   constexpr int kSub = W / kBlk / kGroups;
   static_assert(kSub <= kMaxSub, "kready barriers");
   constexpr uint32_t kTmemCols = 2 * W;
-  // kTA: the hidden layers' A operand lives in TMEM, written IN PLACE over the accumulator
+  // The hidden layers' A operand lives in TMEM, written IN PLACE over the accumulator
   // it is computed from: the epilogue reads D block b (16 fp32 columns of its lane), and
   // stores the block's activations back into the same 16 columns as 8 columns of packed
   // fp16 hi parts + 8 of lo parts, which is exactly K-block b of the next layer's A.  The
@@ -569,7 +566,6 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
     if (lane == 0) {
       const uint32_t idesc = umma_idesc(W);
       const uint32_t a_base = smem_addr(sm.a);
-      const uint32_t alo_base = smem_addr(sm.alo);
       const uint32_t b0_base = smem_addr(sm.b0);
       if (kResident) {
         const uint32_t bytes = uint32_t(n_hidden) * W * W * 2 * 2;
@@ -602,7 +598,7 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
         // ---- hidden layers, K-streamed behind the epilogue ----
         for (int h = 0; h < n_hidden; ++h) {
           const uint32_t d_tmem = tmem + uint32_t((h + 1) & 1) * W;
-          const uint32_t a_tmem = tmem + uint32_t(h & 1) * W;  // kTA: A in place of layer h's D
+          const uint32_t a_tmem = tmem + uint32_t(h & 1) * W;  // A in place of layer h's D
           uint32_t b_base = 0, lo_off = 0;
           int s = 0;
 #pragma unroll 1
@@ -625,25 +621,14 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
                 lo_off = uint32_t(W) * kKC * 2;
               }
             }
-            const uint32_t aoff = uint32_t(blk * 2) * (kRows / 8) * 128, boff = uint32_t(ks * 2) * (W / 8) * 128;
+            const uint32_t boff = uint32_t(ks * 2) * (W / 8) * 128;
             const uint64_t bd = umma_desc(b_base + boff, W * 16, 128);
-            if (kTA) {
-              const uint32_t at = a_tmem + uint32_t(blk * kBlk);
-              tc_mma_ts(d_tmem, at, bd, idesc, blk != 0);
-              if (kTerms == 3) {  // split precision: + A_lo.W_hi + A_hi.W_lo
-                const uint64_t bdl = umma_desc(b_base + lo_off + boff, W * 16, 128);
-                tc_mma_ts(d_tmem, at + 8, bd, idesc, 1);
-                tc_mma_ts(d_tmem, at, bdl, idesc, 1);
-              }
-            } else {
-              const uint64_t ad = umma_desc(a_base + aoff, kRows * 16, 128);
-              tc_mma(d_tmem, ad, bd, idesc, blk != 0);
-              if (kTerms == 3) {  // split precision: + A_lo.W_hi + A_hi.W_lo
-                const uint64_t adl = umma_desc(alo_base + aoff, kRows * 16, 128);
-                const uint64_t bdl = umma_desc(b_base + lo_off + boff, W * 16, 128);
-                tc_mma(d_tmem, adl, bd, idesc, 1);
-                tc_mma(d_tmem, ad, bdl, idesc, 1);
-              }
+            const uint32_t at = a_tmem + uint32_t(blk * kBlk);  // hi parts; lo parts 8 columns on
+            tc_mma_ts(d_tmem, at, bd, idesc, blk != 0);
+            if (kTerms == 3) {  // split precision: + A_lo.W_hi + A_hi.W_lo
+              const uint64_t bdl = umma_desc(b_base + lo_off + boff, W * 16, 128);
+              tc_mma_ts(d_tmem, at + 8, bd, idesc, 1);
+              tc_mma_ts(d_tmem, at, bdl, idesc, 1);
             }
             if (ks == 1) {
               if (!kResident) tc_commit(&empty[s]);  // frees the weight stage once these MMAs retire
@@ -787,35 +772,22 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
           if (i + 1 < kSub) tmem_issue16(treg + uint32_t(cc + kGroups * kBlk), raw[buf ^ 1]);
           float v[16];
           activate(raw[buf], cc, v);
-          if constexpr (kTA && !last) {
-            // in place: A block i of the next layer over the D columns just read
-            uint32_t hw[8];
+          if constexpr (!last) {
+            // in place: A block i of the next layer over the D columns just read; the MMA may
+            // start on block row i while this thread continues with block i + 1 (waiting
+            // for the stores one block later, to overlap their latency, was measured slower:
+            // the MMA start matters more)
+            uint32_t hw[8], lw[8];
 #pragma unroll
             for (int j = 0; j < 8; ++j) hw[j] = pack_half2(v[2 * j], v[2 * j + 1]);
-            tmem_st8(treg + uint32_t(cc), hw[0], hw[1], hw[2], hw[3], hw[4], hw[5], hw[6], hw[7]);
             if (kTerms == 3) {
-              uint32_t lw[8];
 #pragma unroll
               for (int j = 0; j < 8; ++j) lw[j] = pack_half2_lo(v[2 * j], v[2 * j + 1], hw[j]);
+            }
+            tmem_st8(treg + uint32_t(cc), hw[0], hw[1], hw[2], hw[3], hw[4], hw[5], hw[6], hw[7]);
+            if (kTerms == 3)
               tmem_st8(treg + uint32_t(cc + 8), lw[0], lw[1], lw[2], lw[3], lw[4], lw[5], lw[6], lw[7]);
-            }
             tmem_wait_st();
-            tc_fence_before();
-            mbar_arrive(&kready[i]);
-          } else if constexpr (!last) {
-#pragma unroll
-            for (int j = 0; j < 16; j += 8) {
-              const uint32_t h0 = pack_half2(v[j], v[j + 1]), h1 = pack_half2(v[j + 2], v[j + 3]),
-                             h2 = pack_half2(v[j + 4], v[j + 5]), h3 = pack_half2(v[j + 6], v[j + 7]);
-              *reinterpret_cast<uint4*>(&sm.a[a_off(row, cc + j)]) = make_uint4(h0, h1, h2, h3);
-              if (kTerms == 3)
-                *reinterpret_cast<uint4*>(&sm.alo[a_off(row, cc + j)]) =
-                    make_uint4(pack_half2_lo(v[j], v[j + 1], h0), pack_half2_lo(v[j + 2], v[j + 3], h1),
-                               pack_half2_lo(v[j + 4], v[j + 5], h2), pack_half2_lo(v[j + 6], v[j + 7], h3));
-            }
-            // block row i of the next layer's A is complete in this group: the MMA may
-            // start on it while this thread continues with block i + 1
-            fence_proxy_async();
             tc_fence_before();
             mbar_arrive(&kready[i]);
           } else {
@@ -1064,12 +1036,12 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
   }
 }
 
-template <int W, bool kGrad, int kTerms, bool kResident, bool kPersist, bool kTA, int kHid>
+template <int W, bool kGrad, int kTerms, bool kResident, bool kPersist, int kHid>
 bool launch_w(TcArgs& a, int n_max_items, cudaStream_t s) {
   constexpr int kGroups = W == 64 ? 1 : (W == 256 && kTerms == 3 ? 4 : 2);
   constexpr int kThreads = 32 * (kResident ? 1 : 2) + 128 * kGroups;
-  auto kernel = tc_mlp_kernel<W, kGrad, kGroups, kTerms, kResident, kPersist, kTA, kHid>;
-  const size_t smem = tc_smem_bytes(W, a.net.n_layers, kTerms, kResident, kPersist, kTA);
+  auto kernel = tc_mlp_kernel<W, kGrad, kGroups, kTerms, kResident, kPersist, kHid>;
+  const size_t smem = tc_smem_bytes(W, a.net.n_layers, kTerms, kResident, kPersist);
   static size_t configured_smem = 0;
   static int per_sm = 0;
   static int sms = 0;
@@ -1091,9 +1063,8 @@ bool launch_w(TcArgs& a, int n_max_items, cudaStream_t s) {
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     configured_smem = smem;
     if (getenv("NSDF_DEBUG_TC"))
-      fprintf(stderr, "tc_mlp_kernel<%d,%d,%d,%d,%d,%d,%d,%d>: smem %zu B, regs %d, %d CTAs/SM (occupancy API %d)\n",
-              W, int(kGrad), kGroups, kTerms, int(kResident), int(kPersist), int(kTA), kHid, smem, fa.numRegs, per_sm,
-              occ);
+      fprintf(stderr, "tc_mlp_kernel<%d,%d,%d,%d,%d,%d,%d>: smem %zu B, regs %d, %d CTAs/SM (occupancy API %d)\n", W,
+              int(kGrad), kGroups, kTerms, int(kResident), int(kPersist), kHid, smem, fa.numRegs, per_sm, occ);
   }
   const int tmem_limit = 512 / (2 * W);  // two accumulator regions per CTA
   const int per = std::max(1, std::min(per_sm, tmem_limit));
@@ -1109,8 +1080,8 @@ bool launch_w(TcArgs& a, int n_max_items, cudaStream_t s) {
 template <int W, bool kGrad, int kTerms, bool kResident, bool kPersist>
 bool launch_h(TcArgs& a, int n_max_items, cudaStream_t s) {
   constexpr int kStd = W == 64 ? 1 : (W == 128 ? 2 : 3);
-  return a.net.n_layers - 2 == kStd ? launch_w<W, kGrad, kTerms, kResident, kPersist, true, kStd>(a, n_max_items, s)
-                                    : launch_w<W, kGrad, kTerms, kResident, kPersist, true, 0>(a, n_max_items, s);
+  return a.net.n_layers - 2 == kStd ? launch_w<W, kGrad, kTerms, kResident, kPersist, kStd>(a, n_max_items, s)
+                                    : launch_w<W, kGrad, kTerms, kResident, kPersist, 0>(a, n_max_items, s);
 }
 
 template <bool kGrad, int kTerms, bool kPersist>
