@@ -111,16 +111,23 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+// The MMA issuer runs as a whole converged warp (its operands stay warp-uniform, so they
+// live in uniform registers); tcgen05.mma / commit are issued by one elected lane.  Issued
+// from a single divergent lane instead, every MMA was wrapped in a uniformity loop.
 __device__ __forceinline__ void tc_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_addr(bar))
-               : "memory");
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_addr(bar))
+      : "memory");
 }
 __device__ __forceinline__ void tc_mma(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc, uint32_t idesc,
                                        uint32_t accumulate) {
   asm volatile(
-      "{\n\t.reg .pred p;\n\t"
+      "{\n\t.reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
       "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate));
 }
 // Asynchronous 32x32b.x16 load: the registers are only valid after tmem_wait16 (which
@@ -144,9 +151,10 @@ __device__ __forceinline__ void tmem_wait16(uint32_t (&r)[16]) {
 __device__ __forceinline__ void tc_mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
                                           uint32_t accumulate) {
   asm volatile(
-      "{\n\t.reg .pred p;\n\t"
+      "{\n\t.reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
       "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate));
 }
 // Each lane writes 8 consecutive 32-bit columns of its own TMEM lane.
@@ -563,19 +571,23 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
 
   if (warp == 0) {
     // ================= MMA issuer (resident mode: also loads the weights once) =================
-    if (lane == 0) {
+    // the whole warp runs this loop; MMAs and commits are issued by one elected lane
+    {
       const uint32_t idesc = umma_idesc(W);
       const uint32_t a_base = smem_addr(sm.a);
       const uint32_t b0_base = smem_addr(sm.b0);
       if (kResident) {
         const uint32_t bytes = uint32_t(n_hidden) * W * W * 2 * 2;
-        mbar_expect_tx(&full[0], bytes);
-        bulk_g2s(sm.wst, net.wq, bytes, &full[0]);
+        if (lane == 0) {
+          mbar_expect_tx(&full[0], bytes);
+          bulk_g2s(sm.wst, net.wq, bytes, &full[0]);
+        }
         mbar_wait(&full[0], 0);
+        __syncwarp();
       }
       uint32_t chunk_iter = 0, kr_phase = 0, a0_phase = 0;
       // debug timeline (NSDF_TC_TIMELINE): cycles the issuer waits for A0, A blocks, weights
-      const bool mdbg = kTimeline && a.dbg && blockIdx.x == 0;
+      const bool mdbg = kTimeline && a.dbg && blockIdx.x == 0 && lane == 0;
       long long w_a0 = 0, w_k = 0, w_full = 0, t_loop = 0;
       auto timed_wait = [&](uint64_t* bar, uint32_t ph, long long& acc) {
         const long long c0 = mdbg ? clock64() : 0;
@@ -601,7 +613,7 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
           const uint32_t a_tmem = tmem + uint32_t(h & 1) * W;  // A in place of layer h's D
           uint32_t b_base = 0, lo_off = 0;
           int s = 0;
-#pragma unroll 1
+#pragma unroll
           for (int blk = 0; blk < W / kBlk; ++blk) {
             if (blk % kGroups == 0) {  // block row of the A operand written by every group
               timed_wait(&kready[blk / kGroups], kr_phase, w_k);
