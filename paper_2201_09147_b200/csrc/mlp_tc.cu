@@ -536,8 +536,9 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
     }
-    for (int i = 0; i < kSub; ++i) mbar_init(&kready[i], 128 * kGroups);
-    mbar_init(a0ready, 128 * kGroups);
+    // one arrival per epilogue warp (after a __syncwarp behind each thread's fence)
+    for (int i = 0; i < kSub; ++i) mbar_init(&kready[i], 4 * kGroups);
+    mbar_init(a0ready, 4 * kGroups);
     mbar_init(dfull, 1);
     mbar_init(tstart, 1);
     *sm.stage_count = 0;
@@ -740,7 +741,8 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
       }
       // every epilogue thread: done with the previous tile's TMEM (region 0 is reused)
       tc_fence_before();
-      mbar_arrive(a0ready);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(a0ready);
       mark(1);
       float acc_out = 0.0f;
       // one MMA layer's epilogue; the last one (compile-time) folds in the output dot
@@ -801,7 +803,8 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
               tmem_st8(treg + uint32_t(cc + 8), lw[0], lw[1], lw[2], lw[3], lw[4], lw[5], lw[6], lw[7]);
             tmem_wait_st();
             tc_fence_before();
-            mbar_arrive(&kready[i]);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&kready[i]);
           } else {
 #pragma unroll
             for (int j = 0; j < 16; ++j) acc_out = fmaf(sm.wout[cc + j], v[j], acc_out);
