@@ -258,7 +258,7 @@ def run_reference(args):
         ctx = Context(0, "fp32")
         pts = gbuffer_points(ctx, args).cpu().numpy()
         ctx.close()
-    warm = min(args.warmup, 1)
+    warm = min(args.warmup, 3)
     times = []
     for i in range(warm + min(args.steps, 10)):
         sec, units, sample, cores = reference_time(args, pts)
@@ -269,7 +269,7 @@ def run_reference(args):
     unit = "Mnormals/s" if args.cfg.get("kind") == "gbuffer" else "Mrays/s"
     line = {"impl": "reference", "metric": args.cfg["metric"], "value": value, "unit": unit, "n_gpus": args.gpus,
             "steps": len(times), "warmup": warm, "ms_per_step": sec * 1e3, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "scaling": "strong" if args.gpus > 1 else "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": workload_text(args), "config": args.config,
                        "resolution": f"{args.width}x{args.height}", "budgets": args.budgets},
             "cpu_baseline": {"value": value, "unit": unit, "cores": cores, "kind": "reference", "sample": sample},
