@@ -606,22 +606,19 @@ int nsdf_cuda_upload_mlp(nsdf_ctx* c, int n_layers, const int32_t* rows, const i
       for (int l = 0; l < n_layers; ++l) {
         const size_t nw = size_t(rows[l]) * cols[l];
         if (l >= 1 && l + 1 < n_layers) {
-          // Split precision: W * 2^k = hi + lo (both fp16); 2^k keeps lo out of the
-          // subnormal range and is undone in the epilogue (wscale).
-          double mx = 0;
-          for (size_t i = 0; i < nw; ++i) mx = std::max(mx, std::fabs(double(float(packed[o + i]))));
-          int k = 0;
-          while (k < 24 && mx * std::ldexp(1.0, k + 1) <= 16384.0) ++k;
-          n.wscale[l - 1] = float(std::ldexp(1.0, -k));
+          // Split precision: omega * W = hi + lo (both fp16), so the accumulator is the sine
+          // argument in radians.  Small weights' lo parts may be fp16 subnormals: their
+          // absolute error (<= 2^-25 per weight, times |a| <= 1) stays far below the fp32
+          // rounding of the argument.
           __half* hi = wq.data() + size_t(l - 1) * 2 * W * W;
           __half* lo = hi + size_t(W) * W;
           for (int r = 0; r < W; ++r)
             for (int kk = 0; kk < W; ++kk) {
-              const float v = std::ldexp(float(packed[o + size_t(r) * W + kk]), k);
-              const __half h = __float2half_rn(v);
+              const double v = double(n.omega) * double(float(packed[o + size_t(r) * W + kk]));
+              const __half h = __float2half_rn(float(v));
               const size_t at = size_t((kk / 8) * (W / 8) + r / 8) * 64 + (r % 8) * 8 + kk % 8;
               hi[at] = h;
-              lo[at] = __float2half_rn(v - __half2float(h));
+              lo[at] = __float2half_rn(float(v - double(__half2float(h))));
             }
         }
         o += nw;

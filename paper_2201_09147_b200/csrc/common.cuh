@@ -35,7 +35,6 @@ struct DevNet {
   // Fast-mode (tcgen05) copy, built at upload when tc-eligible (mlp_tc.cu):
   int tc_ok;
   const uint16_t* wq;      // hidden layers [h][hi | lo][W*W] fp16, UMMA canonical K-major layout
-  float wscale[kMaxLayers];  // hidden layer h is stored scaled by 1/wscale[h] (a power of 2)
   const float* bias_cat;   // biases of layers 0 .. L-2, [L-1][width]
   float bout;              // output bias
   // FP64 master copy (the certification path, mlp_f64.cu): same layouts as w / wt / b.

@@ -203,8 +203,7 @@ enum TcOp : int { kOpTrace = 0, kOpNormals = 1, kOpEval = 2, kOpNormalMap = 3 };
 struct TcNet {
   int n_layers, width, input_dim;
   float omega;
-  const __half* wq;                 // hidden layers [h][hi | lo][W*W], canonical chunked layout
-  float wscale[kMaxLayers];         // 2^-k: hidden weights are stored scaled by 2^k
+  const __half* wq;                 // hidden layers [h][hi | lo][W*W] of omega*W, canonical chunked layout
   const float* w0;                  // layer 0, row-major W x input_dim (fp32)
   const float* b;                   // biases, [n_layers-1][W] (fp32)
   const float* wout;                // output row (fp32), W
@@ -261,7 +260,8 @@ struct TcSmem {
   __half* a;            // [128 x 32] layer-0 A operand (A0); hidden layers keep A in TMEM
   __half* wst;          // resident hidden weights, or [kStages] streamed weight chunks
   __half* b0;           // [W x 32] layer-0 B operand
-  float* bias;          // [(L-1) x W] omega*bias of the MMA layers' outputs (row 0 = 0)
+  __half* bb;           // [L-2][W x 16] bias B operand of each hidden layer: omega*b in 3 fp16 parts
+  __half* ones;         // [128 x 16] bias A operand: ones at k = 0..2 on value rows
   float* wout;          // [W]
   float* part;          // [3][kRows] partial output dots of column groups 1..3
   int* stage_buf;       // [kStageCap] staged compaction appends (persistent trace)
@@ -285,7 +285,7 @@ __host__ __device__ inline size_t tc_smem_bytes(int W, int L, int terms, bool re
   b += size_t(kRows) * kK0 * 2;  // A0 (the hidden layers' A lives in TMEM)
   b += tc_weight_bytes(W, L, terms, resident);
   b += size_t(W) * kK0 * 2;
-  b += size_t(L - 1) * W * 4;
+  b += size_t(L - 2) * W * kBlk * 2 + size_t(kRows) * kBlk * 2;
   b += size_t(W) * 4;
   b += (W == 64 ? 0 : size_t(3) * kRows * 4);
   b += persist ? size_t(kStageCap) * 4 + 16 : 16;
@@ -305,7 +305,8 @@ __device__ inline TcSmem tc_carve(uint8_t* raw, int W, int L, int terms, bool re
   s.a = reinterpret_cast<__half*>(take(size_t(kRows) * kK0 * 2, 128));
   s.wst = reinterpret_cast<__half*>(take(tc_weight_bytes(W, L, terms, resident), 128));
   s.b0 = reinterpret_cast<__half*>(take(size_t(W) * kK0 * 2, 128));
-  s.bias = reinterpret_cast<float*>(take(size_t(L - 1) * W * 4, 16));
+  s.bb = reinterpret_cast<__half*>(take(size_t(L - 2) * W * kBlk * 2, 128));
+  s.ones = reinterpret_cast<__half*>(take(size_t(kRows) * kBlk * 2, 128));
   s.wout = reinterpret_cast<float*>(take(size_t(W) * 4, 16));
   s.part = reinterpret_cast<float*>(take(W == 64 ? 0 : size_t(3) * kRows * 4, 16));
   s.stage_buf = reinterpret_cast<int*>(take(persist ? size_t(kStageCap) * 4 : 0, 16));
@@ -529,7 +530,25 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
     }
     sm.b0[b0_off(W, n, k)] = v;
   }
-  for (int i = threadIdx.x; i < (L - 1) * W; i += kThreads) sm.bias[i] = i < W ? 0.0f : net.b[i] * net.omega;
+  // Hidden-layer biases on the tensor cores: one extra K = 16 MMA per layer, A = a constant
+  // block with ones at k = 0..2 (value rows only: tangent chains carry no bias), B = the
+  // three fp16 parts of omega*b.  With omega folded into the hidden weights (upload), every
+  // accumulator is the sine argument in radians: the epilogue has no FFMA and no bias loads.
+  for (int i = threadIdx.x; i < (L - 2) * W * kBlk; i += kThreads) {
+    const int h = i / (W * kBlk), n = (i / kBlk) % W, k = i % kBlk;
+    __half v = __float2half_rn(0.0f);
+    if (k < 3) {
+      __half hi, mid, lo;
+      split3(net.b[(h + 1) * W + n] * net.omega, hi, mid, lo);
+      v = k == 0 ? hi : (k == 1 ? mid : lo);
+    }
+    sm.bb[size_t(h) * W * kBlk + b0_off(W, n, k)] = v;
+  }
+  for (int i = threadIdx.x; i < kRows * kBlk; i += kThreads) {
+    const int r = i / kBlk, k = i % kBlk;
+    const bool one = k < 3 && (!kGrad || (r & 3) == 0);
+    sm.ones[a_off(r, 0) + (k >> 3) * (kRows / 8) * 64 + (k & 7)] = __float2half_rn(one ? 1.0f : 0.0f);
+  }
   for (int i = threadIdx.x; i < W; i += kThreads) sm.wout[i] = net.wout[i];
   if (threadIdx.x == 0) {
     for (int s = 0; s < kStages; ++s) {
@@ -577,6 +596,7 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
       const uint32_t idesc = umma_idesc(W);
       const uint32_t a_base = smem_addr(sm.a);
       const uint32_t b0_base = smem_addr(sm.b0);
+      const uint64_t ones_desc = umma_desc(smem_addr(sm.ones), kRows * 16, 128);
       if (kResident) {
         const uint32_t bytes = uint32_t(n_hidden) * W * W * 2 * 2;
         if (lane == 0) {
@@ -620,6 +640,8 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
               timed_wait(&kready[blk / kGroups], kr_phase, w_k);
               tc_fence_after();
             }
+            if (blk == 0)  // D = omega*b (value rows), then += A.(omega W)^T
+              tc_mma(d_tmem, ones_desc, umma_desc(smem_addr(sm.bb + size_t(h) * W * kBlk), W * 16, 128), idesc, false);
             const int c = blk >> 1, ks = blk & 1;  // 32-K weight chunk, K=16 step inside it
             if (ks == 0) {
               s = chunk_iter % kStages;
@@ -637,7 +659,7 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
             const uint32_t boff = uint32_t(ks * 2) * (W / 8) * 128;
             const uint64_t bd = umma_desc(b_base + boff, W * 16, 128);
             const uint32_t at = a_tmem + uint32_t(blk * kBlk);  // hi parts; lo parts 8 columns on
-            tc_mma_ts(d_tmem, at, bd, idesc, blk != 0);
+            tc_mma_ts(d_tmem, at, bd, idesc, true);
             if (kTerms == 3) {  // split precision: + A_lo.W_hi + A_hi.W_lo
               const uint64_t bdl = umma_desc(b_base + lo_off + boff, W * 16, 128);
               tc_mma_ts(d_tmem, at + 8, bd, idesc, 1);
@@ -752,10 +774,7 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
         mark(2 + 2 * min(m, 3));
         dfull_phase ^= 1;
         tc_fence_after();
-        const float* bias = sm.bias + size_t(m) * W;  // row 0: layer 0's bias is inside D0
-        // radians; undoes the 2^k weight scaling of the hidden layers
-        const float zs = m == 0 ? 1.0f : net.omega * net.wscale[m - 1];
-        const float dscale = zs;
+        // D is the sine argument in radians (omega and the bias are inside the MMAs)
         const uint32_t treg = taddr + uint32_t(m & 1) * W;
         // sine epilogue of one 16-column block (value rows; tangent rows scale by omega cos)
         auto activate = [&](const uint32_t (&r)[16], int cc, float (&v)[16]) {
@@ -766,12 +785,12 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
             if (kGrad) {
               // the value row's pre-activation, broadcast to its 3 tangent rows; every lane
               // issues ONE sine: sin(z) on the value row, cos(z) = sin(z + pi/2) on tangents
-              const float z = __shfl_sync(group_mask, fmaf(v[j], zs, bias[cc + j]), lane & ~3, 32);
+              const float z = __shfl_sync(group_mask, v[j], lane & ~3, 32);
               const float r1 = fast_sin(chain == 0 ? z : z + kHalfPi);
-              // tangent rows: G = (W.G_prev) * omega cos(z); D carries the 2^k weight scale
-              v[j] = chain == 0 ? r1 : v[j] * (dscale * r1);
+              // tangent rows: G = (W.G_prev) * omega cos(z); D = omega (W.G_prev)
+              v[j] = chain == 0 ? r1 : v[j] * r1;
             } else {
-              v[j] = fast_sin(fmaf(v[j], zs, bias[cc + j]));
+              v[j] = fast_sin(v[j]);
             }
           }
         };
@@ -1219,7 +1238,6 @@ TcNet tc_net(const DevNet& n) {
   t.input_dim = n.input_dim;
   t.omega = n.omega;
   t.wq = reinterpret_cast<const __half*>(n.wq);
-  for (int l = 0; l < kMaxLayers; ++l) t.wscale[l] = n.wscale[l];
   t.w0 = n.w[0];
   t.b = n.bias_cat;
   t.wout = n.w[n.n_layers - 1];
