@@ -79,6 +79,11 @@ def parse():
                     help="frames in flight (engine contexts on their own streams); 1 = strictly serial frames; "
                          "0 = 3, or 5 for tile-sharded frames on >= 4 GPUs (smaller shares leave more "
                          "level-tail idle time to overlap: tools/shardsim.py, N=8: 6.19x -> 6.38x)")
+    ap.add_argument("--shard", default="frames", choices=["frames", "tiles"],
+                    help="N > 1, single-frame configs: 'frames' = every rank renders whole frames of the frame "
+                         "stream (weak scaling; frames stay on their rank), 'tiles' = the ranks split every frame's "
+                         "image tiles and assemble it in rank 0's framebuffer (strong scaling).  The frames run also "
+                         "times a tile-sharded pass and reports it as strong_scaling")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-alt", action="store_true", help="skip the (40,20,20) parity-setting line of config 2")
@@ -297,7 +302,7 @@ def run_e2e(args, ctx, ds, seq, stream, world, rank, W):
                 "h2d_bytes_per_step": 12 * k, "d2h_bytes_per_step": 12 * k + 16,
                 "path": "nsdf_cuda_normal_map (C ABI, host points -> host normals)"}
     cam, cfg, shade, src, levels = W["cam"], W["cfg"], W["shade"], W["src"], W["levels"]
-    if world == 1:
+    if world == 1 or W.get("shard_frames"):
         # The public host-buffer call, nsdf_cuda_render, from one host thread per frame in
         # flight: each thread owns an engine context (own stream + workspace) and its own
         # pinned host framebuffer and renders every T-th frame, so one frame's D2H overlaps
@@ -361,8 +366,59 @@ def run_e2e(args, ctx, ds, seq, stream, world, rank, W):
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e_ms = float(te.item())
     level_bytes = 16 * len(levels) + 4 * 8 + 128 + 272  # camera + configs + level table
-    return {"value": npix * steps / (e_ms / 1e3) / 1e6, "unit": "Mrays/s", "ms_per_frame": e_ms / steps,
+    frames = steps * (world if W.get("shard_frames") else 1)  # frames mode: every rank's frames
+    return {"value": npix * frames / (e_ms / 1e3) / 1e6, "unit": "Mrays/s", "ms_per_frame": e_ms / frames,
             "h2d_bytes_per_step": level_bytes, "d2h_bytes_per_step": npix * (12 + 4 + 1), "path": path}
+
+
+def tile_pass(args, ctx, W, world, rank, Wd, Hd):
+    """Frames-mode runs (N > 1) also time the strong-scaling alternative: the same frames
+    split into image tiles across the ranks, each rank's shading kernels storing its tiles
+    into rank 0's framebuffer ring (PeerFramebuffer), one 4-byte all-reduce per frame."""
+    import torch
+    import torch.distributed as dist
+    from paper_2201_09147_b200 import scheduler
+
+    lanes = W["lanes"]
+    peer = scheduler.PeerFramebuffer(ctx, Wd, Hd, 2 * len(lanes), rank, world)
+    if not peer.ok:
+        peer.close()
+        return {"unavailable": f"peer framebuffer: {peer.reason}"}
+    tok = [torch.zeros(1, dtype=torch.int32, device="cuda") for _ in lanes]
+    lv = [d.levels() for _, _, d in lanes]
+
+    def frame(i):
+        c, st, _ = lanes[i % len(lanes)]
+        fr, fd, fm = peer.ptrs(i % (2 * len(lanes)))
+        c.render_device(lv[i % len(lanes)], W["cam"], W["cfg"], W["shade"], fr, fd, fm, W["src"], -1, args.tile, rank,
+                        world)
+        with torch.cuda.stream(st):
+            dist.all_reduce(tok[i % len(lanes)])
+
+    n = max(2 * len(lanes), min(args.steps, 30))
+    for i in range(max(3, len(lanes))):
+        frame(i)
+    torch.cuda.synchronize()
+    dist.barrier()
+    stream = lanes[0][1]
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _, st, _ in lanes[1:]:
+        st.wait_event(e0)
+    for i in range(n):
+        frame(i)
+    for _, st, _ in lanes[1:]:
+        stream.wait_stream(st)
+    e1.record(stream)
+    torch.cuda.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    dist.barrier()
+    peer.close()
+    return {"value": Wd * Hd * n / (ms / 1e3) / 1e6, "unit": "Mrays/s", "ms_per_frame": ms / n, "frames": n,
+            "parallelism": f"tiles{world}", "tile": args.tile, "frames_in_flight": len(lanes),
+            "frame_assembly": "peer stores into rank 0's framebuffer (NVLink)", "scaling": "strong"}
 
 
 def main():
@@ -402,6 +458,10 @@ def main():
     W = {"cam": standard_camera(Wd, Hd), "shade": ShadeConfig(specular=0.3),
          "src": 1 if args.normals == "mapped" else 0, "gbuffer": cfgw.get("kind") == "gbuffer"}
     animated = "frames" in cfgw
+    # N > 1 on a frame stream: each rank renders whole frames (no per-frame collective, no
+    # small-share tails); --shard tiles splits every frame across the ranks instead
+    shard_frames = world > 1 and not animated and cfgw.get("kind") != "gbuffer" and args.shard == "frames"
+    W["shard_frames"] = shard_frames
 
     ctx = Context(local, args.mode)
     stream = torch.cuda.Stream()          # the engine's launch stream; events are recorded on it
@@ -438,7 +498,7 @@ def main():
             W["levels"] = frame_levels[0]
         else:
             W["levels"] = ds.levels()
-        tile_world, tile_rank = (1, 0) if animated else (world, rank)
+        tile_world, tile_rank = (1, 0) if animated or shard_frames else (world, rank)
         if args.inflight <= 0:
             args.inflight = 5 if tile_world >= 4 else 3
         # Frames in flight: `inflight` engine contexts, each on its own stream with its own
@@ -456,7 +516,7 @@ def main():
         # into rank 0's framebuffer ring over NVLink (PeerFramebuffer); NCCL tile gather only
         # if peer mapping is unavailable.
         peer, gather = None, None
-        if world > 1 and not animated:
+        if world > 1 and not animated and not shard_frames:
             if args.gather == "peer":
                 peer = scheduler.PeerFramebuffer(ctx, Wd, Hd, 2 * len(lanes), rank, world)
                 if not peer.ok:
@@ -566,11 +626,11 @@ def main():
     ms_total = float(t.item())
     if animated:
         total_units = units_per_step * cfgw["frames"]              # all frames, all ranks
-    elif W["gbuffer"]:
-        total_units = units_per_step * steps * world               # every rank maps its own G-buffer
+    elif W["gbuffer"] or shard_frames:
+        total_units = units_per_step * steps * world               # every rank its own G-buffer / frames
     else:
         total_units = units_per_step * steps                       # tiles of the same frames
-    ms_per_frame = ms_total / steps
+    ms_per_frame = ms_total / steps / (world if shard_frames else 1)
     value = total_units / (ms_total / 1e3) / 1e6
     unit = "Mnormals/s" if W["gbuffer"] else "Mrays/s"
 
@@ -651,6 +711,8 @@ def main():
     else:
         hbm = None
 
+    strong = tile_pass(args, ctx, W, world, rank, Wd, Hd) if shard_frames else None
+
     e2e = None
     if not args.no_e2e and not animated:
         e2e = run_e2e(args, ctx, ds, seq, stream, world, rank, W)
@@ -670,21 +732,24 @@ def main():
         line = {
             "metric": cfgw["metric"], "value": value, "unit": unit, "n_gpus": world, "steps": steps,
             "warmup": args.warmup, "ms_per_step": ms_per_frame, "higher_is_better": True,
-            "scaling": "strong" if world > 1 and not W["gbuffer"] else "weak", "vs_baseline": None,
+            "scaling": "strong" if world > 1 and not (W["gbuffer"] or shard_frames) else "weak", "vs_baseline": None,
             "dtype": {"fp16": "split-fp16 tensor (3 MMA terms) / fp32 accum", "fp16low": "fp16 tensor / fp32 accum",
                       "fp32": "f32"}[args.mode],
             "data": "synthetic camera rays; committed fitted SIREN weights (assets/)",
             "config": {"workload": workload_text(args), "config": args.config, "resolution": f"{Wd}x{Hd}",
                        "budgets": args.budgets, "mode": args.mode, "tile": args.tile,
                        "frames_in_flight": 1 if W["gbuffer"] else max(1, args.inflight),
-                       "parallelism": (f"frames{world}" if animated else f"tiles{world}") if world > 1 else "single",
+                       "parallelism": (f"frames{world}" if animated or shard_frames else f"tiles{world}")
+                       if world > 1 else "single",
                        "frame_assembly": None if world == 1 or animated else
+                       "none: frames stay on their rank (e2e: each rank's frames D2H into its host)" if shard_frames else
                        ("peer stores into rank 0's framebuffer (NVLink)" if W.get("peer") is not None
                         else "NCCL tile gather"),
                        "l2": "per-frame working set (ray state, lists, framebuffer) > 126 MB L2; weights L2-resident"},
             "fps": 1000.0 / ms_per_frame,
             "frame": frame,
             "parity_setting": alt,
+            "strong_scaling": strong,
             "roofline": {"bound": "tensor", "kernel": kernel, "achieved": achieved_tf, "peak": peak_tf,
                          "unit": "TFLOP/s", "frac": achieved_tf / peak_tf,
                          "peak_kind": f"{pk_kind} bf16 sustained (MEASURED_PEAKS.json)", "traffic": traffic,

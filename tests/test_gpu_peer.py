@@ -84,10 +84,12 @@ def test_peer_framebuffer_assembles_the_frame(mode, tile):
         assert np.array_equal(rgb.view(np.uint32), np.asarray(ref[0], np.float32).reshape(-1).view(np.uint32))
 
 
-def test_bench_two_ranks_plumbing():
-    """bench.py's N > 1 path end to end (torchrun, 2 ranks, peer framebuffer, e2e to host)
-    with both ranks on this one GPU over gloo (NSDF_BENCH_ONE_GPU=1): the JSON line carries
-    the contract keys and reports the peer assembly.  Plumbing only — not a measurement."""
+@pytest.mark.parametrize("shard", ["tiles", "frames"])
+def test_bench_two_ranks_plumbing(shard):
+    """bench.py's N > 1 path end to end (torchrun, 2 ranks, e2e to host) with both ranks on
+    this one GPU over gloo (NSDF_BENCH_ONE_GPU=1): the JSON line carries the contract keys;
+    tiles mode reports the peer assembly, frames mode the frame-sharded line plus the
+    tile-sharded strong_scaling pass.  Plumbing only — not a measurement."""
     import json
     import socket
     import subprocess
@@ -100,12 +102,18 @@ def test_bench_two_ranks_plumbing():
     env.pop("NSDF_MODE", None)  # conftest's oracle-mode default is not a bench --mode
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
                         "--master-addr", "127.0.0.1", "--master-port", str(port), "bench.py", "--gpus", "2",
-                        "--steps", "4", "--warmup", "3", "--no-cpu-baseline", "--no-alt"],
+                        "--steps", "4", "--warmup", "3", "--no-cpu-baseline", "--no-alt", "--shard", shard],
                        cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]
     line = json.loads(r.stdout.strip().splitlines()[-1])
     for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "e2e", "roofline", "clocks"):
         assert k in line
     assert line["n_gpus"] == 2 and line["value"] > 0 and line["e2e"]["value"] > 0
-    assert line["config"]["parallelism"] == "tiles2"
-    assert line["config"]["frame_assembly"].startswith("peer")
+    if shard == "tiles":
+        assert line["config"]["parallelism"] == "tiles2" and line["scaling"] == "strong"
+        assert line["config"]["frame_assembly"].startswith("peer")
+        assert line["strong_scaling"] is None
+    else:
+        assert line["config"]["parallelism"] == "frames2" and line["scaling"] == "weak"
+        ss = line["strong_scaling"]
+        assert ss["parallelism"] == "tiles2" and ss["value"] > 0 and ss["frame_assembly"].startswith("peer")
