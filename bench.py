@@ -731,7 +731,8 @@ def main():
         launches = (int(stats.kernel_launches) if stats is not None else 1) * steps
         line = {
             "metric": cfgw["metric"], "value": value, "unit": unit, "n_gpus": world, "steps": steps,
-            "warmup": args.warmup, "ms_per_step": ms_per_frame, "higher_is_better": True,
+            "warmup": args.warmup, "ms_per_step": ms_total / steps, "ms_per_frame": ms_per_frame,
+            "higher_is_better": True,
             "scaling": "strong" if world > 1 and not (W["gbuffer"] or shard_frames) else "weak", "vs_baseline": None,
             "dtype": {"fp16": "split-fp16 tensor (3 MMA terms) / fp32 accum", "fp16low": "fp16 tensor / fp32 accum",
                       "fp32": "f32"}[args.mode],
