@@ -727,7 +727,10 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
           dbg_t - a.dbg_skip < 64)
         a.dbg[(dbg_t - a.dbg_skip) * 16 + k] = clock64();
     };
-    auto eval_tile = [&](const float* p, bool live) -> float {
+    // gap0 / gap1: work for the warp's idle waits on the tensor core — gap0 runs after A0 is
+    // handed to the MMA issuer (the layer-0 round trip), gap1 before the last layer's
+    // accumulator wait (its MMA tail); the persistent trace runs its ray prefetch there.
+    auto eval_tile = [&](const float* p, bool live, auto&& gap0, auto&& gap1) -> float {
       mark(0);
       if (eg == 0) {
         // ---- A0: the point in three fp16 parts (value rows) or a unit tangent ----
@@ -766,10 +769,12 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
       __syncwarp();
       if (lane == 0) mbar_arrive(a0ready);
       mark(1);
+      gap0();
       float acc_out = 0.0f;
       // one MMA layer's epilogue; the last one (compile-time) folds in the output dot
       auto layer = [&](int m, auto last_tag) {
         constexpr bool last = decltype(last_tag)::value;
+        if constexpr (last) gap1();
         mbar_wait(dfull, dfull_phase);
         mark(2 + 2 * min(m, 3));
         dfull_phase ^= 1;
@@ -858,8 +863,9 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
       int res_base = 0, res_end = 0, nres = 0;  // claimed list range; next claim ticket (lane 0)
       bool exhausted = false;
       if (g0 && lane == 0) nres = fetch_ticket(a.cursor);
-      // advance this warp's ray pipeline by one stage (group 0 only)
-      auto refill = [&]() {
+      // the ray pipeline (group 0 only): assign = READY prefetches -> empty rows, right after
+      // the trace update; the other two stages advance in the tile's tensor-core waits
+      auto assign = [&]() {
         // READY prefetches -> empty rows (the k-th empty row takes the k-th ready lane)
         const uint32_t emp = __ballot_sync(0xffffffffu, slot < 0);
         const uint32_t rdy = __ballot_sync(0xffffffffu, pf_stage == kPfReady);
@@ -882,7 +888,9 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
           if (pf_stage == kPfReady && __popc(rdy & lt) < k) pf_stage = kPfNeed;
         }
         if (W == 64) mark(8);  // (64-wide: layer marks 6-9 are free) refill sub-steps
-        // LISTED -> READY: the slot arrived last tile; issue the ray-state loads
+      };
+      // LISTED -> READY: the slot arrived last tile; issue the ray-state loads
+      auto to_ready = [&]() {
         if (pf_stage == kPfListed) {
           fpx = __ldg(st.px + pf_slot);
           fpy = __ldg(st.py + pf_slot);
@@ -894,7 +902,9 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
           pf_stage = kPfReady;
         }
         if (W == 64) mark(9);
-        // NEED -> LISTED: claim list items (warp claims of `claim` items, one claim ahead)
+      };
+      // NEED -> LISTED: claim list items (warp claims of `claim` items, one claim ahead)
+      auto claim_items = [&]() {
         uint32_t need = __ballot_sync(0xffffffffu, pf_stage == kPfNeed);
         while (need && !exhausted) {
           if (res_base == res_end) {
@@ -916,10 +926,17 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
           need = __ballot_sync(0xffffffffu, pf_stage == kPfNeed);
         }
       };
+      auto advance = [&]() {
+        to_ready();
+        claim_items();
+      };
       if (g0)
-        for (int i = 0; i < 3; ++i) refill();  // prime: rows filled, prefetches claimed
+        for (int i = 0; i < 3; ++i) {  // prime: rows filled, prefetches claimed
+          assign();
+          advance();
+        }
       for (bool first = true;; first = false) {
-        if (g0 && !first) refill();
+        if (g0 && !first) assign();
         mark(14);
         // one barrier per tile: the live-row vote also orders every warp's staged appends of
         // the previous tile before the flush decision below
@@ -927,7 +944,10 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
         if (g0 && *sm.stage_count > kStageCap - kRows) stage_flush_now(st_adv, a.adv_list, a.adv_count, sm.stage_base, ctid);
         if (!live) {
           // no live row: either prefetches are still in flight (refill again) or done
-          if (bar_vote_any(3, 128 * kGroups, g0 && pf_stage != kPfNeed)) continue;
+          if (bar_vote_any(3, 128 * kGroups, g0 && pf_stage != kPfNeed)) {
+            if (g0) advance();
+            continue;
+          }
           break;
         }
         mark(15);
@@ -936,7 +956,8 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
           ++n_tiles;
         }
         const float p[3] = {px, py, pz};
-        const float acc = eval_tile(p, slot >= 0);
+        const float acc = eval_tile(
+            p, slot >= 0, [&] { if (g0) to_ready(); }, [&] { if (g0) claim_items(); });
         mark(11);
         if (g0) {
           const int s0 = slot;
@@ -999,7 +1020,7 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
         // prefetch: point of tile t+1 (slot known), list slot of tile t+2
         const RowIn next = t + 1 < my_tiles && eg == 0 ? load_row(a, slot_next) : RowIn{-1};
         slot_next = t + 2 < my_tiles && eg == 0 ? load_slot(a, item_of(t + 2), n_items) : -1;
-        const float acc_out = eval_tile(now.p, valid);
+        const float acc_out = eval_tile(now.p, valid, [] {}, [] {});
         if (eg == 0) {
           // ---- consumer (group 0) ----
           const float fval = (!kGrad || chain == 0) ? acc_out + net.bout : acc_out;
