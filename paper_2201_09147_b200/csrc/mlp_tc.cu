@@ -869,7 +869,16 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
         // READY prefetches -> empty rows (the k-th empty row takes the k-th ready lane)
         const uint32_t emp = __ballot_sync(0xffffffffu, slot < 0);
         const uint32_t rdy = __ballot_sync(0xffffffffu, pf_stage == kPfReady);
-        if (emp && rdy) {
+        if (emp && (emp & ~rdy) == 0) {
+          // common case: every empty row's own prefetch is ready (no shuffles)
+          if (slot < 0) {
+            slot = pf_slot;
+            it = 0;
+            px = fpx, py = fpy, pz = fpz, t = fpt, dx = fdx, dy = fdy, dz = fdz;
+            st.level_reached[slot] = a.lv.level;
+            pf_stage = kPfNeed;
+          }
+        } else if (emp && rdy) {
           const int k = min(__popc(emp), __popc(rdy));
           const int r = __popc(emp & lt);
           const bool take = slot < 0 && r < k;
