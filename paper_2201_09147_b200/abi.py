@@ -8,7 +8,8 @@ import ctypes
 import os
 
 PKG_DIR = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG_DIR, "libnsdf_cuda.so")
+# NSDF_CUDA_LIB: an alternative build of the engine for A/B timing (tools/ab.py); default in-tree
+LIB_PATH = os.environ.get("NSDF_CUDA_LIB") or os.path.join(PKG_DIR, "libnsdf_cuda.so")
 HOST_LIB_PATH = os.path.join(PKG_DIR, "libnsdf_b200.so")
 
 MAX_LEVELS = 8

@@ -935,6 +935,12 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
           need = __ballot_sync(0xffffffffu, pf_stage == kPfNeed);
         }
       };
+      bool pend_conv = false;
+      int pend_slot = -1;
+      auto append_pending = [&]() {
+        stage_append(pend_conv, pend_slot, st_adv);
+        pend_conv = false;
+      };
       auto advance = [&]() {
         to_ready();
         claim_items();
@@ -953,6 +959,7 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
         if (g0 && *sm.stage_count > kStageCap - kRows) stage_flush_now(st_adv, a.adv_list, a.adv_count, sm.stage_base, ctid);
         if (!live) {
           // no live row: either prefetches are still in flight (refill again) or done
+          if (g0) append_pending();
           if (bar_vote_any(3, 128 * kGroups, g0 && pf_stage != kPfNeed)) {
             if (g0) advance();
             continue;
@@ -966,7 +973,14 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
         }
         const float p[3] = {px, py, pz};
         const float acc = eval_tile(
-            p, slot >= 0, [&] { if (g0) to_ready(); }, [&] { if (g0) claim_items(); });
+            p, slot >= 0,
+            [&] {
+              if (g0) {
+                append_pending();
+                to_ready();
+              }
+            },
+            [&] { if (g0) claim_items(); });
         mark(11);
         if (g0) {
           const int s0 = slot;
@@ -1000,7 +1014,10 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
             }
           }
           mark(12);
-          stage_append(conv, s0, st_adv);
+          // the compaction append runs in the next tile's first tensor-core wait (off the
+          // update -> next point chain); the vote before every flush decision orders it
+          pend_conv = conv;
+          pend_slot = s0;
           mark(13);
         }
       }
