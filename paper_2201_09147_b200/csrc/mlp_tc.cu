@@ -3,9 +3,12 @@
 // A CTA evaluates tiles of 128 TMEM lanes: 128 rays (forward) or 32 rays x 4 chains (value +
 // 3 input tangents: the "width x 4" analytic-normal tile).  Per tile:
 //
-//   layer 0              a K = 32 MMA: A0 = the point split into three fp16 parts (+ ones for
-//                        the bias), B0 = fp16 hi/lo parts of omega*W0 and omega*b0 (built per
-//                        CTA at launch) -> D0 = omega*(W0 p + b0) in TMEM
+//   layer 0              a K = 32 MMA: A0 (TMEM) = the point split into three fp16 parts (+
+//                        ones for the bias), B0 = fp16 hi/lo parts of omega*W0 and omega*b0
+//                        (built per CTA at launch) -> D0 = omega*(W0 p + b0) in TMEM
+//   biases               hidden weights hold omega*W; one extra K = 16 MMA per hidden layer
+//                        (constant ones block x 3-part omega*b) -> every accumulator is the
+//                        sine argument in radians
 //   hidden layers        D[128 x W] (fp32, TMEM) = A[128 x W] (fp16 hi/lo, TMEM: written in
 //                        place over the previous layer's accumulator) . W_l^T (fp16
 //                        hi/lo): tcgen05.mma.cta_group::1.kind::f16, M=128 N=W K=16, three
@@ -257,7 +260,6 @@ constexpr int kK0 = 32;
 
 // Dynamic shared-memory carve-up.  SWIZZLE_NONE operands need 16-byte alignment only.
 struct TcSmem {
-  __half* a;            // [128 x 32] layer-0 A operand (A0); hidden layers keep A in TMEM
   __half* wst;          // resident hidden weights, or [kStages] streamed weight chunks
   __half* b0;           // [W x 32] layer-0 B operand
   __half* bb;           // [L-2][W x 16] bias B operand of each hidden layer: omega*b in 3 fp16 parts
@@ -282,7 +284,6 @@ __host__ __device__ inline size_t tc_weight_bytes(int W, int L, int terms, bool 
 
 __host__ __device__ inline size_t tc_smem_bytes(int W, int L, int terms, bool resident, bool persist) {
   size_t b = 0;
-  b += size_t(kRows) * kK0 * 2;  // A0 (the hidden layers' A lives in TMEM)
   b += tc_weight_bytes(W, L, terms, resident);
   b += size_t(W) * kK0 * 2;
   b += size_t(L - 2) * W * kBlk * 2 + size_t(kRows) * kBlk * 2;
@@ -302,7 +303,6 @@ __device__ inline TcSmem tc_carve(uint8_t* raw, int W, int L, int terms, bool re
     return p;
   };
   TcSmem s;
-  s.a = reinterpret_cast<__half*>(take(size_t(kRows) * kK0 * 2, 128));
   s.wst = reinterpret_cast<__half*>(take(tc_weight_bytes(W, L, terms, resident), 128));
   s.b0 = reinterpret_cast<__half*>(take(size_t(W) * kK0 * 2, 128));
   s.bb = reinterpret_cast<__half*>(take(size_t(L - 2) * W * kBlk * 2, 128));
@@ -594,7 +594,6 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
     // the whole warp runs this loop; MMAs and commits are issued by one elected lane
     {
       const uint32_t idesc = umma_idesc(W);
-      const uint32_t a_base = smem_addr(sm.a);
       const uint32_t b0_base = smem_addr(sm.b0);
       const uint64_t ones_desc = umma_desc(smem_addr(sm.ones), kRows * 16, 128);
       if (kResident) {
@@ -623,9 +622,8 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
         tc_fence_after();
 #pragma unroll
         for (int ks = 0; ks < kK0 / 16; ++ks) {
-          const uint64_t ad = umma_desc(a_base + uint32_t(ks * 2) * (kRows / 8) * 128, kRows * 16, 128);
           const uint64_t bd = umma_desc(b0_base + uint32_t(ks * 2) * (W / 8) * 128, W * 16, 128);
-          tc_mma(tmem, ad, bd, idesc, ks != 0);
+          tc_mma_ts(tmem, tmem + uint32_t(W + ks * 8), bd, idesc, ks != 0);
         }
         tc_commit(dfull);
         // ---- hidden layers, K-streamed behind the epilogue ----
@@ -757,12 +755,14 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
             w1 = chain == 3 ? pk2(one, zero) : 0u;
           }
         }
-        *reinterpret_cast<uint4*>(&sm.a[a_off(row, 0)]) = make_uint4(w0, w1, w2, w3);
-        *reinterpret_cast<uint4*>(&sm.a[a_off(row, 8)]) = make_uint4(w4, w0, w1, w2);
-        *reinterpret_cast<uint4*>(&sm.a[a_off(row, 16)]) = make_uint4(w8, 0u, 0u, 0u);
-        *reinterpret_cast<uint4*>(&sm.a[a_off(row, 24)]) = make_uint4(0u, 0u, 0u, 0u);
+        // A0 in TMEM, columns 0-15 of region 1 (K pairs packed per column, 8 columns per
+        // K = 16 step): region 1 is free here — it held the last layer's accumulator (read by
+        // this thread's own earlier loads; the other groups never read block 0) or, for an
+        // even hidden-layer count, an A operand whose MMAs have completed
+        tmem_st8(taddr + uint32_t(W), w0, w1, w2, w3, w4, w0, w1, w2);
+        tmem_st8(taddr + uint32_t(W) + 8u, w8, 0u, 0u, 0u, 0u, 0u, 0u, 0u);
+        tmem_wait_st();
         mark(10);
-        fence_proxy_async();
       }
       // every epilogue thread: done with the previous tile's TMEM (region 0 is reused)
       tc_fence_before();
