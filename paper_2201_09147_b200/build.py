@@ -62,6 +62,8 @@ def build_cuda(force=False, verbose=False):
     for src, extra in CUDA_SOURCES.items():
         if timeline and src == "mlp_tc.cu":
             extra = extra + ["-DNSDF_TC_TIMELINE_BUILD=1"]
+        if src == "mlp_tc.cu" and os.environ.get("NSDF_TC_DEFINES"):  # A/B builds (tools/ab.py)
+            extra = extra + os.environ["NSDF_TC_DEFINES"].split()
         s = os.path.join(CSRC, src)
         o = os.path.join(OBJ, src + ".o")
         objs.append(o)
