@@ -656,6 +656,31 @@ def main():
         act_bound = {"sines_per_frame": sines, "achieved_per_s": sines / (trace_ms / 1e3) if trace_ms > 0 else 0.0,
                      "peak_per_s": xu_peak, "frac": sines / (trace_ms / 1e3) / xu_peak if trace_ms > 0 else 0.0,
                      "note": "MUFU (XU pipe) sine throughput of the trace kernels; 64/128-wide nets are sine-bound"}
+        # each kernel against its own bound: tensor work ISSUED by the fast mode (3 split-precision
+        # terms per hidden K step + the K=32 layer-0 MMA + the K=16 bias MMA per hidden layer)
+        # vs the sustained tensor peak, and MUFU sines vs 16/clk/SM at the max SM clock
+        mult = 3 if args.mode == "fp16" else 1
+        per_kernel = []
+        for j, m in enumerate(seq.members):
+            w, hb = m.width, m.hidden_blocks
+            ev, ms_j = int(stats.evals[j]), prof.level_ms[j] / max(prof.frames, 1)
+            if ev == 0 or ms_j <= 0:
+                continue
+            issued = ev * (2 * 32 * w + hb * (mult * 2 * w * w + 2 * 16 * w))
+            sn = ev * (m.n_layers - 1) * w
+            per_kernel.append({"kernel": f"trace level {j} ({w}x{hb})", "ms": ms_j, "evals": ev,
+                               "tflops_algorithmic": ev * 2 * m.macs_forward() / (ms_j / 1e3) / 1e12,
+                               "tensor_issued_frac": issued / (ms_j / 1e3) / 1e12 / peak_tf,
+                               "mufu_frac": sn / (ms_j / 1e3) / xu_peak})
+        if normals_ms > 0 and int(stats.normal_evals):
+            m = seq.members[normal_idx]
+            w, hb, ev = m.width, m.hidden_blocks, int(stats.normal_evals)
+            issued = 4 * ev * (2 * 32 * w + hb * (mult * 2 * w * w + 2 * 16 * w))
+            per_kernel.append({"kernel": f"normal tiles + shading ({w}x{hb}, 4 rows per hit)", "ms": normals_ms,
+                               "evals": ev, "tflops_algorithmic": flops_normals / (normals_ms / 1e3) / 1e12,
+                               "tensor_issued_frac": issued / (normals_ms / 1e3) / 1e12 / peak_tf,
+                               "mufu_frac": 4 * ev * (m.n_layers - 1) * w / (normals_ms / 1e3) / xu_peak})
+        act_bound["per_kernel"] = per_kernel
         frame = {"evals_per_level": [int(x) for x in list(stats.evals)[:len(seq.members)]], "hits": int(stats.hits),
                  "fallbacks": int(stats.fallback_evals), "tflop_trace": flops_trace / 1e12,
                  "tflop_normals": flops_normals / 1e12, "trace_ms": trace_ms, "normals_ms": normals_ms,
