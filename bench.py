@@ -350,7 +350,7 @@ def run_e2e(args, ctx, ds, seq, stream, world, rank, W):
             W["step"](i)
             if rank == 0:
                 if peer is not None:
-                    W["lanes"][i % len(W["lanes"])][1].synchronize()
+                    W["tok_ev"][i % (2 * len(W["lanes"]))].synchronize()  # every rank's tiles of frame i
                     peer.to_host(i % (2 * len(W["lanes"])), *(t.data_ptr() for t in hb))
                 else:
                     torch.cuda.current_stream().wait_stream(W["gstream"])
@@ -384,7 +384,8 @@ def tile_pass(args, ctx, W, world, rank, Wd, Hd):
     if not peer.ok:
         peer.close()
         return {"unavailable": f"peer framebuffer: {peer.reason}"}
-    tok = [torch.zeros(1, dtype=torch.int32, device="cuda") for _ in lanes]
+    tok = torch.zeros(1, dtype=torch.int32, device="cuda")
+    cs = torch.cuda.Stream()  # every token all-reduce on ONE stream, in frame order
     lv = [d.levels() for _, _, d in lanes]
 
     def frame(i):
@@ -392,8 +393,11 @@ def tile_pass(args, ctx, W, world, rank, Wd, Hd):
         fr, fd, fm = peer.ptrs(i % (2 * len(lanes)))
         c.render_device(lv[i % len(lanes)], W["cam"], W["cfg"], W["shade"], fr, fd, fm, W["src"], -1, args.tile, rank,
                         world)
-        with torch.cuda.stream(st):
-            dist.all_reduce(tok[i % len(lanes)])
+        ev = torch.cuda.Event()
+        ev.record(st)
+        cs.wait_event(ev)
+        with torch.cuda.stream(cs):
+            dist.all_reduce(tok)
 
     n = max(2 * len(lanes), min(args.steps, 30))
     for i in range(max(3, len(lanes))):
@@ -409,6 +413,7 @@ def tile_pass(args, ctx, W, world, rank, Wd, Hd):
         frame(i)
     for _, st, _ in lanes[1:]:
         stream.wait_stream(st)
+    stream.wait_stream(cs)
     e1.record(stream)
     torch.cuda.synchronize()
     t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
@@ -527,7 +532,13 @@ def main():
             if peer is None:
                 gather = scheduler.TileGather(Wd, Hd, args.tile, rank, world)
         W["gather"], W["peer"] = gather, peer
-        tok = [torch.zeros(1, dtype=torch.int32, device="cuda") for _ in lanes]
+        # frame-completion tokens: one 4-byte all-reduce per frame, all on ONE stream (tstream) in
+        # frame order, each behind its frame's kernels (an event on the lane stream), so every
+        # rank issues and executes the collectives in the same order
+        tok = torch.zeros(1, dtype=torch.int32, device="cuda")
+        tstream = torch.cuda.Stream() if peer is not None else None
+        tok_ev = [None] * (2 * len(lanes))
+        W["tok_ev"] = tok_ev
         n_fb = max(len(lanes), 2 if gather is not None else 1)
         fbs = [(rgb, depth, mask)] + [(torch.zeros_like(rgb), torch.zeros_like(depth), torch.zeros_like(mask))
                                       for _ in range(n_fb - 1)]
@@ -535,6 +546,7 @@ def main():
         gstream = torch.cuda.Stream() if gather is not None else None
         free_ev = [None] * n_fb
         W["gstream"] = gstream
+        W["tstream"] = tstream
         if animated:
             lane_levels = [frame_levels] + [[d.levels(time=i / (cfgw["frames"] - 1)) for i in my_frames]
                                             for _, _, d in lanes[1:]]
@@ -551,8 +563,14 @@ def main():
                 fr, fd, fm = peer.ptrs(i % (2 * len(lanes)))
                 c.render_device(lv, W["cam"], cfg, W["shade"], fr, fd, fm, W["src"], -1, args.tile, tile_rank,
                                 tile_world)
-                with torch.cuda.stream(st):
-                    dist.all_reduce(tok[li])
+                ev = torch.cuda.Event()
+                ev.record(st)
+                tstream.wait_event(ev)
+                with torch.cuda.stream(tstream):
+                    dist.all_reduce(tok)
+                    done = torch.cuda.Event()
+                    done.record(tstream)
+                tok_ev[i % (2 * len(lanes))] = done
                 return
             b = i % n_fb
             if free_ev[b] is not None:
@@ -580,7 +598,8 @@ def main():
 
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
-    side = [st for _, st, _ in W.get("lanes", [])[1:]] + ([W["gstream"]] if W.get("gstream") is not None else [])
+    side = [st for _, st, _ in W.get("lanes", [])[1:]] + [x for x in (W.get("gstream"), W.get("tstream"))
+                                                          if x is not None]
     with ClockSampler(local) as clocks:
         for i in range(args.warmup):
             step(i)
