@@ -194,10 +194,11 @@ __device__ __forceinline__ uint32_t pack_half2(float a, float b) {
   return *reinterpret_cast<uint32_t*>(&h);
 }
 // Low parts of a split-precision pair: fp16(x - float(fp16(x))).
+// (one packed FFMA2: a - hi exactly, for both values of the pair)
 __device__ __forceinline__ uint32_t pack_half2_lo(float a, float b, uint32_t hi) {
   const __half2 h = *reinterpret_cast<const __half2*>(&hi);
-  const float2 f = __half22float2(h);
-  return pack_half2(a - f.x, b - f.y);
+  const float2 d = __ffma2_rn(__half22float2(h), make_float2(-1.0f, -1.0f), make_float2(a, b));
+  return pack_half2(d.x, d.y);
 }
 
 // ---- kernel parameters -------------------------------------------------------------------
@@ -770,7 +771,7 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
       if (lane == 0) mbar_arrive(a0ready);
       mark(1);
       gap0();
-      float acc_out = 0.0f;
+      float2 acc2 = make_float2(0.0f, 0.0f);
       // one MMA layer's epilogue; the last one (compile-time) folds in the output dot
       auto layer = [&](int m, auto last_tag) {
         constexpr bool last = decltype(last_tag)::value;
@@ -830,8 +831,10 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
             __syncwarp();
             if (lane == 0) mbar_arrive(&kready[i]);
           } else {
+            // the 1 x W output layer as packed FFMA2s (two partial sums per thread)
+            const float2* wo = reinterpret_cast<const float2*>(sm.wout + cc);
 #pragma unroll
-            for (int j = 0; j < 16; ++j) acc_out = fmaf(sm.wout[cc + j], v[j], acc_out);
+            for (int j = 0; j < 8; ++j) acc2 = __ffma2_rn(wo[j], make_float2(v[2 * j], v[2 * j + 1]), acc2);
           }
         }
         mark(3 + 2 * min(m, 3));
@@ -839,6 +842,7 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
 #pragma unroll
       for (int m = 0; m < n_hidden; ++m) layer(m, std::false_type{});
       layer(n_hidden, std::true_type{});
+      float acc_out = acc2.x + acc2.y;
       ++dbg_t;
       // ---- combine the column groups' partial output dots ----
       if (kGroups > 1) {
