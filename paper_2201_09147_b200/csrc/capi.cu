@@ -62,6 +62,35 @@ struct DeviceGuard {
 
 }  // namespace
 
+// Copy streams + events of the chunked host-buffer batches (run_chunked), created on first use.
+struct BatchPipe {
+  cudaStream_t in = nullptr, out = nullptr;
+  cudaEvent_t ev_in[2] = {}, ev_k[2] = {}, ev_out[2] = {}, start = nullptr;
+  cudaError_t init() {
+    if (in) return cudaSuccess;
+    cudaError_t e = cudaStreamCreateWithFlags(&in, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&out, cudaStreamNonBlocking);
+    for (int b = 0; b < 2 && e == cudaSuccess; ++b) {
+      e = cudaEventCreateWithFlags(&ev_in[b], cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_k[b], cudaEventDisableTiming);
+      if (e == cudaSuccess) e = cudaEventCreateWithFlags(&ev_out[b], cudaEventDisableTiming);
+    }
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&start, cudaEventDisableTiming);
+    return e;
+  }
+  void release() {
+    for (int b = 0; b < 2; ++b) {
+      if (ev_in[b]) cudaEventDestroy(ev_in[b]);
+      if (ev_k[b]) cudaEventDestroy(ev_k[b]);
+      if (ev_out[b]) cudaEventDestroy(ev_out[b]);
+    }
+    if (start) cudaEventDestroy(start);
+    if (in) cudaStreamDestroy(in);
+    if (out) cudaStreamDestroy(out);
+    *this = BatchPipe();
+  }
+};
+
 struct nsdf_ctx {
   int device = 0;
   cudaStream_t own = nullptr;
@@ -73,6 +102,7 @@ struct nsdf_ctx {
   Workspace frame;   // ray state, lists, counters
   Workspace io;      // API staging: points, outputs, framebuffers, records
   Profiler prof;
+  BatchPipe pipe;    // chunked host-buffer batches
 };
 
 namespace {
@@ -402,6 +432,7 @@ int nsdf_cuda_destroy(nsdf_ctx* c) {
     new (&c->frame) Workspace();
     c->io.~Workspace();
     new (&c->io) Workspace();
+    c->pipe.release();
     if (c->own) cudaStreamDestroy(c->own);
   }
   delete c;
@@ -698,6 +729,98 @@ int nsdf_cuda_eval_grad_device(nsdf_ctx* c, nsdf_field h, const float* d_points,
   return NSDF_OK;
 }
 
+}  // extern "C"
+
+namespace {
+
+// Host-buffer batch API over column chunks (points and outputs are rows x k, row-major, in
+// pageable host memory as the reference's Matrix<float> is): the H2D of chunk i+1, the tiles
+// of chunk i and the D2H of chunk i-1 run concurrently (copy-in stream, engine stream,
+// copy-out stream) on double-buffered device chunks, so the host copies overlap the kernels
+// instead of bracketing them.  launch(d_in[], d_out[], n) enqueues chunk kernels on c->stream.
+struct HostIn {
+  const float* h;
+  int rows;
+};
+struct HostOut {
+  float* h;
+  int rows;
+};
+constexpr int kBatchChunk = 65536;
+
+// counters: optional 2 x u64 device counters (zeroed first), placed after the chunk buffers.
+template <class Launch>
+int run_chunked(nsdf_ctx* c, int k, const std::vector<HostIn>& ins, const std::vector<HostOut>& outs, Launch launch,
+                unsigned long long** counters = nullptr) {
+  const int chunk = k <= 2 * kBatchChunk ? k : kBatchChunk;
+  const int n_chunks = (k + chunk - 1) / chunk;
+  int rows_in = 0, rows_out = 0;
+  for (const HostIn& x : ins) rows_in += x.h ? x.rows : 0;
+  for (const HostOut& x : outs) rows_out += x.h ? x.rows : 0;
+  NSDF_CUDA(c->pipe.init());
+  NSDF_CUDA(c->io.reserve(size_t(2) * chunk * (rows_in + rows_out) * 4 + 4096));
+  BatchPipe& p = c->pipe;
+  cudaStream_t s = c->stream;
+  float* base = static_cast<float*>(c->io.base);
+  if (counters) {
+    *counters = reinterpret_cast<unsigned long long*>(base + size_t(2) * chunk * (rows_in + rows_out) + 64);
+    NSDF_CUDA(cudaMemsetAsync(*counters, 0, 16, s));
+  }
+  auto din = [&](int b, int j) {  // input j of buffer b
+    size_t off = size_t(b) * chunk * (rows_in + rows_out);
+    for (int q = 0; q < j; ++q) off += size_t(ins[q].h ? ins[q].rows : 0) * chunk;
+    return base + off;
+  };
+  auto dout = [&](int b, int j) {
+    size_t off = size_t(b) * chunk * (rows_in + rows_out) + size_t(rows_in) * chunk;
+    for (int q = 0; q < j; ++q) off += size_t(outs[q].h ? outs[q].rows : 0) * chunk;
+    return base + off;
+  };
+  NSDF_CUDA(cudaEventRecord(p.start, s));  // earlier work on the engine stream first
+  NSDF_CUDA(cudaStreamWaitEvent(p.in, p.start, 0));
+  NSDF_CUDA(cudaStreamWaitEvent(p.out, p.start, 0));
+  auto copy_out = [&](int i) -> int {
+    const int b = i & 1, c0 = i * chunk, n = std::min(chunk, k - c0);
+    NSDF_CUDA(cudaStreamWaitEvent(p.out, p.ev_k[b], 0));
+    for (size_t j = 0; j < outs.size(); ++j)
+      if (outs[j].h)
+        NSDF_CUDA(cudaMemcpy2DAsync(outs[j].h + c0, size_t(k) * 4, dout(b, int(j)), size_t(n) * 4, size_t(n) * 4,
+                                    outs[j].rows, cudaMemcpyDeviceToHost, p.out));
+    NSDF_CUDA(cudaEventRecord(p.ev_out[b], p.out));
+    return NSDF_OK;
+  };
+  for (int i = 0; i < n_chunks; ++i) {
+    const int b = i & 1, c0 = i * chunk, n = std::min(chunk, k - c0);
+    if (i >= 2) NSDF_CUDA(cudaStreamWaitEvent(p.in, p.ev_k[b], 0));  // chunk i-2 read buffer b
+    for (size_t j = 0; j < ins.size(); ++j)
+      if (ins[j].h)
+        NSDF_CUDA(cudaMemcpy2DAsync(din(b, int(j)), size_t(n) * 4, ins[j].h + c0, size_t(k) * 4, size_t(n) * 4,
+                                    ins[j].rows, cudaMemcpyHostToDevice, p.in));
+    NSDF_CUDA(cudaEventRecord(p.ev_in[b], p.in));
+    NSDF_CUDA(cudaStreamWaitEvent(s, p.ev_in[b], 0));
+    if (i >= 2) NSDF_CUDA(cudaStreamWaitEvent(s, p.ev_out[b], 0));  // chunk i-2's outputs copied
+    const float* di[2] = {ins.size() > 0 && ins[0].h ? din(b, 0) : nullptr,
+                          ins.size() > 1 && ins[1].h ? din(b, 1) : nullptr};
+    float* dd[2] = {outs.size() > 0 && outs[0].h ? dout(b, 0) : nullptr,
+                    outs.size() > 1 && outs[1].h ? dout(b, 1) : nullptr};
+    launch(di, dd, n);
+    NSDF_CUDA(cudaGetLastError());
+    NSDF_CUDA(cudaEventRecord(p.ev_k[b], s));
+    // the previous chunk's D2H after this chunk's kernels are queued (a pageable D2H returns
+    // only when done, so queueing it first would idle the GPU behind the host)
+    if (i >= 1)
+      if (int st = copy_out(i - 1)) return st;
+  }
+  if (int st = copy_out(n_chunks - 1)) return st;
+  NSDF_CUDA(cudaStreamSynchronize(p.out));
+  NSDF_CUDA(cudaStreamSynchronize(s));
+  return NSDF_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
 int nsdf_cuda_eval_grad(nsdf_ctx* c, nsdf_field h, const float* points, int rows, int k, float time, float* out,
                         float* grad) {
   if (!c) return fail(NSDF_ERR_CONTRACT, "context is null");
@@ -708,19 +831,12 @@ int nsdf_cuda_eval_grad(nsdf_ctx* c, nsdf_field h, const float* points, int rows
   if (int st = check_points(f, rows, k)) return st;
   if (k == 0) return NSDF_OK;
   if (!points) return fail(NSDF_ERR_CONTRACT, "points is null");
-  size_t off = 0;
-  NSDF_CUDA(c->io.reserve(size_t(k) * (rows + 4) * 4 + 4096));
-  float* dp = carve<float>(c->io.base, off, size_t(rows) * k);
-  float* dout = carve<float>(c->io.base, off, size_t(k));
-  float* dgrad = carve<float>(c->io.base, off, size_t(3) * k);
-  cudaStream_t s = c->stream;
-  NSDF_CUDA(cudaMemcpyAsync(dp, points, size_t(rows) * k * 4, cudaMemcpyHostToDevice, s));
-  launch_eval(mode_of(c), f->dev, dp, rows, k, time, out ? dout : (grad ? nullptr : dout), grad ? dgrad : nullptr, s);
-  NSDF_CUDA(cudaGetLastError());
-  if (out) NSDF_CUDA(cudaMemcpyAsync(out, dout, size_t(k) * 4, cudaMemcpyDeviceToHost, s));
-  if (grad) NSDF_CUDA(cudaMemcpyAsync(grad, dgrad, size_t(3) * k * 4, cudaMemcpyDeviceToHost, s));
-  NSDF_CUDA(cudaStreamSynchronize(s));
-  return NSDF_OK;
+  if (!out && !grad) return NSDF_OK;
+  const Mode mode = mode_of(c);
+  return run_chunked(c, k, {{points, rows}}, {{out, 1}, {grad, 3}},
+                     [&](const float* const* di, float* const* dd, int n) {
+                       launch_eval(mode, f->dev, di[0], rows, n, time, dd[0], dd[1], c->stream);
+                     });
 }
 
 int nsdf_cuda_eval(nsdf_ctx* c, nsdf_field h, const float* points, int rows, int k, float time, float* out) {
@@ -930,20 +1046,18 @@ int nsdf_cuda_normal_map(nsdf_ctx* c, nsdf_field fine, float time, const float* 
   if (outside_count) *outside_count = 0;
   if (fallback_count) *fallback_count = 0;
   if (k == 0) return NSDF_OK;
-  size_t off = 0;
-  NSDF_CUDA(c->io.reserve(size_t(k) * 36 + 8192));
-  float* dp = carve<float>(c->io.base, off, size_t(3) * k);
-  float* dfb = carve<float>(c->io.base, off, size_t(3) * k);
-  float* dn = carve<float>(c->io.base, off, size_t(3) * k);
-  unsigned long long* dc = carve<unsigned long long>(c->io.base, off, 2);
+  if (!points || !normals) return fail(NSDF_ERR_CONTRACT, "points / normals is null");
   cudaStream_t s = c->stream;
-  NSDF_CUDA(cudaMemcpyAsync(dp, points, size_t(k) * 12, cudaMemcpyHostToDevice, s));
-  if (fallback_normals) NSDF_CUDA(cudaMemcpyAsync(dfb, fallback_normals, size_t(k) * 12, cudaMemcpyHostToDevice, s));
-  NSDF_CUDA(cudaMemsetAsync(dc, 0, 16, s));
-  launch_normal_map(mode_of(c), f->dev, dp, k, time, delta, fallback_normals ? dfb : nullptr, dn, dc, s);
-  NSDF_CUDA(cudaGetLastError());
+  const Mode mode = mode_of(c);
+  unsigned long long* dc = nullptr;
+  if (int st = run_chunked(
+          c, k, {{points, 3}, {fallback_normals, 3}}, {{normals, 3}},
+          [&](const float* const* di, float* const* dd, int n) {
+            launch_normal_map(mode, f->dev, di[0], n, time, delta, di[1], dd[0], dc, s);
+          },
+          &dc))
+    return st;
   unsigned long long hc[2];
-  NSDF_CUDA(cudaMemcpyAsync(normals, dn, size_t(k) * 12, cudaMemcpyDeviceToHost, s));
   NSDF_CUDA(cudaMemcpyAsync(hc, dc, 16, cudaMemcpyDeviceToHost, s));
   NSDF_CUDA(cudaStreamSynchronize(s));
   if (outside_count) *outside_count = hc[0];
