@@ -1,4 +1,4 @@
-import os, sys, time
+"""Host enqueue rate of render_device frames vs their GPU time (is the frame launch-bound?).
 sys.path.insert(0, os.getcwd())
 import torch
 import bench
