@@ -1,4 +1,8 @@
 """Host enqueue rate of render_device frames vs their GPU time (is the frame launch-bound?).
+
+    python tools/hostrate.py
+"""
+import os, sys, time
 sys.path.insert(0, os.getcwd())
 import torch
 import bench
