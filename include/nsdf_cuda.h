@@ -29,6 +29,11 @@
  *   nsdf_cuda_render          shading::render                           src/shading/render.cpp:12-82
  *   nsdf_cuda_render_device   shading::render, device-resident framebuffer + tile sharding
  *                             (the multi-GPU frame/tile scheduler's per-rank call)
+ *   nsdf_cuda_tensor_gemm     tensor::kernels::Table::gemm_f32 / gemm_f64, tensor::gemm
+ *                             include/nsdf/tensor/kernels.hpp:26-29, src/tensor/ops.cpp:24-41
+ *   nsdf_cuda_tensor_hadamard Table::hadamard_f32 / _f64, tensor::hadamard   kernels.hpp:31-32, ops.cpp:43-55
+ *   nsdf_cuda_tensor_scale_rows Table::scale_rows_f32 / _f64, tensor::scale_rows kernels.hpp:34-36, ops.cpp:81-95
+ *   nsdf_cuda_tensor_sine     Table::sine_f32 / _f64, tensor::activate (sine) kernels.hpp:38-39, ops.cpp:57-79
  *   nsdf_cuda_render_multi    shading::render over N contexts (N GPUs) from one process:
  *                             interleaved tiles per context, gathered into a host framebuffer
  *                             (SURVEY.md §8b "nsdf_cuda_render_multi(ctxs[], n, ...)")
@@ -243,6 +248,24 @@ int nsdf_cuda_eval_grad_device(nsdf_ctx* ctx, nsdf_field field, const float* d_p
  * Analytic fields return NSDF_ERR_CONFIG (they evaluate on the host). */
 int nsdf_cuda_eval_f64(nsdf_ctx* ctx, nsdf_field field, const double* points, int rows, int k,
                        double time, double* out, double* grad);
+
+/* ---- the reference's dense kernel table on the device ---------------------------------
+ * HOST buffers, row-major; dtype NSDF_DTYPE_F32 (float) or NSDF_DTYPE_F64 (double).
+ * Bit-exact with the reference's AVX2 backend (kernels_avx2.cpp): gemm c[m x n] = a[m x k] .
+ * b[k x n] (+ bias[m], may be NULL), each output one k-sequential fma chain from the bias (or
+ * 0); hadamard out = a * b (n elements); scale_rows out[i,j] = col[i] * m[i,j]; sine out =
+ * sin(omega*x), or omega*cos(omega*x) when derivative != 0 (f32: omega rounded to float).
+ * Shape checks are the caller's (tensor::gemm etc. in the drop-in library throw the
+ * reference's contract errors). */
+#define NSDF_DTYPE_F32 0
+#define NSDF_DTYPE_F64 1
+int nsdf_cuda_tensor_gemm(nsdf_ctx* ctx, int dtype, const void* a, const void* b, const void* bias, void* c,
+                          int m, int n, int k);
+int nsdf_cuda_tensor_hadamard(nsdf_ctx* ctx, int dtype, const void* a, const void* b, void* out, size_t n);
+int nsdf_cuda_tensor_scale_rows(nsdf_ctx* ctx, int dtype, const void* col, const void* m, void* out, int rows,
+                                int cols);
+int nsdf_cuda_tensor_sine(nsdf_ctx* ctx, int dtype, const void* x, void* out, size_t n, double omega,
+                          int derivative);
 
 /* ---- training (FP64, bit-exact with the reference trainer) ----------------------------
  * Packed parameters as in nsdf_cuda_upload_mlp.  backprop: trainer::backprop_sine_mlp

@@ -118,6 +118,32 @@ tensor::Matrix<float> points_matrix(const float* pts, int rows, int k) {
 
 }  // namespace
 
+// tensor::gemm / hadamard / activate(sine) / scale_rows (ops.cpp:24-95) through the reference's
+// active kernel backend; dtype 0 = float, 1 = double; op 0 gemm (a m x k, b k x n, bias m or
+// null -> c m x n), 1 hadamard (a, b: m x n), 2 sine (a m x n, omega, derivative), 3
+// scale_rows (a = col m x 1, b m x n).
+namespace {
+template <typename T>
+int ref_tensor(int op, const T* a, const T* b, const T* bias, T* out, int m, int n, int k, double omega,
+               int derivative) {
+  auto mat = [](const T* p, int r, int c) { return tensor::Matrix<T>(r, c, std::vector<T>(p, p + size_t(r) * c)); };
+  tensor::Matrix<T> res;
+  if (op == 0) {
+    tensor::Matrix<T> bm;
+    if (bias) bm = mat(bias, m, 1);
+    res = tensor::gemm(mat(a, m, k), mat(b, k, n), bias ? &bm : nullptr);
+  } else if (op == 1) {
+    res = tensor::hadamard(mat(a, m, n), mat(b, m, n));
+  } else if (op == 2) {
+    res = tensor::activate(mat(a, m, n), tensor::ActivationSpec::sine(omega), derivative != 0);
+  } else {
+    res = tensor::scale_rows(mat(a, m, 1), mat(b, m, n));
+  }
+  std::copy(res.data(), res.data() + res.size(), out);
+  return 0;
+}
+}  // namespace
+
 extern "C" {
 
 const char* nsdf_ref_last_error(void) { return g_error.c_str(); }
@@ -133,6 +159,19 @@ int nsdf_ref_set_backend(const char* name) {
 }
 
 const char* nsdf_ref_backend(void) { return tensor::backend_name(tensor::active_backend()); }
+
+
+int nsdf_ref_tensor(int op, int dtype, const void* a, const void* b, const void* bias, void* out, int m, int n, int k,
+                    double omega, int derivative) {
+  SHIM_TRY
+  if (dtype == 1)
+    ref_tensor<double>(op, static_cast<const double*>(a), static_cast<const double*>(b),
+                       static_cast<const double*>(bias), static_cast<double*>(out), m, n, k, omega, derivative);
+  else
+    ref_tensor<float>(op, static_cast<const float*>(a), static_cast<const float*>(b), static_cast<const float*>(bias),
+                      static_cast<float*>(out), m, n, k, omega, derivative);
+  SHIM_CATCH
+}
 
 // mlp::random_init (mlp.cpp:63-88) with Rng(seed); writes the packed layout.
 int nsdf_ref_random_init(int width, int hidden, int input_dim, double omega0, uint64_t seed,

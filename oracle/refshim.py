@@ -53,6 +53,21 @@ def set_backend(name="avx2"):
     _check(lib, lib.nsdf_ref_set_backend(name.encode()))
 
 
+def tensor_op(op, a, b=None, bias=None, m=0, n=0, k=0, omega=30.0, derivative=False):
+    """tensor::gemm (op 0) / hadamard (1) / activate sine (2) / scale_rows (3) of the reference
+    (nsdf_ref_tensor); arrays float32 or float64, row-major; returns the m x n result."""
+    lib = load()
+    dt = np.asarray(a).dtype
+    a = np.ascontiguousarray(a, dt)
+    b = None if b is None else np.ascontiguousarray(b, dt)
+    bias = None if bias is None else np.ascontiguousarray(bias, dt)
+    out = np.zeros((m, n), dt)
+    vp = lambda x: None if x is None else x.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
+    _check(lib, lib.nsdf_ref_tensor(op, 1 if dt == np.float64 else 0, vp(a), vp(b), vp(bias), vp(out), m, n, k,
+                                    D(omega), 1 if derivative else 0))
+    return out
+
+
 def worker_threads() -> int:
     return load().nsdf_ref_worker_threads()
 

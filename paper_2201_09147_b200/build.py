@@ -31,6 +31,7 @@ CUDA_SOURCES = {
     "mlp_tc.cu": [],
     "mlp_f64.cu": ["-fmad=false"],
     "train_f64.cu": ["-fmad=false"],
+    "tensor_ops.cu": ["-fmad=false"],
 }
 
 

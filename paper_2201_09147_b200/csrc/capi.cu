@@ -839,6 +839,90 @@ int nsdf_cuda_eval_grad(nsdf_ctx* c, nsdf_field h, const float* points, int rows
                      });
 }
 
+// ---- dense kernel table (tensor_ops.cu) -------------------------------------------------
+static int tensor_io(nsdf_ctx* c, int dtype, std::initializer_list<std::pair<const void*, size_t>> ins,
+                     std::pair<void*, size_t> out, void** dev_in, void** dev_out) {
+  if (dtype != NSDF_DTYPE_F32 && dtype != NSDF_DTYPE_F64) return fail(NSDF_ERR_CONTRACT, "unknown dtype");
+  const size_t es = dtype == NSDF_DTYPE_F64 ? 8 : 4;
+  size_t total = out.second * es + 256;
+  for (const auto& x : ins) total += x.second * es + 256;
+  NSDF_CUDA(c->io.reserve(total));
+  size_t off = 0;
+  int i = 0;
+  for (const auto& x : ins) {
+    dev_in[i] = static_cast<char*>(c->io.base) + off;
+    if (x.first && x.second) NSDF_CUDA(cudaMemcpyAsync(dev_in[i], x.first, x.second * es, cudaMemcpyHostToDevice, c->stream));
+    if (!x.first) dev_in[i] = nullptr;
+    off += (x.second * es + 255) / 256 * 256;
+    ++i;
+  }
+  *dev_out = static_cast<char*>(c->io.base) + off;
+  return NSDF_OK;
+}
+
+static int tensor_finish(nsdf_ctx* c, void* host_out, const void* dev_out, size_t bytes) {
+  NSDF_CUDA(cudaGetLastError());
+  if (bytes) NSDF_CUDA(cudaMemcpyAsync(host_out, dev_out, bytes, cudaMemcpyDeviceToHost, c->stream));
+  NSDF_CUDA(cudaStreamSynchronize(c->stream));
+  return NSDF_OK;
+}
+
+int nsdf_cuda_tensor_gemm(nsdf_ctx* c, int dtype, const void* a, const void* b, const void* bias, void* out, int m,
+                          int n, int k) {
+  if (!c) return fail(NSDF_ERR_CONTRACT, "context is null");
+  if (m < 0 || n < 0 || k < 0) return fail(NSDF_ERR_CONTRACT, "gemm: negative dimension");
+  if ((size_t(m) * k && !a) || (size_t(k) * n && !b) || (size_t(m) * n && !out))
+    return fail(NSDF_ERR_CONTRACT, "gemm: null buffer");
+  std::lock_guard<std::mutex> lk(c->mu);
+  DeviceGuard g(c->device);
+  void* d[3];
+  void* dc;
+  if (int st = tensor_io(c, dtype, {{a, size_t(m) * k}, {b, size_t(k) * n}, {bias, bias ? size_t(m) : 0}},
+                         {out, size_t(m) * n}, d, &dc))
+    return st;
+  launch_tensor_gemm(dtype == NSDF_DTYPE_F64, d[0], d[1], d[2], dc, m, n, k, c->stream);
+  return tensor_finish(c, out, dc, size_t(m) * n * (dtype == NSDF_DTYPE_F64 ? 8 : 4));
+}
+
+int nsdf_cuda_tensor_hadamard(nsdf_ctx* c, int dtype, const void* a, const void* b, void* out, size_t n) {
+  if (!c) return fail(NSDF_ERR_CONTRACT, "context is null");
+  if (n && (!a || !b || !out)) return fail(NSDF_ERR_CONTRACT, "hadamard: null buffer");
+  std::lock_guard<std::mutex> lk(c->mu);
+  DeviceGuard g(c->device);
+  void* d[2];
+  void* dc;
+  if (int st = tensor_io(c, dtype, {{a, n}, {b, n}}, {out, n}, d, &dc)) return st;
+  launch_tensor_hadamard(dtype == NSDF_DTYPE_F64, d[0], d[1], dc, n, c->stream);
+  return tensor_finish(c, out, dc, n * (dtype == NSDF_DTYPE_F64 ? 8 : 4));
+}
+
+int nsdf_cuda_tensor_scale_rows(nsdf_ctx* c, int dtype, const void* col, const void* m, void* out, int rows,
+                                int cols) {
+  if (!c) return fail(NSDF_ERR_CONTRACT, "context is null");
+  if (rows < 0 || cols < 0) return fail(NSDF_ERR_CONTRACT, "scale_rows: negative dimension");
+  if (size_t(rows) * cols && (!col || !m || !out)) return fail(NSDF_ERR_CONTRACT, "scale_rows: null buffer");
+  std::lock_guard<std::mutex> lk(c->mu);
+  DeviceGuard g(c->device);
+  void* d[2];
+  void* dc;
+  if (int st = tensor_io(c, dtype, {{col, size_t(rows)}, {m, size_t(rows) * cols}}, {out, size_t(rows) * cols}, d, &dc))
+    return st;
+  launch_tensor_scale_rows(dtype == NSDF_DTYPE_F64, d[0], d[1], dc, rows, cols, c->stream);
+  return tensor_finish(c, out, dc, size_t(rows) * cols * (dtype == NSDF_DTYPE_F64 ? 8 : 4));
+}
+
+int nsdf_cuda_tensor_sine(nsdf_ctx* c, int dtype, const void* x, void* out, size_t n, double omega, int derivative) {
+  if (!c) return fail(NSDF_ERR_CONTRACT, "context is null");
+  if (n && (!x || !out)) return fail(NSDF_ERR_CONTRACT, "sine: null buffer");
+  std::lock_guard<std::mutex> lk(c->mu);
+  DeviceGuard g(c->device);
+  void* d[1];
+  void* dc;
+  if (int st = tensor_io(c, dtype, {{x, n}}, {out, n}, d, &dc)) return st;
+  launch_tensor_sine(dtype == NSDF_DTYPE_F64, d[0], dc, n, omega, derivative != 0, c->stream);
+  return tensor_finish(c, out, dc, n * (dtype == NSDF_DTYPE_F64 ? 8 : 4));
+}
+
 int nsdf_cuda_eval(nsdf_ctx* c, nsdf_field h, const float* points, int rows, int k, float time, float* out) {
   if (!out && k > 0) return fail(NSDF_ERR_CONTRACT, "out is null");
   return nsdf_cuda_eval_grad(c, h, points, rows, k, time, out, nullptr);

@@ -157,6 +157,15 @@ cudaError_t train_fit(int n_layers, const int32_t* rows, const int32_t* cols, do
                       int n, const double* val_points_h, const double* val_targets_h, int n_val,
                       const nsdf_train_config* cfg, double* epoch_loss, nsdf_train_report* rep, cudaStream_t s);
 
+// The reference's dense kernel table on the device (tensor_ops.cu, tensor/kernels.hpp:26-39),
+// bit-exact with its AVX2 backend; f64 selects double buffers.  Device pointers, async.
+void launch_tensor_gemm(bool f64, const void* a, const void* b, const void* bias, void* c, int m, int n, int k,
+                        cudaStream_t s);
+void launch_tensor_hadamard(bool f64, const void* a, const void* b, void* out, size_t n, cudaStream_t s);
+void launch_tensor_scale_rows(bool f64, const void* col, const void* m, void* out, int rows, int cols,
+                              cudaStream_t s);
+void launch_tensor_sine(bool f64, const void* x, void* out, size_t n, double omega, bool derivative, cudaStream_t s);
+
 // Tensor-core availability of a net for the fast mode (mlp_tc.cu).
 bool tc_supported(const DevNet& n);
 

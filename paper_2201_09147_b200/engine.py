@@ -161,6 +161,56 @@ class Context:
                                                   ctypes.c_float(time), ctypes.c_void_p(d_out),
                                                   ctypes.c_void_p(d_grad)))
 
+    # ---- the reference's dense kernel table (tensor::gemm / hadamard / activate / scale_rows)
+    @staticmethod
+    def _dt(x):
+        x = np.asarray(x)
+        if x.dtype not in (np.float32, np.float64):
+            raise NsdfError(abi.ERR_CONTRACT, "tensor ops take float32 or float64 arrays")
+        return x.dtype, (1 if x.dtype == np.float64 else 0)
+
+    def tensor_gemm(self, a, b, bias=None):
+        """c = a . b (+ bias column), bit-exact with the reference's AVX2 gemm."""
+        dt, code = self._dt(a)
+        a = np.ascontiguousarray(a, dt)
+        b = np.ascontiguousarray(b, dt)
+        m, k = a.shape
+        n = b.shape[1]
+        bias = None if bias is None else np.ascontiguousarray(bias, dt).reshape(-1)
+        c = np.zeros((m, n), dt)
+        vp = lambda x: None if x is None else x.ctypes.data_as(ctypes.c_void_p)  # noqa: E731
+        check(self.lib.nsdf_cuda_tensor_gemm(self._ctx, code, vp(a), vp(b), vp(bias), vp(c), m, n, k))
+        return c
+
+    def tensor_hadamard(self, a, b):
+        dt, code = self._dt(a)
+        a = np.ascontiguousarray(a, dt)
+        b = np.ascontiguousarray(b, dt)
+        out = np.zeros_like(a)
+        check(self.lib.nsdf_cuda_tensor_hadamard(self._ctx, code, a.ctypes.data_as(ctypes.c_void_p),
+                                                 b.ctypes.data_as(ctypes.c_void_p),
+                                                 out.ctypes.data_as(ctypes.c_void_p), ctypes.c_size_t(a.size)))
+        return out
+
+    def tensor_scale_rows(self, col, m):
+        dt, code = self._dt(m)
+        col = np.ascontiguousarray(col, dt).reshape(-1)
+        m = np.ascontiguousarray(m, dt)
+        out = np.zeros_like(m)
+        check(self.lib.nsdf_cuda_tensor_scale_rows(self._ctx, code, col.ctypes.data_as(ctypes.c_void_p),
+                                                   m.ctypes.data_as(ctypes.c_void_p),
+                                                   out.ctypes.data_as(ctypes.c_void_p), m.shape[0], m.shape[1]))
+        return out
+
+    def tensor_sine(self, x, omega, derivative=False):
+        dt, code = self._dt(x)
+        x = np.ascontiguousarray(x, dt)
+        out = np.zeros_like(x)
+        check(self.lib.nsdf_cuda_tensor_sine(self._ctx, code, x.ctypes.data_as(ctypes.c_void_p),
+                                             out.ctypes.data_as(ctypes.c_void_p), ctypes.c_size_t(x.size),
+                                             ctypes.c_double(omega), 1 if derivative else 0))
+        return out
+
     # ---- tracing --------------------------------------------------------------------------
     def generate_rays(self, cam: Camera):
         rays = np.zeros((cam.width * cam.height, 6), np.float32)

@@ -7,6 +7,7 @@
 
 #include "check.hpp"
 #include "nsdf/shading/shading.hpp"
+#include "nsdf/tensor/ops.hpp"
 
 using namespace nsdf;
 using fields::NestedSequence;
@@ -261,6 +262,44 @@ TEST_CASE("manifest + sdfnet round trip and image / mesh I/O") {
   shading::write_png(img, dir / "a.png");
   CHECK(std::filesystem::file_size(dir / "a.png") > 40);
   CHECK(fields::thresholds_prop2({0.3, 0.1, 0.05})[2] == 0.1 + 0.05);
+}
+
+TEST_CASE("gemm identity and hand examples (test_tensor.cpp:31-48)") {
+  const Matrix<float> a{{1, 2}, {3, 4}};
+  const Matrix<float> ones{{1}, {1}};
+  const Matrix<float> bias{{10}, {10}};
+  const Matrix<float> c = tensor::gemm(a, ones, &bias);
+  CHECK(c.rows() == 2 && c.cols() == 1 && c(0, 0) == 13.0f && c(1, 0) == 17.0f);
+  const Matrix<double> id{{1, 0}, {0, 1}};
+  const Matrix<double> ad{{1, 2}, {3, 4}};
+  const Matrix<double> r = tensor::gemm(id, ad);
+  CHECK(r(0, 0) == 1.0 && r(0, 1) == 2.0 && r(1, 0) == 3.0 && r(1, 1) == 4.0);
+}
+
+TEST_CASE("tensor ops: shape errors name both shapes, sine basics, flops, backends (test_tensor.cpp:84-177, 311-323)") {
+  const Matrix<float> a(2, 3), b(2, 3);
+  bool named = false;
+  try {
+    tensor::gemm(a, b);
+  } catch (const Error& e) {
+    named = e.kind() == ErrorKind::contract && std::string(e.what()).find("2x3") != std::string::npos;
+  }
+  CHECK(named);
+  CHECK_THROWS(tensor::hadamard(a, Matrix<float>(3, 2)));
+  CHECK_THROWS(tensor::scale_rows(Matrix<float>(3, 1), a));
+  const Matrix<float> z(1, 1);
+  CHECK(tensor::activate(z, tensor::ActivationSpec::sine(1.0))(0, 0) == 0.0f);
+  CHECK(tensor::activate(z, tensor::ActivationSpec::sine(1.0), true)(0, 0) == 1.0f);
+  const Matrix<float> h = tensor::hadamard(Matrix<float>{{1, 2, 3}}, Matrix<float>{{4, 5, 6}});
+  CHECK(h(0, 0) == 4.0f && h(0, 1) == 10.0f && h(0, 2) == 18.0f);
+  const Matrix<double> s = tensor::scale_rows(Matrix<double>{{2}, {3}}, Matrix<double>{{1, 2}, {3, 4}});
+  CHECK(s(0, 1) == 4.0 && s(1, 0) == 9.0);
+  tensor::reset_flops();
+  tensor::gemm(Matrix<float>(4, 8), Matrix<float>(8, 16));
+  CHECK(tensor::flops_performed() == 2ull * 4 * 16 * 8);
+  CHECK(tensor::active_backend() == tensor::Backend::b200 && tensor::backend_available(tensor::Backend::b200));
+  CHECK(!tensor::backend_available(tensor::Backend::scalar));
+  CHECK_THROWS(tensor::set_backend(tensor::Backend::scalar));
 }
 
 int main() { return chk::run_all(); }
