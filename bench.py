@@ -288,7 +288,7 @@ def run_e2e(args, ctx, ds, seq, stream, world, rank, W):
     import torch
     import torch.distributed as dist
     npix = args.width * args.height
-    steps = args.steps
+    steps = len(W["frame_times"]) if W.get("frame_times") else args.steps
     if W["gbuffer"]:
         pts = W["pts"].cpu().numpy()
         k = pts.shape[1]
@@ -302,7 +302,8 @@ def run_e2e(args, ctx, ds, seq, stream, world, rank, W):
                 "h2d_bytes_per_step": 12 * k, "d2h_bytes_per_step": 12 * k + 16,
                 "path": "nsdf_cuda_normal_map (C ABI, host points -> host normals)"}
     cam, cfg, shade, src, levels = W["cam"], W["cfg"], W["shade"], W["src"], W["levels"]
-    if world == 1 or W.get("shard_frames"):
+    frame_times = W.get("frame_times")  # animated: this rank's frame times t_i = i/(n-1)
+    if world == 1 or W.get("shard_frames") or frame_times:
         # The public host-buffer call, nsdf_cuda_render, from one host thread per frame in
         # flight: each thread owns an engine context (own stream + workspace) and its own
         # pinned host framebuffer and renders every T-th frame, so one frame's D2H overlaps
@@ -316,14 +317,16 @@ def run_e2e(args, ctx, ds, seq, stream, world, rank, W):
                  torch.empty(npix, dtype=torch.uint8, pin_memory=True)) for _ in range(T)]
         lane_lv = [levels] + [d.levels() for _, _, d in lanes[1:]]
 
-        def work(li, n):
-            c = lanes[li][0]
+        def work(li, n, warm=False):
+            c, _, dseq = lanes[li]
             r, d, m = bufs[li]
-            for _ in range(n):
-                c.render_into(lane_lv[li], cam, cfg, shade, r.data_ptr(), d.data_ptr(), m.data_ptr(), src)
+            for j in range(n):
+                # animated: lane li renders frames li, li+T, ... of this rank (each its own slice)
+                lv = dseq.levels(time=frame_times[li + j * T]) if frame_times and not warm else lane_lv[li]
+                c.render_into(lv, cam, cfg, shade, r.data_ptr(), d.data_ptr(), m.data_ptr(), src)
 
         for li in range(T):
-            work(li, 1)  # warm-up
+            work(li, 1, warm=True)
         counts = [steps // T + (1 if li < steps % T else 0) for li in range(T)]
         threads = [threading.Thread(target=work, args=(li, counts[li])) for li in range(T)]
         w0 = time.perf_counter()
@@ -366,7 +369,8 @@ def run_e2e(args, ctx, ds, seq, stream, world, rank, W):
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
     e_ms = float(te.item())
     level_bytes = 16 * len(levels) + 4 * 8 + 128 + 272  # camera + configs + level table
-    frames = steps * (world if W.get("shard_frames") else 1)  # frames mode: every rank's frames
+    # frames mode: every rank's frames; animated: the whole sequence over all ranks
+    frames = W["total_frames"] if frame_times else steps * (world if W.get("shard_frames") else 1)
     return {"value": npix * frames / (e_ms / 1e3) / 1e6, "unit": "Mrays/s", "ms_per_frame": e_ms / frames,
             "h2d_bytes_per_step": level_bytes, "d2h_bytes_per_step": npix * (12 + 4 + 1), "path": path}
 
@@ -500,6 +504,8 @@ def main():
             my_frames = [i for i in range(n_frames) if i % world == rank]
             steps = len(my_frames)
             frame_levels = [ds.levels(time=i / (n_frames - 1)) for i in my_frames]
+            W["frame_times"] = [i / (n_frames - 1) for i in my_frames]
+            W["total_frames"] = n_frames
             W["levels"] = frame_levels[0]
         else:
             W["levels"] = ds.levels()
@@ -758,7 +764,7 @@ def main():
     strong = tile_pass(args, ctx, W, world, rank, Wd, Hd) if shard_frames else None
 
     e2e = None
-    if not args.no_e2e and not animated:
+    if not args.no_e2e:
         e2e = run_e2e(args, ctx, ds, seq, stream, world, rank, W)
 
     cpu = None

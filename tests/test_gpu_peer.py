@@ -84,7 +84,7 @@ def test_peer_framebuffer_assembles_the_frame(mode, tile):
         assert np.array_equal(rgb.view(np.uint32), np.asarray(ref[0], np.float32).reshape(-1).view(np.uint32))
 
 
-@pytest.mark.parametrize("shard", ["tiles", "frames"])
+@pytest.mark.parametrize("shard", ["tiles", "frames", "animation"])
 def test_bench_two_ranks_plumbing(shard):
     """bench.py's N > 1 path end to end (torchrun, 2 ranks, e2e to host) with both ranks on
     this one GPU over gloo (NSDF_BENCH_ONE_GPU=1): the JSON line carries the contract keys;
@@ -102,14 +102,20 @@ def test_bench_two_ranks_plumbing(shard):
     env.pop("NSDF_MODE", None)  # conftest's oracle-mode default is not a bench --mode
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
                         "--master-addr", "127.0.0.1", "--master-port", str(port), "bench.py", "--gpus", "2",
-                        "--steps", "4", "--warmup", "3", "--no-cpu-baseline", "--no-alt", "--shard", shard],
+                        "--steps", "4", "--warmup", "3", "--no-cpu-baseline", "--no-alt"] +
+                       (["--config", "5", "--width", "480", "--height", "270"] if shard == "animation"
+                        else ["--shard", shard]),
                        cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr[-2000:]
     line = json.loads(r.stdout.strip().splitlines()[-1])
     for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "e2e", "roofline", "clocks"):
         assert k in line
     assert line["n_gpus"] == 2 and line["value"] > 0 and line["e2e"]["value"] > 0
-    if shard == "tiles":
+    if shard == "animation":
+        # config 5: the 120 frames round-robin over the ranks, e2e through the host-buffer API
+        assert line["config"]["parallelism"] == "frames2" and line["steps"] == 60
+        assert line["e2e"]["value"] > 0 and line["e2e"]["d2h_bytes_per_step"] == 480 * 270 * 17
+    elif shard == "tiles":
         assert line["config"]["parallelism"] == "tiles2" and line["scaling"] == "strong"
         assert line["config"]["frame_assembly"].startswith("peer")
         assert line["strong_scaling"] is None
