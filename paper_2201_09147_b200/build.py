@@ -65,6 +65,8 @@ def build_cuda(force=False, verbose=False):
             extra = extra + ["-DNSDF_TC_TIMELINE_BUILD=1"]
         if src == "mlp_tc.cu" and os.environ.get("NSDF_TC_DEFINES"):  # A/B builds (tools/ab.py)
             extra = extra + os.environ["NSDF_TC_DEFINES"].split()
+        if src != "mlp_tc.cu" and os.environ.get("NSDF_ENGINE_DEFINES"):
+            extra = extra + os.environ["NSDF_ENGINE_DEFINES"].split()
         s = os.path.join(CSRC, src)
         o = os.path.join(OBJ, src + ".o")
         objs.append(o)

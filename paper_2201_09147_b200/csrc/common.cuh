@@ -11,7 +11,7 @@ namespace nsdf_b200 {
 constexpr int kMaxLayers = 16;     // hidden blocks <= 14
 constexpr int kMaxLevels = NSDF_MAX_LEVELS;
 constexpr int kMaxWidth = 256;     // widest layer the device engine tiles
-constexpr int kThreads = 256;      // CTA size of the FFMA (oracle-mode) kernels
+constexpr int kThreads = 256;      // CTA size of the narrow FFMA (oracle-mode) tiles (engine.cu: wide_tile)
 constexpr int kTileCols = 64;      // activation columns per FFMA tile (rays, or rays x 4 chains)
 
 enum FieldKind : int { kFieldMlp = 0, kFieldSphere = 1, kFieldTorus = 2, kFieldBox = 3 };

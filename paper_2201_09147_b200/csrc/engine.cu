@@ -258,15 +258,15 @@ void launch_reset_state(RayState st, int n, cudaStream_t s) {
 // ---------------------------------------------------------------------------------------
 // Field tile: MLP (FFMA oracle tile) or analytic member.
 // ---------------------------------------------------------------------------------------
-template <bool kGrad>
+template <bool kGrad, int kT>
 __device__ __forceinline__ void field_tile(const DevField& f, const float* pts, float* bufA, float* bufB,
                                            float* vals) {
   if (f.kind == kFieldMlp) {
-    simt_mlp_tile<kGrad>(f.net, pts, bufA, bufB, vals);
+    simt_mlp_tile<kGrad, kT>(f.net, pts, bufA, bufB, vals);
     return;
   }
   constexpr int kRays = kGrad ? kTileCols / 4 : kTileCols;
-  for (int col = threadIdx.x; col < kTileCols; col += kThreads) {
+  for (int col = threadIdx.x; col < kTileCols; col += kT) {
     const int ray = kGrad ? col / 4 : col, chain = kGrad ? col % 4 : 0;
     const double x = pts[ray], y = pts[kRays + ray], z = pts[2 * kRays + ray];
     if (chain == 0) {
@@ -286,19 +286,24 @@ static size_t field_smem(const DevField& f) {
 }
 
 template <typename K>
-static int blocks_for(K kernel, size_t smem) {
-  static bool configured = false;
-  (void)configured;
+static int blocks_for(K kernel, int threads, size_t smem) {
   cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
   int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kThreads, smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem);
   return num_sms() * std::max(per_sm, 1);
 }
+
+// CTA size of the FFMA tiles: 256 threads (16 row groups x 16 column groups) for nets up to
+// 128 wide; 1024 for 256-wide nets, whose 128 KB activation tile allows one CTA per SM —
+// four times the warps to hide the weight loads (oracle mode 2.5x faster on 256x3 levels;
+// narrower nets keep 256, where 1024 threads would leave row groups idle).
+static bool wide_tile(const DevField& f) { return f.kind == kFieldMlp && f.net.max_width >= 256; }
 
 // ---------------------------------------------------------------------------------------
 // Trace iteration (trace_level body, trace.cpp:46-82) for one compacted active list.
 // ---------------------------------------------------------------------------------------
-__global__ void __launch_bounds__(kThreads) trace_iter_simt(IterArgs a) {
+template <int kT>
+__global__ void __launch_bounds__(kT) trace_iter_simt(IterArgs a) {
   extern __shared__ __align__(16) float smem[];
   const int W = a.lv.field.kind == kFieldMlp ? max(a.lv.field.net.max_width, 4) : 4;
   float* bufA = smem;
@@ -319,7 +324,7 @@ __global__ void __launch_bounds__(kThreads) trace_iter_simt(IterArgs a) {
       pts[3 * kTileCols + tid] = a.lv.time;
     }
     __syncthreads();
-    field_tile<false>(a.lv.field, pts, bufA, bufB, vals);
+    field_tile<false, kT>(a.lv.field, pts, bufA, bufB, vals);
     if (tid < kTileCols) {
       const int slot = slots[tid];
       bool conv = false, cont = false;
@@ -382,12 +387,16 @@ TraceResult run_trace(Mode mode, const std::vector<LevelDesc>& levels, float eps
         const size_t smem = field_smem(lv.field) + kTileCols * sizeof(int);
         static int grid_cache_w = -1, grid_cache = 0;
         const int w = lv.field.kind == kFieldMlp ? lv.field.net.max_width : 4;
+        const bool wide = wide_tile(lv.field);
         if (grid_cache_w != w) {
-          grid_cache = blocks_for(trace_iter_simt, smem);
+          grid_cache = wide ? blocks_for(trace_iter_simt<1024>, 1024, smem) : blocks_for(trace_iter_simt<256>, 256, smem);
           grid_cache_w = w;
         }
         const int grid = std::max(1, std::min(grid_cache, (n_max + kTileCols - 1) / kTileCols));
-        trace_iter_simt<<<grid, kThreads, smem, s>>>(a);
+        if (wide)
+          trace_iter_simt<1024><<<grid, 1024, smem, s>>>(a);
+        else
+          trace_iter_simt<256><<<grid, 256, smem, s>>>(a);
       }
       res.launches++;
       in_list = fb.list[pong];
@@ -511,7 +520,8 @@ __device__ __forceinline__ void write_pixel(const NormalArgs& a, int slot, const
   a.mask[p] = 1;
 }
 
-__global__ void __launch_bounds__(kThreads) normals_shade_simt(NormalArgs a) {
+template <int kT>
+__global__ void __launch_bounds__(kT) normals_shade_simt(NormalArgs a) {
   extern __shared__ __align__(16) float smem[];
   constexpr int kRays = kTileCols / 4;
   const int W = a.field.kind == kFieldMlp ? max(a.field.net.max_width, 4) : 4;
@@ -533,7 +543,7 @@ __global__ void __launch_bounds__(kThreads) normals_shade_simt(NormalArgs a) {
       pts[3 * kRays + tid] = a.time;
     }
     __syncthreads();
-    field_tile<true>(a.field, pts, bufA, bufB, vals);
+    field_tile<true, kT>(a.field, pts, bufA, bufB, vals);
     if (tid < 32) {
       const int slot = tid < kRays ? slots[tid] : -1;
       bool defer = false;
@@ -563,16 +573,21 @@ int launch_normals_shade(Mode mode, const DevField& nf, float time, const int* l
       return 1;
   }
   const size_t smem = field_smem(nf) + kTileCols * sizeof(int);
-  const int grid = std::max(1, std::min(blocks_for(normals_shade_simt, smem), (n_max + 15) / 16));
-  normals_shade_simt<<<grid, kThreads, smem, s>>>(a);
+  if (wide_tile(nf)) {
+    const int grid = std::max(1, std::min(blocks_for(normals_shade_simt<1024>, 1024, smem), (n_max + 15) / 16));
+    normals_shade_simt<1024><<<grid, 1024, smem, s>>>(a);
+  } else {
+    const int grid = std::max(1, std::min(blocks_for(normals_shade_simt<256>, 256, smem), (n_max + 15) / 16));
+    normals_shade_simt<256><<<grid, 256, smem, s>>>(a);
+  }
   return 1;
 }
 
 // ---------------------------------------------------------------------------------------
 // API-path batch kernels.
 // ---------------------------------------------------------------------------------------
-template <bool kGrad>
-__global__ void __launch_bounds__(kThreads) eval_simt(DevField f, const float* pts_g, int rows, int k, float time,
+template <bool kGrad, int kT>
+__global__ void __launch_bounds__(kT) eval_simt(DevField f, const float* pts_g, int rows, int k, float time,
                                                       float* out, float* grad, double delta, const float* fallback,
                                                       unsigned long long* counts, int normal_map) {
   extern __shared__ __align__(16) float smem[];
@@ -591,7 +606,7 @@ __global__ void __launch_bounds__(kThreads) eval_simt(DevField f, const float* p
         pts[r * kRays + tid] = col < k ? (r < rows ? pts_g[size_t(r) * k + col] : time) : 0.0f;
     }
     __syncthreads();
-    field_tile<kGrad>(f, pts, bufA, bufB, vals);
+    field_tile<kGrad, kT>(f, pts, bufA, bufB, vals);
     if (!kGrad) {
       if (tid < kRays && base + tid < k) out[base + tid] = vals[tid];
     } else if (tid < 32) {
@@ -637,8 +652,15 @@ static void launch_eval_impl(const DevField& f, const float* pts, int rows, int 
                              cudaStream_t s) {
   const size_t smem = field_smem(f);
   constexpr int kRays = kGrad ? kTileCols / 4 : kTileCols;
-  const int grid = std::max(1, std::min(blocks_for(eval_simt<kGrad>, smem), (k + kRays - 1) / kRays));
-  eval_simt<kGrad><<<grid, kThreads, smem, s>>>(f, pts, rows, k, time, out, grad, delta, fallback, counts, normal_map);
+  if (wide_tile(f)) {
+    const int grid = std::max(1, std::min(blocks_for(eval_simt<kGrad, 1024>, 1024, smem), (k + kRays - 1) / kRays));
+    eval_simt<kGrad, 1024><<<grid, 1024, smem, s>>>(f, pts, rows, k, time, out, grad, delta, fallback, counts,
+                                                    normal_map);
+  } else {
+    const int grid = std::max(1, std::min(blocks_for(eval_simt<kGrad, 256>, 256, smem), (k + kRays - 1) / kRays));
+    eval_simt<kGrad, 256><<<grid, 256, smem, s>>>(f, pts, rows, k, time, out, grad, delta, fallback, counts,
+                                                  normal_map);
+  }
 }
 
 void launch_eval(Mode mode, const DevField& f, const float* pts, int rows, int k, float time, float* out, float* grad,

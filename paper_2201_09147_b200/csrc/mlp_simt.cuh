@@ -14,8 +14,8 @@
 //   - G0_c = W0[i,c] * dphi, G_i = gemm(W_i, G) * dphi, output = Wn . G_c from 0.
 // Hence results are bit-identical to the CPU path for any batch split.
 //
-// Thread mapping per hidden layer pass: rb = tid/16 owns 4 output rows, cb = tid%16 owns 4
-// columns; per k step one float4 of W^T (L1/L2, broadcast within the warp) and one float4
+// Thread mapping per hidden layer pass (kT threads: 256, or 1024 for 256-wide nets): rb =
+// tid/16 owns 4 output rows, cb = tid%16 owns 4 columns; per k step one float4 of W^T (L1/L2, broadcast within the warp) and one float4
 // of activations (conflict-free shared load) feed 16 FFMA.
 #pragma once
 
@@ -28,7 +28,7 @@ __host__ __device__ constexpr size_t simt_tile_smem_bytes(int max_width) {
   return size_t(2) * size_t(max_width < 4 ? 4 : max_width) * kTileCols * sizeof(float);
 }
 
-template <bool kGrad>
+template <bool kGrad, int kT>
 __device__ __forceinline__ void simt_input_layer(const DevNet& n, const float* __restrict__ pts,
                                                  float* __restrict__ out) {
   // pts: [input_dim][kRays] staged points (row 3 = time for 4-input nets).
@@ -37,7 +37,7 @@ __device__ __forceinline__ void simt_input_layer(const DevNet& n, const float* _
   const float* __restrict__ w = n.w[0];
   const float* __restrict__ b = n.b[0];
   const bool sine = n.activation == NSDF_ACT_SINE;
-  for (int idx = threadIdx.x; idx < M * kRays; idx += kThreads) {
+  for (int idx = threadIdx.x; idx < M * kRays; idx += kT) {
     const int r = idx / kRays, ray = idx - r * kRays;
     float z = __ldg(b + r);
     for (int kk = 0; kk < K; ++kk) z = fmaf(__ldg(w + r * K + kk), pts[kk * kRays + ray], z);
@@ -58,7 +58,7 @@ __device__ __forceinline__ void simt_input_layer(const DevNet& n, const float* _
   }
 }
 
-template <bool kGrad>
+template <bool kGrad, int kT>
 __device__ __forceinline__ void simt_hidden_layer(const DevNet& n, int l, const float* __restrict__ in,
                                                   float* __restrict__ out) {
   const int M = n.rows[l], K = n.cols[l], Mp = n.rows_pad[l];
@@ -67,7 +67,7 @@ __device__ __forceinline__ void simt_hidden_layer(const DevNet& n, int l, const 
   const bool sine = n.activation == NSDF_ACT_SINE;
   const int cb = threadIdx.x & 15, rb = threadIdx.x >> 4;
   const int c0 = cb * 4;
-  for (int r0 = rb * 4; r0 < M; r0 += 64) {
+  for (int r0 = rb * 4; r0 < M; r0 += 4 * (kT / 16)) {
     float acc[4][4];
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
@@ -117,13 +117,13 @@ __device__ __forceinline__ void simt_hidden_layer(const DevNet& n, int l, const 
 // Whole network on one tile.  pts: [input_dim][rays]; results: vals[64] where column j is
 // the network output of column j (for kGrad: column 4r = value, 4r+1..3 = gradient).
 // bufA/bufB: [max_width][64].  Ends with a __syncthreads().
-template <bool kGrad>
+template <bool kGrad, int kT>
 __device__ void simt_mlp_tile(const DevNet& n, const float* pts, float* bufA, float* bufB, float* vals) {
   constexpr int kRays = kGrad ? kTileCols / 4 : kTileCols;
   const int L = n.n_layers;
   if (L == 1) {  // affine network: mlp.cpp:115-126
     const int K = n.cols[0];
-    for (int col = threadIdx.x; col < kTileCols; col += kThreads) {
+    for (int col = threadIdx.x; col < kTileCols; col += kT) {
       const int ray = kGrad ? col / 4 : col, chain = kGrad ? col % 4 : 0;
       float v;
       if (chain == 0) {
@@ -137,12 +137,12 @@ __device__ void simt_mlp_tile(const DevNet& n, const float* pts, float* bufA, fl
     __syncthreads();
     return;
   }
-  simt_input_layer<kGrad>(n, pts, bufA);
+  simt_input_layer<kGrad, kT>(n, pts, bufA);
   __syncthreads();
   float* in = bufA;
   float* out = bufB;
   for (int l = 1; l + 1 < L; ++l) {
-    simt_hidden_layer<kGrad>(n, l, in, out);
+    simt_hidden_layer<kGrad, kT>(n, l, in, out);
     __syncthreads();
     float* t = in;
     in = out;
@@ -151,7 +151,7 @@ __device__ void simt_mlp_tile(const DevNet& n, const float* pts, float* bufA, fl
   // Output layer (1 x K): one fma chain per column, value from the bias, tangents from 0.
   const int K = n.cols[L - 1];
   const float* __restrict__ w = n.w[L - 1];
-  for (int col = threadIdx.x; col < kTileCols; col += kThreads) {
+  for (int col = threadIdx.x; col < kTileCols; col += kT) {
     float acc = (!kGrad || (col & 3) == 0) ? __ldg(n.b[L - 1]) : 0.0f;
     for (int kk = 0; kk < K; ++kk) acc = fmaf(__ldg(w + kk), in[kk * kTileCols + col], acc);
     vals[col] = acc;

@@ -14,6 +14,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--rounds", type=int, default=3)
 ap.add_argument("--steps", type=int, default=50)
 ap.add_argument("--config", type=int, default=2)
+ap.add_argument("--mode", default="fp16")
 ap.add_argument("libs", nargs="+")
 args = ap.parse_args()
 res = {lib: [] for lib in args.libs}
@@ -21,7 +22,7 @@ for r in range(args.rounds):
     for lib in args.libs:
         env = dict(os.environ, NSDF_CUDA_LIB=os.path.abspath(lib))
         out = subprocess.run([sys.executable, "bench.py", "--steps", str(args.steps), "--config", str(args.config),
-                              "--no-cpu-baseline", "--no-e2e", "--no-alt"], cwd=ROOT, env=env,
+                              "--no-cpu-baseline", "--no-e2e", "--no-alt", "--mode", args.mode], cwd=ROOT, env=env,
                              capture_output=True, text=True)
         line = json.loads(out.stdout.strip().splitlines()[-1])
         res[lib].append((line["ms_per_step"], line["frame"].get("level_ms"), line["clocks"]["sm_mhz"]))
