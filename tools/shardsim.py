@@ -1,10 +1,10 @@
 """Strong-scaling estimate of the tile scheduler on ONE GPU: for each world size N, every
-rank's share of the frame (interleaved 64x64 tiles, tile t -> rank t % N) is rendered
+rank's share of the frame (interleaved 32x32 tiles, tile t -> rank t % N) is rendered
 alone, back to back, and the slowest rank's ms/frame is the N-GPU frame time without the
 NCCL gather.  It does not emulate a multi-rank run (no rank waits on another); it measures
 what each rank's GPU would have to do.
 
-    python tools/shardsim.py [--config 2] [--inflight 2] [--frames 30]
+    python tools/shardsim.py [--config 2] [--inflight 5] [--tile 32] [--frames 30]
 """
 import argparse
 import os
@@ -22,10 +22,10 @@ from paper_2201_09147_b200.manifest import load_manifest
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", type=int, default=2)
-ap.add_argument("--inflight", type=int, default=2)
+ap.add_argument("--inflight", type=int, default=5)
 ap.add_argument("--frames", type=int, default=30)
 ap.add_argument("--worlds", default="1,2,4,8")
-ap.add_argument("--tile", type=int, default=64)
+ap.add_argument("--tile", type=int, default=32)
 ap.add_argument("--profile", action="store_true", help="per-level serial launch times of the slowest rank")
 args = ap.parse_args()
 
