@@ -1,0 +1,107 @@
+"""GPU: the reference's acceptance criterion 5 (tests/acceptance/acceptance_main.cpp:152-227)
+on the device path — multiscale tracing over the certified coarse > fine pair (budgets 30, 30)
+against single-field fine tracing (budget 60) at 256x256: >= 99% of the common hits end within
+2*eps_stop of each other.  The criterion's second half (every hit/miss disagreement hugs the
+analytic torus silhouette) was stated for the reference's own omega0 = 10 fixtures; on the
+omega0 = 30 fixtures committed here the REFERENCE renderer itself leaves a few hundred
+grazing rays that exhaust the coarse budget (fine-only hits, multiscale misses) away from the
+silhouette, so the test pins the engine to the reference's own outcome instead: the same
+disagreement counts as oracle/_ref (exactly in the bit-exact FP32 mode, within 0.1% of the
+pixels in the fast mode).  A dense sphere-trace of the analytic torus (numpy) stands in for
+oracles::dense_ray_march."""
+import os
+
+import numpy as np
+import pytest
+
+from conftest import ASSETS
+
+pytestmark = pytest.mark.gpu
+
+
+def _torus_mask(rays, R=0.6, r=0.3, t_max=8.0, eps=1e-5, iters=2000):
+    """Analytic torus hit mask by sphere tracing the exact SDF (float64)."""
+    o = rays[:, 0:3].astype(np.float64)
+    d = rays[:, 3:6].astype(np.float64)
+    t = np.zeros(len(rays))
+    hit = np.zeros(len(rays), bool)
+    live = np.ones(len(rays), bool)
+    for _ in range(iters):
+        p = o[live] + t[live, None] * d[live]
+        q = np.sqrt(p[:, 0] ** 2 + p[:, 2] ** 2) - R
+        f = np.sqrt(q * q + p[:, 1] ** 2) - r
+        idx = np.nonzero(live)[0]
+        done = f < eps
+        hit[idx[done]] = True
+        t[idx] += np.maximum(f, 0.0)
+        live[idx[done | (t[idx] > t_max)]] = False
+        if not live.any():
+            break
+    return hit
+
+
+@pytest.mark.parametrize("mode", ["fp16", "fp32"])
+def test_multiscale_equivalence(mode, oracle_built):
+    import json
+    import tempfile
+    from oracle import refshim
+    from paper_2201_09147_b200.abi import TraceConfig, standard_camera
+    from paper_2201_09147_b200.engine import Context, DeviceSequence
+    from paper_2201_09147_b200.manifest import load_manifest
+    path = os.path.join(ASSETS, "torus_w30.nest")
+    if not os.path.exists(path):
+        pytest.skip("fixture missing")
+    seq = load_manifest(path)
+    cam = standard_camera(256, 256)
+    n = cam.width * cam.height
+    multi, single = TraceConfig((30, 30)), TraceConfig((60,))
+
+    def stats(ms, fs, rays):
+        mh = np.fromiter((x.hit for x in ms), np.int32, n) == 1
+        fh = np.fromiter((x.hit for x in fs), np.int32, n) == 1
+        mp = np.array([tuple(x.point) for x in ms], np.float64)
+        fp = np.array([tuple(x.point) for x in fs], np.float64)
+        both = mh & fh
+        agree = float((np.linalg.norm(mp[both] - fp[both], axis=1) <= 2.0 * 1e-3).mean())
+        oracle = _torus_mask(rays).reshape(cam.height, cam.width)
+        pad = np.pad(oracle, 1, mode="edge")
+        near = np.zeros_like(oracle)
+        for dy in (-1, 0, 1):
+            for dx in (-1, 0, 1):
+                near |= pad[1 + dy:1 + dy + cam.height, 1 + dx:1 + dx + cam.width] != oracle
+        diff = (mh != fh).reshape(cam.height, cam.width)
+        return int(both.sum()), agree, int(diff.sum()), int((diff & ~near).sum())
+
+    c = Context(0, mode)
+    try:
+        ms, _ = c.trace_image(DeviceSequence(c, seq.subsequence([0, 2])).levels(), cam, multi)
+        fs, _ = c.trace_image(DeviceSequence(c, seq.subsequence([2])).levels(), cam, single)
+        rays = c.generate_rays(cam)
+    finally:
+        c.close()
+    both, agree, diffs, off = stats(ms, fs, rays)
+    assert both > 1000 and agree >= 0.99
+
+    # the reference's own outcome on the same fixtures (oracle/_ref, AVX2)
+    refshim.set_backend("avx2")
+    j = json.load(open(path))
+    mans = []
+    for members in ([0, 2], [2]):
+        m = dict(j, fields=[dict(j["fields"][i], weights=os.path.join(ASSETS, j["fields"][i]["weights"]))
+                            for i in members], deltas=[j["deltas"][i] for i in members])
+        fh_ = tempfile.NamedTemporaryFile("w", suffix=".nest", delete=False)
+        json.dump(m, fh_)
+        fh_.close()
+        mans.append(fh_.name)
+    try:
+        r_ms = refshim.trace_image(mans[0], cam, multi)
+        r_fs = refshim.trace_image(mans[1], cam, single)
+    finally:
+        for f in mans:
+            os.unlink(f)
+    r_both, r_agree, r_diffs, r_off = stats(r_ms, r_fs, rays)
+    assert r_agree >= 0.99
+    if mode == "fp32":
+        assert (both, diffs, off) == (r_both, r_diffs, r_off)
+    else:
+        assert abs(diffs - r_diffs) <= 0.001 * n and abs(off - r_off) <= 0.001 * n
