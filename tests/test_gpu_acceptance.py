@@ -105,3 +105,86 @@ def test_multiscale_equivalence(mode, oracle_built):
         assert (both, diffs, off) == (r_both, r_diffs, r_off)
     else:
         assert abs(diffs - r_diffs) <= 0.001 * n and abs(off - r_off) <= 0.001 * n
+
+
+def test_coarse_first_is_faster():
+    """Criterion 7 (acceptance_main.cpp:295-333) on the B200 at 256x256: fine@40 costs >= 4x
+    coarse@40 and multiscale (30, 30) beats fine@60 (CUDA-event timing, fast mode)."""
+    import sys
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools"))
+    import torch
+    from acceptance_speed import time_render
+    from paper_2201_09147_b200.abi import standard_camera
+    from paper_2201_09147_b200.engine import Context, DeviceSequence
+    from paper_2201_09147_b200.manifest import load_manifest
+    path = os.path.join(ASSETS, "torus_w30.nest")
+    if not os.path.exists(path):
+        pytest.skip("fixture missing")
+    seq = load_manifest(path)
+    c = Context(0, "fp16")
+    stream = torch.cuda.Stream()
+    c.set_stream(stream.cuda_stream)
+    try:
+        with torch.cuda.stream(stream):
+            cam = standard_camera(256, 256)
+            coarse = time_render(c, DeviceSequence(c, seq.subsequence([0])).levels(), cam, (40,))
+            fine_seq = DeviceSequence(c, seq.subsequence([2])).levels()
+            fine = time_render(c, fine_seq, cam, (40,))
+            fine60 = time_render(c, fine_seq, cam, (60,))
+            multi = time_render(c, DeviceSequence(c, seq.subsequence([0, 2])).levels(), cam, (30, 30))
+    finally:
+        c.close()
+    assert fine >= 4.0 * coarse and multi < fine60
+
+
+def test_fidelity_ordering_matches_reference(oracle_built):
+    """Criterion 6 (acceptance_main.cpp:230-293) on the torus fixtures at 256x256: image MSE
+    against the fine@40 render for coarse@40, mapped normals (40, 0), own normals (30, 10) and
+    (30, 30).  The fast mode must reproduce the reference renderer's ordering verdicts
+    (mapped <= 0.9 coarse, (30,30) < (30,10), (30,30) < mapped) and MSEs within 10%."""
+    import json
+    import tempfile
+    from oracle import refshim
+    from paper_2201_09147_b200.abi import ShadeConfig, TraceConfig, standard_camera
+    from paper_2201_09147_b200.engine import Context, DeviceSequence
+    from paper_2201_09147_b200.manifest import load_manifest
+    path = os.path.join(ASSETS, "torus_w30.nest")
+    if not os.path.exists(path):
+        pytest.skip("fixture missing")
+    seq = load_manifest(path)
+    cam = standard_camera(256, 256)
+    shade = ShadeConfig(specular=0.3)
+    runs = {"fine": ([2], (40,), 0), "coarse": ([0], (40,), 0), "mapped": ([0, 2], (40, 0), 1),
+            "30_10": ([0, 2], (30, 10), 0), "30_30": ([0, 2], (30, 30), 0)}
+    j = json.load(open(path))
+
+    def mse(a, b):
+        return float(np.mean((a.astype(np.float64) - b.astype(np.float64)) ** 2))
+
+    def verdict(img):
+        m = {k: mse(img[k], img["fine"]) for k in ("coarse", "mapped", "30_10", "30_30")}
+        return m, (m["mapped"] <= 0.9 * m["coarse"], m["30_30"] < m["30_10"], m["30_30"] < m["mapped"])
+
+    ours, ref = {}, {}
+    c = Context(0, "fp16")
+    try:
+        for k, (members, budgets, src) in runs.items():
+            ours[k] = c.render(DeviceSequence(c, seq.subsequence(members)).levels(), cam, TraceConfig(budgets),
+                               shade, src)[0]
+    finally:
+        c.close()
+    refshim.set_backend("avx2")
+    for k, (members, budgets, src) in runs.items():
+        m = dict(j, fields=[dict(j["fields"][i], weights=os.path.join(ASSETS, j["fields"][i]["weights"]))
+                            for i in members], deltas=[j["deltas"][i] for i in members])
+        with tempfile.NamedTemporaryFile("w", suffix=".nest", delete=False) as fh:
+            json.dump(m, fh)
+        try:
+            ref[k] = refshim.render(fh.name, cam, TraceConfig(budgets), shade, src)[0]
+        finally:
+            os.unlink(fh.name)
+    m_ours, v_ours = verdict(ours)
+    m_ref, v_ref = verdict(ref)
+    assert v_ours == v_ref
+    for k in m_ref:
+        assert abs(m_ours[k] - m_ref[k]) <= 0.1 * m_ref[k] + 1e-9
