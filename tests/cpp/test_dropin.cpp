@@ -302,4 +302,66 @@ TEST_CASE("tensor ops: shape errors name both shapes, sine basics, flops, backen
   CHECK_THROWS(tensor::set_backend(tensor::Backend::scalar));
 }
 
+template <typename T>
+Matrix<T> rand_mat(int r, int c, Rng& rng) {
+  Matrix<T> m(r, c);
+  for (auto& v : m.storage()) v = T(rng.uniform(-1, 1));
+  return m;
+}
+
+TEST_CASE("acceptance 1: f64 analytic gradients vs central differences (acceptance_main.cpp:30-71)") {
+  const double h = 1e-4;
+  const int points = 1000;
+  double worst = 0;
+  for (auto arch : {mlp::Architecture{16, 1, 3}, {64, 1, 3}, {256, 1, 3}, {256, 3, 3}}) {
+    for (uint64_t seed = 1; seed <= 3; ++seed) {
+      Rng rng(seed * 7919 + arch.width);
+      auto net = mlp::random_init(arch, 30.0, rng);
+      Matrix<double> pts = rand_mat<double>(3, points, rng);
+      Matrix<double> grad = mlp::gradient_batch(net, pts);
+      Matrix<double> fd(3, points);
+      for (int c = 0; c < 3; ++c) {
+        Matrix<double> hi = pts, lo = pts;
+        for (int j = 0; j < points; ++j) {
+          hi(c, j) += h;
+          lo(c, j) -= h;
+        }
+        auto up = mlp::forward_batch(net, hi);
+        auto dn = mlp::forward_batch(net, lo);
+        for (int j = 0; j < points; ++j) fd(c, j) = (up(0, j) - dn(0, j)) / (2 * h);
+      }
+      for (int j = 0; j < points; ++j) {
+        const double dx = grad(0, j) - fd(0, j), dy = grad(1, j) - fd(1, j), dz = grad(2, j) - fd(2, j);
+        const double scale =
+            std::max(std::sqrt(fd(0, j) * fd(0, j) + fd(1, j) * fd(1, j) + fd(2, j) * fd(2, j)), 1e-9);
+        worst = std::max(worst, std::sqrt(dx * dx + dy * dy + dz * dz) / scale);
+      }
+    }
+  }
+  CHECK(worst < 1e-4);
+}
+
+TEST_CASE("acceptance 2: commutation identity behind the cheap gradient form (acceptance_main.cpp:74-98)") {
+  Rng rng(1234);
+  const tensor::ActivationSpec spec = tensor::ActivationSpec::sine(30.0);
+  double worst = 0;
+  for (int iter = 0; iter < 20; ++iter) {
+    const int n = 2 + int(rng.next_u64() % 63);
+    const int k = 1 + int(rng.next_u64() % 32);
+    auto w = rand_mat<double>(n, n, rng);
+    auto g = rand_mat<double>(n, k, rng);
+    auto a = rand_mat<double>(n, 1, rng);
+    Matrix<double> a_cols(n, n);
+    for (int i = 0; i < n; ++i)
+      for (int j = 0; j < n; ++j) a_cols(i, j) = a(i, 0);
+    auto lhs = tensor::gemm(tensor::hadamard(w, tensor::activate(a_cols, spec, true)), g);
+    auto rhs = tensor::scale_rows(tensor::activate(a, spec, true), tensor::gemm(w, g));
+    double scale = 0;  // max-abs-scaled error (oracles.hpp:39-48)
+    for (size_t i = 0; i < rhs.size(); ++i) scale = std::max(scale, std::fabs(rhs.data()[i]));
+    if (scale == 0) scale = 1;
+    for (size_t i = 0; i < lhs.size(); ++i) worst = std::max(worst, std::fabs(lhs.data()[i] - rhs.data()[i]) / scale);
+  }
+  CHECK(worst < 1e-10);
+}
+
 int main() { return chk::run_all(); }
