@@ -8,6 +8,7 @@
 #include "check.hpp"
 #include "nsdf/shading/shading.hpp"
 #include "nsdf/tensor/ops.hpp"
+#include "nsdf/fields/nesting.hpp"
 
 using namespace nsdf;
 using fields::NestedSequence;
@@ -362,6 +363,33 @@ TEST_CASE("acceptance 2: commutation identity behind the cheap gradient form (ac
     for (size_t i = 0; i < lhs.size(); ++i) worst = std::max(worst, std::fabs(lhs.data()[i] - rhs.data()[i]) / scale);
   }
   CHECK(worst < 1e-10);
+}
+
+TEST_CASE("acceptance 3: threshold recurrences reproduce the hand tables (acceptance_main.cpp:100-121)") {
+  auto near = [](double a, double b) { return std::fabs(a - b) <= 1e-15; };
+  auto p2 = fields::thresholds_prop2({0.01, 0.02, 0.03});
+  CHECK(near(p2[0], 0.13) && near(p2[1], 0.10) && near(p2[2], 0.05));
+  auto p1 = fields::thresholds_prop1({0.02, 0.03});
+  CHECK(near(p1[2], 0.03) && near(p1[1], 0.06) && near(p1[0], 0.08));
+  auto p1e = fields::thresholds_prop1({0.01, 0.01, 0.01});
+  for (size_t i = 0; i < p1e.size(); ++i) CHECK(near(p1e[i], 0.01 * double(4 - i)));
+  auto p3 = fields::thresholds_prop3({0.05}, 0.01);
+  CHECK(near(p3[1], 0.01) && near(p3[0], 0.08));
+}
+
+TEST_CASE("acceptance 4: exact concentric pair certifies, halved threshold violates (acceptance_main.cpp:123-150)") {
+  NestedSequence seq = spheres({1.0, 0.95}, fields::thresholds_prop1({0.05}));
+  fields::VerifyConfig cfg;
+  cfg.samples = 200000;
+  cfg.seed = 99;
+  auto good = fields::verify_nesting(seq, cfg);
+  auto again = fields::verify_nesting(seq, cfg);
+  NestedSequence bad = seq;
+  bad.deltas[0] *= 0.5;
+  bad.deltas[1] = std::min(bad.deltas[1], bad.deltas[0] * 0.98);
+  auto violated = fields::verify_nesting(bad, cfg);
+  CHECK(good.violation_count == 0 && violated.violation_count >= 1);
+  CHECK(good.checked == again.checked && good.violation_count == again.violation_count);
 }
 
 int main() { return chk::run_all(); }
