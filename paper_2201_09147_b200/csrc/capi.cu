@@ -12,6 +12,7 @@
 #include <algorithm>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include <cuda_fp16.h>
@@ -103,6 +104,7 @@ struct nsdf_ctx {
   Workspace io;      // API staging: points, outputs, framebuffers, records
   Profiler prof;
   BatchPipe pipe;    // chunked host-buffer batches
+  std::vector<cudaEvent_t> copy_events;  // staged pageable framebuffer copies (copy_out_frame)
 };
 
 namespace {
@@ -433,6 +435,7 @@ int nsdf_cuda_destroy(nsdf_ctx* c) {
     c->io.~Workspace();
     new (&c->io) Workspace();
     c->pipe.release();
+    for (cudaEvent_t e : c->copy_events) cudaEventDestroy(e);
     if (c->own) cudaStreamDestroy(c->own);
   }
   delete c;
@@ -1343,6 +1346,81 @@ int nsdf_cuda_render_multi(nsdf_ctx* const* ctxs, int n, const nsdf_level* const
   return NSDF_OK;
 }
 
+}  // extern "C"
+
+namespace {
+
+bool is_pageable(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return true;
+  }
+  return a.type == cudaMemoryTypeUnregistered;
+}
+
+// Device -> PAGEABLE host copies of a frame's planes (the reference API's ImageBuffer is
+// std::vector storage): every plane is DMA'd in 4 MB chunks into a pinned staging area at
+// full PCIe rate (one event per chunk), and host threads copy each chunk out to the
+// destination as soon as its event fires — instead of the driver's single-threaded pageable
+// staging.  Pinned destinations take one direct cudaMemcpyAsync each.
+int copy_out_frame(nsdf_ctx* c, const std::vector<std::pair<void*, const void*>>& dst_src,
+                   const std::vector<size_t>& bytes) {
+  cudaStream_t s = c->stream;
+  struct Piece {
+    uint8_t* dst;
+    const uint8_t* src;
+    size_t n, stage_off;
+  };
+  constexpr size_t kChunk = size_t(4) << 20;
+  std::vector<Piece> pieces;
+  size_t staged = 0;
+  for (size_t i = 0; i < dst_src.size(); ++i) {
+    if (!is_pageable(dst_src[i].first)) {
+      NSDF_CUDA(cudaMemcpyAsync(dst_src[i].first, dst_src[i].second, bytes[i], cudaMemcpyDeviceToHost, s));
+      continue;
+    }
+    for (size_t o = 0; o < bytes[i]; o += kChunk) {
+      const size_t n = std::min(kChunk, bytes[i] - o);
+      pieces.push_back({static_cast<uint8_t*>(dst_src[i].first) + o, static_cast<const uint8_t*>(dst_src[i].second) + o,
+                        n, staged});
+      staged += (n + 255) / 256 * 256;
+    }
+  }
+  if (pieces.empty()) {
+    NSDF_CUDA(cudaStreamSynchronize(s));
+    return NSDF_OK;
+  }
+  NSDF_CUDA(c->io.reserve_host(staged));
+  uint8_t* stage = static_cast<uint8_t*>(c->io.host_pinned);
+  while (c->copy_events.size() < pieces.size()) {
+    cudaEvent_t e;
+    NSDF_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming | cudaEventBlockingSync));
+    c->copy_events.push_back(e);
+  }
+  for (size_t i = 0; i < pieces.size(); ++i) {
+    NSDF_CUDA(cudaMemcpyAsync(stage + pieces[i].stage_off, pieces[i].src, pieces[i].n, cudaMemcpyDeviceToHost, s));
+    NSDF_CUDA(cudaEventRecord(c->copy_events[i], s));
+  }
+  const int workers = int(std::max(1u, std::min(8u, std::thread::hardware_concurrency() / 2)));
+  auto work = [&](int w) {
+    for (size_t i = size_t(w); i < pieces.size(); i += size_t(workers)) {
+      cudaEventSynchronize(c->copy_events[i]);
+      std::memcpy(pieces[i].dst, stage + pieces[i].stage_off, pieces[i].n);
+    }
+  };
+  std::vector<std::thread> th;
+  for (int w = 1; w < workers; ++w) th.emplace_back(work, w);
+  work(0);
+  for (auto& t : th) t.join();
+  NSDF_CUDA(cudaStreamSynchronize(s));
+  return NSDF_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
 int nsdf_cuda_render(nsdf_ctx* c, const nsdf_level* levels, int m, const nsdf_camera* camera,
                      const nsdf_trace_config* trace, const nsdf_shade_config* shade, int normal_source,
                      int fine_index, float* rgb, float* depth, uint8_t* mask, nsdf_frame_stats* stats) {
@@ -1364,12 +1442,7 @@ int nsdf_cuda_render(nsdf_ctx* c, const nsdf_level* levels, int m, const nsdf_ca
   fo.d_mask = dmask;
   if (int st = run_frame(c, levels, m, trace, &cb, nullptr, 0, &sp, normal_source, fine_index, 1, 0, 1, fo, stats))
     return st;
-  cudaStream_t s = c->stream;
-  NSDF_CUDA(cudaMemcpyAsync(rgb, drgb, 3 * n * 4, cudaMemcpyDeviceToHost, s));
-  NSDF_CUDA(cudaMemcpyAsync(depth, ddepth, n * 4, cudaMemcpyDeviceToHost, s));
-  NSDF_CUDA(cudaMemcpyAsync(mask, dmask, n, cudaMemcpyDeviceToHost, s));
-  NSDF_CUDA(cudaStreamSynchronize(s));
-  return NSDF_OK;
+  return copy_out_frame(c, {{rgb, drgb}, {depth, ddepth}, {mask, dmask}}, {3 * n * 4, n * 4, n});
 }
 
 }  // extern "C"
