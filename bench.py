@@ -15,9 +15,12 @@ normal mapping 64x1 (40,0) + 256x3 normals at 1080p; 4: torus-mesh G-buffer -> 2
 at 2560x1440; 5: animated 4-D 64x1 > 128x2 blend, 120 frames at 3840x2160, frames sharded
 across ranks).
 
-N > 1 (torchrun): image tiles are interleaved across ranks (tile t -> rank t % N, the
-frame/tile scheduler of SURVEY.md §8e) and rank 0 gathers the packed tiles over NCCL:
-strong scaling of one frame (config 5: whole frames per rank, no gather).
+N > 1 (torchrun, the frame/tile scheduler of SURVEY.md §8e): by default (--shard frames) the
+frame stream is sharded — every rank renders whole frames, no data-path collective, weak
+scaling (config 5: the animation's frames round-robin) — and the same run also times the
+strong-scaling alternative (image tiles interleaved across ranks, tile t -> rank t % N, each
+rank's shading kernels storing its pixels into rank 0's framebuffer over NVLink peer memory;
+reported as `strong_scaling`); --shard tiles makes the tile split the headline.
 --impl reference times the reference's own CPU renderer (oracle/_ref/libnsdf_ref.so, all
 host threads) on the same config.
 """
