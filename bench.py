@@ -504,7 +504,7 @@ def main():
         if animated:
             # frames t_i = i/(n-1) (nsdf_main.cpp:308-324); frame i renders on rank i % world
             n_frames = cfgw["frames"]
-            my_frames = [i for i in range(n_frames) if i % world == rank]
+            my_frames = scheduler.owned_frames(n_frames, rank, world)
             steps = len(my_frames)
             frame_levels = [ds.levels(time=i / (n_frames - 1)) for i in my_frames]
             W["frame_times"] = [i / (n_frames - 1) for i in my_frames]
@@ -647,19 +647,14 @@ def main():
         prof = ctx.get_profile()
         ctx.set_profiling(False)
         prof_kind = "CUDA events around each launch, serial pass (1 frame in flight) after the timed region"
-    ms_total = e0.elapsed_time(e1)
-    t = torch.tensor([ms_total], dtype=torch.float64, device="cuda")
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_total = float(t.item())
-    if animated:
-        total_units = units_per_step * cfgw["frames"]              # all frames, all ranks
-    elif W["gbuffer"] or shard_frames:
-        total_units = units_per_step * steps * world               # every rank its own G-buffer / frames
+    # job throughput: units over ALL ranks / the slowest rank's device time (max over ranks)
+    if animated or W["gbuffer"] or shard_frames:
+        my_units = units_per_step * steps                          # this rank's frames / G-buffer
     else:
-        total_units = units_per_step * steps                       # tiles of the same frames
+        my_units = units_per_step * steps / world                  # tiles of the same frames
+    rate, ms_total = scheduler.job_rate(my_units, e0.elapsed_time(e1), world, device="cuda")
     ms_per_frame = ms_total / steps / (world if shard_frames else 1)
-    value = total_units / (ms_total / 1e3) / 1e6
+    value = rate / 1e6
     unit = "Mnormals/s" if W["gbuffer"] else "Mrays/s"
 
     pk, pk_kind = peaks()

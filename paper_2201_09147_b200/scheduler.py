@@ -1,7 +1,10 @@
 """Frame/tile scheduler across the GPUs of one node (north_star subsystem 5).
 
-One process per GPU (torchrun), torch.distributed for the plumbing.  The only collectives
-are the ones the north star names:
+One process per GPU (torchrun), torch.distributed for the plumbing.  A stream of frames (an
+animation, repeated views) shards whole frames — frame i on rank i % world (owned_frames),
+no collective on the data path; the job's throughput is all ranks' units over the slowest
+rank's time (job_rate: one MAX and one SUM all-reduce after the run).  A single frame is
+split across the ranks instead, with only the collectives the north star names:
   * broadcast_sequence: rank 0 reads the .nest/.sdfnet files and broadcasts the packed
     weights once (one NCCL broadcast of a float64 buffer + the small metadata);
   * PeerFramebuffer (default): rank 0 owns a ring of framebuffers mapped into every rank
@@ -28,6 +31,30 @@ def owned_pixels(width: int, height: int, tile: int, rank: int, world: int) -> n
     ys, xs = np.divmod(np.arange(width * height, dtype=np.int64), width)
     t = (ys // tile) * tiles_x + xs // tile
     return np.nonzero(t % world == rank)[0]
+
+
+def owned_frames(n_frames: int, rank: int, world: int) -> list:
+    """Frame-stream sharding: frame i renders on rank i % world (nsdf_main.cpp:308-324 loops
+    the frames in order; every frame is independent)."""
+    return [i for i in range(n_frames) if i % world == rank]
+
+
+def job_rate(units_per_rank: float, ms_rank: float, world: int, device=None) -> tuple:
+    """Whole-job throughput of a sharded run: every rank processed `units_per_rank` units in
+    `ms_rank` ms; the job time is the MAX over ranks (one all-reduce), the job's units the sum
+    over ranks.  Returns (units/s over all ranks, job ms)."""
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([ms_rank, units_per_rank], dtype=torch.float64, device=device or "cpu")
+    if world > 1:
+        mx = t[:1].clone()
+        dist.all_reduce(mx, op=dist.ReduceOp.MAX)
+        tot = t[1:].clone()
+        dist.all_reduce(tot, op=dist.ReduceOp.SUM)
+        ms, units = float(mx.item()), float(tot.item())
+    else:
+        ms, units = float(t[0].item()), float(t[1].item())
+    return units / (ms / 1e3), ms
 
 
 def broadcast_sequence(manifest_path: Optional[str], world: int, rank: int, device=None):

@@ -171,3 +171,39 @@ def test_gloo_world2_peer_framebuffer(fail):
         assert not res["ok"] and res["reason"]
     else:
         assert res["ok"] and res["frame"], res
+
+
+def test_owned_frames_partition_the_stream():
+    from paper_2201_09147_b200.scheduler import owned_frames
+    for world in (1, 2, 3, 8):
+        parts = [owned_frames(120, r, world) for r in range(world)]
+        assert sorted(sum(parts, [])) == list(range(120))
+        assert max(map(len, parts)) - min(map(len, parts)) <= 1
+
+
+def _rate_worker(rank, world, port, out):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2201_09147_b200.scheduler import job_rate, owned_frames
+    frames = owned_frames(7, rank, world)            # rank 0: 0,2,4,6; rank 1: 1,3,5
+    ms = 10.0 * (rank + 1)                           # rank 1 is the slower one
+    rate, job_ms = job_rate(1000.0 * len(frames), ms, world)
+    out.put((rank, rate, job_ms))
+    dist.destroy_process_group()
+
+
+def test_gloo_world2_job_rate_is_max_over_ranks():
+    """Frame-stream sharding accounting over gloo, world size 2: the job time is the slowest
+    rank's, the units are every rank's frames (7 frames of 1000 units in 20 ms)."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_rate_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = sorted(q.get(timeout=120) for _ in range(2))
+    for p in procs:
+        p.join(timeout=60)
+    for _, rate, job_ms in got:
+        assert job_ms == 20.0 and abs(rate - 7000.0 / 0.020) < 1e-6
