@@ -301,14 +301,36 @@ def run_e2e(args, ctx, ds, seq, stream, world, rank, W):
         pts = W["pts"].cpu().numpy()
         k = pts.shape[1]
         delta = float(seq.deltas[0])
-        ctx.normal_map(ds.handles[0], pts, delta)
+        # The public host-buffer call, nsdf_cuda_normal_map, from one host thread per
+        # G-buffer in flight (each its own engine context: stream, staging pipe, weights), so
+        # one G-buffer's H2D / D2H overlaps another's normal tiles.  Every G-buffer's normals
+        # land in host memory inside the timing.
+        import threading
+        from paper_2201_09147_b200.engine import Context, DeviceSequence
+        T = 3
+        extra = [Context(ctx.device, args.mode) for _ in range(T - 1)]
+        lanes = [(ctx, ds)] + [(c, DeviceSequence(c, seq)) for c in extra]
+        srcs = [np.array(pts, copy=True) for _ in range(T)]
+
+        def work(li, n):
+            c, d = lanes[li]
+            for _ in range(n):
+                c.normal_map(d.handles[0], srcs[li], delta)
+
+        for li in range(T):
+            work(li, 1)
+        counts = [steps // T + (1 if li < steps % T else 0) for li in range(T)]
+        threads = [threading.Thread(target=work, args=(li, counts[li])) for li in range(T)]
         w0 = time.perf_counter()
-        for _ in range(steps):
-            ctx.normal_map(ds.handles[0], pts, delta)
+        for t in threads:
+            t.start()
+        for t in threads:
+            t.join()
         e_ms = (time.perf_counter() - w0) * 1e3
         return {"value": k * steps / (e_ms / 1e3) / 1e6, "unit": "Mnormals/s", "ms_per_frame": e_ms / steps,
                 "h2d_bytes_per_step": 12 * k, "d2h_bytes_per_step": 12 * k + 16,
-                "path": "nsdf_cuda_normal_map (C ABI, host points -> host normals)"}
+                "path": f"nsdf_cuda_normal_map (C ABI, host points -> host normals) from {T} host threads, "
+                        f"one context each"}
     cam, cfg, shade, src, levels = W["cam"], W["cfg"], W["shade"], W["src"], W["levels"]
     frame_times = W.get("frame_times")  # animated: this rank's frame times t_i = i/(n-1)
     if world == 1 or W.get("shard_frames") or frame_times:
