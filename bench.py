@@ -82,11 +82,12 @@ def parse():
                     help="frames in flight (engine contexts on their own streams); 1 = strictly serial frames; "
                          "0 = 3, or 5 for tile-sharded frames on >= 4 GPUs (smaller shares leave more "
                          "level-tail idle time to overlap: tools/shardsim.py, N=8: 6.19x -> 6.38x)")
-    ap.add_argument("--shard", default="frames", choices=["frames", "tiles"],
-                    help="N > 1, single-frame configs: 'frames' = every rank renders whole frames of the frame "
-                         "stream (weak scaling; frames stay on their rank), 'tiles' = the ranks split every frame's "
-                         "image tiles and assemble it in rank 0's framebuffer (strong scaling).  The frames run also "
-                         "times a tile-sharded pass and reports it as strong_scaling")
+    ap.add_argument("--shard", default="tiles", choices=["frames", "tiles"],
+                    help="N > 1, single-frame configs 1-4: 'tiles' (default, the headline) = the ranks split every "
+                         "frame's image tiles and assemble it in rank 0's framebuffer (strong scaling, ms_per_frame "
+                         "is the latency of one whole frame); 'frames' = every rank renders whole frames of the "
+                         "frame stream (weak scaling; frames stay on their rank) and a tile-sharded pass is timed "
+                         "beside it as strong_scaling.  Config 5 (animation) always shards frames")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-alt", action="store_true", help="skip the (40,20,20) parity-setting line of config 2")
@@ -123,6 +124,17 @@ def ncu_traffic(gbuffer: bool):
         return None, None
     return sum(sel.values()), f"DRAM read+write bytes of the {len(sel)} trace-level launches of one frame, " \
                              f"ncu --set full ({d['source']})"
+
+
+def ncu_kernel_traffic(prefix: str):
+    """DRAM bytes per launch of one kernel (name prefix) from the committed ncu capture."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_traffic.json")))
+    if not files:
+        return None
+    d = json.load(open(files[-1]))
+    sel = [v for k, v in d["dram_bytes_per_launch"].items() if k.startswith(prefix)]
+    return sel[0] if len(sel) == 1 else None
 
 
 class ClockSampler:
@@ -186,6 +198,18 @@ class ClockSampler:
                           s[3 + i].lower().startswith("active")})
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
                 "reasons": reasons, "samples": len(inside), "window": window}
+
+
+def check_paths(stats, budgets, mode):
+    """Every traced level and the normal tiles must have run the kernel family of the mode
+    (tcgen05 in the fast modes): a bench line measured on another path is invalid."""
+    from paper_2201_09147_b200.abi import PATH_NONE, PATH_SIMT, PATH_TCGEN05
+    want = PATH_SIMT if mode == "fp32" else PATH_TCGEN05
+    got = [int(stats.level_path[j]) for j in range(len(budgets))]
+    exp = [want if b > 0 else PATH_NONE for b in budgets]
+    if got != exp or (stats.hits and int(stats.normals_path) != want):
+        raise SystemExit(f"kernel path check failed: levels {got} (expected {exp}), normals {int(stats.normals_path)}")
+    return got
 
 
 def sub_manifest(args):
@@ -327,7 +351,11 @@ def run_e2e(args, ctx, ds, seq, stream, world, rank, W):
         for t in threads:
             t.join()
         e_ms = (time.perf_counter() - w0) * 1e3
-        return {"value": k * steps / (e_ms / 1e3) / 1e6, "unit": "Mnormals/s", "ms_per_frame": e_ms / steps,
+        for c in extra:
+            c.close()
+        from paper_2201_09147_b200 import scheduler
+        rate, e_ms = scheduler.job_rate(k * steps, e_ms, world, device="cuda")  # all ranks / slowest rank
+        return {"value": rate / 1e6, "unit": "Mnormals/s", "ms_per_frame": e_ms / steps,
                 "h2d_bytes_per_step": 12 * k, "d2h_bytes_per_step": 12 * k + 16,
                 "path": f"nsdf_cuda_normal_map (C ABI, host points -> host normals) from {T} host threads, "
                         f"one context each"}
@@ -401,8 +429,23 @@ def run_e2e(args, ctx, ds, seq, stream, world, rank, W):
     level_bytes = 16 * len(levels) + 4 * 8 + 128 + 272  # camera + configs + level table
     # frames mode: every rank's frames; animated: the whole sequence over all ranks
     frames = W["total_frames"] if frame_times else steps * (world if W.get("shard_frames") else 1)
+    # The reference-shaped caller: shading::render returns an ImageBuffer of std::vectors, i.e.
+    # PAGEABLE host memory — nsdf_cuda_render into fresh numpy arrays, one frame at a time from
+    # one thread (rank 0, N = 1), next to the pinned multi-lane number above.
+    pageable = None
+    if rank == 0 and world == 1 and not frame_times:
+        ctx.render(levels, cam, cfg, shade, src)
+        n_pg = max(3, min(steps, 10))
+        w0 = time.perf_counter()
+        for _ in range(n_pg):
+            ctx.render(levels, cam, cfg, shade, src)
+        pg_ms = (time.perf_counter() - w0) * 1e3 / n_pg
+        pageable = {"value": npix / (pg_ms / 1e3) / 1e6, "unit": "Mrays/s", "ms_per_frame": pg_ms, "frames": n_pg,
+                    "path": "nsdf_cuda_render into pageable host arrays (ImageBuffer-shaped), 1 thread, 1 frame "
+                            "in flight"}
     return {"value": npix * frames / (e_ms / 1e3) / 1e6, "unit": "Mrays/s", "ms_per_frame": e_ms / frames,
-            "h2d_bytes_per_step": level_bytes, "d2h_bytes_per_step": npix * (12 + 4 + 1), "path": path}
+            "h2d_bytes_per_step": level_bytes, "d2h_bytes_per_step": npix * (12 + 4 + 1), "path": path,
+            "pageable": pageable}
 
 
 def tile_pass(args, ctx, W, world, rank, Wd, Hd):
@@ -421,10 +464,14 @@ def tile_pass(args, ctx, W, world, rank, Wd, Hd):
     tok = torch.zeros(1, dtype=torch.int32, device="cuda")
     cs = torch.cuda.Stream()  # every token all-reduce on ONE stream, in frame order
     lv = [d.levels() for _, _, d in lanes]
+    R = 2 * len(lanes)
+    tok_ev = [None] * R
 
     def frame(i):
         c, st, _ = lanes[i % len(lanes)]
-        fr, fd, fm = peer.ptrs(i % (2 * len(lanes)))
+        if tok_ev[(i + 1) % R] is not None:  # slot i % R is free once frame i-R+1's token completed
+            st.wait_event(tok_ev[(i + 1) % R])
+        fr, fd, fm = peer.ptrs(i % R)
         c.render_device(lv[i % len(lanes)], W["cam"], W["cfg"], W["shade"], fr, fd, fm, W["src"], -1, args.tile, rank,
                         world)
         ev = torch.cuda.Event()
@@ -432,6 +479,9 @@ def tile_pass(args, ctx, W, world, rank, Wd, Hd):
         cs.wait_event(ev)
         with torch.cuda.stream(cs):
             dist.all_reduce(tok)
+            done = torch.cuda.Event()
+            done.record(cs)
+        tok_ev[i % R] = done
 
     n = max(2 * len(lanes), min(args.steps, 30))
     for i in range(max(3, len(lanes))):
@@ -595,8 +645,16 @@ def main():
             lv = lane_levels[li][i % len(lane_levels[li])]
             if peer is not None:
                 # this rank's tiles of frame i land in rank 0's ring slot; the 4-byte all-reduce
-                # on the lane stream completes once every rank's kernels of frame i are done
-                fr, fd, fm = peer.ptrs(i % (2 * len(lanes)))
+                # on the token stream completes once every rank's kernels of frame i are done.
+                # Slot reuse: frame i overwrites the slot of frame i-R (R = ring depth) only after
+                # the token of frame i-R+1 completed here — i.e. after every rank finished frames
+                # <= i-R+1 and rank 0 issued that all-reduce, which it does only after its host
+                # copy of frame i-R (the e2e loop reads a slot synchronously before the next step)
+                R = 2 * len(lanes)
+                prev = tok_ev[(i + 1) % R]
+                if prev is not None:
+                    st.wait_event(prev)
+                fr, fd, fm = peer.ptrs(i % R)
                 c.render_device(lv, W["cam"], cfg, W["shade"], fr, fd, fm, W["src"], -1, args.tile, tile_rank,
                                 tile_world)
                 ev = torch.cuda.Event()
@@ -628,6 +686,7 @@ def main():
         fb0 = peer.ptrs(0) if peer is not None else (rgb.data_ptr(), depth.data_ptr(), mask.data_ptr())
         stats = ctx.render_device(W["levels"], W["cam"], cfg, W["shade"], *fb0, W["src"], -1, args.tile, tile_rank,
                                   tile_world, stats=True)
+        check_paths(stats, budgets, args.mode)
         if peer is not None:
             dist.barrier()
     W["step"] = step
@@ -686,12 +745,16 @@ def main():
 
     pk, pk_kind = peaks()
     traffic, traffic_note = ncu_traffic(W["gbuffer"]) if args.config == 2 else (None, None)
-    peak_tf = pk.get("bf16_tflops_sustained", pk["bf16_tflops"])
+    # the roofline denominator: the BURST bf16 figure (kernels timed in short launches at the
+    # clock they actually run at); the sustained figure is reported beside it
+    peak_tf = pk["bf16_tflops"]
+    peak_sust = pk.get("bf16_tflops_sustained", peak_tf)
     if W["gbuffer"]:
         flops_trace, flops_normals = 0, units_per_step * 2 * seq.members[0].macs_normal()
         achieved_tf = flops_normals / (ms_per_frame / 1e3) / 1e12
         kernel = "fused fwd+3-tangent normal tiles (256x3)"
         frame = {"points": units_per_step}
+        all_levels = None
     else:
         normal_idx = len(seq.members) - 1 if W["src"] == 1 else max(j for j, b in enumerate(budgets) if b > 0)
         flops_trace, flops_normals = frame_flops(seq, stats, normal_idx)
@@ -718,8 +781,9 @@ def main():
                 continue
             issued = ev * (2 * 32 * w + hb * (mult * 2 * w * w + 2 * 16 * w))
             sn = ev * (m.n_layers - 1) * w
-            per_kernel.append({"kernel": f"trace level {j} ({w}x{hb})", "ms": ms_j, "evals": ev,
-                               "tflops_algorithmic": ev * 2 * m.macs_forward() / (ms_j / 1e3) / 1e12,
+            tf = ev * 2 * m.macs_forward() / (ms_j / 1e3) / 1e12
+            per_kernel.append({"kernel": f"trace level {j} ({w}x{hb})", "ncu_name": f"tc_mlp_kernel<{w}, 0,",
+                               "ms": ms_j, "evals": ev, "tflops_algorithmic": tf, "frac_burst": tf / peak_tf,
                                "tensor_issued_frac": issued / (ms_j / 1e3) / 1e12 / peak_tf,
                                "mufu_frac": sn / (ms_j / 1e3) / xu_peak})
         if normals_ms > 0 and int(stats.normal_evals):
@@ -727,10 +791,22 @@ def main():
             w, hb, ev = m.width, m.hidden_blocks, int(stats.normal_evals)
             issued = 4 * ev * (2 * 32 * w + hb * (mult * 2 * w * w + 2 * 16 * w))
             per_kernel.append({"kernel": f"normal tiles + shading ({w}x{hb}, 4 rows per hit)", "ms": normals_ms,
-                               "evals": ev, "tflops_algorithmic": flops_normals / (normals_ms / 1e3) / 1e12,
+                               "ncu_name": f"tc_mlp_kernel<{w}, 1,", "evals": ev,
+                               "tflops_algorithmic": flops_normals / (normals_ms / 1e3) / 1e12,
+                               "frac_burst": flops_normals / (normals_ms / 1e3) / 1e12 / peak_tf,
                                "tensor_issued_frac": issued / (normals_ms / 1e3) / 1e12 / peak_tf,
                                "mufu_frac": 4 * ev * (m.n_layers - 1) * w / (normals_ms / 1e3) / xu_peak})
         act_bound["per_kernel"] = per_kernel
+        # roofline = the DOMINANT kernel (largest share of the frame), algorithmic FLOPs per
+        # launch / its CUDA-event launch time; the all-levels aggregate is reported beside it
+        all_levels = {"achieved": achieved_tf, "frac_burst": achieved_tf / peak_tf,
+                      "frac_sustained": achieved_tf / peak_sust, "kernel": kernel}
+        if per_kernel:
+            dom = max(per_kernel, key=lambda r: r["ms"])
+            achieved_tf, kernel = dom["tflops_algorithmic"], dom["kernel"]
+            traffic = ncu_kernel_traffic(dom["ncu_name"]) if args.config == 2 else None
+            traffic_note = "DRAM read+write bytes per launch of the dominant kernel, ncu --set full" \
+                if traffic is not None else None
         frame = {"evals_per_level": [int(x) for x in list(stats.evals)[:len(seq.members)]], "hits": int(stats.hits),
                  "fallbacks": int(stats.fallback_evals), "tflop_trace": flops_trace / 1e12,
                  "tflop_normals": flops_normals / 1e12, "trace_ms": trace_ms, "normals_ms": normals_ms,
@@ -828,8 +904,9 @@ def main():
             "strong_scaling": strong,
             "roofline": {"bound": "tensor", "kernel": kernel, "achieved": achieved_tf, "peak": peak_tf,
                          "unit": "TFLOP/s", "frac": achieved_tf / peak_tf,
-                         "peak_kind": f"{pk_kind} bf16 sustained (MEASURED_PEAKS.json)", "traffic": traffic,
-                         "traffic_note": traffic_note,
+                         "peak_kind": f"{pk_kind} bf16 burst (MEASURED_PEAKS.json bf16_tflops)",
+                         "frac_vs_sustained": achieved_tf / peak_sust, "traffic": traffic,
+                         "traffic_note": traffic_note, "all_trace_levels": all_levels,
                          "whole_frame_tflops": (flops_trace + flops_normals) / (ms_per_frame / 1e3) / 1e12,
                          "activation_bound": None if W["gbuffer"] else act_bound,
                          "hbm": hbm},

@@ -35,8 +35,11 @@
  *   nsdf_cuda_tensor_scale_rows Table::scale_rows_f32 / _f64, tensor::scale_rows kernels.hpp:34-36, ops.cpp:81-95
  *   nsdf_cuda_tensor_sine     Table::sine_f32 / _f64, tensor::activate (sine) kernels.hpp:38-39, ops.cpp:57-79
  *   nsdf_cuda_render_multi    shading::render over N contexts (N GPUs) from one process:
- *                             interleaved tiles per context, gathered into a host framebuffer
- *                             (SURVEY.md §8b "nsdf_cuda_render_multi(ctxs[], n, ...)")
+ *                             interleaved tiles per context, stored by each GPU straight into
+ *                             the root GPU's framebuffer over NVLink (SURVEY.md §8b
+ *                             "nsdf_cuda_render_multi(ctxs[], n, ...)")
+ *   nsdf_cuda_replicate_field the once-per-sequence weight broadcast of the multi-GPU path
+ *                             (device-to-device; NeuralField ctor on the other GPUs)
  *
  * Conventions
  *   - Plain C types only; no exceptions cross this boundary.  Every function returns an
@@ -62,7 +65,7 @@
 extern "C" {
 #endif
 
-#define NSDF_CUDA_ABI_VERSION 1
+#define NSDF_CUDA_ABI_VERSION 2
 #define NSDF_MAX_LEVELS 8 /* tracer::kMaxLevels, trace.hpp:32 */
 #define NSDF_MAX_LIGHTS 8
 
@@ -153,7 +156,21 @@ typedef struct {
   uint64_t normal_evals;           /* fwd+gradient evaluations for normals         */
   uint64_t fallback_evals;         /* own-field normals computed for the fallback  */
   uint64_t kernel_launches;        /* engine kernels launched for the frame        */
+  /* Which kernel family ran each part of the frame (nsdf_kernel_path).  A fast-mode frame
+   * whose MLP levels do not all report NSDF_PATH_TCGEN05 did not run on the tensor cores;
+   * a failed tcgen05 launch is an error (NSDF_ERR_DEVICE), never a silent FFMA fallback. */
+  uint8_t level_path[NSDF_MAX_LEVELS]; /* per traced level; NSDF_PATH_NONE if skipped    */
+  uint8_t normals_path;                /* the normal + shade tiles of the hit list      */
+  uint8_t fallback_path;               /* own-field fallback normals (mapped mode)      */
+  uint8_t reserved_[6];
 } nsdf_frame_stats;
+
+/* Kernel families reported in nsdf_frame_stats. */
+typedef enum {
+  NSDF_PATH_NONE = 0,    /* not run                                                       */
+  NSDF_PATH_SIMT = 1,    /* FFMA tiles (FP32 oracle mode, analytic fields, other widths)  */
+  NSDF_PATH_TCGEN05 = 2  /* tcgen05 tensor-core tiles (persistent level / normal tiles)   */
+} nsdf_kernel_path;
 
 /* Per-kernel-family device time (CUDA events on the context stream), accumulated over
  * frames while profiling is enabled — the "CUDA events per level and per frame" of
@@ -193,6 +210,8 @@ typedef struct {
 /* ---- context ---------------------------------------------------------------------- */
 int nsdf_cuda_abi_version(void);
 const char* nsdf_cuda_last_error(void);
+/* Number of visible CUDA devices (NSDF_ERR_DEVICE when there is none). */
+int nsdf_cuda_device_count(int* n);
 int nsdf_cuda_create(int device, nsdf_ctx** out);
 int nsdf_cuda_destroy(nsdf_ctx* ctx);
 int nsdf_cuda_set_mode(nsdf_ctx* ctx, int mode);
@@ -228,6 +247,11 @@ int nsdf_cuda_upload_mlp(nsdf_ctx* ctx, int n_layers, const int32_t* rows, const
 int nsdf_cuda_upload_analytic(nsdf_ctx* ctx, int kind, const double* params, int n_params,
                               nsdf_field* out);
 int nsdf_cuda_release(nsdf_ctx* ctx, nsdf_field field);
+/* Weight broadcast for multi-GPU rendering: copies field `field` of `src` (its packed device
+ * image: f32/f64 weights and the fp16 tensor-core copy, one allocation) to `dst`'s device
+ * with one device-to-device peer copy (NVLink), no host round trip; *out is the handle in
+ * dst.  The replica evaluates bit-identically to the source. */
+int nsdf_cuda_replicate_field(nsdf_ctx* src, nsdf_field field, nsdf_ctx* dst, nsdf_field* out);
 int nsdf_cuda_field_info(nsdf_ctx* ctx, nsdf_field field, int* input_dim, int* n_layers,
                          int* width);
 
@@ -330,10 +354,15 @@ int nsdf_cuda_render(nsdf_ctx* ctx, const nsdf_level* levels, int m, const nsdf_
  * may be NULL) forces a synchronize. */
 /* Single-process multi-GPU render: context i (its own device and stream) renders the image
  * tiles t % n == i (tile_size x tile_size, row-major tile order) with its own field handles
- * levels[i][0..m); the owned pixels are packed on each device, copied to the host and
- * scattered into the caller's HOST framebuffer (synchronous).  The contexts render
- * concurrently; the image equals nsdf_cuda_render's for any n (per-ray work does not depend
- * on the partition).  stats (optional) sums the contexts' counters. */
+ * levels[i][0..m) (nsdf_cuda_replicate_field copies ctxs[0]'s weights device to device).
+ * The framebuffer lives on ctxs[0]'s device: every context's background and shading
+ * kernels store their pixels straight into it over NVLink (peer access, enabled on first
+ * use); device pairs that cannot be peers pack their pixels, peer-copy them and scatter on
+ * ctxs[0]'s device.  No host scatter: one D2H of the assembled frame into the caller's HOST
+ * framebuffer (synchronous).  The contexts render concurrently (cross-device events, no
+ * host synchronisation between them); the image equals nsdf_cuda_render's for any n
+ * (per-ray work does not depend on the partition).  stats (optional) sums the contexts'
+ * counters; a level's path is NSDF_PATH_TCGEN05 only if every context ran it there. */
 int nsdf_cuda_render_multi(nsdf_ctx* const* ctxs, int n, const nsdf_level* const* levels, int m,
                            const nsdf_camera* camera, const nsdf_trace_config* trace,
                            const nsdf_shade_config* shade, int normal_source, int fine_index,

@@ -13,6 +13,7 @@ LIB_PATH = os.environ.get("NSDF_CUDA_LIB") or os.path.join(PKG_DIR, "libnsdf_cud
 HOST_LIB_PATH = os.path.join(PKG_DIR, "libnsdf_b200.so")
 
 MAX_LEVELS = 8
+PATH_NONE, PATH_SIMT, PATH_TCGEN05 = 0, 1, 2  # nsdf_kernel_path
 MAX_LIGHTS = 8
 
 OK, ERR_CONTRACT, ERR_CONFIG, ERR_VALIDATION, ERR_PARSE, ERR_DIVERGENCE, ERR_DEVICE = range(7)
@@ -105,7 +106,8 @@ class Level(ctypes.Structure):
 class FrameStats(ctypes.Structure):
     _fields_ = [("evals", ctypes.c_uint64 * MAX_LEVELS), ("hits", ctypes.c_uint64),
                 ("normal_evals", ctypes.c_uint64), ("fallback_evals", ctypes.c_uint64),
-                ("kernel_launches", ctypes.c_uint64)]
+                ("kernel_launches", ctypes.c_uint64), ("level_path", ctypes.c_uint8 * MAX_LEVELS),
+                ("normals_path", ctypes.c_uint8), ("fallback_path", ctypes.c_uint8), ("reserved_", ctypes.c_uint8 * 6)]
 
 
 class Profile(ctypes.Structure):

@@ -39,14 +39,53 @@ int fail(int status, const std::string& msg) {
 
 struct FieldRec {
   DevField dev{};
-  std::vector<void*> allocs;
+  void* image = nullptr;  // every device array of the field (one allocation, see FieldImage)
+  size_t image_bytes = 0;
+  int device = 0;
   int input_dim = 3;
   int n_layers = 0;
   int width = 0;
   ~FieldRec() {
-    for (void* p : allocs) cudaFree(p);
+    if (image) {
+      int prev = -1;
+      cudaGetDevice(&prev);
+      if (prev != device) cudaSetDevice(device);
+      cudaFree(image);
+      if (prev >= 0 && prev != device) cudaSetDevice(prev);
+    }
   }
 };
+
+// Host staging of a field image: arrays appended at 256-byte aligned offsets.
+struct FieldImage {
+  std::vector<uint8_t> bytes;
+  template <typename T>
+  size_t add(const std::vector<T>& v) {
+    const size_t off = (bytes.size() + 255) / 256 * 256;
+    bytes.resize(off + v.size() * sizeof(T));
+    if (!v.empty()) std::memcpy(bytes.data() + off, v.data(), v.size() * sizeof(T));
+    return off;
+  }
+};
+
+// Rebases every device pointer of a field image copied from `from` to `to`.
+template <typename T>
+void rebase_ptr(const T*& p, const void* from, const void* to) {
+  if (p) p = reinterpret_cast<const T*>(static_cast<const char*>(to) + (reinterpret_cast<const char*>(p) -
+                                                                        static_cast<const char*>(from)));
+}
+void rebase_net(DevNet& n, const void* from, const void* to) {
+  for (int l = 0; l < n.n_layers; ++l) {
+    rebase_ptr(n.w[l], from, to);
+    rebase_ptr(n.wt[l], from, to);
+    rebase_ptr(n.b[l], from, to);
+    rebase_ptr(n.w64[l], from, to);
+    rebase_ptr(n.wt64[l], from, to);
+    rebase_ptr(n.b64[l], from, to);
+  }
+  rebase_ptr(n.wq, from, to);
+  rebase_ptr(n.bias_cat, from, to);
+}
 
 struct DeviceGuard {
   int prev = -1;
@@ -105,6 +144,8 @@ struct nsdf_ctx {
   Profiler prof;
   BatchPipe pipe;    // chunked host-buffer batches
   std::vector<cudaEvent_t> copy_events;  // staged pageable framebuffer copies (copy_out_frame)
+  std::vector<cudaEvent_t> frame_events; // render_multi: cross-device frame ordering
+  Workspace stage;   // render_multi copy path: other devices' packed pixels on this device
 };
 
 namespace {
@@ -270,19 +311,43 @@ struct FrameOut {
   int* d_pack_count = nullptr;
 };
 
+// Frame accounting whose counter read-back is still in flight (render_multi: the devices
+// must not be serialised by a per-context synchronize); finish_stats() completes it.
+struct PendingStats {
+  std::vector<LevelDesc> lv;
+  TraceResult tr;
+  int n_counters = 0;
+  const int* h_counters = nullptr;  // pinned (the context's frame workspace)
+  uint64_t launches = 0;
+  int normals_path = NSDF_PATH_NONE, fallback_path = NSDF_PATH_NONE;
+  bool rgb = false;
+};
+
+void finish_stats(const PendingStats& p, nsdf_frame_stats* stats) {
+  std::vector<int> counters(p.h_counters, p.h_counters + p.n_counters);
+  fill_stats(p.lv, p.tr, counters, stats);
+  stats->normal_evals = p.rgb ? stats->hits : 0;
+  stats->fallback_evals = p.rgb ? uint64_t(counters[p.n_counters - 2]) : 0;
+  stats->kernel_launches = p.launches;
+  for (size_t i = 0; i < p.lv.size(); ++i)
+    stats->level_path[p.lv[i].level] = uint8_t(p.tr.persistent[i] ? NSDF_PATH_TCGEN05 : NSDF_PATH_SIMT);
+  stats->normals_path = uint8_t(p.normals_path);
+  stats->fallback_path = uint8_t(p.fallback_path);
+}
+
 int run_frame_impl(nsdf_ctx* c, const nsdf_level* levels, int m, const nsdf_trace_config* cfg, const CamBasis* cam,
                    const float* d_rays6, int n_rays, const ShadeParams* sp, int normal_source, int fine_index,
                    int tile_size, int tile_rank, int tile_world, const FrameOut& out, nsdf_frame_stats* stats,
-                   float final_delta);
+                   float final_delta, PendingStats* pending);
 
 // NVTX range per frame (host-side launch sequence; visible in Nsight timelines, free otherwise)
 int run_frame(nsdf_ctx* c, const nsdf_level* levels, int m, const nsdf_trace_config* cfg, const CamBasis* cam,
               const float* d_rays6, int n_rays, const ShadeParams* sp, int normal_source, int fine_index,
               int tile_size, int tile_rank, int tile_world, const FrameOut& out, nsdf_frame_stats* stats,
-              float final_delta = 0.0f) {
+              float final_delta = 0.0f, PendingStats* pending = nullptr) {
   nvtxRangePushA(out.d_rgb ? "nsdf render frame" : "nsdf trace frame");
   const int st = run_frame_impl(c, levels, m, cfg, cam, d_rays6, n_rays, sp, normal_source, fine_index, tile_size,
-                                tile_rank, tile_world, out, stats, final_delta);
+                                tile_rank, tile_world, out, stats, final_delta, pending);
   nvtxRangePop();
   return st;
 }
@@ -290,7 +355,7 @@ int run_frame(nsdf_ctx* c, const nsdf_level* levels, int m, const nsdf_trace_con
 int run_frame_impl(nsdf_ctx* c, const nsdf_level* levels, int m, const nsdf_trace_config* cfg, const CamBasis* cam,
                    const float* d_rays6, int n_rays, const ShadeParams* sp, int normal_source, int fine_index,
                    int tile_size, int tile_rank, int tile_world, const FrameOut& out, nsdf_frame_stats* stats,
-                   float final_delta) {
+                   float final_delta, PendingStats* pending) {
   int n_counters = 0;
   std::vector<LevelDesc> lv = traced_levels(c, levels, m, cfg, &n_counters, final_delta);
   // slots needed: every pixel, or only the pixels of the owned tiles (tile % world == rank)
@@ -322,7 +387,11 @@ int run_frame_impl(nsdf_ctx* c, const nsdf_level* levels, int m, const nsdf_trac
   launches++;
   launch_reset_state(fb.st, n_max, s);
   TraceResult tr = run_trace(mode_of(c), lv, cfg->eps_stop, cfg->t_max, fb, n_max, n_slots, s, prof);
+  if (tr.error != cudaSuccess)
+    return fail(NSDF_ERR_DEVICE, "tcgen05 trace launch of level " + std::to_string(tr.failed_level) +
+                                     " failed: " + cudaGetErrorString(tr.error));
   launches += tr.launches;
+  int normals_path = NSDF_PATH_NONE, fallback_path = NSDF_PATH_NONE;
   if (out.d_records) {
     launch_mark_hits(tr.hit_list, tr.hit_count, n_max, fb.st, s);
     launch_write_records(fb.st, n_max, out.d_records, s);
@@ -340,13 +409,18 @@ int run_frame_impl(nsdf_ctx* c, const nsdf_level* levels, int m, const nsdf_trac
     const bool defer = mapped && fine != eff;
     const DevField& nf = c->fields[levels[nidx].field]->dev;
     cudaEvent_t ev_n = prof ? prof->begin(s) : nullptr;
-    launch_normals_shade(mode_of(c), nf, levels[nidx].time, tr.hit_list, tr.hit_count, n_max, fb.st, *sp, defer,
-                         fb.fallback_list, fb_count, out.d_rgb, out.d_depth, out.d_mask, s);
+    normals_path = launch_normals_shade(mode_of(c), nf, levels[nidx].time, tr.hit_list, tr.hit_count, n_max, fb.st,
+                                        *sp, defer, fb.fallback_list, fb_count, out.d_rgb, out.d_depth, out.d_mask, s);
+    if (normals_path < 0)
+      return fail(NSDF_ERR_DEVICE, std::string("tcgen05 normal tiles failed: ") + cudaGetErrorString(tc_last_error()));
     launches += 2;
     if (defer) {  // own-field normals only where the fine gradient vanished (render.cpp:62-65)
       const DevField& own = c->fields[levels[eff].field]->dev;
-      launch_normals_shade(mode_of(c), own, levels[eff].time, fb.fallback_list, fb_count, n_max, fb.st, *sp, false,
-                           nullptr, nullptr, out.d_rgb, out.d_depth, out.d_mask, s);
+      fallback_path = launch_normals_shade(mode_of(c), own, levels[eff].time, fb.fallback_list, fb_count, n_max,
+                                           fb.st, *sp, false, nullptr, nullptr, out.d_rgb, out.d_depth, out.d_mask, s);
+      if (fallback_path < 0)
+        return fail(NSDF_ERR_DEVICE,
+                    std::string("tcgen05 fallback normal tiles failed: ") + cudaGetErrorString(tc_last_error()));
       launches++;
     }
     if (prof) {
@@ -362,14 +436,24 @@ int run_frame_impl(nsdf_ctx* c, const nsdf_level* levels, int m, const nsdf_trac
   }
   if (prof) prof->end(Profiler::kFrame, ev_frame, s);
   NSDF_CUDA(cudaGetLastError());
-  if (stats) {
-    std::vector<int> counters(n_counters);
-    NSDF_CUDA(cudaMemcpyAsync(counters.data(), fb.counters, size_t(n_counters) * 4, cudaMemcpyDeviceToHost, s));
-    NSDF_CUDA(cudaStreamSynchronize(s));
-    fill_stats(lv, tr, counters, stats);
-    stats->normal_evals = out.d_rgb ? stats->hits : 0;
-    stats->fallback_evals = out.d_rgb ? uint64_t(counters[n_counters - 2]) : 0;
-    stats->kernel_launches = launches;
+  if (stats || pending) {
+    PendingStats local;
+    PendingStats& p = pending ? *pending : local;
+    NSDF_CUDA(c->frame.reserve_host(size_t(n_counters) * 4));
+    int* h = static_cast<int*>(c->frame.host_pinned);
+    NSDF_CUDA(cudaMemcpyAsync(h, fb.counters, size_t(n_counters) * 4, cudaMemcpyDeviceToHost, s));
+    p.lv = lv;
+    p.tr = tr;
+    p.n_counters = n_counters;
+    p.h_counters = h;
+    p.launches = launches;
+    p.normals_path = normals_path;
+    p.fallback_path = fallback_path;
+    p.rgb = out.d_rgb != nullptr;
+    if (!pending) {
+      NSDF_CUDA(cudaStreamSynchronize(s));
+      finish_stats(p, stats);
+    }
   }
   return NSDF_OK;
 }
@@ -398,6 +482,14 @@ extern "C" {
 int nsdf_cuda_abi_version(void) { return NSDF_CUDA_ABI_VERSION; }
 
 const char* nsdf_cuda_last_error(void) { return g_error.c_str(); }
+
+int nsdf_cuda_device_count(int* n) {
+  if (!n) return fail(NSDF_ERR_CONTRACT, "null argument");
+  *n = 0;
+  NSDF_CUDA(cudaGetDeviceCount(n));
+  if (*n < 1) return fail(NSDF_ERR_DEVICE, "no CUDA device");
+  return NSDF_OK;
+}
 
 int nsdf_cuda_create(int device, nsdf_ctx** out) {
   if (!out) return fail(NSDF_ERR_CONTRACT, "out is null");
@@ -435,7 +527,10 @@ int nsdf_cuda_destroy(nsdf_ctx* c) {
     c->io.~Workspace();
     new (&c->io) Workspace();
     c->pipe.release();
+    c->stage.~Workspace();
+    new (&c->stage) Workspace();
     for (cudaEvent_t e : c->copy_events) cudaEventDestroy(e);
+    for (cudaEvent_t e : c->frame_events) cudaEventDestroy(e);
     if (c->own) cudaStreamDestroy(c->own);
   }
   delete c;
@@ -570,6 +665,7 @@ int nsdf_cuda_upload_mlp(nsdf_ctx* c, int n_layers, const int32_t* rows, const i
   std::lock_guard<std::mutex> lk(c->mu);
   DeviceGuard g(c->device);
   auto rec = std::make_unique<FieldRec>();
+  rec->device = c->device;
   DevNet& n = rec->dev.net;
   rec->dev.kind = kFieldMlp;
   n.n_layers = n_layers;
@@ -578,7 +674,13 @@ int nsdf_cuda_upload_mlp(nsdf_ctx* c, int n_layers, const int32_t* rows, const i
   n.omega = float(omega0);
   n.omega_d = omega0;
   n.max_width = maxw;
+  // Every device array of the field lives in ONE allocation (the field image): uploaded
+  // with one copy, and replicated to other devices with one peer copy
+  // (nsdf_cuda_replicate_field) plus a pointer rebase.
+  FieldImage img;
   size_t off = 0;
+  size_t o_w64[kMaxLayers], o_wt64[kMaxLayers], o_b64[kMaxLayers], o_w[kMaxLayers], o_wt[kMaxLayers],
+      o_b[kMaxLayers];
   for (int l = 0; l < n_layers; ++l) {
     const int R = rows[l], K = cols[l], Rp = (R + 3) / 4 * 4;
     std::vector<float> w(size_t(R) * K), wt(size_t(K) * Rp, 0.0f), b(R);
@@ -593,41 +695,22 @@ int nsdf_cuda_upload_mlp(nsdf_ctx* c, int n_layers, const int32_t* rows, const i
         wt[size_t(k) * Rp + i] = w[size_t(i) * K + k];
         wt64[size_t(k) * Rp + i] = w64[size_t(i) * K + k];
       }
-    double *dw64, *dwt64, *db64;
-    NSDF_CUDA(cudaMalloc(&dw64, w64.size() * 8));
-    rec->allocs.push_back(dw64);
-    NSDF_CUDA(cudaMalloc(&dwt64, wt64.size() * 8));
-    rec->allocs.push_back(dwt64);
-    NSDF_CUDA(cudaMalloc(&db64, b64.size() * 8));
-    rec->allocs.push_back(db64);
-    NSDF_CUDA(cudaMemcpy(dw64, w64.data(), w64.size() * 8, cudaMemcpyHostToDevice));
-    NSDF_CUDA(cudaMemcpy(dwt64, wt64.data(), wt64.size() * 8, cudaMemcpyHostToDevice));
-    NSDF_CUDA(cudaMemcpy(db64, b64.data(), b64.size() * 8, cudaMemcpyHostToDevice));
-    n.w64[l] = dw64;
-    n.wt64[l] = dwt64;
-    n.b64[l] = db64;
-    float *dw, *dwt, *db;
-    NSDF_CUDA(cudaMalloc(&dw, w.size() * 4));
-    rec->allocs.push_back(dw);
-    NSDF_CUDA(cudaMalloc(&dwt, wt.size() * 4));
-    rec->allocs.push_back(dwt);
-    NSDF_CUDA(cudaMalloc(&db, b.size() * 4));
-    rec->allocs.push_back(db);
-    NSDF_CUDA(cudaMemcpy(dw, w.data(), w.size() * 4, cudaMemcpyHostToDevice));
-    NSDF_CUDA(cudaMemcpy(dwt, wt.data(), wt.size() * 4, cudaMemcpyHostToDevice));
-    NSDF_CUDA(cudaMemcpy(db, b.data(), b.size() * 4, cudaMemcpyHostToDevice));
+    o_w64[l] = img.add(w64);
+    o_wt64[l] = img.add(wt64);
+    o_b64[l] = img.add(b64);
+    o_w[l] = img.add(w);
+    o_wt[l] = img.add(wt);
+    o_b[l] = img.add(b);
     n.rows[l] = R;
     n.cols[l] = K;
     n.rows_pad[l] = Rp;
-    n.w[l] = dw;
-    n.wt[l] = dwt;
-    n.b[l] = db;
   }
   // Fast-mode copy (mlp_tc.cu): sine nets whose hidden layers are square W x W with
   // W in {64, 128, 256}.  Hidden weights -> fp16 in the UMMA canonical K-major layout,
   // element (n, k) at ((k/8)*(W/8) + n/8)*64 + (n%8)*8 + k%8, so every 32-wide K chunk is
   // one contiguous bulk copy.
   n.tc_ok = 0;
+  size_t o_wq = 0, o_bias = 0;
   {
     const int W = rows[0];
     bool ok = activation == NSDF_ACT_SINE && n_layers >= 3 && (W == 64 || W == 128 || W == 256);
@@ -662,17 +745,26 @@ int nsdf_cuda_upload_mlp(nsdf_ctx* c, int n_layers, const int32_t* rows, const i
           n.bout = float(packed[o]);
         o += rows[l];
       }
-      void *dq, *db;
-      NSDF_CUDA(cudaMalloc(&dq, wq.size() * 2));
-      rec->allocs.push_back(dq);
-      NSDF_CUDA(cudaMalloc(&db, bias.size() * 4));
-      rec->allocs.push_back(db);
-      NSDF_CUDA(cudaMemcpy(dq, wq.data(), wq.size() * 2, cudaMemcpyHostToDevice));
-      NSDF_CUDA(cudaMemcpy(db, bias.data(), bias.size() * 4, cudaMemcpyHostToDevice));
-      n.wq = static_cast<const uint16_t*>(dq);
-      n.bias_cat = static_cast<const float*>(db);
+      o_wq = img.add(wq);
+      o_bias = img.add(bias);
       n.tc_ok = 1;
     }
+  }
+  NSDF_CUDA(cudaMalloc(&rec->image, img.bytes.size()));
+  rec->image_bytes = img.bytes.size();
+  NSDF_CUDA(cudaMemcpy(rec->image, img.bytes.data(), img.bytes.size(), cudaMemcpyHostToDevice));
+  const char* base = static_cast<const char*>(rec->image);
+  for (int l = 0; l < n_layers; ++l) {
+    n.w64[l] = reinterpret_cast<const double*>(base + o_w64[l]);
+    n.wt64[l] = reinterpret_cast<const double*>(base + o_wt64[l]);
+    n.b64[l] = reinterpret_cast<const double*>(base + o_b64[l]);
+    n.w[l] = reinterpret_cast<const float*>(base + o_w[l]);
+    n.wt[l] = reinterpret_cast<const float*>(base + o_wt[l]);
+    n.b[l] = reinterpret_cast<const float*>(base + o_b[l]);
+  }
+  if (n.tc_ok) {
+    n.wq = reinterpret_cast<const uint16_t*>(base + o_wq);
+    n.bias_cat = reinterpret_cast<const float*>(base + o_bias);
   }
   rec->input_dim = input_dim;
   rec->n_layers = n_layers;
@@ -690,6 +782,7 @@ int nsdf_cuda_upload_analytic(nsdf_ctx* c, int kind, const double* params, int n
   if (n_params != want) return fail(NSDF_ERR_CONTRACT, "analytic field expects " + std::to_string(want) + " params");
   std::lock_guard<std::mutex> lk(c->mu);
   auto rec = std::make_unique<FieldRec>();
+  rec->device = c->device;
   rec->dev.kind = kind;
   for (int i = 0; i < n_params; ++i) rec->dev.analytic[i] = params[i];
   rec->input_dim = 3;
@@ -727,8 +820,7 @@ int nsdf_cuda_eval_grad_device(nsdf_ctx* c, nsdf_field h, const float* d_points,
   FieldRec* f;
   if (int st = find_field(c, h, &f)) return st;
   if (int st = check_points(f, rows, k)) return st;
-  launch_eval(mode_of(c), f->dev, d_points, rows, k, time, d_out, d_grad, c->stream);
-  NSDF_CUDA(cudaGetLastError());
+  NSDF_CUDA(launch_eval(mode_of(c), f->dev, d_points, rows, k, time, d_out, d_grad, c->stream));
   return NSDF_OK;
 }
 
@@ -806,8 +898,7 @@ int run_chunked(nsdf_ctx* c, int k, const std::vector<HostIn>& ins, const std::v
                           ins.size() > 1 && ins[1].h ? din(b, 1) : nullptr};
     float* dd[2] = {outs.size() > 0 && outs[0].h ? dout(b, 0) : nullptr,
                     outs.size() > 1 && outs[1].h ? dout(b, 1) : nullptr};
-    launch(di, dd, n);
-    NSDF_CUDA(cudaGetLastError());
+    NSDF_CUDA(launch(di, dd, n));
     NSDF_CUDA(cudaEventRecord(p.ev_k[b], s));
     // the previous chunk's D2H after this chunk's kernels are queued (a pageable D2H returns
     // only when done, so queueing it first would idle the GPU behind the host)
@@ -838,7 +929,7 @@ int nsdf_cuda_eval_grad(nsdf_ctx* c, nsdf_field h, const float* points, int rows
   const Mode mode = mode_of(c);
   return run_chunked(c, k, {{points, rows}}, {{out, 1}, {grad, 3}},
                      [&](const float* const* di, float* const* dd, int n) {
-                       launch_eval(mode, f->dev, di[0], rows, n, time, dd[0], dd[1], c->stream);
+                       return launch_eval(mode, f->dev, di[0], rows, n, time, dd[0], dd[1], c->stream);
                      });
 }
 
@@ -956,8 +1047,7 @@ int nsdf_cuda_eval_f64(nsdf_ctx* c, nsdf_field h, const double* points, int rows
   double* dgrad = carve<double>(c->io.base, off, size_t(3) * k);
   cudaStream_t s = c->stream;
   NSDF_CUDA(cudaMemcpyAsync(dp, points, size_t(rows) * k * 8, cudaMemcpyHostToDevice, s));
-  launch_eval_f64(f->dev.net, dp, rows, k, time, out ? dout : nullptr, grad ? dgrad : nullptr, s);
-  NSDF_CUDA(cudaGetLastError());
+  NSDF_CUDA(launch_eval_f64(f->dev.net, dp, rows, k, time, out ? dout : nullptr, grad ? dgrad : nullptr, s));
   if (out) NSDF_CUDA(cudaMemcpyAsync(out, dout, size_t(k) * 8, cudaMemcpyDeviceToHost, s));
   if (grad) NSDF_CUDA(cudaMemcpyAsync(grad, dgrad, size_t(3) * k * 8, cudaMemcpyDeviceToHost, s));
   NSDF_CUDA(cudaStreamSynchronize(s));
@@ -1140,7 +1230,7 @@ int nsdf_cuda_normal_map(nsdf_ctx* c, nsdf_field fine, float time, const float* 
   if (int st = run_chunked(
           c, k, {{points, 3}, {fallback_normals, 3}}, {{normals, 3}},
           [&](const float* const* di, float* const* dd, int n) {
-            launch_normal_map(mode, f->dev, di[0], n, time, delta, di[1], dd[0], dc, s);
+            return launch_normal_map(mode, f->dev, di[0], n, time, delta, di[1], dd[0], dc, s);
           },
           &dc))
     return st;
@@ -1160,9 +1250,8 @@ int nsdf_cuda_normal_map_device(nsdf_ctx* c, nsdf_field fine, float time, const 
   FieldRec* f;
   if (int st = find_field(c, fine, &f)) return st;
   if (k < 0) return fail(NSDF_ERR_CONTRACT, "points must be 3xk");
-  launch_normal_map(mode_of(c), f->dev, d_points, k, time, delta, d_fallback, d_normals,
-                    reinterpret_cast<unsigned long long*>(d_counts), c->stream);
-  NSDF_CUDA(cudaGetLastError());
+  NSDF_CUDA(launch_normal_map(mode_of(c), f->dev, d_points, k, time, delta, d_fallback, d_normals,
+                              reinterpret_cast<unsigned long long*>(d_counts), c->stream));
   return NSDF_OK;
 }
 
@@ -1214,12 +1303,34 @@ int nsdf_cuda_shade(nsdf_ctx* c, const float* points, const float* normals, int 
   return NSDF_OK;
 }
 
+// The reference validates the lights inside shade(), which render() calls only when the
+// frame has hits (render.cpp:41, shade.cpp:47-49,61): a light error is therefore deferred
+// (LightCheck) — the frame renders with a placeholder light, and the error is raised only if
+// some ray hit (a hit-free frame is the background image, as in the reference).
+struct LightCheck {
+  int status = NSDF_OK;
+  std::string msg;
+};
+
 static int render_checks(nsdf_ctx* c, const nsdf_level* levels, int m, const nsdf_camera* camera,
                          const nsdf_trace_config* trace, const nsdf_shade_config* shade, int normal_source,
-                         int fine_index, CamBasis* cb, ShadeParams* sp) {
+                         int fine_index, CamBasis* cb, ShadeParams* sp, LightCheck* lc) {
   if (int st = validate_sequence(c, levels, m, trace)) return st;
   if (int st = camera_basis(camera, cb)) return st;
-  if (int st = shade_params(shade, camera, sp)) return st;
+  if (!shade) return fail(NSDF_ERR_CONTRACT, "shade config is null");
+  if (shade->n_lights > NSDF_MAX_LIGHTS)
+    return fail(NSDF_ERR_CONFIG, "at most " + std::to_string(NSDF_MAX_LIGHTS) + " lights supported");
+  if (int st = shade_params(shade, camera, sp)) {
+    lc->status = st;
+    lc->msg = g_error;
+    nsdf_shade_config placeholder = *shade;
+    placeholder.n_lights = 1;
+    placeholder.light_direction[0][0] = 0.0f;
+    placeholder.light_direction[0][1] = 1.0f;
+    placeholder.light_direction[0][2] = 0.0f;
+    placeholder.light_intensity[0] = 1.0f;
+    if (int st2 = shade_params(&placeholder, camera, sp)) return st2;
+  }
   if (normal_source != NSDF_NORMALS_OWN && normal_source != NSDF_NORMALS_MAPPED)
     return fail(NSDF_ERR_CONFIG, "normal source must be own or mapped");
   const int fine = fine_index < 0 ? m - 1 : fine_index;
@@ -1237,7 +1348,8 @@ int nsdf_cuda_render_device(nsdf_ctx* c, const nsdf_level* levels, int m, const 
   DeviceGuard g(c->device);
   CamBasis cb;
   ShadeParams sp;
-  if (int st = render_checks(c, levels, m, camera, trace, shade, normal_source, fine_index, &cb, &sp)) return st;
+  LightCheck lc;
+  if (int st = render_checks(c, levels, m, camera, trace, shade, normal_source, fine_index, &cb, &sp, &lc)) return st;
   if (tile_world < 1 || tile_rank < 0 || tile_rank >= tile_world)
     return fail(NSDF_ERR_CONFIG, "tile rank/world out of range");
   if (tile_world > 1 && tile_size < 1) return fail(NSDF_ERR_CONFIG, "tile size must be positive");
@@ -1245,8 +1357,76 @@ int nsdf_cuda_render_device(nsdf_ctx* c, const nsdf_level* levels, int m, const 
   fo.d_rgb = d_rgb;
   fo.d_depth = d_depth;
   fo.d_mask = d_mask;
-  return run_frame(c, levels, m, trace, &cb, nullptr, 0, &sp, normal_source, fine_index, tile_size, tile_rank,
-                   tile_world, fo, stats);
+  nsdf_frame_stats local;
+  if (int st = run_frame(c, levels, m, trace, &cb, nullptr, 0, &sp, normal_source, fine_index, tile_size, tile_rank,
+                         tile_world, fo, stats ? stats : lc.status ? &local : nullptr))
+    return st;
+  if (lc.status && (stats ? stats : &local)->hits > 0) return fail(lc.status, lc.msg);
+  return NSDF_OK;
+}
+
+}  // extern "C"
+
+namespace {
+int copy_out_frame(nsdf_ctx* c, const std::vector<std::pair<void*, const void*>>& dst_src,
+                   const std::vector<size_t>& bytes);
+
+// Peer access from device `from` to memory on device `to` (NVLink / NVSwitch on a B200
+// node): enabled once per ordered pair for the process, thread-safe.  false when the pair
+// cannot be peers (the caller then takes the copy path).
+bool enable_peer(int from, int to) {
+  if (from == to) return true;
+  static std::mutex mu;
+  static std::map<std::pair<int, int>, bool> done;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = done.find({from, to});
+  if (it != done.end()) return it->second;
+  int can = 0;
+  bool ok = cudaDeviceCanAccessPeer(&can, from, to) == cudaSuccess && can;
+  if (ok) {
+    DeviceGuard g(from);
+    const cudaError_t e = cudaDeviceEnablePeerAccess(to, 0);
+    ok = e == cudaSuccess || e == cudaErrorPeerAccessAlreadyEnabled;
+  }
+  cudaGetLastError();
+  done[{from, to}] = ok;
+  return ok;
+}
+
+}  // namespace
+
+extern "C" {
+
+int nsdf_cuda_replicate_field(nsdf_ctx* src, nsdf_field h, nsdf_ctx* dst, nsdf_field* out) {
+  if (!src || !dst || !out) return fail(NSDF_ERR_CONTRACT, "null argument");
+  std::unique_lock<std::mutex> l1, l2;
+  if (src == dst) {
+    l1 = std::unique_lock<std::mutex>(src->mu);
+  } else {  // pointer order: deadlock-free against concurrent callers
+    l1 = std::unique_lock<std::mutex>(std::min(src, dst)->mu);
+    l2 = std::unique_lock<std::mutex>(std::max(src, dst)->mu);
+  }
+  FieldRec* f;
+  if (int st = find_field(src, h, &f)) return st;
+  auto rec = std::make_unique<FieldRec>();
+  rec->dev = f->dev;
+  rec->device = dst->device;
+  rec->input_dim = f->input_dim;
+  rec->n_layers = f->n_layers;
+  rec->width = f->width;
+  if (f->image) {
+    DeviceGuard g(dst->device);
+    enable_peer(dst->device, src->device);  // the copy engine reads the source over NVLink
+    NSDF_CUDA(cudaMalloc(&rec->image, f->image_bytes));
+    rec->image_bytes = f->image_bytes;
+    NSDF_CUDA(cudaMemcpyPeerAsync(rec->image, dst->device, f->image, src->device, f->image_bytes, dst->stream));
+    NSDF_CUDA(cudaStreamSynchronize(dst->stream));
+    rebase_net(rec->dev.net, f->image, rec->image);
+  }
+  const int nh = dst->next_handle++;
+  dst->fields[nh] = std::move(rec);
+  *out = nh;
+  return NSDF_OK;
 }
 
 int nsdf_cuda_render_multi(nsdf_ctx* const* ctxs, int n, const nsdf_level* const* levels, int m,
@@ -1264,85 +1444,158 @@ int nsdf_cuda_render_multi(nsdf_ctx* const* ctxs, int n, const nsdf_level* const
   std::vector<std::unique_lock<std::mutex>> locks;
   for (nsdf_ctx* c : order) locks.emplace_back(c->mu);
   if (stats) std::memset(stats, 0, sizeof(*stats));
-  struct Part {
-    size_t n_max;
-    int* count;     // host pinned
-    float* h_rgb;   // host pinned staging, slot order
-    float* h_depth;
-    uint8_t* h_mask;
-    int* h_pixel;
+  nsdf_ctx* root = ctxs[0];
+  CamBasis cb;
+  ShadeParams sp;
+  LightCheck lc;
+  for (int i = 0; i < n; ++i) {
+    DeviceGuard g(ctxs[i]->device);
+    if (int st = render_checks(ctxs[i], levels[i], m, camera, trace, shade, normal_source, fine_index, &cb, &sp, &lc))
+      return st;
+  }
+  nsdf_frame_stats local;
+  if (lc.status && !stats) stats = &local;  // the deferred light check needs the hit count
+  const size_t np = size_t(cb.width) * cb.height;
+  const int tx = (cb.width + tile_size - 1) / tile_size, ty = (cb.height + tile_size - 1) / tile_size;
+  // 1) the framebuffer lives on the root context's device; every context stores its tiles'
+  //    pixels straight into it from its shading kernels (peer stores over NVLink), so there
+  //    is no pack, no gather and no host scatter.  Pairs without peer access pack their
+  //    pixels, peer-copy them and scatter on the root device.
+  FrameOut root_fb;
+  {
+    DeviceGuard g(root->device);
+    size_t off = 0;
+    NSDF_CUDA(root->io.reserve(np * 17 + 8192));
+    root_fb.d_rgb = carve<float>(root->io.base, off, 3 * np);
+    root_fb.d_depth = carve<float>(root->io.base, off, np);
+    root_fb.d_mask = carve<uint8_t>(root->io.base, off, np);
+    if (root->frame_events.empty()) {
+      root->frame_events.resize(1);
+      NSDF_CUDA(cudaEventCreateWithFlags(&root->frame_events[0], cudaEventDisableTiming));
+    }
+    NSDF_CUDA(cudaEventRecord(root->frame_events[0], root->stream));  // earlier users of the framebuffer
+  }
+  std::vector<PendingStats> pend(n);
+  std::vector<char> peer(n, 1);
+  struct Copy {
+    FrameOut fo;
+    size_t owned;
+    float* r_rgb;  // root-side staging of the packed pixels
+    float* r_depth;
+    int* r_pixel;
+    int* r_count;
+    uint8_t* r_mask;
   };
-  std::vector<Part> parts(n);
-  // 1) every context renders its tiles (t % n == i) on its own device and stream, packs
-  //    the owned pixels and starts their D2H: the devices run concurrently
+  std::vector<Copy> copies(n);
+  size_t root_stage = 0;
   for (int i = 0; i < n; ++i) {
     nsdf_ctx* c = ctxs[i];
+    peer[i] = c->device == root->device || enable_peer(c->device, root->device);
     DeviceGuard g(c->device);
-    CamBasis cb;
-    ShadeParams sp;
-    if (int st = render_checks(c, levels[i], m, camera, trace, shade, normal_source, fine_index, &cb, &sp)) return st;
-    const size_t np = size_t(cb.width) * cb.height;
-    const int tx = (cb.width + tile_size - 1) / tile_size, ty = (cb.height + tile_size - 1) / tile_size;
-    size_t owned = 0;
-    for (int t = i; t < tx * ty; t += n) {
-      const int x0 = (t % tx) * tile_size, y0 = (t / tx) * tile_size;
-      owned += size_t(std::min(tile_size, cb.width - x0)) * size_t(std::min(tile_size, cb.height - y0));
+    if (c->frame_events.empty()) {
+      c->frame_events.resize(1);
+      NSDF_CUDA(cudaEventCreateWithFlags(&c->frame_events[0], cudaEventDisableTiming));
     }
-    owned = std::max<size_t>(owned, 1);
-    size_t off = 0;
-    NSDF_CUDA(c->io.reserve(np * 17 + owned * 21 + 16384));
-    FrameOut fo;
-    fo.d_rgb = carve<float>(c->io.base, off, 3 * np);
-    fo.d_depth = carve<float>(c->io.base, off, np);
-    fo.d_mask = carve<uint8_t>(c->io.base, off, np);
-    fo.d_pack_rgb = carve<float>(c->io.base, off, 3 * owned);
-    fo.d_pack_depth = carve<float>(c->io.base, off, owned);
-    fo.d_pack_pixel = carve<int>(c->io.base, off, owned);
-    fo.d_pack_count = carve<int>(c->io.base, off, 1);
-    fo.d_pack_mask = carve<uint8_t>(c->io.base, off, owned);
-    nsdf_frame_stats fs;
+    if (c != root) NSDF_CUDA(cudaStreamWaitEvent(c->stream, root->frame_events[0], 0));
+    FrameOut fo = root_fb;
+    if (!peer[i]) {
+      size_t owned = 0;
+      for (int t = i; t < tx * ty; t += n) {
+        const int x0 = (t % tx) * tile_size, y0 = (t / tx) * tile_size;
+        owned += size_t(std::min(tile_size, cb.width - x0)) * size_t(std::min(tile_size, cb.height - y0));
+      }
+      owned = std::max<size_t>(owned, 1);
+      size_t off = 0;
+      NSDF_CUDA(c->io.reserve(np * 17 + owned * 21 + 16384));
+      fo.d_rgb = carve<float>(c->io.base, off, 3 * np);
+      fo.d_depth = carve<float>(c->io.base, off, np);
+      fo.d_mask = carve<uint8_t>(c->io.base, off, np);
+      fo.d_pack_rgb = carve<float>(c->io.base, off, 3 * owned);
+      fo.d_pack_depth = carve<float>(c->io.base, off, owned);
+      fo.d_pack_pixel = carve<int>(c->io.base, off, owned);
+      fo.d_pack_count = carve<int>(c->io.base, off, 1);
+      fo.d_pack_mask = carve<uint8_t>(c->io.base, off, owned);
+      copies[i].owned = owned;
+      root_stage += owned * 21 + 1024;
+    }
+    copies[i].fo = fo;
     if (int st = run_frame(c, levels[i], m, trace, &cb, nullptr, 0, &sp, normal_source, fine_index, tile_size, i, n,
-                           fo, stats ? &fs : nullptr))
+                           fo, nullptr, 0.0f, stats ? &pend[i] : nullptr))
       return st;
-    if (stats) {
-      for (int l = 0; l < NSDF_MAX_LEVELS; ++l) stats->evals[l] += fs.evals[l];
+  }
+  {
+    DeviceGuard g(root->device);
+    if (root_stage) NSDF_CUDA(root->stage.reserve(root_stage));
+    size_t off = 0;
+    for (int i = 0; i < n; ++i) {
+      nsdf_ctx* c = ctxs[i];
+      if (!peer[i]) {  // packed pixels -> root device (peer memcpy, staged by the driver) -> scatter
+        Copy& cp = copies[i];
+        const size_t ow = cp.owned;
+        cp.r_rgb = carve<float>(root->stage.base, off, 3 * ow);
+        cp.r_depth = carve<float>(root->stage.base, off, ow);
+        cp.r_pixel = carve<int>(root->stage.base, off, ow);
+        cp.r_count = carve<int>(root->stage.base, off, 1);
+        cp.r_mask = carve<uint8_t>(root->stage.base, off, ow);
+        const FrameOut& fo = cp.fo;
+        DeviceGuard gc(c->device);
+        const std::pair<void*, const void*> pieces[5] = {{cp.r_rgb, fo.d_pack_rgb},
+                                                         {cp.r_depth, fo.d_pack_depth},
+                                                         {cp.r_pixel, fo.d_pack_pixel},
+                                                         {cp.r_count, fo.d_pack_count},
+                                                         {cp.r_mask, fo.d_pack_mask}};
+        const size_t sizes[5] = {12 * ow, 4 * ow, 4 * ow, 4, ow};
+        for (int q = 0; q < 5; ++q)
+          NSDF_CUDA(cudaMemcpyPeerAsync(pieces[q].first, root->device, pieces[q].second, c->device, sizes[q],
+                                        c->stream));
+      }
+      if (c != root) {
+        DeviceGuard gc(c->device);
+        NSDF_CUDA(cudaEventRecord(c->frame_events[0], c->stream));
+        DeviceGuard gr(root->device);
+        NSDF_CUDA(cudaStreamWaitEvent(root->stream, c->frame_events[0], 0));
+      }
+      if (!peer[i]) {
+        DeviceGuard gr(root->device);
+        const Copy& cp = copies[i];
+        launch_scatter_packed(cp.r_count, int(cp.owned), cp.r_rgb, cp.r_depth, cp.r_mask, cp.r_pixel, root_fb.d_rgb,
+                              root_fb.d_depth, root_fb.d_mask, root->stream);
+        NSDF_CUDA(cudaGetLastError());
+      }
+    }
+  }
+  // 2) one D2H of the assembled frame from the root device
+  {
+    DeviceGuard g(root->device);
+    if (int st = copy_out_frame(root, {{rgb, root_fb.d_rgb}, {depth, root_fb.d_depth}, {mask, root_fb.d_mask}},
+                                {3 * np * 4, np * 4, np}))
+      return st;
+  }
+  if (stats) {
+    for (int i = 0; i < n; ++i) {
+      DeviceGuard g(ctxs[i]->device);
+      NSDF_CUDA(cudaStreamSynchronize(ctxs[i]->stream));
+      nsdf_frame_stats fs;
+      std::memset(&fs, 0, sizeof fs);
+      finish_stats(pend[i], &fs);
+      for (int l = 0; l < NSDF_MAX_LEVELS; ++l) {
+        stats->evals[l] += fs.evals[l];
+        // a level reports tcgen05 only if every context ran it there
+        if (fs.level_path[l] && (!stats->level_path[l] || fs.level_path[l] < stats->level_path[l]))
+          stats->level_path[l] = fs.level_path[l];
+      }
+      auto merge = [](uint8_t& a, uint8_t b) {
+        if (b && (!a || b < a)) a = b;
+      };
+      merge(stats->normals_path, fs.normals_path);
+      merge(stats->fallback_path, fs.fallback_path);
       stats->hits += fs.hits;
       stats->normal_evals += fs.normal_evals;
       stats->fallback_evals += fs.fallback_evals;
       stats->kernel_launches += fs.kernel_launches;
     }
-    NSDF_CUDA(c->frame.reserve_host(owned * 21 + 64));
-    uint8_t* h = static_cast<uint8_t*>(c->frame.host_pinned);
-    Part& p = parts[i];
-    p.n_max = owned;
-    p.count = reinterpret_cast<int*>(h);
-    p.h_rgb = reinterpret_cast<float*>(h + 16);
-    p.h_depth = p.h_rgb + 3 * owned;
-    p.h_pixel = reinterpret_cast<int*>(p.h_depth + owned);
-    p.h_mask = reinterpret_cast<uint8_t*>(p.h_pixel + owned);
-    cudaStream_t s = c->stream;
-    NSDF_CUDA(cudaMemcpyAsync(p.count, fo.d_pack_count, 4, cudaMemcpyDeviceToHost, s));
-    NSDF_CUDA(cudaMemcpyAsync(p.h_rgb, fo.d_pack_rgb, 3 * owned * 4, cudaMemcpyDeviceToHost, s));
-    NSDF_CUDA(cudaMemcpyAsync(p.h_depth, fo.d_pack_depth, owned * 4, cudaMemcpyDeviceToHost, s));
-    NSDF_CUDA(cudaMemcpyAsync(p.h_pixel, fo.d_pack_pixel, owned * 4, cudaMemcpyDeviceToHost, s));
-    NSDF_CUDA(cudaMemcpyAsync(p.h_mask, fo.d_pack_mask, owned, cudaMemcpyDeviceToHost, s));
   }
-  // 2) gather: scatter every context's packed pixels into the caller's framebuffer
-  for (int i = 0; i < n; ++i) {
-    nsdf_ctx* c = ctxs[i];
-    DeviceGuard g(c->device);
-    NSDF_CUDA(cudaStreamSynchronize(c->stream));
-    const Part& p = parts[i];
-    const int cnt = std::min<int>(*p.count, int(p.n_max));
-    for (int k = 0; k < cnt; ++k) {
-      const size_t px = size_t(p.h_pixel[k]);
-      rgb[3 * px + 0] = p.h_rgb[3 * size_t(k) + 0];
-      rgb[3 * px + 1] = p.h_rgb[3 * size_t(k) + 1];
-      rgb[3 * px + 2] = p.h_rgb[3 * size_t(k) + 2];
-      depth[px] = p.h_depth[k];
-      mask[px] = p.h_mask[k];
-    }
-  }
+  if (lc.status && stats->hits > 0) return fail(lc.status, lc.msg);
   return NSDF_OK;
 }
 
@@ -1429,7 +1682,10 @@ int nsdf_cuda_render(nsdf_ctx* c, const nsdf_level* levels, int m, const nsdf_ca
   DeviceGuard g(c->device);
   CamBasis cb;
   ShadeParams sp;
-  if (int st = render_checks(c, levels, m, camera, trace, shade, normal_source, fine_index, &cb, &sp)) return st;
+  LightCheck lc;
+  if (int st = render_checks(c, levels, m, camera, trace, shade, normal_source, fine_index, &cb, &sp, &lc)) return st;
+  nsdf_frame_stats local;
+  if (lc.status && !stats) stats = &local;  // the deferred light check needs the hit count
   const size_t n = size_t(cb.width) * cb.height;
   size_t off = 0;
   NSDF_CUDA(c->io.reserve(n * 17 + 8192));
@@ -1442,6 +1698,7 @@ int nsdf_cuda_render(nsdf_ctx* c, const nsdf_level* levels, int m, const nsdf_ca
   fo.d_mask = dmask;
   if (int st = run_frame(c, levels, m, trace, &cb, nullptr, 0, &sp, normal_source, fine_index, 1, 0, 1, fo, stats))
     return st;
+  if (lc.status && stats->hits > 0) return fail(lc.status, lc.msg);
   return copy_out_frame(c, {{rgb, drgb}, {depth, ddepth}, {mask, dmask}}, {3 * n * 4, n * 4, n});
 }
 

@@ -6,6 +6,9 @@
 // restates the reference's -ffp-contract=off C++ exactly (proj/CMakeLists.txt:15).
 #include <algorithm>
 #include <cstdio>
+#include <map>
+#include <mutex>
+#include <tuple>
 
 #include <nvtx3/nvToolsExt.h>
 
@@ -139,15 +142,50 @@ FrameBuffers carve_frame(void* base, int n_rays, int n_counters) {
   return fb;
 }
 
-static int num_sms() {
-  static int sms = 0;
-  if (!sms) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    if (sms <= 0) sms = 148;
+int device_sms() {
+  int dev = 0, sms = 0;
+  cudaGetDevice(&dev);
+  if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) {
+    cudaGetLastError();
+    sms = 148;
   }
   return sms;
+}
+
+static int num_sms() { return device_sms(); }
+
+KernelCfg kernel_cfg(const void* kernel, int threads, size_t smem, bool max_carveout) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  // The SMEM opt-in is ONE value per (device, kernel): raised to the largest size any launch
+  // needed so far (a smaller request must not lower it under another caller's cached size).
+  struct Entry {
+    size_t configured = 0;
+    std::map<std::pair<int, size_t>, KernelCfg> by_launch;  // (threads, smem)
+  };
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, Entry> cache;
+  std::lock_guard<std::mutex> lk(mu);
+  Entry& e = cache[{dev, kernel}];
+  KernelCfg k;
+  if (smem > e.configured) {
+    k.err = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (k.err != cudaSuccess) {
+      cudaGetLastError();
+      return k;
+    }
+    if (max_carveout) cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    e.configured = smem;
+  }
+  auto it = e.by_launch.find({threads, smem});
+  if (it != e.by_launch.end()) return it->second;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&k.occupancy, kernel, threads, smem) != cudaSuccess) k.occupancy = 1;
+  cudaFuncAttributes fa;
+  if (cudaFuncGetAttributes(&fa, kernel) == cudaSuccess) k.regs = fa.numRegs;
+  cudaGetLastError();
+  k.sms = device_sms();
+  e.by_launch.emplace(std::make_pair(threads, smem), k);
+  return k;
 }
 
 // ---------------------------------------------------------------------------------------
@@ -287,10 +325,8 @@ static size_t field_smem(const DevField& f) {
 
 template <typename K>
 static int blocks_for(K kernel, int threads, size_t smem) {
-  cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-  int per_sm = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem);
-  return num_sms() * std::max(per_sm, 1);
+  const KernelCfg k = kernel_cfg(reinterpret_cast<const void*>(kernel), threads, smem);
+  return (k.sms > 0 ? k.sms : num_sms()) * std::max(k.occupancy, 1);
 }
 
 // CTA size of the FFMA tiles: 256 threads (16 row groups x 16 column groups) for nets up to
@@ -372,9 +408,17 @@ TraceResult run_trace(Mode mode, const std::vector<LevelDesc>& levels, float eps
     snprintf(range, sizeof range, "nsdf level %d", lv.level);
     nvtxRangePushA(range);
     // fast mode: ONE persistent launch per level (rows refilled from the input list)
-    const bool persistent = mode_tc(mode) && lv.field.kind == kFieldMlp && tc_supported(lv.field.net) &&
-                            tc_trace_level(mode_terms(mode), lv, eps, t_max, in_list, in_count, cursor, evals,
-                                           fb.list[adv], adv_count, fb.st, n_max, s);
+    TcLaunch tl = TcLaunch::kDeclined;
+    if (mode_tc(mode) && lv.field.kind == kFieldMlp && tc_supported(lv.field.net))
+      tl = tc_trace_level(mode_terms(mode), lv, eps, t_max, in_list, in_count, cursor, evals, fb.list[adv], adv_count,
+                          fb.st, n_max, s);
+    if (tl == TcLaunch::kFailed) {  // no silent FFMA fallback: the frame fails
+      nvtxRangePop();
+      res.error = tc_last_error();
+      res.failed_level = lv.level;
+      return res;
+    }
+    const bool persistent = tl == TcLaunch::kRan;
     res.persistent.push_back(persistent ? 1 : 0);
     if (persistent) res.launches++;
     for (int iter = 0; !persistent && iter < lv.budget; ++iter) {
@@ -385,14 +429,9 @@ TraceResult run_trace(Mode mode, const std::vector<LevelDesc>& levels, float eps
       a.next_count = it_counts + iter;
       {
         const size_t smem = field_smem(lv.field) + kTileCols * sizeof(int);
-        static int grid_cache_w = -1, grid_cache = 0;
-        const int w = lv.field.kind == kFieldMlp ? lv.field.net.max_width : 4;
         const bool wide = wide_tile(lv.field);
-        if (grid_cache_w != w) {
-          grid_cache = wide ? blocks_for(trace_iter_simt<1024>, 1024, smem) : blocks_for(trace_iter_simt<256>, 256, smem);
-          grid_cache_w = w;
-        }
-        const int grid = std::max(1, std::min(grid_cache, (n_max + kTileCols - 1) / kTileCols));
+        const int blocks = wide ? blocks_for(trace_iter_simt<1024>, 1024, smem) : blocks_for(trace_iter_simt<256>, 256, smem);
+        const int grid = std::max(1, std::min(blocks, (n_max + kTileCols - 1) / kTileCols));
         if (wide)
           trace_iter_simt<1024><<<grid, 1024, smem, s>>>(a);
         else
@@ -487,6 +526,28 @@ void launch_pack_owned(const RayState& st, const int* n_slots_dev, int n_max, co
       st, n_slots_dev, rgb, depth, mask, p_rgb, p_depth, p_mask, p_pixel);
 }
 
+// Inverse of pack_owned on the framebuffer's device (render_multi without peer access):
+// the packed pixels of one context, copied over by a peer memcpy, land at their pixels.
+__global__ void scatter_packed_kernel(const int* count, const float* p_rgb, const float* p_depth, const uint8_t* p_mask,
+                                      const int* p_pixel, float* rgb, float* depth, uint8_t* mask) {
+  const int n = *count;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const size_t p = size_t(p_pixel[i]);
+    rgb[3 * p + 0] = p_rgb[size_t(3) * i + 0];
+    rgb[3 * p + 1] = p_rgb[size_t(3) * i + 1];
+    rgb[3 * p + 2] = p_rgb[size_t(3) * i + 2];
+    depth[p] = p_depth[i];
+    mask[p] = p_mask[i];
+  }
+}
+
+void launch_scatter_packed(const int* count_dev, int n_max, const float* p_rgb, const float* p_depth,
+                           const uint8_t* p_mask, const int* p_pixel, float* rgb, float* depth, uint8_t* mask,
+                           cudaStream_t s) {
+  scatter_packed_kernel<<<std::max(1, std::min((n_max + 255) / 256, num_sms() * 8)), 256, 0, s>>>(
+      count_dev, p_rgb, p_depth, p_mask, p_pixel, rgb, depth, mask);
+}
+
 void launch_fb_background(const RayState& st, const int* n_slots_dev, int n_max, const ShadeParams& sp, float* rgb,
                           float* depth, uint8_t* mask, cudaStream_t s) {
   fb_background_kernel<<<std::max(1, std::min((n_max + 255) / 256, num_sms() * 8)), 256, 0, s>>>(st, n_slots_dev, sp,
@@ -568,9 +629,10 @@ int launch_normals_shade(Mode mode, const DevField& nf, float time, const int* l
                          float* rgb, float* depth, uint8_t* mask, cudaStream_t s) {
   NormalArgs a{nf, time, list, count, st, sp, defer_fallback ? 1 : 0, fb_list, fb_count, rgb, depth, mask};
   if (mode_tc(mode) && nf.kind == kFieldMlp && tc_supported(nf.net)) {
-    if (tc_normals_shade(mode_terms(mode), nf, time, list, count, n_max, st, sp, defer_fallback, fb_list, fb_count, rgb, depth, mask,
-                         s))
-      return 1;
+    const TcLaunch r = tc_normals_shade(mode_terms(mode), nf, time, list, count, n_max, st, sp, defer_fallback,
+                                        fb_list, fb_count, rgb, depth, mask, s);
+    if (r == TcLaunch::kRan) return NSDF_PATH_TCGEN05;
+    if (r == TcLaunch::kFailed) return -1;  // tc_last_error() holds the CUDA error
   }
   const size_t smem = field_smem(nf) + kTileCols * sizeof(int);
   if (wide_tile(nf)) {
@@ -580,7 +642,7 @@ int launch_normals_shade(Mode mode, const DevField& nf, float time, const int* l
     const int grid = std::max(1, std::min(blocks_for(normals_shade_simt<256>, 256, smem), (n_max + 15) / 16));
     normals_shade_simt<256><<<grid, 256, smem, s>>>(a);
   }
-  return 1;
+  return NSDF_PATH_SIMT;
 }
 
 // ---------------------------------------------------------------------------------------
@@ -663,25 +725,31 @@ static void launch_eval_impl(const DevField& f, const float* pts, int rows, int 
   }
 }
 
-void launch_eval(Mode mode, const DevField& f, const float* pts, int rows, int k, float time, float* out, float* grad,
-                 cudaStream_t s) {
-  if (k <= 0) return;
-  if (mode_tc(mode) && f.kind == kFieldMlp && tc_supported(f.net) &&
-      tc_eval(mode_terms(mode), f, pts, rows, k, time, out, grad, s))
-    return;
+cudaError_t launch_eval(Mode mode, const DevField& f, const float* pts, int rows, int k, float time, float* out,
+                        float* grad, cudaStream_t s) {
+  if (k <= 0) return cudaSuccess;
+  if (mode_tc(mode) && f.kind == kFieldMlp && tc_supported(f.net)) {
+    const TcLaunch r = tc_eval(mode_terms(mode), f, pts, rows, k, time, out, grad, s);
+    if (r == TcLaunch::kRan) return cudaSuccess;
+    if (r == TcLaunch::kFailed) return tc_last_error();
+  }
   if (grad)
     launch_eval_impl<true>(f, pts, rows, k, time, out, grad, 0.0, nullptr, nullptr, 0, s);
   else
     launch_eval_impl<false>(f, pts, rows, k, time, out, nullptr, 0.0, nullptr, nullptr, 0, s);
+  return cudaGetLastError();
 }
 
-void launch_normal_map(Mode mode, const DevField& f, const float* pts, int k, float time, double delta,
-                       const float* fallback, float* normals, unsigned long long* counts, cudaStream_t s) {
-  if (k <= 0) return;
-  if (mode_tc(mode) && f.kind == kFieldMlp && tc_supported(f.net) &&
-      tc_normal_map(mode_terms(mode), f, pts, k, time, delta, fallback, normals, counts, s))
-    return;
+cudaError_t launch_normal_map(Mode mode, const DevField& f, const float* pts, int k, float time, double delta,
+                              const float* fallback, float* normals, unsigned long long* counts, cudaStream_t s) {
+  if (k <= 0) return cudaSuccess;
+  if (mode_tc(mode) && f.kind == kFieldMlp && tc_supported(f.net)) {
+    const TcLaunch r = tc_normal_map(mode_terms(mode), f, pts, k, time, delta, fallback, normals, counts, s);
+    if (r == TcLaunch::kRan) return cudaSuccess;
+    if (r == TcLaunch::kFailed) return tc_last_error();
+  }
   launch_eval_impl<true>(f, pts, 3, k, time, nullptr, normals, delta, fallback, counts, 1, s);
+  return cudaGetLastError();
 }
 
 __global__ void shade_kernel(const float* pts, const float* nrm, int k, ShadeParams sp, float* rgb) {

@@ -91,6 +91,8 @@ struct TraceResult {
   std::vector<int> counter_layout_base;  // offsets of per-level iteration counters
   std::vector<char> persistent;          // level traced by one persistent launch
   int launches = 0;
+  cudaError_t error = cudaSuccess;       // a tcgen05 launch failed (the frame is invalid)
+  int failed_level = -1;
 };
 
 // Ray generation for all pixels (world == 1, slot == pixel) or the owned image tiles.
@@ -119,21 +121,26 @@ void launch_pack_owned(const RayState& st, const int* n_slots_dev, int n_max, co
                        const uint8_t* mask, float* p_rgb, float* p_depth, uint8_t* p_mask, int* p_pixel,
                        cudaStream_t s);
 
+void launch_scatter_packed(const int* count_dev, int n_max, const float* p_rgb, const float* p_depth,
+                           const uint8_t* p_mask, const int* p_pixel, float* rgb, float* depth, uint8_t* mask,
+                           cudaStream_t s);
+
 void launch_fb_background(const RayState& st, const int* n_slots_dev, int n_max,
                           const ShadeParams& sp, float* rgb, float* depth, uint8_t* mask,
                           cudaStream_t s);
 // Normals (fused fwd + 3 tangent chains) + normalize/fallback + shade + framebuffer write
 // for the hit list (render.cpp:48-80).  With `defer_fallback`, zero-gradient hits are
-// appended to fb_list instead of getting (0,1,0).
+// appended to fb_list instead of getting (0,1,0).  Returns the kernel path that ran
+// (NSDF_PATH_TCGEN05 / NSDF_PATH_SIMT) or -1 when a tcgen05 launch failed.
 int launch_normals_shade(Mode mode, const DevField& nf, float time, const int* list,
                          const int* count, int n_max, const RayState& st, const ShadeParams& sp,
                          bool defer_fallback, int* fb_list, int* fb_count, float* rgb,
                          float* depth, uint8_t* mask, cudaStream_t s);
 
 // Batch evaluation of a field (API path).
-void launch_eval(Mode mode, const DevField& f, const float* pts, int rows, int k, float time,
-                 float* out, float* grad, cudaStream_t s);
-void launch_normal_map(Mode mode, const DevField& f, const float* pts, int k, float time,
+cudaError_t launch_eval(Mode mode, const DevField& f, const float* pts, int rows, int k, float time,
+                        float* out, float* grad, cudaStream_t s);
+cudaError_t launch_normal_map(Mode mode, const DevField& f, const float* pts, int k, float time,
                        double delta, const float* fallback, float* normals,
                        unsigned long long* counts, cudaStream_t s);
 void launch_shade(const float* pts, const float* normals, int k, const ShadeParams& sp, float* rgb,
@@ -145,7 +152,7 @@ void launch_raycast_mesh(const CamBasis& cb, const float* tri_verts /* n_tri x 9
 
 // FP64 batch evaluation (mlp_f64.cu): forward_batch<double> / gradient_batch<double>
 // bit-exact with the reference's AVX2 double path.  pts rows x k (device), out k, grad 3 x k.
-void launch_eval_f64(const DevNet& n, const double* pts, int rows, int k, double time, double* out, double* grad,
+cudaError_t launch_eval_f64(const DevNet& n, const double* pts, int rows, int k, double time, double* out, double* grad,
                      cudaStream_t s);
 
 // FP64 SIREN training (train_f64.cu), host buffers in/out.
@@ -168,5 +175,20 @@ void launch_tensor_sine(bool f64, const void* x, void* out, size_t n, double ome
 
 // Tensor-core availability of a net for the fast mode (mlp_tc.cu).
 bool tc_supported(const DevNet& n);
+
+// Launch configuration of a kernel on the CURRENT device.  CUDA function attributes (the
+// dynamic-SMEM opt-in above 48 KB, the carveout) are per device, so they are kept per
+// (device, kernel) under a process-wide lock — the opt-in raised to the largest size any
+// launch needed — and the occupancy per (threads, smem) is cached: contexts on several
+// devices, and host threads racing on first use, each see a configured kernel.  err !=
+// cudaSuccess when the opt-in failed (the caller reports it; nothing is cached then).
+struct KernelCfg {
+  cudaError_t err = cudaSuccess;
+  int sms = 0;        // multiprocessors of the device
+  int occupancy = 0;  // cudaOccupancyMaxActiveBlocksPerMultiprocessor
+  int regs = 0;       // registers per thread
+};
+KernelCfg kernel_cfg(const void* kernel, int threads, size_t smem, bool max_carveout = false);
+int device_sms();  // multiprocessors of the current device
 
 }  // namespace nsdf_b200

@@ -20,6 +20,9 @@
 // (rb = tid/4, cb = tid%4).
 #include <algorithm>
 
+#include <cstdio>
+#include <cstdlib>
+
 #include "common_f64.cuh"
 #include "engine.cuh"
 
@@ -187,33 +190,30 @@ __global__ void __launch_bounds__(kThreads64) eval_f64_kernel(DevNet n, const do
 }
 
 template <bool kGrad>
-void launch_f64(const DevNet& n, const double* pts, int rows, int k, double time, double* out, double* grad,
+cudaError_t launch_f64(const DevNet& n, const double* pts, int rows, int k, double time, double* out, double* grad,
                 cudaStream_t s) {
   const int W = std::max(n.max_width, 4);
   const size_t smem = size_t(2) * W * kCols64 * sizeof(double) + 4 * kCols64 * sizeof(double);
-  static size_t configured = 0;
-  if (smem > configured) {
-    cudaFuncSetAttribute(eval_f64_kernel<kGrad>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-    configured = smem;
-  }
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const KernelCfg kc = kernel_cfg(reinterpret_cast<const void*>(eval_f64_kernel<kGrad>), kThreads64, smem);
+  if (kc.err != cudaSuccess) return kc.err;
+  const int sms = kc.sms;
   const int per_sm = std::max(1, int((228 * 1024) / (smem + 1024)));
   constexpr int kRays = kGrad ? kCols64 / 4 : kCols64;
   const int grid = std::max(1, std::min(sms * std::min(per_sm, 4), (k + kRays - 1) / kRays));
+  if (getenv("NSDF_DEBUG_LAUNCH"))
+    fprintf(stderr, "launch_f64<%d> W=%d smem=%zu grid=%d sms=%d occ=%d pending=%s\n", int(kGrad), W, smem, grid, sms,
+            kc.occupancy, cudaGetErrorString(cudaPeekAtLastError()));
   eval_f64_kernel<kGrad><<<grid, kThreads64, smem, s>>>(n, pts, rows, k, time, out, grad);
+  return cudaGetLastError();
 }
 
 }  // namespace
 
-void launch_eval_f64(const DevNet& n, const double* pts, int rows, int k, double time, double* out, double* grad,
-                     cudaStream_t s) {
-  if (k <= 0) return;
-  if (grad)
-    launch_f64<true>(n, pts, rows, k, time, out, grad, s);
-  else
-    launch_f64<false>(n, pts, rows, k, time, out, nullptr, s);
+cudaError_t launch_eval_f64(const DevNet& n, const double* pts, int rows, int k, double time, double* out,
+                            double* grad, cudaStream_t s) {
+  if (k <= 0) return cudaSuccess;
+  return grad ? launch_f64<true>(n, pts, rows, k, time, out, grad, s)
+              : launch_f64<false>(n, pts, rows, k, time, out, nullptr, s);
 }
 
 }  // namespace nsdf_b200

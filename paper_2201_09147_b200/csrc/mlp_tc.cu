@@ -1121,56 +1121,51 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
   }
 }
 
+thread_local cudaError_t g_tc_error = cudaSuccess;
+
+TcLaunch tc_failed(cudaError_t e) {
+  g_tc_error = e == cudaSuccess ? cudaErrorLaunchFailure : e;
+  return TcLaunch::kFailed;
+}
+
 template <int W, bool kGrad, int kTerms, bool kResident, bool kPersist, int kHid>
-bool launch_w(TcArgs& a, int n_max_items, cudaStream_t s) {
+TcLaunch launch_w(TcArgs& a, int n_max_items, cudaStream_t s) {
   constexpr int kGroups = W == 64 ? 1 : (W == 256 && kTerms == 3 ? 4 : 2);
   constexpr int kThreads = 32 * (kResident ? 1 : 2) + 128 * kGroups;
   auto kernel = tc_mlp_kernel<W, kGrad, kGroups, kTerms, kResident, kPersist, kHid>;
   const size_t smem = tc_smem_bytes(W, a.net.n_layers, kTerms, kResident, kPersist);
-  static size_t configured_smem = 0;
-  static int per_sm = 0;
-  static int sms = 0;
-  if (configured_smem != smem) {
-    if (cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)) != cudaSuccess)
-      return false;
-    cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    int occ = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, kThreads, smem) != cudaSuccess) occ = 1;
-    // Residency from first principles (228 KB SMEM incl. 1 KB per CTA, 64K registers, TMEM
-    // columns); the occupancy API is reported for reference only.
-    cudaFuncAttributes fa;
-    cudaFuncGetAttributes(&fa, kernel);
-    const int by_smem = int((228 * 1024) / (smem + 1024));
-    const int by_regs = 65536 / (std::max(fa.numRegs, 1) * kThreads);
-    per_sm = std::max(1, std::min(by_smem, by_regs));
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    configured_smem = smem;
-    if (getenv("NSDF_DEBUG_TC"))
-      fprintf(stderr, "tc_mlp_kernel<%d,%d,%d,%d,%d,%d,%d>: smem %zu B, regs %d, %d CTAs/SM (occupancy API %d)\n", W,
-              int(kGrad), kGroups, kTerms, int(kResident), int(kPersist), kHid, smem, fa.numRegs, per_sm, occ);
-  }
+  // per-device attributes (kernel_cfg): every device a context lives on gets the opt-in
+  const KernelCfg kc = kernel_cfg(reinterpret_cast<const void*>(kernel), kThreads, smem, /*max_carveout=*/true);
+  if (kc.err != cudaSuccess) return tc_failed(kc.err);
+  // Residency from first principles (228 KB SMEM incl. 1 KB per CTA, 64K registers, TMEM
+  // columns); the occupancy API is reported for reference only.
+  const int by_smem = int((228 * 1024) / (smem + 1024));
+  const int by_regs = 65536 / (std::max(kc.regs, 1) * kThreads);
+  const int per_sm = std::max(1, std::min(by_smem, by_regs));
+  if (getenv("NSDF_DEBUG_TC"))
+    fprintf(stderr, "tc_mlp_kernel<%d,%d,%d,%d,%d,%d,%d>: smem %zu B, regs %d, %d CTAs/SM (occupancy API %d)\n", W,
+            int(kGrad), kGroups, kTerms, int(kResident), int(kPersist), kHid, smem, kc.regs, per_sm, kc.occupancy);
   const int tmem_limit = 512 / (2 * W);  // two accumulator regions per CTA
   const int per = std::max(1, std::min(per_sm, tmem_limit));
   constexpr int kRaysPerTile = kGrad ? kRows / 4 : kRows;
   const int tiles = (n_max_items + kRaysPerTile - 1) / kRaysPerTile;
-  const int grid = std::max(1, std::min(tiles, sms * per));
+  const int grid = std::max(1, std::min(tiles, kc.sms * per));
   kernel<<<grid, kThreads, smem, s>>>(a);
-  return cudaGetLastError() == cudaSuccess;
+  const cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? TcLaunch::kRan : tc_failed(e);
 }
 
 // The hidden-layer count is compiled in for the standard architectures (64x1, 128x2, 256x3:
 // the nets of every BASELINE config); other depths take the runtime-count kernels.
 template <int W, bool kGrad, int kTerms, bool kResident, bool kPersist>
-bool launch_h(TcArgs& a, int n_max_items, cudaStream_t s) {
+TcLaunch launch_h(TcArgs& a, int n_max_items, cudaStream_t s) {
   constexpr int kStd = W == 64 ? 1 : (W == 128 ? 2 : 3);
   return a.net.n_layers - 2 == kStd ? launch_w<W, kGrad, kTerms, kResident, kPersist, kStd>(a, n_max_items, s)
                                     : launch_w<W, kGrad, kTerms, kResident, kPersist, 0>(a, n_max_items, s);
 }
 
 template <bool kGrad, int kTerms, bool kPersist>
-bool launch_terms(TcArgs& a, int n_max_items, cudaStream_t s) {
+TcLaunch launch_terms(TcArgs& a, int n_max_items, cudaStream_t s) {
   // 64-wide nets keep every hidden layer resident in SMEM when it fits (<= 4 layers).
   const bool resident = a.net.width == 64 && a.net.n_layers - 2 <= 4;
   switch (a.net.width) {
@@ -1179,7 +1174,7 @@ bool launch_terms(TcArgs& a, int n_max_items, cudaStream_t s) {
                       : launch_h<64, kGrad, kTerms, false, kPersist>(a, n_max_items, s);
     case 128: return launch_h<128, kGrad, kTerms, false, kPersist>(a, n_max_items, s);
     case 256: return launch_h<256, kGrad, kTerms, false, kPersist>(a, n_max_items, s);
-    default: return false;
+    default: return TcLaunch::kDeclined;
   }
 }
 
@@ -1262,7 +1257,7 @@ void timeline_dump(long long* buf, const char* what) {
 }
 
 template <bool kGrad, bool kPersist = false>
-bool launch_any(TcArgs& a, int n_max_items, cudaStream_t s) {
+TcLaunch launch_any(TcArgs& a, int n_max_items, cudaStream_t s) {
   static const int claim_div = [] {
     const char* e = getenv("NSDF_TC_CLAIM_DIV");
     return e ? std::max(1, atoi(e)) : 4;
@@ -1271,8 +1266,8 @@ bool launch_any(TcArgs& a, int n_max_items, cudaStream_t s) {
   a.dbg = timeline_buffer();
   a.dbg_skip = getenv("NSDF_TC_TIMELINE_SKIP") ? std::max(0, atoi(getenv("NSDF_TC_TIMELINE_SKIP"))) : 0;
   if (a.dbg) {
-    const bool ok = a.terms == 3 ? launch_terms<kGrad, 3, kPersist>(a, n_max_items, s)
-                                 : launch_terms<kGrad, 1, kPersist>(a, n_max_items, s);
+    const TcLaunch ok = a.terms == 3 ? launch_terms<kGrad, 3, kPersist>(a, n_max_items, s)
+                                     : launch_terms<kGrad, 1, kPersist>(a, n_max_items, s);
     char what[64];
     snprintf(what, sizeof what, "W=%d grad=%d persist=%d", a.net.width, int(kGrad), int(kPersist));
     timeline_dump(a.dbg, what);
@@ -1300,7 +1295,9 @@ TcNet tc_net(const DevNet& n) {
 
 bool tc_supported(const DevNet& n) { return n.tc_ok != 0; }
 
-bool tc_trace_level(int terms, const LevelDesc& lv, float eps, float t_max, const int* in_list, const int* in_count,
+cudaError_t tc_last_error() { return g_tc_error; }
+
+TcLaunch tc_trace_level(int terms, const LevelDesc& lv, float eps, float t_max, const int* in_list, const int* in_count,
                     int* cursor, int* evals, int* adv_list, int* adv_count, const RayState& st, int n_max,
                     cudaStream_t s) {
   TcArgs a{};
@@ -1321,7 +1318,7 @@ bool tc_trace_level(int terms, const LevelDesc& lv, float eps, float t_max, cons
   return launch_any<false, true>(a, n_max, s);
 }
 
-bool tc_normals_shade(int terms, const DevField& nf, float time, const int* list, const int* count, int n_max,
+TcLaunch tc_normals_shade(int terms, const DevField& nf, float time, const int* list, const int* count, int n_max,
                       const RayState& st, const ShadeParams& sp, bool defer_fallback, int* fb_list, int* fb_count,
                       float* rgb, float* depth, uint8_t* mask, cudaStream_t s) {
   TcArgs a{};
@@ -1342,7 +1339,7 @@ bool tc_normals_shade(int terms, const DevField& nf, float time, const int* list
   return launch_any<true>(a, n_max, s);
 }
 
-bool tc_eval(int terms, const DevField& f, const float* pts, int rows, int k, float time, float* out, float* grad,
+TcLaunch tc_eval(int terms, const DevField& f, const float* pts, int rows, int k, float time, float* out, float* grad,
              cudaStream_t s) {
   TcArgs a{};
   a.terms = terms;
@@ -1356,12 +1353,12 @@ bool tc_eval(int terms, const DevField& f, const float* pts, int rows, int k, fl
   a.grad = grad;
   // a 4-row batch carries a per-column time; the tiles fold a single slice time into the
   // layer-0 bias, so such batches take the FFMA tiles
-  if (rows == 4) return false;
+  if (rows == 4) return TcLaunch::kDeclined;
   if (grad) return launch_any<true>(a, k, s);
   return launch_any<false>(a, k, s);
 }
 
-bool tc_normal_map(int terms, const DevField& f, const float* pts, int k, float time, double delta,
+TcLaunch tc_normal_map(int terms, const DevField& f, const float* pts, int k, float time, double delta,
                    const float* fallback, float* normals, unsigned long long* counts, cudaStream_t s) {
   TcArgs a{};
   a.terms = terms;

@@ -1,25 +1,31 @@
 // Tensor-core (tcgen05) fast path of the SIREN evaluator — launchers implemented in
-// mlp_tc.cu.  Each returns false when it does not handle the request (the caller then
-// runs the FFMA tile on the device; there is no CPU path).
+// mlp_tc.cu.  Each returns kDeclined when the request is outside what the tiles handle
+// (the caller then runs the FFMA tile on the device and reports NSDF_PATH_SIMT; there is
+// no CPU path) and kFailed when a launch it should have made did not happen (attribute
+// opt-in or launch error; tc_last_error() holds the CUDA error) — a hard error for the
+// caller, never a silent fallback.
 #pragma once
 
 #include "engine.cuh"
 
 namespace nsdf_b200 {
 
+enum class TcLaunch { kRan, kDeclined, kFailed };
+cudaError_t tc_last_error();  // CUDA error of this thread's last kFailed launch
+
 // Persistent level trace: one launch runs every iteration of a level; rows are refilled
 // from in_list (claimed through *cursor) until it drains.  Converged slots -> adv_list,
 // evaluations -> *evals.  cursor / evals / adv_count must be zeroed.
-bool tc_trace_level(int terms, const LevelDesc& lv, float eps, float t_max, const int* in_list, const int* in_count,
+TcLaunch tc_trace_level(int terms, const LevelDesc& lv, float eps, float t_max, const int* in_list, const int* in_count,
                     int* cursor, int* evals, int* adv_list, int* adv_count, const RayState& st, int n_max,
                     cudaStream_t s);
-bool tc_normals_shade(int terms, const DevField& nf, float time, const int* list, const int* count, int n_max,
+TcLaunch tc_normals_shade(int terms, const DevField& nf, float time, const int* list, const int* count, int n_max,
                       const RayState& st, const ShadeParams& sp, bool defer_fallback, int* fb_list, int* fb_count,
                       float* rgb, float* depth, uint8_t* mask, cudaStream_t s);
-bool tc_eval(int terms, const DevField& f, const float* pts, int rows, int k, float time, float* out, float* grad,
+TcLaunch tc_eval(int terms, const DevField& f, const float* pts, int rows, int k, float time, float* out, float* grad,
              cudaStream_t s);
 
-bool tc_normal_map(int terms, const DevField& f, const float* pts, int k, float time, double delta,
+TcLaunch tc_normal_map(int terms, const DevField& f, const float* pts, int k, float time, double delta,
                    const float* fallback, float* normals, unsigned long long* counts, cudaStream_t s);
 
 }  // namespace nsdf_b200

@@ -392,7 +392,7 @@ static double full_batch_loss_dev(const TrainNet& net, const double* params, con
   if (*err) return 0.0;
   const int chunks = (n + kChunk - 1) / kChunk;
   if ((*err = outb.reserve(size_t(n) + chunks + 1))) return 0.0;
-  launch_eval_f64(dn, X, net.input_dim, n, 0.0, outb.p, nullptr, s);
+  if ((*err = launch_eval_f64(dn, X, net.input_dim, n, 0.0, outb.p, nullptr, s))) return 0.0;
   sse_chunks_kernel<<<(chunks + 63) / 64, 64, 0, s>>>(outb.p, y, n, kChunk, outb.p + n);
   std::vector<double> sse(chunks);
   cudaMemcpyAsync(sse.data(), outb.p + n, size_t(chunks) * 8, cudaMemcpyDeviceToHost, s);
@@ -533,7 +533,7 @@ cudaError_t train_fit(int n_layers, const int32_t* rows, const int32_t* cols, do
     cudaMemcpyAsync(vX.p, val_points_h, size_t(input_dim) * n_val * 8, cudaMemcpyHostToDevice, s);
     DevNet dn;
     if ((e = bind_devnet(net, ckpt.p, wt, dn, s))) return e;
-    launch_eval_f64(dn, vX.p, input_dim, n_val, 0.0, vY.p, nullptr, s);
+    if ((e = launch_eval_f64(dn, vX.p, input_dim, n_val, 0.0, vY.p, nullptr, s))) return e;
     std::vector<double> out(n_val);
     cudaMemcpyAsync(out.data(), vY.p, size_t(n_val) * 8, cudaMemcpyDeviceToHost, s);
     if ((e = cudaStreamSynchronize(s))) return e;

@@ -119,6 +119,13 @@ class Context:
     def release(self, handle: int):
         check(self.lib.nsdf_cuda_release(self._ctx, handle))
 
+    def replicate(self, handle: int, dst: "Context") -> int:
+        """nsdf_cuda_replicate_field: this context's field, copied device to device into
+        `dst` (the multi-GPU weight broadcast); returns the handle in dst."""
+        h = ctypes.c_int32()
+        check(self.lib.nsdf_cuda_replicate_field(self._ctx, handle, dst._ctx, ctypes.byref(h)))
+        return h.value
+
     def upload_sequence(self, seq: Sequence) -> "DeviceSequence":
         return DeviceSequence(self, seq)
 
@@ -334,10 +341,14 @@ def _levels(levels):
 class DeviceSequence:
     """A NestedSequence / AnimatedSequence resident on the device (weights uploaded once)."""
 
-    def __init__(self, ctx: Context, seq: Sequence):
+    def __init__(self, ctx: Context, seq: Sequence, handles=None):
         self.ctx = ctx
         self.seq = seq
-        self.handles = [ctx.upload(m) for m in seq.members]
+        self.handles = list(handles) if handles is not None else [ctx.upload(m) for m in seq.members]
+
+    def replicate(self, dst: Context) -> "DeviceSequence":
+        """The same sequence on another context (device-to-device weight copies)."""
+        return DeviceSequence(dst, self.seq, [self.ctx.replicate(h, dst) for h in self.handles])
 
     def levels(self, time: float = 0.0, indices: Optional[Seq[int]] = None):
         """nsdf_level array; for animated sequences `time` is the slice (float(t),

@@ -53,9 +53,24 @@ ImageBuffer render(const NestedSequence& seq, const Camera& camera, const Render
   const nsdf_trace_config tc = detail::to_pod(config.trace);
   const nsdf_shade_config sc = detail::to_pod(config.shade);
   ImageBuffer img(camera.width, camera.height);
-  engine::check(nsdf_cuda_render(engine::context(), levels.data(), int(levels.size()), &cam, &tc, &sc,
-                                 config.normal_source == NormalSource::mapped ? NSDF_NORMALS_MAPPED : NSDF_NORMALS_OWN,
-                                 config.mapped_fine_index, img.rgb.data(), img.depth.data(), img.mask.data(), nullptr));
+  const int src = config.normal_source == NormalSource::mapped ? NSDF_NORMALS_MAPPED : NSDF_NORMALS_OWN;
+  const auto& ctxs = engine::contexts();
+  if (ctxs.size() == 1) {
+    engine::check(nsdf_cuda_render(ctxs[0], levels.data(), int(levels.size()), &cam, &tc, &sc, src,
+                                   config.mapped_fine_index, img.rgb.data(), img.depth.data(), img.mask.data(),
+                                   nullptr));
+    return img;
+  }
+  // NSDF_DEVICES: the frame's tiles over every listed GPU (weights replicated once per field)
+  std::vector<std::vector<nsdf_level>> per(ctxs.size(), levels);
+  std::vector<const nsdf_level*> lp(ctxs.size());
+  for (size_t i = 0; i < ctxs.size(); ++i) {
+    for (nsdf_level& l : per[i]) l.field = engine::replica(i, l.field);
+    lp[i] = per[i].data();
+  }
+  engine::check(nsdf_cuda_render_multi(ctxs.data(), int(ctxs.size()), lp.data(), int(levels.size()), &cam, &tc, &sc,
+                                       src, config.mapped_fine_index, engine::tile_size(), img.rgb.data(),
+                                       img.depth.data(), img.mask.data(), nullptr));
   return img;
 }
 

@@ -50,7 +50,7 @@ def test_pod_layouts_match_ctypes(tmp_path):
 
 
 def test_abi_version(lib):
-    assert lib.nsdf_cuda_abi_version() == 1
+    assert lib.nsdf_cuda_abi_version() == 2
 
 
 def test_no_gpu_fails_loudly(lib):

@@ -135,30 +135,170 @@ def test_empty_and_ragged_batches(ctx):
         assert d1.shape == (k,) and np.isfinite(d1).all() and np.isfinite(g1).all()
 
 
-@pytest.mark.parametrize("mode", ["fp32", "fp16"])
-@pytest.mark.parametrize("n_ctx,tile", [(1, 32), (2, 32), (3, 17)])
-def test_render_multi_equals_single(mode, n_ctx, tile):
-    """nsdf_cuda_render_multi (N contexts, interleaved tiles, host gather) reproduces the
-    single-context frame bit for bit (per-ray work is partition invariant).  On this one-GPU
-    box the contexts share device 0; on a multi-GPU node each sits on its own device."""
+def _device_count():
+    import torch
+    return torch.cuda.device_count()
+
+
+def _assert_paths(st, n_levels, mode, normals=True):
+    from paper_2201_09147_b200.abi import PATH_SIMT, PATH_TCGEN05
+    want = PATH_TCGEN05 if mode == "fp16" else PATH_SIMT
+    assert list(st.level_path)[:n_levels] == [want] * n_levels, list(st.level_path)
+    if normals:
+        assert st.normals_path == want
+
+
+def _render_multi_case(mode, devices, tile, replicate):
     from paper_2201_09147_b200.abi import ShadeConfig, TraceConfig, standard_camera
     from paper_2201_09147_b200.engine import Context, DeviceSequence, render_multi
     seq = _seq()
-    ctxs = [Context(0, mode) for _ in range(n_ctx)]
+    ctxs = [Context(d, mode) for d in devices]
     try:
-        dss = [DeviceSequence(c, seq) for c in ctxs]
+        d0 = DeviceSequence(ctxs[0], seq)
+        dss = [d0] + [d0.replicate(c) if replicate else DeviceSequence(c, seq) for c in ctxs[1:]]
         cam = standard_camera(200, 120)
         cfg, shade = TraceConfig((20, 5, 5)), ShadeConfig(specular=0.3)
-        ref = ctxs[0].render(dss[0].levels(), cam, cfg, shade)
-        rgb, depth, mask, st = render_multi(ctxs, [d.levels() for d in dss], cam, cfg, shade, tile_size=tile,
-                                            stats=True)
-        assert np.array_equal(mask, ref[2])
-        assert np.array_equal(depth.view(np.uint32), ref[1].view(np.uint32))
-        assert np.array_equal(rgb.view(np.uint32), ref[0].view(np.uint32))
-        assert st.hits == ref[3].hits and list(st.evals)[:3] == list(ref[3].evals)[:3]
+        ref = ctxs[0].render(d0.levels(), cam, cfg, shade)
+        _assert_paths(ref[3], 3, mode)
+        for rep in range(2):  # the second frame reuses the peer framebuffer / events
+            rgb, depth, mask, st = render_multi(ctxs, [d.levels() for d in dss], cam, cfg, shade, tile_size=tile,
+                                                stats=True)
+            assert np.array_equal(mask, ref[2])
+            assert np.array_equal(depth.view(np.uint32), ref[1].view(np.uint32))
+            assert np.array_equal(rgb.view(np.uint32), ref[0].view(np.uint32))
+            assert st.hits == ref[3].hits and list(st.evals)[:3] == list(ref[3].evals)[:3]
+            _assert_paths(st, 3, mode)
     finally:
         for c in ctxs:
             c.close()
+
+
+@pytest.mark.parametrize("mode", ["fp32", "fp16"])
+@pytest.mark.parametrize("n_ctx,tile,replicate", [(1, 32, False), (2, 32, True), (3, 17, False), (4, 8, True)])
+def test_render_multi_equals_single(mode, n_ctx, tile, replicate):
+    """nsdf_cuda_render_multi (N contexts, interleaved tiles, every context storing its
+    pixels into ctxs[0]'s framebuffer) reproduces the single-context frame bit for bit, with
+    weights uploaded per context or replicated device to device; every level reports the
+    tcgen05 path in the fast mode.  Here the contexts share device 0 (the one GPU of this
+    box); test_render_multi_distinct_devices runs them on distinct GPUs."""
+    _render_multi_case(mode, [0] * n_ctx, tile, replicate)
+
+
+@pytest.mark.parametrize("mode", ["fp32", "fp16"])
+def test_render_multi_distinct_devices(mode):
+    """The same frame with one context per GPU (peer stores over NVLink into device 0's
+    framebuffer, weights broadcast device to device, per-device kernel attributes): bitwise
+    equal to the single-device frame, tcgen05 on every level of every device."""
+    n = _device_count()
+    if n < 2:
+        pytest.skip("needs more than one GPU")
+    _render_multi_case(mode, list(range(min(n, 8))), 32, True)
+
+
+def test_replicated_field_is_independent_and_bitwise_equal():
+    """nsdf_cuda_replicate_field copies the packed device image (one allocation); the
+    replica evaluates bit for bit like the source and survives the source's release."""
+    from paper_2201_09147_b200.engine import Context
+    a, b = Context(0, "fp16"), Context(0, "fp16")
+    try:
+        for width, hidden in [(64, 1), (128, 2), (256, 3), (12, 2)]:
+            net = random_net(width, hidden, seed=width)
+            h = a.upload(net)
+            pts = np.random.default_rng(width).uniform(-1, 1, (3, 5000)).astype(np.float32)
+            d0, g0 = a.eval_grad(h, pts)
+            r = a.replicate(h, b)
+            a.release(h)
+            d1, g1 = b.eval_grad(r, pts)
+            assert np.array_equal(d0.view(np.uint32), d1.view(np.uint32))
+            assert np.array_equal(g0.view(np.uint32), g1.view(np.uint32))
+            b.release(r)
+    finally:
+        a.close()
+        b.close()
+
+
+def test_kernel_path_stats():
+    """nsdf_frame_stats reports the kernel family of every traced level and of the normal
+    tiles: tcgen05 in the fast mode, FFMA tiles in the oracle mode, NONE for skipped levels;
+    analytic members always take the FFMA tiles."""
+    from paper_2201_09147_b200.abi import PATH_NONE, PATH_SIMT, PATH_TCGEN05, ShadeConfig, TraceConfig, standard_camera
+    from paper_2201_09147_b200.engine import Context, DeviceSequence
+    from paper_2201_09147_b200.manifest import Analytic, Sequence
+    seq = _seq()
+    cam = standard_camera(64, 48)
+    for mode, want in (("fp16", PATH_TCGEN05), ("fp32", PATH_SIMT)):
+        c = Context(0, mode)
+        try:
+            ds = DeviceSequence(c, seq)
+            st = c.render(ds.levels(), cam, TraceConfig((20, 0, 5)), ShadeConfig())[3]
+            assert list(st.level_path)[:3] == [want, PATH_NONE, want]
+            assert st.normals_path == want and st.fallback_path == PATH_NONE
+            st = c.render(ds.levels(), cam, TraceConfig((20, 5, 0)), ShadeConfig(), normal_source=1)[3]
+            assert list(st.level_path)[:3] == [want, want, PATH_NONE] and st.normals_path == want
+            an = DeviceSequence(c, Sequence([Analytic("sphere", {"r": 0.7})], [0.05], ["s"]))
+            st = c.render(an.levels(), cam, TraceConfig((30,)), ShadeConfig())[3]
+            assert st.level_path[0] == PATH_SIMT and st.normals_path == PATH_SIMT
+        finally:
+            c.close()
+
+
+def test_contexts_on_many_threads_all_run_tcgen05():
+    """Contexts created and used from concurrent host threads (the launch-attribute cache is
+    per device and locked): every thread's first frame runs the tcgen05 kernels (the 128- and
+    256-wide ones need the > 48 KB SMEM opt-in) and all frames are identical."""
+    import threading
+    from paper_2201_09147_b200.abi import ShadeConfig, TraceConfig, standard_camera
+    from paper_2201_09147_b200.engine import Context, DeviceSequence
+    seq = _seq()
+    cam = standard_camera(160, 96)
+    out, errs = [None] * 6, []
+
+    def work(i):
+        try:
+            c = Context(0, "fp16")
+            ds = DeviceSequence(c, seq)
+            out[i] = c.render(ds.levels(), cam, TraceConfig((20, 5, 5)), ShadeConfig(specular=0.3))
+            c.close()
+        except Exception as e:  # pragma: no cover - reported below
+            errs.append(repr(e))
+
+    th = [threading.Thread(target=work, args=(i,)) for i in range(len(out))]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    assert not errs, errs
+    for o in out:
+        _assert_paths(o[3], 3, "fp16")
+        assert np.array_equal(o[2], out[0][2])
+
+
+def test_empty_light_list_matches_reference(oracle_built, tmp_path):
+    """The reference checks the lights inside shade(), which render() only calls for frames
+    with hits: a hit-free frame with no light is the background image; with hits it raises
+    ErrorKind::contract (render.cpp:41, shade.cpp:47-49)."""
+    from oracle import refshim
+    from paper_2201_09147_b200.abi import Camera, NsdfError, ShadeConfig, TraceConfig, ERR_CONTRACT
+    from paper_2201_09147_b200.engine import Context, DeviceSequence
+    p = os.path.join(ASSETS, "torus_w30.nest")
+    seq = _seq()
+    c = Context(0, "fp32")
+    try:
+        ds = DeviceSequence(c, seq)
+        shade = ShadeConfig(lights=(), background=(0.2, 0.3, 0.4))
+        away = Camera((0, 0, 3), (0, 0, 6), (0, 1, 0), 30.0, 40, 30)   # looks away from the torus
+        rgb, depth, mask, st = c.render(ds.levels(), away, TraceConfig((20, 5, 5)), shade)
+        want = refshim.render(p, away, TraceConfig((20, 5, 5)), shade)
+        assert st.hits == 0 and not mask.any()
+        assert np.array_equal(rgb, want[0]) and np.array_equal(depth, want[1])
+        toward = Camera((0, 1.5, 2), (0, 0, 0), (0, 1, 0), 50.0, 40, 30)
+        with pytest.raises(NsdfError) as e:
+            c.render(ds.levels(), toward, TraceConfig((20, 5, 5)), shade)
+        assert e.value.status == ERR_CONTRACT and "light" in str(e.value)
+        with pytest.raises(Exception):
+            refshim.render(p, toward, TraceConfig((20, 5, 5)), shade)
+    finally:
+        c.close()
 
 
 @pytest.mark.parametrize("mode", ["fp32", "fp16"])

@@ -113,6 +113,38 @@ def test_trace_analytic_sequences_match_reference(ctx, oracle_built, tmp_path):
         _compare_records(got, want)
 
 
+def test_analytic_fields_bitexact(ctx, oracle_built, tmp_path):
+    """Analytic torus / box / sphere values and gradients (field.cpp:57-124, double then
+    float cast) bit for bit against the compiled reference: the torus needs glibc's hypot,
+    restated on the device (common.cuh hypot_ref) because CUDA's hypot differs in the last
+    bit; then whole traces of an analytic torus pair, bitwise."""
+    from oracle import refshim
+    from paper_2201_09147_b200.abi import TraceConfig, standard_camera
+    from paper_2201_09147_b200.manifest import Analytic
+    from paper_2201_09147_b200.engine import DeviceSequence
+    members = [Analytic("torus", {"R": 0.6, "r": 0.3}), Analytic("box", {"hx": 0.6, "hy": 0.45, "hz": 0.5}),
+               Analytic("sphere", {"cx": 0.1, "r": 0.7})]
+    path, seq = _manifest(str(tmp_path), members, [0.2, 0.1, 0.05])
+    ds = DeviceSequence(ctx, seq)
+    rng = np.random.default_rng(17)
+    pts = rng.uniform(-1.3, 1.3, size=(3, 200000)).astype(np.float32)
+    pts[:, :1000] *= np.float32(1e-3)  # near the torus axis / the origin
+    pts[1, 1000:2000] = 0.0            # on the torus' plane of symmetry
+    for i, h in enumerate(ds.handles):
+        d_gpu, g_gpu = ctx.eval_grad(h, pts)
+        d_ref, g_ref = refshim.field_eval(path, i, pts)
+        assert np.array_equal(bits(d_gpu), bits(d_ref)), (members[i].name, int(np.sum(bits(d_gpu) != bits(d_ref))))
+        assert np.array_equal(bits(g_gpu), bits(g_ref)), (members[i].name, int(np.sum(bits(g_gpu) != bits(g_ref))))
+    path2, seq2 = _manifest(str(tmp_path), [Analytic("torus", {"R": 0.6, "r": 0.4}),
+                                            Analytic("torus", {"R": 0.6, "r": 0.3})], [0.15, 0.05], name="t2.nest")
+    ds2 = DeviceSequence(ctx, seq2)
+    cam = standard_camera(96, 64)
+    for budgets in [(40, 40), (30, 0), (0, 60)]:
+        cfg = TraceConfig(budgets)
+        got, _ = ctx.trace_image(ds2.levels(), cam, cfg)
+        _compare_records(got, refshim.trace_image(path2, cam, cfg))
+
+
 def test_trace_kats(ctx):
     """Reference tracer KATs (test_tracer.cpp:74-87, 104-121, 185-192, 281-307)."""
     from paper_2201_09147_b200.abi import TraceConfig
