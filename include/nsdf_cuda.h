@@ -25,6 +25,7 @@
  *   nsdf_cuda_sphere_trace    tracer::sphere_trace                      src/tracer/trace.cpp:136-160
  *   nsdf_cuda_trace_image     tracer::trace_image                       src/tracer/trace.cpp:171-186
  *   nsdf_cuda_normal_map      shading::neural_normal_map                src/shading/shade.cpp:8-42
+ *   nsdf_cuda_map_normals_to_mesh shading::map_normals_to_mesh          src/shading/mesh.cpp:122-156
  *   nsdf_cuda_shade           shading::shade                            src/shading/shade.cpp:44-93
  *   nsdf_cuda_render          shading::render                           src/shading/render.cpp:12-82
  *   nsdf_cuda_render_device   shading::render, device-resident framebuffer + tile sharding
@@ -326,6 +327,13 @@ int nsdf_cuda_trace_image(nsdf_ctx* ctx, const nsdf_level* levels, int m,
 int nsdf_cuda_normal_map(nsdf_ctx* ctx, nsdf_field fine, float time, const float* points, int k,
                          double delta, const float* fallback_normals, float* normals,
                          uint64_t* outside_count, uint64_t* fallback_count);
+/* shading::map_normals_to_mesh (mesh.cpp:122-156) on the device: vertices k x 3 doubles (the
+ * Mesh::vertices Vec3 array), normals k x 3 doubles — in: the normals kept for violators and
+ * zero-gradient vertices (the mesh's own, or zeros), out: g/|g| (double) for mapped
+ * vertices; counts = {mapped, violators, fallbacks}.  The caller replaces the mesh normals
+ * only if mapped > 0, as the reference does.  Synchronous. */
+int nsdf_cuda_map_normals_to_mesh(nsdf_ctx* ctx, nsdf_field fine, float time, const double* vertices,
+                                  int k, double delta, double* normals, uint64_t* counts);
 /* Device-pointer variant (async): points/normals/fallback 3 x k, counts = 2 x u64
  * {outside, fallback} accumulated (zero them first).  Used for mesh G-buffers. */
 int nsdf_cuda_normal_map_device(nsdf_ctx* ctx, nsdf_field fine, float time, const float* d_points,

@@ -324,6 +324,33 @@ int nsdf_ref_normal_map(const char* manifest, double time, int index, const floa
   SHIM_CATCH
 }
 
+// shading::map_normals_to_mesh (mesh.cpp:122-156) on a Mesh built from k x 3 double
+// vertices and (has_normals) k x 3 double normals; normals_out receives mesh.normals after
+// the call (k x 3, or untouched when the mesh ends without normals); counts {mapped,
+// violators, fallbacks}; *out_has = whether the mesh has normals afterwards.
+int nsdf_ref_map_normals_mesh(const char* manifest, double time, int index, const double* verts, int k,
+                              const double* normals_in, int has_normals, double delta, double* normals_out,
+                              uint64_t* counts, int* out_has) {
+  SHIM_TRY
+  auto seq = load_sequence(manifest, time);
+  shading::Mesh mesh;
+  for (int j = 0; j < k; ++j) mesh.vertices.push_back({verts[3 * j], verts[3 * j + 1], verts[3 * j + 2]});
+  if (has_normals)
+    for (int j = 0; j < k; ++j)
+      mesh.normals.push_back({normals_in[3 * j], normals_in[3 * j + 1], normals_in[3 * j + 2]});
+  auto r = shading::map_normals_to_mesh(mesh, seq.field(index), delta);
+  counts[0] = r.mapped;
+  counts[1] = r.violators;
+  counts[2] = r.fallbacks;
+  *out_has = mesh.has_normals() ? 1 : 0;
+  for (size_t j = 0; j < mesh.normals.size(); ++j) {
+    normals_out[3 * j] = mesh.normals[j].x;
+    normals_out[3 * j + 1] = mesh.normals[j].y;
+    normals_out[3 * j + 2] = mesh.normals[j].z;
+  }
+  SHIM_CATCH
+}
+
 int nsdf_ref_shade(const float* pts, const float* normals, int k, const nsdf_shade_config* shade,
                    const nsdf_camera* camera, float* rgb) {
   SHIM_TRY

@@ -222,6 +222,22 @@ def normal_map(manifest, index, points, delta, fallback=None, time=0.0):
     return nrm, o.value, f.value
 
 
+def map_normals_to_mesh(manifest, index, vertices, delta, normals=None, time=0.0):
+    """shading::map_normals_to_mesh; returns (normals k x 3 or None, (mapped, violators,
+    fallbacks))."""
+    lib = load()
+    v = np.ascontiguousarray(vertices, np.float64)
+    k = v.shape[0]
+    nin = None if normals is None else np.ascontiguousarray(normals, np.float64)
+    out = np.zeros((k, 3), np.float64)
+    counts = (U64 * 3)()
+    has = ctypes.c_int(0)
+    _check(lib, lib.nsdf_ref_map_normals_mesh(manifest.encode(), D(time), index, _p(v, D), k,
+                                              None if nin is None else _p(nin, D), 0 if nin is None else 1,
+                                              D(delta), _p(out, D), counts, ctypes.byref(has)))
+    return (out if has.value else None), tuple(int(c) for c in counts)
+
+
 def shade(points, normals, cfg: ShadeConfig, cam: Camera):
     lib = load()
     pts = np.ascontiguousarray(points, np.float32)

@@ -1211,6 +1211,36 @@ int nsdf_cuda_trace_image(nsdf_ctx* c, const nsdf_level* levels, int m, const ns
   return NSDF_OK;
 }
 
+int nsdf_cuda_map_normals_to_mesh(nsdf_ctx* c, nsdf_field fine, float time, const double* vertices, int k,
+                                  double delta, double* normals, uint64_t* counts) {
+  if (!c) return fail(NSDF_ERR_CONTRACT, "context is null");
+  if (k <= 0 || !vertices) return fail(NSDF_ERR_CONTRACT, "mesh has no vertices");
+  if (!normals || !counts) return fail(NSDF_ERR_CONTRACT, "null argument");
+  std::lock_guard<std::mutex> lk(c->mu);
+  DeviceGuard g(c->device);
+  FieldRec* f;
+  if (int st = find_field(c, fine, &f)) return st;
+  size_t off = 0;
+  NSDF_CUDA(c->io.reserve(size_t(k) * (24 + 24 + 12 + 4 + 12) + 8192));
+  double* dv = carve<double>(c->io.base, off, size_t(3) * k);
+  double* dn = carve<double>(c->io.base, off, size_t(3) * k);
+  float* dp = carve<float>(c->io.base, off, size_t(3) * k);
+  float* dval = carve<float>(c->io.base, off, size_t(k));
+  float* dg = carve<float>(c->io.base, off, size_t(3) * k);
+  unsigned long long* dc = carve<unsigned long long>(c->io.base, off, 3);
+  cudaStream_t s = c->stream;
+  NSDF_CUDA(cudaMemcpyAsync(dv, vertices, size_t(k) * 24, cudaMemcpyHostToDevice, s));
+  NSDF_CUDA(cudaMemcpyAsync(dn, normals, size_t(k) * 24, cudaMemcpyHostToDevice, s));
+  NSDF_CUDA(cudaMemsetAsync(dc, 0, 24, s));
+  NSDF_CUDA(launch_map_mesh_normals(mode_of(c), f->dev, time, dv, k, delta, dp, dval, dg, dn, dc, s));
+  unsigned long long hc[3];
+  NSDF_CUDA(cudaMemcpyAsync(hc, dc, 24, cudaMemcpyDeviceToHost, s));
+  NSDF_CUDA(cudaMemcpyAsync(normals, dn, size_t(k) * 24, cudaMemcpyDeviceToHost, s));
+  NSDF_CUDA(cudaStreamSynchronize(s));
+  for (int i = 0; i < 3; ++i) counts[i] = hc[i];
+  return NSDF_OK;
+}
+
 int nsdf_cuda_normal_map(nsdf_ctx* c, nsdf_field fine, float time, const float* points, int k, double delta,
                          const float* fallback_normals, float* normals, uint64_t* outside_count,
                          uint64_t* fallback_count) {

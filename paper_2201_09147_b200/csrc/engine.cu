@@ -752,6 +752,57 @@ cudaError_t launch_normal_map(Mode mode, const DevField& f, const float* pts, in
   return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------------------------------
+// Per-vertex mesh normal mapping (shading::map_normals_to_mesh, mesh.cpp:122-156): the
+// vertices (double) cast to float points, the fine field's value + gradient by the batch
+// kernels, then this gate: |value| > delta -> violator (normal kept); |g| < 1e-8 (double
+// norm of the float gradient) -> fallback (kept); else normal = g / |g| in double
+// (Vec3::norm / operator/, separately rounded).
+// ---------------------------------------------------------------------------------------
+__global__ void cast_vertices_kernel(const double* v, int k, float* pts) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < k; j += gridDim.x * blockDim.x) {
+    pts[j] = __double2float_rn(v[3 * size_t(j) + 0]);
+    pts[size_t(k) + j] = __double2float_rn(v[3 * size_t(j) + 1]);
+    pts[2 * size_t(k) + j] = __double2float_rn(v[3 * size_t(j) + 2]);
+  }
+}
+
+__global__ void mesh_map_kernel(const float* vals, const float* grads, int k, double delta, double* normals,
+                                unsigned long long* counts) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < k; j += gridDim.x * blockDim.x) {
+    int what = 0;  // 0 mapped, 1 violator, 2 fallback
+    if (fabs(double(vals[j])) > delta) {
+      what = 1;
+    } else {
+      const double gx = grads[j], gy = grads[size_t(k) + j], gz = grads[2 * size_t(k) + j];
+      const double n = __dsqrt_rn(__dadd_rn(__dadd_rn(__dmul_rn(gx, gx), __dmul_rn(gy, gy)), __dmul_rn(gz, gz)));
+      if (n < 1e-8) {
+        what = 2;
+      } else {
+        normals[3 * size_t(j) + 0] = __ddiv_rn(gx, n);
+        normals[3 * size_t(j) + 1] = __ddiv_rn(gy, n);
+        normals[3 * size_t(j) + 2] = __ddiv_rn(gz, n);
+      }
+    }
+    const unsigned lanes = __activemask();
+    for (int w = 0; w < 3; ++w) {
+      const unsigned m = __ballot_sync(lanes, what == w);
+      if (m && (threadIdx.x & 31) == __ffs(lanes) - 1) atomicAdd(counts + w, (unsigned long long)__popc(m));
+    }
+  }
+}
+
+cudaError_t launch_map_mesh_normals(Mode mode, const DevField& f, float time, const double* vertices, int k,
+                                    double delta, float* pts, float* vals, float* grads, double* normals,
+                                    unsigned long long* counts, cudaStream_t s) {
+  if (k <= 0) return cudaSuccess;
+  const int grid = std::max(1, std::min((k + 255) / 256, num_sms() * 8));
+  cast_vertices_kernel<<<grid, 256, 0, s>>>(vertices, k, pts);
+  if (cudaError_t e = launch_eval(mode, f, pts, 3, k, time, vals, grads, s)) return e;
+  mesh_map_kernel<<<grid, 256, 0, s>>>(vals, grads, k, delta, normals, counts);
+  return cudaGetLastError();
+}
+
 __global__ void shade_kernel(const float* pts, const float* nrm, int k, ShadeParams sp, float* rgb) {
   for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < k; j += gridDim.x * blockDim.x) {
     float c[3];

@@ -143,6 +143,12 @@ cudaError_t launch_eval(Mode mode, const DevField& f, const float* pts, int rows
 cudaError_t launch_normal_map(Mode mode, const DevField& f, const float* pts, int k, float time,
                        double delta, const float* fallback, float* normals,
                        unsigned long long* counts, cudaStream_t s);
+// shading::map_normals_to_mesh on the device: vertices k x 3 double (Vec3 array), normals
+// k x 3 double (pre-filled with the kept normals), counts {mapped, violators, fallbacks};
+// pts / vals / grads are 3k / k / 3k float scratch.
+cudaError_t launch_map_mesh_normals(Mode mode, const DevField& f, float time, const double* vertices, int k,
+                                    double delta, float* pts, float* vals, float* grads, double* normals,
+                                    unsigned long long* counts, cudaStream_t s);
 void launch_shade(const float* pts, const float* normals, int k, const ShadeParams& sp, float* rgb,
                   cudaStream_t s);
 

@@ -251,6 +251,21 @@ class Context:
                                             _fp(nrm), ctypes.byref(o), ctypes.byref(f)))
         return nrm, o.value, f.value
 
+    def map_normals_to_mesh(self, handle, vertices, delta, normals=None, time=0.0):
+        """nsdf_cuda_map_normals_to_mesh (shading::map_normals_to_mesh, mesh.cpp:122-156):
+        returns (normals k x 3 float64 or None when nothing was mapped and the mesh had none,
+        (mapped, violators, fallbacks))."""
+        v = np.ascontiguousarray(vertices, np.float64)
+        k = v.shape[0]
+        out = np.zeros((k, 3), np.float64) if normals is None else np.array(normals, np.float64, order="C")
+        counts = (ctypes.c_uint64 * 3)()
+        check(self.lib.nsdf_cuda_map_normals_to_mesh(self._ctx, handle, ctypes.c_float(time), v.ctypes.data_as(_D), k,
+                                                     ctypes.c_double(delta), out.ctypes.data_as(_D), counts))
+        c = tuple(int(x) for x in counts)
+        if c[0] == 0:  # the reference replaces the mesh normals only if some vertex was mapped
+            out = None if normals is None else np.asarray(normals, np.float64)
+        return out, c
+
     def normal_map_device(self, handle, d_points: int, k: int, delta: float, d_normals: int, d_counts: int,
                           d_fallback: int = 0, time: float = 0.0):
         check(self.lib.nsdf_cuda_normal_map_device(self._ctx, handle, ctypes.c_float(time), ctypes.c_void_p(d_points),

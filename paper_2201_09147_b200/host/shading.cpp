@@ -74,11 +74,31 @@ ImageBuffer render(const NestedSequence& seq, const Camera& camera, const Render
   return img;
 }
 
-// Per-vertex normal mapping (reference mesh.cpp:122-156): device eval + gradient, host
-// delta gate and double-precision normalisation.
+// Per-vertex normal mapping (reference mesh.cpp:122-156).  Fields with a device binding run
+// entirely on the GPU (nsdf_cuda_map_normals_to_mesh: float cast, value + gradient tiles, the
+// delta gate and the double normalisation in one device pass); other fields evaluate through
+// their own eval_batch / grad_batch with the same gate on the host.
 MeshMapReport map_normals_to_mesh(Mesh& mesh, const Field& fine, double delta) {
   if (mesh.vertices.empty()) throw Error(ErrorKind::contract, "mesh has no vertices");
   const int k = int(mesh.vertices.size());
+  if (mesh.has_normals() && mesh.normals.size() != mesh.vertices.size())
+    throw Error(ErrorKind::validation, "mesh has " + std::to_string(mesh.normals.size()) + " normals for " +
+                                           std::to_string(mesh.vertices.size()) + " vertices");
+  static_assert(sizeof(Vec3) == 3 * sizeof(double), "Vec3 must be three packed doubles");
+  fields::DeviceBinding b;
+  if (fine.device_binding(b)) {
+    std::vector<Vec3> updated = mesh.has_normals() ? mesh.normals : std::vector<Vec3>(mesh.vertices.size());
+    uint64_t counts[3] = {0, 0, 0};
+    engine::check(nsdf_cuda_map_normals_to_mesh(engine::context(), b.handle, b.time,
+                                                reinterpret_cast<const double*>(mesh.vertices.data()), k, delta,
+                                                reinterpret_cast<double*>(updated.data()), counts));
+    MeshMapReport rep;
+    rep.mapped = counts[0];
+    rep.violators = counts[1];
+    rep.fallbacks = counts[2];
+    if (rep.mapped > 0) mesh.normals = std::move(updated);
+    return rep;
+  }
   Matrix<float> pts(3, k);
   for (int j = 0; j < k; ++j) {
     pts(0, j) = float(mesh.vertices[j].x);

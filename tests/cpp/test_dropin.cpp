@@ -2,8 +2,11 @@
 // Cases follow the reference's own suites (proj/tests/test_mlp.cpp, test_tracer.cpp,
 // test_shading.cpp); file:line of the originals is given per case.  Run with
 // NSDF_MODE=oracle for the bit-exact assertions.
+#include <algorithm>
+#include <array>
 #include <cstdlib>
 #include <filesystem>
+#include <map>
 
 #include "check.hpp"
 #include "nsdf/shading/shading.hpp"
@@ -237,6 +240,66 @@ TEST_CASE("self-mapped normals reproduce the own-normal render exactly (test_sha
   shading::RenderConfig mapped = own;
   mapped.normal_source = shading::NormalSource::mapped;
   CHECK(shading::image_mse(shading::render(seq, cam, own), shading::render(seq, cam, mapped)) == 0.0);
+}
+
+// The reference test suite's icosphere builder (test_shading.cpp:74-112), restated.
+shading::Mesh test_icosphere(int subdivisions, double radius) {
+  const double phi = (1.0 + std::sqrt(5.0)) / 2.0;
+  std::vector<Vec3> v = {{-1, phi, 0}, {1, phi, 0}, {-1, -phi, 0}, {1, -phi, 0}, {0, -1, phi}, {0, 1, phi},
+                         {0, -1, -phi}, {0, 1, -phi}, {phi, 0, -1}, {phi, 0, 1}, {-phi, 0, -1}, {-phi, 0, 1}};
+  for (auto& x : v) x = x.normalized();
+  std::vector<std::array<int, 3>> f = {{0, 11, 5}, {0, 5, 1},  {0, 1, 7},   {0, 7, 10}, {0, 10, 11},
+                                       {1, 5, 9},  {5, 11, 4}, {11, 10, 2}, {10, 7, 6}, {7, 1, 8},
+                                       {3, 9, 4},  {3, 4, 2},  {3, 2, 6},   {3, 6, 8},  {3, 8, 9},
+                                       {4, 9, 5},  {2, 4, 11}, {6, 2, 10},  {8, 6, 7},  {9, 8, 1}};
+  for (int s = 0; s < subdivisions; ++s) {
+    std::map<std::pair<int, int>, int> memo;
+    auto mid = [&](int a, int b) {
+      const auto key = std::minmax(a, b);
+      auto it = memo.find(key);
+      if (it != memo.end()) return it->second;
+      v.push_back(((v[a] + v[b]) * 0.5).normalized());
+      return memo[key] = int(v.size()) - 1;
+    };
+    std::vector<std::array<int, 3>> next;
+    for (const auto& t : f) {
+      const int a = mid(t[0], t[1]), b = mid(t[1], t[2]), c = mid(t[2], t[0]);
+      next.push_back({t[0], a, c});
+      next.push_back({t[1], b, a});
+      next.push_back({t[2], c, b});
+      next.push_back({a, b, c});
+    }
+    f = std::move(next);
+  }
+  shading::Mesh m;
+  m.triangles = f;
+  for (const auto& x : v) {
+    m.normals.push_back(x);
+    m.vertices.push_back(x * radius);
+  }
+  return m;
+}
+
+TEST_CASE("mesh normal mapping on the device (test_shading.cpp:215-261)") {
+  auto mesh = test_icosphere(2, 1.0);
+  SphereField sphere({0, 0, 0}, 1.0);
+  auto rep = shading::map_normals_to_mesh(mesh, sphere, 0.05);
+  CHECK(rep.violators == 0 && rep.mapped == mesh.vertices.size());
+  for (size_t i = 0; i < mesh.vertices.size(); ++i) CHECK((mesh.normals[i] - mesh.vertices[i].normalized()).norm() < 1e-6);
+  auto small = test_icosphere(1, 1.0);
+  const auto original = small.normals;
+  fields::TorusField far_torus(0.2, 0.05);
+  rep = shading::map_normals_to_mesh(small, far_torus, 0.01);
+  CHECK(rep.mapped == 0 && rep.violators == small.vertices.size());
+  for (size_t i = 0; i < original.size(); ++i) CHECK((small.normals[i] - original[i]).norm() == 0);
+  auto a = test_icosphere(2, 1.02), b = test_icosphere(2, 1.02);
+  std::reverse(b.triangles.begin(), b.triangles.end());
+  shading::map_normals_to_mesh(a, sphere, 0.1);
+  shading::map_normals_to_mesh(b, sphere, 0.1);
+  for (size_t i = 0; i < a.normals.size(); ++i)
+    CHECK(a.normals[i].x == b.normals[i].x && a.normals[i].y == b.normals[i].y && a.normals[i].z == b.normals[i].z);
+  shading::Mesh empty;
+  CHECK_THROWS(shading::map_normals_to_mesh(empty, sphere, 0.1));
 }
 
 TEST_CASE("manifest + sdfnet round trip and image / mesh I/O") {
