@@ -24,6 +24,11 @@ int nsdf_host_trace_image_manifest(const char* manifest, double time, const nsdf
 int nsdf_host_forward_and_gradient(const char* sdfnet, const float* points, int k, float* dist,
                                    float* grad);
 
+/* Framebuffer output (shading::write_ppm / write_png / read_ppm, image.cpp:32-120): the
+ * format follows the path's extension (.png, else binary PPM); rgb is 3 x W x H floats. */
+int nsdf_host_write_image(const char* path, int width, int height, const float* rgb);
+int nsdf_host_read_ppm(const char* path, int* width, int* height, float* rgb, size_t capacity);
+
 /* Certification (fields::sample_near_surface / estimate_sup_diff / verify_nesting,
  * nesting.cpp:131-361) through the drop-in library; neural fields evaluate on the device
  * FP64 path.  A field source is "weights:<file.sdfnet>" or an analytic spec

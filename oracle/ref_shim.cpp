@@ -8,6 +8,7 @@
 
 #include <chrono>
 #include <cstring>
+#include <filesystem>
 #include <memory>
 #include <string>
 #include <vector>
@@ -348,6 +349,18 @@ int nsdf_ref_map_normals_mesh(const char* manifest, double time, int index, cons
     normals_out[3 * j + 1] = mesh.normals[j].y;
     normals_out[3 * j + 2] = mesh.normals[j].z;
   }
+  SHIM_CATCH
+}
+
+int nsdf_ref_write_image(const char* path, int width, int height, const float* rgb) {
+  SHIM_TRY
+  shading::ImageBuffer img(width, height);
+  std::memcpy(img.rgb.data(), rgb, sizeof(float) * img.rgb.size());
+  const std::filesystem::path p(path);
+  if (p.extension() == ".png")
+    shading::write_png(img, p);
+  else
+    shading::write_ppm(img, p);
   SHIM_CATCH
 }
 

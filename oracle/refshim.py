@@ -238,6 +238,37 @@ def map_normals_to_mesh(manifest, index, vertices, delta, normals=None, time=0.0
     return (out if has.value else None), tuple(int(c) for c in counts)
 
 
+_WRITE_IMAGE = r'''
+import array, ctypes, sys
+lib = ctypes.CDLL(sys.argv[1])
+w, h = int(sys.argv[4]), int(sys.argv[5])
+px = array.array("f")
+with open(sys.argv[3], "rb") as f:
+    px.frombytes(f.read())
+buf = (ctypes.c_float * len(px)).from_buffer(px)
+sys.exit(lib.nsdf_ref_write_image(sys.argv[2].encode(), w, h, buf))
+'''
+
+
+def write_image(path_, rgb_hw3):
+    """shading::write_ppm / write_png by extension.  Runs in a child interpreter that never
+    imports numpy: with numpy's bundled runtime libraries loaded, the reference library's
+    std::ofstream crashes in this process (a libstdc++ symbol clash, test-side only)."""
+    import subprocess
+    import sys
+    import tempfile
+    rgb = np.ascontiguousarray(rgb_hw3, np.float32)
+    with tempfile.NamedTemporaryFile(suffix=".f32", delete=False) as fh:
+        fh.write(rgb.tobytes())
+    try:
+        r = subprocess.run([sys.executable, "-c", _WRITE_IMAGE, path(), str(path_), fh.name,
+                            str(rgb.shape[1]), str(rgb.shape[0])], capture_output=True, text=True)
+    finally:
+        os.unlink(fh.name)
+    if r.returncode != 0:
+        raise RuntimeError(f"reference write_image failed ({r.returncode}): {r.stderr[-400:]}")
+
+
 def shade(points, normals, cfg: ShadeConfig, cam: Camera):
     lib = load()
     pts = np.ascontiguousarray(points, np.float32)

@@ -2,6 +2,7 @@
 // reference-shaped call chain (load_manifest -> shading::render / tracer::trace_image ->
 // C ABI -> B200) in-process through ctypes.  Declared in include/nsdf_host.h.
 #include <cstring>
+#include <filesystem>
 #include <string>
 
 #include "device_seq.hpp"
@@ -130,6 +131,33 @@ int nsdf_host_forward_and_gradient(const char* sdfnet, const float* points, int 
     auto [d, g] = mlp::forward_and_gradient_batch(p, pts);
     std::memcpy(dist, d.data(), sizeof(float) * size_t(k));
     std::memcpy(grad, g.data(), sizeof(float) * size_t(3) * k);
+    return NSDF_OK;
+  } catch (const std::exception& e) {
+    return fail_from(e);
+  }
+}
+
+int nsdf_host_write_image(const char* path, int width, int height, const float* rgb) {
+  try {
+    shading::ImageBuffer img(width, height);
+    std::memcpy(img.rgb.data(), rgb, sizeof(float) * img.rgb.size());
+    const std::filesystem::path p(path);
+    if (p.extension() == ".png")
+      shading::write_png(img, p);
+    else
+      shading::write_ppm(img, p);
+    return NSDF_OK;
+  } catch (const std::exception& e) {
+    return fail_from(e);
+  }
+}
+
+int nsdf_host_read_ppm(const char* path, int* width, int* height, float* rgb, size_t capacity) {
+  try {
+    const auto img = shading::read_ppm(path);
+    *width = img.width;
+    *height = img.height;
+    if (rgb && capacity >= img.rgb.size()) std::memcpy(rgb, img.rgb.data(), sizeof(float) * img.rgb.size());
     return NSDF_OK;
   } catch (const std::exception& e) {
     return fail_from(e);

@@ -210,7 +210,7 @@ void write_png(const ImageBuffer& img, const std::filesystem::path& path) {
   }
   uLongf zlen = compressBound(uLong(raw.size()));
   std::vector<uint8_t> z(zlen);
-  if (compress2(z.data(), &zlen, raw.data(), uLong(raw.size()), 6) != Z_OK)
+  if (compress2(z.data(), &zlen, raw.data(), uLong(raw.size()), 9) != Z_OK)
     throw Error(ErrorKind::validation, "zlib compression failed for " + path.string());
   z.resize(zlen);
   png_chunk(out, "IDAT", z);
