@@ -24,6 +24,12 @@ int nsdf_host_trace_image_manifest(const char* manifest, double time, const nsdf
 int nsdf_host_forward_and_gradient(const char* sdfnet, const float* points, int k, float* dist,
                                    float* grad);
 
+/* The reference CLI flows (proj/tools/nsdf_main.cpp) over this library: argv[1] is
+ * train | render | bench, followed by the reference's --flag value pairs.  Returns the
+ * reference's exit code (0 ok, 1 usage/config, 2 validation, 3 divergence); tools/nsdf_b200
+ * is a main() around it. */
+int nsdf_host_cli(int argc, const char* const* argv);
+
 /* Framebuffer output (shading::write_ppm / write_png / read_ppm, image.cpp:32-120): the
  * format follows the path's extension (.png, else binary PPM); rgb is 3 x W x H floats. */
 int nsdf_host_write_image(const char* path, int width, int height, const float* rgb);

@@ -352,6 +352,69 @@ int nsdf_ref_map_normals_mesh(const char* manifest, double time, int index, cons
   SHIM_CATCH
 }
 
+// The reference CLI's train flow (nsdf_main.cpp:163-258: fit_sequence(_4d) -> save_params,
+// report.write, save_manifest) through the reference library, minus the config echo.
+int nsdf_ref_train(const char* shape, const char* archs_csv, int epochs, const char* epochs_list, double lr,
+                   double omega0, uint64_t seed, uint64_t n_uniform, uint64_t n_surface, double sigma,
+                   uint64_t sup_uniform, uint64_t sup_surface, uint64_t verify_samples, double domain_half,
+                   const char* out_dir, const char* name) {
+  SHIM_TRY
+  auto split = [](const std::string& s) {
+    std::vector<std::string> out;
+    std::string cur;
+    for (char ch : s + ",") {
+      if (ch == ',') {
+        if (!cur.empty()) out.push_back(cur);
+        cur.clear();
+      } else {
+        cur += ch;
+      }
+    }
+    return out;
+  };
+  fields::AnalyticSpec spec = fields::parse_field_spec(shape);
+  const bool td = spec.name == "blend";
+  std::vector<mlp::Architecture> archs;
+  for (const auto& a : split(archs_csv)) archs.push_back(mlp::parse_architecture(a, td ? 4 : 3));
+  std::filesystem::path dir(out_dir);
+  std::filesystem::create_directories(dir);
+  trainer::SequenceFitConfig config;
+  config.train.epochs = epochs;
+  config.train.learning_rate = lr;
+  config.train.omega0 = omega0;
+  config.train.seed = seed;
+  config.samples = {n_uniform, n_surface, sigma, 10000, seed};
+  config.sup.n_uniform = sup_uniform;
+  config.sup.n_surface = sup_surface;
+  config.sup.seed = seed + 1;
+  config.verify.samples = verify_samples;
+  config.verify.seed = seed + 2;
+  for (const auto& e : split(epochs_list)) config.epochs_per_arch.push_back(std::stoi(e));
+  auto save = [&](size_t i, const mlp::MlpParams<double>& p, const trainer::TrainReport& r) {
+    std::string stem = std::string(name) + "_" + archs[i].name();
+    mlp::save_params(p, dir / (stem + ".sdfnet"));
+    r.write(dir / (stem + ".report.txt"));
+    return stem + ".sdfnet";
+  };
+  if (td) {
+    auto oracle = std::const_pointer_cast<fields::TimeVaryingField>(
+        std::shared_ptr<const fields::TimeVaryingField>(fields::make_analytic_time_field(spec)));
+    oracle->set_domain(Aabb::cube(domain_half));
+    auto fit = trainer::fit_sequence_4d(archs, *oracle, config);
+    for (size_t i = 0; i < archs.size(); ++i)
+      fit.sequence.entries[i].source = {fields::FieldSource::Kind::weights, {}, save(i, fit.params[i], fit.reports[i])};
+    fields::save_manifest(fit.sequence, dir / (std::string(name) + ".nest"));
+  } else {
+    auto oracle = std::const_pointer_cast<fields::Field>(fields::make_analytic_field(spec));
+    oracle->set_domain(Aabb::cube(domain_half));
+    auto fit = trainer::fit_sequence(archs, *oracle, config);
+    for (size_t i = 0; i < archs.size(); ++i)
+      fit.sequence.entries[i].source = {fields::FieldSource::Kind::weights, {}, save(i, fit.params[i], fit.reports[i])};
+    fields::save_manifest(fit.sequence, dir / (std::string(name) + ".nest"));
+  }
+  SHIM_CATCH
+}
+
 int nsdf_ref_write_image(const char* path, int width, int height, const float* rgb) {
   SHIM_TRY
   shading::ImageBuffer img(width, height);

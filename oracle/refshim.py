@@ -269,6 +269,34 @@ def write_image(path_, rgb_hw3):
         raise RuntimeError(f"reference write_image failed ({r.returncode}): {r.stderr[-400:]}")
 
 
+_TRAIN = r'''
+import ctypes, sys
+lib = ctypes.CDLL(sys.argv[1])
+lib.nsdf_ref_last_error.restype = ctypes.c_char_p
+a = sys.argv[2:]
+D, U = ctypes.c_double, ctypes.c_uint64
+st = lib.nsdf_ref_train(a[0].encode(), a[1].encode(), int(a[2]), a[3].encode(), D(float(a[4])), D(float(a[5])),
+                        U(int(a[6])), U(int(a[7])), U(int(a[8])), D(float(a[9])), U(int(a[10])), U(int(a[11])),
+                        U(int(a[12])), D(float(a[13])), a[14].encode(), a[15].encode())
+if st:
+    sys.stderr.write(lib.nsdf_ref_last_error().decode())
+sys.exit(st)
+'''
+
+
+def train(out_dir, name, shape, archs, epochs, epochs_list, lr, omega0, seed, n_uniform, n_surface, sigma,
+          sup_uniform, sup_surface, verify_samples, domain_half=1.0):
+    """The reference CLI's train flow (fit_sequence(_4d) -> .sdfnet, .report.txt, .nest) in a
+    child interpreter without numpy (see write_image).  Returns (status, message)."""
+    import subprocess
+    import sys
+    args = [shape, archs, epochs, epochs_list, lr, omega0, seed, n_uniform, n_surface, sigma, sup_uniform,
+            sup_surface, verify_samples, domain_half, out_dir, name]
+    r = subprocess.run([sys.executable, "-c", _TRAIN, path(), *[str(x) for x in args]], capture_output=True,
+                       text=True)
+    return r.returncode, r.stderr[-2000:]
+
+
 def shade(points, normals, cfg: ShadeConfig, cam: Camera):
     lib = load()
     pts = np.ascontiguousarray(points, np.float32)

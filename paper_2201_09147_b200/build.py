@@ -139,10 +139,31 @@ def build_cpp_tests(force=False):
     return bins
 
 
+def build_tools(force=False):
+    """tools/cli/*.cpp -> tools/bin/*: the reference CLI's flows over libnsdf_b200.so."""
+    src_dir = os.path.join(ROOT, "tools", "cli")
+    if not os.path.isdir(src_dir):
+        return []
+    out = os.path.join(ROOT, "tools", "bin")
+    os.makedirs(out, exist_ok=True)
+    lib = os.path.join(PKG, "libnsdf_b200.so")
+    bins = []
+    for f in sorted(os.listdir(src_dir)):
+        if not f.endswith(".cpp"):
+            continue
+        src, exe = os.path.join(src_dir, f), os.path.join(out, f[:-4])
+        bins.append(exe)
+        if force or _stale(exe, [src, lib, os.path.join(INC, "nsdf_host.h")]):
+            _run(["g++", *HOST_FLAGS, "-I", INC, src, "-o", exe, "-L", PKG, "-lnsdf_b200", "-lnsdf_cuda",
+                  "-Wl,-rpath,$ORIGIN/../../paper_2201_09147_b200"])
+    return bins
+
+
 def build(force=False, verbose=False):
     build_cuda(force, verbose)
     build_host(force)
     build_cpp_tests(force)
+    build_tools(force)
 
 
 if __name__ == "__main__":
