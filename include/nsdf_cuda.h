@@ -211,6 +211,11 @@ typedef struct {
 /* ---- context ---------------------------------------------------------------------- */
 int nsdf_cuda_abi_version(void);
 const char* nsdf_cuda_last_error(void);
+/* Diagnostics: the fast mode's activation exactly as its tile epilogues evaluate it —
+ * sin(x) and sin(x + pi/2) on the MUFU pipe (sin.approx: FMUL.RZ by 1/2pi reduces the
+ * argument to revolutions, MUFU.SIN evaluates the fraction) — for x[0..n) (host buffers).
+ * tests/test_gpu_fast.py bounds its error at the largest omega0 * z the fixtures produce. */
+int nsdf_cuda_probe_fast_sine(nsdf_ctx* ctx, const float* x, int n, float* sin_out, float* cos_out);
 /* Number of visible CUDA devices (NSDF_ERR_DEVICE when there is none). */
 int nsdf_cuda_device_count(int* n);
 int nsdf_cuda_create(int device, nsdf_ctx** out);

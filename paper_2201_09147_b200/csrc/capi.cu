@@ -483,6 +483,25 @@ int nsdf_cuda_abi_version(void) { return NSDF_CUDA_ABI_VERSION; }
 
 const char* nsdf_cuda_last_error(void) { return g_error.c_str(); }
 
+int nsdf_cuda_probe_fast_sine(nsdf_ctx* c, const float* x, int n, float* sin_out, float* cos_out) {
+  if (!c || !x || !sin_out || !cos_out || n < 0) return fail(NSDF_ERR_CONTRACT, "null argument");
+  std::lock_guard<std::mutex> lk(c->mu);
+  DeviceGuard g(c->device);
+  if (n == 0) return NSDF_OK;
+  size_t off = 0;
+  NSDF_CUDA(c->io.reserve(size_t(n) * 12 + 4096));
+  float* dx = carve<float>(c->io.base, off, size_t(n));
+  float* ds = carve<float>(c->io.base, off, size_t(n));
+  float* dc = carve<float>(c->io.base, off, size_t(n));
+  cudaStream_t s = c->stream;
+  NSDF_CUDA(cudaMemcpyAsync(dx, x, size_t(n) * 4, cudaMemcpyHostToDevice, s));
+  NSDF_CUDA(launch_fast_sine_probe(dx, n, ds, dc, s));
+  NSDF_CUDA(cudaMemcpyAsync(sin_out, ds, size_t(n) * 4, cudaMemcpyDeviceToHost, s));
+  NSDF_CUDA(cudaMemcpyAsync(cos_out, dc, size_t(n) * 4, cudaMemcpyDeviceToHost, s));
+  NSDF_CUDA(cudaStreamSynchronize(s));
+  return NSDF_OK;
+}
+
 int nsdf_cuda_device_count(int* n) {
   if (!n) return fail(NSDF_ERR_CONTRACT, "null argument");
   *n = 0;

@@ -1375,4 +1375,19 @@ TcLaunch tc_normal_map(int terms, const DevField& f, const float* pts, int k, fl
   return launch_any<true>(a, k, s);
 }
 
+// The fast mode's activation, exactly as the tile epilogues evaluate it: sin(x) for value
+// rows and sin(x + pi/2) = cos(x) for the tangent rows' derivative factor.
+__global__ void fast_sine_probe_kernel(const float* x, int n, float* s, float* c) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    s[i] = fast_sin(x[i]);
+    c[i] = fast_sin(x[i] + kHalfPi);
+  }
+}
+
+cudaError_t launch_fast_sine_probe(const float* x, int n, float* s, float* c, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  fast_sine_probe_kernel<<<std::min((n + 255) / 256, 148 * 8), 256, 0, st>>>(x, n, s, c);
+  return cudaGetLastError();
+}
+
 }  // namespace nsdf_b200

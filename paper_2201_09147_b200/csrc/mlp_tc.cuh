@@ -28,4 +28,8 @@ TcLaunch tc_eval(int terms, const DevField& f, const float* pts, int rows, int k
 TcLaunch tc_normal_map(int terms, const DevField& f, const float* pts, int k, float time, double delta,
                    const float* fallback, float* normals, unsigned long long* counts, cudaStream_t s);
 
+// The fast-mode sine exactly as the epilogues use it (sin and sin(x + pi/2)), for the
+// accuracy test at large omega0 * z arguments.
+cudaError_t launch_fast_sine_probe(const float* x, int n, float* s, float* c, cudaStream_t st);
+
 }  // namespace nsdf_b200

@@ -2,6 +2,7 @@
 reference CPU path on identical weights and rays, with the BASELINE tolerances
 (SURVEY.md §8d): hit/miss mask agreement >= 99.9%, |dt| <= 1e-3 on common hits (scene
 scale 1), normals within 0.5 deg — end to end and at identical points."""
+import ctypes
 import os
 
 import numpy as np
@@ -287,3 +288,52 @@ def test_fast_mixed_analytic_and_neural_levels(ctx, fast, tmp_path):
     b = fast.render(DeviceSequence(fast, seq).levels(), cam, cfg, shade)
     _assert_render_parity(a, b)
     assert a[2].sum() > 1000
+
+
+def _max_sine_argument(seq, n=100000, seed=3):
+    """Largest |omega0 * (W a + b)| any sine of the sequence's nets sees, over uniform points
+    of the domain and the 4-D slice times (float64 forward pass of the fixture weights)."""
+    rng = np.random.default_rng(seed)
+    worst = 0.0
+    for net in seq.members:
+        if not hasattr(net, "layers"):
+            continue
+        x = rng.uniform(-1.0, 1.0, size=(net.input_dim, n))
+        for w, b in net.layers()[:-1]:
+            z = net.omega0 * (w @ x + b[:, None])
+            worst = max(worst, float(np.max(np.abs(z))))
+            x = np.sin(z)
+    return worst
+
+
+def test_fast_sine_at_large_arguments(fast):
+    """The fast mode's activation (MUFU sin.approx behind FMUL.RZ(x, 1/2pi): the explicit
+    range reduction to revolutions is that one RZ multiply) against float64 sin of the same
+    fp32 argument, over the full range of omega0 * z the committed fixtures produce (with
+    omega0 = 30 that is well beyond pi): absolute error <= 2^-20 + |x| * 2^-22 — one RZ
+    rounding of x/2pi plus the MUFU approximation — for sin and for the cos(x) = sin(x + pi/2)
+    derivative factor of the tangent rows."""
+    from paper_2201_09147_b200.manifest import load_manifest
+    top = 0.0
+    for name in ("torus_w30.nest", "blend4d_w30.nest"):
+        p = os.path.join(ASSETS, name)
+        if os.path.exists(p):
+            top = max(top, _max_sine_argument(load_manifest(p)))
+    assert top > 3.5, top  # the fixtures do leave [-pi, pi]
+    rng = np.random.default_rng(0)
+    lim = 1.05 * top
+    x = np.concatenate([np.linspace(-lim, lim, 400001), rng.uniform(-lim, lim, 400000),
+                        np.arange(-64, 65) * np.pi / 2, [0.0, 1e-30, -1e-30]]).astype(np.float32)
+    s = np.zeros_like(x)
+    c = np.zeros_like(x)
+    fp = ctypes.POINTER(ctypes.c_float)
+    st = fast.lib.nsdf_cuda_probe_fast_sine(fast._ctx, x.ctypes.data_as(fp), len(x), s.ctypes.data_as(fp),
+                                            c.ctypes.data_as(fp))
+    assert st == 0
+    xd = x.astype(np.float64)
+    bound = 2.0 ** -20 + np.abs(xd) * 2.0 ** -22
+    es = np.abs(s - np.sin(xd))
+    ec = np.abs(c - np.cos(xd))
+    assert np.all(es <= bound), (float(np.max(es / bound)), float(xd[np.argmax(es / bound)]))
+    assert np.all(ec <= bound + np.abs(xd) * 2.0 ** -24), float(np.max(ec / bound))
+    print(f"max |omega0 z| of the fixtures {top:.1f}; max sine error {es.max():.2e}, cos {ec.max():.2e}")

@@ -227,3 +227,50 @@ def test_config4_gbuffer_normal_map(ref):
         os.unlink(fh.name)
     assert (g_out, g_fb) == (r_out, r_fb)
     assert np.max(_angle_deg(g_nrm, r_nrm)) <= NORMAL_DEG_MAX
+
+
+def _records(recs):
+    from conftest import records_np
+    return records_np(recs)
+
+
+@pytest.mark.parametrize("budgets", [(20, 5, 5), (40, 20, 20)])
+def test_depth_outliers_are_stop_band_steps(ref, budgets):
+    """The max |dt| above 1e-3 (p99.9 is ~1e-5): a ray whose last |f| lands within the fast
+    mode's |df| ~ 1e-5 of eps_stop stops one iteration earlier or later than the reference's,
+    so the two hit parameters differ by ONE final step, itself <= eps_stop + |df|.  Asserted
+    per ray: every common hit with |dt| > 1e-3 has a different total iteration count, and
+    |dt| <= 1.05 eps_stop.  The reference's own two backends (scalar vs AVX2, same weights and
+    rays) show the same stop-band jitter; its spread is printed beside ours."""
+    from paper_2201_09147_b200.abi import TraceConfig, standard_camera
+    from paper_2201_09147_b200.engine import Context, DeviceSequence
+    from paper_2201_09147_b200.manifest import load_manifest
+    path = _manifest()
+    cam = standard_camera(1920, 1080)
+    cfg = TraceConfig(budgets)
+    r = _records(ref.trace_image(path, cam, cfg))
+    ref.set_backend("scalar")
+    try:
+        s = _records(ref.trace_image(path, cam, cfg))
+    finally:
+        ref.set_backend("avx2")
+    c = Context(0, "fp16")
+    try:
+        recs, _ = c.trace_image(DeviceSequence(c, load_manifest(path)).levels(), cam, cfg)
+        f = _records(recs)
+    finally:
+        c.close()
+    both = (f["hit"] == 1) & (r["hit"] == 1)
+    dt = np.abs(f["t"] - r["t"])[both]
+    its_f = f["iters"].astype(np.int64).sum(1)[both]
+    its_r = r["iters"].astype(np.int64).sum(1)[both]
+    out = dt > DT_MAX
+    sb = (s["hit"] == 1) & (r["hit"] == 1)
+    dt_s = np.abs(s["t"] - r["t"])[sb]
+    msg = (f"fast vs reference: max |dt| {dt.max():.3e}, p99.9 {np.percentile(dt, 99.9):.2e}, {int(out.sum())} rays "
+           f"> 1e-3 of {int(both.sum())}; reference scalar vs AVX2: max {dt_s.max():.3e}, "
+           f"{int((dt_s > DT_MAX).sum())} rays > 1e-3")
+    print(msg)
+    assert np.percentile(dt, 99.9) <= DT_MAX, msg
+    assert np.all(its_f[out] != its_r[out]), msg
+    assert dt.max() <= 1.05 * cfg.eps_stop, msg
