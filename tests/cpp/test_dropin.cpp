@@ -362,8 +362,46 @@ TEST_CASE("tensor ops: shape errors name both shapes, sine basics, flops, backen
   tensor::gemm(Matrix<float>(4, 8), Matrix<float>(8, 16));
   CHECK(tensor::flops_performed() == 2ull * 4 * 16 * 8);
   CHECK(tensor::active_backend() == tensor::Backend::b200 && tensor::backend_available(tensor::Backend::b200));
-  CHECK(!tensor::backend_available(tensor::Backend::scalar));
-  CHECK_THROWS(tensor::set_backend(tensor::Backend::scalar));
+  CHECK(!tensor::backend_available(tensor::Backend::neon));
+  CHECK_THROWS(tensor::set_backend(tensor::Backend::neon));
+}
+
+TEST_CASE("backend loop of the reference suite: scalar / avx2 / b200 (test_tensor.cpp:17-28, 230-280)") {
+  // the reference's available_backends(): scalar always, then the SIMD backends present
+  std::vector<tensor::Backend> backends{tensor::Backend::scalar};
+  for (auto b : {tensor::Backend::avx2, tensor::Backend::neon})
+    if (tensor::backend_available(b)) backends.push_back(b);
+  CHECK(backends.size() == 2);
+  const tensor::Backend saved = tensor::active_backend();
+  Rng rng(77);
+  Matrix<float> a(37, 29), b(29, 41), bias(37, 1);
+  for (auto* m : {&a, &b, &bias})
+    for (auto& v : m->storage()) v = float(rng.uniform(-1, 1));
+  tensor::set_backend(tensor::Backend::scalar);
+  const Matrix<float> want = tensor::gemm(a, b, &bias);
+  const Matrix<float> sw = tensor::activate(a, tensor::ActivationSpec::sine(30.0));
+  for (auto be : backends) {
+    tensor::set_backend(be);
+    CHECK(tensor::active_backend() == be);
+    CHECK(std::string(tensor::kernels::active().name) == tensor::backend_name(be));
+    const Matrix<float> got = tensor::gemm(a, b, &bias);
+    const Matrix<float> s = tensor::activate(a, tensor::ActivationSpec::sine(30.0));
+    double worst = 0, worst_s = 0;
+    for (size_t i = 0; i < got.storage().size(); ++i)
+      worst = std::max(worst, double(std::abs(got.storage()[i] - want.storage()[i])));
+    for (size_t i = 0; i < s.storage().size(); ++i)
+      worst_s = std::max(worst_s, double(std::abs(s.storage()[i] - sw.storage()[i])));
+    CHECK(worst < 1e-5 && worst_s < 1e-5);  // the SIMD variants agree with scalar up to rounding
+    const Matrix<float> ten{{10}, {10}};
+    const Matrix<float> hand = tensor::gemm(Matrix<float>{{1, 2}, {3, 4}}, Matrix<float>{{1}, {1}}, &ten);
+    CHECK(hand(0, 0) == 13.0f && hand(1, 0) == 17.0f);
+  }
+  // the avx2 table IS the device table's arithmetic
+  tensor::set_backend(tensor::Backend::avx2);
+  const Matrix<float> x = tensor::gemm(a, b, &bias);
+  tensor::set_backend(tensor::Backend::b200);
+  CHECK(x.storage() == tensor::gemm(a, b, &bias).storage());
+  tensor::set_backend(saved);
 }
 
 template <typename T>
