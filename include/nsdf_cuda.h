@@ -18,6 +18,7 @@
  *                             gradient_batch<double>                    src/mlp/mlp.cpp:104-210
  *                             NeuralField / NeuralTimeField f64 batches src/fields/field.cpp:167-178, 301-311
  *                             (the certification path: nesting.cpp:131-361)
+ *   nsdf_cuda_project_to_surface fields::sample_near_surface projection nesting.cpp:98-127
  *   nsdf_cuda_backprop_f64    trainer::backprop_sine_mlp                src/trainer/backprop.cpp:66-78
  *   nsdf_cuda_fit_mlp         trainer::fit_mlp (device-resident loop)   src/trainer/fit.cpp:87-196
  *   nsdf_cuda_generate_rays   tracer::generate_rays                     src/tracer/camera.cpp:20-43
@@ -261,6 +262,16 @@ int nsdf_cuda_replicate_field(nsdf_ctx* src, nsdf_field field, nsdf_ctx* dst, ns
 int nsdf_cuda_field_info(nsdf_ctx* ctx, nsdf_field field, int* input_dim, int* n_layers,
                          int* width);
 
+/* Certification: the projection step of fields::sample_near_surface (nesting.cpp:98-127)
+ * with the points resident on the device — `steps` Newton steps p -= f/|g|^2 g (skipped
+ * where |g|^2 < 1e-16) from n candidates (Vec3 array, n <= 2^20), then the points with
+ * |f| <= keep_tol, in input order, with the field's gradient there (Vec3 arrays); FP64,
+ * bit-identical to the reference's double path.  Replaces 4 x (eval + grad) host round trips
+ * per round with one H2D and one D2H. */
+int nsdf_cuda_project_to_surface(nsdf_ctx* ctx, nsdf_field field, double time, const double* candidates,
+                                 int n, double keep_tol, int steps, double* kept, double* kept_grads,
+                                 int* n_kept);
+
 /* ---- batch evaluation (Field::eval_batch / grad_batch, mlp::*_batch) ------------------
  * points: rows x k; out: 1 x k; grad: 3 x k.  Either output may be NULL in eval_grad. */
 int nsdf_cuda_eval(nsdf_ctx* ctx, nsdf_field field, const float* points, int rows, int k,
@@ -275,7 +286,8 @@ int nsdf_cuda_eval_grad_device(nsdf_ctx* ctx, nsdf_field field, const float* d_p
  * (certification: estimate_sup_diff / verify_nesting / sample_near_surface).  points:
  * rows x k doubles (HOST); out: k or NULL; grad: 3 x k or NULL (not both NULL).  A 3-row
  * batch for a 4-input net gets the constant `time` row (double, field.cpp:213-220).
- * Analytic fields return NSDF_ERR_CONFIG (they evaluate on the host). */
+ * Sphere / torus / box fields evaluate in double exactly as field.cpp:57-124 (glibc hypot
+ * restated for the torus). */
 int nsdf_cuda_eval_f64(nsdf_ctx* ctx, nsdf_field field, const double* points, int rows, int k,
                        double time, double* out, double* grad);
 

@@ -1053,8 +1053,6 @@ int nsdf_cuda_eval_f64(nsdf_ctx* c, nsdf_field h, const double* points, int rows
   DeviceGuard g(c->device);
   FieldRec* f;
   if (int st = find_field(c, h, &f)) return st;
-  if (f->dev.kind != kFieldMlp)
-    return fail(NSDF_ERR_CONFIG, "f64 device evaluation covers neural fields; analytic fields evaluate on the host");
   if (int st = check_points(f, rows, k)) return st;
   if (k == 0) return NSDF_OK;
   if (!points) return fail(NSDF_ERR_CONTRACT, "points is null");
@@ -1066,10 +1064,43 @@ int nsdf_cuda_eval_f64(nsdf_ctx* c, nsdf_field h, const double* points, int rows
   double* dgrad = carve<double>(c->io.base, off, size_t(3) * k);
   cudaStream_t s = c->stream;
   NSDF_CUDA(cudaMemcpyAsync(dp, points, size_t(rows) * k * 8, cudaMemcpyHostToDevice, s));
-  NSDF_CUDA(launch_eval_f64(f->dev.net, dp, rows, k, time, out ? dout : nullptr, grad ? dgrad : nullptr, s));
+  NSDF_CUDA(launch_eval_field_f64(f->dev, dp, rows, k, time, out ? dout : nullptr, grad ? dgrad : nullptr, s));
   if (out) NSDF_CUDA(cudaMemcpyAsync(out, dout, size_t(k) * 8, cudaMemcpyDeviceToHost, s));
   if (grad) NSDF_CUDA(cudaMemcpyAsync(grad, dgrad, size_t(3) * k * 8, cudaMemcpyDeviceToHost, s));
   NSDF_CUDA(cudaStreamSynchronize(s));
+  return NSDF_OK;
+}
+
+int nsdf_cuda_project_to_surface(nsdf_ctx* c, nsdf_field h, double time, const double* candidates, int n,
+                                 double keep_tol, int steps, double* kept, double* kept_grads, int* n_kept) {
+  if (!c || !candidates || !kept || !kept_grads || !n_kept) return fail(NSDF_ERR_CONTRACT, "null argument");
+  if (n < 0 || n > (1 << 20)) return fail(NSDF_ERR_CONTRACT, "projection batches hold 0 .. 2^20 points");
+  if (steps < 0) return fail(NSDF_ERR_CONTRACT, "negative projection step count");
+  std::lock_guard<std::mutex> lk(c->mu);
+  DeviceGuard g(c->device);
+  FieldRec* f;
+  if (int st = find_field(c, h, &f)) return st;
+  *n_kept = 0;
+  if (n == 0) return NSDF_OK;
+  size_t off = 0;
+  NSDF_CUDA(c->io.reserve((size_t(n) * 9 + projection_workspace_doubles(n)) * 8 + 8192));
+  double* dc = carve<double>(c->io.base, off, size_t(3) * n);
+  double* dk = carve<double>(c->io.base, off, size_t(3) * n);
+  double* dg = carve<double>(c->io.base, off, size_t(3) * n);
+  int* dcount = carve<int>(c->io.base, off, 1);
+  double* ws = carve<double>(c->io.base, off, projection_workspace_doubles(n));
+  cudaStream_t s = c->stream;
+  NSDF_CUDA(cudaMemcpyAsync(dc, candidates, size_t(n) * 24, cudaMemcpyHostToDevice, s));
+  NSDF_CUDA(launch_project_to_surface(f->dev, time, dc, n, keep_tol, steps, ws, dk, dg, dcount, s));
+  int cnt = 0;
+  NSDF_CUDA(cudaMemcpyAsync(&cnt, dcount, sizeof(int), cudaMemcpyDeviceToHost, s));
+  NSDF_CUDA(cudaStreamSynchronize(s));
+  if (cnt > 0) {
+    NSDF_CUDA(cudaMemcpyAsync(kept, dk, size_t(cnt) * 24, cudaMemcpyDeviceToHost, s));
+    NSDF_CUDA(cudaMemcpyAsync(kept_grads, dg, size_t(cnt) * 24, cudaMemcpyDeviceToHost, s));
+    NSDF_CUDA(cudaStreamSynchronize(s));
+  }
+  *n_kept = cnt;
   return NSDF_OK;
 }
 

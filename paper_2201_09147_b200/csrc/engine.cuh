@@ -161,6 +161,18 @@ void launch_raycast_mesh(const CamBasis& cb, const float* tri_verts /* n_tri x 9
 cudaError_t launch_eval_f64(const DevNet& n, const double* pts, int rows, int k, double time, double* out, double* grad,
                      cudaStream_t s);
 
+// FP64 evaluation of any device field (neural: launch_eval_f64; sphere / torus / box in
+// double as field.cpp:57-124), device buffers.
+cudaError_t launch_eval_field_f64(const DevField& f, const double* pts, int rows, int k, double time, double* out,
+                                  double* grad, cudaStream_t s);
+// sample_near_surface's projection (nesting.cpp:98-127) on resident points: `steps` Newton
+// steps from the k candidates (Vec3 array), keep |f| <= keep_tol; the kept points and the
+// field gradient at them (Vec3 arrays, input order) and their count (device int).
+size_t projection_workspace_doubles(int k);
+cudaError_t launch_project_to_surface(const DevField& f, double time, const double* cand, int k, double keep_tol,
+                                      int steps, double* ws, double* kept, double* kept_g, int* d_count,
+                                      cudaStream_t s);
+
 // FP64 SIREN training (train_f64.cu), host buffers in/out.
 cudaError_t train_backprop(int n_layers, const int32_t* rows, const int32_t* cols, const double* params_h,
                            int activation, double omega0, int input_dim, const double* points_h,

@@ -216,4 +216,133 @@ cudaError_t launch_eval_f64(const DevNet& n, const double* pts, int rows, int k,
               : launch_f64<false>(n, pts, rows, k, time, out, nullptr, s);
 }
 
+// ---------------------------------------------------------------------------------------
+// Certification on the device: the Newton projection of
+// sample_near_surface (nesting.cpp:98-127) with the points resident, and the FP64 analytic
+// members so that every bound field evaluates here.
+// ---------------------------------------------------------------------------------------
+namespace {
+
+__global__ void analytic_f64_kernel(DevField f, const double* pts, int k, double* out, double* grad) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < k; j += gridDim.x * blockDim.x) {
+    const double x = pts[j], y = pts[size_t(k) + j], z = pts[2 * size_t(k) + j];
+    if (out) out[j] = analytic_eval(f, x, y, z);
+    if (grad) {
+      double g[3];
+      analytic_grad(f, x, y, z, g);
+      for (int r = 0; r < 3; ++r) grad[size_t(r) * k + j] = g[r];
+    }
+  }
+}
+
+int grid_for(int k) { return std::max(1, std::min((k + 255) / 256, 148 * 8)); }
+
+// Vec3 array (x y z per point) -> 3 x k rows
+__global__ void aos_to_rows_kernel(const double* v, int k, double* p) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < k; j += gridDim.x * blockDim.x)
+    for (int r = 0; r < 3; ++r) p[size_t(r) * k + j] = v[3 * size_t(j) + r];
+}
+
+// p -= (f / |g|^2) g where |g|^2 >= 1e-16 (separately rounded, left to right)
+__global__ void newton_kernel(double* p, const double* f, const double* g, int k) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < k; j += gridDim.x * blockDim.x) {
+    const double gx = g[j], gy = g[size_t(k) + j], gz = g[2 * size_t(k) + j];
+    const double n2 = __dadd_rn(__dadd_rn(__dmul_rn(gx, gx), __dmul_rn(gy, gy)), __dmul_rn(gz, gz));
+    if (n2 < 1e-16) continue;
+    const double s = __ddiv_rn(f[j], n2);
+    p[j] = __dsub_rn(p[j], __dmul_rn(s, gx));
+    p[size_t(k) + j] = __dsub_rn(p[size_t(k) + j], __dmul_rn(s, gy));
+    p[2 * size_t(k) + j] = __dsub_rn(p[2 * size_t(k) + j], __dmul_rn(s, gz));
+  }
+}
+
+constexpr int kScanBlock = 1024;
+
+// per 1024-point block: number of kept points (|f| <= tol)
+__global__ void keep_count_kernel(const double* f, int k, double tol, int* block_counts) {
+  const int j = blockIdx.x * kScanBlock + threadIdx.x;
+  const bool keep = j < k && fabs(f[j]) <= tol;
+  const int n = __syncthreads_count(keep);
+  if (threadIdx.x == 0) block_counts[blockIdx.x] = n;
+}
+
+// exclusive scan of the block counts (<= 1024 blocks, one CTA); total -> counts[n_blocks]
+__global__ void scan_counts_kernel(int* counts, int n_blocks) {
+  __shared__ int sh[kScanBlock];
+  const int i = threadIdx.x;
+  const int v = i < n_blocks ? counts[i] : 0;
+  sh[i] = v;
+  __syncthreads();
+  for (int o = 1; o < kScanBlock; o <<= 1) {
+    const int add = i >= o ? sh[i - o] : 0;
+    __syncthreads();
+    sh[i] += add;
+    __syncthreads();
+  }
+  if (i < n_blocks) counts[i] = sh[i] - v;
+  if (i == kScanBlock - 1) counts[n_blocks] = sh[i];
+}
+
+// kept points and their gradients, in input order, as Vec3 arrays
+__global__ void keep_scatter_kernel(const double* p, const double* f, const double* g, int k, double tol,
+                                    const int* offsets, double* kept, double* kept_g) {
+  __shared__ int warp_base[kScanBlock / 32];
+  const int j = blockIdx.x * kScanBlock + threadIdx.x;
+  const bool keep = j < k && fabs(f[j]) <= tol;
+  const unsigned m = __ballot_sync(0xffffffffu, keep);
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  if (lane == 0) warp_base[w] = __popc(m);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int run = 0;
+    for (int i = 0; i < kScanBlock / 32; ++i) {
+      const int c = warp_base[i];
+      warp_base[i] = run;
+      run += c;
+    }
+  }
+  __syncthreads();
+  if (!keep) return;
+  const size_t o = size_t(offsets[blockIdx.x] + warp_base[w] + __popc(m & ((1u << lane) - 1u)));
+  for (int r = 0; r < 3; ++r) {
+    kept[3 * o + r] = p[size_t(r) * k + j];
+    kept_g[3 * o + r] = g[size_t(r) * k + j];
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_eval_field_f64(const DevField& f, const double* pts, int rows, int k, double time, double* out,
+                                  double* grad, cudaStream_t s) {
+  if (k <= 0) return cudaSuccess;
+  if (f.kind == kFieldMlp) return launch_eval_f64(f.net, pts, rows, k, time, out, grad, s);
+  analytic_f64_kernel<<<grid_for(k), 256, 0, s>>>(f, pts, k, out, grad);
+  return cudaGetLastError();
+}
+
+size_t projection_workspace_doubles(int k) { return size_t(k) * 16 + 2 * (size_t(k) / kScanBlock + 2); }
+
+cudaError_t launch_project_to_surface(const DevField& f, double time, const double* cand, int k, double keep_tol,
+                                      int steps, double* ws, double* kept, double* kept_g, int* d_count,
+                                      cudaStream_t s) {
+  if (k <= 0) return cudaMemsetAsync(d_count, 0, sizeof(int), s);
+  double* p = ws;
+  double* fv = p + 3 * size_t(k);
+  double* g = fv + size_t(k);
+  int* counts = reinterpret_cast<int*>(g + 3 * size_t(k));
+  const int n_blocks = (k + kScanBlock - 1) / kScanBlock;
+  if (n_blocks > kScanBlock) return cudaErrorInvalidValue;  // batches are <= 2^20 points
+  aos_to_rows_kernel<<<grid_for(k), 256, 0, s>>>(cand, k, p);
+  for (int step = 0; step < steps; ++step) {
+    if (cudaError_t e = launch_eval_field_f64(f, p, 3, k, time, fv, g, s)) return e;
+    newton_kernel<<<grid_for(k), 256, 0, s>>>(p, fv, g, k);
+  }
+  if (cudaError_t e = launch_eval_field_f64(f, p, 3, k, time, fv, g, s)) return e;
+  keep_count_kernel<<<n_blocks, kScanBlock, 0, s>>>(fv, k, keep_tol, counts);
+  scan_counts_kernel<<<1, kScanBlock, 0, s>>>(counts, n_blocks);
+  keep_scatter_kernel<<<n_blocks, kScanBlock, 0, s>>>(p, fv, g, k, keep_tol, counts, kept, kept_g);
+  if (cudaError_t e = cudaMemcpyAsync(d_count, counts + n_blocks, sizeof(int), cudaMemcpyDeviceToDevice, s)) return e;
+  return cudaGetLastError();
+}
+
 }  // namespace nsdf_b200

@@ -18,7 +18,7 @@ from paper_2201_09147_b200.abi import ShadeConfig, TraceConfig, standard_camera 
 from paper_2201_09147_b200.engine import Context, DeviceSequence  # noqa: E402
 from paper_2201_09147_b200.manifest import load_manifest  # noqa: E402
 
-BUDGETS = [(20, 5, 5), (20, 10, 5), (20, 10, 10), (30, 10, 10), (40, 20, 20), (40, 40, 40)]
+BUDGETS = [tuple(int(x) for x in b.split(",")) for b in os.environ.get("NSDF_SCAN_BUDGETS", "20,5,5;20,10,10;40,20,20;40,40,40").split(";")]
 
 
 def scan(path, w=1920, h=1080):
