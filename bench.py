@@ -2,27 +2,30 @@
 """Benchmark: Mrays/s & ms/frame at 1080p, multiscale sphere tracing + analytic normals.
 
 Default workload (BASELINE.json configs[1]): the nested 3-level SIREN
-sequence 64x1 > 128x2 > 256x3 (omega0 = 30, Prop-2 certified, assets/torus_w30.nest) traced
-at 1920x1080 from the standard camera with budgets (20,5,5), own analytic normals from the
-256x3 net, Lambert + Blinn-Phong (specular 0.3, the `nsdf bench` shading,
-nsdf_main.cpp:446).  One step = one whole frame: rays -> multiscale trace -> normals ->
-shade -> framebuffer.  Weights are resident (uploaded once; broadcast over NCCL for N>1);
-the per-frame working set (ray state + lists + framebuffer, ~160 MB at 1080p) exceeds the
-126 MB L2, so no flush is needed between steps.
+sequence 64x1 > 128x2 > 256x3 (assets/torus3.nest: the reference trainer's fit of the torus,
+omega0 = 10, Prop-2 certified; tools/build_assets.sh) traced at 1920x1080 from the standard
+camera with budgets (40,20,20) — the setting whose frame converges (hits within ~5% of
+(40,40,40); `frame_quality` reports the hit fraction and the image MSE against that frame) —
+own analytic normals from the 256x3 net, Lambert + Blinn-Phong (specular 0.3, the `nsdf
+bench` shading, nsdf_main.cpp:446).  The paper-style speed setting (20,5,5) is timed beside
+it (`speed_setting`, with its MSE).  One step = one whole frame: rays -> multiscale trace ->
+normals -> shade -> framebuffer.  Weights are resident (uploaded once; broadcast over NCCL for
+N>1); the per-frame working set (ray state + lists + framebuffer, ~160 MB at 1080p) exceeds
+the 126 MB L2, so no flush is needed between steps.
 
---config 1|3|4|5 selects the other BASELINE workloads (1: single 256x3 at 512^2; 3: neural
-normal mapping 64x1 (40,0) + 256x3 normals at 1080p; 4: torus-mesh G-buffer -> 256x3 normals
-at 2560x1440; 5: animated 4-D 64x1 > 128x2 blend, 120 frames at 3840x2160, frames sharded
-across ranks).
+--config 1|3|4|5 selects the other BASELINE workloads (1: single 256x3 omega0 = 30 at 512^2;
+3: neural normal mapping 64x1 (40,0) + 256x3 normals at 1080p; 4: torus-mesh G-buffer ->
+256x3 normals at 2560x1440; 5: animated 4-D 64x1 > 128x2 blend (omega0 = 30), 120 frames at
+3840x2160, frames sharded across ranks).
 
-N > 1 (torchrun, the frame/tile scheduler of SURVEY.md §8e): by default (--shard frames) the
-frame stream is sharded — every rank renders whole frames, no data-path collective, weak
-scaling (config 5: the animation's frames round-robin) — and the same run also times the
-strong-scaling alternative (image tiles interleaved across ranks, tile t -> rank t % N, each
-rank's shading kernels storing its pixels into rank 0's framebuffer over NVLink peer memory;
-reported as `strong_scaling`); --shard tiles makes the tile split the headline.
---impl reference times the reference's own CPU renderer (oracle/_ref/libnsdf_ref.so, all
-host threads) on the same config.
+N > 1 (torchrun, the frame/tile scheduler of SURVEY.md §8e): by default (--shard tiles) every
+frame is split into image tiles interleaved across the ranks (tile t -> rank t % N), each
+rank's shading kernels storing its pixels into rank 0's framebuffer over NVLink peer memory
+(strong scaling; ms_per_frame is the latency of a whole frame); --shard frames shards the
+frame stream instead (every rank renders whole frames, no data-path collective, weak scaling)
+and times the tile split beside it as `strong_scaling`; config 5's animation always shards
+frames.  --impl reference times the reference's own CPU renderer (oracle/_ref/libnsdf_ref.so,
+all host threads) on the same config.
 """
 from __future__ import annotations
 
@@ -40,7 +43,8 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
-TORUS = os.path.join(ROOT, "assets", "torus_w30.nest")
+TORUS = os.path.join(ROOT, "assets", "torus_w30.nest")   # omega0 = 30 (PyTorch fit, certified by the reference)
+TORUS3 = os.path.join(ROOT, "assets", "torus3.nest")      # reference trainer, omega0 = 10 (tools/build_assets.sh)
 BLEND = os.path.join(ROOT, "assets", "blend4d_w30.nest")
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
 
@@ -48,14 +52,14 @@ CONFIGS = {
     1: dict(manifest=TORUS, members=[2], budgets="40", normals="own", res=(512, 512),
             metric="Mrays/s & ms/frame at 512x512 (single 256x3 SIREN ST + analytic normals)",
             desc="config1: single 256x3 SIREN (torus, omega0=30), 512x512, budgets ({b}), own analytic normals"),
-    2: dict(manifest=TORUS, members=[0, 1, 2], budgets="20,5,5", normals="own", res=(1920, 1080),
-            metric="Mrays/s & ms/frame at 1080p (multiscale ST + analytic normals)",
-            desc="config2: nested 64x1>128x2>256x3 SIREN (torus, omega0=30), 1920x1080, budgets ({b}), "
-                 "own analytic normals, specular 0.3"),
-    3: dict(manifest=TORUS, members=[0, 2], budgets="40,0", normals="mapped", res=(1920, 1080),
+    2: dict(manifest=TORUS3, members=[0, 1, 2], budgets="40,20,20", speed_budgets="20,5,5", normals="own",
+            res=(1920, 1080), metric="Mrays/s & ms/frame at 1080p (multiscale ST + analytic normals)",
+            desc="config2: nested 64x1>128x2>256x3 SIREN (torus, reference trainer, omega0=10), 1920x1080, "
+                 "budgets ({b}), own analytic normals, specular 0.3"),
+    3: dict(manifest=TORUS3, members=[0, 2], budgets="40,0", normals="mapped", res=(1920, 1080),
             metric="Mrays/s & ms/frame at 1080p (neural normal mapping: 64x1 traced, 256x3 normals)",
-            desc="config3: 64x1 traced with budgets ({b}), normals mapped from 256x3, 1920x1080"),
-    4: dict(manifest=TORUS, members=[2], kind="gbuffer", res=(2560, 1440),
+            desc="config3: 64x1 traced with budgets ({b}), normals mapped from 256x3 (torus3), 1920x1080"),
+    4: dict(manifest=TORUS3, members=[2], kind="gbuffer", res=(2560, 1440),
             metric="Mnormals/s & ms/frame at 2560x1440 (mesh G-buffer -> neural normals)",
             desc="config4: torus mesh (96x48 quads) G-buffer at 2560x1440 -> 256x3 neural normal map"),
     5: dict(manifest=BLEND, members=[0, 1], budgets="20,10", normals="own", res=(3840, 2160), frames=120,
@@ -90,7 +94,8 @@ def parse():
                          "beside it as strong_scaling.  Config 5 (animation) always shards frames")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--no-alt", action="store_true", help="skip the (40,20,20) parity-setting line of config 2")
+    ap.add_argument("--no-alt", action="store_true",
+                    help="skip the frame-quality renders and the (20,5,5) speed-setting line of config 2")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     args.width = args.width or cfg["res"][0]
@@ -813,37 +818,59 @@ def main():
                  "profiled_frame_ms": prof.frame_ms / max(prof.frames, 1), "profile": prof_kind,
                  "level_ms": [prof.level_ms[j] / max(prof.frames, 1) for j in range(len(seq.members))]}
 
-    # config 2 is reported at the speed setting (20,5,5) — the headline — and
-    # at the generous parity setting (40,20,20), same frames-in-flight harness, device buffers.
-    alt = None
-    if args.config == 2 and world == 1 and args.budgets == "20,5,5" and not args.no_alt:
-        cfg_alt = TraceConfig((40, 20, 20))
+    # config 2 is reported at the generous setting (40,20,20) — the headline,
+    # whose frame converges (hits within ~5% of (40,40,40)) — and at the paper-style speed
+    # setting (20,5,5) beside it, each with the image MSE against the (40,40,40) frame, as
+    # `nsdf bench` reports every row against its baseline row (nsdf_main.cpp:484-500).
+    alt, quality = None, None
+    if not W["gbuffer"] and not animated and world == 1 and not args.no_alt:
         lanes = W.get("lanes") or [(ctx, stream, ds)]
-        lv_alt = [d.levels() for _, _, d in lanes]
-        n_alt = max(6, min(steps, 30))
 
-        def alt_frame(i):
-            c, st_, _ = lanes[i % len(lanes)]
-            fr, fd, fm = W["fbs"][i % len(W["fbs"])]
-            c.render_device(lv_alt[i % len(lanes)], W["cam"], cfg_alt, W["shade"], fr.data_ptr(), fd.data_ptr(),
-                            fm.data_ptr(), W["src"], -1, args.tile, 0, 1)
+        def frame_image(budgets_):
+            c0, s0, d0 = lanes[0]
+            fr, fd, fm = W["fbs"][0]
+            torch.cuda.synchronize()
+            c0.render_device(d0.levels(), W["cam"], TraceConfig(budgets_), W["shade"], fr.data_ptr(), fd.data_ptr(),
+                             fm.data_ptr(), W["src"], -1, args.tile, 0, 1)
+            torch.cuda.synchronize()
+            return fr.double().cpu().numpy(), int(fm.sum().item())
 
-        for i in range(len(lanes)):
-            alt_frame(i)
-        torch.cuda.synchronize()
-        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a0.record(stream)
-        for _, st_, _ in lanes[1:]:
-            st_.wait_event(a0)
-        for i in range(n_alt):
-            alt_frame(i)
-        for _, st_, _ in lanes[1:]:
-            stream.wait_stream(st_)
-        a1.record(stream)
-        torch.cuda.synchronize()
-        alt_ms = a0.elapsed_time(a1) / n_alt
-        alt = {"budgets": "40,20,20", "frames": n_alt, "ms_per_frame": alt_ms,
-               "value": units_per_step / (alt_ms / 1e3) / 1e6, "unit": "Mrays/s"}
+        conv = tuple(40 if b > 0 else 0 for b in budgets)
+        ref_img, ref_hits = frame_image(conv)
+        img, hits = frame_image(budgets)
+        quality = {"reference_budgets": ",".join(map(str, conv)), "hits": hits, "hits_reference": ref_hits,
+                   "hits_frac": hits / max(ref_hits, 1), "mse_vs_reference": float(np.mean((img - ref_img) ** 2)),
+                   "note": "image MSE against the same frame at budgets 40 per traced level (nsdf bench's MSE column)"}
+        if cfgw.get("speed_budgets"):
+            sb = tuple(int(x) for x in cfgw["speed_budgets"].split(","))
+            cfg_alt = TraceConfig(sb)
+            lv_alt = [d.levels() for _, _, d in lanes]
+            n_alt = max(6, min(steps, 30))
+
+            def alt_frame(i):
+                c, st_, _ = lanes[i % len(lanes)]
+                fr, fd, fm = W["fbs"][i % len(W["fbs"])]
+                c.render_device(lv_alt[i % len(lanes)], W["cam"], cfg_alt, W["shade"], fr.data_ptr(), fd.data_ptr(),
+                                fm.data_ptr(), W["src"], -1, args.tile, 0, 1)
+
+            for i in range(len(lanes)):
+                alt_frame(i)
+            torch.cuda.synchronize()
+            a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a0.record(stream)
+            for _, st_, _ in lanes[1:]:
+                st_.wait_event(a0)
+            for i in range(n_alt):
+                alt_frame(i)
+            for _, st_, _ in lanes[1:]:
+                stream.wait_stream(st_)
+            a1.record(stream)
+            torch.cuda.synchronize()
+            alt_ms = a0.elapsed_time(a1) / n_alt
+            simg, shits = frame_image(sb)
+            alt = {"budgets": cfgw["speed_budgets"], "frames": n_alt, "ms_per_frame": alt_ms,
+                   "value": units_per_step / (alt_ms / 1e3) / 1e6, "unit": "Mrays/s", "hits": shits,
+                   "hits_frac": shits / max(ref_hits, 1), "mse_vs_reference": float(np.mean((simg - ref_img) ** 2))}
 
     # HBM side of the roofline (north_star: "achieved HBM GB/s for compaction and normal
     # mapping"): the trace kernels' measured DRAM bytes per frame (ncu capture, config 2) over
@@ -900,7 +927,8 @@ def main():
                        "l2": "per-frame working set (ray state, lists, framebuffer) > 126 MB L2; weights L2-resident"},
             "fps": 1000.0 / ms_per_frame,
             "frame": frame,
-            "parity_setting": alt,
+            "frame_quality": quality,
+            "speed_setting": alt,
             "strong_scaling": strong,
             "roofline": {"bound": "tensor", "kernel": kernel, "achieved": achieved_tf, "peak": peak_tf,
                          "unit": "TFLOP/s", "frac": achieved_tf / peak_tf,
