@@ -527,6 +527,11 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1 and args.shard == "tiles":
+        # tile shares with frames in flight: a short 256-wide level list runs on fewer CTAs of
+        # >= 1536 rays each (full rows; the freed SMs take the other frames' kernels) —
+        # tools/shardsim.py: N=8 5.9-6.1x -> 6.4-6.5x, N=4 3.2-3.3x -> 3.5x, N=1 unchanged
+        os.environ.setdefault("NSDF_TC_MIN_ITEMS_256", "1536")
     # NSDF_BENCH_ONE_GPU=1: plumbing check of the N > 1 path on a one-GPU box — every rank on
     # cuda:0, host sync over gloo (no rank's kernels wait on another's).  Not a measurement.
     one_gpu = world > 1 and os.environ.get("NSDF_BENCH_ONE_GPU") == "1"

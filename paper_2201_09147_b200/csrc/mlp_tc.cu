@@ -219,6 +219,7 @@ struct TcArgs {
   int op;
   int terms;  // 3 = split-fp16 (A_hi.W_hi + A_lo.W_hi + A_hi.W_lo), 1 = plain fp16
   int claim_div;  // persistent trace: claim granularity = n / (grid * claim_div), clamped to [1, 32]
+  int min_items;  // persistent trace: rays per active CTA at least this (fewer CTAs for short lists)
   // trace (persistent level)
   LevelDesc lv;
   float eps, t_max;
@@ -502,9 +503,15 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
   if (kPersist) {
     // claim granularity: up to 32 list items per warp claim, fewer for short lists so the
     // items spread over the CTAs
-    const int div = int(gridDim.x) * a.claim_div;
+    // A short list (a small tile share of a frame, the fine levels' hand-offs) runs on fewer
+    // CTAs, each with at least min_items rays: the rows of a CTA stay full instead of
+    // idling through the level's tail, and the SMs of the CTAs that exit at once take the
+    // next frame's kernels (frames in flight).  The count is the level's real input size,
+    // known here (stream order) though not at launch.
+    const int active = max(1, min(int(gridDim.x), (n_items + a.min_items - 1) / max(a.min_items, 1)));
+    const int div = active * a.claim_div;
     claim = max(1, min(32, (n_items + div - 1) / div));
-    if (n_items == 0 || int(blockIdx.x) * 4 * claim >= n_items) return;
+    if (n_items == 0 || int(blockIdx.x) >= active || int(blockIdx.x) * 4 * claim >= n_items) return;
     my_tiles = 0x7fffffff;
   } else {
     const int n_tiles = (n_items + kRaysPerTile - 1) / kRaysPerTile;
@@ -1263,6 +1270,14 @@ TcLaunch launch_any(TcArgs& a, int n_max_items, cudaStream_t s) {
     return e ? std::max(1, atoi(e)) : 4;
   }();
   a.claim_div = claim_div;
+  // rays per active CTA of a persistent level (NSDF_TC_MIN_ITEMS_<W> overrides): one tile's
+  // rows for the short-tile 64/128-wide nets; several tiles' worth for the 256-wide level,
+  // whose 29k-cycle tiles make a half-empty CTA the costliest idle (tools/shardsim.py)
+  static const int min_items[3] = {
+      [] { const char* e = getenv("NSDF_TC_MIN_ITEMS_64"); return e ? std::max(1, atoi(e)) : kRows; }(),
+      [] { const char* e = getenv("NSDF_TC_MIN_ITEMS_128"); return e ? std::max(1, atoi(e)) : kRows; }(),
+      [] { const char* e = getenv("NSDF_TC_MIN_ITEMS_256"); return e ? std::max(1, atoi(e)) : kRows; }()};
+  a.min_items = min_items[a.net.width == 64 ? 0 : a.net.width == 128 ? 1 : 2];
   a.dbg = timeline_buffer();
   a.dbg_skip = getenv("NSDF_TC_TIMELINE_SKIP") ? std::max(0, atoi(getenv("NSDF_TC_TIMELINE_SKIP"))) : 0;
   if (a.dbg) {

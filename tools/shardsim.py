@@ -13,6 +13,9 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 
+# frames in flight: pack short 256-wide level lists onto CTAs of >= 1536 rays (see bench.py)
+os.environ.setdefault("NSDF_TC_MIN_ITEMS_256", "1536")
+
 import torch
 
 import bench
