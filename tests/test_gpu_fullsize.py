@@ -46,10 +46,20 @@ def _render(mode, path, cam, cfg, shade, members=None):
         c.close()
 
 
-@pytest.mark.parametrize("budgets", [(20, 5, 5), (40, 20, 20)])
-def test_config2_1080p(ref, budgets):
+def _torus3():
+    p = os.path.join(ASSETS, "torus3.nest")
+    if not os.path.exists(p):
+        pytest.skip("fixture missing")
+    return p
+
+
+@pytest.mark.parametrize("fixture,budgets", [("w30", (20, 5, 5)), ("w30", (40, 20, 20)), ("torus3", (40, 20, 20)),
+                                             ("torus3", (20, 5, 5))])
+def test_config2_1080p(ref, fixture, budgets):
+    """Config 2 at 1920x1080: the bench headline (torus3, reference trainer, (40,20,20)), its
+    speed setting, and the omega0 = 30 sequence at both settings."""
     from paper_2201_09147_b200.abi import ShadeConfig, TraceConfig, standard_camera
-    path = _manifest()
+    path = _torus3() if fixture == "torus3" else _manifest()
     cam = standard_camera(1920, 1080)
     cfg = TraceConfig(budgets)
     shade = ShadeConfig(specular=0.3)
@@ -234,8 +244,8 @@ def _records(recs):
     return records_np(recs)
 
 
-@pytest.mark.parametrize("budgets", [(20, 5, 5), (40, 20, 20)])
-def test_depth_outliers_are_stop_band_steps(ref, budgets):
+@pytest.mark.parametrize("fixture,budgets", [("w30", (20, 5, 5)), ("w30", (40, 20, 20)), ("torus3", (40, 20, 20))])
+def test_depth_outliers_are_stop_band_steps(ref, fixture, budgets):
     """The max |dt| above 1e-3 (p99.9 is ~1e-5): a ray whose last |f| lands within the fast
     mode's |df| ~ 1e-5 of eps_stop stops one iteration earlier or later than the reference's,
     so the two hit parameters differ by ONE final step, itself <= eps_stop + |df|.  Asserted
@@ -245,7 +255,7 @@ def test_depth_outliers_are_stop_band_steps(ref, budgets):
     from paper_2201_09147_b200.abi import TraceConfig, standard_camera
     from paper_2201_09147_b200.engine import Context, DeviceSequence
     from paper_2201_09147_b200.manifest import load_manifest
-    path = _manifest()
+    path = _torus3() if fixture == "torus3" else _manifest()
     cam = standard_camera(1920, 1080)
     cfg = TraceConfig(budgets)
     r = _records(ref.trace_image(path, cam, cfg))

@@ -9,7 +9,7 @@ tolerance the north star names (SURVEY.md §8d "Parity metrics"):
         normal kernel
 plus the oracle mode's bitwise agreement (mask, depth bits) for the same frame.
 
-    python tools/parity_report.py [--out profiles/r1_parity.json]
+    python tools/parity_report.py [--out profiles/r2_parity.json]
 Test/measurement infrastructure: reads the reference through oracle/refshim only.
 """
 import argparse
@@ -29,14 +29,16 @@ from paper_2201_09147_b200.engine import Context, DeviceSequence  # noqa: E402
 from paper_2201_09147_b200.manifest import load_manifest  # noqa: E402
 
 TORUS = os.path.join(ROOT, "assets", "torus_w30.nest")
+TORUS3 = os.path.join(ROOT, "assets", "torus3.nest")
 BLEND = os.path.join(ROOT, "assets", "blend4d_w30.nest")
 # (name, manifest, members, resolution, budgets, time, normal source: 0 own / 1 mapped)
 CASES = [
-    ("config2 1080p (20,5,5)", TORUS, None, (1920, 1080), (20, 5, 5), 0.0, 0),
-    ("config2 1080p (40,20,20)", TORUS, None, (1920, 1080), (40, 20, 20), 0.0, 0),
-    ("config1 512x512 256x3 (40)", TORUS, [2], (512, 512), (40,), 0.0, 0),
-    ("config3 1080p 64x1 (40,0), normals mapped from 256x3", TORUS, [0, 2], (1920, 1080), (40, 0), 0.0, 1),
-    ("config5 4K slice t=0.5 (20,10)", BLEND, None, (3840, 2160), (20, 10), 0.5, 0),
+    ("config2 1080p torus3 (40,20,20) [headline]", TORUS3, None, (1920, 1080), (40, 20, 20), 0.0, 0),
+    ("config2 1080p torus3 (20,5,5) [speed setting]", TORUS3, None, (1920, 1080), (20, 5, 5), 0.0, 0),
+    ("config2 1080p torus_w30 omega0=30 (40,20,20)", TORUS, None, (1920, 1080), (40, 20, 20), 0.0, 0),
+    ("config1 512x512 256x3 omega0=30 (40)", TORUS, [2], (512, 512), (40,), 0.0, 0),
+    ("config3 1080p torus3 64x1 (40,0), normals mapped from 256x3", TORUS3, [0, 2], (1920, 1080), (40, 0), 0.0, 1),
+    ("config5 4K slice t=0.5 omega0=30 (20,10)", BLEND, None, (3840, 2160), (20, 10), 0.5, 0),
 ]
 
 
