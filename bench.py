@@ -42,6 +42,7 @@ import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+sys.path.insert(1, os.path.join(ROOT, "tools"))
 
 TORUS = os.path.join(ROOT, "assets", "torus_w30.nest")   # omega0 = 30 (PyTorch fit, certified by the reference)
 TORUS3 = os.path.join(ROOT, "assets", "torus3.nest")      # reference trainer, omega0 = 10 (tools/build_assets.sh)
@@ -92,6 +93,8 @@ def parse():
                          "is the latency of one whole frame); 'frames' = every rank renders whole frames of the "
                          "frame stream (weak scaling; frames stay on their rank) and a tile-sharded pass is timed "
                          "beside it as strong_scaling.  Config 5 (animation) always shards frames")
+    ap.add_argument("--balance", type=int, default=1,
+                    help="N > 1 tile split: 1 = cost-balanced tile owners from one traced frame, 0 = tile t -> rank t %% N")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-alt", action="store_true",
@@ -613,6 +616,25 @@ def main():
             c2.set_stream(s2.cuda_stream)
             lanes.append((c2, s2, DeviceSequence(c2, seq)))
         W["lanes"] = lanes
+        # N > 1 (tiles of one frame): a cost-balanced tile map (--balance, default on) from one
+        # frame traced on rank 0 — per tile, the evaluations its pixels took at each level and
+        # its hits, weighted by the per-evaluation device time of each net (scheduler.tile_costs),
+        # assigned longest-first to the least-loaded rank — the same map on every rank
+        owners = None
+        if world > 1 and not animated and not shard_frames and args.balance:
+            obj = [None]
+            if rank == 0:
+                from conftest_free_records import records_np
+                nidx = len(seq.members) - 1 if W["src"] == 1 else max(j for j, b in enumerate(budgets) if b > 0)
+                rec = records_np(ctx.trace_image(W["levels"], W["cam"], cfg)[0])
+                costs = scheduler.tile_costs(rec["iters"], rec["hit"], Wd, Hd, args.tile,
+                                             [m.width for m in seq.members], seq.members[nidx].width)
+                obj = [scheduler.balanced_tile_owners(costs, world).tolist()]
+            dist.broadcast_object_list(obj, src=0)
+            owners = np.asarray(obj[0], np.int32)
+            for c_, _, _ in lanes:
+                c_.set_tile_owners(owners)
+        W["owners"] = owners
         # N > 1 (tiles of one frame): the ranks' shading kernels store their tiles straight
         # into rank 0's framebuffer ring over NVLink (PeerFramebuffer); NCCL tile gather only
         # if peer mapping is unavailable.
@@ -626,7 +648,7 @@ def main():
                     peer.close()
                     peer = None
             if peer is None:
-                gather = scheduler.TileGather(Wd, Hd, args.tile, rank, world)
+                gather = scheduler.TileGather(Wd, Hd, args.tile, rank, world, owners=owners)
         W["gather"], W["peer"] = gather, peer
         # frame-completion tokens: one 4-byte all-reduce per frame, all on ONE stream (tstream) in
         # frame order, each behind its frame's kernels (an event on the lane stream), so every

@@ -377,6 +377,13 @@ int nsdf_cuda_render(nsdf_ctx* ctx, const nsdf_level* levels, int m, const nsdf_
  * tile order; tile_world = 1 renders everything) into full-frame device buffers.  Pixels
  * of other tiles are left untouched.  Asynchronous on the context stream; `stats` (host,
  * may be NULL) forces a synchronize. */
+/* Explicit tile ownership for the tile-sharded renders (nsdf_cuda_render_device with
+ * tile_world > 1): owners[t] is the tile_rank that renders tile t (row-major tiles of
+ * tile_size) instead of t % tile_world — e.g. a cost-balanced assignment from a previous
+ * frame's per-tile work (scheduler.balanced_tile_owners).  The map must cover exactly the
+ * frame's tiles (else NSDF_ERR_CONFIG at render); n_tiles = 0 restores t % tile_world.
+ * Synchronizes the context stream. */
+int nsdf_cuda_set_tile_owners(nsdf_ctx* ctx, const int32_t* owners, int n_tiles);
 /* Single-process multi-GPU render: context i (its own device and stream) renders the image
  * tiles t % n == i (tile_size x tile_size, row-major tile order) with its own field handles
  * levels[i][0..m) (nsdf_cuda_replicate_field copies ctxs[0]'s weights device to device).

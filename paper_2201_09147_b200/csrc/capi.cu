@@ -146,6 +146,8 @@ struct nsdf_ctx {
   std::vector<cudaEvent_t> copy_events;  // staged pageable framebuffer copies (copy_out_frame)
   std::vector<cudaEvent_t> frame_events; // render_multi: cross-device frame ordering
   Workspace stage;   // render_multi copy path: other devices' packed pixels on this device
+  std::vector<int> tile_owners;  // nsdf_cuda_set_tile_owners (host copy); empty = t % world
+  int* d_tile_owners = nullptr;
 };
 
 namespace {
@@ -360,14 +362,21 @@ int run_frame_impl(nsdf_ctx* c, const nsdf_level* levels, int m, const nsdf_trac
   std::vector<LevelDesc> lv = traced_levels(c, levels, m, cfg, &n_counters, final_delta);
   // slots needed: every pixel, or only the pixels of the owned tiles (tile % world == rank)
   int n_max = cam ? cam->width * cam->height : n_rays;
+  const int* owners = nullptr;
   if (cam && tile_world > 1) {
     const int tx = (cam->width + tile_size - 1) / tile_size, ty = (cam->height + tile_size - 1) / tile_size;
+    const bool mapped = !c->tile_owners.empty();
+    if (mapped && int(c->tile_owners.size()) != tx * ty)
+      return fail(NSDF_ERR_CONFIG, "tile owner map covers " + std::to_string(c->tile_owners.size()) +
+                                       " tiles but the frame has " + std::to_string(tx * ty));
     long owned = 0;
-    for (int t = tile_rank; t < tx * ty; t += tile_world) {
+    for (int t = 0; t < tx * ty; ++t) {
+      if ((mapped ? c->tile_owners[size_t(t)] : t % tile_world) != tile_rank) continue;
       const int x0 = (t % tx) * tile_size, y0 = (t / tx) * tile_size;
       owned += long(std::min(tile_size, cam->width - x0)) * std::min(tile_size, cam->height - y0);
     }
     n_max = int(std::max(owned, 1L));
+    owners = mapped ? c->d_tile_owners : nullptr;
   }
   NSDF_CUDA(c->frame.reserve(frame_workspace_bytes(n_max, n_counters)));
   FrameBuffers fb = carve_frame(c->frame.base, n_max, n_counters);
@@ -379,7 +388,7 @@ int run_frame_impl(nsdf_ctx* c, const nsdf_level* levels, int m, const nsdf_trac
   cudaEvent_t ev_frame = prof ? prof->begin(s) : nullptr;
   if (cam) {
     if (tile_world <= 1) NSDF_CUDA(cudaMemcpyAsync(n_slots, &n_max, 4, cudaMemcpyHostToDevice, s));
-    launch_generate_rays(*cam, tile_size, tile_rank, tile_world, fb.st, n_slots, s);
+    launch_generate_rays(*cam, tile_size, tile_rank, tile_world, owners, fb.st, n_slots, s);
   } else {
     NSDF_CUDA(cudaMemcpyAsync(n_slots, &n_rays, 4, cudaMemcpyHostToDevice, s));
     launch_init_state_from_rays(d_rays6, n_rays, fb.st, s);
@@ -502,6 +511,23 @@ int nsdf_cuda_probe_fast_sine(nsdf_ctx* c, const float* x, int n, float* sin_out
   return NSDF_OK;
 }
 
+int nsdf_cuda_set_tile_owners(nsdf_ctx* c, const int32_t* owners, int n_tiles) {
+  if (!c || (n_tiles > 0 && !owners) || n_tiles < 0) return fail(NSDF_ERR_CONTRACT, "null argument");
+  std::lock_guard<std::mutex> lk(c->mu);
+  DeviceGuard g(c->device);
+  for (int t = 0; t < n_tiles; ++t)
+    if (owners[t] < 0) return fail(NSDF_ERR_CONFIG, "tile owners must be non-negative ranks");
+  NSDF_CUDA(cudaStreamSynchronize(c->stream));  // frames in flight may still read the old map
+  if (c->d_tile_owners) cudaFree(c->d_tile_owners);
+  c->d_tile_owners = nullptr;
+  c->tile_owners.assign(owners, owners + n_tiles);
+  if (n_tiles > 0) {
+    NSDF_CUDA(cudaMalloc(&c->d_tile_owners, size_t(n_tiles) * 4));
+    NSDF_CUDA(cudaMemcpy(c->d_tile_owners, owners, size_t(n_tiles) * 4, cudaMemcpyHostToDevice));
+  }
+  return NSDF_OK;
+}
+
 int nsdf_cuda_device_count(int* n) {
   if (!n) return fail(NSDF_ERR_CONTRACT, "null argument");
   *n = 0;
@@ -550,6 +576,7 @@ int nsdf_cuda_destroy(nsdf_ctx* c) {
     new (&c->stage) Workspace();
     for (cudaEvent_t e : c->copy_events) cudaEventDestroy(e);
     for (cudaEvent_t e : c->frame_events) cudaEventDestroy(e);
+    if (c->d_tile_owners) cudaFree(c->d_tile_owners);
     if (c->own) cudaStreamDestroy(c->own);
   }
   delete c;
@@ -1171,7 +1198,7 @@ int nsdf_cuda_generate_rays(nsdf_ctx* c, const nsdf_camera* camera, float* rays)
   size_t off = 0;
   NSDF_CUDA(c->io.reserve(size_t(n) * 24 + 4096));
   float* d = carve<float>(c->io.base, off, size_t(6) * n);
-  launch_generate_rays(cb, 1, 0, 1, fb.st, fb.counters, c->stream);
+  launch_generate_rays(cb, 1, 0, 1, nullptr, fb.st, fb.counters, c->stream);
   launch_rays_to_host_layout(fb.st, n, d, c->stream);
   NSDF_CUDA(cudaGetLastError());
   NSDF_CUDA(cudaMemcpyAsync(rays, d, size_t(n) * 24, cudaMemcpyDeviceToHost, c->stream));

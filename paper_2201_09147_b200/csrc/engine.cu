@@ -204,8 +204,8 @@ __device__ __forceinline__ void pixel_ray(const CamBasis& c, int px, int py, flo
   for (int i = 0; i < 3; ++i) d[i] = n > 0 ? __double2float_rn(__ddiv_rn(e[i], n)) : 0.0f;
 }
 
-__global__ void rays_kernel(CamBasis c, int tile_size, int tile_rank, int tile_world, RayState st,
-                            int* n_slots) {
+__global__ void rays_kernel(CamBasis c, int tile_size, int tile_rank, int tile_world, const int* owners,
+                            RayState st, int* n_slots) {
   const int npix = c.width * c.height;
   const int tiles_x = (c.width + tile_size - 1) / tile_size;
   // Whole warps iterate together so warp_append sees full masks.
@@ -216,7 +216,7 @@ __global__ void rays_kernel(CamBasis c, int tile_size, int tile_rank, int tile_w
     bool own = inside;
     if (tile_world > 1 && inside) {
       const int tile = (py / tile_size) * tiles_x + px / tile_size;
-      own = tile % tile_world == tile_rank;
+      own = (owners ? owners[tile] : tile % tile_world) == tile_rank;
     }
     int slot = pix;
     if (tile_world > 1) {
@@ -242,11 +242,11 @@ __global__ void rays_kernel(CamBasis c, int tile_size, int tile_rank, int tile_w
   }
 }
 
-void launch_generate_rays(const CamBasis& cb, int tile_size, int tile_rank, int tile_world,
+void launch_generate_rays(const CamBasis& cb, int tile_size, int tile_rank, int tile_world, const int* owners,
                           RayState st, int* n_slots_dev, cudaStream_t s) {
   const int npix = cb.width * cb.height;
   const int blocks = std::min((npix + 255) / 256, num_sms() * 8);
-  rays_kernel<<<std::max(blocks, 1), 256, 0, s>>>(cb, tile_size, tile_rank, tile_world, st, n_slots_dev);
+  rays_kernel<<<std::max(blocks, 1), 256, 0, s>>>(cb, tile_size, tile_rank, tile_world, owners, st, n_slots_dev);
 }
 
 __global__ void rays_to_host_kernel(RayState st, int n, float* rays6) {

@@ -98,7 +98,9 @@ struct TraceResult {
 // Ray generation for all pixels (world == 1, slot == pixel) or the owned image tiles.
 // Returns the number of slots on the device counter `n_slots` (host value written when
 // world == 1).
-void launch_generate_rays(const CamBasis& cb, int tile_size, int tile_rank, int tile_world,
+// `owners` (device, one entry per tile, may be null): explicit tile -> rank map instead of
+// tile % tile_world (nsdf_cuda_set_tile_owners).
+void launch_generate_rays(const CamBasis& cb, int tile_size, int tile_rank, int tile_world, const int* owners,
                           RayState st, int* n_slots_dev, cudaStream_t s);
 void launch_rays_to_host_layout(const RayState& st, int n, float* rays6, cudaStream_t s);
 void launch_init_state_from_rays(const float* rays6, int n, RayState st, cudaStream_t s);

@@ -119,6 +119,15 @@ class Context:
     def release(self, handle: int):
         check(self.lib.nsdf_cuda_release(self._ctx, handle))
 
+    def set_tile_owners(self, owners=None):
+        """nsdf_cuda_set_tile_owners: explicit tile -> rank map for tile-sharded renders
+        (None restores t % world)."""
+        if owners is None:
+            check(self.lib.nsdf_cuda_set_tile_owners(self._ctx, None, 0))
+            return
+        o = np.ascontiguousarray(owners, np.int32)
+        check(self.lib.nsdf_cuda_set_tile_owners(self._ctx, o.ctypes.data_as(_I32), len(o)))
+
     def replicate(self, handle: int, dst: "Context") -> int:
         """nsdf_cuda_replicate_field: this context's field, copied device to device into
         `dst` (the multi-GPU weight broadcast); returns the handle in dst."""

@@ -25,12 +25,49 @@ from typing import Optional
 import numpy as np
 
 
-def owned_pixels(width: int, height: int, tile: int, rank: int, world: int) -> np.ndarray:
-    """Row-major pixel indices of the tiles this rank owns (tile index row-major)."""
+def owned_pixels(width: int, height: int, tile: int, rank: int, world: int, owners=None) -> np.ndarray:
+    """Row-major pixel indices of the tiles this rank owns (tile index row-major): tile t is
+    rank t % world's, or owners[t]'s with an explicit map (nsdf_cuda_set_tile_owners)."""
     tiles_x = (width + tile - 1) // tile
     ys, xs = np.divmod(np.arange(width * height, dtype=np.int64), width)
     t = (ys // tile) * tiles_x + xs // tile
-    return np.nonzero(t % world == rank)[0]
+    return np.nonzero((t % world if owners is None else np.asarray(owners)[t]) == rank)[0]
+
+
+# Device time per evaluation of one ray at a level (picoseconds, B200, fast mode; bench.py
+# per-kernel times of the config-2 frame): the weights of a tile's predicted cost.
+EVAL_PS = {64: 47.0, 128: 187.0, 256: 997.0}
+NORMAL_PS_PER_WIDTH = {64: 190.0, 128: 760.0, 256: 4030.0}
+
+
+def tile_costs(iters: np.ndarray, hit: np.ndarray, width: int, height: int, tile: int, level_widths,
+               normal_width: int) -> np.ndarray:
+    """Predicted device time of every image tile (row-major) from a traced frame: per pixel,
+    the evaluations it took at each level (HitRecord.iterations_used, W*H x levels) times the
+    level's per-evaluation cost, plus the normal tile of a hit."""
+    w = np.array([EVAL_PS.get(int(x), 1000.0 * (int(x) / 256.0) ** 2) for x in level_widths], np.float64)
+    per_pixel = iters[:, :len(w)].astype(np.float64) @ w + hit.astype(np.float64) * NORMAL_PS_PER_WIDTH.get(
+        int(normal_width), 4030.0)
+    tiles_x = (width + tile - 1) // tile
+    ys, xs = np.divmod(np.arange(width * height, dtype=np.int64), width)
+    t = (ys // tile) * tiles_x + xs // tile
+    n_tiles = tiles_x * ((height + tile - 1) // tile)
+    return np.bincount(t, weights=per_pixel, minlength=n_tiles)
+
+
+def balanced_tile_owners(costs: np.ndarray, world: int) -> np.ndarray:
+    """Longest-processing-time assignment of tiles to ranks: tiles in decreasing predicted
+    cost, each to the currently least-loaded rank (ties: lowest rank; equal costs keep the
+    tile order) — the ranks' predicted loads end within one tile of each other."""
+    import heapq
+    order = np.argsort(-np.asarray(costs, np.float64), kind="stable")
+    heap = [(0.0, r) for r in range(world)]
+    owners = np.zeros(len(costs), np.int32)
+    for t in order:
+        load, r = heapq.heappop(heap)
+        owners[t] = r
+        heapq.heappush(heap, (load + float(costs[t]), r))
+    return owners
 
 
 def owned_frames(n_frames: int, rank: int, world: int) -> list:
@@ -111,14 +148,14 @@ class TileGather:
     remote ranks together (precomputed combined indices) — a handful of kernels, so rank 0's
     extra work does not grow with the world size."""
 
-    def __init__(self, width: int, height: int, tile: int, rank: int, world: int, device=None):
+    def __init__(self, width: int, height: int, tile: int, rank: int, world: int, device=None, owners=None):
         import torch
 
         self.rank, self.world = rank, world
         if device is None:
             device = torch.device("cuda", torch.cuda.current_device()) if torch.cuda.is_available() else "cpu"
         self.device = device
-        idx = [torch.from_numpy(owned_pixels(width, height, tile, r, world)) for r in range(world)]
+        idx = [torch.from_numpy(owned_pixels(width, height, tile, r, world, owners)) for r in range(world)]
         self.n = [int(i.numel()) for i in idx]
         self.n_max = max(self.n)
         self.idx = idx[rank].to(device)

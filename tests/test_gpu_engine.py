@@ -20,18 +20,28 @@ def _seq():
 
 
 @pytest.mark.parametrize("mode", ["fp32", "fp16"])
-@pytest.mark.parametrize("world,tile", [(2, 64), (3, 32), (8, 16)])
-def test_tile_sharded_ranks_reassemble_the_frame(mode, world, tile):
-    """Each simulated rank renders only its tiles (t % world == rank) into its own device
-    framebuffer, exactly as bench.py's ranks do; the packed-tile gather (scheduler.py) is
-    emulated by the same index sets.  The union must equal the single-GPU frame bitwise."""
+@pytest.mark.parametrize("world,tile,balanced", [(2, 64, False), (3, 32, False), (8, 16, False), (3, 16, True),
+                                                 (8, 32, True)])
+def test_tile_sharded_ranks_reassemble_the_frame(mode, world, tile, balanced):
+    """Each simulated rank renders only its tiles (t % world == rank, or the cost-balanced
+    owner map of scheduler.balanced_tile_owners set with nsdf_cuda_set_tile_owners) into its
+    own device framebuffer, exactly as bench.py's ranks do; the packed-tile gather
+    (scheduler.py) is emulated by the same index sets.  The union must equal the single-GPU
+    frame bitwise."""
     import torch
     from paper_2201_09147_b200.abi import ShadeConfig, TraceConfig, standard_camera
     from paper_2201_09147_b200.engine import Context, DeviceSequence
-    from paper_2201_09147_b200.scheduler import owned_pixels
+    from paper_2201_09147_b200.scheduler import balanced_tile_owners, owned_pixels, tile_costs
+    from conftest import records_np
     ctx = Context(0, mode)
     ds = DeviceSequence(ctx, _seq())
     W, H = 200, 120
+    owners = None
+    if balanced:
+        rec = records_np(ctx.trace_image(ds.levels(), standard_camera(W, H), TraceConfig((20, 5, 5)))[0])
+        costs = tile_costs(rec["iters"], rec["hit"], W, H, tile, [64, 128, 256], 256)
+        owners = balanced_tile_owners(costs, world)
+        ctx.set_tile_owners(owners)
     cam = standard_camera(W, H)
     cfg = TraceConfig((20, 5, 5))
     shade = ShadeConfig(specular=0.3)
@@ -50,7 +60,7 @@ def test_tile_sharded_ranks_reassemble_the_frame(mode, world, tile):
         ctx.render_device(ds.levels(), cam, cfg, shade, *(b.data_ptr() for b in mine), tile_size=tile,
                           tile_rank=rank, tile_world=world)
         torch.cuda.synchronize()
-        idx = torch.from_numpy(owned_pixels(W, H, tile, rank, world)).cuda()
+        idx = torch.from_numpy(owned_pixels(W, H, tile, rank, world, owners)).cuda()
         # untouched pixels keep the sentinel, owned pixels are written
         others = torch.ones(n, dtype=torch.bool, device="cuda")
         others[idx] = False
@@ -61,6 +71,12 @@ def test_tile_sharded_ranks_reassemble_the_frame(mode, world, tile):
     for a, b in zip(out, full):
         assert torch.equal(a.view(torch.uint8) if a.dtype != torch.uint8 else a,
                            b.view(torch.uint8) if b.dtype != torch.uint8 else b)
+    if balanced:  # a map for another tiling is a config error, not a silent mis-render
+        from paper_2201_09147_b200.abi import NsdfError
+        with pytest.raises(NsdfError):
+            ctx.render_device(ds.levels(), cam, cfg, shade, *(b.data_ptr() for b in bufs()), tile_size=tile * 2,
+                              tile_rank=0, tile_world=world)
+        ctx.set_tile_owners(None)
     ctx.close()
 
 

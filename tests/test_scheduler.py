@@ -207,3 +207,30 @@ def test_gloo_world2_job_rate_is_max_over_ranks():
         p.join(timeout=60)
     for _, rate, job_ms in got:
         assert job_ms == 20.0 and abs(rate - 7000.0 / 0.020) < 1e-6
+
+
+def test_balanced_tile_owners_lpt():
+    """Cost-balanced tile map (longest processing time first): every tile gets one rank in
+    [0, world), the ranks' loads end within one tile's cost of each other, and the map is
+    deterministic; tile_costs sums per-pixel work per row-major tile."""
+    from paper_2201_09147_b200.scheduler import balanced_tile_owners, tile_costs
+    rng = np.random.default_rng(5)
+    costs = rng.gamma(0.5, 10.0, size=2040)
+    for world in (2, 3, 8):
+        owners = balanced_tile_owners(costs, world)
+        assert owners.shape == costs.shape and owners.min() >= 0 and owners.max() < world
+        loads = np.bincount(owners, weights=costs, minlength=world)
+        assert loads.max() - loads.min() <= costs.max() + 1e-9
+        static = np.bincount(np.arange(len(costs)) % world, weights=costs, minlength=world)
+        assert loads.max() <= static.max() + 1e-9
+        assert np.array_equal(owners, balanced_tile_owners(costs, world))
+    W, H, T = 70, 33, 16
+    iters = np.zeros((W * H, 8), np.uint16)
+    iters[:, 0] = 2
+    iters[5, 1] = 3
+    hit = np.zeros(W * H, np.int32)
+    hit[W * 20 + 40] = 1
+    c = tile_costs(iters, hit, W, H, T, [64, 256], 256)
+    assert c.shape == (5 * 3,)
+    assert np.isclose(c.sum(), W * H * 2 * 47.0 + 3 * 997.0 + 4030.0)
+    assert np.isclose(c[0], T * T * 2 * 47.0 + 3 * 997.0)

@@ -30,6 +30,8 @@ ap.add_argument("--frames", type=int, default=30)
 ap.add_argument("--worlds", default="1,2,4,8")
 ap.add_argument("--tile", type=int, default=32)
 ap.add_argument("--profile", action="store_true", help="per-level serial launch times of the slowest rank")
+ap.add_argument("--balanced", action="store_true",
+                help="cost-balanced tile owners (scheduler.balanced_tile_owners from one traced frame) instead of t % N")
 args = ap.parse_args()
 
 cfgw = bench.CONFIGS[args.config]
@@ -67,8 +69,20 @@ def run(rank, world, frames):
     return e0.elapsed_time(e1) / frames
 
 
+costs = None
+if args.balanced:
+    from conftest_free_records import records_np  # noqa: E402  (tools-local copy of the HitRecord view)
+    from paper_2201_09147_b200.scheduler import balanced_tile_owners, tile_costs  # noqa: E402
+    rec = records_np(lanes[0][0].trace_image(lanes[0][2], cam, cfg)[0])
+    costs = tile_costs(rec["iters"], rec["hit"], w, h, args.tile, [m.width for m in seq.members],
+                       seq.members[-1].width if src == 0 else seq.members[-1].width)
+
 base = None
 for world in [int(x) for x in args.worlds.split(",")]:
+    if costs is not None:
+        owners = balanced_tile_owners(costs, world) if world > 1 else None
+        for c, _, _, _ in lanes:
+            c.set_tile_owners(owners)
     per = []
     for rank in range(world):
         run(rank, world, 3)
