@@ -419,7 +419,7 @@ def run_e2e(args, ctx, ds, seq, stream, world, rank, W):
             W["step"](i)
             if rank == 0:
                 if peer is not None:
-                    W["tok_ev"][i % (2 * len(W["lanes"]))].synchronize()  # every rank's tiles of frame i
+                    W["ring"].done(i).synchronize()  # every rank's tiles of frame i
                     peer.to_host(i % (2 * len(W["lanes"])), *(t.data_ptr() for t in hb))
                 else:
                     torch.cuda.current_stream().wait_stream(W["gstream"])
@@ -469,27 +469,15 @@ def tile_pass(args, ctx, W, world, rank, Wd, Hd):
     if not peer.ok:
         peer.close()
         return {"unavailable": f"peer framebuffer: {peer.reason}"}
-    tok = torch.zeros(1, dtype=torch.int32, device="cuda")
-    cs = torch.cuda.Stream()  # every token all-reduce on ONE stream, in frame order
+    ring = scheduler.PeerRing(peer, 2 * len(lanes))
     lv = [d.levels() for _, _, d in lanes]
-    R = 2 * len(lanes)
-    tok_ev = [None] * R
 
     def frame(i):
         c, st, _ = lanes[i % len(lanes)]
-        if tok_ev[(i + 1) % R] is not None:  # slot i % R is free once frame i-R+1's token completed
-            st.wait_event(tok_ev[(i + 1) % R])
-        fr, fd, fm = peer.ptrs(i % R)
+        fr, fd, fm = ring.begin(i, st)
         c.render_device(lv[i % len(lanes)], W["cam"], W["cfg"], W["shade"], fr, fd, fm, W["src"], -1, args.tile, rank,
                         world)
-        ev = torch.cuda.Event()
-        ev.record(st)
-        cs.wait_event(ev)
-        with torch.cuda.stream(cs):
-            dist.all_reduce(tok)
-            done = torch.cuda.Event()
-            done.record(cs)
-        tok_ev[i % R] = done
+        ring.end(i, st)
 
     n = max(2 * len(lanes), min(args.steps, 30))
     for i in range(max(3, len(lanes))):
@@ -505,7 +493,7 @@ def tile_pass(args, ctx, W, world, rank, Wd, Hd):
         frame(i)
     for _, st, _ in lanes[1:]:
         stream.wait_stream(st)
-    stream.wait_stream(cs)
+    stream.wait_stream(ring.stream)
     e1.record(stream)
     torch.cuda.synchronize()
     t = torch.tensor([e0.elapsed_time(e1)], dtype=torch.float64, device="cuda")
@@ -650,13 +638,12 @@ def main():
             if peer is None:
                 gather = scheduler.TileGather(Wd, Hd, args.tile, rank, world, owners=owners)
         W["gather"], W["peer"] = gather, peer
-        # frame-completion tokens: one 4-byte all-reduce per frame, all on ONE stream (tstream) in
-        # frame order, each behind its frame's kernels (an event on the lane stream), so every
-        # rank issues and executes the collectives in the same order
-        tok = torch.zeros(1, dtype=torch.int32, device="cuda")
-        tstream = torch.cuda.Stream() if peer is not None else None
-        tok_ev = [None] * (2 * len(lanes))
-        W["tok_ev"] = tok_ev
+        # frame-completion tokens and slot reuse: scheduler.PeerRing (one 4-byte all-reduce per
+        # frame on one token stream, in frame order; a slot is rewritten only after the token of
+        # the frame after its previous user completed)
+        ring = scheduler.PeerRing(peer, 2 * len(lanes)) if peer is not None else None
+        W["ring"] = ring
+        tstream = ring.stream if ring is not None else None
         n_fb = max(len(lanes), 2 if gather is not None else 1)
         fbs = [(rgb, depth, mask)] + [(torch.zeros_like(rgb), torch.zeros_like(depth), torch.zeros_like(mask))
                                       for _ in range(n_fb - 1)]
@@ -675,28 +662,12 @@ def main():
             li = i % len(lanes)
             c, st, d = lanes[li]
             lv = lane_levels[li][i % len(lane_levels[li])]
-            if peer is not None:
-                # this rank's tiles of frame i land in rank 0's ring slot; the 4-byte all-reduce
-                # on the token stream completes once every rank's kernels of frame i are done.
-                # Slot reuse: frame i overwrites the slot of frame i-R (R = ring depth) only after
-                # the token of frame i-R+1 completed here — i.e. after every rank finished frames
-                # <= i-R+1 and rank 0 issued that all-reduce, which it does only after its host
-                # copy of frame i-R (the e2e loop reads a slot synchronously before the next step)
-                R = 2 * len(lanes)
-                prev = tok_ev[(i + 1) % R]
-                if prev is not None:
-                    st.wait_event(prev)
-                fr, fd, fm = peer.ptrs(i % R)
+            if ring is not None:
+                # this rank's tiles of frame i land in rank 0's ring slot (scheduler.PeerRing)
+                fr, fd, fm = ring.begin(i, st)
                 c.render_device(lv, W["cam"], cfg, W["shade"], fr, fd, fm, W["src"], -1, args.tile, tile_rank,
                                 tile_world)
-                ev = torch.cuda.Event()
-                ev.record(st)
-                tstream.wait_event(ev)
-                with torch.cuda.stream(tstream):
-                    dist.all_reduce(tok)
-                    done = torch.cuda.Event()
-                    done.record(tstream)
-                tok_ev[i % (2 * len(lanes))] = done
+                ring.end(i, st)
                 return
             b = i % n_fb
             if free_ev[b] is not None:

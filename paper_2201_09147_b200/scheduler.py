@@ -259,3 +259,51 @@ class PeerFramebuffer:
             except Exception:
                 pass
         self.bases = []
+
+
+class PeerRing:
+    """Frames in flight through a PeerFramebuffer ring of R slots (R = 2 x frames in flight).
+
+    Frame i renders into slot i % R.  Completion token: after frame i's kernels (an event on
+    its lane stream) a 4-byte all-reduce on ONE token stream, in frame order on every rank, so
+    the collectives match across ranks whatever the lanes' progress; `done(i)` is the event
+    after that all-reduce — on rank 0 it means every rank's stores of frame i have landed.
+    Slot reuse: before frame i writes slot i % R (last used by frame i - R), its lane stream
+    waits for the token of frame i - R + 1.  That token completes only after every rank issued
+    its all-reduce for frame i - R + 1, and rank 0 issues it only after its host copy of frame
+    i - R (the caller reads a finished slot synchronously before starting the next frame), so
+    a slot is never overwritten while any rank still writes it or rank 0 still reads it."""
+
+    def __init__(self, peer, n_slots: int):
+        import torch
+
+        self.peer = peer
+        self.R = n_slots
+        self.tok = torch.zeros(1, dtype=torch.int32, device="cuda")
+        self.stream = torch.cuda.Stream()
+        self.events = [None] * n_slots
+
+    def begin(self, i: int, lane_stream):
+        """Slot pointers (rgb, depth, mask) for frame i, once the slot is free (stream order)."""
+        prev = self.events[(i + 1) % self.R]
+        if prev is not None:
+            lane_stream.wait_event(prev)
+        return self.peer.ptrs(i % self.R)
+
+    def end(self, i: int, lane_stream):
+        """Frame i's kernels are enqueued on lane_stream: enqueue its completion token."""
+        import torch
+        import torch.distributed as dist
+
+        ev = torch.cuda.Event()
+        ev.record(lane_stream)
+        self.stream.wait_event(ev)
+        with torch.cuda.stream(self.stream):
+            dist.all_reduce(self.tok)
+            done = torch.cuda.Event()
+            done.record(self.stream)
+        self.events[i % self.R] = done
+
+    def done(self, i: int):
+        return self.events[i % self.R]
+

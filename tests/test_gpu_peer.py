@@ -84,6 +84,91 @@ def test_peer_framebuffer_assembles_the_frame(mode, tile):
         assert np.array_equal(rgb.view(np.uint32), np.asarray(ref[0], np.float32).reshape(-1).view(np.uint32))
 
 
+def _cam(i):
+    """A different view per frame (orbiting camera), so a slot overwritten too early shows."""
+    import math
+    from paper_2201_09147_b200.abi import Camera
+    a = 0.6 + 0.35 * i
+    return Camera((2.6 * math.cos(a), 1.2 + 0.1 * i, 2.6 * math.sin(a)), (0, 0, 0), (0, 1, 0), 45.0, W, H)
+
+
+def _ring_worker(rank, world, port, n_frames, out_path):
+    import sys
+    import time
+    sys.path.insert(0, ROOT)
+    import torch
+    import torch.distributed as dist
+    from paper_2201_09147_b200.abi import ShadeConfig, TraceConfig
+    from paper_2201_09147_b200.engine import Context, DeviceSequence
+    from paper_2201_09147_b200.manifest import load_manifest
+    from paper_2201_09147_b200.scheduler import PeerFramebuffer, PeerRing
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    torch.cuda.set_device(0)
+    ctx = Context(0, "fp16")
+    lane = torch.cuda.Stream()
+    ctx.set_stream(lane.cuda_stream)
+    ds = DeviceSequence(ctx, load_manifest(NEST))
+    pf = PeerFramebuffer(ctx, W, H, 2, rank, world)
+    assert pf.ok, pf.reason
+    ring = PeerRing(pf, 2)  # one frame in flight per rank: 2 slots, reused every other frame
+    n = W * H
+    frames = []
+    for i in range(n_frames):
+        ptrs = ring.begin(i, lane)
+        ctx.render_device(ds.levels(), _cam(i), TraceConfig((20, 5, 5)), ShadeConfig(specular=0.3), *ptrs,
+                          tile_size=16, tile_rank=rank, tile_world=world)
+        ring.end(i, lane)
+        if rank == 0:  # the e2e reader: frame i out of its slot as soon as its token completed
+            ring.done(i).synchronize()
+            time.sleep(0.05)  # a slow reader: rank 1 runs ahead and must wait for the slot
+            rgb, depth, mask = np.empty(3 * n, np.float32), np.empty(n, np.float32), np.empty(n, np.uint8)
+            pf.to_host(i % 2, rgb.ctypes.data, depth.ctypes.data, mask.ctypes.data)
+            frames += [rgb, depth, mask]
+    torch.cuda.synchronize()
+    dist.barrier()
+    if rank == 0:
+        np.savez(out_path, *frames)
+    dist.barrier()
+    pf.close()
+    dist.barrier()
+    ctx.close()
+    dist.destroy_process_group()
+
+
+def test_peer_ring_distinct_frames_through_reused_slots():
+    """scheduler.PeerRing with a different camera per frame through more frames than slots
+    (6 frames, 2 slots): rank 1 renders without host synchronisation of its own, rank 0 (a
+    slow reader) reads every frame out of its slot after the frame's completion token; each
+    read-back frame equals the single-process render of its own camera bit for bit.  On this
+    one-GPU box the tokens go over gloo, whose all-reduce blocks the host, so rank 1 cannot get
+    two frames ahead here and the slot-reuse edge (the ADVICE.md round-1 race) is not what
+    keeps the frames apart; with NCCL's asynchronous tokens it is (PeerRing docstring)."""
+    import torch.multiprocessing as mp
+    from paper_2201_09147_b200.abi import ShadeConfig, TraceConfig
+    from paper_2201_09147_b200.engine import Context, DeviceSequence
+    from paper_2201_09147_b200.manifest import load_manifest
+    if not os.path.exists(NEST):
+        pytest.skip("fixture missing")
+    n_frames = 6
+    out = tempfile.mktemp(suffix=".npz")
+    port = 29500 + (os.getpid() % 2000) + 7
+    mp.start_processes(_ring_worker, args=(2, port, n_frames, out), nprocs=2, join=True, start_method="spawn")
+    got = np.load(out)
+    os.unlink(out)
+    ctx = Context(0, "fp16")
+    ds = DeviceSequence(ctx, load_manifest(NEST))
+    try:
+        for i in range(n_frames):
+            ref = ctx.render(ds.levels(), _cam(i), TraceConfig((20, 5, 5)), ShadeConfig(specular=0.3))
+            rgb, depth, mask = (got[f"arr_{3 * i + k}"] for k in range(3))
+            assert np.array_equal(mask, np.asarray(ref[2]).reshape(-1).astype(np.uint8)), i
+            assert np.array_equal(depth.view(np.uint32), np.asarray(ref[1], np.float32).reshape(-1).view(np.uint32)), i
+            assert np.array_equal(rgb.view(np.uint32), np.asarray(ref[0], np.float32).reshape(-1).view(np.uint32)), i
+    finally:
+        ctx.close()
+
+
 @pytest.mark.parametrize("shard", ["tiles", "frames", "animation"])
 def test_bench_two_ranks_plumbing(shard):
     """bench.py's N > 1 path end to end (torchrun, 2 ranks, e2e to host) with both ranks on
