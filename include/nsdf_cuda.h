@@ -217,6 +217,16 @@ const char* nsdf_cuda_last_error(void);
  * argument to revolutions, MUFU.SIN evaluates the fraction) — for x[0..n) (host buffers).
  * tests/test_gpu_fast.py bounds its error at the largest omega0 * z the fixtures produce. */
 int nsdf_cuda_probe_fast_sine(nsdf_ctx* ctx, const float* x, int n, float* sin_out, float* cos_out);
+/* Checked build (libnsdf_cuda.so built with NSDF_CHECKED=1, paper_2201_09147_b200/_checked/):
+ * the number of out-of-bounds list indices, ray slots, staged appends and framebuffer pixels
+ * the device kernels detected (and skipped) since the last reset, with the first one's site
+ * (1 list read, 2 slot, 3 CTA staging, 4 list write, 5 pixel), value and bound;
+ * *checked_build = 0 and *count = 0 in the normal build.  Synchronizes the context stream. */
+int nsdf_cuda_check_report(nsdf_ctx* ctx, int reset, uint64_t* count, int32_t* site, int32_t* value,
+                           int32_t* bound, int32_t* checked_build);
+/* Positive control for the checked build: one deliberate out-of-bounds check on the device
+ * (count + 1 in the checked build, no effect otherwise). */
+int nsdf_cuda_check_selftest(nsdf_ctx* ctx);
 /* Number of visible CUDA devices (NSDF_ERR_DEVICE when there is none). */
 int nsdf_cuda_device_count(int* n);
 int nsdf_cuda_create(int device, nsdf_ctx** out);

@@ -54,8 +54,16 @@ def _headers(d):
     return [os.path.join(d, f) for f in os.listdir(d) if f.endswith((".cuh", ".h", ".hpp"))]
 
 
-def build_cuda(force=False, verbose=False):
-    os.makedirs(OBJ, exist_ok=True)
+CHECKED_DIR = os.path.join(PKG, "_checked")
+
+
+def build_cuda(force=False, verbose=False, checked=False):
+    """checked=True: the bounds-checked variant (-DNSDF_CHECKED=1, common.cuh) into
+    _checked/libnsdf_cuda.so — every list index, ray slot, staged append and framebuffer pixel
+    of the kernels checked on the device (tests/test_gpu_checked.py loads it through
+    NSDF_CUDA_LIB)."""
+    obj_dir = os.path.join(PKG, "_obj_checked") if checked else OBJ
+    os.makedirs(obj_dir, exist_ok=True)
     deps_common = _headers(CSRC) + [os.path.join(INC, "nsdf_cuda.h")]
     jobs = []
     objs = []
@@ -67,8 +75,10 @@ def build_cuda(force=False, verbose=False):
             extra = extra + os.environ["NSDF_TC_DEFINES"].split()
         if src != "mlp_tc.cu" and os.environ.get("NSDF_ENGINE_DEFINES"):
             extra = extra + os.environ["NSDF_ENGINE_DEFINES"].split()
+        if checked:
+            extra = extra + ["-DNSDF_CHECKED=1"]
         s = os.path.join(CSRC, src)
-        o = os.path.join(OBJ, src + ".o")
+        o = os.path.join(obj_dir, src + ".o")
         objs.append(o)
         if force or _stale(o, [s] + deps_common):
             cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-ffp-contract=off",
@@ -79,7 +89,9 @@ def build_cuda(force=False, verbose=False):
     if verbose:
         for o in outs:
             print(o)
-    lib = os.path.join(PKG, "libnsdf_cuda.so")
+    if checked:
+        os.makedirs(CHECKED_DIR, exist_ok=True)
+    lib = os.path.join(CHECKED_DIR if checked else PKG, "libnsdf_cuda.so")
     if force or jobs or _stale(lib, objs):
         _run([NVCC, *ARCH, "-shared", "-cudart=static", "-o", lib, *objs])
     return lib
@@ -161,6 +173,7 @@ def build_tools(force=False):
 
 def build(force=False, verbose=False):
     build_cuda(force, verbose)
+    build_cuda(force, verbose, checked=True)
     build_host(force)
     build_cpp_tests(force)
     build_tools(force)

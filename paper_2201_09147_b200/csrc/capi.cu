@@ -380,6 +380,7 @@ int run_frame_impl(nsdf_ctx* c, const nsdf_level* levels, int m, const nsdf_trac
   }
   NSDF_CUDA(c->frame.reserve(frame_workspace_bytes(n_max, n_counters)));
   FrameBuffers fb = carve_frame(c->frame.base, n_max, n_counters);
+  fb.st.n_pix = cam ? cam->width * cam->height : n_rays;
   cudaStream_t s = c->stream;
   NSDF_CUDA(cudaMemsetAsync(fb.counters, 0, size_t(n_counters) * 4, s));
   int* n_slots = fb.counters;
@@ -525,6 +526,33 @@ int nsdf_cuda_set_tile_owners(nsdf_ctx* c, const int32_t* owners, int n_tiles) {
     NSDF_CUDA(cudaMalloc(&c->d_tile_owners, size_t(n_tiles) * 4));
     NSDF_CUDA(cudaMemcpy(c->d_tile_owners, owners, size_t(n_tiles) * 4, cudaMemcpyHostToDevice));
   }
+  return NSDF_OK;
+}
+
+int nsdf_cuda_check_report(nsdf_ctx* c, int reset, uint64_t* count, int32_t* site, int32_t* value, int32_t* bound,
+                           int32_t* checked_build) {
+  if (!c || !count) return fail(NSDF_ERR_CONTRACT, "null argument");
+  std::lock_guard<std::mutex> lk(c->mu);
+  DeviceGuard g(c->device);
+  NSDF_CUDA(cudaStreamSynchronize(c->stream));
+  CheckRecord r[2];
+  NSDF_CUDA(check_report_engine(&r[0], reset != 0));
+  NSDF_CUDA(check_report_tc(&r[1], reset != 0));
+  const CheckRecord& first = r[0].count ? r[0] : r[1];
+  *count = r[0].count + r[1].count;
+  if (site) *site = first.site;
+  if (value) *value = first.value;
+  if (bound) *bound = first.bound;
+  if (checked_build) *checked_build = NSDF_CHECKED;
+  return NSDF_OK;
+}
+
+int nsdf_cuda_check_selftest(nsdf_ctx* c) {
+  if (!c) return fail(NSDF_ERR_CONTRACT, "null argument");
+  std::lock_guard<std::mutex> lk(c->mu);
+  DeviceGuard g(c->device);
+  NSDF_CUDA(launch_check_selftest(c->stream));
+  NSDF_CUDA(cudaStreamSynchronize(c->stream));
   return NSDF_OK;
 }
 

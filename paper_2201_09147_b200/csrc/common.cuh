@@ -64,6 +64,8 @@ struct RayState {
   float* final_dist;
   uint8_t* hit;
   int* pixel;           // image pixel of the slot (render/trace_image); null = identity
+  int cap;              // slot capacity (the length of every per-slot array and list)
+  int n_pix;            // framebuffer pixels (W*H) the slots' pixels index
 };
 
 // ---------------------------------------------------------------------------------
@@ -222,15 +224,56 @@ __device__ __forceinline__ void analytic_grad(const DevField& f, double x, doubl
   else g[2] = sgn(z);
 }
 
-// Warp-aggregated append of `pred` lanes to a global list (one atomic per warp).
-__device__ __forceinline__ void warp_append(bool pred, int value, int* list, int* count) {
+// ---------------------------------------------------------------------------------
+// Checked build (NSDF_CHECKED=1: build.py build_cuda(checked=True) ->
+// paper_2201_09147_b200/_checked/libnsdf_cuda.so).  Every list index, ray slot, staged
+// append and framebuffer pixel the kernels compute is bounds-checked on the device: a
+// violation is counted (the first one's site, value and bound recorded, per translation
+// unit) and the access skipped, so tests can assert a clean run
+// (nsdf_cuda_check_report; tests/test_gpu_checked.py).  Compiled out otherwise.
+// ---------------------------------------------------------------------------------
+#ifndef NSDF_CHECKED
+#define NSDF_CHECKED 0
+#endif
+enum CheckSite : int {
+  kChkListRead = 1,   // list item index < list length
+  kChkSlot = 2,       // ray slot < slot capacity
+  kChkStage = 3,      // CTA staging index < staging capacity
+  kChkListWrite = 4,  // compaction / flush write index < list capacity
+  kChkPixel = 5,      // framebuffer pixel < W*H
+};
+struct CheckRecord {
+  unsigned long long count;
+  int site, value, bound, pad;
+};
+#if NSDF_CHECKED
+static __device__ CheckRecord g_check;
+#endif
+__device__ __forceinline__ bool in_bounds(long long v, long long bound, int site) {
+#if NSDF_CHECKED
+  if (v >= 0 && v < bound) return true;
+  if (atomicAdd(&g_check.count, 1ull) == 0ull) {
+    g_check.site = site;
+    g_check.value = int(v);
+    g_check.bound = int(bound);
+  }
+  return false;
+#else
+  (void)v, (void)bound, (void)site;
+  return true;
+#endif
+}
+
+// Warp-aggregated append of `pred` lanes to a global list of `cap` entries (one atomic per warp).
+__device__ __forceinline__ void warp_append(bool pred, int value, int* list, int* count, int cap = 0x7fffffff) {
   const unsigned mask = __ballot_sync(0xffffffffu, pred);
   if (mask == 0) return;
   const int lane = threadIdx.x & 31;
   int base = 0;
   if (lane == __ffs(mask) - 1) base = atomicAdd(count, __popc(mask));
   base = __shfl_sync(0xffffffffu, base, __ffs(mask) - 1);
-  if (pred) list[base + __popc(mask & ((1u << lane) - 1u))] = value;
+  const int at = base + __popc(mask & ((1u << lane) - 1u));
+  if (pred && in_bounds(at, cap, kChkListWrite)) list[at] = value;
 }
 
 }  // namespace nsdf_b200

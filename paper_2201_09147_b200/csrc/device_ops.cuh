@@ -107,6 +107,7 @@ __device__ __forceinline__ void shade_and_write(const ShadeParams& sp, const Ray
   float c[3];
   shade_point(sp, st.px[slot], st.py[slot], st.pz[slot], n[0], n[1], n[2], c);
   const int p = st.pixel[slot];
+  if (!in_bounds(p, st.n_pix, kChkPixel)) return;
   rgb[size_t(3) * p + 0] = c[0];
   rgb[size_t(3) * p + 1] = c[1];
   rgb[size_t(3) * p + 2] = c[2];

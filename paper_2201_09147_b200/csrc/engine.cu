@@ -123,6 +123,8 @@ FrameBuffers carve_frame(void* base, int n_rays, int n_counters) {
     return r;
   };
   FrameBuffers fb;
+  fb.st.cap = int(n);
+  fb.st.n_pix = int(n);  // callers with a camera set the frame's W*H
   fb.st.px = reinterpret_cast<float*>(take(n * 4));
   fb.st.py = reinterpret_cast<float*>(take(n * 4));
   fb.st.pz = reinterpret_cast<float*>(take(n * 4));
@@ -229,7 +231,7 @@ __global__ void rays_kernel(CamBasis c, int tile_size, int tile_rank, int tile_w
       }
       slot = b + __popc(mask & ((1u << lane) - 1u));
     }
-    if (!own) continue;
+    if (!own || !in_bounds(slot, st.cap, kChkSlot)) continue;
     float d[3];
     pixel_ray(c, px, py, d);
     st.px[slot] = c.origin[0];
@@ -352,7 +354,8 @@ __global__ void __launch_bounds__(kT) trace_iter_simt(IterArgs a) {
   for (int base = blockIdx.x * kTileCols; base < n; base += gridDim.x * kTileCols) {
     const int cnt = min(kTileCols, n - base);
     if (tid < kTileCols) {
-      const int slot = tid < cnt ? a.in_list[base + tid] : -1;
+      int slot = tid < cnt && in_bounds(base + tid, a.st.cap, kChkListRead) ? a.in_list[base + tid] : -1;
+      if (slot >= 0 && !in_bounds(slot, a.st.cap, kChkSlot)) slot = -1;
       slots[tid] = slot;
       pts[tid] = slot >= 0 ? a.st.px[slot] : 0.0f;
       pts[kTileCols + tid] = slot >= 0 ? a.st.py[slot] : 0.0f;
@@ -365,8 +368,8 @@ __global__ void __launch_bounds__(kT) trace_iter_simt(IterArgs a) {
       const int slot = slots[tid];
       bool conv = false, cont = false;
       if (slot >= 0) trace_update(a, slot, vals[tid], conv, cont);
-      warp_append(conv, slot, a.adv_list, a.adv_count);
-      warp_append(cont, slot, a.next_list, a.next_count);
+      warp_append(conv, slot, a.adv_list, a.adv_count, a.st.cap);
+      warp_append(cont, slot, a.next_list, a.next_count, a.st.cap);
     }
     __syncthreads();
   }
@@ -461,7 +464,8 @@ TraceResult run_trace(Mode mode, const std::vector<LevelDesc>& levels, float eps
 
 __global__ void mark_hits_kernel(const int* list, const int* count, RayState st) {
   const int n = *count;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) st.hit[list[i]] = 1;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    if (in_bounds(list[i], st.cap, kChkSlot)) st.hit[list[i]] = 1;
 }
 
 void launch_mark_hits(const int* list, const int* count, int n_max, RayState st, cudaStream_t s) {
@@ -497,6 +501,7 @@ __global__ void fb_background_kernel(RayState st, const int* n_slots, ShadeParam
   const int n = *n_slots;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
     const int p = st.pixel[i];
+    if (!in_bounds(p, st.n_pix, kChkPixel)) continue;
     rgb[size_t(3) * p + 0] = sp.background[0];
     rgb[size_t(3) * p + 1] = sp.background[1];
     rgb[size_t(3) * p + 2] = sp.background[2];
@@ -574,6 +579,7 @@ __device__ __forceinline__ void write_pixel(const NormalArgs& a, int slot, const
   const float px = a.st.px[slot], py = a.st.py[slot], pz = a.st.pz[slot];
   shade_point(a.sp, px, py, pz, n[0], n[1], n[2], c);
   const int p = a.st.pixel[slot];
+  if (!in_bounds(p, a.st.n_pix, kChkPixel)) return;
   a.rgb[size_t(3) * p + 0] = c[0];
   a.rgb[size_t(3) * p + 1] = c[1];
   a.rgb[size_t(3) * p + 2] = c[2];
@@ -596,7 +602,8 @@ __global__ void __launch_bounds__(kT) normals_shade_simt(NormalArgs a) {
   for (int base = blockIdx.x * kRays; base < n; base += gridDim.x * kRays) {
     const int cnt = min(kRays, n - base);
     if (tid < kRays) {
-      const int slot = tid < cnt ? a.list[base + tid] : -1;
+      int slot = tid < cnt && in_bounds(base + tid, a.st.cap, kChkListRead) ? a.list[base + tid] : -1;
+      if (slot >= 0 && !in_bounds(slot, a.st.cap, kChkSlot)) slot = -1;
       slots[tid] = slot;
       pts[tid] = slot >= 0 ? a.st.px[slot] : 0.0f;
       pts[kRays + tid] = slot >= 0 ? a.st.py[slot] : 0.0f;
@@ -618,7 +625,7 @@ __global__ void __launch_bounds__(kT) normals_shade_simt(NormalArgs a) {
         }
         if (!defer) write_pixel(a, slot, nrm);
       }
-      warp_append(defer, slot, a.fb_list, a.fb_count);
+      warp_append(defer, slot, a.fb_list, a.fb_count, a.st.cap);
     }
     __syncthreads();
   }
@@ -864,6 +871,31 @@ void launch_raycast_mesh(const CamBasis& cb, const float* tri_verts, int n_tri, 
                          cudaStream_t s) {
   const int npix = cb.width * cb.height;
   raycast_mesh_kernel<<<(npix + 255) / 256, 256, 0, s>>>(cb, tri_verts, n_tri, positions, mask);
+}
+
+// Positive control of the checked build: one deliberate out-of-bounds index (-1 of 1).
+__global__ void check_selftest_kernel() {
+  if (threadIdx.x == 0 && blockIdx.x == 0) (void)in_bounds(-1, 1, kChkSlot);
+}
+
+cudaError_t launch_check_selftest(cudaStream_t s) {
+  check_selftest_kernel<<<1, 32, 0, s>>>();
+  return cudaGetLastError();
+}
+
+cudaError_t check_report_engine(CheckRecord* out, bool reset) {
+#if NSDF_CHECKED
+  if (cudaError_t e = cudaMemcpyFromSymbol(out, g_check, sizeof(CheckRecord))) return e;
+  if (reset) {
+    const CheckRecord zero{};
+    return cudaMemcpyToSymbol(g_check, &zero, sizeof(CheckRecord));
+  }
+  return cudaSuccess;
+#else
+  (void)reset;
+  *out = CheckRecord{};
+  return cudaSuccess;
+#endif
 }
 
 }  // namespace nsdf_b200

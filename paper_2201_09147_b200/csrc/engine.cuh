@@ -211,4 +211,10 @@ struct KernelCfg {
 KernelCfg kernel_cfg(const void* kernel, int threads, size_t smem, bool max_carveout = false);
 int device_sms();  // multiprocessors of the current device
 
+// Checked-build violation records of the engine / tensor-core translation units (zero in the
+// normal build); `reset` clears them.
+cudaError_t check_report_engine(CheckRecord* out, bool reset);
+cudaError_t check_report_tc(CheckRecord* out, bool reset);
+cudaError_t launch_check_selftest(cudaStream_t s);  // one deliberate violation (positive control)
+
 }  // namespace nsdf_b200

@@ -341,7 +341,8 @@ struct RowIn {
 __device__ __forceinline__ int load_slot(const TcArgs& a, int item, int n_items) {
   if (item >= n_items) return -1;
   if (a.op == kOpEval || a.op == kOpNormalMap) return item;
-  return __ldg(a.in_list + item);
+  const int slot = __ldg(a.in_list + item);
+  return in_bounds(slot, a.st.cap, kChkSlot) ? slot : -1;
 }
 
 __device__ __forceinline__ RowIn load_row(const TcArgs& a, int slot) {
@@ -415,29 +416,34 @@ __device__ __forceinline__ void stage_append(bool pred, int value, StageList s) 
   int base = 0;
   if (lane == leader) base = atomicAdd(s.count, __popc(mask));
   base = __shfl_sync(0xffffffffu, base, leader);
-  if (pred) s.buf[base + __popc(mask & ((1u << lane) - 1u))] = value;
+  const int at = base + __popc(mask & ((1u << lane) - 1u));
+  if (pred && in_bounds(at, kStageCap, kChkStage)) s.buf[at] = value;
 }
 
 // Flush body for callers that already synchronised the appends (the count is uniform).
-__device__ __forceinline__ void stage_flush_now(StageList s, int* list, int* gcount, int* gbase, int ctid) {
-  const int n = *s.count;
+// `cap`: capacity of the destination list.
+__device__ __forceinline__ void stage_flush_now(StageList s, int* list, int* gcount, int* gbase, int ctid, int cap) {
+  const int n = min(*s.count, kStageCap);
   if (ctid == 0) *gbase = atomicAdd(gcount, n);
   named_bar(2, 128);
   const int base = *gbase;
-  for (int i = ctid; i < n; i += 128) list[base + i] = s.buf[i];
+  for (int i = ctid; i < n; i += 128)
+    if (in_bounds(base + i, cap, kChkListWrite)) list[base + i] = s.buf[i];
   named_bar(2, 128);
   if (ctid == 0) *s.count = 0;
 }
 
 // Called by the 128 consumer threads (named barrier 2) after a tile's appends.
-__device__ __forceinline__ void stage_flush(StageList s, int* list, int* gcount, int* gbase, int ctid, bool force) {
+__device__ __forceinline__ void stage_flush(StageList s, int* list, int* gcount, int* gbase, int ctid, bool force,
+                                            int cap) {
   named_bar(2, 128);
-  const int n = *s.count;
+  const int n = min(*s.count, kStageCap);
   if (n == 0 || (!force && n <= kStageCap - kRows)) return;  // uniform decision
   if (ctid == 0) *gbase = atomicAdd(gcount, n);
   named_bar(2, 128);
   const int base = *gbase;
-  for (int i = ctid; i < n; i += 128) list[base + i] = s.buf[i];
+  for (int i = ctid; i < n; i += 128)
+    if (in_bounds(base + i, cap, kChkListWrite)) list[base + i] = s.buf[i];
   named_bar(2, 128);
   if (ctid == 0) *s.count = 0;
 }
@@ -938,9 +944,9 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
           }
           const int k = min(__popc(need), res_end - res_base);
           const int r = __popc(need & lt);
-          if (((need >> lane) & 1u) && r < k) {
+          if (((need >> lane) & 1u) && r < k && in_bounds(res_base + r, n_items, kChkListRead)) {
             pf_slot = __ldg(a.in_list + res_base + r);
-            pf_stage = kPfListed;
+            if (in_bounds(pf_slot, st.cap, kChkSlot)) pf_stage = kPfListed;
           }
           res_base += k;
           need = __ballot_sync(0xffffffffu, pf_stage == kPfNeed);
@@ -967,7 +973,7 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
         // one barrier per tile: the live-row vote also orders every warp's staged appends of
         // the previous tile before the flush decision below
         const bool live = bar_vote_any(3, 128 * kGroups, g0 && slot >= 0);
-        if (g0 && *sm.stage_count > kStageCap - kRows) stage_flush_now(st_adv, a.adv_list, a.adv_count, sm.stage_base, ctid);
+        if (g0 && *sm.stage_count > kStageCap - kRows) stage_flush_now(st_adv, a.adv_list, a.adv_count, sm.stage_base, ctid, st.cap);
         if (!live) {
           // no live row: either prefetches are still in flight (refill again) or done
           if (g0) append_pending();
@@ -1041,7 +1047,7 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
         }
       }
       if (g0) {
-        stage_flush(st_adv, a.adv_list, a.adv_count, sm.stage_base, ctid, true);
+        stage_flush(st_adv, a.adv_list, a.adv_count, sm.stage_base, ctid, true, st.cap);
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) evals += __shfl_xor_sync(0xffffffffu, evals, o);
         if (lane == 0 && evals) atomicAdd(a.evals, evals);
@@ -1080,7 +1086,7 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
                 }
                 if (!defer) shade_and_write(a.sp, a.st, now.slot, nrm, a.rgb, a.depth, a.mask);
               }
-              warp_append(defer, now.slot, a.fb_list, a.fb_count);
+              warp_append(defer, now.slot, a.fb_list, a.fb_count, a.st.cap);
             } else if (a.op == kOpNormalMap) {
               bool outside = false, fell_back = false;
               if (lead) {
@@ -1403,6 +1409,21 @@ cudaError_t launch_fast_sine_probe(const float* x, int n, float* s, float* c, cu
   if (n <= 0) return cudaSuccess;
   fast_sine_probe_kernel<<<std::min((n + 255) / 256, 148 * 8), 256, 0, st>>>(x, n, s, c);
   return cudaGetLastError();
+}
+
+cudaError_t check_report_tc(CheckRecord* out, bool reset) {
+#if NSDF_CHECKED
+  if (cudaError_t e = cudaMemcpyFromSymbol(out, g_check, sizeof(CheckRecord))) return e;
+  if (reset) {
+    const CheckRecord zero{};
+    return cudaMemcpyToSymbol(g_check, &zero, sizeof(CheckRecord));
+  }
+  return cudaSuccess;
+#else
+  (void)reset;
+  *out = CheckRecord{};
+  return cudaSuccess;
+#endif
 }
 
 }  // namespace nsdf_b200
