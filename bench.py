@@ -449,11 +449,31 @@ def run_e2e(args, ctx, ds, seq, stream, world, rank, W):
             ctx.render(levels, cam, cfg, shade, src)
         pg_ms = (time.perf_counter() - w0) * 1e3 / n_pg
         pageable = {"value": npix / (pg_ms / 1e3) / 1e6, "unit": "Mrays/s", "ms_per_frame": pg_ms, "frames": n_pg,
-                    "path": "nsdf_cuda_render into pageable host arrays (ImageBuffer-shaped), 1 thread, 1 frame "
+                    "path": "nsdf_cuda_render into fresh numpy arrays (pageable, lazily mapped), 1 thread, 1 frame "
                             "in flight"}
+    # The reference's own call: C++ shading::render(seq, cam, cfg) -> ImageBuffer (the drop-in
+    # library, libnsdf_b200.so), one frame at a time as `nsdf bench` does, after a warm-up
+    dropin = None
+    if rank == 0 and world == 1 and not frame_times and not W["gbuffer"]:
+        import ctypes
+        from paper_2201_09147_b200 import certify
+        man = sub_manifest(args)
+        try:
+            sec = ctypes.c_double()
+            st = certify._lib().nsdf_host_bench_render(man.encode(), ctypes.c_double(0.0), ctypes.byref(cam),
+                                                       ctypes.byref(cfg), ctypes.byref(shade), src, -1, 2,
+                                                       max(3, min(steps, 10)), ctypes.byref(sec))
+            if st == 0:
+                dropin = {"value": npix / sec.value / 1e6, "unit": "Mrays/s", "ms_per_frame": sec.value * 1e3,
+                          "path": "C++ nsdf::shading::render -> ImageBuffer (libnsdf_b200.so, the reference API; "
+                                  "the GPU renders while the ImageBuffer is allocated), 1 frame in flight"}
+            else:
+                dropin = {"unavailable": certify._lib().nsdf_host_last_error().decode()}
+        finally:
+            os.unlink(man)
     return {"value": npix * frames / (e_ms / 1e3) / 1e6, "unit": "Mrays/s", "ms_per_frame": e_ms / frames,
             "h2d_bytes_per_step": level_bytes, "d2h_bytes_per_step": npix * (12 + 4 + 1), "path": path,
-            "pageable": pageable}
+            "pageable": pageable, "dropin": dropin}
 
 
 def tile_pass(args, ctx, W, world, rank, Wd, Hd):

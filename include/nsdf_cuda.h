@@ -382,6 +382,15 @@ int nsdf_cuda_render(nsdf_ctx* ctx, const nsdf_level* levels, int m, const nsdf_
                      const nsdf_trace_config* trace, const nsdf_shade_config* shade,
                      int normal_source, int fine_index, float* rgb, float* depth, uint8_t* mask,
                      nsdf_frame_stats* stats);
+/* The same frame in two calls: begin validates and enqueues the whole frame into the
+ * context's device framebuffer and returns at once; end (synchronous) copies it into the
+ * caller's HOST buffers — so a caller can allocate and zero its framebuffer (the reference's
+ * ImageBuffer is value-initialised std::vector storage) while the GPU renders.  One frame in
+ * flight per context; end reports the frame's errors (e.g. the deferred light check). */
+int nsdf_cuda_render_begin(nsdf_ctx* ctx, const nsdf_level* levels, int m, const nsdf_camera* camera,
+                           const nsdf_trace_config* trace, const nsdf_shade_config* shade,
+                           int normal_source, int fine_index);
+int nsdf_cuda_render_end(nsdf_ctx* ctx, float* rgb, float* depth, uint8_t* mask, nsdf_frame_stats* stats);
 /* Device framebuffer variant used by the frame/tile scheduler: renders the pixels of the
  * image tiles t with t % tile_world == tile_rank (tile_size x tile_size tiles, row-major
  * tile order; tile_world = 1 renders everything) into full-frame device buffers.  Pixels

@@ -19,6 +19,12 @@ int nsdf_host_render_manifest(const char* manifest, double time, const nsdf_came
                               const nsdf_trace_config* trace, const nsdf_shade_config* shade,
                               int normal_source, int fine_index, float* rgb, float* depth,
                               uint8_t* mask);
+/* The reference-shaped caller timed: shading::render(seq, cam, cfg) into a fresh ImageBuffer
+ * (pageable, value-initialised), `warmup` untimed frames then the mean seconds per frame of
+ * `repeats` frames — the `nsdf bench` row timing with a warm-up. */
+int nsdf_host_bench_render(const char* manifest, double time, const nsdf_camera* camera,
+                           const nsdf_trace_config* trace, const nsdf_shade_config* shade, int normal_source,
+                           int fine_index, int warmup, int repeats, double* seconds_per_frame);
 int nsdf_host_trace_image_manifest(const char* manifest, double time, const nsdf_camera* camera,
                                    const nsdf_trace_config* trace, nsdf_hit_record* out);
 int nsdf_host_forward_and_gradient(const char* sdfnet, const float* points, int k, float* dist,

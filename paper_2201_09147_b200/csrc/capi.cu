@@ -131,6 +131,8 @@ struct BatchPipe {
   }
 };
 
+struct PendingFrame;  // nsdf_cuda_render_begin's frame in flight (defined with the render entry points)
+
 struct nsdf_ctx {
   int device = 0;
   cudaStream_t own = nullptr;
@@ -148,6 +150,8 @@ struct nsdf_ctx {
   Workspace stage;   // render_multi copy path: other devices' packed pixels on this device
   std::vector<int> tile_owners;  // nsdf_cuda_set_tile_owners (host copy); empty = t % world
   int* d_tile_owners = nullptr;
+  std::unique_ptr<PendingFrame> pending;  // nsdf_cuda_render_begin .. _end
+  ~nsdf_ctx();
 };
 
 namespace {
@@ -1809,32 +1813,102 @@ int copy_out_frame(nsdf_ctx* c, const std::vector<std::pair<void*, const void*>>
 
 extern "C" {
 
+}  // extern "C"
+
+// Split form of nsdf_cuda_render: begin enqueues the whole frame into the context's device
+// framebuffer and returns; end copies it into the caller's host buffers.  A caller can
+// allocate (and zero) its host framebuffer while the GPU renders — the reference API's
+// ImageBuffer is value-initialised std::vector storage (shading.hpp:22-34).
+struct PendingFrame {
+  bool active = false;
+  size_t n = 0;
+  float* drgb = nullptr;
+  float* ddepth = nullptr;
+  uint8_t* dmask = nullptr;
+  LightCheck lc;
+  nsdf_frame_stats stats{};
+  bool want_stats = false;
+};
+
+nsdf_ctx::~nsdf_ctx() = default;
+
+namespace {
+
+int render_begin_locked(nsdf_ctx* c, const nsdf_level* levels, int m, const nsdf_camera* camera,
+                        const nsdf_trace_config* trace, const nsdf_shade_config* shade, int normal_source,
+                        int fine_index, bool want_stats, PendingFrame* pf) {
+  CamBasis cb;
+  ShadeParams sp;
+  if (int st = render_checks(c, levels, m, camera, trace, shade, normal_source, fine_index, &cb, &sp, &pf->lc))
+    return st;
+  pf->want_stats = want_stats || pf->lc.status != NSDF_OK;  // the deferred light check needs the hit count
+  const size_t n = size_t(cb.width) * cb.height;
+  size_t off = 0;
+  NSDF_CUDA(c->io.reserve(n * 17 + 8192));
+  pf->n = n;
+  pf->drgb = carve<float>(c->io.base, off, 3 * n);
+  pf->ddepth = carve<float>(c->io.base, off, n);
+  pf->dmask = carve<uint8_t>(c->io.base, off, n);
+  FrameOut fo;
+  fo.d_rgb = pf->drgb;
+  fo.d_depth = pf->ddepth;
+  fo.d_mask = pf->dmask;
+  PendingStats ps;
+  if (int st = run_frame(c, levels, m, trace, &cb, nullptr, 0, &sp, normal_source, fine_index, 1, 0, 1, fo, nullptr,
+                         0.0f, pf->want_stats ? &ps : nullptr))
+    return st;
+  if (pf->want_stats) {
+    NSDF_CUDA(cudaStreamSynchronize(c->stream));
+    finish_stats(ps, &pf->stats);
+  }
+  pf->active = true;
+  return NSDF_OK;
+}
+
+int render_end_locked(nsdf_ctx* c, PendingFrame* pf, float* rgb, float* depth, uint8_t* mask, nsdf_frame_stats* stats) {
+  if (!pf->active) return fail(NSDF_ERR_CONTRACT, "no frame in flight (nsdf_cuda_render_begin first)");
+  pf->active = false;
+  if (pf->lc.status && pf->stats.hits > 0) return fail(pf->lc.status, pf->lc.msg);
+  if (stats) *stats = pf->stats;
+  const size_t n = pf->n;
+  return copy_out_frame(c, {{rgb, pf->drgb}, {depth, pf->ddepth}, {mask, pf->dmask}}, {3 * n * 4, n * 4, n});
+}
+
+}  // namespace
+
+extern "C" {
+
 int nsdf_cuda_render(nsdf_ctx* c, const nsdf_level* levels, int m, const nsdf_camera* camera,
                      const nsdf_trace_config* trace, const nsdf_shade_config* shade, int normal_source,
                      int fine_index, float* rgb, float* depth, uint8_t* mask, nsdf_frame_stats* stats) {
   if (!c || !rgb || !depth || !mask) return fail(NSDF_ERR_CONTRACT, "null argument");
   std::lock_guard<std::mutex> lk(c->mu);
   DeviceGuard g(c->device);
-  CamBasis cb;
-  ShadeParams sp;
-  LightCheck lc;
-  if (int st = render_checks(c, levels, m, camera, trace, shade, normal_source, fine_index, &cb, &sp, &lc)) return st;
-  nsdf_frame_stats local;
-  if (lc.status && !stats) stats = &local;  // the deferred light check needs the hit count
-  const size_t n = size_t(cb.width) * cb.height;
-  size_t off = 0;
-  NSDF_CUDA(c->io.reserve(n * 17 + 8192));
-  float* drgb = carve<float>(c->io.base, off, 3 * n);
-  float* ddepth = carve<float>(c->io.base, off, n);
-  uint8_t* dmask = carve<uint8_t>(c->io.base, off, n);
-  FrameOut fo;
-  fo.d_rgb = drgb;
-  fo.d_depth = ddepth;
-  fo.d_mask = dmask;
-  if (int st = run_frame(c, levels, m, trace, &cb, nullptr, 0, &sp, normal_source, fine_index, 1, 0, 1, fo, stats))
+  PendingFrame pf;
+  if (int st = render_begin_locked(c, levels, m, camera, trace, shade, normal_source, fine_index, stats != nullptr,
+                                   &pf))
     return st;
-  if (lc.status && stats->hits > 0) return fail(lc.status, lc.msg);
-  return copy_out_frame(c, {{rgb, drgb}, {depth, ddepth}, {mask, dmask}}, {3 * n * 4, n * 4, n});
+  return render_end_locked(c, &pf, rgb, depth, mask, stats);
+}
+
+int nsdf_cuda_render_begin(nsdf_ctx* c, const nsdf_level* levels, int m, const nsdf_camera* camera,
+                           const nsdf_trace_config* trace, const nsdf_shade_config* shade, int normal_source,
+                           int fine_index) {
+  if (!c) return fail(NSDF_ERR_CONTRACT, "null argument");
+  std::lock_guard<std::mutex> lk(c->mu);
+  DeviceGuard g(c->device);
+  if (c->pending && c->pending->active) return fail(NSDF_ERR_CONTRACT, "a frame is already in flight on this context");
+  if (!c->pending) c->pending = std::make_unique<PendingFrame>();
+  *c->pending = PendingFrame{};
+  return render_begin_locked(c, levels, m, camera, trace, shade, normal_source, fine_index, false, c->pending.get());
+}
+
+int nsdf_cuda_render_end(nsdf_ctx* c, float* rgb, float* depth, uint8_t* mask, nsdf_frame_stats* stats) {
+  if (!c || !rgb || !depth || !mask) return fail(NSDF_ERR_CONTRACT, "null argument");
+  std::lock_guard<std::mutex> lk(c->mu);
+  DeviceGuard g(c->device);
+  if (!c->pending) return fail(NSDF_ERR_CONTRACT, "no frame in flight (nsdf_cuda_render_begin first)");
+  return render_end_locked(c, c->pending.get(), rgb, depth, mask, stats);
 }
 
 }  // extern "C"

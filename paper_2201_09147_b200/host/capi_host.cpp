@@ -1,6 +1,8 @@
 // extern "C" entry points into the drop-in C++ API, so tests and bench.py can drive the
 // reference-shaped call chain (load_manifest -> shading::render / tracer::trace_image ->
 // C ABI -> B200) in-process through ctypes.  Declared in include/nsdf_host.h.
+#include <algorithm>
+#include <chrono>
 #include <cstring>
 #include <filesystem>
 #include <string>
@@ -96,6 +98,28 @@ int nsdf_host_render_manifest(const char* manifest, double time, const nsdf_came
     std::memcpy(rgb, img.rgb.data(), img.rgb.size() * sizeof(float));
     std::memcpy(depth, img.depth.data(), img.depth.size() * sizeof(float));
     std::memcpy(mask, img.mask.data(), img.mask.size());
+    return NSDF_OK;
+  } catch (const std::exception& e) {
+    return fail_from(e);
+  }
+}
+
+int nsdf_host_bench_render(const char* manifest, double time, const nsdf_camera* camera,
+                           const nsdf_trace_config* trace, const nsdf_shade_config* shade, int normal_source,
+                           int fine_index, int warmup, int repeats, double* seconds_per_frame) {
+  try {
+    const auto seq = sequence_of(manifest, time);
+    shading::RenderConfig cfg;
+    cfg.trace = trace_of(trace);
+    cfg.shade = shade_of(shade);
+    cfg.normal_source = normal_source == NSDF_NORMALS_MAPPED ? shading::NormalSource::mapped : shading::NormalSource::own;
+    cfg.mapped_fine_index = fine_index;
+    const tracer::Camera cam = camera_of(camera);
+    for (int i = 0; i < warmup; ++i) (void)shading::render(seq, cam, cfg);
+    const auto t0 = std::chrono::steady_clock::now();
+    for (int i = 0; i < repeats; ++i) (void)shading::render(seq, cam, cfg);
+    *seconds_per_frame =
+        std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() / std::max(repeats, 1);
     return NSDF_OK;
   } catch (const std::exception& e) {
     return fail_from(e);

@@ -52,15 +52,17 @@ ImageBuffer render(const NestedSequence& seq, const Camera& camera, const Render
   const nsdf_camera cam = detail::to_pod(camera);
   const nsdf_trace_config tc = detail::to_pod(config.trace);
   const nsdf_shade_config sc = detail::to_pod(config.shade);
-  ImageBuffer img(camera.width, camera.height);
   const int src = config.normal_source == NormalSource::mapped ? NSDF_NORMALS_MAPPED : NSDF_NORMALS_OWN;
   const auto& ctxs = engine::contexts();
   if (ctxs.size() == 1) {
-    engine::check(nsdf_cuda_render(ctxs[0], levels.data(), int(levels.size()), &cam, &tc, &sc, src,
-                                   config.mapped_fine_index, img.rgb.data(), img.depth.data(), img.mask.data(),
-                                   nullptr));
+    // the frame renders while the ImageBuffer (35 MB at 1080p, value-initialised) is allocated
+    engine::check(nsdf_cuda_render_begin(ctxs[0], levels.data(), int(levels.size()), &cam, &tc, &sc, src,
+                                         config.mapped_fine_index));
+    ImageBuffer img(camera.width, camera.height);
+    engine::check(nsdf_cuda_render_end(ctxs[0], img.rgb.data(), img.depth.data(), img.mask.data(), nullptr));
     return img;
   }
+  ImageBuffer img(camera.width, camera.height);
   // NSDF_DEVICES: the frame's tiles over every listed GPU (weights replicated once per field)
   std::vector<std::vector<nsdf_level>> per(ctxs.size(), levels);
   std::vector<const nsdf_level*> lp(ctxs.size());
