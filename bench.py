@@ -756,6 +756,12 @@ def main():
         prof = ctx.get_profile()
         ctx.set_profiling(False)
         prof_kind = "CUDA events around each launch, serial pass (1 frame in flight) after the timed region"
+    # single-frame latency (one frame in flight: rays .. framebuffer; at N > 1 the slowest
+    # rank's share of a tile-split frame) beside the frames-in-flight throughput
+    lat = torch.tensor([prof.frame_ms / max(prof.frames, 1)], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(lat, op=dist.ReduceOp.MAX)
+    frame_latency_ms = float(lat.item())
     # job throughput: units over ALL ranks / the slowest rank's device time (max over ranks)
     if animated or W["gbuffer"] or shard_frames:
         my_units = units_per_step * steps                          # this rank's frames / G-buffer
@@ -944,6 +950,7 @@ def main():
                         else "NCCL tile gather"),
                        "l2": "per-frame working set (ray state, lists, framebuffer) > 126 MB L2; weights L2-resident"},
             "fps": 1000.0 / ms_per_frame,
+            "frame_latency_ms": None if W["gbuffer"] else frame_latency_ms,
             "frame": frame,
             "frame_quality": quality,
             "speed_setting": alt,

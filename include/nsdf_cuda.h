@@ -227,6 +227,10 @@ int nsdf_cuda_check_report(nsdf_ctx* ctx, int reset, uint64_t* count, int32_t* s
 /* Positive control for the checked build: one deliberate out-of-bounds check on the device
  * (count + 1 in the checked build, no effect otherwise). */
 int nsdf_cuda_check_selftest(nsdf_ctx* ctx);
+/* Diagnostics: forget the per-(device, kernel) launch configuration (the dynamic-SMEM opt-in
+ * and occupancy), so the next launch on every device takes the configuration path again —
+ * how a test exercises the per-device setup on a one-GPU box. */
+int nsdf_cuda_reset_kernel_config(void);
 /* Number of visible CUDA devices (NSDF_ERR_DEVICE when there is none). */
 int nsdf_cuda_device_count(int* n);
 int nsdf_cuda_create(int device, nsdf_ctx** out);

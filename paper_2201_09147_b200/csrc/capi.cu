@@ -560,6 +560,11 @@ int nsdf_cuda_check_selftest(nsdf_ctx* c) {
   return NSDF_OK;
 }
 
+int nsdf_cuda_reset_kernel_config(void) {
+  reset_kernel_cfg();
+  return NSDF_OK;
+}
+
 int nsdf_cuda_device_count(int* n) {
   if (!n) return fail(NSDF_ERR_CONTRACT, "null argument");
   *n = 0;

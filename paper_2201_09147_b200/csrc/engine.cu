@@ -156,18 +156,28 @@ int device_sms() {
 
 static int num_sms() { return device_sms(); }
 
+namespace {
+// The SMEM opt-in is ONE value per (device, kernel): raised to the largest size any launch
+// needed so far (a smaller request must not lower it under another caller's cached size).
+struct KernelCfgEntry {
+  size_t configured = 0;
+  std::map<std::pair<int, size_t>, KernelCfg> by_launch;  // (threads, smem)
+};
+std::mutex g_cfg_mu;
+std::map<std::pair<int, const void*>, KernelCfgEntry> g_cfg_cache;
+}  // namespace
+
+void reset_kernel_cfg() {
+  std::lock_guard<std::mutex> lk(g_cfg_mu);
+  g_cfg_cache.clear();
+}
+
 KernelCfg kernel_cfg(const void* kernel, int threads, size_t smem, bool max_carveout) {
   int dev = 0;
   cudaGetDevice(&dev);
-  // The SMEM opt-in is ONE value per (device, kernel): raised to the largest size any launch
-  // needed so far (a smaller request must not lower it under another caller's cached size).
-  struct Entry {
-    size_t configured = 0;
-    std::map<std::pair<int, size_t>, KernelCfg> by_launch;  // (threads, smem)
-  };
-  static std::mutex mu;
-  static std::map<std::pair<int, const void*>, Entry> cache;
-  std::lock_guard<std::mutex> lk(mu);
+  using Entry = KernelCfgEntry;
+  auto& cache = g_cfg_cache;
+  std::lock_guard<std::mutex> lk(g_cfg_mu);
   Entry& e = cache[{dev, kernel}];
   KernelCfg k;
   if (smem > e.configured) {

@@ -209,6 +209,7 @@ struct KernelCfg {
   int regs = 0;       // registers per thread
 };
 KernelCfg kernel_cfg(const void* kernel, int threads, size_t smem, bool max_carveout = false);
+void reset_kernel_cfg();  // forget every cached configuration (the next launches redo the opt-in)
 int device_sms();  // multiprocessors of the current device
 
 // Checked-build violation records of the engine / tensor-core translation units (zero in the

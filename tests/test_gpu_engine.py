@@ -258,6 +258,38 @@ def test_kernel_path_stats():
             c.close()
 
 
+def test_every_new_context_takes_the_configuration_path():
+    """The kernel launch configuration (dynamic-SMEM opt-in > 48 KB for the 128/256-wide
+    tiles, occupancy) is per device: with the cache cleared before each new context, every
+    context configures the kernels itself — first a small launch then a large one of the same
+    kernel (f64 evaluator: 64- then 256-wide), then the reverse order in the next context, whose
+    smaller request must not lower the opt-in under the cached larger one — and its frame runs
+    tcgen05 on every level."""
+    from paper_2201_09147_b200 import abi
+    from paper_2201_09147_b200.abi import ShadeConfig, TraceConfig, standard_camera
+    from paper_2201_09147_b200.engine import Context, DeviceSequence
+    seq = _seq()
+    lib = abi.load_library()
+    ref = None
+    for order in ((64, 256), (256, 64), (128, 64)):
+        assert lib.nsdf_cuda_reset_kernel_config() == 0
+        c = Context(0, "fp16")
+        try:
+            for w in order:
+                net = random_net(w, 1 if w == 64 else 2, seed=w)
+                h = c.upload(net)
+                d, g = c.eval_f64(h, np.random.default_rng(w).uniform(-1, 1, (3, 777)))
+                assert np.isfinite(d).all() and np.isfinite(g).all()
+            out = c.render(DeviceSequence(c, seq).levels(), standard_camera(96, 64), TraceConfig((20, 5, 5)),
+                           ShadeConfig(specular=0.3))
+            _assert_paths(out[3], 3, "fp16")
+            if ref is None:
+                ref = out
+            assert np.array_equal(out[1].view(np.uint32), ref[1].view(np.uint32))
+        finally:
+            c.close()
+
+
 def test_contexts_on_many_threads_all_run_tcgen05():
     """Contexts created and used from concurrent host threads (the launch-attribute cache is
     per device and locked): every thread's first frame runs the tcgen05 kernels (the 128- and
