@@ -1501,7 +1501,7 @@ int nsdf_cuda_render_device(nsdf_ctx* c, const nsdf_level* levels, int m, const 
   fo.d_rgb = d_rgb;
   fo.d_depth = d_depth;
   fo.d_mask = d_mask;
-  nsdf_frame_stats local;
+  nsdf_frame_stats local{};
   if (int st = run_frame(c, levels, m, trace, &cb, nullptr, 0, &sp, normal_source, fine_index, tile_size, tile_rank,
                          tile_world, fo, stats ? stats : lc.status ? &local : nullptr))
     return st;
@@ -1597,7 +1597,7 @@ int nsdf_cuda_render_multi(nsdf_ctx* const* ctxs, int n, const nsdf_level* const
     if (int st = render_checks(ctxs[i], levels[i], m, camera, trace, shade, normal_source, fine_index, &cb, &sp, &lc))
       return st;
   }
-  nsdf_frame_stats local;
+  nsdf_frame_stats local{};
   if (lc.status && !stats) stats = &local;  // the deferred light check needs the hit count
   const size_t np = size_t(cb.width) * cb.height;
   const int tx = (cb.width + tile_size - 1) / tile_size, ty = (cb.height + tile_size - 1) / tile_size;
@@ -1889,6 +1889,8 @@ int nsdf_cuda_render(nsdf_ctx* c, const nsdf_level* levels, int m, const nsdf_ca
   if (!c || !rgb || !depth || !mask) return fail(NSDF_ERR_CONTRACT, "null argument");
   std::lock_guard<std::mutex> lk(c->mu);
   DeviceGuard g(c->device);
+  if (c->pending && c->pending->active)
+    return fail(NSDF_ERR_CONTRACT, "a frame is in flight on this context (nsdf_cuda_render_end first)");
   PendingFrame pf;
   if (int st = render_begin_locked(c, levels, m, camera, trace, shade, normal_source, fine_index, stats != nullptr,
                                    &pf))

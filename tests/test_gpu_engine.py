@@ -345,6 +345,47 @@ def test_empty_light_list_matches_reference(oracle_built, tmp_path):
         assert e.value.status == ERR_CONTRACT and "light" in str(e.value)
         with pytest.raises(Exception):
             refshim.render(p, toward, TraceConfig((20, 5, 5)), shade)
+        # the same over two contexts (render_multi) and through the split render
+        from paper_2201_09147_b200.engine import render_multi
+        c2 = Context(0, "fp32")
+        try:
+            lv = [ds.levels(), ds.replicate(c2).levels()]
+            rgb2, depth2, mask2 = render_multi([c, c2], lv, away, TraceConfig((20, 5, 5)), shade, tile_size=8)
+            assert np.array_equal(rgb2, want[0]) and not mask2.any()
+            with pytest.raises(NsdfError) as e:
+                render_multi([c, c2], lv, toward, TraceConfig((20, 5, 5)), shade, tile_size=8)
+            assert e.value.status == ERR_CONTRACT
+        finally:
+            c2.close()
+    finally:
+        c.close()
+
+
+def test_split_render_begin_end():
+    """nsdf_cuda_render_begin / _end equal nsdf_cuda_render; one frame in flight per context
+    (a second begin, or a plain render in between, is a contract error)."""
+    import ctypes
+    from paper_2201_09147_b200.abi import ERR_CONTRACT, FrameStats, ShadeConfig, TraceConfig, standard_camera
+    from paper_2201_09147_b200.engine import Context, DeviceSequence, _levels
+    c = Context(0, "fp16")
+    try:
+        ds = DeviceSequence(c, _seq())
+        cam, cfg, shade = standard_camera(120, 80), TraceConfig((40, 20, 20)), ShadeConfig(specular=0.3)
+        ref = c.render(ds.levels(), cam, cfg, shade)
+        lv, m = _levels(ds.levels())
+        assert c.lib.nsdf_cuda_render_begin(c._ctx, lv, m, ctypes.byref(cam), ctypes.byref(cfg), ctypes.byref(shade),
+                                            0, -1) == 0
+        assert c.lib.nsdf_cuda_render_begin(c._ctx, lv, m, ctypes.byref(cam), ctypes.byref(cfg), ctypes.byref(shade),
+                                            0, -1) == ERR_CONTRACT
+        n = cam.width * cam.height
+        rgb, depth, mask = np.zeros(3 * n, np.float32), np.zeros(n, np.float32), np.zeros(n, np.uint8)
+        fp = ctypes.POINTER(ctypes.c_float)
+        st = FrameStats()
+        assert c.lib.nsdf_cuda_render_end(c._ctx, rgb.ctypes.data_as(fp), depth.ctypes.data_as(fp),
+                                          mask.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)), ctypes.byref(st)) == 0
+        assert np.array_equal(rgb.reshape(ref[0].shape), ref[0]) and np.array_equal(mask.reshape(ref[2].shape), ref[2])
+        assert c.lib.nsdf_cuda_render_end(c._ctx, rgb.ctypes.data_as(fp), depth.ctypes.data_as(fp),
+                                          mask.ctypes.data_as(ctypes.POINTER(ctypes.c_uint8)), None) == ERR_CONTRACT
     finally:
         c.close()
 
