@@ -818,7 +818,10 @@ def main():
         if normals_ms > 0 and int(stats.normal_evals):
             m = seq.members[normal_idx]
             w, hb, ev = m.width, m.hidden_blocks, int(stats.normal_evals)
-            issued = 4 * ev * (2 * 32 * w + hb * (mult * 2 * w * w + 2 * 16 * w))
+            # the normal tiles run one fp16 term (their tolerance is an angle; engine.cuh
+            # normal_tile_terms) unless NSDF_NORMAL_TERMS=3
+            mult_n = 3 if args.mode == "fp16" and os.environ.get("NSDF_NORMAL_TERMS") == "3" else 1
+            issued = 4 * ev * (2 * 32 * w + hb * (mult_n * 2 * w * w + 2 * 16 * w))
             per_kernel.append({"kernel": f"normal tiles + shading ({w}x{hb}, 4 rows per hit)", "ms": normals_ms,
                                "ncu_name": f"tc_mlp_kernel<{w}, 1,", "evals": ev,
                                "tflops_algorithmic": flops_normals / (normals_ms / 1e3) / 1e12,
@@ -936,7 +939,8 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_total / steps, "ms_per_frame": ms_per_frame,
             "higher_is_better": True,
             "scaling": "strong" if world > 1 and not (W["gbuffer"] or shard_frames) else "weak", "vs_baseline": None,
-            "dtype": {"fp16": "split-fp16 tensor (3 MMA terms) / fp32 accum", "fp16low": "fp16 tensor / fp32 accum",
+            "dtype": {"fp16": "split-fp16 tensor (3 MMA terms; the normal tiles 1 term) / fp32 accum",
+                      "fp16low": "fp16 tensor / fp32 accum",
                       "fp32": "f32"}[args.mode],
             "data": "synthetic camera rays; committed fitted SIREN weights (assets/)",
             "config": {"workload": workload_text(args), "config": args.config, "resolution": f"{Wd}x{Hd}",

@@ -6,6 +6,7 @@
 // restates the reference's -ffp-contract=off C++ exactly (proj/CMakeLists.txt:15).
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <map>
 #include <mutex>
 #include <tuple>
@@ -142,6 +143,15 @@ FrameBuffers carve_frame(void* base, int n_rays, int n_counters) {
   fb.counters = reinterpret_cast<int*>(take(size_t(n_counters) * 4));
   fb.n_counters = n_counters;
   return fb;
+}
+
+int normal_tile_terms(Mode m) {
+  static const int forced = [] {
+    const char* e = getenv("NSDF_NORMAL_TERMS");
+    return e ? atoi(e) : 0;
+  }();
+  if (m == Mode::Fp16Low) return 1;
+  return forced == 3 ? 3 : 1;
 }
 
 int device_sms() {
@@ -646,7 +656,7 @@ int launch_normals_shade(Mode mode, const DevField& nf, float time, const int* l
                          float* rgb, float* depth, uint8_t* mask, cudaStream_t s) {
   NormalArgs a{nf, time, list, count, st, sp, defer_fallback ? 1 : 0, fb_list, fb_count, rgb, depth, mask};
   if (mode_tc(mode) && nf.kind == kFieldMlp && tc_supported(nf.net)) {
-    const TcLaunch r = tc_normals_shade(mode_terms(mode), nf, time, list, count, n_max, st, sp, defer_fallback,
+    const TcLaunch r = tc_normals_shade(normal_tile_terms(mode), nf, time, list, count, n_max, st, sp, defer_fallback,
                                         fb_list, fb_count, rgb, depth, mask, s);
     if (r == TcLaunch::kRan) return NSDF_PATH_TCGEN05;
     if (r == TcLaunch::kFailed) return -1;  // tc_last_error() holds the CUDA error

@@ -83,6 +83,13 @@ struct Profiler {
 // Which kernel family runs the MLP tiles.
 enum class Mode : int { Fp32Oracle = 0, Fp16Fast = 1, Fp16Low = 2 };
 inline int mode_terms(Mode m) { return m == Mode::Fp16Low ? 1 : 3; }
+// The render's normal + shading tiles only need a DIRECTION within the 0.5 deg tolerance:
+// one fp16 term per K step (angle error at identical points <= 0.07 deg on the omega0 = 10
+// sequence, 0.16 deg at omega0 = 30; tests/test_gpu_fast.py) instead of the trace's three,
+// whose depth tolerance (1e-3, the eps_stop jitter) needs |df| ~ 1e-5.  NSDF_NORMAL_TERMS=3
+// restores the split.  The normal-map API (a13: its delta-gate counts compare |f| with delta)
+// keeps the trace's arithmetic.
+int normal_tile_terms(Mode m);
 inline bool mode_tc(Mode m) { return m != Mode::Fp32Oracle; }
 
 struct TraceResult {

@@ -284,3 +284,61 @@ def test_depth_outliers_are_stop_band_steps(ref, fixture, budgets):
     assert np.percentile(dt, 99.9) <= DT_MAX, msg
     assert np.all(its_f[out] != its_r[out]), msg
     assert dt.max() <= 1.05 * cfg.eps_stop, msg
+
+
+def _render_normals(render_fn):
+    """The shading normals of a render, recovered exactly from six renders with one unit
+    light along +-x, +-y, +-z (albedo 1, ambient 0, diffuse 1, no specular): the red channel
+    is max(n.l, 0), so n_x = R(+x) - R(-x), etc."""
+    from paper_2201_09147_b200.abi import ShadeConfig
+    comps, mask = [], None
+    for axis in range(3):
+        pair = []
+        for sgn in (1.0, -1.0):
+            d = [0.0, 0.0, 0.0]
+            d[axis] = sgn
+            shade = ShadeConfig(specular=0.0, lights=((tuple(d), 1.0),), albedo=(1.0, 1.0, 1.0), ambient=0.0,
+                                diffuse=1.0)
+            rgb, _, m = render_fn(shade)[:3]
+            pair.append(np.asarray(rgb, np.float64)[..., 0])
+            mask = np.asarray(m)
+        comps.append(pair[0] - pair[1])
+    return np.stack(comps, -1), mask == 1
+
+
+@pytest.mark.parametrize("fixture", ["torus3", "w30"])
+def test_render_normal_tiles_within_tolerance(ref, fixture):
+    """The render's own shading normals (the fused normal + shade tiles, one fp16 MMA term in
+    the fast mode) against the reference renderer's, recovered from the framebuffer
+    (_render_normals) at 1080p: within 0.5 deg on every common hit whose hit points agree to
+    1e-4 (the other rays are the stop-band outliers, whose points differ by a step), and the
+    FP32 oracle mode's normals bit for bit."""
+    from paper_2201_09147_b200.abi import TraceConfig, standard_camera
+    from paper_2201_09147_b200.engine import Context, DeviceSequence
+    from paper_2201_09147_b200.manifest import load_manifest
+    path = _torus3() if fixture == "torus3" else _manifest()
+    cam = standard_camera(1920, 1080)
+    cfg = TraceConfig((40, 20, 20))
+    n_ref, m_ref = _render_normals(lambda sh: ref.render(path, cam, cfg, sh))
+    _, d_ref, _, _ = ref.render(path, cam, cfg, __import__("paper_2201_09147_b200.abi", fromlist=["x"]).ShadeConfig())
+    out = {}
+    for mode in ("fp32", "fp16"):
+        c = Context(0, mode)
+        try:
+            ds = DeviceSequence(c, load_manifest(path))
+            out[mode] = _render_normals(lambda sh: c.render(ds.levels(), cam, cfg, sh))
+            out[mode + "_depth"] = c.render(ds.levels(), cam, cfg,
+                                            __import__("paper_2201_09147_b200.abi", fromlist=["x"]).ShadeConfig())[1]
+        finally:
+            c.close()
+    n32, m32 = out["fp32"]
+    assert np.array_equal(m32, m_ref) and np.array_equal(n32, n_ref)
+    n16, m16 = out["fp16"]
+    both = m16 & m_ref & (np.abs(out["fp16_depth"] - d_ref) <= 1e-4)
+    a, b = n16[both], n_ref[both]
+    cosang = np.sum(a * b, -1) / (np.linalg.norm(a, axis=-1) * np.linalg.norm(b, axis=-1))
+    ang = np.degrees(np.arccos(np.clip(cosang, -1.0, 1.0)))
+    print(f"{fixture}: render normals vs reference over {int(both.sum())} hits: p99.9 "
+          f"{np.percentile(ang, 99.9):.4f} max {ang.max():.4f} deg")
+    assert both.sum() > 0.99 * (m16 & m_ref).sum()
+    assert ang.max() <= NORMAL_DEG_MAX
