@@ -19,6 +19,7 @@
 #include <sstream>
 
 #include "engine.hpp"
+#include "nsdf/b200.hpp"
 #include "nsdf/fields/nesting.hpp"
 #include "nsdf/shading/shading.hpp"
 #include "nsdf/trainer/trainer.hpp"
@@ -278,14 +279,17 @@ int cmd_render(Flags& f) {
   echo("render", e, out);
   const tracer::Camera camera = cam.camera();
   if (m.time_dependent && steps > 0) {
+    // the frame stream sharded across the engine's GPUs (NSDF_DEVICES): b200::render_frames
     const fs::path base(out);
+    std::vector<double> times;
+    for (int i = 0; i < steps; ++i) times.push_back(steps == 1 ? 0.0 : double(i) / double(steps - 1));
+    const auto frames = b200::render_frames(m.animated, times, camera, cfg);
     for (int i = 0; i < steps; ++i) {
-      const double t = steps == 1 ? 0.0 : double(i) / double(steps - 1);
       std::ostringstream name;
       name << base.stem().string() << "_" << std::setw(3) << std::setfill('0') << i << base.extension().string();
       const fs::path frame = base.parent_path().empty() ? fs::path(name.str()) : base.parent_path() / name.str();
-      save_image(shading::render(m.animated.slice(t), camera, cfg), frame);
-      std::cout << "frame " << i << " (t=" << t << ") -> " << frame << "\n";
+      save_image(frames[size_t(i)], frame);
+      std::cout << "frame " << i << " (t=" << times[size_t(i)] << ") -> " << frame << "\n";
     }
     return 0;
   }

@@ -44,7 +44,7 @@ std::vector<int> parse_devices(int primary) {
       char* end = nullptr;
       const long d = std::strtol(tok.c_str(), &end, 10);
       if (!end || *end || d < 0) throw Error(ErrorKind::config, "NSDF_DEVICES: bad device '" + tok + "'");
-      if (std::find(out.begin(), out.end(), int(d)) == out.end()) out.push_back(int(d));
+      out.push_back(int(d));  // a repeated device gets another context (own stream + workspace)
     }
     pos = comma + 1;
   }

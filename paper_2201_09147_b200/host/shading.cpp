@@ -6,7 +6,11 @@
 #include <fstream>
 #include <sstream>
 
+#include <exception>
+#include <thread>
+
 #include "device_seq.hpp"
+#include "nsdf/b200.hpp"
 #include "engine.hpp"
 #include "nsdf/shading/shading.hpp"
 
@@ -75,6 +79,54 @@ ImageBuffer render(const NestedSequence& seq, const Camera& camera, const Render
                                        img.depth.data(), img.mask.data(), nullptr));
   return img;
 }
+
+}  // namespace nsdf::shading
+
+namespace nsdf::b200 {
+
+int context_count() { return int(engine::contexts().size()); }
+
+std::vector<shading::ImageBuffer> render_frames(const fields::AnimatedSequence& anim, const std::vector<double>& times,
+                                                const tracer::Camera& camera, const shading::RenderConfig& config) {
+  anim.validate();
+  camera.validate();
+  const auto& ctxs = engine::contexts();
+  const size_t n = ctxs.size();
+  std::vector<shading::ImageBuffer> out(times.size());
+  std::vector<std::exception_ptr> errors(n);
+  const nsdf_camera cam = detail::to_pod(camera);
+  const nsdf_trace_config tc = detail::to_pod(config.trace);
+  const nsdf_shade_config sc = detail::to_pod(config.shade);
+  const int src = config.normal_source == shading::NormalSource::mapped ? NSDF_NORMALS_MAPPED : NSDF_NORMALS_OWN;
+  auto work = [&](size_t i) {
+    try {
+      for (size_t f = i; f < times.size(); f += n) {
+        const fields::NestedSequence seq = anim.slice(times[f]);
+        config.trace.validate(seq.size());
+        auto levels = detail::levels_of(seq);
+        for (nsdf_level& l : levels) l.field = engine::replica(i, l.field);
+        engine::check(nsdf_cuda_render_begin(ctxs[i], levels.data(), int(levels.size()), &cam, &tc, &sc, src,
+                                             config.mapped_fine_index));
+        shading::ImageBuffer img(camera.width, camera.height);
+        engine::check(nsdf_cuda_render_end(ctxs[i], img.rgb.data(), img.depth.data(), img.mask.data(), nullptr));
+        out[f] = std::move(img);
+      }
+    } catch (...) {
+      errors[i] = std::current_exception();
+    }
+  };
+  std::vector<std::thread> threads;
+  for (size_t i = 1; i < n; ++i) threads.emplace_back(work, i);
+  work(0);
+  for (auto& t : threads) t.join();
+  for (const auto& e : errors)
+    if (e) std::rethrow_exception(e);
+  return out;
+}
+
+}  // namespace nsdf::b200
+
+namespace nsdf::shading {
 
 // Per-vertex normal mapping (reference mesh.cpp:122-156).  Fields with a device binding run
 // entirely on the GPU (nsdf_cuda_map_normals_to_mesh: float cast, value + gradient tiles, the
