@@ -375,6 +375,9 @@ int run_frame_impl(nsdf_ctx* c, const nsdf_level* levels, int m, const nsdf_trac
                                        " tiles but the frame has " + std::to_string(tx * ty));
     long owned = 0;
     for (int t = 0; t < tx * ty; ++t) {
+      if (mapped && c->tile_owners[size_t(t)] >= tile_world)
+        return fail(NSDF_ERR_CONFIG, "tile owner map names rank " + std::to_string(c->tile_owners[size_t(t)]) +
+                                         " but the frame is split over " + std::to_string(tile_world));
       if ((mapped ? c->tile_owners[size_t(t)] : t % tile_world) != tile_rank) continue;
       const int x0 = (t % tx) * tile_size, y0 = (t / tx) * tile_size;
       owned += long(std::min(tile_size, cam->width - x0)) * std::min(tile_size, cam->height - y0);
