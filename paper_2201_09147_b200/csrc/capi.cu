@@ -792,9 +792,9 @@ int nsdf_cuda_upload_mlp(nsdf_ctx* c, int n_layers, const int32_t* rows, const i
     n.rows_pad[l] = Rp;
   }
   // Fast-mode copy (mlp_tc.cu): sine nets whose hidden layers are square W x W with
-  // W in {64, 128, 256}.  Hidden weights -> fp16 in the UMMA canonical K-major layout,
-  // element (n, k) at ((k/8)*(W/8) + n/8)*64 + (n%8)*8 + k%8, so every 32-wide K chunk is
-  // one contiguous bulk copy.
+  // W in {64, 128, 256}.  Hidden weights -> fp16 in the UMMA canonical K-major layout, in
+  // N-blocks (tc_wq_offset, mlp_tc.cuh), so every streamed (N-block, K chunk) piece is one
+  // contiguous bulk copy.
   n.tc_ok = 0;
   size_t o_wq = 0, o_bias = 0;
   {
@@ -819,7 +819,7 @@ int nsdf_cuda_upload_mlp(nsdf_ctx* c, int n_layers, const int32_t* rows, const i
             for (int kk = 0; kk < W; ++kk) {
               const double v = double(n.omega) * double(float(packed[o + size_t(r) * W + kk]));
               const __half h = __float2half_rn(float(v));
-              const size_t at = size_t((kk / 8) * (W / 8) + r / 8) * 64 + (r % 8) * 8 + kk % 8;
+              const size_t at = tc_wq_offset(W, r, kk);
               hi[at] = h;
               lo[at] = __float2half_rn(float(v - double(__half2float(h))));
             }

@@ -34,7 +34,7 @@ struct DevNet {
   const float* b[kMaxLayers];
   // Fast-mode (tcgen05) copy, built at upload when tc-eligible (mlp_tc.cu):
   int tc_ok;
-  const uint16_t* wq;      // hidden layers [h][hi | lo][W*W] fp16, UMMA canonical K-major layout
+  const uint16_t* wq;      // hidden layers [h][hi | lo][W*W] fp16, canonical layout in N-blocks (tc_wq_offset)
   const float* bias_cat;   // biases of layers 0 .. L-2, [L-1][width]
   float bout;              // output bias
   // FP64 master copy (the certification path, mlp_f64.cu): same layouts as w / wt / b.

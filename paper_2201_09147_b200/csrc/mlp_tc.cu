@@ -12,10 +12,13 @@
 //   hidden layers        D[128 x W] (fp32, TMEM) = A[128 x W] (fp16 hi/lo, TMEM: written in
 //                        place over the previous layer's accumulator) . W_l^T (fp16
 //                        hi/lo): tcgen05.mma.cta_group::1.kind::f16, M=128 N=W K=16, three
-//                        terms per K step (split precision), issued by one thread; weights
-//                        SMEM-resident (64-wide) or streamed in 32-K chunks through a 2-stage
-//                        cp.async.bulk ring by a producer warp (pre-arranged in the UMMA
-//                        canonical layout at upload, so a chunk is one contiguous bulk copy)
+//                        terms per K step (split precision), issued by one thread; 256-wide
+//                        layers as two N = 128 column blocks with their own completion
+//                        barriers (the epilogue of block 0 runs under block 1's MMAs and the
+//                        next layer follows without a drain); weights SMEM-resident (64-wide)
+//                        or streamed in (N-block, K chunk) pieces of W*32 halves through a
+//                        2-3 stage cp.async.bulk ring by a producer warp (pre-arranged in the
+//                        UMMA canonical layout at upload, so a piece is one contiguous copy)
 //   K streaming          16-column block b belongs to column group b % groups; the MMA of
 //                        layer m+1 consumes block rows as the epilogue of layer m writes them
 //                        (kready mbarriers); accumulators alternate between two TMEM regions
@@ -51,7 +54,13 @@ namespace {
 
 constexpr int kRows = 128;   // TMEM lanes per tile
 constexpr int kKC = 32;      // K elements per streamed weight chunk
-constexpr int kStages = 2;
+constexpr int kMaxStages = 4;  // weight ring depth: tc_stages(W) (256-wide: 3 — 2 starves the
+                               // N-block pipeline at layer boundaries, 4 gains nothing more)
+#ifndef NSDF_TC_STAGES256
+#define NSDF_TC_STAGES256 3
+#endif
+__host__ __device__ constexpr int tc_stages(int W) { return W == 256 ? NSDF_TC_STAGES256 : 2; }
+static_assert(NSDF_TC_STAGES256 >= 2 && NSDF_TC_STAGES256 <= kMaxStages, "ring depth");
 constexpr int kBlk = 16;     // columns per epilogue block = K per MMA step
 constexpr int kMaxSub = 8;   // max blocks per column group per layer (kready barriers)
 constexpr float kHalfPi = 1.5707963267948966f;
@@ -262,7 +271,7 @@ constexpr int kK0 = 32;
 
 // Dynamic shared-memory carve-up.  SWIZZLE_NONE operands need 16-byte alignment only.
 struct TcSmem {
-  __half* wst;          // resident hidden weights, or [kStages] streamed weight chunks
+  __half* wst;          // resident hidden weights, or [tc_stages(W)] streamed weight chunks
   __half* b0;           // [W x 32] layer-0 B operand
   __half* bb;           // [L-2][W x 16] bias B operand of each hidden layer: omega*b in 3 fp16 parts
   __half* ones;         // [128 x 16] bias A operand: ones at k = 0..2 on value rows
@@ -271,17 +280,17 @@ struct TcSmem {
   int* stage_buf;       // [kStageCap] staged compaction appends (persistent trace)
   int* stage_count;
   int* stage_base;      // flush base broadcast
-  uint64_t* bars;       // full[kStages], empty[kStages], kready[kMaxSub], a0ready, dfull, tstart
+  uint64_t* bars;       // full[kMaxStages], empty[kMaxStages], kready[kMaxSub], a0ready, tstart, dfull[2]
   uint32_t* tmem_base;
   int* done;            // persistent level: no more tiles
 };
 constexpr int kStageCap = 512;
-constexpr int kNumBars = 2 * kStages + kMaxSub + 3;
+constexpr int kNumBars = 2 * kMaxStages + kMaxSub + 4;  // full, empty, kready, a0ready, tstart, dfull[2]
 
 __host__ __device__ inline size_t tc_weight_bytes(int W, int L, int terms, bool resident) {
   const int nw = terms == 3 ? 2 : 1;
   // resident: every hidden layer's [hi | lo] pair, as laid out in global memory
-  return resident ? size_t(L - 2) * W * W * 2 * 2 : size_t(kStages) * W * kKC * 2 * nw;
+  return resident ? size_t(L - 2) * W * W * 2 * 2 : size_t(tc_stages(W)) * W * kKC * 2 * nw;
 }
 
 __host__ __device__ inline size_t tc_smem_bytes(int W, int L, int terms, bool resident, bool persist) {
@@ -475,27 +484,38 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
   const TcSmem sm = tc_carve(smem_raw, W, L, kTerms, kResident, kPersist);
   constexpr int kNW = kTerms == 3 ? 2 : 1;  // weight parts (hi [, lo])
   uint64_t* full = sm.bars;
-  uint64_t* empty = sm.bars + kStages;
-  uint64_t* kready = sm.bars + 2 * kStages;  // [kSub]: A block row i written by every group
-  uint64_t* a0ready = sm.bars + 2 * kStages + kMaxSub;
-  uint64_t* dfull = sm.bars + 2 * kStages + kMaxSub + 1;
-  uint64_t* tstart = sm.bars + 2 * kStages + kMaxSub + 2;
+  constexpr int kStages = tc_stages(W);
+  uint64_t* empty = sm.bars + kMaxStages;
+  uint64_t* kready = sm.bars + 2 * kMaxStages;  // [kSub]: A block row i written by every group
+  uint64_t* a0ready = sm.bars + 2 * kMaxStages + kMaxSub;
+  uint64_t* tstart = sm.bars + 2 * kMaxStages + kMaxSub + 1;
+  uint64_t* dfull = sm.bars + 2 * kMaxStages + kMaxSub + 2;  // [kNH]: N-block nb of a layer complete
   float* part = sm.part;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // hidden (W x W) MMA layers: compile-time for the standard architectures (kHid > 0), so
   // the layer loops unroll and every per-layer constant folds
   const int n_hidden = kHid > 0 ? kHid : L - 2;
   constexpr int kRaysPerTile = kGrad ? kRows / 4 : kRows;
-  constexpr int kChunks = W / kKC;
-  constexpr uint32_t kChunkBytes = uint32_t(W) * kKC * 2;
-  constexpr size_t kStageHalves = size_t(W) * kKC * kNW;
+  // N-blocks: every MMA layer is issued as kNH column blocks of kNB outputs, each with its
+  // own completion barrier (dfull[nb]), so the epilogue of block 0 (and with it the next
+  // layer's first K rows) runs under the MMAs of block 1 and the tensor pipe goes straight
+  // on into the next layer.  Weights stream as (N-block, K chunk) pieces of kNB x kKCh.
+  constexpr int kNH = tc_halves(W);
+  constexpr int kNB = W / kNH;
+  constexpr int kKCh = kKC * kNH;           // K per streamed chunk (same bytes per stage)
+  constexpr int kChunks = W / kKCh;         // chunks per N-block
+  constexpr int kStepsPerChunk = kKCh / kBlk;
+  constexpr uint32_t kChunkBytes = uint32_t(kNB) * kKCh * 2;
+  constexpr size_t kStageHalves = size_t(kNB) * kKCh * kNW;
   // K streaming: block b of a layer's output belongs to group b % kGroups, so the groups
   // together produce the next layer's A operand in natural K order, block row i = blocks
   // [i*kGroups, (i+1)*kGroups), and the MMA of layer m+1 starts on block row 0 while the
   // epilogue still works on layer m.  Accumulators alternate between two TMEM regions
   // (layer m in columns (m & 1) * W).
   constexpr int kSub = W / kBlk / kGroups;
+  constexpr int kSubNB = kSub / kNH;  // blocks per group per N-block
   static_assert(kSub <= kMaxSub, "kready barriers");
+  static_assert(kSub % kNH == 0 && kChunkBytes * kNW == size_t(W) * kKC * 2 * kNW, "N-block split");
   constexpr uint32_t kTmemCols = 2 * W;
   // The hidden layers' A operand lives in TMEM, written IN PLACE over the accumulator
   // it is computed from: the epilogue reads D block b (16 fp32 columns of its lane), and
@@ -572,7 +592,7 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
     // one arrival per epilogue warp (after a __syncwarp behind each thread's fence)
     for (int i = 0; i < kSub; ++i) mbar_init(&kready[i], 4 * kGroups);
     mbar_init(a0ready, 4 * kGroups);
-    mbar_init(dfull, 1);
+    for (int nb = 0; nb < kNH; ++nb) mbar_init(&dfull[nb], 1);
     mbar_init(tstart, 1);
     *sm.stage_count = 0;
     *sm.done = 0;
@@ -607,7 +627,7 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
     // ================= MMA issuer (resident mode: also loads the weights once) =================
     // the whole warp runs this loop; MMAs and commits are issued by one elected lane
     {
-      const uint32_t idesc = umma_idesc(W);
+      const uint32_t idesc = umma_idesc(kNB);
       const uint32_t b0_base = smem_addr(sm.b0);
       const uint64_t ones_desc = umma_desc(smem_addr(sm.ones), kRows * 16, 128);
       if (kResident) {
@@ -635,55 +655,64 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
         a0_phase ^= 1;
         tc_fence_after();
 #pragma unroll
-        for (int ks = 0; ks < kK0 / 16; ++ks) {
-          const uint64_t bd = umma_desc(b0_base + uint32_t(ks * 2) * (W / 8) * 128, W * 16, 128);
-          tc_mma_ts(tmem, tmem + uint32_t(W + ks * 8), bd, idesc, ks != 0);
+        for (int nb = 0; nb < kNH; ++nb) {
+#pragma unroll
+          for (int ks = 0; ks < kK0 / 16; ++ks) {
+            const uint64_t bd = umma_desc(b0_base + uint32_t(ks * 2) * (W / 8) * 128 + uint32_t(nb * kNB * 16), W * 16, 128);
+            tc_mma_ts(tmem + uint32_t(nb * kNB), tmem + uint32_t(W + ks * 8), bd, idesc, ks != 0);
+          }
+          tc_commit(&dfull[nb]);
         }
-        tc_commit(dfull);
-        // ---- hidden layers, K-streamed behind the epilogue ----
+        // ---- hidden layers, K-streamed behind the epilogue, N-block by N-block ----
         for (int h = 0; h < n_hidden; ++h) {
           const uint32_t d_tmem = tmem + uint32_t((h + 1) & 1) * W;
           const uint32_t a_tmem = tmem + uint32_t(h & 1) * W;  // A in place of layer h's D
-          uint32_t b_base = 0, lo_off = 0;
-          int s = 0;
 #pragma unroll
-          for (int blk = 0; blk < W / kBlk; ++blk) {
-            if (blk % kGroups == 0) {  // block row of the A operand written by every group
-              timed_wait(&kready[blk / kGroups], kr_phase, w_k);
-              tc_fence_after();
-            }
-            if (blk == 0)  // D = omega*b (value rows), then += A.(omega W)^T
-              tc_mma(d_tmem, ones_desc, umma_desc(smem_addr(sm.bb + size_t(h) * W * kBlk), W * 16, 128), idesc, false);
-            const int c = blk >> 1, ks = blk & 1;  // 32-K weight chunk, K=16 step inside it
-            if (ks == 0) {
-              s = chunk_iter % kStages;
-              if (kResident) {
-                // resident layout per layer: [hi W*W][lo W*W], chunk c contiguous inside each
-                b_base = smem_addr(sm.wst + size_t(h) * 2 * W * W + size_t(c) * W * kKC);
-                lo_off = uint32_t(W) * W * 2;
-              } else {
-                timed_wait(&full[s], (chunk_iter / kStages) & 1, w_full);
+          for (int nb = 0; nb < kNH; ++nb) {
+            const uint32_t dn = d_tmem + uint32_t(nb * kNB);
+            // D = omega*b (value rows) first: it reads no A, and this region's last readers
+            // (the previous layer's MMAs) precede it in the tensor pipe's issue order
+            tc_mma(dn, ones_desc, umma_desc(smem_addr(sm.bb + size_t(h) * W * kBlk) + uint32_t(nb * kNB * 16), W * 16, 128),
+                   idesc, false);
+            uint32_t b_base = 0, lo_off = 0;
+            int s = 0;
+#pragma unroll
+            for (int blk = 0; blk < W / kBlk; ++blk) {
+              if (nb == 0 && blk % kGroups == 0) {  // block row of the A operand written by every group
+                timed_wait(&kready[blk / kGroups], kr_phase, w_k);
                 tc_fence_after();
-                b_base = smem_addr(sm.wst + size_t(s) * kStageHalves);
-                lo_off = uint32_t(W) * kKC * 2;
+              }
+              const int c = blk / kStepsPerChunk, ks = blk % kStepsPerChunk;  // weight chunk, K=16 step in it
+              if (ks == 0) {
+                s = chunk_iter % kStages;
+                if (kResident) {
+                  // resident layout per layer: [hi W*W][lo W*W] (tc_wq_offset)
+                  b_base = smem_addr(sm.wst + size_t(h) * 2 * W * W + size_t(nb) * kNB * W + size_t(c) * kNB * kKCh);
+                  lo_off = uint32_t(W) * W * 2;
+                } else {
+                  timed_wait(&full[s], (chunk_iter / kStages) & 1, w_full);
+                  tc_fence_after();
+                  b_base = smem_addr(sm.wst + size_t(s) * kStageHalves);
+                  lo_off = kChunkBytes;
+                }
+              }
+              const uint32_t boff = uint32_t(ks * 2) * (kNB / 8) * 128;
+              const uint64_t bd = umma_desc(b_base + boff, kNB * 16, 128);
+              const uint32_t at = a_tmem + uint32_t(blk * kBlk);  // hi parts; lo parts 8 columns on
+              tc_mma_ts(dn, at, bd, idesc, true);
+              if (kTerms == 3) {  // split precision: + A_lo.W_hi + A_hi.W_lo
+                const uint64_t bdl = umma_desc(b_base + lo_off + boff, kNB * 16, 128);
+                tc_mma_ts(dn, at + 8, bd, idesc, 1);
+                tc_mma_ts(dn, at, bdl, idesc, 1);
+              }
+              if (ks == kStepsPerChunk - 1) {
+                if (!kResident) tc_commit(&empty[s]);  // frees the weight stage once these MMAs retire
+                ++chunk_iter;
               }
             }
-            const uint32_t boff = uint32_t(ks * 2) * (W / 8) * 128;
-            const uint64_t bd = umma_desc(b_base + boff, W * 16, 128);
-            const uint32_t at = a_tmem + uint32_t(blk * kBlk);  // hi parts; lo parts 8 columns on
-            tc_mma_ts(d_tmem, at, bd, idesc, true);
-            if (kTerms == 3) {  // split precision: + A_lo.W_hi + A_hi.W_lo
-              const uint64_t bdl = umma_desc(b_base + lo_off + boff, W * 16, 128);
-              tc_mma_ts(d_tmem, at + 8, bd, idesc, 1);
-              tc_mma_ts(d_tmem, at, bdl, idesc, 1);
-            }
-            if (ks == 1) {
-              if (!kResident) tc_commit(&empty[s]);  // frees the weight stage once these MMAs retire
-              ++chunk_iter;
-            }
+            tc_commit(&dfull[nb]);  // N-block nb of the accumulator complete
           }
           kr_phase ^= 1;
-          tc_commit(dfull);  // accumulator complete
         }
         if (mdbg && t >= a.dbg_skip && t - a.dbg_skip < 64) {
           t_loop = clock64() - tl0;
@@ -702,15 +731,17 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
       for (int t = 0; more_tiles(t); ++t) {
         for (int h = 0; h < n_hidden; ++h) {
           const __half* lw = reinterpret_cast<const __half*>(net.wq) + size_t(h) * 2 * W * W;
-          for (int c = 0; c < kChunks; ++c, ++chunk_iter) {
-            const int s = chunk_iter % kStages;
-            mbar_wait(&empty[s], ((chunk_iter / kStages) & 1) ^ 1);
-            mbar_expect_tx(&full[s], kChunkBytes * kNW);
-            bulk_g2s(sm.wst + size_t(s) * kStageHalves, lw + size_t(c) * (W * kKC), kChunkBytes, &full[s]);
-            if (kTerms == 3)
-              bulk_g2s(sm.wst + size_t(s) * kStageHalves + size_t(W) * kKC, lw + size_t(W) * W + size_t(c) * (W * kKC),
-                       kChunkBytes, &full[s]);
-          }
+          for (int nb = 0; nb < kNH; ++nb)
+            for (int c = 0; c < kChunks; ++c, ++chunk_iter) {
+              const int s = chunk_iter % kStages;
+              const size_t piece = size_t(nb) * kNB * W + size_t(c) * kNB * kKCh;  // (N-block, chunk)
+              mbar_wait(&empty[s], ((chunk_iter / kStages) & 1) ^ 1);
+              mbar_expect_tx(&full[s], kChunkBytes * kNW);
+              bulk_g2s(sm.wst + size_t(s) * kStageHalves, lw + piece, kChunkBytes, &full[s]);
+              if (kTerms == 3)
+                bulk_g2s(sm.wst + size_t(s) * kStageHalves + size_t(kNB) * kKCh, lw + size_t(W) * W + piece, kChunkBytes,
+                         &full[s]);
+            }
         }
       }
     }
@@ -789,10 +820,6 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
       auto layer = [&](int m, auto last_tag) {
         constexpr bool last = decltype(last_tag)::value;
         if constexpr (last) gap1();
-        mbar_wait(dfull, dfull_phase);
-        mark(2 + 2 * min(m, 3));
-        dfull_phase ^= 1;
-        tc_fence_after();
         // D is the sine argument in radians (omega and the bias are inside the MMAs)
         const uint32_t treg = taddr + uint32_t(m & 1) * W;
         // sine epilogue of one 16-column block (value rows; tangent rows scale by omega cos)
@@ -813,15 +840,20 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
             }
           }
         };
-        // TMEM loads software-pipelined one block ahead of the math
+        // TMEM loads software-pipelined one block ahead of the math, within an N-block
         uint32_t raw[2][16];
-        tmem_issue16(treg + uint32_t(eg * kBlk), raw[0]);
 #pragma unroll
         for (int i = 0; i < kSub; ++i) {
           const int buf = i & 1;
           const int cc = (i * kGroups + eg) * kBlk;
+          if (i % kSubNB == 0) {  // first block of N-block i / kSubNB: wait for its MMAs
+            mbar_wait(&dfull[i / kSubNB], dfull_phase);
+            if (i == 0) mark(2 + 2 * min(m, 3));
+            tc_fence_after();
+            tmem_issue16(treg + uint32_t(cc), raw[buf]);
+          }
           tmem_wait16(raw[buf]);
-          if (i + 1 < kSub) tmem_issue16(treg + uint32_t(cc + kGroups * kBlk), raw[buf ^ 1]);
+          if (i + 1 < kSub && (i + 1) % kSubNB != 0) tmem_issue16(treg + uint32_t(cc + kGroups * kBlk), raw[buf ^ 1]);
           float v[16];
           activate(raw[buf], cc, v);
           if constexpr (!last) {
@@ -850,6 +882,7 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
             for (int j = 0; j < 8; ++j) acc2 = __ffma2_rn(wo[j], make_float2(v[2 * j], v[2 * j + 1]), acc2);
           }
         }
+        dfull_phase ^= 1;
         mark(3 + 2 * min(m, 3));
       };
 #pragma unroll

@@ -11,6 +11,21 @@
 namespace nsdf_b200 {
 
 enum class TcLaunch { kRan, kDeclined, kFailed };
+
+// Hidden-layer weights of a W-wide net are issued as tc_halves(W) N-blocks of W / halves
+// output columns each (256-wide: two), so the epilogue of a layer's first half runs under the
+// MMAs of its second half.  (128-wide: one — two 64-column blocks measured slower, 1.66 vs
+// 1.60 ms for the level; two CTAs per SM already overlap each other's layer boundaries.)  Upload layout of one part (hi or lo, W x W fp16):
+// [N-block][K/8][NB/8][8 rows][8 k], NB = W / halves — every (N-block, K chunk) piece is one
+// contiguous bulk copy in the UMMA canonical K-major layout (SBO 128 B, LBO NB*16 B).
+#ifndef NSDF_TC_NH128
+#define NSDF_TC_NH128 1
+#endif
+__host__ __device__ constexpr int tc_halves(int W) { return W == 256 ? 2 : (W == 128 ? NSDF_TC_NH128 : 1); }
+__host__ __device__ constexpr size_t tc_wq_offset(int W, int n, int k) {
+  return size_t(n / (W / tc_halves(W))) * size_t(W / tc_halves(W)) * W +
+         size_t(((k / 8) * (W / tc_halves(W) / 8) + (n % (W / tc_halves(W))) / 8) * 64 + (n % 8) * 8 + k % 8);
+}
 cudaError_t tc_last_error();  // CUDA error of this thread's last kFailed launch
 
 // Persistent level trace: one launch runs every iteration of a level; rows are refilled
