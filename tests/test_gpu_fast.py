@@ -52,7 +52,10 @@ def test_fast_mlp_close_to_oracle(ctx, fast, name):
     assert np.percentile(angle_deg(g0[:, near], g1[:, near]), 99.9) < ANGLE_MAX
 
 
-@pytest.mark.parametrize("width,hidden", [(64, 1), (128, 2), (256, 3)])
+# the standard depths (compiled-in layer counts) and others (runtime layer loops; 64x5 streams
+# its weights instead of keeping them resident; 256-wide layers run as two N-blocks)
+@pytest.mark.parametrize("width,hidden", [(64, 1), (128, 2), (256, 3), (64, 2), (64, 5), (128, 1), (128, 3),
+                                          (256, 1), (256, 2), (256, 4)])
 def test_fast_mlp_random_init(ctx, fast, width, hidden):
     net = random_net(width, hidden, seed=40 + width)
     pts = np.random.default_rng(2).uniform(-1.2, 1.2, (3, 3000)).astype(np.float32)
