@@ -119,12 +119,12 @@ int main() {
         for (int i = 0; i < sms; ++i) m = h[i] > m ? h[i] : m;
         best = m < best ? m : best;
       }
-      // bytes moved per SM: every warp covers 32 lanes x its column slice x iters (x4 B)
-      const double elems = double(iters) * 128 * 512;  // lanes x columns per iteration, whole SM
-      const double bytes = op == 2 ? elems * 2 : elems * 4;  // st: x8 of every 16 columns... see below
+      // per SM and iteration the warps cover 128 lanes x 512 columns; loads move 4 B per
+      // column, stores (x8 of every 16 columns) half of that
+      const double elems = double(iters) * 128 * 512;
+      const double bytes = op == 2 ? elems * 2 : elems * 4;
       printf("%-40s warps %2d: %8.1f B/clk/SM (%s), %.2f activations/clk/SM\n", names[op], warps,
-             (op == 2 ? elems * 4 / 2 : elems * 4) / double(best), op == 2 ? "stored" : "loaded", elems / double(best));
-      (void)bytes;
+             bytes / double(best), op == 2 ? "stored" : "loaded", elems / double(best));
     }
   return 0;
 }
