@@ -1819,10 +1819,6 @@ int copy_out_frame(nsdf_ctx* c, const std::vector<std::pair<void*, const void*>>
 
 }  // namespace
 
-extern "C" {
-
-}  // extern "C"
-
 // Split form of nsdf_cuda_render: begin enqueues the whole frame into the context's device
 // framebuffer and returns; end copies it into the caller's host buffers.  A caller can
 // allocate (and zero) its host framebuffer while the GPU renders — the reference API's
