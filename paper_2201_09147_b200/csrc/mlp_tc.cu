@@ -55,11 +55,15 @@ namespace {
 constexpr int kRows = 128;   // TMEM lanes per tile
 constexpr int kKC = 32;      // K elements per streamed weight chunk
 constexpr int kMaxStages = 4;  // weight ring depth: tc_stages(W) (256-wide: 3 — 2 starves the
-                               // N-block pipeline at layer boundaries, 4 gains nothing more)
+                               // N-block pipeline at layer boundaries, 4 gains nothing more;
+                               // 128-wide: 3 — level 1.65 -> 1.57 ms, 4 the same)
 #ifndef NSDF_TC_STAGES256
 #define NSDF_TC_STAGES256 3
 #endif
-__host__ __device__ constexpr int tc_stages(int W) { return W == 256 ? NSDF_TC_STAGES256 : 2; }
+#ifndef NSDF_TC_STAGES128
+#define NSDF_TC_STAGES128 3
+#endif
+__host__ __device__ constexpr int tc_stages(int W) { return W == 256 ? NSDF_TC_STAGES256 : (W == 128 ? NSDF_TC_STAGES128 : 2); }
 static_assert(NSDF_TC_STAGES256 >= 2 && NSDF_TC_STAGES256 <= kMaxStages, "ring depth");
 constexpr int kBlk = 16;     // columns per epilogue block = K per MMA step
 constexpr int kMaxSub = 8;   // max blocks per column group per layer (kready barriers)
