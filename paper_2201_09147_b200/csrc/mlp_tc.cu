@@ -472,7 +472,7 @@ enum PfStage : int { kPfNeed = 0, kPfListed = 1, kPfReady = 2 };
 //  kGroups   column groups of 4 epilogue warps; 16-column block b of every layer belongs
 //            to group b % kGroups (TMEM lane quadrant = warp % 4)
 //  kResident all hidden-layer weights stay in SMEM (64-wide nets); otherwise a producer
-//            warp streams 32-wide K chunks through a 2-stage ring
+//            warp streams (N-block, K chunk) pieces through a tc_stages(W)-deep ring
 //  kPersist  one launch traces a whole level: rows are refilled from the level's input
 //            list until it drains (sphere_trace_level, trace.cpp:61-84)
 // MMA layer m = 0 is layer 0 (K = 32, B0 resident), m = 1..L-2 the hidden layers; the
