@@ -475,11 +475,13 @@ enum PfStage : int { kPfNeed = 0, kPfListed = 1, kPfReady = 2 };
 //            warp streams (N-block, K chunk) pieces through a tc_stages(W)-deep ring
 //  kPersist  one launch traces a whole level: rows are refilled from the level's input
 //            list until it drains (sphere_trace_level, trace.cpp:61-84)
+// Residency: 64-wide 4 CTAs/SM, 128-wide 2, 256-wide 1 (TMEM), so the 256-wide kernels get
+// the registers of a whole SM (the 1-term normal tiles use ~160: config 4 1.54 -> 1.51 ms).
 // MMA layer m = 0 is layer 0 (K = 32, B0 resident), m = 1..L-2 the hidden layers; the
 // last hidden layer's epilogue folds in the 1 x W output layer.
 template <int W, bool kGrad, int kGroups, int kTerms, bool kResident, bool kPersist, int kHid>
 __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
-                                  (W == 64 ? 4 : (kGroups > 2 ? 1 : 2))) tc_mlp_kernel(TcArgs a) {
+                                  (W == 64 ? 4 : (W == 256 ? 1 : 2))) tc_mlp_kernel(TcArgs a) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
   constexpr int kCtl = kResident ? 1 : 2;  // control warps: MMA issuer [+ weight producer]
   constexpr int kThreads = 32 * kCtl + 128 * kGroups;
