@@ -934,6 +934,13 @@ def main():
 
     if rank == 0:
         launches = (int(stats.kernel_launches) if stats is not None else 1) * steps
+        clk = clocks.summary()
+        if not W["gbuffer"] and clk.get("sm_mhz"):
+            # the same MUFU fractions against 16/clk/SM at the SM clock measured in the timed
+            # region (power-capped runs sit well below the 1965 MHz maximum)
+            for k in act_bound["per_kernel"]:
+                k["mufu_frac_at_sm_clock"] = k["mufu_frac"] * 1965.0 / clk["sm_mhz"]
+            act_bound["frac_at_sm_clock"] = act_bound["frac"] * 1965.0 / clk["sm_mhz"]
         line = {
             "metric": cfgw["metric"], "value": value, "unit": unit, "n_gpus": world, "steps": steps,
             "warmup": args.warmup, "ms_per_step": ms_total / steps, "ms_per_frame": ms_per_frame,
@@ -970,7 +977,7 @@ def main():
             "cpu_baseline": cpu,
             "e2e": e2e,
             "gpu_launches": launches,
-            "clocks": clocks.summary(),
+            "clocks": clk,
         }
         print(json.dumps(line), flush=True)
     for c, _, _ in W.get("lanes", [(ctx, None, None)]):
