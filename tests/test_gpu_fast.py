@@ -340,3 +340,49 @@ def test_fast_sine_at_large_arguments(fast):
     assert np.all(es <= bound), (float(np.max(es / bound)), float(xd[np.argmax(es / bound)]))
     assert np.all(ec <= bound + np.abs(xd) * 2.0 ** -24), float(np.max(ec / bound))
     print(f"max |omega0 z| of the fixtures {top:.1f}; max sine error {es.max():.2e}, cos {ec.max():.2e}")
+
+
+@pytest.mark.parametrize("seed", range(int(os.environ.get("NSDF_FUZZ_N", "10"))))
+def test_fast_render_randomized(ctx, fast, seed):
+    """Randomised scenes through both modes: image size (1 x 1 up to 200 x 200), camera
+    position and field of view, per-level budgets (zeros included), specular, normal source.
+    The fast frame agrees with the oracle-mode frame within the BASELINE tolerances (mask
+    disagreement counted in pixels, so a one-pixel image is held to the same standard), and
+    the fast frame assembled from tile shares (random tile size and rank count) equals the
+    whole fast frame bit for bit.  NSDF_FUZZ_N sets the number of scenes (default 10)."""
+    import torch
+    from paper_2201_09147_b200.abi import Camera, ShadeConfig, TraceConfig
+    from paper_2201_09147_b200.engine import DeviceSequence
+    from paper_2201_09147_b200.manifest import load_manifest
+    rng = np.random.default_rng(1000 + seed)
+    seq = load_manifest(_fixture("torus3.nest"))
+    w, h = (1, 1) if seed == 0 else (int(rng.integers(1, 201)), int(rng.integers(1, 201)))
+    d = rng.normal(size=3)
+    pos = d / np.linalg.norm(d) * rng.uniform(1.6, 4.0)
+    cam = Camera(tuple(pos), tuple(rng.uniform(-0.2, 0.2, 3)), (0, 1, 0), float(rng.uniform(20, 90)), w, h)
+    budgets = [int(b) for b in rng.integers(0, 31, 3)]
+    if not any(budgets):
+        budgets[-1] = 20
+    cfg = TraceConfig(tuple(budgets))
+    shade = ShadeConfig(specular=float(rng.uniform(0, 1)))
+    src = int(rng.integers(0, 2))
+    a = ctx.render(DeviceSequence(ctx, seq).levels(), cam, cfg, shade, src)
+    ds = DeviceSequence(fast, seq)
+    b = fast.render(ds.levels(), cam, cfg, shade, src)
+    rgb0, d0, m0, _ = a
+    rgb1, d1, m1, _ = b
+    n = w * h
+    assert np.sum(m0 != m1) <= max(1, int(1e-3 * n)), (w, h, budgets)
+    both = (m0 == 1) & (m1 == 1)
+    if both.any():
+        assert np.percentile(np.abs(d0 - d1)[both], 99.9) <= DT_MAX
+    # tile shares of the same fast frame into one device framebuffer
+    tile, world = int(rng.choice([8, 16, 32, 64])), int(rng.integers(2, 5))
+    fb = [torch.zeros(3 * n, device="cuda"), torch.zeros(n, device="cuda"),
+          torch.zeros(n, dtype=torch.uint8, device="cuda")]
+    for r in range(world):
+        fast.render_device(ds.levels(), cam, cfg, shade, *(x.data_ptr() for x in fb), src, -1, tile, r, world)
+    torch.cuda.synchronize()
+    assert np.array_equal(fb[2].cpu().numpy(), m1.reshape(-1))
+    assert np.array_equal(fb[1].cpu().numpy().view(np.uint32), d1.reshape(-1).view(np.uint32))
+    assert np.array_equal(fb[0].cpu().numpy().view(np.uint32), rgb1.reshape(-1).view(np.uint32))
