@@ -4,7 +4,8 @@ bounds-checked build of the engine (paper_2201_09147_b200/_checked/libnsdf_cuda.
 append, list write and framebuffer pixel the kernels compute — the persistent trace's claimed
 list items and staged appends included — counting (and skipping) any out-of-bounds access.
 A workload covering the engine's index paths runs on it in a fresh process: full and tile-
-sharded renders (static and cost-balanced owners), render_multi, ragged trace_rays batches,
+sharded renders (static and cost-balanced owners), renders of random views at ragged image
+sizes, render_multi, ragged trace_rays batches,
 batch evaluation, the normal map and the mesh normal map, in the fast (tcgen05) and the
 FP32 oracle modes.  Every frame must equal the normal build's bit for bit and the violation
 count must be zero."""
@@ -27,7 +28,7 @@ import json, os, sys
 import numpy as np
 sys.path.insert(0, sys.argv[1]); sys.path.insert(0, os.path.join(sys.argv[1], "tools"))
 from paper_2201_09147_b200 import abi
-from paper_2201_09147_b200.abi import ShadeConfig, TraceConfig, standard_camera
+from paper_2201_09147_b200.abi import Camera, ShadeConfig, TraceConfig, standard_camera
 from paper_2201_09147_b200.engine import Context, DeviceSequence, render_multi
 from paper_2201_09147_b200.manifest import load_manifest
 from paper_2201_09147_b200.meshes import torus_mesh
@@ -48,6 +49,15 @@ for mode in ("fp16", "fp32"):
         out["digests"][f"{mode} render {b}"] = digest(rgb) + digest(depth) + digest(mask)
         rgb, depth, mask, st = c.render(ds.levels(), cam, TraceConfig(b), ShadeConfig(), normal_source=1)
         out["digests"][f"{mode} mapped {b}"] = digest(rgb) + digest(depth)
+    rng = np.random.default_rng(5)
+    for k in range(6):  # ragged image sizes, random views and budgets
+        w, h = int(rng.integers(1, 151)), int(rng.integers(1, 151))
+        d = rng.normal(size=3)
+        rc = Camera(tuple(d / np.linalg.norm(d) * rng.uniform(1.6, 4.0)), (0, 0, 0), (0, 1, 0), float(rng.uniform(20, 90)), w, h)
+        b = tuple(int(x) for x in rng.integers(0, 31, 3))
+        b = b if any(b) else (0, 0, 20)
+        rgb, depth, mask, st = c.render(ds.levels(), rc, TraceConfig(b), ShadeConfig(specular=0.5), normal_source=k % 2)
+        out["digests"][f"{mode} random {k}"] = digest(rgb) + digest(depth) + digest(mask)
     n = cam.width * cam.height
     rec = records_np(c.trace_image(ds.levels(), cam, TraceConfig((40, 20, 20)))[0])
     for world, tile, bal in ((3, 16, False), (8, 32, True)):
