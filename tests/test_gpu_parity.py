@@ -259,3 +259,43 @@ def test_render_randomized_bitexact(ctx, oracle_built, seed):
     assert np.array_equal(mask.reshape(-1), rmask.reshape(-1)), (w, h, budgets)
     assert np.array_equal(depth.reshape(-1).view(np.uint32), rdepth.reshape(-1).view(np.uint32))
     assert np.max(np.abs(rgb.reshape(-1) - rrgb.reshape(-1))) <= 1e-6
+
+
+@pytest.mark.parametrize("seed", range(int(os.environ.get("NSDF_FUZZ_N", "8"))))
+def test_trace_rays_and_normal_map_randomized_bitexact(ctx, oracle_built, seed):
+    """Randomised ray batches through trace_rays (batch sizes from 1, origins outside, near
+    and inside the surface, directions aimed or random, per-level budgets with zeros) and
+    random point sets through the normal map (on, near and far off the surface: the δ gate,
+    with and without fallback normals) in the FP32 oracle mode against the reference: every
+    HitRecord field and every normal bit for bit, the outside/fallback counts equal."""
+    from oracle import refshim
+    from paper_2201_09147_b200.abi import TraceConfig
+    from paper_2201_09147_b200.engine import DeviceSequence
+    from paper_2201_09147_b200.manifest import load_manifest
+    path = _fixture("torus3.nest")
+    seq = load_manifest(path)
+    ds = DeviceSequence(ctx, seq)
+    rng = np.random.default_rng(3000 + seed)
+    n = 1 if seed == 0 else int(rng.integers(1, 3000))
+    d = rng.normal(size=(n, 3))
+    o = d / np.linalg.norm(d, axis=1, keepdims=True) * rng.uniform(0.0, 4.0, (n, 1))
+    aim = rng.uniform(-0.3, 0.3, (n, 3)) - o
+    rnd = rng.normal(size=(n, 3))
+    dirs = np.where(rng.uniform(size=(n, 1)) < 0.7, aim, rnd)
+    dirs /= np.maximum(np.linalg.norm(dirs, axis=1, keepdims=True), 1e-12)
+    rays = np.concatenate([o, dirs], axis=1).astype(np.float32)
+    budgets = [int(b) for b in rng.integers(0, 31, 3)]
+    if not any(budgets):
+        budgets[1] = 15
+    cfg = TraceConfig(tuple(budgets))
+    _compare_records(ctx.trace_rays(ds.levels(), cfg, rays), refshim.trace_rays(path, cfg, rays))
+    # normal map of the finest member on the traced hits plus random points
+    rec = records_np(refshim.trace_rays(path, cfg, rays))
+    pts = np.concatenate([rec["point"][rec["hit"] == 1], rng.uniform(-1.5, 1.5, (int(rng.integers(1, 500)), 3))])
+    pts = np.ascontiguousarray(pts.T, np.float32)
+    delta = float(seq.deltas[2])
+    fb = None if seed % 2 else rng.normal(size=pts.shape).astype(np.float32)
+    n_gpu, o_gpu, f_gpu = ctx.normal_map(ds.handles[2], pts, delta, fb)
+    n_ref, o_ref, f_ref = refshim.normal_map(path, 2, pts, delta, fb)
+    assert (o_gpu, f_gpu) == (o_ref, f_ref)
+    assert np.array_equal(bits(n_gpu), bits(n_ref))
