@@ -1182,7 +1182,9 @@ TcLaunch tc_failed(cudaError_t e) {
 
 template <int W, bool kGrad, int kTerms, bool kResident, bool kPersist, int kHid>
 TcLaunch launch_w(TcArgs& a, int n_max_items, cudaStream_t s) {
-  constexpr int kGroups = W == 64 ? 1 : (W == 256 && kTerms == 3 ? 4 : 2);
+  // column groups: 256-wide 4 (16 epilogue warps; the 1-term normal tiles too: 24.2k -> 21.6k
+  // cycles per tile, their epilogue being the tile's critical path), 128-wide 2, 64-wide 1
+  constexpr int kGroups = W == 64 ? 1 : (W == 256 ? 4 : 2);
   constexpr int kThreads = 32 * (kResident ? 1 : 2) + 128 * kGroups;
   auto kernel = tc_mlp_kernel<W, kGrad, kGroups, kTerms, kResident, kPersist, kHid>;
   const size_t smem = tc_smem_bytes(W, a.net.n_layers, kTerms, kResident, kPersist);
