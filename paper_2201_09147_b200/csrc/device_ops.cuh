@@ -78,9 +78,15 @@ __device__ __forceinline__ void shade_point(const ShadeParams& sp, float px, flo
         if (hn > 0) {
           const float ndoth = __fdiv_rn(dot3_rn(nx, ny, nz, hx, hy, hz), hn);
           if (ndoth > 0) {
-            // std::pow(float, float): evaluated in double and rounded once (within an ulp of
-            // libm's powf); shading is compared within tolerance, not bitwise.
+            // std::pow(float, float) (libm powf): CUDA's powf is within 2 ulp of it — with
+            // specular * intensity <= 1 that is <= 2.4e-7 of the colour, inside the 1e-6 the
+            // shading is compared at (it is not bitwise: libm's transcendentals are not
+            // restated); NSDF_SHADE_POW_F64=1 evaluates in double and rounds once instead
+#if NSDF_SHADE_POW_F64
             const float pw = __double2float_rn(pow(double(ndoth), double(sp.shininess)));
+#else
+            const float pw = powf(ndoth, sp.shininess);
+#endif
             spec = __fadd_rn(spec, __fmul_rn(__fmul_rn(sp.specular, li), pw));
           }
         }
