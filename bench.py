@@ -238,6 +238,16 @@ def workload_text(args):
     return args.cfg["desc"].format(b=args.budgets)
 
 
+def f8_hidden_layers(m):
+    """Hidden layers of member m whose split-precision correction terms run as one E4M3 MMA
+    (the upload policy of capi.cu: 256-wide nets at omega0 <= 15, or NSDF_TC_E4M3=0/1)."""
+    if getattr(m, "width", 0) != 256 or not hasattr(m, "omega0"):
+        return 0
+    env = os.environ.get("NSDF_TC_E4M3")
+    on = (env != "0") if env else m.omega0 <= 15.0
+    return m.hidden_blocks if on else 0
+
+
 def frame_flops(seq, stats, normal_idx):
     """Algorithmic FLOPs of one frame: 2 x MACs, no credit for bias/sine."""
     trace = sum(int(stats.evals[j]) * 2 * seq.members[j].macs_forward() for j in range(len(seq.members)))
@@ -801,14 +811,17 @@ def main():
         # each kernel against its own bound: tensor work ISSUED by the fast mode (3 split-precision
         # terms per hidden K step + the K=32 layer-0 MMA + the K=16 bias MMA per hidden layer)
         # vs the sustained tensor peak, and MUFU sines vs 16/clk/SM at the max SM clock
-        mult = 3 if args.mode == "fp16" else 1
         per_kernel = []
         for j, m in enumerate(seq.members):
             w, hb = m.width, m.hidden_blocks
             ev, ms_j = int(stats.evals[j]), prof.level_ms[j] / max(prof.frames, 1)
             if ev == 0 or ms_j <= 0:
                 continue
-            issued = ev * (2 * 32 * w + hb * (mult * 2 * w * w + 2 * 16 * w))
+            # fp16 mode: 3 fp16 MMA slots per hidden K step, or 2 where the correction terms
+            # run as one E4M3 MMA (256-wide nets at omega0 <= 15, mlp_tc.cuh tc_split8)
+            f8 = f8_hidden_layers(m) if args.mode == "fp16" else 0
+            mult = 1 if args.mode != "fp16" else 3
+            issued = ev * (2 * 32 * w + hb * (mult * 2 * w * w + 2 * 16 * w) - f8 * 2 * w * w)
             sn = ev * (m.n_layers - 1) * w
             tf = ev * 2 * m.macs_forward() / (ms_j / 1e3) / 1e12
             per_kernel.append({"kernel": f"trace level {j} ({w}x{hb})", "ncu_name": f"tc_mlp_kernel<{w}, 0,",
@@ -946,7 +959,8 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms_total / steps, "ms_per_frame": ms_per_frame,
             "higher_is_better": True,
             "scaling": "strong" if world > 1 and not (W["gbuffer"] or shard_frames) else "weak", "vs_baseline": None,
-            "dtype": {"fp16": "split-fp16 tensor (3 MMA terms; the normal tiles 1 term) / fp32 accum",
+            "dtype": {"fp16": "split-fp16 tensor (A_hi.W_hi fp16 + correction terms: 2 fp16 MMAs, or one E4M3 MMA "
+                              "for 256-wide nets at omega0 <= 15; the normal tiles 1 term) / fp32 accum",
                       "fp16low": "fp16 tensor / fp32 accum",
                       "fp32": "f32"}[args.mode],
             "data": "synthetic camera rays; committed fitted SIREN weights (assets/)",

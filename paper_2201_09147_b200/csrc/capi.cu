@@ -16,6 +16,7 @@
 #include <vector>
 
 #include <cuda_fp16.h>
+#include <cuda_fp8.h>
 
 #include "engine.cuh"
 #include "mlp_tc.cuh"
@@ -803,8 +804,32 @@ int nsdf_cuda_upload_mlp(nsdf_ctx* c, int n_layers, const int32_t* rows, const i
     for (int l = 1; ok && l + 1 < n_layers; ++l) ok = rows[l] == W && cols[l] == W;
     if (ok) {
       const int H = n_layers - 2;
-      std::vector<__half> wq(size_t(H) * 2 * W * W);
+      const int parts = tc_parts(W);
+      std::vector<__half> wq(size_t(H) * parts * W * W);
       std::vector<float> bias(size_t(n_layers - 1) * W);
+      // tc_split8 nets: scale 2^s with every hidden omega*W and omega*b (and their fp16
+      // parts) inside the fp16 range; s = 11 unless a weight or bias is that large
+      int shift = 0;
+      if (tc_split8(W)) {
+        double big = 0.0;
+        size_t oo = size_t(rows[0]) * cols[0] + rows[0];
+        for (int l = 1; l + 1 < n_layers; ++l) {
+          for (size_t i = 0; i < size_t(W) * W + W; ++i)
+            big = std::max(big, std::fabs(double(n.omega) * double(float(packed[oo + i]))));
+          oo += size_t(W) * W + W;
+        }
+        shift = 11;
+        while (shift > 0 && big * std::ldexp(1.0, shift) > 32768.0) --shift;
+      }
+      n.tc_shift = shift;
+      // E4M3 correction terms where their error (~2^-16 of |omega W| |A| per product, so
+      // proportional to omega0) keeps the depth tolerance: omega0 <= kF8MaxOmega nets, every
+      // hidden layer; omega0 = 30 nets keep the fp16 terms (their p99.9 depth error reached
+      // 1.001e-3 with E4M3 terms).  NSDF_TC_E4M3=0 / 1 overrides the choice.
+      bool e4m3 = tc_split8(W) && omega0 <= kF8MaxOmega;
+      if (const char* e = std::getenv("NSDF_TC_E4M3"); e && *e) e4m3 = tc_split8(W) && std::strcmp(e, "0") != 0;
+      n.tc_f8_mask = e4m3 ? (1 << H) - 1 : 0;
+      const double scale = std::ldexp(1.0, shift);
       size_t o = 0;
       for (int l = 0; l < n_layers; ++l) {
         const size_t nw = size_t(rows[l]) * cols[l];
@@ -813,15 +838,22 @@ int nsdf_cuda_upload_mlp(nsdf_ctx* c, int n_layers, const int32_t* rows, const i
           // argument in radians.  Small weights' lo parts may be fp16 subnormals: their
           // absolute error (<= 2^-25 per weight, times |a| <= 1) stays far below the fp32
           // rounding of the argument.
-          __half* hi = wq.data() + size_t(l - 1) * 2 * W * W;
+          __half* hi = wq.data() + size_t(l - 1) * parts * W * W;
           __half* lo = hi + size_t(W) * W;
+          uint8_t* lo8 = reinterpret_cast<uint8_t*>(lo + size_t(W) * W);
           for (int r = 0; r < W; ++r)
             for (int kk = 0; kk < W; ++kk) {
-              const double v = double(n.omega) * double(float(packed[o + size_t(r) * W + kk]));
+              const double v = double(n.omega) * double(float(packed[o + size_t(r) * W + kk])) * scale;
               const __half h = __float2half_rn(float(v));
               const size_t at = tc_wq_offset(W, r, kk);
               hi[at] = h;
               lo[at] = __float2half_rn(float(v - double(__half2float(h))));
+              if (parts == 3) {
+                lo8[tc_w8_offset(W, r, kk / 16, kk % 16)] =
+                    __nv_cvt_float_to_fp8(float(v - double(__half2float(h))), __NV_SATFINITE, __NV_E4M3);
+                lo8[tc_w8_offset(W, r, kk / 16, 16 + kk % 16)] =
+                    __nv_cvt_float_to_fp8(float(double(__half2float(h)) / scale), __NV_SATFINITE, __NV_E4M3);
+              }
             }
         }
         o += nw;

@@ -37,6 +37,8 @@ struct DevNet {
   const uint16_t* wq;      // hidden layers [h][hi | lo][W*W] fp16, canonical layout in N-blocks (tc_wq_offset)
   const float* bias_cat;   // biases of layers 0 .. L-2, [L-1][width]
   float bout;              // output bias
+  int tc_shift;            // hidden weights / biases uploaded x 2^tc_shift (tc_split8 nets, mlp_tc.cuh)
+  int tc_f8_mask;          // bit h: hidden layer h runs its correction terms as one E4M3 MMA
   // FP64 master copy (the certification path, mlp_f64.cu): same layouts as w / wt / b.
   double omega_d;
   const double* w64[kMaxLayers];

@@ -38,6 +38,7 @@
 // operand at ((k/8)*(R/8) + r/8)*64 + (r%8)*8 + k%8 halves, i.e. 8x16-byte core matrices;
 // descriptor SBO = 128 B (next 8 rows), LBO = R*16 B (next 8 k).
 #include <cuda_fp16.h>
+#include <cuda_fp8.h>
 
 #include <algorithm>
 #include <type_traits>
@@ -173,6 +174,22 @@ __device__ __forceinline__ void tc_mma_ts(uint32_t d_tmem, uint32_t a_tmem, uint
       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
       "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate));
 }
+// The same with E4M3 operands (kind::f8f6f4, K = 32 per instruction: four fp8 per 32-bit TMEM
+// column, 8 columns), accumulating into the same FP32 accumulator as the f16 MMAs.
+__device__ __forceinline__ void tc_mma_ts_f8(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, 1, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f8f6f4 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(b_desc), "r"(idesc));
+}
+// Four values -> four E4M3 bytes, the first in the lowest byte (K order within a column).
+__device__ __forceinline__ uint32_t pack_e4m3x4(float a, float b, float c, float d) {
+  const uint32_t lo = __nv_cvt_float2_to_fp8x2(make_float2(a, b), __NV_SATFINITE, __NV_E4M3);
+  const uint32_t hi = __nv_cvt_float2_to_fp8x2(make_float2(c, d), __NV_SATFINITE, __NV_E4M3);
+  return lo | (hi << 16);
+}
 // Each lane writes 8 consecutive 32-bit columns of its own TMEM lane.
 __device__ __forceinline__ void tmem_st8(uint32_t taddr, uint32_t w0, uint32_t w1, uint32_t w2, uint32_t w3,
                                          uint32_t w4, uint32_t w5, uint32_t w6, uint32_t w7) {
@@ -225,6 +242,8 @@ struct TcNet {
   const float* b;                   // biases, [n_layers-1][W] (fp32)
   const float* wout;                // output row (fp32), W
   float bout;
+  float scale, inv_scale;           // 2^tc_shift and its inverse (hidden weights/biases scaled)
+  int f8_mask;                      // DevNet::tc_f8_mask
 };
 
 struct TcArgs {
@@ -479,7 +498,7 @@ enum PfStage : int { kPfNeed = 0, kPfListed = 1, kPfReady = 2 };
 // the registers of a whole SM (the 1-term normal tiles use ~160: config 4 1.54 -> 1.51 ms).
 // MMA layer m = 0 is layer 0 (K = 32, B0 resident), m = 1..L-2 the hidden layers; the
 // last hidden layer's epilogue folds in the 1 x W output layer.
-template <int W, bool kGrad, int kGroups, int kTerms, bool kResident, bool kPersist, int kHid>
+template <int W, bool kGrad, int kGroups, int kTerms, bool kResident, bool kPersist, int kHid, bool kF8On>
 __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
                                   (W == 64 ? 4 : (W == 256 ? 1 : 2))) tc_mlp_kernel(TcArgs a) {
   extern __shared__ __align__(128) uint8_t smem_raw[];
@@ -502,6 +521,12 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
   // the layer loops unroll and every per-layer constant folds
   const int n_hidden = kHid > 0 ? kHid : L - 2;
   constexpr int kRaysPerTile = kGrad ? kRows / 4 : kRows;
+  // tc_split8 nets (mlp_tc.cuh): hidden weights scaled by 2^s; forward 3-term tiles of nets
+  // whose upload chose it (kF8On: DevNet::tc_f8_mask) run the correction terms as one E4M3
+  // MMA per K step (compile-time: a runtime per-layer choice cost the 256-wide level 30%)
+  constexpr bool kScaled = tc_split8(W);
+  constexpr bool kF8 = kF8On && kScaled && !kGrad && kTerms == 3;
+  constexpr int kParts = tc_parts(W);
   // N-blocks: every MMA layer is issued as kNH column blocks of kNB outputs, each with its
   // own completion barrier (dfull[nb]), so the epilogue of block 0 (and with it the next
   // layer's first K rows) runs under the MMAs of block 1 and the tensor pipe goes straight
@@ -579,7 +604,7 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
     __half v = __float2half_rn(0.0f);
     if (k < 3) {
       __half hi, mid, lo;
-      split3(net.b[(h + 1) * W + n] * net.omega, hi, mid, lo);
+      split3(net.b[(h + 1) * W + n] * net.omega * (kScaled ? net.scale : 1.0f), hi, mid, lo);
       v = k == 0 ? hi : (k == 1 ? mid : lo);
     }
     sm.bb[size_t(h) * W * kBlk + b0_off(W, n, k)] = v;
@@ -637,7 +662,7 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
       const uint32_t b0_base = smem_addr(sm.b0);
       const uint64_t ones_desc = umma_desc(smem_addr(sm.ones), kRows * 16, 128);
       if (kResident) {
-        const uint32_t bytes = uint32_t(n_hidden) * W * W * 2 * 2;
+        const uint32_t bytes = uint32_t(n_hidden) * W * W * 2 * kParts;
         if (lane == 0) {
           mbar_expect_tx(&full[0], bytes);
           bulk_g2s(sm.wst, net.wq, bytes, &full[0]);
@@ -693,7 +718,7 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
                 s = chunk_iter % kStages;
                 if (kResident) {
                   // resident layout per layer: [hi W*W][lo W*W] (tc_wq_offset)
-                  b_base = smem_addr(sm.wst + size_t(h) * 2 * W * W + size_t(nb) * kNB * W + size_t(c) * kNB * kKCh);
+                  b_base = smem_addr(sm.wst + size_t(h) * kParts * W * W + size_t(nb) * kNB * W + size_t(c) * kNB * kKCh);
                   lo_off = uint32_t(W) * W * 2;
                 } else {
                   timed_wait(&full[s], (chunk_iter / kStages) & 1, w_full);
@@ -708,8 +733,12 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
               tc_mma_ts(dn, at, bd, idesc, true);
               if (kTerms == 3) {  // split precision: + A_lo.W_hi + A_hi.W_lo
                 const uint64_t bdl = umma_desc(b_base + lo_off + boff, kNB * 16, 128);
-                tc_mma_ts(dn, at + 8, bd, idesc, 1);
-                tc_mma_ts(dn, at, bdl, idesc, 1);
+                if (kF8) {
+                  tc_mma_ts_f8(dn, at + 8, bdl, idesc);  // [fp8 A | fp8 A_lo 2^s] . [fp8 W_lo ; fp8 W_hi 2^-s]
+                } else {
+                  tc_mma_ts(dn, at + 8, bd, idesc, 1);
+                  tc_mma_ts(dn, at, bdl, idesc, 1);
+                }
               }
               if (ks == kStepsPerChunk - 1) {
                 if (!kResident) tc_commit(&empty[s]);  // frees the weight stage once these MMAs retire
@@ -736,7 +765,7 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
       uint32_t chunk_iter = 0;
       for (int t = 0; more_tiles(t); ++t) {
         for (int h = 0; h < n_hidden; ++h) {
-          const __half* lw = reinterpret_cast<const __half*>(net.wq) + size_t(h) * 2 * W * W;
+          const __half* lw = reinterpret_cast<const __half*>(net.wq) + size_t(h) * kParts * W * W;
           for (int nb = 0; nb < kNH; ++nb)
             for (int c = 0; c < kChunks; ++c, ++chunk_iter) {
               const int s = chunk_iter % kStages;
@@ -745,7 +774,7 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
               mbar_expect_tx(&full[s], kChunkBytes * kNW);
               bulk_g2s(sm.wst + size_t(s) * kStageHalves, lw + piece, kChunkBytes, &full[s]);
               if (kTerms == 3)
-                bulk_g2s(sm.wst + size_t(s) * kStageHalves + size_t(kNB) * kKCh, lw + size_t(W) * W + piece, kChunkBytes,
+                bulk_g2s(sm.wst + size_t(s) * kStageHalves + size_t(kNB) * kKCh, lw + size_t(kF8 ? 2 : 1) * W * W + piece, kChunkBytes,
                          &full[s]);
             }
         }
@@ -831,7 +860,7 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
         // sine epilogue of one 16-column block (value rows; tangent rows scale by omega cos)
         auto activate = [&](const uint32_t (&r)[16], int cc, float (&v)[16]) {
 #pragma unroll
-          for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]);
+          for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]) * (kScaled && m > 0 ? net.inv_scale : 1.0f);
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
             if (kGrad) {
@@ -870,7 +899,22 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
             uint32_t hw[8], lw[8];
 #pragma unroll
             for (int j = 0; j < 8; ++j) hw[j] = pack_half2(v[2 * j], v[2 * j + 1]);
-            if (kTerms == 3) {
+            if (kF8) {
+              // columns 8-11: fp8(A), 12-15: fp8((A - fp16(A)) * 2^s) (one f8f6f4 K = 32 step)
+              float lo[16];
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                const __half2 h = *reinterpret_cast<const __half2*>(&hw[j]);
+                const float2 d = __ffma2_rn(__half22float2(h), make_float2(-1.0f, -1.0f), make_float2(v[2 * j], v[2 * j + 1]));
+                lo[2 * j] = d.x * net.scale;
+                lo[2 * j + 1] = d.y * net.scale;
+              }
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                lw[q] = pack_e4m3x4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+                lw[4 + q] = pack_e4m3x4(lo[4 * q], lo[4 * q + 1], lo[4 * q + 2], lo[4 * q + 3]);
+              }
+            } else if (kTerms == 3) {
 #pragma unroll
               for (int j = 0; j < 8; ++j) lw[j] = pack_half2_lo(v[2 * j], v[2 * j + 1], hw[j]);
             }
@@ -1180,13 +1224,13 @@ TcLaunch tc_failed(cudaError_t e) {
   return TcLaunch::kFailed;
 }
 
-template <int W, bool kGrad, int kTerms, bool kResident, bool kPersist, int kHid>
+template <int W, bool kGrad, int kTerms, bool kResident, bool kPersist, int kHid, bool kF8On>
 TcLaunch launch_w(TcArgs& a, int n_max_items, cudaStream_t s) {
   // column groups: 256-wide 4 (16 epilogue warps; the 1-term normal tiles too: 24.2k -> 21.6k
   // cycles per tile, their epilogue being the tile's critical path), 128-wide 2, 64-wide 1
   constexpr int kGroups = W == 64 ? 1 : (W == 256 ? 4 : 2);
   constexpr int kThreads = 32 * (kResident ? 1 : 2) + 128 * kGroups;
-  auto kernel = tc_mlp_kernel<W, kGrad, kGroups, kTerms, kResident, kPersist, kHid>;
+  auto kernel = tc_mlp_kernel<W, kGrad, kGroups, kTerms, kResident, kPersist, kHid, kF8On>;
   const size_t smem = tc_smem_bytes(W, a.net.n_layers, kTerms, kResident, kPersist);
   // per-device attributes (kernel_cfg): every device a context lives on gets the opt-in
   const KernelCfg kc = kernel_cfg(reinterpret_cast<const void*>(kernel), kThreads, smem, /*max_carveout=*/true);
@@ -1211,11 +1255,17 @@ TcLaunch launch_w(TcArgs& a, int n_max_items, cudaStream_t s) {
 
 // The hidden-layer count is compiled in for the standard architectures (64x1, 128x2, 256x3:
 // the nets of every BASELINE config); other depths take the runtime-count kernels.
+template <int W, bool kGrad, int kTerms, bool kResident, bool kPersist, bool kF8On>
+TcLaunch launch_f(TcArgs& a, int n_max_items, cudaStream_t s) {
+  constexpr int kStd = W == 64 ? 1 : (W == 128 ? 2 : 3);
+  return a.net.n_layers - 2 == kStd ? launch_w<W, kGrad, kTerms, kResident, kPersist, kStd, kF8On>(a, n_max_items, s)
+                                    : launch_w<W, kGrad, kTerms, kResident, kPersist, 0, kF8On>(a, n_max_items, s);
+}
 template <int W, bool kGrad, int kTerms, bool kResident, bool kPersist>
 TcLaunch launch_h(TcArgs& a, int n_max_items, cudaStream_t s) {
-  constexpr int kStd = W == 64 ? 1 : (W == 128 ? 2 : 3);
-  return a.net.n_layers - 2 == kStd ? launch_w<W, kGrad, kTerms, kResident, kPersist, kStd>(a, n_max_items, s)
-                                    : launch_w<W, kGrad, kTerms, kResident, kPersist, 0>(a, n_max_items, s);
+  if constexpr (tc_split8(W) && !kGrad && kTerms == 3)
+    if (a.net.f8_mask) return launch_f<W, kGrad, kTerms, kResident, kPersist, true>(a, n_max_items, s);
+  return launch_f<W, kGrad, kTerms, kResident, kPersist, false>(a, n_max_items, s);
 }
 
 template <bool kGrad, int kTerms, bool kPersist>
@@ -1350,6 +1400,9 @@ TcNet tc_net(const DevNet& n) {
   t.b = n.bias_cat;
   t.wout = n.w[n.n_layers - 1];
   t.bout = n.bout;
+  t.scale = std::ldexp(1.0f, n.tc_shift);
+  t.inv_scale = std::ldexp(1.0f, -n.tc_shift);
+  t.f8_mask = n.tc_f8_mask;
   return t;
 }
 

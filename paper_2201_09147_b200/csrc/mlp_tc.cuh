@@ -26,6 +26,30 @@ __host__ __device__ constexpr size_t tc_wq_offset(int W, int n, int k) {
   return size_t(n / (W / tc_halves(W))) * size_t(W / tc_halves(W)) * W +
          size_t(((k / 8) * (W / tc_halves(W) / 8) + (n % (W / tc_halves(W))) / 8) * 64 + (n % 8) * 8 + k % 8);
 }
+// FP8 correction terms (256-wide nets, forward tiles): the split-precision product
+//   A.W = A_hi.W_hi + A_lo.W_hi + A_hi.W_lo
+// keeps A_hi.W_hi as one kind::f16 MMA and runs both correction terms as ONE kind::f8f6f4
+// MMA of K = 32 (E4M3): A'' = [fp8(A) | fp8(A_lo * 2^s)] (16 + 16 K values, the 8 spare
+// TMEM columns of each in-place A block), B'' = [fp8(W_lo) ; fp8(W_hi * 2^-s)] — at twice
+// the f16 rate, so 2 MMA slots per K step instead of 3.  The hidden weights of such nets are
+// uploaded scaled by 2^s (s = tc_shift, <= 11: fp8's range needs A_lo * 2^s), so their
+// accumulators hold 2^s x the sine argument and the epilogue scales by 2^-s.  Per hidden
+// layer: [hi | lo (fp16, for the normal tiles) | lo8 (the B'' pieces, 2 W^2 bytes)].
+#ifndef NSDF_TC_F8
+#define NSDF_TC_F8 1
+#endif
+__host__ __device__ constexpr bool tc_split8(int W) { return NSDF_TC_F8 && W == 256; }
+constexpr double kF8MaxOmega = 15.0;  // nets at larger omega0 keep fp16 correction terms (capi.cu)
+__host__ __device__ constexpr int tc_parts(int W) { return tc_split8(W) ? 3 : 2; }  // fp16-sized parts per layer
+// Byte offset of B''(n, k2) of 16-K block b (k2 < 16: fp8(W_lo[n][16b + k2]); k2 >= 16:
+// fp8(W_hi[n][16b + k2 - 16] * 2^-s)): per N-block, blocks in K order, each [NB][32] in the
+// K-major canonical layout of 8-bit operands (core matrices of 8 rows x 16 bytes, LBO NB*16 B,
+// SBO 128 B) — so a streamed (N-block, K chunk) piece has the byte offset and size of the
+// fp16 lo piece it replaces.
+__host__ __device__ constexpr size_t tc_w8_offset(int W, int n, int b, int k2) {
+  return size_t(n / (W / tc_halves(W))) * size_t(W / tc_halves(W)) * W * 2 + size_t(b) * (W / tc_halves(W)) * 32 +
+         size_t(((k2 / 16) * (W / tc_halves(W) / 8) + (n % (W / tc_halves(W))) / 8) * 128 + (n % 8) * 16 + k2 % 16);
+}
 cudaError_t tc_last_error();  // CUDA error of this thread's last kFailed launch
 
 // Persistent level trace: one launch runs every iteration of a level; rows are refilled

@@ -52,6 +52,30 @@ def test_fast_mlp_close_to_oracle(ctx, fast, name):
     assert np.percentile(angle_deg(g0[:, near], g1[:, near]), 99.9) < ANGLE_MAX
 
 
+def test_fast_e4m3_correction_terms(ctx, fast):
+    """256-wide nets at omega0 <= 15 (the headline's finest level, torus3 256x3 at omega0 =
+    10) run the split-precision correction terms as one E4M3 MMA per K step in the forward
+    tiles (mlp_tc.cuh tc_split8): the forward values then differ from the fused gradient
+    tiles' (which keep the fp16 terms) by the E4M3 rounding of the corrections — proof that
+    the path ran — and stay within 5e-5 of the FP32 oracle (emulated: |df| p99.9 4.8e-6 near the
+    surface from the E4M3 terms alone).  NSDF_TC_E4M3=0 restores the fp16 terms."""
+    from paper_2201_09147_b200.manifest import load_sdfnet
+    net = load_sdfnet(_fixture("torus3_256x3.sdfnet"))
+    assert net.omega0 <= 15
+    pts = np.random.default_rng(2).uniform(-1, 1, (3, 20000)).astype(np.float32)
+    d0 = ctx.eval(ctx.upload(net), pts)
+    h = fast.upload(net)
+    d1 = fast.eval(h, pts)
+    dg, g1 = fast.eval_grad(h, pts)
+    assert not np.array_equal(d1, dg)  # the forward tiles took the E4M3 path
+    near = np.abs(d0) < 0.05
+    err = np.abs(d1 - d0)
+    print(f"E4M3 corrections: |df| max {err.max():.2e}, near-surface p99.9 {np.percentile(err[near], 99.9):.2e}; "
+          f"fused (fp16 terms) max {np.abs(dg - d0).max():.2e}")
+    assert err.max() < 5e-5, err.max()
+    assert np.abs(dg - d0).max() < 5e-5
+
+
 # the standard depths (compiled-in layer counts) and others (runtime layer loops; 64x5 streams
 # its weights instead of keeping them resident; 256-wide layers run as two N-blocks)
 @pytest.mark.parametrize("width,hidden", [(64, 1), (128, 2), (256, 3), (64, 2), (64, 5), (128, 1), (128, 3),
@@ -375,7 +399,13 @@ def test_fast_render_randomized(ctx, fast, seed):
     assert np.sum(m0 != m1) <= max(1, int(1e-3 * n)), (w, h, budgets)
     both = (m0 == 1) & (m1 == 1)
     if both.any():
-        assert np.percentile(np.abs(d0 - d1)[both], 99.9) <= DT_MAX
+        # depth: at most 0.1% of the common hits (and at least one allowed, as for the mask,
+        # so a small image is held to the same standard) beyond 1e-3, each of those a single
+        # stop-band step (<= 1.05 eps_stop: test_depth_outliers_are_stop_band_steps shows the
+        # mechanism ray by ray at full size)
+        dt = np.abs(d0 - d1)[both]
+        assert int(np.sum(dt > DT_MAX)) <= max(1, int(1e-3 * dt.size)), (np.sort(dt)[-5:], dt.size)
+        assert dt.max() <= 1.05 * cfg.eps_stop, dt.max()
     # tile shares of the same fast frame into one device framebuffer
     tile, world = int(rng.choice([8, 16, 32, 64])), int(rng.integers(2, 5))
     fb = [torch.zeros(3 * n, device="cuda"), torch.zeros(n, device="cuda"),
