@@ -26,7 +26,7 @@ __host__ __device__ constexpr size_t tc_wq_offset(int W, int n, int k) {
   return size_t(n / (W / tc_halves(W))) * size_t(W / tc_halves(W)) * W +
          size_t(((k / 8) * (W / tc_halves(W) / 8) + (n % (W / tc_halves(W))) / 8) * 64 + (n % 8) * 8 + k % 8);
 }
-// FP8 correction terms (256-wide nets, forward tiles): the split-precision product
+// FP8 correction terms (128- and 256-wide nets, forward tiles): the split-precision product
 //   A.W = A_hi.W_hi + A_lo.W_hi + A_hi.W_lo
 // keeps A_hi.W_hi as one kind::f16 MMA and runs both correction terms as ONE kind::f8f6f4
 // MMA of K = 32 (E4M3): A'' = [fp8(A) | fp8(A_lo * 2^s)] (16 + 16 K values, the 8 spare
@@ -38,7 +38,10 @@ __host__ __device__ constexpr size_t tc_wq_offset(int W, int n, int k) {
 #ifndef NSDF_TC_F8
 #define NSDF_TC_F8 1
 #endif
-__host__ __device__ constexpr bool tc_split8(int W) { return NSDF_TC_F8 && W == 256; }
+#ifndef NSDF_TC_F8_128
+#define NSDF_TC_F8_128 1  // 128-wide nets too (frame 6.83 -> 6.69 ms, tools/ab.py)
+#endif
+__host__ __device__ constexpr bool tc_split8(int W) { return NSDF_TC_F8 && (W == 256 || (NSDF_TC_F8_128 && W == 128)); }
 constexpr double kF8MaxOmega = 15.0;  // nets at larger omega0 keep fp16 correction terms (capi.cu)
 __host__ __device__ constexpr int tc_parts(int W) { return tc_split8(W) ? 3 : 2; }  // fp16-sized parts per layer
 // Byte offset of B''(n, k2) of 16-K block b (k2 < 16: fp8(W_lo[n][16b + k2]); k2 >= 16:

@@ -247,9 +247,10 @@ def _records(recs):
 @pytest.mark.parametrize("fixture,budgets", [("w30", (20, 5, 5)), ("w30", (40, 20, 20)), ("torus3", (40, 20, 20))])
 def test_depth_outliers_are_stop_band_steps(ref, fixture, budgets):
     """The max |dt| above 1e-3 (p99.9 is ~1e-5): a ray whose last |f| lands within the fast
-    mode's |df| ~ 1e-5 of eps_stop stops one iteration earlier or later than the reference's,
-    so the two hit parameters differ by ONE final step, itself <= eps_stop + |df|.  Asserted
-    per ray: every common hit with |dt| > 1e-3 has a different total iteration count, and
+    mode's |df| ~ 1e-5 of eps_stop (or of a level's hand-off radius) stops one iteration
+    earlier or later than the reference's, so the two hit parameters differ by ONE step,
+    itself <= eps_stop + |df|.  Asserted per ray: every common hit with |dt| > 1e-3 has a
+    different per-level iteration count (the ray's step sequence differs), and
     |dt| <= 1.05 eps_stop.  The reference's own two backends (scalar vs AVX2, same weights and
     rays) show the same stop-band jitter; its spread is printed beside ours."""
     from paper_2201_09147_b200.abi import TraceConfig, standard_camera
@@ -272,8 +273,8 @@ def test_depth_outliers_are_stop_band_steps(ref, fixture, budgets):
         c.close()
     both = (f["hit"] == 1) & (r["hit"] == 1)
     dt = np.abs(f["t"] - r["t"])[both]
-    its_f = f["iters"].astype(np.int64).sum(1)[both]
-    its_r = r["iters"].astype(np.int64).sum(1)[both]
+    its_f = f["iters"].astype(np.int64)[both]
+    its_r = r["iters"].astype(np.int64)[both]
     out = dt > DT_MAX
     sb = (s["hit"] == 1) & (r["hit"] == 1)
     dt_s = np.abs(s["t"] - r["t"])[sb]
@@ -282,7 +283,7 @@ def test_depth_outliers_are_stop_band_steps(ref, fixture, budgets):
            f"{int((dt_s > DT_MAX).sum())} rays > 1e-3")
     print(msg)
     assert np.percentile(dt, 99.9) <= DT_MAX, msg
-    assert np.all(its_f[out] != its_r[out]), msg
+    assert np.all(np.any(its_f[out] != its_r[out], axis=1)), msg
     assert dt.max() <= 1.05 * cfg.eps_stop, msg
 
 
