@@ -276,7 +276,7 @@ std::vector<LevelDesc> traced_levels(nsdf_ctx* c, const nsdf_level* levels, int 
     d.budget = cfg->budgets[j];
     d.level = j;
     out.push_back(d);
-    nc += 3 + d.budget;  // adv count, claim cursor, evaluations, iteration list sizes
+    nc += 5 + d.budget;  // adv count, claim cursor, evaluations, refine count + cursor, iteration list sizes
   }
   *n_counters = nc + 2;  // + fallback count + spare
   return out;
@@ -295,7 +295,7 @@ void fill_stats(const std::vector<LevelDesc>& lv, const TraceResult& tr, const s
     } else {
       for (int it = 0; it < lv[i].budget; ++it) {
         ev += uint64_t(cur);
-        cur = counters[base + 3 + it];
+        cur = counters[base + 5 + it];
       }
     }
     stats->evals[lv[i].level] = ev;

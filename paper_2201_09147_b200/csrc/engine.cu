@@ -413,9 +413,11 @@ TraceResult run_trace(Mode mode, const std::vector<LevelDesc>& levels, float eps
     int* adv_count = fb.counters + coff;
     int* cursor = fb.counters + coff + 1;
     int* evals = fb.counters + coff + 2;
-    int* it_counts = fb.counters + coff + 3;
+    int* refine_count = fb.counters + coff + 3;
+    int* refine_cursor = fb.counters + coff + 4;
+    int* it_counts = fb.counters + coff + 5;
     res.counter_layout_base.push_back(coff);
-    coff += 3 + lv.budget;
+    coff += 5 + lv.budget;
     IterArgs a;
     a.lv = lv;
     a.eps = eps;
@@ -432,9 +434,20 @@ TraceResult run_trace(Mode mode, const std::vector<LevelDesc>& levels, float eps
     nvtxRangePushA(range);
     // fast mode: ONE persistent launch per level (rows refilled from the input list)
     TcLaunch tl = TcLaunch::kDeclined;
+    // An E4M3 final level parks near-threshold stop decisions on the free list (fb.list[nxt]:
+    // the persistent path does not ping-pong) and finishes them in a resume launch with the
+    // fp16 correction terms: a flipped stop decision moves the hit by one ~eps_stop step (a
+    // flipped hand-off between levels only shifts where the next level starts)
+    const bool refine = lv.final_level && mode_tc(mode) && mode_terms(mode) == 3 && lv.field.kind == kFieldMlp &&
+                        tc_supported(lv.field.net) && tc_uses_e4m3(lv.field.net);
     if (mode_tc(mode) && lv.field.kind == kFieldMlp && tc_supported(lv.field.net))
       tl = tc_trace_level(mode_terms(mode), lv, eps, t_max, in_list, in_count, cursor, evals, fb.list[adv], adv_count,
-                          fb.st, n_max, s);
+                          fb.st, n_max, s, refine ? fb.list[nxt] : nullptr, refine ? refine_count : nullptr);
+    if (tl == TcLaunch::kRan && refine) {
+      tl = tc_trace_level(mode_terms(mode), lv, eps, t_max, fb.list[nxt], refine_count, refine_cursor, evals,
+                          fb.list[adv], adv_count, fb.st, n_max, s, nullptr, nullptr, /*resume=*/true);
+      res.launches++;
+    }
     if (tl == TcLaunch::kFailed) {  // no silent FFMA fallback: the frame fails
       nvtxRangePop();
       res.error = tc_last_error();

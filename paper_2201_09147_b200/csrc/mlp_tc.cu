@@ -12,7 +12,9 @@
 //   hidden layers        D[128 x W] (fp32, TMEM) = A[128 x W] (fp16 hi/lo, TMEM: written in
 //                        place over the previous layer's accumulator) . W_l^T (fp16
 //                        hi/lo): tcgen05.mma.cta_group::1.kind::f16, M=128 N=W K=16, three
-//                        terms per K step (split precision), issued by one thread; 256-wide
+//                        terms per K step (split precision) — or, for 128/256-wide nets at
+//                        omega0 <= 15, A_hi.W_hi in f16 + both corrections as one
+//                        kind::f8f6f4 K=32 MMA (mlp_tc.cuh tc_split8) — issued by one thread; 256-wide
 //                        layers as two N = 128 column blocks with their own completion
 //                        barriers (the epilogue of block 0 runs under block 1's MMAs and the
 //                        next layer follows without a drain); weights SMEM-resident (64-wide)
@@ -261,6 +263,12 @@ struct TcArgs {
   int* adv_count;
   int* cursor;   // claim cursor into in_list
   int* evals;    // evaluation counter
+  // E4M3 final levels: a ray whose stop decision lies within kRefineBand of eps is parked
+  // (state written back, the evaluation not counted) on refine_list; a second launch with
+  // the fp16 correction terms resumes those rays (resume: iteration count from st.iters)
+  int* refine_list;
+  int* refine_count;
+  int resume;
   RayState st;
   // normals
   float time;
@@ -308,6 +316,10 @@ struct TcSmem {
   int* done;            // persistent level: no more tiles
 };
 constexpr int kStageCap = 512;
+// |decision - eps| below which an E4M3 level defers a ray's stop / hand-off decision to the
+// fp16-term resume launch: > 2x the largest E4M3-vs-fp16 difference of f measured on the
+// fixtures (2.1e-5), so both launches decide every ray as the fp16 terms would
+constexpr float kRefineBand = 5e-5f;
 constexpr int kNumBars = 2 * kMaxStages + kMaxSub + 4;  // full, empty, kready, a0ready, tstart, dfull[2]
 
 __host__ __device__ inline size_t tc_weight_bytes(int W, int L, int terms, bool resident) {
@@ -958,7 +970,7 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
       const uint32_t lt = (1u << lane) - 1u;
       int slot = -1, it = 0, evals = 0, n_tiles = 0;
       float px = 0.f, py = 0.f, pz = 0.f, t = 0.f, dx = 0.f, dy = 0.f, dz = 0.f;
-      int pf_slot = -1, pf_stage = kPfNeed;
+      int pf_slot = -1, pf_stage = kPfNeed, fit = 0;  // fit: prefetched iteration count (resume)
       float fpx = 0.f, fpy = 0.f, fpz = 0.f, fpt = 0.f, fdx = 0.f, fdy = 0.f, fdz = 0.f;
       int res_base = 0, res_end = 0, nres = 0;  // claimed list range; next claim ticket (lane 0)
       bool exhausted = false;
@@ -973,7 +985,7 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
           // common case: every empty row's own prefetch is ready (no shuffles)
           if (slot < 0) {
             slot = pf_slot;
-            it = 0;
+            it = fit;
             px = fpx, py = fpy, pz = fpz, t = fpt, dx = fdx, dy = fdy, dz = fdz;
             st.level_reached[slot] = a.lv.level;
             pf_stage = kPfNeed;
@@ -984,13 +996,14 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
           const bool take = slot < 0 && r < k;
           const int src = take ? nth_set_bit(rdy, r) : lane;
           const int s_slot = __shfl_sync(0xffffffffu, pf_slot, src);
+          const int s_it = __shfl_sync(0xffffffffu, fit, src);
           const float s_px = __shfl_sync(0xffffffffu, fpx, src), s_py = __shfl_sync(0xffffffffu, fpy, src),
                       s_pz = __shfl_sync(0xffffffffu, fpz, src), s_t = __shfl_sync(0xffffffffu, fpt, src),
                       s_dx = __shfl_sync(0xffffffffu, fdx, src), s_dy = __shfl_sync(0xffffffffu, fdy, src),
                       s_dz = __shfl_sync(0xffffffffu, fdz, src);
           if (take) {
             slot = s_slot;
-            it = 0;
+            it = s_it;
             px = s_px, py = s_py, pz = s_pz, t = s_t, dx = s_dx, dy = s_dy, dz = s_dz;
             st.level_reached[slot] = a.lv.level;
           }
@@ -1008,6 +1021,7 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
           fdx = __ldg(st.dx + pf_slot);
           fdy = __ldg(st.dy + pf_slot);
           fdz = __ldg(st.dz + pf_slot);
+          fit = a.resume ? int(st.iters[size_t(pf_slot) * kMaxLevels + a.lv.level]) : 0;
           pf_stage = kPfReady;
         }
         if (W == 64) mark(9);
@@ -1084,7 +1098,7 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
         mark(11);
         if (g0) {
           const int s0 = slot;
-          bool conv = false;
+          bool conv = false, parked = false;
           if (slot >= 0) {
             // trace update (trace.cpp:61-84; same arithmetic as trace_update, device_ops.cuh)
             ++evals;
@@ -1093,7 +1107,19 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
             const float afd = fabsf(fd);
             conv = a.lv.final_level ? afd <= a.eps : fd <= a.eps;
             bool cont = false;
-            if (!conv) {
+            bool park = false;
+            if constexpr (kF8) park = a.refine_list && fabsf(afd - a.eps) <= kRefineBand;
+            parked = park;
+            if (park) {
+              // defer the decision: the state as it was before this evaluation, for the resume
+              st.px[slot] = px;
+              st.py[slot] = py;
+              st.pz[slot] = pz;
+              st.t[slot] = t;
+              st.iters[size_t(slot) * kMaxLevels + a.lv.level] = uint16_t(it);
+              --evals;
+              conv = false;
+            } else if (!conv) {
               float step = fd;
               if (a.lv.final_level && step < 0.0f) step = 0.0f;  // trace.cpp:73
               px = __fadd_rn(px, __fmul_rn(step, dx));
@@ -1102,8 +1128,10 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
               t = __fadd_rn(t, step);
               cont = !(t > a.t_max);  // trace.cpp:78
             }
-            ++it;
-            if (!cont || it == a.lv.budget) {  // the ray leaves the level: write its state once
+            if (!park) ++it;
+            if (park) {
+              slot = -1;
+            } else if (!cont || it == a.lv.budget) {  // the ray leaves the level: write its state once
               st.px[slot] = px;
               st.py[slot] = py;
               st.pz[slot] = pz;
@@ -1111,6 +1139,20 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
               st.iters[size_t(slot) * kMaxLevels + a.lv.level] = uint16_t(it);
               st.final_dist[slot] = afd;
               slot = -1;
+            }
+          }
+          if constexpr (kF8) {
+            // parked rays -> refine list (rare: one aggregated atomic per warp that has any)
+            if (a.refine_list) {
+              const unsigned pm = __ballot_sync(0xffffffffu, parked);
+              if (pm) {
+                const int leader = __ffs(pm) - 1;
+                int base = 0;
+                if (lane == leader) base = atomicAdd(a.refine_count, __popc(pm));
+                base = __shfl_sync(0xffffffffu, base, leader);
+                const int at = base + __popc(pm & lt);
+                if (parked && in_bounds(at, st.cap, kChkListWrite)) a.refine_list[at] = s0;
+              }
             }
           }
           mark(12);
@@ -1264,7 +1306,7 @@ TcLaunch launch_f(TcArgs& a, int n_max_items, cudaStream_t s) {
 template <int W, bool kGrad, int kTerms, bool kResident, bool kPersist>
 TcLaunch launch_h(TcArgs& a, int n_max_items, cudaStream_t s) {
   if constexpr (tc_split8(W) && !kGrad && kTerms == 3)
-    if (a.net.f8_mask) return launch_f<W, kGrad, kTerms, kResident, kPersist, true>(a, n_max_items, s);
+    if (a.net.f8_mask && !a.resume) return launch_f<W, kGrad, kTerms, kResident, kPersist, true>(a, n_max_items, s);
   return launch_f<W, kGrad, kTerms, kResident, kPersist, false>(a, n_max_items, s);
 }
 
@@ -1409,13 +1451,17 @@ TcNet tc_net(const DevNet& n) {
 }  // namespace
 
 bool tc_supported(const DevNet& n) { return n.tc_ok != 0; }
+bool tc_uses_e4m3(const DevNet& n) { return n.tc_ok != 0 && n.tc_f8_mask != 0 && tc_split8(n.rows[0]); }
 
 cudaError_t tc_last_error() { return g_tc_error; }
 
 TcLaunch tc_trace_level(int terms, const LevelDesc& lv, float eps, float t_max, const int* in_list, const int* in_count,
                     int* cursor, int* evals, int* adv_list, int* adv_count, const RayState& st, int n_max,
-                    cudaStream_t s) {
+                    cudaStream_t s, int* refine_list, int* refine_count, bool resume) {
   TcArgs a{};
+  a.refine_list = refine_list;
+  a.refine_count = refine_count;
+  a.resume = resume ? 1 : 0;
   a.terms = terms;
   a.net = tc_net(lv.field.net);
   a.op = kOpTrace;

@@ -58,9 +58,14 @@ cudaError_t tc_last_error();  // CUDA error of this thread's last kFailed launch
 // Persistent level trace: one launch runs every iteration of a level; rows are refilled
 // from in_list (claimed through *cursor) until it drains.  Converged slots -> adv_list,
 // evaluations -> *evals.  cursor / evals / adv_count must be zeroed.
+// E4M3 levels (tc_uses_e4m3): with refine_list (final levels), rays whose stop decision falls
+// within a small band of eps are parked there (count in *refine_count); a second call with
+// resume = true over that list (fp16 correction terms, iteration counts from st.iters)
+// finishes them, so every decision is the fp16-term one.
 TcLaunch tc_trace_level(int terms, const LevelDesc& lv, float eps, float t_max, const int* in_list, const int* in_count,
                     int* cursor, int* evals, int* adv_list, int* adv_count, const RayState& st, int n_max,
-                    cudaStream_t s);
+                    cudaStream_t s, int* refine_list = nullptr, int* refine_count = nullptr, bool resume = false);
+bool tc_uses_e4m3(const DevNet& n);
 TcLaunch tc_normals_shade(int terms, const DevField& nf, float time, const int* list, const int* count, int n_max,
                       const RayState& st, const ShadeParams& sp, bool defer_fallback, int* fb_list, int* fb_count,
                       float* rgb, float* depth, uint8_t* mask, cudaStream_t s);

@@ -343,3 +343,33 @@ def test_render_normal_tiles_within_tolerance(ref, fixture):
           f"{np.percentile(ang, 99.9):.4f} max {ang.max():.4f} deg")
     assert both.sum() > 0.99 * (m16 & m_ref).sum()
     assert ang.max() <= NORMAL_DEG_MAX
+
+
+def test_e4m3_stop_decisions_refined(ref, monkeypatch):
+    """The headline's finest level runs E4M3 correction terms (mlp_tc.cuh tc_split8); its
+    stop decisions within kRefineBand of eps_stop are parked and re-decided by a resume
+    launch with the fp16 terms (engine.cu run_trace).  Against the reference on the headline
+    frame, the E4M3 engine then has no more rays beyond the 1e-3 depth tolerance than the
+    all-fp16 engine (NSDF_TC_E4M3=0) — without the resume pass it had ~20x more (155 vs 7 of
+    223,683 hits) — and each of them is a one-step stop-band difference."""
+    from paper_2201_09147_b200.abi import TraceConfig, standard_camera
+    from paper_2201_09147_b200.engine import Context, DeviceSequence
+    from paper_2201_09147_b200.manifest import load_manifest
+    path = _torus3()
+    cam, cfg = standard_camera(1920, 1080), TraceConfig((40, 20, 20))
+    r = _records(ref.trace_image(path, cam, cfg))
+    counts = {}
+    for e4m3 in ("0", "1"):
+        monkeypatch.setenv("NSDF_TC_E4M3", e4m3)  # read at upload
+        c = Context(0, "fp16")
+        try:
+            recs, _ = c.trace_image(DeviceSequence(c, load_manifest(path)).levels(), cam, cfg)
+        finally:
+            c.close()
+        f = _records(recs)
+        both = (f["hit"] == 1) & (r["hit"] == 1)
+        dt = np.abs(f["t"] - r["t"])[both]
+        counts[e4m3] = int((dt > DT_MAX).sum())
+        assert dt.max() <= 1.05 * cfg.eps_stop, (e4m3, dt.max())
+    print(f"rays beyond 1e-3 of the reference: fp16 terms {counts['0']}, E4M3 terms + resume {counts['1']}")
+    assert counts["1"] <= max(3, 2 * counts["0"]), counts
