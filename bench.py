@@ -127,7 +127,7 @@ def ncu_traffic(gbuffer: bool):
     if not files or gbuffer:
         return None, None
     d = json.load(open(files[-1]))
-    sel = {k: v for k, v in d["dram_bytes_per_launch"].items() if re.match(r"tc_mlp_kernel<\d+, 0, \d, \d, \d, 1(, \d)?>", k)}
+    sel = {k: v for k, v in d["dram_bytes_per_launch"].items() if re.match(r"tc_mlp_kernel<\d+, 0, \d, \d, \d, 1(, \d)*>", k)}
     if not sel:
         return None, None
     return sum(sel.values()), f"DRAM read+write bytes of the {len(sel)} trace-level launches of one frame, " \

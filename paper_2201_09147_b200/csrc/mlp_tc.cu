@@ -325,7 +325,7 @@ constexpr int kNumBars = 2 * kMaxStages + kMaxSub + 4;  // full, empty, kready, 
 __host__ __device__ inline size_t tc_weight_bytes(int W, int L, int terms, bool resident) {
   const int nw = terms == 3 ? 2 : 1;
   // resident: every hidden layer's [hi | lo] pair, as laid out in global memory
-  return resident ? size_t(L - 2) * W * W * 2 * 2 : size_t(tc_stages(W)) * W * kKC * 2 * nw;
+  return resident ? size_t(L - 2) * W * W * 2 * tc_parts(W) : size_t(tc_stages(W)) * W * kKC * 2 * nw;
 }
 
 __host__ __device__ inline size_t tc_smem_bytes(int W, int L, int terms, bool resident, bool persist) {
@@ -731,7 +731,7 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
                 if (kResident) {
                   // resident layout per layer: [hi W*W][lo W*W] (tc_wq_offset)
                   b_base = smem_addr(sm.wst + size_t(h) * kParts * W * W + size_t(nb) * kNB * W + size_t(c) * kNB * kKCh);
-                  lo_off = uint32_t(W) * W * 2;
+                  lo_off = uint32_t(kF8 ? 2 : 1) * W * W * 2;
                 } else {
                   timed_wait(&full[s], (chunk_iter / kStages) & 1, w_full);
                   tc_fence_after();

@@ -41,7 +41,12 @@ __host__ __device__ constexpr size_t tc_wq_offset(int W, int n, int k) {
 #ifndef NSDF_TC_F8_128
 #define NSDF_TC_F8_128 1  // 128-wide nets too (frame 6.83 -> 6.69 ms, tools/ab.py)
 #endif
-__host__ __device__ constexpr bool tc_split8(int W) { return NSDF_TC_F8 && (W == 256 || (NSDF_TC_F8_128 && W == 128)); }
+#ifndef NSDF_TC_F8_64
+#define NSDF_TC_F8_64 0
+#endif
+__host__ __device__ constexpr bool tc_split8(int W) {
+  return NSDF_TC_F8 && (W == 256 || (NSDF_TC_F8_128 && W == 128) || (NSDF_TC_F8_64 && W == 64));
+}
 constexpr double kF8MaxOmega = 15.0;  // nets at larger omega0 keep fp16 correction terms (capi.cu)
 __host__ __device__ constexpr int tc_parts(int W) { return tc_split8(W) ? 3 : 2; }  // fp16-sized parts per layer
 // Byte offset of B''(n, k2) of 16-K block b (k2 < 16: fp8(W_lo[n][16b + k2]); k2 >= 16:
