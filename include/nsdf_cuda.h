@@ -86,8 +86,11 @@ typedef enum {
  *                operation (k-sequential fma chains from the bias, Cephes sincos with
  *                separately rounded mul/add) — bit-exact with the reference CPU path.
  *   FP16_FAST:   tcgen05 tensor-core tiles with split-fp16 operands (A_hi.W_hi +
- *                A_lo.W_hi + A_hi.W_lo, fp32 TMEM accumulators), fp32 first/output
- *                layers, range-reduced MUFU sine; |df| ~1e-5, parity within the BASELINE
+ *                A_lo.W_hi + A_hi.W_lo, fp32 TMEM accumulators; for 128/256-wide nets at
+ *                omega0 <= 15 the two correction terms run as one E4M3 MMA, and stop
+ *                decisions near eps_stop are re-decided with fp16 terms — env
+ *                NSDF_TC_E4M3=0/1 at upload overrides), fp32 first/output layers,
+ *                range-reduced MUFU sine; |df| ~1e-5, parity within the BASELINE
  *                tolerances (mask >= 99.9%, |dt| <= 1e-3, normals <= 0.5 deg).
  *   FP16_LOW:    the same tiles with plain fp16 operands (one MMA per K step); fastest,
  *                |df| up to ~1e-3 at omega0 = 30 (depth p99.9 ~1.5e-3: outside tolerance). */
