@@ -295,6 +295,29 @@ def test_fast_stats_match_records(fast):
     assert st.hits == int(r["hit"].sum())
 
 
+@pytest.mark.parametrize("budgets", [(40, 20, 20), (40, 20, 2), (40, 20, 1), (1, 1, 3)])
+def test_fast_e4m3_resume_bookkeeping(ctx, fast, budgets):
+    """torus3's 128/256-wide levels run E4M3 correction terms, and the final level parks
+    near-threshold stop decisions for the fp16-term resume launch.  The parked evaluation is
+    not counted twice and the resumed rays keep their iteration counts: the kernels'
+    evaluation counters equal the records' iterations_used, no level exceeds its budget (also
+    with a final budget of 1 or 2, where a parked ray resumes at its last allowed iteration),
+    the hit count matches, and the frame agrees with the oracle mode's."""
+    from paper_2201_09147_b200.abi import TraceConfig, standard_camera
+    from paper_2201_09147_b200.engine import DeviceSequence
+    from paper_2201_09147_b200.manifest import load_manifest
+    seq = load_manifest(_fixture("torus3.nest"))
+    cam, cfg = standard_camera(640, 360), TraceConfig(budgets)
+    recs, st = fast.trace_image(DeviceSequence(fast, seq).levels(), cam, cfg)
+    r = records_np(recs)
+    for j in range(3):
+        assert st.evals[j] == int(r["iters"][:, j].astype(np.int64).sum()), j
+    assert (r["iters"][:, :3] <= np.array(budgets)).all()
+    assert st.hits == int(r["hit"].sum())
+    r0 = records_np(ctx.trace_image(DeviceSequence(ctx, seq).levels(), cam, cfg)[0])
+    assert np.sum(r0["hit"] != r["hit"]) <= max(1, int(1e-3 * r["hit"].size))
+
+
 def test_fast_mixed_analytic_and_neural_levels(ctx, fast, tmp_path):
     """An analytic coarse level (FFMA iterations) feeding the persistent tcgen05 levels."""
     import json
