@@ -316,9 +316,9 @@ struct TcSmem {
   int* done;            // persistent level: no more tiles
 };
 constexpr int kStageCap = 512;
-// |decision - eps| below which an E4M3 level defers a ray's stop / hand-off decision to the
-// fp16-term resume launch: > 2x the largest E4M3-vs-fp16 difference of f measured on the
-// fixtures (2.1e-5), so both launches decide every ray as the fp16 terms would
+// |f - eps| below which an E4M3 final level defers a ray's stop decision to the fp16-term
+// resume launch: > 2x the largest E4M3-vs-fp16 difference of f measured on the fixtures
+// (2.1e-5), so every stop at the evaluated point is decided as the fp16 terms would
 constexpr float kRefineBand = 5e-5f;
 constexpr int kNumBars = 2 * kMaxStages + kMaxSub + 4;  // full, empty, kready, a0ready, tstart, dfull[2]
 
