@@ -826,8 +826,10 @@ int nsdf_cuda_upload_mlp(nsdf_ctx* c, int n_layers, const int32_t* rows, const i
       // proportional to omega0) keeps the depth tolerance: omega0 <= kF8MaxOmega nets, every
       // hidden layer; omega0 = 30 nets keep the fp16 terms (their p99.9 depth error reached
       // 1.001e-3 with E4M3 terms).  NSDF_TC_E4M3=0 / 1 overrides the choice.
-      bool e4m3 = tc_split8(W) && omega0 <= kF8MaxOmega;
-      if (const char* e = std::getenv("NSDF_TC_E4M3"); e && *e) e4m3 = tc_split8(W) && std::strcmp(e, "0") != 0;
+      // (and only at the full 2^11 shift: a smaller one would push A_lo * 2^s below E4M3's
+      // subnormal range, i.e. drop a correction term)
+      bool e4m3 = tc_split8(W) && omega0 <= kF8MaxOmega && shift == 11;
+      if (const char* e = std::getenv("NSDF_TC_E4M3"); e && *e) e4m3 = tc_split8(W) && shift == 11 && std::strcmp(e, "0") != 0;
       n.tc_f8_mask = e4m3 ? (1 << H) - 1 : 0;
       const double scale = std::ldexp(1.0, shift);
       size_t o = 0;
