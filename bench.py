@@ -784,6 +784,7 @@ def main():
 
     pk, pk_kind = peaks()
     traffic, traffic_note = ncu_traffic(W["gbuffer"]) if args.config == 2 else (None, None)
+    levels_traffic = traffic  # all trace levels of one frame (roofline.hbm); `traffic` becomes the dominant kernel's
     # the roofline denominator: the BURST bf16 figure (kernels timed in short launches at the
     # clock they actually run at); the sustained figure is reported beside it
     peak_tf = pk["bf16_tflops"]
@@ -921,10 +922,10 @@ def main():
         gbs = nbytes / (ms_per_frame / 1e3) / 1e9
         hbm = {"kernel": "normal map (12 B point in, 12 B normal out per point)", "bytes": nbytes,
                "achieved_gbs": gbs, "peak_gbs": hbm_peak, "frac": gbs / hbm_peak, "bytes_kind": "algorithmic"}
-    elif traffic is not None:
+    elif levels_traffic is not None:
         tms = frame["trace_ms"]
-        gbs = traffic / (tms / 1e3) / 1e9 if tms > 0 else 0.0
-        hbm = {"kernel": "persistent trace levels incl. compaction", "bytes": traffic, "achieved_gbs": gbs,
+        gbs = levels_traffic / (tms / 1e3) / 1e9 if tms > 0 else 0.0
+        hbm = {"kernel": "persistent trace levels incl. compaction", "bytes": levels_traffic, "achieved_gbs": gbs,
                "peak_gbs": hbm_peak, "frac": gbs / hbm_peak, "bytes_kind": "ncu dram read+write per frame"}
     else:
         hbm = None
