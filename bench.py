@@ -353,11 +353,12 @@ def run_e2e(args, ctx, ds, seq, stream, world, rank, W):
         extra = [Context(ctx.device, args.mode) for _ in range(T - 1)]
         lanes = [(ctx, ds)] + [(c, DeviceSequence(c, seq)) for c in extra]
         srcs = [np.array(pts, copy=True) for _ in range(T)]
+        last = [None] * T  # each lane's last result, checked against a single-thread call below
 
         def work(li, n):
             c, d = lanes[li]
             for _ in range(n):
-                c.normal_map(d.handles[0], srcs[li], delta)
+                last[li] = c.normal_map(d.handles[0], srcs[li], delta)
 
         for li in range(T):
             work(li, 1)
@@ -369,11 +370,14 @@ def run_e2e(args, ctx, ds, seq, stream, world, rank, W):
         for t in threads:
             t.join()
         e_ms = (time.perf_counter() - w0) * 1e3
+        single = ctx.normal_map(ds.handles[0], pts, delta)
+        same = all(r is not None and np.array_equal(r[0], single[0]) and r[1:] == single[1:] for r in last)
         for c in extra:
             c.close()
         from paper_2201_09147_b200 import scheduler
         rate, e_ms = scheduler.job_rate(k * steps, e_ms, world, device="cuda")  # all ranks / slowest rank
         return {"value": rate / 1e6, "unit": "Mnormals/s", "ms_per_frame": e_ms / steps,
+                "outputs_equal_single_thread": bool(same),
                 "h2d_bytes_per_step": 12 * k, "d2h_bytes_per_step": 12 * k + 16,
                 "path": f"nsdf_cuda_normal_map (C ABI, host points -> host normals) from {T} host threads, "
                         f"one context each"}

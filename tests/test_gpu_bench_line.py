@@ -28,5 +28,6 @@ def test_bench_gbuffer_line():
     e2e = line["e2e"]
     assert e2e["unit"] == "Mnormals/s" and e2e["value"] > 0
     assert "3 host threads" in e2e["path"]
+    assert e2e["outputs_equal_single_thread"] is True  # the threaded lanes' normals == one call's
     k = e2e["h2d_bytes_per_step"] // 12          # G-buffer hit points per step
     assert k > 0 and e2e["h2d_bytes_per_step"] == 12 * k and e2e["d2h_bytes_per_step"] == 12 * k + 16
