@@ -872,7 +872,16 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
         // sine epilogue of one 16-column block (value rows; tangent rows scale by omega cos)
         auto activate = [&](const uint32_t (&r)[16], int cc, float (&v)[16]) {
 #pragma unroll
-          for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]) * (kScaled && m > 0 ? net.inv_scale : 1.0f);
+          for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]);
+          if (kScaled && m > 0) {  // accumulators of scaled weights hold 2^s x the argument
+            const float2 is = make_float2(net.inv_scale, net.inv_scale);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              const float2 t = __fmul2_rn(make_float2(v[2 * j], v[2 * j + 1]), is);
+              v[2 * j] = t.x;
+              v[2 * j + 1] = t.y;
+            }
+          }
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
             if (kGrad) {
@@ -914,12 +923,14 @@ __global__ void __launch_bounds__(32 * (kResident ? 1 : 2) + 128 * kGroups,
             if (kF8) {
               // columns 8-11: fp8(A), 12-15: fp8((A - fp16(A)) * 2^s) (one f8f6f4 K = 32 step)
               float lo[16];
+              const float2 sc = make_float2(net.scale, net.scale);
 #pragma unroll
               for (int j = 0; j < 8; ++j) {
                 const __half2 h = *reinterpret_cast<const __half2*>(&hw[j]);
                 const float2 d = __ffma2_rn(__half22float2(h), make_float2(-1.0f, -1.0f), make_float2(v[2 * j], v[2 * j + 1]));
-                lo[2 * j] = d.x * net.scale;
-                lo[2 * j + 1] = d.y * net.scale;
+                const float2 ds = __fmul2_rn(d, sc);  // exact (power of 2)
+                lo[2 * j] = ds.x;
+                lo[2 * j + 1] = ds.y;
               }
 #pragma unroll
               for (int q = 0; q < 4; ++q) {
